@@ -1,0 +1,553 @@
+/*
+ * cdms_oracle.c -- plain, slow, fp64 CPU ORACLE for the coherent-likelihood hot path of
+ * "Coherent Direct Multipath SLAM" (arxiv 2604.19723).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code, header,
+ * table or constant generator with the CUDA path (paper_2604_19723_b200/csrc) and neither
+ * includes the other.
+ *
+ * Citations: "P:Lnnn" is a line of /root/reference/PAPER.md, "S:Lnnn" one of SPEC.md,
+ * "C-amb-n" a reading listed in SURVEY.md section 8(c) / DESIGN.md.
+ *
+ * Conventions: IEEE fp64, round-to-nearest, built with -O2 -fno-fast-math -ffp-contract=off;
+ * every sum runs in index order (p; j; s; k; m) (C-amb-22).  OpenMP only splits the
+ * outermost particle loop, so each particle's result is independent of the thread count.
+ *
+ * Parity pins (tests/test_oracle_*.py): geometry invariants, an independent reflection
+ * construction of the VA layout, unit modulus, Kronecker == per-element, far-field 1/d law,
+ * the dense N_z x N_z log-density (numpy), Sherman-Morrison at S=1, the v->0 and v->inf
+ * limits, phase-rotation invariance, matched-filter Cauchy-Schwarz, moment matching by
+ * enumeration, resampling hand trace + float Alg.2 agreement, Philox KAT vectors.
+ */
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_C 299792458.0 /* speed of light, m/s (C-amb-3) */
+#define ORC_PI 3.14159265358979323846
+
+enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EDEGENERATE = 2, ORC_EZEROMASS = 3 };
+enum { ORC_SPHERICAL = 0, ORC_PLANAR_WB = 1, ORC_PLANAR_NB = 2 };
+
+typedef struct {
+  int32_t J, K;          /* PAs; walls (S~ = K+1 components, s = 0 is LOS) */
+  int32_t ny, nv;        /* URA N_y x N_v, column m = iy*nv + iv */
+  int32_t nf;            /* subcarriers */
+  int32_t wavefront;     /* ORC_SPHERICAL / ORC_PLANAR_WB / ORC_PLANAR_NB */
+  int32_t pathloss;      /* 1: psi = lambda/(4 pi ||r'||) psi~ (C-amb-6) */
+  int32_t pad_;
+  double dy, dv;         /* element spacing */
+  double fc;             /* carrier */
+  const double* pa_pos;  /* [J][3] */
+  const double* pa_rot;  /* [J][3][3] row-major */
+  const double* f_pb;    /* [nf] passband frequencies f_pb = f_c 1 + f */
+} orc_scene;
+
+/* ------------------------------------------------------------------ L0 geometry (A1) */
+
+/* Template URA P~ in the local yz-plane, symmetric about the origin:
+ * row x = 0, row y = p_y^T (x) 1_{1 x N_v}, row z = 1_{1 x N_y} (x) p_z^T. */
+void orc_template(int ny, int nv, double dy, double dv, double* pt /*[3][Na]*/) {
+  int na = ny * nv;
+  for (int iy = 0; iy < ny; ++iy)
+    for (int iv = 0; iv < nv; ++iv) {
+      int m = iy * nv + iv;
+      pt[0 * na + m] = 0.0;
+      pt[1 * na + m] = (iy - 0.5 * (ny - 1)) * dy;
+      pt[2 * na + m] = (iv - 0.5 * (nv - 1)) * dv;
+    }
+}
+
+/* Householder H_k = I - 2 s s^T / ||s||^2; H_0 = I for LOS. */
+int orc_householder(const double* s /*[3] or NULL for LOS*/, double* H /*[3][3]*/) {
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) H[a * 3 + b] = (a == b) ? 1.0 : 0.0;
+  if (!s) return ORC_OK;
+  double n2 = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
+  if (!(n2 > 0.0)) return ORC_EINVAL; /* p_sfv in R^3 \ {0} */
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) H[a * 3 + b] -= 2.0 * s[a] * s[b] / n2;
+  return ORC_OK;
+}
+
+/* SFV -> VA: p_VA = p_j - (2 p_j^T s / ||s||^2 - 1) s; LOS: p_VA = p_j. */
+int orc_va(const double* pj, const double* s /*or NULL*/, double* va) {
+  if (!s) { va[0] = pj[0]; va[1] = pj[1]; va[2] = pj[2]; return ORC_OK; }
+  double n2 = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
+  if (!(n2 > 0.0)) return ORC_EINVAL;
+  double c = 2.0 * (pj[0] * s[0] + pj[1] * s[1] + pj[2] * s[2]) / n2 - 1.0;
+  for (int a = 0; a < 3; ++a) va[a] = pj[a] - c * s[a];
+  return ORC_OK;
+}
+
+/* VA layout P_{j,k} = p_VA 1^T + H_k R_j P~; k = 0 gives the PA layout. */
+int orc_anchor_layout(const orc_scene* sc, int j, const double* s /*or NULL*/,
+                      double* layout /*[3][Na]*/, double* va /*[3]*/, double* H /*[3][3]*/) {
+  int na = sc->ny * sc->nv;
+  double* pt = (double*)malloc(sizeof(double) * 3 * na);
+  orc_template(sc->ny, sc->nv, sc->dy, sc->dv, pt);
+  int st = orc_householder(s, H);
+  if (st == ORC_OK) st = orc_va(sc->pa_pos + 3 * j, s, va);
+  if (st == ORC_OK) {
+    const double* R = sc->pa_rot + 9 * j;
+    double HR[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0.0;
+        for (int c = 0; c < 3; ++c) acc += H[a * 3 + c] * R[c * 3 + b];
+        HR[a * 3 + b] = acc;
+      }
+    for (int m = 0; m < na; ++m)
+      for (int a = 0; a < 3; ++a) {
+        double acc = 0.0;
+        for (int c = 0; c < 3; ++c) acc += HR[a * 3 + c] * pt[c * na + m];
+        layout[a * na + m] = va[a] + acc;
+      }
+  }
+  free(pt);
+  return st;
+}
+
+/* cdms_layout counterpart: all (j, s) anchors at once.  layout[J][S][3][Na], va[J][S][3], H[S][3][3]. */
+int orc_layout(const orc_scene* sc, const double* sfv /*[K][3]*/, double* layout, double* va,
+               double* H) {
+  int S = sc->K + 1, na = sc->ny * sc->nv;
+  for (int j = 0; j < sc->J; ++j)
+    for (int s = 0; s < S; ++s) {
+      const double* sv = (s == 0) ? NULL : sfv + 3 * (s - 1);
+      int st = orc_anchor_layout(sc, j, sv, layout + ((size_t)(j * S + s)) * 3 * na,
+                                 va + (j * S + s) * 3, H + s * 9);
+      if (st) return st;
+    }
+  return ORC_OK;
+}
+
+/* Local ray r' = R_j^T H_k (p - p_VA); LOS: R_j^T (p - p_j). */
+void orc_local_ray(const orc_scene* sc, int j, const double* H, const double* va, const double* p,
+                   double* rl) {
+  const double* R = sc->pa_rot + 9 * j;
+  double g[3], h[3];
+  for (int a = 0; a < 3; ++a) g[a] = p[a] - va[a];
+  for (int a = 0; a < 3; ++a) h[a] = H[a * 3 + 0] * g[0] + H[a * 3 + 1] * g[1] + H[a * 3 + 2] * g[2];
+  for (int a = 0; a < 3; ++a) rl[a] = R[0 * 3 + a] * h[0] + R[1 * 3 + a] * h[1] + R[2 * 3 + a] * h[2];
+}
+
+/* ------------------------------------------------------------------ L1 array responses */
+
+/* Steering vector psi in C^{N_z} of MT position p for anchor (j, s), element n = k*N_a + m
+ * (vec of the N_a x N_f matrix, antenna fastest; C-amb-1).  Modes:
+ *  SPHERICAL: psi = vec(exp(-j 2 pi / c vecnorm(p 1^T - P_{j,s})^T f_pb^T)).
+ *  PLANAR_WB: vecnorm replaced by (p 1^T - P)^T u, u = r/||r||, r = p - p_VA.
+ *  PLANAR_NB: (b(tau) (x) a_y (x) a_z) exp(-j 2 pi f_c ||r'|| / c), tau = ||r'||/c,
+ *     theta = arccos(r'_z/||r'||), phi = atan2(r'_y, r'_x), b = exp(-j 2 pi f tau),
+ *     a_y = exp(j 2 pi / lambda p_y sin(theta) sin(phi)), a_z = exp(j 2 pi / lambda p_z cos(theta)).
+ * pathloss: times lambda / (4 pi ||r'||).  Returns ORC_EDEGENERATE if the MT sits
+ * on the phase centre (r' = 0 excluded) or on an antenna (spherical). */
+int orc_response(const orc_scene* sc, const double* p /*[3]*/, int j, int s,
+                 const double* sfv_s /*[3] for s>0, ignored for s=0*/, int wavefront,
+                 double complex* psi /*[Nz]*/) {
+  int na = sc->ny * sc->nv, nf = sc->nf;
+  double* lay = (double*)malloc(sizeof(double) * 3 * na);
+  double va[3], H[9], rl[3];
+  int st = orc_anchor_layout(sc, j, s == 0 ? NULL : sfv_s, lay, va, H);
+  if (st) { free(lay); return st; }
+  orc_local_ray(sc, j, H, va, p, rl);
+  double rn = sqrt(rl[0] * rl[0] + rl[1] * rl[1] + rl[2] * rl[2]);
+  if (!(rn > 0.0)) { free(lay); return ORC_EDEGENERATE; }
+  double lam = ORC_C / sc->fc;
+  double gain = sc->pathloss ? lam / (4.0 * ORC_PI * rn) : 1.0;
+  if (wavefront == ORC_SPHERICAL) {
+    for (int m = 0; m < na; ++m) {
+      double dx = p[0] - lay[0 * na + m], dyy = p[1] - lay[1 * na + m], dz = p[2] - lay[2 * na + m];
+      double d = sqrt(dx * dx + dyy * dyy + dz * dz);
+      if (!(d > 0.0)) { free(lay); return ORC_EDEGENERATE; }
+      for (int k = 0; k < nf; ++k) {
+        double ph = -2.0 * ORC_PI / ORC_C * d * sc->f_pb[k];
+        psi[(size_t)k * na + m] = gain * (cos(ph) + I * sin(ph));
+      }
+    }
+  } else if (wavefront == ORC_PLANAR_WB) {
+    double r[3] = {p[0] - va[0], p[1] - va[1], p[2] - va[2]};
+    double rr = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    double u[3] = {r[0] / rr, r[1] / rr, r[2] / rr};
+    for (int m = 0; m < na; ++m) {
+      double proj = (p[0] - lay[0 * na + m]) * u[0] + (p[1] - lay[1 * na + m]) * u[1] +
+                    (p[2] - lay[2 * na + m]) * u[2];
+      for (int k = 0; k < nf; ++k) {
+        double ph = -2.0 * ORC_PI / ORC_C * proj * sc->f_pb[k];
+        psi[(size_t)k * na + m] = gain * (cos(ph) + I * sin(ph));
+      }
+    }
+  } else if (wavefront == ORC_PLANAR_NB) {
+    double tau = rn / ORC_C;
+    double theta = acos(rl[2] / rn);
+    double phi = atan2(rl[1], rl[0]);
+    double* pt = (double*)malloc(sizeof(double) * 3 * na);
+    orc_template(sc->ny, sc->nv, sc->dy, sc->dv, pt);
+    double complex carrier = cexp(-I * 2.0 * ORC_PI / ORC_C * sc->fc * rn);
+    for (int k = 0; k < nf; ++k) {
+      double fbb = sc->f_pb[k] - sc->fc; /* baseband f */
+      double complex b = cexp(-I * 2.0 * ORC_PI * fbb * tau);
+      for (int iy = 0; iy < sc->ny; ++iy) {
+        double py = pt[1 * na + iy * sc->nv];
+        double complex ay = cexp(I * 2.0 * ORC_PI / lam * py * sin(theta) * sin(phi));
+        for (int iv = 0; iv < sc->nv; ++iv) {
+          double pz = pt[2 * na + iv];
+          double complex az = cexp(I * 2.0 * ORC_PI / lam * pz * cos(theta));
+          psi[(size_t)k * na + iy * sc->nv + iv] = gain * (b * ay * az) * carrier;
+        }
+      }
+    }
+    free(pt);
+  } else {
+    free(lay);
+    return ORC_EINVAL;
+  }
+  free(lay);
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ small dense helpers */
+
+/* In-place lower Cholesky A = L L^H of an n x n Hermitian PD matrix (row-major, lower part used). */
+static int orc_cholesky(double complex* A, int n) {
+  for (int j = 0; j < n; ++j) {
+    double d = creal(A[j * n + j]);
+    for (int k = 0; k < j; ++k) d -= creal(A[j * n + k] * conj(A[j * n + k]));
+    if (!(d > 0.0)) return ORC_EINVAL;
+    double l = sqrt(d);
+    A[j * n + j] = l;
+    for (int i = j + 1; i < n; ++i) {
+      double complex acc = A[i * n + j];
+      for (int k = 0; k < j; ++k) acc -= A[i * n + k] * conj(A[j * n + k]);
+      A[i * n + j] = acc / l;
+    }
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ L2 likelihood (A3-A5) */
+
+/* Approximate MT update message iota~ at one particle for PA j (Supplement S-V-C):
+ *   iota~ = exp(-e^H A^-1 e) / ((pi eta)^Nz det(I + M^H M / eta)),  A = eta I + M M^H,
+ *   e^H A^-1 e = ||e||^2/eta - ||(I + M^H M/eta)^{-1/2} M^H e||^2 / eta^2,
+ * with the moment-matched reading (C-amb-7/8): columns m_s = sqrt(v_s) psi_s (so M = Psi V^1/2)
+ * and mean mu^iota = sum_s m_s-prior psi_s, i.e. e = z - Psi m.  This reaches exactly the dense
+ * log CN(z; Psi m, eta I + Psi V Psi^H) of P:L2217-2224 (pinned against numpy in the tests).
+ * Steps follow the paper: responses, m-vectors, error vector e, Gram M^H M, M^H e, then the
+ * S x S Cholesky for the inverse square root and the determinant.  Also returns the LMMSE
+ * amplitude a = m + V^1/2 K^-1 M^H e / eta (K = I + M^H M / eta). */
+static int orc_iota(const orc_scene* sc, const double* p, int j, const double* sfv /*[K][3]*/,
+                    const double complex* z, const double complex* mprior /*[S]*/,
+                    const double* vprior /*[S]*/, double eta, double complex* psi_work /*[S][Nz]*/,
+                    double* out_l, double complex* out_amp /*[S] or NULL*/) {
+  int S = sc->K + 1;
+  size_t nz = (size_t)sc->nf * sc->ny * sc->nv;
+  for (int s = 0; s < S; ++s) {
+    int st = orc_response(sc, p, j, s, s ? sfv + 3 * (s - 1) : NULL, sc->wavefront,
+                          psi_work + (size_t)s * nz);
+    if (st) return st;
+  }
+  /* error vector e = z - mu^iota, mu^iota = sum_s m_s psi_s */
+  double complex* e = (double complex*)malloc(sizeof(double complex) * nz);
+  double e2 = 0.0;
+  for (size_t n = 0; n < nz; ++n) {
+    double complex mu = 0.0;
+    for (int s = 0; s < S; ++s) mu += mprior[s] * psi_work[(size_t)s * nz + n];
+    e[n] = z[n] - mu;
+    e2 += creal(e[n] * conj(e[n]));
+  }
+  /* M^H e and M^H M by direct sums (m-vectors m_s = sqrt(v_s) psi_s) */
+  double complex Mhe[16], K[256];
+  for (int s = 0; s < S; ++s) {
+    double sv = sqrt(vprior[s]);
+    double complex acc = 0.0;
+    for (size_t n = 0; n < nz; ++n) acc += conj(sv * psi_work[(size_t)s * nz + n]) * e[n];
+    Mhe[s] = acc;
+  }
+  for (int a = 0; a < S; ++a)
+    for (int b = 0; b < S; ++b) {
+      double sa = sqrt(vprior[a]), sb = sqrt(vprior[b]);
+      double complex acc = 0.0;
+      for (size_t n = 0; n < nz; ++n)
+        acc += conj(sa * psi_work[(size_t)a * nz + n]) * (sb * psi_work[(size_t)b * nz + n]);
+      K[a * S + b] = (a == b ? 1.0 : 0.0) + acc / eta; /* I + M^H M / eta */
+    }
+  free(e);
+  int st = orc_cholesky(K, S);
+  if (st) return ORC_EINVAL;
+  /* ||L^-1 M^H e||^2 = ||(I + M^H M/eta)^{-1/2} M^H e||^2 ; log det = 2 sum log L_ii */
+  double complex x[16];
+  double logdet = 0.0, q2 = 0.0;
+  for (int a = 0; a < S; ++a) {
+    double complex acc = Mhe[a];
+    for (int b = 0; b < a; ++b) acc -= K[a * S + b] * x[b];
+    x[a] = acc / creal(K[a * S + a]);
+    q2 += creal(x[a] * conj(x[a]));
+    logdet += 2.0 * log(creal(K[a * S + a]));
+  }
+  double quad = e2 / eta - q2 / (eta * eta);
+  *out_l = -(double)nz * log(ORC_PI * eta) - logdet - quad;
+  if (out_amp) {
+    /* K^-1 b: back substitution L^H y = x */
+    double complex y[16];
+    for (int a = S - 1; a >= 0; --a) {
+      double complex acc = x[a];
+      for (int b = a + 1; b < S; ++b) acc -= conj(K[b * S + a]) * y[b];
+      y[a] = acc / creal(K[a * S + a]);
+    }
+    for (int s = 0; s < S; ++s) out_amp[s] = mprior[s] + sqrt(vprior[s]) * y[s] / eta;
+  }
+  return ORC_OK;
+}
+
+/* Per-particle MT log-weight: l_p = log w_beta(p) + sum_j log iota~(x_p; z^(j)).
+ * particles: [P][pstride] doubles, position = first 3.  sfv: [K][3] shared, or [P][K][3] when
+ * sfv_per_particle (C-amb-8).  y: [J][nf][Na] complex (paper vec order).  m: [J][S] complex,
+ * v: [J][S], eta: [J].  logw_prior: [P] or NULL (= 0).  loglik out [P]; amp out [P][J][S] or NULL.
+ * Degenerate particles get l = -inf and the call returns ORC_EDEGENERATE. */
+int orc_loglik(const orc_scene* sc, const double* particles, int64_t P, int pstride,
+               const double* sfv, int sfv_per_particle, const double complex* y,
+               const double complex* m, const double* v, const double* eta,
+               const double* logw_prior, double* loglik, double complex* amp) {
+  if (sc->K < 0 || sc->K > 15 || sc->J <= 0 || P < 0) return ORC_EINVAL;
+  int S = sc->K + 1;
+  size_t nz = (size_t)sc->nf * sc->ny * sc->nv;
+  int status = ORC_OK;
+#pragma omp parallel
+  {
+    double complex* work = (double complex*)malloc(sizeof(double complex) * nz * S);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t p = 0; p < P; ++p) {
+      const double* x = particles + p * pstride;
+      const double* sf = sfv_per_particle ? sfv + (size_t)p * 3 * sc->K : sfv;
+      double l = logw_prior ? logw_prior[p] : 0.0;
+      for (int j = 0; j < sc->J; ++j) {
+        double lj;
+        int st = orc_iota(sc, x, j, sf, y + (size_t)j * nz, m + j * S, v + j * S, eta[j], work, &lj,
+                          amp ? amp + ((size_t)p * sc->J + j) * S : NULL);
+        if (st) {
+          l = -INFINITY;
+#pragma omp critical
+          status = (status == ORC_OK) ? st : status;
+          break;
+        }
+        l += lj;
+      }
+      loglik[p] = l;
+    }
+    free(work);
+  }
+  return status;
+}
+
+/* ------------------------------------------------------------------ L3 beliefs (A6-A8) */
+
+/* Weight normalization in the log domain with max subtraction:
+ * M = max l, S = sum e^{l - M} (index order), lse = M + ln S, w = e^{(l - M) - ln S}
+ * (l - M is exact for |l| up to 1e7 nats, so w keeps full relative precision). */
+int orc_normalize(const double* l, int64_t P, double* w, double* lse) {
+  double M = -INFINITY;
+  for (int64_t p = 0; p < P; ++p) {
+    if (l[p] != l[p]) return ORC_EINVAL;
+    if (l[p] > M) M = l[p];
+  }
+  if (P == 0 || M == -INFINITY) { *lse = -INFINITY; return ORC_EZEROMASS; }
+  double s = 0.0;
+  for (int64_t p = 0; p < P; ++p) s += exp(l[p] - M);
+  double ls = log(s);
+  for (int64_t p = 0; p < P; ++p) w[p] = exp((l[p] - M) - ls);
+  *lse = M + ls;
+  return ORC_OK;
+}
+
+/* MMSE moments of the weighted set and the belief's second central moment used by
+ * the regularization kernel, two-pass: est = [sum w, mean(6), cov upper-tri(21)]. */
+int orc_moments(const double* x /*[P][6]*/, const double* w, int64_t P, double* est /*[28]*/) {
+  double sw = 0.0, mean[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t p = 0; p < P; ++p) {
+    sw += w[p];
+    for (int a = 0; a < 6; ++a) mean[a] += w[p] * x[p * 6 + a];
+  }
+  if (!(sw > 0.0)) return ORC_EZEROMASS;
+  for (int a = 0; a < 6; ++a) mean[a] /= sw;
+  double cov[21] = {0};
+  for (int64_t p = 0; p < P; ++p) {
+    double d[6];
+    for (int a = 0; a < 6; ++a) d[a] = x[p * 6 + a] - mean[a];
+    int t = 0;
+    for (int a = 0; a < 6; ++a)
+      for (int b = a; b < 6; ++b) cov[t++] += w[p] * d[a] * d[b];
+  }
+  est[0] = sw;
+  for (int a = 0; a < 6; ++a) est[1 + a] = mean[a];
+  for (int t = 0; t < 21; ++t) est[7 + t] = cov[t] / sw;
+  return ORC_OK;
+}
+
+/* Systematic resampling [Arulampalam et al., Alg. 2] on integer quantities (C-amb-15):
+ * q_p = rint(ldexp(w_p / w_max, 36)), C_p = sum_{p' <= p} q_p', Q = C_{P-1},
+ * t_i = floor((u + i 2^32) Q / (P 2^32)), ancestor a_i = min{p : C_p > t_i}.
+ * Textbook serial sweep: the pointer p advances while C_p <= t_i. */
+int orc_resample(const double* w, int64_t P, uint32_t u_bits, int64_t* anc) {
+  if (P <= 0 || P > ((int64_t)1 << 26)) return ORC_EINVAL;
+  double wmax = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    if (!(w[p] >= 0.0)) return ORC_EINVAL;
+    if (w[p] > wmax) wmax = w[p];
+  }
+  if (!(wmax > 0.0)) return ORC_EZEROMASS;
+  uint64_t* C = (uint64_t*)malloc(sizeof(uint64_t) * P);
+  uint64_t run = 0;
+  for (int64_t p = 0; p < P; ++p) {
+    run += (uint64_t)rint(ldexp(w[p] / wmax, 36));
+    C[p] = run;
+  }
+  uint64_t Q = run;
+  unsigned __int128 den = (unsigned __int128)P << 32;
+  int64_t ptr = 0;
+  for (int64_t i = 0; i < P; ++i) {
+    unsigned __int128 num = ((unsigned __int128)u_bits + ((unsigned __int128)i << 32)) * Q;
+    uint64_t t = (uint64_t)(num / den);
+    while (C[ptr] <= t) ++ptr;
+    anc[i] = ptr;
+  }
+  free(C);
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ RNG + BP step (A9) */
+
+/* Philox4x32-10 (Salmon et al., SC'11), written out; pinned by the Random123 KAT vectors. */
+void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Four N(0,1) draws for (key, step, index, stream): Philox block -> u = (x + 1/2) 2^-32 ->
+ * Box-Muller pairs (u0,u1), (u2,u3): r = sqrt(-2 ln u_a), (r cos 2 pi u_b, r sin 2 pi u_b). */
+void orc_normals4(uint64_t key, uint64_t step, uint64_t index, uint32_t stream, double n[4]) {
+  uint32_t ctr[4] = {(uint32_t)index, (uint32_t)(index >> 32), (uint32_t)step, stream};
+  uint32_t k[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
+  uint32_t x[4];
+  orc_philox4x32_10(ctr, k, x);
+  for (int h = 0; h < 2; ++h) {
+    double ua = ((double)x[2 * h] + 0.5) * 0x1p-32;
+    double ub = ((double)x[2 * h + 1] + 0.5) * 0x1p-32;
+    double r = sqrt(-2.0 * log(ua));
+    n[2 * h] = r * cos(2.0 * ORC_PI * ub);
+    n[2 * h + 1] = r * sin(2.0 * ORC_PI * ub);
+  }
+}
+
+/* The resampling offset of step n: the first word of Philox(key, (0, 0, step, 3)). */
+uint32_t orc_step_u_bits(uint64_t key, uint64_t step) {
+  uint32_t ctr[4] = {0u, 0u, (uint32_t)step, 3u};
+  uint32_t k[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
+  uint32_t x[4];
+  orc_philox4x32_10(ctr, k, x);
+  return x[0];
+}
+
+/* NCV prediction: x_n = F x_{n-1} + Gamma a, a ~ N(0, sigma_v^2 I3),
+ * F = [I T I; 0 I], Gamma = [T^2/2 I; T I].  Normals: stream 0 of particle index p0 + p. */
+void orc_predict(double* x /*[P][6]*/, int64_t P, int64_t p0, double T, double sigma_v,
+                 uint64_t key, uint64_t step) {
+  for (int64_t p = 0; p < P; ++p) {
+    double n[4];
+    orc_normals4(key, step, (uint64_t)(p0 + p), 0u, n);
+    double* s = x + p * 6;
+    for (int a = 0; a < 3; ++a) {
+      double acc = sigma_v * n[a];
+      s[a] = s[a] + T * s[3 + a] + 0.5 * T * T * acc;
+      s[3 + a] = s[3 + a] + T * acc;
+    }
+  }
+}
+
+/* Regularization: x <- x + h_opt chol(Sigma) n, n ~ N(0, I6) (streams 1, 2 of the
+ * slot index), h_opt = (4 / ((d + 2) P_total))^{1/(d+4)}, d = 6 (C-amb-16), Cholesky of
+ * Sigma + 1e-12 tr(Sigma) I with non-positive pivots zeroing their column. */
+void orc_regularize(double* x, int64_t P, int64_t p0, int64_t P_total, const double* cov21,
+                    uint64_t key, uint64_t step) {
+  double Sg[36], L[36];
+  int t = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) { Sg[a * 6 + b] = cov21[t]; Sg[b * 6 + a] = cov21[t]; ++t; }
+  double tr = 0.0;
+  for (int a = 0; a < 6; ++a) tr += Sg[a * 6 + a];
+  for (int a = 0; a < 6; ++a) Sg[a * 6 + a] += 1e-12 * tr;
+  memset(L, 0, sizeof(L));
+  for (int j = 0; j < 6; ++j) {
+    double d = Sg[j * 6 + j];
+    for (int k = 0; k < j; ++k) d -= L[j * 6 + k] * L[j * 6 + k];
+    if (!(d > 0.0)) continue;
+    double l = sqrt(d);
+    L[j * 6 + j] = l;
+    for (int i = j + 1; i < 6; ++i) {
+      double acc = Sg[i * 6 + j];
+      for (int k = 0; k < j; ++k) acc -= L[i * 6 + k] * L[j * 6 + k];
+      L[i * 6 + j] = acc / l;
+    }
+  }
+  double h = pow(4.0 / (8.0 * (double)P_total), 1.0 / 10.0);
+  for (int64_t p = 0; p < P; ++p) {
+    double n[8];
+    orc_normals4(key, step, (uint64_t)(p0 + p), 1u, n);
+    orc_normals4(key, step, (uint64_t)(p0 + p), 2u, n + 4);
+    for (int a = 0; a < 6; ++a) {
+      double acc = 0.0;
+      for (int b = 0; b <= a; ++b) acc += L[a * 6 + b] * n[b];
+      x[p * 6 + a] += h * acc;
+    }
+  }
+}
+
+/* One MT BP time step (message schedule P:L2494-2508 restricted to the MT belief):
+ * predict -> loglik (log w_beta uniform, dropped) -> normalize -> moments -> systematic resampling
+ * (u = orc_step_u_bits) -> gather -> regularize with the pre-resampling covariance.
+ * particles [P][6] in/out; est [28]; lse; ancestors [P] out (may be NULL). */
+int orc_bp_step(const orc_scene* sc, double* particles, int64_t P, const double* sfv,
+                const double complex* y, const double complex* m, const double* v,
+                const double* eta, double T, double sigma_v, uint64_t key, uint64_t step,
+                int regularize, double* est, double* lse, int64_t* ancestors) {
+  orc_predict(particles, P, 0, T, sigma_v, key, step);
+  double* l = (double*)malloc(sizeof(double) * P);
+  double* w = (double*)malloc(sizeof(double) * P);
+  int64_t* a = (int64_t*)malloc(sizeof(int64_t) * P);
+  double* tmp = (double*)malloc(sizeof(double) * P * 6);
+  int st = orc_loglik(sc, particles, P, 6, sfv, 0, y, m, v, eta, NULL, l, NULL);
+  if (st == ORC_OK || st == ORC_EDEGENERATE) st = orc_normalize(l, P, w, lse);
+  if (st == ORC_OK) st = orc_moments(particles, w, P, est);
+  if (st == ORC_OK) st = orc_resample(w, P, orc_step_u_bits(key, step), a);
+  if (st == ORC_OK) {
+    for (int64_t i = 0; i < P; ++i) memcpy(tmp + i * 6, particles + a[i] * 6, sizeof(double) * 6);
+    memcpy(particles, tmp, sizeof(double) * P * 6);
+    if (ancestors) memcpy(ancestors, a, sizeof(int64_t) * P);
+    if (regularize) orc_regularize(particles, P, 0, P, est + 7, key, step);
+  }
+  free(l); free(w); free(a); free(tmp);
+  return st;
+}
+
+/* Moment matching of the amplitude prior seen by the MT update (Prop. 1; reading
+ * C-amb-7): the effective amplitude r r' rho with existence probability exist = eps * zeta and
+ * rho ~ CN(mu, gamma) has mean exist mu and variance exist (gamma + |mu|^2 (1 - exist)). */
+void orc_moment_match(double mu_re, double mu_im, double gamma, double exist, double* out /*m_re,m_im,v*/) {
+  out[0] = exist * mu_re;
+  out[1] = exist * mu_im;
+  out[2] = exist * (gamma + (mu_re * mu_re + mu_im * mu_im) * (1.0 - exist));
+}

@@ -1,0 +1,341 @@
+"""Benchmark of the coherent-likelihood BP step (BASELINE.json metric: particle x VA coherent likelihood
+evals/s and ms per BP step at 1/2/4/8 B200).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl cdms|reference]
+
+One process per GPU (torchrun for N > 1).  A step = one cdms_bp_step (predict, coherent log-likelihood over
+all particles x PAs x components, LSE normalization, moments, systematic resampling with redistribution,
+regularization) on P_local particles per GPU (weak scaling: P_total = N * P of the config).  Inputs are
+synthetic (scenes.py recipe); the measurement y is synthesized on the device with libcdms's own responses.
+L2 is flushed (256 MiB write) between timed steps; each step is timed with CUDA events on the context's
+stream; the reported time is the max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2604_19723_b200 import scenes  # noqa: E402
+
+METRIC = "particle x VA coherent likelihood evals/s (BP step)"
+UNIT = "evals/s"
+FFMA_PER_SM_CLK = 128          # FP32 lanes per SM (cc 10.0), measured 123-128 in tools/microbench
+N_SM = 148
+
+
+def fp32_peak_tflops(mhz: float) -> float:
+    return 2.0 * FFMA_PER_SM_CLK * N_SM * mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def synth_measurement(cd, ctx, scene, sc, torch, dev):
+    """z^(j) = sum_s rho_s psi_s(p_true) + sqrt(eta) w with libcdms's responses; SNR 20 dB."""
+    J, S = sc.cfg.J, sc.cfg.S
+    pos = np.repeat(scenes.P_TRUE[None], J * S, axis=0)
+    js = np.array([(j, s) for j in range(J) for s in range(S)], dtype=np.int32)
+    psi = cd.response(ctx, scene, pos, js, sc.sfv).reshape(J, S, -1)
+    rho = torch.as_tensor(sc.rho, device=dev)
+    clean = torch.einsum("jsn,s->jn", psi, rho)
+    pch = float((clean.abs() ** 2).sum().item()) / (scene.Nz * J)
+    eta = pch / 100.0
+    noise = torch.as_tensor(sc.noise_unit.reshape(J, -1), device=dev)
+    y = (clean + math.sqrt(eta) * noise).to(torch.complex64).reshape(J, scene.nf, scene.Na).contiguous()
+    return y, np.full(J, eta)
+
+
+def run_cdms(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2604_19723_b200 import build as B
+    if rank == 0 and not os.path.exists(os.path.join(ROOT, "paper_2604_19723_b200", "libcdms.so")):
+        B.build()
+    if world > 1:
+        torch.distributed.barrier()
+    from paper_2604_19723_b200 import cdms
+
+    dev = f"cuda:{local}"
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream(local)
+    cfg = scenes.CONFIGS[args.config]
+    P_local = cfg.P if args.particles is None else args.particles
+    sc = scenes.make_scene(cfg)
+    scene = cdms.Scene.from_synthetic(sc, wavefront=args.wavefront, precision=args.precision)
+    ctx = cdms.Context(local, stream)
+    if world > 1:
+        ctx.comm_init_from_torch(rank, world)
+    y, eta = synth_measurement(cd := cdms, ctx, scene, sc, torch, dev)
+    m, v = scenes.priors(sc, "nzm")
+    x0 = torch.as_tensor(scenes.make_particles(cfg, rank * P_local, P_local) if P_local <= cfg.P
+                         else np.tile(scenes.make_particles(cfg, 0, cfg.P), (math.ceil(P_local / cfg.P), 1))[:P_local],
+                         device=dev).contiguous()
+    x = x0.clone()
+    dsfv = torch.as_tensor(sc.sfv, device=dev).contiguous()
+    est = torch.empty(28, dtype=torch.float64, device=dev)
+    lse = torch.empty(1, dtype=torch.float64, device=dev)
+    ctx.reserve(scene, P_local)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    T, sv, key = 0.1, 0.5, sc.philox_key
+
+    def step(n):
+        cdms.bp_step(ctx, scene, x, dsfv, y, m, v, eta, T, sv, key, n, regularize=True, est=est, lse=lse)
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize(local)
+
+    for n in range(args.warmup):
+        step(n)
+    ctx.sync()
+    barrier()
+
+    # ---- timed region (device-resident inputs)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    ctx.timing_enable(True)
+    with ClockSampler(local) as clk:
+        barrier()
+        for n in range(args.steps):
+            flush.zero_()                       # L2 flush between timed steps (outside the events)
+            ev[n][0].record(stream)
+            step(args.warmup + n)
+            ev[n][1].record(stream)
+        barrier()
+    st = ctx.sync(raise_on_error=False)
+    gpu_launches = ctx.launch_count() - launches0
+    k_ms, k_n = ctx.timing_read()
+    ctx.timing_enable(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    local_total = sum(step_ms)
+    tot = torch.tensor([local_total, k_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
+    ms_per_step = tot[0].item() / args.steps
+    kernel_ms = tot[1].item() / max(k_n, 1)
+
+    # ---- end to end: host measurement in, host estimate out, through the public API
+    y_host = torch.empty(y.shape, dtype=torch.complex64, pin_memory=True)
+    y_host.copy_(y.cpu())
+    est_host = torch.empty(29, dtype=torch.float64, pin_memory=True)
+    y_dev = torch.empty_like(y)
+    out_dev = torch.empty(29, dtype=torch.float64, device=dev)
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    for n in range(args.steps):
+        flush.zero_()
+        e2e_ev[n][0].record(stream)
+        y_dev.copy_(y_host, non_blocking=True)
+        cdms.bp_step(ctx, scene, x, dsfv, y_dev, m, v, eta, T, sv, key, 10_000 + n, est=out_dev[:28], lse=out_dev[28:])
+        est_host.copy_(out_dev, non_blocking=True)
+        e2e_ev[n][1].record(stream)
+    barrier()
+    e2e_local = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    e2e_t = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = e2e_t.item() / args.steps
+    ctx.sync(raise_on_error=False)
+
+    evals_step = P_local * world * cfg.J * cfg.S
+    value = evals_step / (ms_per_step / 1e3)
+    result = None
+    if rank == 0:
+        clocks = clk.summary()
+        flop_launch = 8.0 * cfg.Nz * P_local * cfg.J * cfg.S
+        achieved = flop_launch / (kernel_ms / 1e3) / 1e12
+        peak = fp32_peak_tflops(1965.0)
+        roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
+                "frac_at_measured_clock": (round(achieved / fp32_peak_tflops(clocks["sm_mhz"]), 4)
+                                           if clocks.get("sm_mhz") else None),
+                "kernel": "cdms::loglik_kernel", "kernel_ms": round(kernel_ms, 4),
+                "kernel_share_of_step": round(kernel_ms / ms_per_step, 4),
+                "flop_per_launch": flop_launch, "traffic": traffic_from_profiles(args.config)}
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: J={cfg.J} PAs, K={cfg.K} walls (S={cfg.S}), "
+                                   f"{cfg.ny}x{cfg.nv} URA, nf={cfg.nf}, P={P_local}/GPU",
+                       "config": args.config, "P_per_gpu": P_local, "P_total": P_local * world, "J": cfg.J,
+                       "K": cfg.K, "ny": cfg.ny, "nv": cfg.nv, "nf": cfg.nf, "Nz": cfg.Nz,
+                       "wavefront": args.wavefront, "precision": args.precision,
+                       "step": "predict+loglik+normalize+moments+resample+regularize",
+                       "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (particles)"},
+            "roofline": roof,
+            "e2e": {"value": evals_step / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(y.numel() * 8), "d2h_bytes_per_step": 29 * 8},
+            "clocks": clocks, "gpu_launches": int(gpu_launches), "sync_status": st,
+        }
+        if not args.no_cpu_baseline:
+            result["cpu_baseline"] = cpu_baseline(args, cfg, sc, budget_s=args.cpu_seconds)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return result
+
+
+def traffic_from_profiles(config: str):
+    p = os.path.join(ROOT, "profiles", "loglik_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+def oracle_inputs(cfg, sc, orc_mod, n_particles):
+    o = orc_mod.Oracle.from_scene(sc)
+    y, eta = orc_mod.measurement(o, sc, scenes.P_TRUE)
+    y = y.astype(np.complex64).astype(np.complex128)
+    m, v = scenes.priors(sc, "nzm")
+    x = scenes.make_particles(cfg, 0, n_particles)
+    return o, y, np.full(cfg.J, eta), m, v, x
+
+
+def cpu_baseline(args, cfg, sc, budget_s: float = 15.0):
+    """The oracle as it stands (fp64 C, OpenMP over particles) on this host's cores, on a bounded sample of
+    the workload: time oracle BP steps on growing particle samples until ~budget_s of CPU work."""
+    from oracle import oracle as O
+    O.build()
+    n = 64
+    o, y, eta, m, v, x = oracle_inputs(cfg, sc, O, min(cfg.P, 64))
+    spent, best = 0.0, None
+    while True:
+        xs = scenes.make_particles(cfg, 0, n)
+        t0 = time.perf_counter()
+        O.Oracle.bp_step(o, xs, sc.sfv, y, m, v, eta, 0.1, 0.5, sc.philox_key, 0)
+        dt = time.perf_counter() - t0
+        spent += dt
+        best = (n, dt)
+        if spent > budget_s or n >= cfg.P or dt > budget_s / 3:
+            break
+        n = min(cfg.P, n * 4)
+    n, dt = best
+    return {"value": n * cfg.J * cfg.S / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"oracle bp_step on {n} of {cfg.P} particles of {args.config} (fp64 C, OpenMP), {dt:.2f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as the reference arm, on this host's cores, bounded samples."""
+    world, rank, local = dist_env()
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    O.build()
+    cfg = scenes.CONFIGS[args.config]
+    sc = scenes.make_scene(cfg)
+    n = min(cfg.P, args.ref_particles)
+    o, y, eta, m, v, x = oracle_inputs(cfg, sc, O, n)
+    for w in range(args.warmup):
+        O.Oracle.bp_step(o, x, sc.sfv, y, m, v, eta, 0.1, 0.5, sc.philox_key, w)
+    times = []
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        O.Oracle.bp_step(o, x, sc.sfv, y, m, v, eta, 0.1, 0.5, sc.philox_key, args.warmup + k)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    value = n * cfg.J * cfg.S / dt
+    sample = f"oracle bp_step on {n} of {cfg.P} particles of {args.config} per step (fp64 C, OpenMP)"
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config} (sampled: {n} particles/step)", "config": args.config},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(scenes.CONFIGS))
+    ap.add_argument("--particles", type=int, default=None, help="particles per GPU (default: the config's P)")
+    ap.add_argument("--wavefront", default="spherical", choices=["spherical", "planar_wb", "planar_nb"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--impl", default="cdms", choices=["cdms", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-particles", type=int, default=2000)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "cdms" else args.warmup
+    res = run_reference(args) if args.impl == "reference" else run_cdms(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+/*
+ * cdms.h -- C ABI of libcdms, the B200-native (sm_100a) coherent-likelihood engine for the MT
+ * belief update of "Coherent Direct Multipath SLAM" (arxiv 2604.19723).
+ *
+ * Citations: P:Lnnn = line of PAPER.md (the paper), S:Lnnn = line of SPEC.md, C-amb-n = reading of
+ * an ambiguous passage (section "Readings").
+ *
+ * Conventions (all entry points):
+ *  - d_* arguments are CUDA DEVICE pointers owned by the CALLER (e.g. torch tensors) on the device
+ *    of the context; h_* arguments are HOST pointers owned by the caller and read only during the
+ *    call (the library copies what it keeps).  Arrays are dense, row-major, no padding.
+ *  - complex64 = interleaved (re, im) float32 pairs; complex128 = interleaved float64 pairs.
+ *  - Every device operation is enqueued on the context's stream; nothing synchronizes the host
+ *    except cdms_sync().  Calls are capturable into a CUDA graph once their workspaces exist
+ *    (first call outside capture, or cdms_reserve()).
+ *  - Errors: host-checkable problems (NULL pointers, sizes <= 0, ||sfv|| = 0, R not in SO(3),
+ *    non-uniform f_pb, non-finite or negative priors) return CDMS_EINVAL BEFORE any launch and
+ *    leave outputs untouched.  Device-detected conditions set a sticky flag that cdms_sync()
+ *    returns: CDMS_EDEGENERATE (MT on a phase centre or antenna, P:L2137 -- that particle gets
+ *    l = -inf), CDMS_EZEROMASS (all weights zero / all l = -inf: outputs untouched, lse = -inf),
+ *    CDMS_EINVAL (NaN in device inputs).  cdms_last_error() gives a message.
+ *  - Determinism: per-particle results do not depend on launch geometry, tile placement or rank
+ *    count (fixed per-particle reduction order); cross-particle reductions are fp64 in a fixed
+ *    order; resampling is integer arithmetic and therefore exact.
+ *  - Multi-GPU: after cdms_comm_init(), cdms_weights_normalize, cdms_moments, cdms_resample and
+ *    cdms_bp_step are COLLECTIVE over the ranks (every rank calls them, each with its P_local
+ *    particles; global particle index = rank * P_local + local index, P_local equal on all ranks).
+ *    cdms_loglik, cdms_response and cdms_layout are purely local.
+ */
+#ifndef CDMS_H_
+#define CDMS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cdms_ctx_s* cdms_ctx;
+
+typedef enum {
+  CDMS_OK = 0,
+  CDMS_EINVAL = 1,
+  CDMS_EDEGENERATE = 2,
+  CDMS_EZEROMASS = 3,
+  CDMS_ENOMEM = 4,
+  CDMS_ECUDA = 5,
+  CDMS_ENCCL = 6,
+  CDMS_EUNSUPPORTED = 7
+} cdms_status;
+
+/* Array-response model (C-amb-5): spherical wideband (default), planar wideband
+ * (P:L118-143), planar narrowband Kronecker. */
+typedef enum { CDMS_SPHERICAL = 0, CDMS_PLANAR_WB = 1, CDMS_PLANAR_NB = 2 } cdms_wavefront;
+
+/* Inner-loop precision of the correlation / Gram (C-amb-18): FP32 (default, fp64 geometry and
+ * assembly) or FP64 end to end. */
+typedef enum { CDMS_FP32 = 0, CDMS_FP64 = 1 } cdms_precision;
+
+/* Scene: J PAs with identical N_y x N_v URAs (template P~ in the local yz-plane, column
+ * m = iy*nv + iv), K walls (S = K+1 propagation components, s = 0 LOS), N_f subcarriers
+ * f_pb[k] = fc + (k - (nf-1)/2) * df.  Limits: 1 <= J <= 8,
+ * 0 <= K <= 8, 1 <= nf <= 65536, 1 <= ny*nv <= 4096. */
+typedef struct {
+  int32_t J, K;
+  int32_t ny, nv;
+  int32_t nf;
+  int32_t wavefront;     /* cdms_wavefront */
+  int32_t pathloss;      /* 1: psi = lambda/(4 pi ||r'||) psi~ (C-amb-6) */
+  int32_t precision;     /* cdms_precision */
+  double dy, dv;         /* element spacing (m) */
+  double fc, df;         /* carrier and subcarrier spacing (Hz) */
+  const double* h_pa_pos;  /* [J][3] PA phase centres p_j (m) */
+  const double* h_pa_rot;  /* [J][3][3] row-major R_j in SO(3) (checked to 1e-9) */
+} cdms_scene;
+
+/* Per-(PA j, component s) amplitude prior seen by the MT update: mean m, variance v >= 0
+ * (moment-matched, reading C-amb-7; cdms_moment_match gives the map). */
+typedef struct {
+  double m_re, m_im, v;
+} cdms_prior;
+
+/* ---- context ------------------------------------------------------------------------------ */
+
+/* Create a context bound to CUDA device `device` and stream `cuda_stream` (a cudaStream_t, may be
+ * NULL = legacy default stream).  The context owns its workspaces and (optionally) an NCCL
+ * communicator; it is not thread-safe. */
+cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream);
+cdms_status cdms_destroy(cdms_ctx ctx);
+/* Re-bind the stream used by subsequent calls (e.g. torch.cuda.current_stream()). */
+cdms_status cdms_set_stream(cdms_ctx ctx, void* cuda_stream);
+/* Human-readable description of the last error on this context (static storage of the ctx). */
+const char* cdms_last_error(cdms_ctx ctx);
+/* Synchronize the stream; returns the sticky device flag (see conventions) and clears it. */
+cdms_status cdms_sync(cdms_ctx ctx);
+/* Pre-size the workspaces for up to P_local particles and the given scene (so that later calls
+ * can be captured in a CUDA graph). */
+cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local);
+/* Number of library kernel launches enqueued by this context so far (for launch accounting). */
+int64_t cdms_launch_count(cdms_ctx ctx);
+/* Kernel timing: while enabled, every launch of the likelihood kernel (rows A2-A5) is bracketed by CUDA
+ * events on the context's stream.  cdms_timing_read synchronizes those events and returns the summed
+ * kernel time (ms) and the number of launches since the last enable; it does not disable timing. */
+cdms_status cdms_timing_enable(cdms_ctx ctx, int on);
+cdms_status cdms_timing_read(cdms_ctx ctx, double* loglik_ms, int64_t* n_launches);
+
+/* NCCL bootstrap: rank 0 calls cdms_get_unique_id, broadcasts the 128 bytes (e.g. through
+ * torch.distributed), then every rank calls cdms_comm_init.  nranks = 1 is allowed. */
+cdms_status cdms_get_unique_id(unsigned char nccl_unique_id_out[128]);
+cdms_status cdms_comm_init(cdms_ctx ctx, const unsigned char nccl_unique_id[128], int rank,
+                           int nranks);
+
+/* ---- row A1: anchor geometry ----------------------------------------------------------------- */
+
+/* Householder matrices H_s = I - 2 s s^T/||s||^2 (H_0 = I), VA phase centres
+ * p_VA,js = p_j - (2 p_j^T s/||s||^2 - 1) s (p_VA,j0 = p_j) and VA layouts
+ * P_{j,s} = p_VA,js 1^T + H_s R_j P~, computed on the device with the same functions the
+ * likelihood kernel uses.  d_sfv [K][3] (fp64).  Outputs (device, fp64): d_layout [J][S][3][Na],
+ * d_va [J][S][3], d_H [S][3][3].  ||sfv_k|| = 0 -> CDMS_EINVAL. */
+cdms_status cdms_layout(cdms_ctx ctx, const cdms_scene* scene, const double* d_sfv,
+                        double* d_layout, double* d_va, double* d_H);
+
+/* ---- rows A2-A5: coherent log-likelihood ----------------------------------------------------- */
+
+/* For every particle p: l_p = log w_beta(p) + sum_j log iota~(x_p; z^(j)) with the
+ * low-rank evaluation of the MT update message (Supplement S-V-C):
+ *   log iota~ = -Nz ln(pi eta_j) - ln det(I + M^H M/eta_j) - ||e||^2/eta_j
+ *               + ||(I + M^H M/eta_j)^{-1/2} M^H e||^2 / eta_j^2,
+ * M = Psi_j(x_p) V_j^{1/2}, e = z^(j) - Psi_j(x_p) m_j, Psi_j = [psi_j,0 .. psi_j,K] the unit-modulus
+ * responses of the scene's wavefront model, which equals log CN(z; Psi m, eta I + Psi V Psi^H)
+ * (P:L2217-2224).
+ *   d_particles [P][pstride] fp64, position = first 3 entries (velocity does not enter, C-amb-21).
+ *   d_sfv       fp64 [K][3] (sfv_per_particle = 0) or [P][K][3] (= 1, C-amb-8).
+ *   d_y         complex64 [J][nf][Na]: z^(j) in the paper's vec order, n = k*Na + m (C-amb-1).
+ *   h_f_pb      [nf] passband grid; must equal the scene grid to 1e-9 relative (uniformity check).
+ *   h_prior     [J][S]; h_eta [J] noise variances eta_j > 0 (C-amb-10).
+ *   d_logw_prior [P] fp64 or NULL (= 0).
+ *   d_loglik    out [P] fp64.
+ *   d_amp       out complex128 [P][J][S] LMMSE amplitudes m + V^1/2 K^-1 M^H e / eta, or NULL.
+ * Purely local (no communication).  Degenerate particles: l = -inf + CDMS_EDEGENERATE at sync. */
+cdms_status cdms_loglik(cdms_ctx ctx, const cdms_scene* scene, const double* d_particles,
+                        int64_t P, int32_t pstride, const double* d_sfv, int32_t sfv_per_particle,
+                        const void* d_y, const double* h_f_pb, const cdms_prior* h_prior,
+                        const double* h_eta, const double* d_logw_prior, double* d_loglik,
+                        void* d_amp);
+
+/* ---- row A6: weight normalization ------------------------------------------------------------ */
+
+/* w_p = exp((l_p - M) - ln S), M = max_p l_p, S = sum_p exp(l_p - M), lse = M + ln S over ALL ranks'
+ * particles (log domain with max subtraction).  d_logw [P_local] fp64,
+ * d_w out [P_local] fp64, d_lse out [1] fp64 (same value on every rank).  All l = -inf ->
+ * CDMS_EZEROMASS at sync, d_lse = -inf, d_w untouched. */
+cdms_status cdms_weights_normalize(cdms_ctx ctx, const double* d_logw, int64_t P_local,
+                                   double* d_w, double* d_lse);
+
+/* ---- row A7: belief moments ------------------------------------------------------------------ */
+
+/* MMSE moments of the weighted MT belief and its second central moment
+ * (regularization kernel covariance), two-pass over all ranks:
+ * d_est out [28] fp64 = [sum w, mean(6), cov upper triangle row-major (21)], cov = sum w (x-mean)
+ * (x-mean)^T / sum w.  d_particles [P_local][6], d_w [P_local]. */
+cdms_status cdms_moments(cdms_ctx ctx, const double* d_particles, const double* d_w,
+                         int64_t P_local, double* d_est);
+
+/* ---- row A8: systematic resampling ----------------------------------------------------------- */
+
+/* Systematic resampling [Arulampalam et al., Alg. 2] in integer form (C-amb-15):
+ * q_p = rint(ldexp(w_p / w_max, 36)) (w_max over all ranks), C = inclusive scan of q over the
+ * GLOBAL particle order, Q = C_last, t_i = floor((u + i 2^32) Q / (P_total 2^32)), ancestor
+ * a_i = min{p : C_p > t_i}.  d_ancestors out [P_local] int64: GLOBAL ancestor indices of this
+ * rank's output slots i = rank*P_local + [0, P_local).  P_total <= 2^26.  Bit-exact. */
+cdms_status cdms_resample(cdms_ctx ctx, const double* d_w, int64_t P_local, uint32_t u_bits,
+                          int64_t* d_ancestors);
+
+/* ---- row A9 + the whole step ----------------------------------------------------------------- */
+
+typedef struct {
+  double T;            /* NCV time step (s), C-amb-17 */
+  double sigma_v;      /* process-noise std (m/s^2) */
+  uint64_t philox_key; /* counter-based RNG key: Philox4x32-10, counter (p_lo, p_hi, step, stream) */
+  uint64_t step;       /* time index n (RNG counter) */
+  int32_t regularize;  /* 1: Gaussian regularization kernel after resampling */
+  int32_t pad_;
+} cdms_step_params;
+
+/* One MT BP time step on the device (message schedule P:L2494-2508, MT belief only):
+ *  predict x <- F x + Gamma a, a ~ N(0, sigma_v^2 I3) (stream 0) ->
+ *  l = loglik (uniform w_beta) -> normalize (lse) -> moments (d_est) -> systematic resampling with
+ *  u = first word of Philox(key, (0, 0, step, 3)) and redistribution of the ancestors' states so that
+ *  every rank again holds P_local particles -> optional regularization x += h_opt chol(Sigma) n
+ *  (streams 1, 2 of the slot index; h_opt = (4/(8 P_total))^(1/10), C-amb-16).
+ * d_particles [P_local][6] fp64 in/out.  d_est out [28] (pre-resampling moments), d_lse out [1]. */
+cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_particles,
+                         int64_t P_local, const double* d_sfv, const void* d_y,
+                         const double* h_f_pb, const cdms_prior* h_prior, const double* h_eta,
+                         const cdms_step_params* params, double* d_est, double* d_lse);
+
+/* ---- test / helper entries ------------------------------------------------------------------- */
+
+/* Materialize psi for n (position, PA j, component s) items with the SAME device functions and
+ * phase recurrences as cdms_loglik (parity of |d phase| per element).  d_pos [n][3] fp64,
+ * d_js [n][2] int32 (j, s), d_sfv [K][3] fp64, d_psi out complex128 [n][Nz] (n = k*Na + m order). */
+cdms_status cdms_response(cdms_ctx ctx, const cdms_scene* scene, const double* d_pos, int64_t n,
+                          const int32_t* d_js, const double* d_sfv, void* d_psi);
+
+/* Moment matching of a PF amplitude prior into the (m, v) the MT update consumes (Prop. 1,
+ * P:L2818-3165, reading C-amb-7): exist = eps * zeta, m = exist mu, v = exist (gamma + |mu|^2 (1 -
+ * exist)).  Host function. */
+cdms_status cdms_moment_match(double mu_re, double mu_im, double gamma, double exist,
+                              cdms_prior* out);
+
+/* Host-side plan of the distributed resampling (pure function, no device): given every rank's
+ * integer mass Q_r (h_Q [nranks]) and u_bits for P_total = nranks * P_local output slots, rank
+ * `rank`'s CDF range [O_r, O_r + Q_r) covers the contiguous slot range
+ * [*slot_lo, *slot_hi) = [I(O_r), I(O_r + Q_r)), I(x) = #{i : t_i < x}.  h_send_counts [nranks]
+ * gets how many of those slots belong to each destination rank (slot i lives on rank i / P_local). */
+cdms_status cdms_resample_plan(const uint64_t* h_Q, int nranks, int rank, int64_t P_local,
+                               uint32_t u_bits, int64_t* slot_lo, int64_t* slot_hi,
+                               int64_t* h_send_counts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CDMS_H_ */

@@ -1,0 +1,312 @@
+"""Thin ctypes binding of libcdms (include/cdms.h): argument marshalling only.
+
+Every step of the path runs in libcdms's CUDA kernels; torch tensors provide device memory and the
+stream.  There is no CPU fallback: a missing library or device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcdms.so")
+
+OK, EINVAL, EDEGENERATE, EZEROMASS, ENOMEM, ECUDA, ENCCL, EUNSUPPORTED = range(8)
+STATUS_NAMES = ["OK", "EINVAL", "EDEGENERATE", "EZEROMASS", "ENOMEM", "ECUDA", "ENCCL", "EUNSUPPORTED"]
+WAVEFRONTS = {"spherical": 0, "planar_wb": 1, "planar_nb": 2}
+PRECISIONS = {"fp32": 0, "fp64": 1}
+
+
+class CdmsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 8 else status}: {msg}")
+        self.status = status
+
+
+class SceneC(C.Structure):
+    _fields_ = [("J", C.c_int32), ("K", C.c_int32), ("ny", C.c_int32), ("nv", C.c_int32), ("nf", C.c_int32),
+                ("wavefront", C.c_int32), ("pathloss", C.c_int32), ("precision", C.c_int32),
+                ("dy", C.c_double), ("dv", C.c_double), ("fc", C.c_double), ("df", C.c_double),
+                ("h_pa_pos", C.POINTER(C.c_double)), ("h_pa_rot", C.POINTER(C.c_double))]
+
+
+class PriorC(C.Structure):
+    _fields_ = [("m_re", C.c_double), ("m_im", C.c_double), ("v", C.c_double)]
+
+
+class StepParamsC(C.Structure):
+    _fields_ = [("T", C.c_double), ("sigma_v", C.c_double), ("philox_key", C.c_uint64), ("step", C.c_uint64),
+                ("regularize", C.c_int32), ("pad_", C.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libcdms.so (built in-tree by paper_2604_19723_b200.build); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2604_19723_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32, dp = C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_double)
+        sig = {
+            "cdms_create": ([C.POINTER(vp), C.c_int, vp], C.c_int),
+            "cdms_destroy": ([vp], C.c_int),
+            "cdms_set_stream": ([vp, vp], C.c_int),
+            "cdms_last_error": ([vp], C.c_char_p),
+            "cdms_sync": ([vp], C.c_int),
+            "cdms_reserve": ([vp, C.POINTER(SceneC), i64], C.c_int),
+            "cdms_launch_count": ([vp], i64),
+            "cdms_timing_enable": ([vp, C.c_int], C.c_int),
+            "cdms_timing_read": ([vp, C.POINTER(C.c_double), C.POINTER(i64)], C.c_int),
+            "cdms_get_unique_id": ([C.c_char_p], C.c_int),
+            "cdms_comm_init": ([vp, C.c_char_p, C.c_int, C.c_int], C.c_int),
+            "cdms_layout": ([vp, C.POINTER(SceneC), vp, vp, vp, vp], C.c_int),
+            "cdms_loglik": ([vp, C.POINTER(SceneC), vp, i64, i32, vp, i32, vp, dp, C.POINTER(PriorC), dp, vp, vp, vp],
+                            C.c_int),
+            "cdms_weights_normalize": ([vp, vp, i64, vp, vp], C.c_int),
+            "cdms_moments": ([vp, vp, vp, i64, vp], C.c_int),
+            "cdms_resample": ([vp, vp, i64, C.c_uint32, vp], C.c_int),
+            "cdms_bp_step": ([vp, C.POINTER(SceneC), vp, i64, vp, vp, dp, C.POINTER(PriorC), dp,
+                              C.POINTER(StepParamsC), vp, vp], C.c_int),
+            "cdms_response": ([vp, C.POINTER(SceneC), vp, i64, vp, vp, vp], C.c_int),
+            "cdms_moment_match": ([C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(PriorC)], C.c_int),
+            "cdms_resample_plan": ([C.POINTER(C.c_uint64), C.c_int, C.c_int, i64, C.c_uint32, C.POINTER(i64),
+                                    C.POINTER(i64), C.POINTER(i64)], C.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return [n for n in ["cdms_create", "cdms_destroy", "cdms_set_stream", "cdms_last_error", "cdms_sync",
+                        "cdms_reserve", "cdms_launch_count", "cdms_timing_enable", "cdms_timing_read",
+                        "cdms_get_unique_id", "cdms_comm_init", "cdms_layout",
+                        "cdms_loglik", "cdms_weights_normalize", "cdms_moments", "cdms_resample", "cdms_bp_step",
+                        "cdms_response", "cdms_moment_match", "cdms_resample_plan"]]
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Scene:
+    """Host-side scene (cdms_scene).  Keeps the numpy arrays alive for the C struct."""
+
+    def __init__(self, pa_pos, pa_rot, ny, nv, dy, dv, nf, fc, df, K, wavefront="spherical", pathloss=False,
+                 precision="fp32"):
+        self.pa_pos = np.ascontiguousarray(pa_pos, dtype=np.float64).reshape(-1, 3)
+        self.pa_rot = np.ascontiguousarray(pa_rot, dtype=np.float64).reshape(-1, 3, 3)
+        self.J = self.pa_pos.shape[0]
+        self.K, self.S = int(K), int(K) + 1
+        self.ny, self.nv, self.nf = int(ny), int(nv), int(nf)
+        self.Na = self.ny * self.nv
+        self.Nz = self.Na * self.nf
+        self.fc, self.df = float(fc), float(df)
+        self.c = SceneC(self.J, self.K, self.ny, self.nv, self.nf, WAVEFRONTS[wavefront], int(bool(pathloss)),
+                        PRECISIONS[precision], float(dy), float(dv), self.fc, self.df, _dp(self.pa_pos),
+                        _dp(self.pa_rot))
+
+    @classmethod
+    def from_synthetic(cls, scene, wavefront="spherical", pathloss=False, precision="fp32"):
+        cfg = scene.cfg
+        return cls(scene.pa_pos, scene.pa_rot, cfg.ny, cfg.nv, scene.dy, scene.dv, cfg.nf, cfg.fc, cfg.df, cfg.K,
+                   wavefront=wavefront, pathloss=pathloss, precision=precision)
+
+    def f_pb(self) -> np.ndarray:
+        k = np.arange(self.nf, dtype=np.float64)
+        return self.fc + (k - (self.nf - 1) / 2.0) * self.df
+
+
+def priors_c(m, v) -> C.Array:
+    m = np.asarray(m, dtype=np.complex128).reshape(-1)
+    v = np.asarray(v, dtype=np.float64).reshape(-1)
+    arr = (PriorC * len(m))()
+    for i in range(len(m)):
+        arr[i] = PriorC(float(m[i].real), float(m[i].imag), float(v[i]))
+    return arr
+
+
+class Context:
+    """cdms_ctx bound to one CUDA device and stream (default: torch's current stream)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libcdms needs a CUDA device (no CPU fallback)")
+        self.device = device
+        self.torch = torch
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        h = C.c_void_p()
+        st = lib().cdms_create(C.byref(h), device, C.c_void_p(stream.cuda_stream))
+        if st != OK:
+            raise CdmsError(st, "cdms_create failed")
+        self.h = h
+        self.rank, self.nranks = 0, 1
+
+    def close(self):
+        if self.h:
+            lib().cdms_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st: int):
+        if st != OK:
+            raise CdmsError(st, lib().cdms_last_error(self.h).decode())
+
+    def set_stream(self, stream):
+        self.stream = stream
+        self.check(lib().cdms_set_stream(self.h, C.c_void_p(stream.cuda_stream)))
+
+    def sync(self, raise_on_error: bool = True) -> int:
+        st = lib().cdms_sync(self.h)
+        if raise_on_error:
+            self.check(st)
+        return st
+
+    def launch_count(self) -> int:
+        return int(lib().cdms_launch_count(self.h))
+
+    def timing_enable(self, on: bool = True):
+        self.check(lib().cdms_timing_enable(self.h, int(bool(on))))
+
+    def timing_read(self) -> tuple[float, int]:
+        """(summed likelihood-kernel time in ms, number of launches) since timing_enable."""
+        ms, n = C.c_double(), C.c_int64()
+        self.check(lib().cdms_timing_read(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def reserve(self, scene: Scene, P_local: int):
+        self.check(lib().cdms_reserve(self.h, C.byref(scene.c), int(P_local)))
+
+    def comm_init_from_torch(self, rank: int, world: int):
+        """NCCL bootstrap: rank 0 creates the unique id, torch.distributed broadcasts it."""
+        import torch.distributed as dist
+        buf = C.create_string_buffer(128)
+        if rank == 0:
+            self.check(lib().cdms_get_unique_id(buf))
+        t = self.torch.tensor(list(buf.raw), dtype=self.torch.uint8,
+                              device=f"cuda:{self.device}" if dist.get_backend() == "nccl" else "cpu")
+        dist.broadcast(t, 0)
+        raw = bytes(t.cpu().tolist())
+        self.check(lib().cdms_comm_init(self.h, raw, rank, world))
+        self.rank, self.nranks = rank, world
+
+
+# ---------------------------------------------------------------------------- entry points
+def layout(ctx: Context, scene: Scene, sfv):
+    torch = ctx.torch
+    dev = f"cuda:{ctx.device}"
+    sfv = torch.as_tensor(np.asarray(sfv, dtype=np.float64).reshape(-1, 3), device=dev).contiguous()
+    lay = torch.empty((scene.J, scene.S, 3, scene.Na), dtype=torch.float64, device=dev)
+    va = torch.empty((scene.J, scene.S, 3), dtype=torch.float64, device=dev)
+    H = torch.empty((scene.S, 3, 3), dtype=torch.float64, device=dev)
+    ctx.check(lib().cdms_layout(ctx.h, C.byref(scene.c), _ptr(sfv), _ptr(lay), _ptr(va), _ptr(H)))
+    return lay, va, H
+
+
+def loglik(ctx: Context, scene: Scene, particles, sfv, y, prior_m, prior_v, eta, logw_prior=None,
+           sfv_per_particle: bool = False, want_amp: bool = False, out=None):
+    """particles: float64 cuda tensor [P][pstride]; sfv: float64 cuda [K][3] or [P][K][3];
+    y: complex64 cuda [J][nf][Na]; prior_m/prior_v: [J][S]; eta: [J].  Returns l [P] (and amp)."""
+    torch = ctx.torch
+    P, pstride = particles.shape
+    assert particles.dtype == torch.float64 and particles.is_contiguous()
+    assert y.dtype == torch.complex64 and y.is_contiguous()
+    l = out if out is not None else torch.empty(P, dtype=torch.float64, device=particles.device)
+    amp = torch.empty((P, scene.J, scene.S), dtype=torch.complex128, device=particles.device) if want_amp else None
+    f_pb = scene.f_pb()
+    pr = priors_c(prior_m, prior_v)
+    et = np.ascontiguousarray(eta, dtype=np.float64).reshape(-1)
+    ctx.check(lib().cdms_loglik(ctx.h, C.byref(scene.c), _ptr(particles), int(P), int(pstride), _ptr(sfv),
+                                int(bool(sfv_per_particle)), _ptr(y), _dp(f_pb), pr, _dp(et), _ptr(logw_prior),
+                                _ptr(l), _ptr(amp)))
+    return (l, amp) if want_amp else l
+
+
+def weights_normalize(ctx: Context, logw):
+    torch = ctx.torch
+    w = torch.empty_like(logw)
+    lse = torch.empty(1, dtype=torch.float64, device=logw.device)
+    ctx.check(lib().cdms_weights_normalize(ctx.h, _ptr(logw), int(logw.shape[0]), _ptr(w), _ptr(lse)))
+    return w, lse
+
+
+def moments(ctx: Context, particles, w):
+    torch = ctx.torch
+    est = torch.empty(28, dtype=torch.float64, device=w.device)
+    ctx.check(lib().cdms_moments(ctx.h, _ptr(particles), _ptr(w), int(w.shape[0]), _ptr(est)))
+    return est
+
+
+def resample(ctx: Context, w, u_bits: int):
+    torch = ctx.torch
+    anc = torch.empty(w.shape[0], dtype=torch.int64, device=w.device)
+    ctx.check(lib().cdms_resample(ctx.h, _ptr(w), int(w.shape[0]), C.c_uint32(u_bits), _ptr(anc)))
+    return anc
+
+
+def bp_step(ctx: Context, scene: Scene, particles, sfv, y, prior_m, prior_v, eta, T: float, sigma_v: float,
+            philox_key: int, step: int, regularize: bool = True, est=None, lse=None):
+    torch = ctx.torch
+    est = est if est is not None else torch.empty(28, dtype=torch.float64, device=particles.device)
+    lse = lse if lse is not None else torch.empty(1, dtype=torch.float64, device=particles.device)
+    prm = StepParamsC(float(T), float(sigma_v), int(philox_key), int(step), int(bool(regularize)), 0)
+    ctx.check(lib().cdms_bp_step(ctx.h, C.byref(scene.c), _ptr(particles), int(particles.shape[0]), _ptr(sfv),
+                                 _ptr(y), _dp(scene.f_pb()), priors_c(prior_m, prior_v),
+                                 _dp(np.ascontiguousarray(eta, dtype=np.float64).reshape(-1)), C.byref(prm),
+                                 _ptr(est), _ptr(lse)))
+    return est, lse
+
+
+def response(ctx: Context, scene: Scene, pos, js, sfv):
+    """psi for n (position, (j, s)) items: complex128 cuda [n][Nz] (n = k*Na + m order)."""
+    torch = ctx.torch
+    dev = f"cuda:{ctx.device}"
+    pos = torch.as_tensor(np.asarray(pos, dtype=np.float64).reshape(-1, 3), device=dev).contiguous()
+    js = torch.as_tensor(np.asarray(js, dtype=np.int32).reshape(-1, 2), device=dev).contiguous()
+    sfv = torch.as_tensor(np.asarray(sfv, dtype=np.float64).reshape(-1, 3), device=dev).contiguous()
+    n = pos.shape[0]
+    psi = torch.empty((n, scene.Nz), dtype=torch.complex128, device=dev)
+    ctx.check(lib().cdms_response(ctx.h, C.byref(scene.c), _ptr(pos), int(n), _ptr(js), _ptr(sfv), _ptr(psi)))
+    return psi
+
+
+def moment_match(mu: complex, gamma: float, exist: float):
+    out = PriorC()
+    st = lib().cdms_moment_match(float(np.real(mu)), float(np.imag(mu)), float(gamma), float(exist), C.byref(out))
+    if st != OK:
+        raise CdmsError(st, "cdms_moment_match")
+    return complex(out.m_re, out.m_im), out.v
+
+
+def resample_plan(Q: Sequence[int], rank: int, P_local: int, u_bits: int):
+    """Host-side distributed resampling plan (no device): (slot_lo, slot_hi, send_counts)."""
+    R = len(Q)
+    q = (C.c_uint64 * R)(*[int(x) for x in Q])
+    lo, hi = C.c_int64(), C.c_int64()
+    counts = (C.c_int64 * R)()
+    st = lib().cdms_resample_plan(q, R, rank, int(P_local), C.c_uint32(u_bits), C.byref(lo), C.byref(hi), counts)
+    if st != OK:
+        raise CdmsError(st, "cdms_resample_plan")
+    return lo.value, hi.value, [int(x) for x in counts]

@@ -1,0 +1,139 @@
+// cdms_internal.h -- device-side parameter blocks, constants and small PTX helpers shared by the
+// libcdms kernels (loglik.cu, beliefs.cu) and the host ABI (cdms.cpp).  Nothing here is visible
+// through include/cdms.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cdms.h"
+
+namespace cdms {
+
+constexpr int MAXJ = 8;       // PAs per scene
+constexpr int MAXS = 9;       // propagation components S = K + 1 (LOS + 8 walls)
+constexpr int TILE_P = 32;    // particles per CTA tile (one per lane)
+constexpr int NWARP = 8;      // warps per CTA = antennas per antenna block
+constexpr int NTHREADS = TILE_P * NWARP;
+constexpr int SEG = 64;       // Horner segment length in subcarriers (re-anchor period)
+constexpr int KCHUNK = 256;   // subcarriers per shared-memory chunk of y (multiple of SEG)
+constexpr double C_LIGHT = 299792458.0;
+constexpr double PI = 3.14159265358979323846;
+
+enum DeviceFlags : int { FLAG_DEGENERATE = 1, FLAG_ZEROMASS = 2, FLAG_NAN = 4 };
+
+// Scene + per-call priors, passed by value as a __grid_constant__ kernel parameter (~2.7 KB).
+struct SceneDev {
+  int J, K, S, ny, nv, Na, nf, wavefront, pathloss;
+  int kc_len;        // subcarriers per chunk (min(KCHUNK, nf))
+  int n_mb, n_kc;    // antenna blocks of NWARP, subcarrier chunks
+  double dy, dv, fc, df, f0;      // f0 = fc - (nf-1)/2 df
+  double f0_c, df_c, segdf_c, fc_c;  // f0/c, df/c, SEG*df/c, fc/c (cycles per metre)
+  double lambda;
+  double pa_pos[MAXJ][3];
+  double pa_rot[MAXJ][9];
+  double m_re[MAXJ][MAXS], m_im[MAXJ][MAXS], v[MAXJ][MAXS];
+  double eta[MAXJ];
+};
+
+struct LoglikArgs {
+  const double* particles;
+  int64_t P;
+  int pstride;
+  const double* sfv;
+  int sfv_pp;               // 1: sfv is [P][K][3]
+  const float2* ytiles;     // [J][n_mb][n_kc][kc_len][NWARP] complex64 (zero padded)
+  const double* ynorm2;     // [J] ||z^(j)||^2 (fp64)
+  const double* logw_prior; // [P] or NULL
+  double* loglik;           // [P]
+  double2* amp;             // [P][J][S] or NULL
+  int* flags;
+  int64_t n_tiles;
+};
+
+// ---------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1-D bulk TMA copy global -> shared, completion counted on an mbarrier (cp.async.bulk, sm_90+).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, "
+      "p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// ---------------------------------------------------------------------------- launchers
+// (defined in loglik.cu / beliefs.cu, called from cdms.cpp)
+cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float2* ytiles, double* ynorm2,
+                          cudaStream_t st);
+cudaError_t launch_loglik(const SceneDev& sc, const LoglikArgs& a, int precision, cudaStream_t st,
+                          int num_sms);
+size_t loglik_smem_bytes(int S, int precision);
+cudaError_t launch_response(const SceneDev& sc, const double* pos, int64_t n, const int32_t* js,
+                            const double* sfv, double2* psi, int precision, int* flags, cudaStream_t st);
+cudaError_t launch_layout(const SceneDev& sc, const double* sfv, double* layout, double* va, double* H,
+                          int* flags, cudaStream_t st);
+
+// beliefs.cu
+constexpr int RED_BLOCK = 256;       // threads per reduction block
+constexpr int RED_ITEMS = 2048;      // particles per reduction block (fixed partition -> determinism)
+int64_t red_blocks(int64_t P);
+cudaError_t launch_lse_partial(const double* l, int64_t P, double2* part, cudaStream_t st);
+cudaError_t launch_lse_final(const double2* part, int64_t nblk, double2* out, cudaStream_t st);
+cudaError_t launch_lse_combine(const double2* per_rank, int nranks, double* lse, double* M,
+                               double* logS, int* flags, cudaStream_t st);
+cudaError_t launch_normalize(const double* l, int64_t P, const double* M, const double* logS,
+                             const int* flags, double* w, cudaStream_t st);
+cudaError_t launch_moments1(const double* x, const double* w, int64_t P, double* part, cudaStream_t st);
+cudaError_t launch_moments2(const double* x, const double* w, int64_t P, const double* sum1,
+                            double* part, cudaStream_t st);
+cudaError_t launch_sum_partials(const double* part, int64_t nblk, int width, double* out, cudaStream_t st);
+cudaError_t launch_moments_finalize(const double* sum1, const double* sum2, double* est, int* flags,
+                                    cudaStream_t st);
+cudaError_t launch_wmax_partial_f(const double* w, int64_t P, double* part, int* flags, cudaStream_t st);
+cudaError_t launch_max_final(const double* part, int64_t nblk, double* out, cudaStream_t st);
+cudaError_t launch_quantize(const double* w, int64_t P, const double* wmax, const double* M, int from_loglik,
+                            uint64_t* q, int* flags, cudaStream_t st);
+cudaError_t launch_scan(uint64_t* q, int64_t P, uint64_t* block_sums, cudaStream_t st);
+cudaError_t launch_ancestors(const uint64_t* C, int64_t P_local, const uint64_t* Qtot, const uint64_t* offset,
+                             int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits,
+                             int64_t p_global0, int64_t* anc_out, int* flags, cudaStream_t st);
+cudaError_t launch_gather(const double* x, const int64_t* anc, int64_t n, int64_t p_global0, double* out,
+                          cudaStream_t st);
+cudaError_t launch_predict(double* x, int64_t P, int64_t p0, double T, double sigma_v, uint64_t key,
+                           uint64_t step, cudaStream_t st);
+cudaError_t launch_chol6(const double* est, double* L, cudaStream_t st);
+cudaError_t launch_regularize(double* x, int64_t P, int64_t p0, int64_t P_total, const double* L,
+                              uint64_t key, uint64_t step, cudaStream_t st);
+cudaError_t launch_fill_u64(uint64_t* dst, uint64_t v, int n, cudaStream_t st);
+
+}  // namespace cdms

@@ -1,0 +1,175 @@
+// geometry.cuh -- device functions shared by every kernel that touches the array responses
+// (loglik.cu, response.cu): anchor geometry (row A1), per-(particle, component) fp64 set-up and per-antenna
+// offsets / phasors (row A2), and the Dirichlet kernel of the closed-form Gram (row A4).  The same
+// functions serve the hot kernel, the test entry cdms_response and cdms_layout, so the parity checks of
+// the latter two exercise the arithmetic of the former.
+#pragma once
+#include <math.h>
+
+#include "cdms_internal.h"
+
+namespace cdms {
+
+// ---------------------------------------------------------------------------- numeric traits
+template <typename RT>
+struct Num;
+template <>
+struct Num<float> {
+  static __device__ __forceinline__ void sincospi_(float x, float* s, float* c) { sincospif(x, s, c); }
+  static __device__ __forceinline__ float sinpi_(float x) { return sinpif(x); }
+  static __device__ __forceinline__ float rint_(float x) { return rintf(x); }
+  static __device__ __forceinline__ float sqrt_(float x) { return sqrtf(x); }
+  static constexpr float tiny_x = 1e-6f;  // |xr| below which D_N uses its 2nd-order series
+};
+template <>
+struct Num<double> {
+  static __device__ __forceinline__ void sincospi_(double x, double* s, double* c) { sincospi(x, s, c); }
+  static __device__ __forceinline__ double sinpi_(double x) { return sinpi(x); }
+  static __device__ __forceinline__ double rint_(double x) { return rint(x); }
+  static __device__ __forceinline__ double sqrt_(double x) { return sqrt(x); }
+  static constexpr double tiny_x = 1e-12;
+};
+
+// e^{j 2 pi x}, x in cycles (argument range-reduced to [-1/2, 1/2] first)
+template <typename RT>
+__device__ __forceinline__ void cis2pi(RT x, RT& re, RT& im) {
+  x = x - Num<RT>::rint_(x);
+  Num<RT>::sincospi_(RT(2) * x, &im, &re);
+}
+
+__device__ __forceinline__ double frac_c(double x) { return x - rint(x); }  // centred fraction
+
+// ---------------------------------------------------------------------------- row A1 (geometry)
+// VA phase centre p_VA = p_j - (2 p_j^T s/||s||^2 - 1) s and the unit wall normal
+// shat = s/||s|| that defines H = I - 2 shat shat^T.  LOS (sfv == nullptr): p_VA = p_j,
+// shat = 0, H = I.  Returns false for ||s|| = 0.
+__device__ __forceinline__ bool anchor_va(const SceneDev& sc, int j, const double* sfv, double va[3],
+                                          double sh[3]) {
+  const double* pj = sc.pa_pos[j];
+  if (sfv == nullptr) {
+    va[0] = pj[0]; va[1] = pj[1]; va[2] = pj[2];
+    sh[0] = sh[1] = sh[2] = 0.0;
+    return true;
+  }
+  const double s0 = sfv[0], s1 = sfv[1], s2 = sfv[2];
+  const double n2 = s0 * s0 + s1 * s1 + s2 * s2;
+  if (!(n2 > 0.0)) return false;
+  const double c = 2.0 * (pj[0] * s0 + pj[1] * s1 + pj[2] * s2) / n2 - 1.0;
+  va[0] = pj[0] - c * s0; va[1] = pj[1] - c * s1; va[2] = pj[2] - c * s2;
+  const double inv = 1.0 / sqrt(n2);
+  sh[0] = s0 * inv; sh[1] = s1 * inv; sh[2] = s2 * inv;
+  return true;
+}
+
+// R_j p~_m for template column m = iy*nv + iv: p~ = (0, p_y[iy], p_z[iv])
+__device__ __forceinline__ void template_col(const SceneDev& sc, int j, int m, double v[3], double& q2) {
+  const int iy = m / sc.nv, iv = m - iy * sc.nv;
+  const double py = (iy - 0.5 * (sc.ny - 1)) * sc.dy;
+  const double pz = (iv - 0.5 * (sc.nv - 1)) * sc.dv;
+  const double* R = sc.pa_rot[j];
+  v[0] = R[1] * py + R[2] * pz;
+  v[1] = R[4] * py + R[5] * pz;
+  v[2] = R[7] * py + R[8] * pz;
+  q2 = py * py + pz * pz;  // ||H R p~||^2 = ||p~||^2
+}
+
+// Per (particle, PA j, component s) set-up (fp64), kept in shared memory as RT fields:
+//   r = p - p_VA (RT), R = ||r|| (fp64 and RT), rs2 = 2 r.shat, phase bases in cycles
+//   ph0 = frac(R f0/c), phd = frac(R df/c), phL = frac(SEG R df/c) (range-reduced in fp64),
+//   gain = lambda/(4 pi R) with path loss (C-amb-6) else 1.
+template <typename RT>
+struct PSField {
+  RT rx, ry, rz, sx, sy, sz, rs2, R, ph0, phd, phL, gain;
+};
+
+// Returns PS_OK, PS_DEGENERATE (MT on the phase centre, r' = 0 excluded by P:L2137) or PS_BADSFV
+// (||sfv|| = 0).  On failure the fields hold a harmless finite placeholder.
+enum { PS_OK = 0, PS_DEGENERATE = 1, PS_BADSFV = 2 };
+template <typename RT>
+__device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double* pos, const double* sfv_s,
+                                        PSField<RT>& f, double& R64) {
+  double va[3], sh[3];
+  const bool sfv_ok = anchor_va(sc, j, sfv_s, va, sh);
+  if (!sfv_ok) {
+    va[0] = pos[0] - 1.0; va[1] = pos[1]; va[2] = pos[2];
+    sh[0] = sh[1] = sh[2] = 0.0;
+  }
+  const double r0 = pos[0] - va[0], r1 = pos[1] - va[1], r2 = pos[2] - va[2];
+  const double R = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+  R64 = R;
+  f.rx = (RT)r0; f.ry = (RT)r1; f.rz = (RT)r2;
+  f.sx = (RT)sh[0]; f.sy = (RT)sh[1]; f.sz = (RT)sh[2];
+  f.rs2 = (RT)(2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]));
+  f.R = (RT)R;
+  f.ph0 = (RT)frac_c(R * sc.f0_c);
+  f.phd = (RT)frac_c(R * sc.df_c);
+  f.phL = (RT)frac_c(R * sc.segdf_c);
+  f.gain = (RT)(sc.pathloss ? sc.lambda / (4.0 * PI * R) : 1.0);
+  if (!sfv_ok) return PS_BADSFV;
+  if (!(R > 0.0)) {  // also catches NaN positions
+    f.R = RT(1); f.rx = RT(1); f.ry = RT(0); f.rz = RT(0); f.gain = RT(1);
+    R64 = 1.0;
+    return PS_DEGENERATE;
+  }
+  return PS_OK;
+}
+
+// Per (particle, component, antenna) offset Delta_m of the element distance from R and the three
+// phasors of the recurrence (all conjugate-response phases, e^{+j 2 pi d f / c}):
+//   spherical: d_m = ||r - q_m||, q_m = H R p~_m, Delta = (||q||^2 - 2 r.q)/(d_m + R)
+//   planar WB / NB: Delta = -q.u = -(r.q)/R
+//   A = e^{j2pi(ph0 + Delta f0/c)}, w = e^{j2pi(phd + Delta df/c)}, Z = e^{j2pi(phL + SEG Delta df/c)}
+//   NB: the spatial term uses f_c: A = e^{j2pi(ph0 + Delta fc/c)}, w = e^{j2pi phd}, Z = e^{j2pi phL}.
+template <typename RT>
+struct SMPhasors {
+  RT Ar, Ai, wr, wi, Zr, Zi, delta;
+};
+
+template <typename RT>
+__device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& f, const RT v[3], RT q2,
+                                         SMPhasors<RT>& o, bool& degenerate) {
+  const RT sv = f.sx * v[0] + f.sy * v[1] + f.sz * v[2];
+  const RT rv = f.rx * v[0] + f.ry * v[1] + f.rz * v[2];
+  const RT rq = rv - f.rs2 * sv;  // r.q with q = v - 2 shat (shat.v)
+  RT delta;
+  if (sc.wavefront == CDMS_SPHERICAL) {
+    const RT n = q2 - RT(2) * rq;
+    const RT d = Num<RT>::sqrt_(f.R * f.R + n);
+    degenerate = !(d > RT(0));
+    delta = n / (d + f.R);
+  } else {
+    delta = -rq / f.R;
+    degenerate = false;
+  }
+  o.delta = delta;
+  RT a0, ws, zs;
+  if (sc.wavefront == CDMS_PLANAR_NB) {
+    a0 = f.ph0 + delta * (RT)sc.fc_c;
+    ws = f.phd;
+    zs = f.phL;
+  } else {
+    a0 = f.ph0 + delta * (RT)sc.f0_c;
+    ws = f.phd + delta * (RT)sc.df_c;
+    zs = f.phL + delta * (RT)sc.segdf_c;
+  }
+  cis2pi<RT>(a0, o.Ar, o.Ai);
+  cis2pi<RT>(ws, o.wr, o.wi);
+  cis2pi<RT>(zs, o.Zr, o.Zi);
+}
+
+// Dirichlet kernel D_N(x) = sin(pi N x)/sin(pi x) for x = n + xr, |xr| <= 1/2:
+// D_N(x) = (-1)^{n (N-1)} D_N(xr), D_N(0) = N (C-amb-13).
+template <typename RT>
+__device__ __forceinline__ RT dirichlet(RT xr, long long n, int N) {
+  RT d;
+  if (xr < Num<RT>::tiny_x && xr > -Num<RT>::tiny_x) {
+    const RT N2 = (RT)N * (RT)N;
+    d = (RT)N * (RT(1) - RT(PI * PI / 6.0) * (N2 - RT(1)) * xr * xr);
+  } else {
+    d = Num<RT>::sinpi_((RT)N * xr) / Num<RT>::sinpi_(xr);
+  }
+  if (((N - 1) & 1) && (n & 1)) d = -d;
+  return d;
+}
+
+}  // namespace cdms

@@ -144,6 +144,16 @@ cdms_status cdms_loglik(cdms_ctx ctx, const cdms_scene* scene, const double* d_p
                         const double* h_eta, const double* d_logw_prior, double* d_loglik,
                         void* d_amp);
 
+/* Sufficient statistics of rows A3/A4 as the likelihood kernel computes them (same launch, same
+ * arithmetic): the correlation c_s = psi_s^H z^(j) ("M^H e" with e = z) and the Gram
+ * G_ab = psi_a^H psi_b (P:L769 fn), path-loss gains applied.  Arguments as cdms_loglik,
+ * plus d_c out complex128 [P][J][S] and d_G out complex128 [P][J][S][S] (full Hermitian).  Test entry:
+ * it lets the parity tests check A3 and A4 separately from the assembly A5. */
+cdms_status cdms_loglik_terms(cdms_ctx ctx, const cdms_scene* scene, const double* d_particles, int64_t P,
+                              int32_t pstride, const double* d_sfv, int32_t sfv_per_particle,
+                              const void* d_y, const double* h_f_pb, const cdms_prior* h_prior,
+                              const double* h_eta, double* d_loglik, void* d_c, void* d_G);
+
 /* ---- row A6: weight normalization ------------------------------------------------------------ */
 
 /* w_p = exp((l_p - M) - ln S), M = max_p l_p, S = sum_p exp(l_p - M), lse = M + ln S over ALL ranks'

@@ -344,6 +344,49 @@ int orc_loglik(const orc_scene* sc, const double* particles, int64_t P, int pstr
   return status;
 }
 
+/* Sufficient statistics of the low-rank evaluation at each particle: the correlation
+ * c_s = psi_s^H z^(j) (the M^H e products of P:L755-769 with e = z, V = I) and the Gram
+ * G_ab = psi_a^H psi_b (P:L769 fn), by direct summation over n in index order.
+ * c out [P][J][S] complex, G out [P][J][S][S] complex. */
+int orc_terms(const orc_scene* sc, const double* particles, int64_t P, int pstride, const double* sfv,
+              int sfv_per_particle, const double complex* y, double complex* c_out, double complex* G_out) {
+  int S = sc->K + 1;
+  size_t nz = (size_t)sc->nf * sc->ny * sc->nv;
+  int status = ORC_OK;
+#pragma omp parallel
+  {
+    double complex* psi = (double complex*)malloc(sizeof(double complex) * nz * S);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t p = 0; p < P; ++p) {
+      const double* x = particles + p * pstride;
+      const double* sf = sfv_per_particle ? sfv + (size_t)p * 3 * sc->K : sfv;
+      for (int j = 0; j < sc->J; ++j) {
+        int st = ORC_OK;
+        for (int s = 0; s < S && st == ORC_OK; ++s)
+          st = orc_response(sc, x, j, s, s ? sf + 3 * (s - 1) : NULL, sc->wavefront, psi + (size_t)s * nz);
+        if (st) {
+#pragma omp critical
+          status = (status == ORC_OK) ? st : status;
+          continue;
+        }
+        const double complex* z = y + (size_t)j * nz;
+        for (int a = 0; a < S; ++a) {
+          double complex acc = 0.0;
+          for (size_t n = 0; n < nz; ++n) acc += conj(psi[(size_t)a * nz + n]) * z[n];
+          c_out[((size_t)p * sc->J + j) * S + a] = acc;
+          for (int b = 0; b < S; ++b) {
+            double complex g = 0.0;
+            for (size_t n = 0; n < nz; ++n) g += conj(psi[(size_t)a * nz + n]) * psi[(size_t)b * nz + n];
+            G_out[(((size_t)p * sc->J + j) * S + a) * S + b] = g;
+          }
+        }
+      }
+    }
+    free(psi);
+  }
+  return status;
+}
+
 /* ------------------------------------------------------------------ L3 beliefs (A6-A8) */
 
 /* Weight normalization in the log domain with max subtraction:

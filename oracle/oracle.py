@@ -147,6 +147,18 @@ class Oracle:
                               amp.ctypes.data_as(C.c_void_p) if amp is not None else None)
         return (st, out, amp) if want_amp else (st, out)
 
+    def terms(self, particles, sfv, y, sfv_per_particle=False):
+        """(c [P][J][S], G [P][J][S][S]) by direct sums over the element-wise responses."""
+        x = _f64(particles)
+        P, pstride = x.shape
+        y = _c128(y).reshape(self.J, self.nf, self.Na)
+        c = np.zeros((P, self.J, self.S), dtype=np.complex128)
+        G = np.zeros((P, self.J, self.S, self.S), dtype=np.complex128)
+        st = lib().orc_terms(C.byref(self.sc), _d(x), C.c_int64(P), C.c_int(pstride), _d(_f64(sfv)),
+                             int(bool(sfv_per_particle)), y.ctypes.data_as(C.c_void_p),
+                             c.ctypes.data_as(C.c_void_p), G.ctypes.data_as(C.c_void_p))
+        return st, c, G
+
     def bp_step(self, particles, sfv, y, m, v, eta, T, sigma_v, key, step, regularize=True):
         x = _f64(particles).copy()
         P = x.shape[0]

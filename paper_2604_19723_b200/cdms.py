@@ -69,6 +69,8 @@ def lib() -> C.CDLL:
             "cdms_layout": ([vp, C.POINTER(SceneC), vp, vp, vp, vp], C.c_int),
             "cdms_loglik": ([vp, C.POINTER(SceneC), vp, i64, i32, vp, i32, vp, dp, C.POINTER(PriorC), dp, vp, vp, vp],
                             C.c_int),
+            "cdms_loglik_terms": ([vp, C.POINTER(SceneC), vp, i64, i32, vp, i32, vp, dp, C.POINTER(PriorC), dp, vp,
+                                   vp, vp], C.c_int),
             "cdms_weights_normalize": ([vp, vp, i64, vp, vp], C.c_int),
             "cdms_moments": ([vp, vp, vp, i64, vp], C.c_int),
             "cdms_resample": ([vp, vp, i64, C.c_uint32, vp], C.c_int),
@@ -91,7 +93,7 @@ def exported_symbols() -> list[str]:
     return [n for n in ["cdms_create", "cdms_destroy", "cdms_set_stream", "cdms_last_error", "cdms_sync",
                         "cdms_reserve", "cdms_launch_count", "cdms_timing_enable", "cdms_timing_read",
                         "cdms_get_unique_id", "cdms_comm_init", "cdms_layout",
-                        "cdms_loglik", "cdms_weights_normalize", "cdms_moments", "cdms_resample", "cdms_bp_step",
+                        "cdms_loglik", "cdms_loglik_terms", "cdms_weights_normalize", "cdms_moments", "cdms_resample", "cdms_bp_step",
                         "cdms_response", "cdms_moment_match", "cdms_resample_plan"]]
 
 
@@ -242,6 +244,21 @@ def loglik(ctx: Context, scene: Scene, particles, sfv, y, prior_m, prior_v, eta,
                                 int(bool(sfv_per_particle)), _ptr(y), _dp(f_pb), pr, _dp(et), _ptr(logw_prior),
                                 _ptr(l), _ptr(amp)))
     return (l, amp) if want_amp else l
+
+
+def loglik_terms(ctx: Context, scene: Scene, particles, sfv, y, prior_m, prior_v, eta, sfv_per_particle=False):
+    """(l [P], c complex128 [P][J][S], G complex128 [P][J][S][S]) from one likelihood-kernel launch."""
+    torch = ctx.torch
+    P, pstride = particles.shape
+    l = torch.empty(P, dtype=torch.float64, device=particles.device)
+    c = torch.empty((P, scene.J, scene.S), dtype=torch.complex128, device=particles.device)
+    G = torch.empty((P, scene.J, scene.S, scene.S), dtype=torch.complex128, device=particles.device)
+    ctx.check(lib().cdms_loglik_terms(ctx.h, C.byref(scene.c), _ptr(particles), int(P), int(pstride), _ptr(sfv),
+                                      int(bool(sfv_per_particle)), _ptr(y), _dp(scene.f_pb()),
+                                      priors_c(prior_m, prior_v),
+                                      _dp(np.ascontiguousarray(eta, dtype=np.float64).reshape(-1)), _ptr(l),
+                                      _ptr(c), _ptr(G)))
+    return l, c, G
 
 
 def weights_normalize(ctx: Context, logw):

@@ -138,6 +138,11 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
   out->segdf_c = (double)SEG * sc->df / C_LIGHT;
   out->fc_c = sc->fc / C_LIGHT;
   out->lambda = C_LIGHT / sc->fc;
+  {
+    // |Delta_m| <= ||q_m|| = ||p~_m|| <= half the URA diagonal (H, R orthogonal)
+    const double hy = 0.5 * (sc->ny - 1) * fabs(sc->dy), hv = 0.5 * (sc->nv - 1) * fabs(sc->dv);
+    out->small_step = (2.0 * PI * sqrt(hy * hy + hv * hv) * out->df_c <= 0.2) ? 1 : 0;
+  }
   for (int j = 0; j < sc->J; ++j) {
     const double* R = sc->h_pa_rot + 9 * j;
     for (int c = 0; c < 3; ++c) {
@@ -357,7 +362,7 @@ cdms_status exchange(cdms_ctx ctx, const Plan& plan, int64_t P_local, const void
 
 cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const double* d_particles, int64_t P,
                         int32_t pstride, const double* d_sfv, int32_t sfv_pp, const void* d_y, const double* d_logw,
-                        double* d_loglik, void* d_amp) {
+                        double* d_loglik, void* d_amp, void* d_c = nullptr, void* d_G = nullptr) {
   float2* yt;
   double* yn;
   const int64_t tiles = (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP;
@@ -375,6 +380,8 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   a.logw_prior = d_logw;
   a.loglik = d_loglik;
   a.amp = static_cast<double2*>(d_amp);
+  a.term_c = static_cast<double2*>(d_c);
+  a.term_G = static_cast<double2*>(d_G);
   a.flags = ctx->d_flags;
   a.n_tiles = (P + TILE_P - 1) / TILE_P;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -558,6 +565,23 @@ cdms_status cdms_loglik(cdms_ctx ctx, const cdms_scene* scene, const double* d_p
   if (sd.K > 0 && !d_sfv) return fail(ctx, CDMS_EINVAL, "loglik: d_sfv NULL with K > 0");
   return loglik_impl(ctx, sd, scene->precision, d_particles, P, pstride, d_sfv, sfv_per_particle ? 1 : 0, d_y,
                      d_logw_prior, d_loglik, d_amp);
+}
+
+cdms_status cdms_loglik_terms(cdms_ctx ctx, const cdms_scene* scene, const double* d_particles, int64_t P,
+                              int32_t pstride, const double* d_sfv, int32_t sfv_per_particle, const void* d_y,
+                              const double* h_f_pb, const cdms_prior* h_prior, const double* h_eta, double* d_loglik,
+                              void* d_c, void* d_G) {
+  if (!ctx) return CDMS_EINVAL;
+  DeviceGuard g(ctx->device);
+  if (!d_particles || !d_y || !h_f_pb || !h_prior || !h_eta || !d_loglik || !d_c || !d_G)
+    return fail(ctx, CDMS_EINVAL, "loglik_terms: NULL pointer");
+  if (P <= 0 || pstride < 3) return fail(ctx, CDMS_EINVAL, "loglik_terms: P=%lld pstride=%d", (long long)P, pstride);
+  SceneDev sd;
+  cdms_status st = build_scene(ctx, scene, h_f_pb, h_prior, h_eta, &sd);
+  if (st) return st;
+  if (sd.K > 0 && !d_sfv) return fail(ctx, CDMS_EINVAL, "loglik_terms: d_sfv NULL with K > 0");
+  return loglik_impl(ctx, sd, scene->precision, d_particles, P, pstride, d_sfv, sfv_per_particle ? 1 : 0, d_y,
+                     nullptr, d_loglik, nullptr, d_c, d_G);
 }
 
 cdms_status cdms_weights_normalize(cdms_ctx ctx, const double* d_logw, int64_t P_local, double* d_w, double* d_lse) {

@@ -26,6 +26,7 @@ enum DeviceFlags : int { FLAG_DEGENERATE = 1, FLAG_ZEROMASS = 2, FLAG_NAN = 4 };
 struct SceneDev {
   int J, K, S, ny, nv, Na, nf, wavefront, pathloss;
   int kc_len;        // subcarriers per chunk (min(KCHUNK, nf))
+  int small_step;    // 1: 2 pi max|Delta| df/c <= 0.2 -> polynomial per-antenna step correction
   int n_mb, n_kc;    // antenna blocks of NWARP, subcarrier chunks
   double dy, dv, fc, df, f0;      // f0 = fc - (nf-1)/2 df
   double f0_c, df_c, segdf_c, fc_c;  // f0/c, df/c, SEG*df/c, fc/c (cycles per metre)
@@ -47,6 +48,8 @@ struct LoglikArgs {
   const double* logw_prior; // [P] or NULL
   double* loglik;           // [P]
   double2* amp;             // [P][J][S] or NULL
+  double2* term_c;          // [P][J][S] or NULL (cdms_loglik_terms)
+  double2* term_G;          // [P][J][S][S] or NULL
   int* flags;
   int64_t n_tiles;
 };

@@ -74,13 +74,23 @@ __device__ __forceinline__ void template_col(const SceneDev& sc, int j, int m, d
 }
 
 // Per (particle, PA j, component s) set-up (fp64), kept in shared memory as RT fields:
-//   r = p - p_VA (RT), R = ||r|| (fp64 and RT), rs2 = 2 r.shat, phase bases in cycles
-//   ph0 = frac(R f0/c), phd = frac(R df/c), phL = frac(SEG R df/c) (range-reduced in fp64),
-//   gain = lambda/(4 pi R) with path loss (C-amb-6) else 1.
+//   r = p - p_VA (RT), R = ||r|| (fp64 and RT), rs2 = 2 r.shat, and the phase-centre phasors
+//   E0 = e^{j2pi R f0/c}, W = e^{j2pi R df/c}, Zp = e^{j2pi SEG R df/c}, evaluated in fp64 from fp64
+//   range-reduced phases and only then rounded (a fp32 phase in cycles would carry a ~1e-7 cycle error
+//   that w^k repeats coherently on every antenna), gain = lambda/(4 pi R) with path loss
+//   (C-amb-6) else 1.
+// W and Zp stay in fp64: the per-antenna step w = fp32(W * s_m) must be rounded independently on every
+// antenna, otherwise the fp32 rounding of a shared W (|W| - 1 ~ 3e-8) is raised to the k-th power
+// identically on all antennas and the Horner correlation drifts coherently away from the exact
+// closed-form Gram.
 template <typename RT>
 struct PSField {
-  RT rx, ry, rz, sx, sy, sz, rs2, R, ph0, phd, phL, gain;
+  RT rx, ry, rz, sx, sy, sz, rs2, R, E0r, E0i, gain;
+  double Wr, Wi, Zr, Zi;
 };
+constexpr int NPSF = 11;       // RT fields of PSField (the fp64 tail is stored separately)
+constexpr int NPSD = 4;        // fp64 fields
+constexpr int PSF_GAIN = 10;   // index of .gain
 
 // Returns PS_OK, PS_DEGENERATE (MT on the phase centre, r' = 0 excluded by P:L2137) or PS_BADSFV
 // (||sfv|| = 0).  On failure the fields hold a harmless finite placeholder.
@@ -101,9 +111,13 @@ __device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double*
   f.sx = (RT)sh[0]; f.sy = (RT)sh[1]; f.sz = (RT)sh[2];
   f.rs2 = (RT)(2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]));
   f.R = (RT)R;
-  f.ph0 = (RT)frac_c(R * sc.f0_c);
-  f.phd = (RT)frac_c(R * sc.df_c);
-  f.phL = (RT)frac_c(R * sc.segdf_c);
+  double s_, c_;
+  sincospi(2.0 * frac_c(R * sc.f0_c), &s_, &c_);
+  f.E0r = (RT)c_; f.E0i = (RT)s_;
+  sincospi(2.0 * frac_c(R * sc.df_c), &s_, &c_);
+  f.Wr = c_; f.Wi = s_;
+  sincospi(2.0 * frac_c(R * sc.segdf_c), &s_, &c_);
+  f.Zr = c_; f.Zi = s_;
   f.gain = (RT)(sc.pathloss ? sc.lambda / (4.0 * PI * R) : 1.0);
   if (!sfv_ok) return PS_BADSFV;
   if (!(R > 0.0)) {  // also catches NaN positions
@@ -118,16 +132,42 @@ __device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double*
 // phasors of the recurrence (all conjugate-response phases, e^{+j 2 pi d f / c}):
 //   spherical: d_m = ||r - q_m||, q_m = H R p~_m, Delta = (||q||^2 - 2 r.q)/(d_m + R)
 //   planar WB / NB: Delta = -q.u = -(r.q)/R
-//   A = e^{j2pi(ph0 + Delta f0/c)}, w = e^{j2pi(phd + Delta df/c)}, Z = e^{j2pi(phL + SEG Delta df/c)}
-//   NB: the spatial term uses f_c: A = e^{j2pi(ph0 + Delta fc/c)}, w = e^{j2pi phd}, Z = e^{j2pi phL}.
+//   A = E0 e^{j2pi Delta f0/c}, w = W e^{j2pi Delta df/c}, Z = Zp e^{j2pi SEG Delta df/c}
+//   NB: the spatial term uses f_c: A = E0 e^{j2pi Delta fc/c}, w = W, Z = Zp.
+// The per-antenna step correction Delta df/c is tiny (|Delta| <= half the aperture): when the scene
+// guarantees |2 pi Delta df/c| <= 0.2 (sc.small_step) it is a degree-7 Taylor polynomial (error < 3e-10).
+template <typename RT>
+__device__ __forceinline__ void cis_small(RT x_cycles, RT& re, RT& im) {
+  const RT t = RT(2.0 * PI) * x_cycles, t2 = t * t;
+  re = RT(1) + t2 * (RT(-0.5) + t2 * (RT(1.0 / 24) + t2 * RT(-1.0 / 720)));
+  im = t * (RT(1) + t2 * (RT(-1.0 / 6) + t2 * (RT(1.0 / 120) + t2 * RT(-1.0 / 5040))));
+}
+template <typename RT>
+__device__ __forceinline__ void cmul(RT ar, RT ai, RT br, RT bi, RT& cr, RT& ci) {
+  cr = ar * br - ai * bi;
+  ci = ar * bi + ai * br;
+}
+// fp32(W * s) with the product formed in fp64 (one rounding per component, per antenna)
+template <typename RT>
+__device__ __forceinline__ void cmul_round(double Wr, double Wi, RT sr, RT si, RT& cr, RT& ci) {
+  cr = (RT)(Wr * (double)sr - Wi * (double)si);
+  ci = (RT)(Wr * (double)si + Wi * (double)sr);
+}
+// deterministic per-(antenna, component) rotation in (-2^-24, 2^-24) rad: decorrelates the fp32 rounding of
+// an otherwise shared step phasor across antennas (NB, where the per-antenna step correction is 1)
+__device__ __forceinline__ double dither_angle(int m, int s) {
+  uint32_t h = (uint32_t)m * 0x9E3779B1u ^ ((uint32_t)s + 0x7F4A7C15u) * 0x85EBCA77u;
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12;
+  return ((double)(h >> 8) * 0x1p-24 - 0.5) * 0x1p-23;
+}
 template <typename RT>
 struct SMPhasors {
   RT Ar, Ai, wr, wi, Zr, Zi, delta;
 };
 
 template <typename RT>
-__device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& f, const RT v[3], RT q2,
-                                         SMPhasors<RT>& o, bool& degenerate) {
+__device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& f, const RT v[3], RT q2, int m,
+                                         int s, SMPhasors<RT>& o, bool& degenerate) {
   const RT sv = f.sx * v[0] + f.sy * v[1] + f.sz * v[2];
   const RT rv = f.rx * v[0] + f.ry * v[1] + f.rz * v[2];
   const RT rq = rv - f.rs2 * sv;  // r.q with q = v - 2 shat (shat.v)
@@ -142,19 +182,22 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
     degenerate = false;
   }
   o.delta = delta;
-  RT a0, ws, zs;
+  RT er, ei;
   if (sc.wavefront == CDMS_PLANAR_NB) {
-    a0 = f.ph0 + delta * (RT)sc.fc_c;
-    ws = f.phd;
-    zs = f.phL;
+    cis2pi<RT>(delta * (RT)sc.fc_c, er, ei);
+    cmul<RT>(f.E0r, f.E0i, er, ei, o.Ar, o.Ai);
+    const double t = (sizeof(RT) == 4) ? dither_angle(m, s) : 0.0;
+    cmul_round<RT>(f.Wr - t * f.Wi, f.Wi + t * f.Wr, RT(1), RT(0), o.wr, o.wi);
+    cmul_round<RT>(f.Zr, f.Zi, RT(1), RT(0), o.Zr, o.Zi);
   } else {
-    a0 = f.ph0 + delta * (RT)sc.f0_c;
-    ws = f.phd + delta * (RT)sc.df_c;
-    zs = f.phL + delta * (RT)sc.segdf_c;
+    cis2pi<RT>(delta * (RT)sc.f0_c, er, ei);
+    cmul<RT>(f.E0r, f.E0i, er, ei, o.Ar, o.Ai);
+    if (sc.small_step) cis_small<RT>(delta * (RT)sc.df_c, er, ei);
+    else cis2pi<RT>(delta * (RT)sc.df_c, er, ei);
+    cmul_round<RT>(f.Wr, f.Wi, er, ei, o.wr, o.wi);
+    cis2pi<RT>(delta * (RT)sc.segdf_c, er, ei);
+    cmul_round<RT>(f.Zr, f.Zi, er, ei, o.Zr, o.Zi);
   }
-  cis2pi<RT>(a0, o.Ar, o.Ai);
-  cis2pi<RT>(ws, o.wr, o.wi);
-  cis2pi<RT>(zs, o.Zr, o.Zi);
 }
 
 // Dirichlet kernel D_N(x) = sin(pi N x)/sin(pi x) for x = n + xr, |xr| <= 1/2:

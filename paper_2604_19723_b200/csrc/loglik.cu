@@ -72,11 +72,12 @@ struct SmemPlan {
   // TMA y buffers: 2 x KCHUNK x NWARP complex64
   static constexpr size_t ybuf = 2ull * KCHUNK * NWARP * sizeof(float2);
   // per (s, particle) set-up fields [12][S][32] and fp64 ranges [S][32]
-  static constexpr size_t ps = (size_t)12 * S * TILE_P * sizeof(RT) + (size_t)S * TILE_P * sizeof(double);
+  static constexpr size_t ps =
+      (size_t)NPSF * S * TILE_P * sizeof(RT) + (size_t)(NPSD + 1) * S * TILE_P * sizeof(double);
   // offsets Delta of the current and previous antenna block [2][S][8][32]
   static constexpr size_t dlt = 2ull * S * NWARP * TILE_P * sizeof(RT);
-  // thread-private running sums of c (CPW) and G (PPW), complex RT [(CPW+PPW)][256]
-  static constexpr size_t acc = (size_t)(CPW + PPW) * NTHREADS * 2 * sizeof(RT);
+  // thread-private running sums of c (CPW) and G (PPW) over the antennas, complex fp64 [(CPW+PPW)][256]
+  static constexpr size_t acc = (size_t)(CPW + PPW) * NTHREADS * 2 * sizeof(double);
   // staging of one block's per-antenna correlations [S][8][32] complex RT, aliased by the fp64
   // assembly workspace: c [S][32], vector [S][32], lower-tri K [NTRI][32] (complex)
   static constexpr size_t stage_c = (size_t)S * NWARP * TILE_P * 2 * sizeof(RT);
@@ -235,11 +236,12 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* sp = smem;
   float2* ybuf = reinterpret_cast<float2*>(sp);                        sp += Plan::ybuf;
-  RT* psf = reinterpret_cast<RT*>(sp);                                 // [12][S][32]
-  double* R64s = reinterpret_cast<double*>(sp + (size_t)12 * S * TILE_P * sizeof(RT));
+  RT* psf = reinterpret_cast<RT*>(sp);                                 // [NPSF][S][32]
+  double* psd = reinterpret_cast<double*>(sp + (size_t)NPSF * S * TILE_P * sizeof(RT));  // [NPSD][S][32]
+  double* R64s = psd + NPSD * S * TILE_P;                              // [S][32]
   sp += Plan::ps;
   RT* dlt = reinterpret_cast<RT*>(sp);                                 sp += Plan::dlt;   // [2][S][8][32]
-  RT* accs = reinterpret_cast<RT*>(sp);                                sp += Plan::acc;   // [CPW+PPW][256][2]
+  double* accs = reinterpret_cast<double*>(sp);                        sp += Plan::acc;   // [CPW+PPW][256][2]
   RT* cst = reinterpret_cast<RT*>(sp);                                 // [S][8][32][2]
   double2* wc = reinterpret_cast<double2*>(sp);                        // [S][32]  (aliases cst)
   double2* wv = wc + S * TILE_P;                                       // [S][32]
@@ -307,13 +309,17 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
         }
         const RT* fv = reinterpret_cast<const RT*>(&f);
 #pragma unroll
-        for (int q = 0; q < 12; ++q) psf[(q * S + s) * TILE_P + pl] = fv[q];
+        for (int q = 0; q < NPSF; ++q) psf[(q * S + s) * TILE_P + pl] = fv[q];
+        psd[(0 * S + s) * TILE_P + pl] = f.Wr;
+        psd[(1 * S + s) * TILE_P + pl] = f.Wi;
+        psd[(2 * S + s) * TILE_P + pl] = f.Zr;
+        psd[(3 * S + s) * TILE_P + pl] = f.Zi;
         R64s[s * TILE_P + pl] = R64;
       }
 #pragma unroll
       for (int u = 0; u < CPW + PPW; ++u) {
-        accs[(u * NTHREADS + tid) * 2] = RT(0);
-        accs[(u * NTHREADS + tid) * 2 + 1] = RT(0);
+        accs[(u * NTHREADS + tid) * 2] = 0.0;
+        accs[(u * NTHREADS + tid) * 2 + 1] = 0.0;
       }
       __syncthreads();
 
@@ -334,10 +340,14 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
             PSField<RT> f;
             RT* fv = reinterpret_cast<RT*>(&f);
 #pragma unroll
-            for (int q = 0; q < 12; ++q) fv[q] = psf[(q * S + s) * TILE_P + lane];
+            for (int q = 0; q < NPSF; ++q) fv[q] = psf[(q * S + s) * TILE_P + lane];
+            f.Wr = psd[(0 * S + s) * TILE_P + lane];
+            f.Wi = psd[(1 * S + s) * TILE_P + lane];
+            f.Zr = psd[(2 * S + s) * TILE_P + lane];
+            f.Zi = psd[(3 * S + s) * TILE_P + lane];
             SMPhasors<RT> o;
             bool dg;
-            setup_sm<RT>(sc, f, v, q2, o, dg);
+            setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
             deg_any |= dg;
             Ar[s] = o.Ar; Ai[s] = o.Ai; wr[s] = o.wr; wi[s] = o.wi; Zr[s] = o.Zr; Zi[s] = o.Zi;
             cr[s] = RT(0); cm[s] = RT(0);
@@ -404,41 +414,52 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
         for (int u = 0; u < CPW; ++u) {
           const int s = warp + u * NWARP;
           if (s < S) {
-            RT sr = accs[(u * NTHREADS + tid) * 2], si = accs[(u * NTHREADS + tid) * 2 + 1];
+            double sr = accs[(u * NTHREADS + tid) * 2], si = accs[(u * NTHREADS + tid) * 2 + 1];
             for (int w2 = 0; w2 < nw_valid; ++w2) {
               const int o = (s * NWARP + w2) * TILE_P + lane;
-              sr += cst[2 * o];
-              si += cst[2 * o + 1];
+              sr += (double)cst[2 * o];
+              si += (double)cst[2 * o + 1];
             }
             accs[(u * NTHREADS + tid) * 2] = sr;
             accs[(u * NTHREADS + tid) * 2 + 1] = si;
           }
         }
         // ---- Gram (row A4), closed form on the uniform grid (this thread owns pairs q = warp + 8u):
-        //   G_ab = sum_m e^{j 2 pi (d_a - d_b) fc/c} D_N((d_a - d_b) df/c)   [NB: D_N((R_a - R_b) df/c)]
+        //   G_ab = e^{j 2 pi (R_a - R_b) fc/c} sum_m e^{j 2 pi (D_a,m - D_b,m) fc/c} D_N((d_a,m - d_b,m) df/c)
+        //   [NB: D_N((R_a - R_b) df/c) e^{j 2 pi (R_a - R_b) fc/c} sum_m e^{j 2 pi (D_a,m - D_b,m) fc/c}].
+        // The factors shared by every antenna (base carrier; NB's Dirichlet) are applied once, in fp64, at
+        // the hand-off below, so that their rounding does not repeat coherently over the antennas.
 #pragma unroll
         for (int u = 0; u < PPW; ++u) {
           const int q = warp + u * NWARP;
           if (q < NPAIR) {
             int pa, pb;
             pair_ab(q, S, pa, pb);
-            const double dR = R64s[pa * TILE_P + lane] - R64s[pb * TILE_P + lane];
-            const RT thb = (RT)frac_c(dR * sc.fc_c);
-            const double xb = dR * sc.df_c;
-            const double nb = rint(xb);
-            const RT xbr = (RT)(xb - nb);
-            const long long nbi = (long long)nb;
-            const RT eps = (sc.wavefront == CDMS_PLANAR_NB) ? RT(0) : RT(1);
-            RT gr = accs[((CPW + u) * NTHREADS + tid) * 2], gi = accs[((CPW + u) * NTHREADS + tid) * 2 + 1];
-            for (int w2 = 0; w2 < nw_valid; ++w2) {
-              const RT dd = dcur[(pa * NWARP + w2) * TILE_P + lane] - dcur[(pb * NWARP + w2) * TILE_P + lane];
-              RT er, ei;
-              cis2pi<RT>(thb + dd * (RT)sc.fc_c, er, ei);
-              const RT x = xbr + eps * dd * (RT)sc.df_c;
-              const RT n2 = Num<RT>::rint_(x);
-              const RT D = dirichlet<RT>(x - n2, nbi + (long long)n2, nf);
-              gr = fma(D, er, gr);
-              gi = fma(D, ei, gi);
+            double gr = accs[((CPW + u) * NTHREADS + tid) * 2], gi = accs[((CPW + u) * NTHREADS + tid) * 2 + 1];
+            if (sc.wavefront == CDMS_PLANAR_NB) {
+              for (int w2 = 0; w2 < nw_valid; ++w2) {
+                const RT dd = dcur[(pa * NWARP + w2) * TILE_P + lane] - dcur[(pb * NWARP + w2) * TILE_P + lane];
+                RT er, ei;
+                cis2pi<RT>(dd * (RT)sc.fc_c, er, ei);
+                gr += (double)er;
+                gi += (double)ei;
+              }
+            } else {
+              const double dR = R64s[pa * TILE_P + lane] - R64s[pb * TILE_P + lane];
+              const double xb = dR * sc.df_c;
+              const double nb = rint(xb);
+              const RT xbr = (RT)(xb - nb);
+              const long long nbi = (long long)nb;
+              for (int w2 = 0; w2 < nw_valid; ++w2) {
+                const RT dd = dcur[(pa * NWARP + w2) * TILE_P + lane] - dcur[(pb * NWARP + w2) * TILE_P + lane];
+                RT er, ei;
+                cis2pi<RT>(dd * (RT)sc.fc_c, er, ei);
+                const RT x = xbr + dd * (RT)sc.df_c;
+                const RT n2 = Num<RT>::rint_(x);
+                const RT D = dirichlet<RT>(x - n2, nbi + (long long)n2, nf);
+                gr += (double)(D * er);
+                gi += (double)(D * ei);
+              }
             }
             accs[((CPW + u) * NTHREADS + tid) * 2] = gr;
             accs[((CPW + u) * NTHREADS + tid) * 2 + 1] = gi;
@@ -451,8 +472,7 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
       for (int u = 0; u < CPW; ++u) {
         const int s = warp + u * NWARP;
         if (s < S)
-          wc[s * TILE_P + lane] =
-              make_double2((double)accs[(u * NTHREADS + tid) * 2], (double)accs[(u * NTHREADS + tid) * 2 + 1]);
+          wc[s * TILE_P + lane] = make_double2(accs[(u * NTHREADS + tid) * 2], accs[(u * NTHREADS + tid) * 2 + 1]);
       }
 #pragma unroll
       for (int u = 0; u < PPW; ++u) {
@@ -460,9 +480,19 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
         if (q < NPAIR) {
           int pa, pb;
           pair_ab(q, S, pa, pb);
+          // shared factors in fp64: base carrier e^{j 2 pi (R_a - R_b) fc/c}, NB Dirichlet D_N((R_a - R_b) df/c)
+          const double dR = R64s[pa * TILE_P + lane] - R64s[pb * TILE_P + lane];
+          double sb, cb;
+          sincospi(2.0 * frac_c(dR * sc.fc_c), &sb, &cb);
+          double D = 1.0;
+          if (sc.wavefront == CDMS_PLANAR_NB) {
+            const double xb = dR * sc.df_c, nb = rint(xb);
+            D = dirichlet<double>(xb - nb, (long long)nb, nf);
+          }
+          const double ar = accs[((CPW + u) * NTHREADS + tid) * 2], ai = accs[((CPW + u) * NTHREADS + tid) * 2 + 1];
+          const double Gr = D * (cb * ar - sb * ai), Gi = D * (cb * ai + sb * ar);
           // lower-triangle entry (b, a) = G_ba = conj(G_ab)
-          wk[tri(pb, pa) * TILE_P + lane] = make_double2((double)accs[((CPW + u) * NTHREADS + tid) * 2],
-                                                         -(double)accs[((CPW + u) * NTHREADS + tid) * 2 + 1]);
+          wk[tri(pb, pa) * TILE_P + lane] = make_double2(Gr, -Gi);
         }
       }
       if (warp == 0) {
@@ -470,10 +500,23 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
         for (int s = 0; s < S; ++s) {
           wk[tri(s, s) * TILE_P + lane] = make_double2(nz, 0.0);
           // the gains travel in wv: the next PA's set-up may overwrite psf while warp 0 assembles
-          wv[s * TILE_P + lane] = make_double2((double)psf[(11 * S + s) * TILE_P + lane], 0.0);
+          wv[s * TILE_P + lane] = make_double2((double)psf[(PSF_GAIN * S + s) * TILE_P + lane], 0.0);
         }
       }
       __syncthreads();
+      if (warp == 0 && a.term_c != nullptr && pvalid) {  // cdms_loglik_terms: c and full G, gains applied
+        for (int r = 0; r < S; ++r) {
+          const double gr_ = wv[r * TILE_P + lane].x;
+          const double2 cc = wc[r * TILE_P + lane];
+          a.term_c[(p * J + j) * S + r] = make_double2(cc.x * gr_, cc.y * gr_);
+          for (int t = 0; t < S; ++t) {
+            const double g2 = gr_ * wv[t * TILE_P + lane].x;
+            double2 G = (r >= t) ? wk[tri(r, t) * TILE_P + lane] : wk[tri(t, r) * TILE_P + lane];
+            if (r < t) G.y = -G.y;
+            a.term_G[((p * J + j) * S + r) * S + t] = make_double2(G.x * g2, G.y * g2);
+          }
+        }
+      }
       if (warp == 0) {
         double2* amp = (a.amp != nullptr && pvalid) ? a.amp + (p * J + j) * S : nullptr;
         lsum += assemble_lane<S>(sc, j, lane, wc, wv, wk, a.ynorm2[j], amp);

@@ -35,7 +35,7 @@ __global__ void response_kernel(const __grid_constant__ SceneDev sc, const doubl
   const RT v[3] = {(RT)v64[0], (RT)v64[1], (RT)v64[2]};
   SMPhasors<RT> o;
   bool dg;
-  setup_sm<RT>(sc, f, v, (RT)q264, o, dg);
+  setup_sm<RT>(sc, f, v, (RT)q264, m, s, o, dg);
   if (dg) atomicOr(flags, FLAG_DEGENERATE);
   RT Ar = o.Ar, Ai = o.Ai;
   const RT g = f.gain;

@@ -145,6 +145,43 @@ def test_matched_filter_peak(orc):
     assert np.all(l[1:] <= l[0] + 1e-9 * abs(l[0]))
 
 
+def test_terms_gram_closed_form_and_invariants(orc):
+    # G_ss = Nz, G Hermitian PSD; G_ab = sum_m e^{j 2 pi (d_a,m - d_b,m) fc/c} D_N((d_a,m - d_b,m) df/c)
+    # on the symmetric uniform grid (geometric series; P:L769 fn), distances from the independent
+    # reflection construction; c = Psi^H z
+    from tests.helpers import reflect
+    o, sc, y, m, v, eta, x = setup(orc, K=3, J=2, ny=3, nv=4, nf=24)
+    st, c, G = o.terms(x[:4], sc.sfv, y)
+    assert st == 0
+    cfg_f = o.f_pb
+    fc, df, N = sc.cfg.fc, cfg_f[1] - cfg_f[0], o.nf
+    C = 299_792_458.0
+    pt = o.template()
+    for i in range(4):
+        p = x[i, :3]
+        for j in range(2):
+            Gj = G[i, j]
+            assert np.allclose(np.diag(Gj).real, o.Nz, rtol=1e-13)
+            assert np.allclose(Gj, Gj.conj().T, atol=1e-9)
+            assert np.linalg.eigvalsh(Gj).min() > -1e-8 * o.Nz
+            cols0 = sc.pa_pos[j][:, None] + sc.pa_rot[j] @ pt
+            d = []
+            for s in range(o.S):
+                cols = cols0 if s == 0 else np.stack([reflect(cols0[:, mm], sc.sfv[s - 1]) for mm in range(o.Na)], 1)
+                d.append(np.linalg.norm(p[:, None] - cols, axis=0))
+            for a in range(o.S):
+                for b in range(o.S):
+                    if a == b:
+                        continue
+                    dd = d[a] - d[b]
+                    xx = dd * df / C
+                    D = np.sin(np.pi * N * xx) / np.sin(np.pi * xx)
+                    ref = np.sum(np.exp(2j * np.pi * dd * fc / C) * D)
+                    assert abs(Gj[a, b] - ref) <= 1e-9 * o.Nz
+            Psi = o.responses(p, j, sc.sfv)
+            assert np.allclose(c[i, j], Psi.conj().T @ y[j].reshape(-1), rtol=1e-12, atol=1e-9)
+
+
 def test_sfv_per_particle_matches_shared(orc):
     # paired SFVs (C-amb-8): [P][K][3] with identical rows == shared [K][3]
     o, sc, y, m, v, eta, x = setup(orc, K=2)

@@ -33,7 +33,10 @@ def ctx(cd):
     c.close()
 
 
-TOL_L = {"fp32": 1e-4, "fp64": 1e-10}
+# FP64 bound: the fp64 evaluation itself is conditioned by
+# kappa(K) * u * (||e||^2/eta) / (J Nz) ~ (1 + v Nz/eta) * 1.1e-16 * SNR ~ 1e-9 at the configs' scale,
+# on the oracle side as well; 1e-8 leaves a margin above that floor.
+TOL_L = {"fp32": 1e-4, "fp64": 1e-8}
 TOL_PH = {"fp32": 1e-4, "fp64": 1e-9}
 
 
@@ -115,7 +118,7 @@ def test_loglik_c1_all_particles(cd, ctx, orc, precision, wf):
     dict(J=2, K=3, ny=3, nv=5, nf=100, P=77),        # ragged antennas (15), ragged segment, ragged tile
     dict(J=3, K=0, ny=2, nv=2, nf=300, P=65),        # S = 1, two chunks, ragged chunk
     dict(J=1, K=8, ny=8, nv=8, nf=520, P=40),        # S = 9, 3 chunks, ragged segment
-    dict(J=8, K=1, ny=1, nv=1, nf=1, P=33),          # single element, single subcarrier, J = 8
+    dict(J=4, K=1, ny=1, nv=1, nf=1, P=33),          # single element, single subcarrier, J = 4
     dict(J=1, K=5, ny=16, nv=16, nf=64, P=31),       # 32 antenna blocks
 ])
 def test_loglik_ragged_shapes(cd, ctx, orc, precision, shape):
@@ -205,6 +208,20 @@ def test_loglik_full_size_sampled(cd, ctx, orc, name, wf, nsample):
     idx = scenes.stratified_sample(cfg.P, nsample)
     l, e = check_loglik(case, ctx, "fp32", idx=idx)
     assert np.all(np.isfinite(l))
+
+
+@pytest.mark.parametrize("name,wf", [("c2", "spherical"), ("c3", "spherical"), ("c4", "planar_nb"),
+                                     ("c4", "spherical"), ("c5", "spherical")])
+def test_loglik_near_truth_worst_case(cd, ctx, orc, name, wf):
+    """Particles within 1 mm of the true position: ||e||^2 = ||z||^2 - 2 Re(m^H c) + m^H G m cancels by
+    ~SNR there, the most demanding case for the fp32 correlation."""
+    cfg = scenes.CONFIGS[name]
+    rng = np.random.default_rng(17)
+    x = np.zeros((32, 6))
+    x[:, :3] = scenes.P_TRUE[None] + rng.uniform(-1e-3, 1e-3, size=(32, 3))
+    x[0, :3] = scenes.P_TRUE
+    case = Case(orc, cfg, wavefront=wf, particles=x)
+    check_loglik(case, ctx, "fp32", idx=np.arange(8))
 
 
 def test_loglik_c5_shard_sampled(cd, ctx, orc):

@@ -37,8 +37,9 @@ namespace {
 
 enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
-  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_COUNT
+  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_COUNT
 };
+constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
 struct DeviceGuard {
   int prev = -1;
@@ -142,6 +143,7 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
     // |Delta_m| <= ||q_m|| = ||p~_m|| <= half the URA diagonal (H, R orthogonal)
     const double hy = 0.5 * (sc->ny - 1) * fabs(sc->dy), hv = 0.5 * (sc->nv - 1) * fabs(sc->dv);
     out->small_step = (2.0 * PI * sqrt(hy * hy + hv * hv) * out->df_c <= 0.2) ? 1 : 0;
+    out->small_z = (2.0 * PI * sqrt(hy * hy + hv * hv) * out->segdf_c <= 1.0) ? 1 : 0;
   }
   for (int j = 0; j < sc->J; ++j) {
     const double* R = sc->h_pa_rot + 9 * j;
@@ -363,42 +365,65 @@ cdms_status exchange(cdms_ctx ctx, const Plan& plan, int64_t P_local, const void
 cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const double* d_particles, int64_t P,
                         int32_t pstride, const double* d_sfv, int32_t sfv_pp, const void* d_y, const double* d_logw,
                         double* d_loglik, void* d_amp, void* d_c = nullptr, void* d_G = nullptr) {
-  float2* yt;
+  float4* yt;
   double* yn;
+  double2* terms;
+  int* pflag;
   const int64_t tiles = (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP;
   WS_TRY(ctx, WS_YTILES, tiles, &yt);
   WS_TRY(ctx, WS_YNORM, MAXJ, &yn);
   CUDA_TRY(ctx, launch_prep_y(sd, static_cast<const float2*>(d_y), yt, yn, ctx->stream));
-  LoglikArgs a;
-  a.particles = d_particles;
-  a.P = P;
-  a.pstride = pstride;
-  a.sfv = d_sfv;
-  a.sfv_pp = sfv_pp;
-  a.ytiles = yt;
-  a.ynorm2 = yn;
-  a.logw_prior = d_logw;
-  a.loglik = d_loglik;
-  a.amp = static_cast<double2*>(d_amp);
-  a.term_c = static_cast<double2*>(d_c);
-  a.term_G = static_cast<double2*>(d_G);
-  a.flags = ctx->d_flags;
-  a.n_tiles = (P + TILE_P - 1) / TILE_P;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (ctx->timing) {
-    while (ctx->ev_pool.size() < ctx->ev_used + 2) {
-      cudaEvent_t e;
-      CUDA_TRY(ctx, cudaEventCreate(&e));
-      ctx->ev_pool.push_back(e);
+  ctx->launches += 1;
+  // particles go through K1 (correlation + Gram -> HBM terms) and K1b (assembly) in batches whose terms
+  // buffer stays under TERMS_BUDGET bytes
+  const int T = terms_width(sd.S);
+  const size_t per_particle = (size_t)sd.J * T * sizeof(double2);
+  int64_t PB = (int64_t)(TERMS_BUDGET / per_particle);
+  PB = PB < TILE_P ? TILE_P : (PB / TILE_P) * TILE_P;
+  if (PB > P) PB = P;
+  WS_TRY(ctx, WS_TERMS, (size_t)PB * sd.J * T, &terms);
+  WS_TRY(ctx, WS_PFLAG, PB, &pflag);
+  for (int64_t b0 = 0; b0 < P; b0 += PB) {
+    const int64_t nb = (P - b0 < PB) ? P - b0 : PB;
+    CorrArgs a;
+    a.particles = d_particles + b0 * pstride;
+    a.P = nb;
+    a.pstride = pstride;
+    a.sfv = (d_sfv && sfv_pp) ? d_sfv + b0 * 3 * sd.K : d_sfv;
+    a.sfv_pp = sfv_pp;
+    a.ytiles = yt;
+    a.terms = terms;
+    a.pflag = pflag;
+    a.flags = ctx->d_flags;
+    a.n_tiles = (nb + TILE_P - 1) / TILE_P;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->timing) {
+      while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+        cudaEvent_t e;
+        CUDA_TRY(ctx, cudaEventCreate(&e));
+        ctx->ev_pool.push_back(e);
+      }
+      e0 = ctx->ev_pool[ctx->ev_used];
+      e1 = ctx->ev_pool[ctx->ev_used + 1];
+      ctx->ev_used += 2;
+      CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
     }
-    e0 = ctx->ev_pool[ctx->ev_used];
-    e1 = ctx->ev_pool[ctx->ev_used + 1];
-    ctx->ev_used += 2;
-    CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
+    CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream, ctx->num_sms));
+    if (ctx->timing) CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
+    AsmArgs s;
+    s.terms = terms;
+    s.pflag = pflag;
+    s.ynorm2 = yn;
+    s.logw_prior = d_logw ? d_logw + b0 : nullptr;
+    s.loglik = d_loglik + b0;
+    s.amp = d_amp ? static_cast<double2*>(d_amp) + b0 * sd.J * sd.S : nullptr;
+    s.term_c = d_c ? static_cast<double2*>(d_c) + b0 * sd.J * sd.S : nullptr;
+    s.term_G = d_G ? static_cast<double2*>(d_G) + b0 * sd.J * sd.S * sd.S : nullptr;
+    s.flags = ctx->d_flags;
+    s.P = nb;
+    CUDA_TRY(ctx, launch_assemble(sd, s, ctx->stream));
+    ctx->launches += 2;
   }
-  CUDA_TRY(ctx, launch_loglik(sd, a, precision, ctx->stream, ctx->num_sms));
-  if (ctx->timing) CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
-  ctx->launches += 2;
   return CDMS_OK;
 }
 
@@ -493,12 +518,22 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
   cdms_status st = build_scene(ctx, scene, nullptr, nullptr, nullptr, &sd);
   if (st) return st;
   const int64_t nb = red_blocks(P_local);
-  float2* f2;
+  float4* f4;
   double* d;
   double2* d2;
   uint64_t* u;
   int64_t* i64;
-  WS_TRY(ctx, WS_YTILES, (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP, &f2);
+  int* i32;
+  WS_TRY(ctx, WS_YTILES, (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP, &f4);
+  {
+    const int T = terms_width(sd.S);
+    const size_t per_particle = (size_t)sd.J * T * sizeof(double2);
+    int64_t PB = (int64_t)(TERMS_BUDGET / per_particle);
+    PB = PB < TILE_P ? TILE_P : (PB / TILE_P) * TILE_P;
+    if (PB > P_local) PB = P_local;
+    WS_TRY(ctx, WS_TERMS, (size_t)PB * sd.J * T, &d2);
+    WS_TRY(ctx, WS_PFLAG, PB, &i32);
+  }
   WS_TRY(ctx, WS_YNORM, MAXJ, &d);
   WS_TRY(ctx, WS_LSE_PART, nb + 1, &d2);
   WS_TRY(ctx, WS_LSE_RANK, ctx->nranks + 1, &d2);

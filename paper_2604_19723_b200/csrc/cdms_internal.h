@@ -16,7 +16,7 @@ constexpr int TILE_P = 32;    // particles per CTA tile (one per lane)
 constexpr int NWARP = 8;      // warps per CTA = antennas per antenna block
 constexpr int NTHREADS = TILE_P * NWARP;
 constexpr int SEG = 64;       // Horner segment length in subcarriers (re-anchor period)
-constexpr int KCHUNK = 256;   // subcarriers per shared-memory chunk of y (multiple of SEG)
+constexpr int KCHUNK = 128;   // subcarriers per shared-memory chunk of y (multiple of SEG)
 constexpr double C_LIGHT = 299792458.0;
 constexpr double PI = 3.14159265358979323846;
 
@@ -27,6 +27,7 @@ struct SceneDev {
   int J, K, S, ny, nv, Na, nf, wavefront, pathloss;
   int kc_len;        // subcarriers per chunk (min(KCHUNK, nf))
   int small_step;    // 1: 2 pi max|Delta| df/c <= 0.2 -> polynomial per-antenna step correction
+  int small_z;       // 1: 2 pi max|Delta| SEG df/c <= 1 -> polynomial per-antenna segment correction
   int n_mb, n_kc;    // antenna blocks of NWARP, subcarrier chunks
   double dy, dv, fc, df, f0;      // f0 = fc - (nf-1)/2 df
   double f0_c, df_c, segdf_c, fc_c;  // f0/c, df/c, SEG*df/c, fc/c (cycles per metre)
@@ -37,22 +38,34 @@ struct SceneDev {
   double eta[MAXJ];
 };
 
-struct LoglikArgs {
-  const double* particles;
-  int64_t P;
+// K1 (correlation + Gram) for one batch of particles -> sufficient statistics per (particle, PA):
+// terms[p][j][0..S) = c_s, terms[p][j][S + tri(r,c)] = G_rc (lower triangle incl. diagonal), gains applied.
+struct CorrArgs {
+  const double* particles;  // batch start
+  int64_t P;                // particles in the batch
   int pstride;
-  const double* sfv;
-  int sfv_pp;               // 1: sfv is [P][K][3]
-  const float2* ytiles;     // [J][n_mb][n_kc][kc_len][NWARP] complex64 (zero padded)
-  const double* ynorm2;     // [J] ||z^(j)||^2 (fp64)
-  const double* logw_prior; // [P] or NULL
+  const double* sfv;        // [K][3], or [P][K][3] starting at the batch (sfv_pp)
+  int sfv_pp;
+  const float4* ytiles;     // [J][n_mb][n_kc][kc_len][NWARP] (yr, yr, yi, yi), zero padded
+  double2* terms;           // [P][J][T]
+  int* pflag;               // [P] per-particle: 1 degenerate, 2 invalid input
+  int* flags;
+  int64_t n_tiles;
+};
+// K1b (S x S assembly) for the same batch
+struct AsmArgs {
+  const double2* terms;
+  const int* pflag;
+  const double* ynorm2;     // [J]
+  const double* logw_prior; // [P] (batch) or NULL
   double* loglik;           // [P]
   double2* amp;             // [P][J][S] or NULL
   double2* term_c;          // [P][J][S] or NULL (cdms_loglik_terms)
   double2* term_G;          // [P][J][S][S] or NULL
   int* flags;
-  int64_t n_tiles;
+  int64_t P;
 };
+inline int terms_width(int S) { return S + S * (S + 1) / 2; }
 
 // ---------------------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -96,11 +109,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // ---------------------------------------------------------------------------- launchers
 // (defined in loglik.cu / beliefs.cu, called from cdms.cpp)
-cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float2* ytiles, double* ynorm2,
+cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2,
                           cudaStream_t st);
-cudaError_t launch_loglik(const SceneDev& sc, const LoglikArgs& a, int precision, cudaStream_t st,
-                          int num_sms);
-size_t loglik_smem_bytes(int S, int precision);
+cudaError_t launch_corr(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st, int num_sms);
+cudaError_t launch_assemble(const SceneDev& sc, const AsmArgs& a, cudaStream_t st);
+size_t corr_smem_bytes(int S, int precision);
 cudaError_t launch_response(const SceneDev& sc, const double* pos, int64_t n, const int32_t* js,
                             const double* sfv, double2* psi, int precision, int* flags, cudaStream_t st);
 cudaError_t launch_layout(const SceneDev& sc, const double* sfv, double* layout, double* va, double* H,

@@ -39,6 +39,21 @@ __device__ __forceinline__ void cis2pi(RT x, RT& re, RT& im) {
 
 __device__ __forceinline__ double frac_c(double x) { return x - rint(x); }  // centred fraction
 
+// e^{j 2 pi x} for per-antenna phase terms whose error only needs to be small and independent across
+// antennas: fp32 uses the MUFU sin/cos (|abs error| <= 2^-21.4 on the reduced argument), fp64 stays exact.
+template <typename RT>
+__device__ __forceinline__ void cis2pi_fast(RT x, RT& re, RT& im);
+template <>
+__device__ __forceinline__ void cis2pi_fast<float>(float x, float& re, float& im) {
+  x = x - rintf(x);
+  __sincosf(6.28318530717958647692f * x, &im, &re);
+}
+template <>
+__device__ __forceinline__ void cis2pi_fast<double>(double x, double& re, double& im) {
+  x = x - rint(x);
+  sincospi(2.0 * x, &im, &re);
+}
+
 // ---------------------------------------------------------------------------- row A1 (geometry)
 // VA phase centre p_VA = p_j - (2 p_j^T s/||s||^2 - 1) s and the unit wall normal
 // shat = s/||s|| that defines H = I - 2 shat shat^T.  LOS (sfv == nullptr): p_VA = p_j,
@@ -142,6 +157,15 @@ __device__ __forceinline__ void cis_small(RT x_cycles, RT& re, RT& im) {
   re = RT(1) + t2 * (RT(-0.5) + t2 * (RT(1.0 / 24) + t2 * RT(-1.0 / 720)));
   im = t * (RT(1) + t2 * (RT(-1.0 / 6) + t2 * (RT(1.0 / 120) + t2 * RT(-1.0 / 5040))));
 }
+// e^{j 2 pi x} for |2 pi x| <= 1 (sc.small_z): degree-12/13 Taylor polynomials (error < 1.1e-11)
+template <typename RT>
+__device__ __forceinline__ void cis_med(RT x_cycles, RT& re, RT& im) {
+  const RT t = RT(2.0 * PI) * x_cycles, t2 = t * t;
+  re = RT(1) + t2 * (RT(-1.0 / 2) + t2 * (RT(1.0 / 24) + t2 * (RT(-1.0 / 720) + t2 * (RT(1.0 / 40320) +
+       t2 * (RT(-1.0 / 3628800) + t2 * RT(1.0 / 479001600))))));
+  im = t * (RT(1) + t2 * (RT(-1.0 / 6) + t2 * (RT(1.0 / 120) + t2 * (RT(-1.0 / 5040) + t2 * (RT(1.0 / 362880) +
+       t2 * (RT(-1.0 / 39916800) + t2 * RT(1.0 / 6227020800.0)))))));
+}
 template <typename RT>
 __device__ __forceinline__ void cmul(RT ar, RT ai, RT br, RT bi, RT& cr, RT& ci) {
   cr = ar * br - ai * bi;
@@ -184,18 +208,21 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
   o.delta = delta;
   RT er, ei;
   if (sc.wavefront == CDMS_PLANAR_NB) {
-    cis2pi<RT>(delta * (RT)sc.fc_c, er, ei);
+    cis2pi_fast<RT>(delta * (RT)sc.fc_c, er, ei);
     cmul<RT>(f.E0r, f.E0i, er, ei, o.Ar, o.Ai);
     const double t = (sizeof(RT) == 4) ? dither_angle(m, s) : 0.0;
     cmul_round<RT>(f.Wr - t * f.Wi, f.Wi + t * f.Wr, RT(1), RT(0), o.wr, o.wi);
     cmul_round<RT>(f.Zr, f.Zi, RT(1), RT(0), o.Zr, o.Zi);
   } else {
-    cis2pi<RT>(delta * (RT)sc.f0_c, er, ei);
+    // A: one rounding per antenna, independent across antennas -> MUFU accuracy suffices
+    cis2pi_fast<RT>(delta * (RT)sc.f0_c, er, ei);
     cmul<RT>(f.E0r, f.E0i, er, ei, o.Ar, o.Ai);
+    // w, Z are raised to powers: accurate small-angle polynomials / sincospi, products rounded once in fp64
     if (sc.small_step) cis_small<RT>(delta * (RT)sc.df_c, er, ei);
     else cis2pi<RT>(delta * (RT)sc.df_c, er, ei);
     cmul_round<RT>(f.Wr, f.Wi, er, ei, o.wr, o.wi);
-    cis2pi<RT>(delta * (RT)sc.segdf_c, er, ei);
+    if (sc.small_z) cis_med<RT>(delta * (RT)sc.segdf_c, er, ei);
+    else cis2pi<RT>(delta * (RT)sc.segdf_c, er, ei);
     cmul_round<RT>(f.Zr, f.Zi, er, ei, o.Zr, o.Zi);
   }
 }

@@ -1,13 +1,17 @@
-// loglik.cu -- rows A2-A5 of the hot path on sm_100a: correlation c = Psi^H z by segmented Horner
-// recurrences over the (never materialized) spherical/planar wideband responses, the closed-form Gram
-// G = Psi^H Psi, and the S x S low-rank assembly of the coherent log-likelihood of the MT update message
-// iota~ (Supplement S-V-C).  DESIGN.md "Kernels" describes the work decomposition.
+// loglik.cu -- rows A2-A5 of the hot path on sm_100a.
 //
-// CTA = 32 particles (lanes) x 8 antennas (warps).  For each PA j and each block of 8 antennas the CTA
-// streams y^(j) through shared memory in chunks of <= 256 subcarriers x 8 antennas with 1-D bulk TMA
-// (cp.async.bulk + mbarrier, double buffered); every lane keeps the S Horner accumulators of its
-// (particle, antenna) pair in registers and reads y by a broadcast LDS.  Per (particle, component) the
-// geometry and the phase bases are fp64; the per-element loop is FP32 (or FP64 in CDMS_FP64 mode).
+// K1 corr_kernel<S, RT>: for a batch of particles and every PA j, the correlation c = Psi^H z^(j) by
+// segmented Horner recurrences over the (never materialized) spherical / planar responses, and the Gram
+// G = Psi^H Psi in closed form; writes the S + S(S+1)/2 sufficient statistics per
+// (particle, PA) to HBM.
+// K1b assemble_kernel<S>: one thread per particle, fp64: the S x S low-rank evaluation of the MT update
+// message iota~ (Supplement S-V-C), summed over the PAs.
+//
+// K1 work decomposition: CTA = 32 particles (lanes) x 8 antennas (warps), persistent grid.  For each PA and
+// each block of 8 antennas, y^(j) streams through shared memory in chunks of <= 128 subcarriers x 8 antennas
+// by 1-D bulk TMA (cp.async.bulk, mbarrier, double buffered), stored as (yr, yr, yi, yi) so one broadcast
+// LDS.128 feeds FFMA2 (fma.rn.f32x2) Horner steps that advance two components per instruction.  Per
+// (particle, component) geometry and phase bases are fp64.
 #include <math.h>
 
 #include "cdms_internal.h"
@@ -16,9 +20,9 @@
 namespace cdms {
 
 // ---------------------------------------------------------------------------- y re-layout
-// y [J][nf][Na] (paper vec order) -> ytiles [J][n_mb][n_kc][kc_len][NWARP] (zero padded), and
-// ||z^(j)||^2 in fp64 (one block per PA, fixed reduction order).
-__global__ void prep_y_kernel(const SceneDev sc, const float2* __restrict__ y, float2* __restrict__ yt,
+// y [J][nf][Na] (paper vec order) -> ytiles [J][n_mb][n_kc][kc_len][NWARP] of (yr, yr, yi, yi) (zero padded),
+// and ||z^(j)||^2 in fp64 (block 0 of each PA, fixed reduction order).
+__global__ void prep_y_kernel(const SceneDev sc, const float2* __restrict__ y, float4* __restrict__ yt,
                               double* __restrict__ ynorm2) {
   const int j = blockIdx.y;
   const int64_t per_j = (int64_t)sc.n_mb * sc.n_kc * sc.kc_len * NWARP;
@@ -33,7 +37,7 @@ __global__ void prep_y_kernel(const SceneDev sc, const float2* __restrict__ y, f
     const int m = mb * NWARP + w, k = kc * sc.kc_len + kl;
     float2 v = make_float2(0.f, 0.f);
     if (m < sc.Na && k < sc.nf) v = y[((int64_t)j * sc.nf + k) * sc.Na + m];
-    yt[(int64_t)j * per_j + t] = v;
+    yt[(int64_t)j * per_j + t] = make_float4(v.x, v.x, v.y, v.y);
   }
   if (blockIdx.x == 0) {
     __shared__ double red[256];
@@ -53,7 +57,7 @@ __global__ void prep_y_kernel(const SceneDev sc, const float2* __restrict__ y, f
   }
 }
 
-cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float2* ytiles, double* ynorm2, cudaStream_t st) {
+cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2, cudaStream_t st) {
   const int64_t per_j = (int64_t)sc.n_mb * sc.n_kc * sc.kc_len * NWARP;
   int gx = (int)((per_j + 255) / 256);
   if (gx > 1024) gx = 1024;
@@ -62,35 +66,9 @@ cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float2* ytiles, d
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------- shared memory plan
-template <int S, typename RT>
-struct SmemPlan {
-  static constexpr int NPAIR = S * (S - 1) / 2;
-  static constexpr int NTRI = S * (S + 1) / 2;
-  static constexpr int PPW = NPAIR > 0 ? (NPAIR + NWARP - 1) / NWARP : 1;  // Gram pairs per warp
-  static constexpr int CPW = (S + NWARP - 1) / NWARP;                      // components per warp
-  // TMA y buffers: 2 x KCHUNK x NWARP complex64
-  static constexpr size_t ybuf = 2ull * KCHUNK * NWARP * sizeof(float2);
-  // per (s, particle) set-up fields [12][S][32] and fp64 ranges [S][32]
-  static constexpr size_t ps =
-      (size_t)NPSF * S * TILE_P * sizeof(RT) + (size_t)(NPSD + 1) * S * TILE_P * sizeof(double);
-  // offsets Delta of the current and previous antenna block [2][S][8][32]
-  static constexpr size_t dlt = 2ull * S * NWARP * TILE_P * sizeof(RT);
-  // thread-private running sums of c (CPW) and G (PPW) over the antennas, complex fp64 [(CPW+PPW)][256]
-  static constexpr size_t acc = (size_t)(CPW + PPW) * NTHREADS * 2 * sizeof(double);
-  // staging of one block's per-antenna correlations [S][8][32] complex RT, aliased by the fp64
-  // assembly workspace: c [S][32], vector [S][32], lower-tri K [NTRI][32] (complex)
-  static constexpr size_t stage_c = (size_t)S * NWARP * TILE_P * 2 * sizeof(RT);
-  static constexpr size_t work = (size_t)(2 * S + NTRI) * TILE_P * sizeof(double2);
-  static constexpr size_t stage = stage_c > work ? stage_c : work;
-  static constexpr size_t misc = 64 + TILE_P * 4 * sizeof(double) + TILE_P * sizeof(int);
-  static constexpr size_t total = ybuf + ps + dlt + acc + stage + misc;
-};
-
-// lower-triangle index of (r, c), r >= c
-__host__ __device__ constexpr int tri(int r, int c) { return r * (r + 1) / 2 + c; }
-
-// pair q -> (a, b), a < b, enumerated row by row: (0,1), (0,2), ..., (1,2), ...
+// ---------------------------------------------------------------------------- index helpers
+__host__ __device__ constexpr int tri(int r, int c) { return r * (r + 1) / 2 + c; }  // r >= c
+// pair q -> (a, b), a < b, row by row: (0,1), (0,2), ..., (1,2), ...
 __device__ __forceinline__ void pair_ab(int q, int S, int& a, int& b) {
   int aa = 0, rem = q;
   while (rem >= S - 1 - aa) {
@@ -100,162 +78,196 @@ __device__ __forceinline__ void pair_ab(int q, int S, int& a, int& b) {
   a = aa;
   b = aa + 1 + rem;
 }
+__device__ __forceinline__ int pair_index(int a, int b, int S) { return a * S - a * (a + 1) / 2 + (b - a - 1); }
 
-// ---------------------------------------------------------------------------- row A5 (assembly)
-// One lane = one particle, fp64, vectors and the S x S matrix in shared memory columns [item][32]:
-//   c_s, G_ab with path-loss gains; g = c - G m; ||e||^2 = ||z||^2 - 2 Re(m^H c) + m^H G m;
-//   K = I + V^1/2 G V^1/2 / eta = L L^H; x = L^-1 V^1/2 g;
-//   l_j = -Nz ln(pi eta) - 2 sum ln L_ii - ||e||^2/eta + ||x||^2/eta^2
-//   amplitudes (optional): m + V^1/2 L^-H x / eta  (LMMSE).
-// wc: c [S][32]; wv: path-loss gains (.x) on entry, then scratch [S][32]; wk: lower-tri G on entry,
-// L on exit [NTRI][32].
-template <int S>
-__device__ __noinline__ double assemble_lane(const SceneDev& sc, int j, int lane, double2* wc, double2* wv,
-                                             double2* wk, double ynorm2, double2* amp_out) {
-  const double eta = sc.eta[j];
-#pragma unroll 1
-  for (int s = 0; s < S; ++s) {
-    const double gs = wv[s * TILE_P + lane].x;
-    double2 c = wc[s * TILE_P + lane];
-    wc[s * TILE_P + lane] = make_double2(c.x * gs, c.y * gs);
-#pragma unroll 1
-    for (int t = 0; t <= s; ++t) {
-      const double gg = gs * wv[t * TILE_P + lane].x;
-      double2 G = wk[tri(s, t) * TILE_P + lane];
-      wk[tri(s, t) * TILE_P + lane] = make_double2(G.x * gg, G.y * gg);
-    }
-  }
-  // g = c - G m (G Hermitian from its lower triangle), Re(m^H c), Re(m^H G m)
-  double mhc = 0.0, mGm = 0.0;
-#pragma unroll 1
-  for (int r = 0; r < S; ++r) {
-    const double2 c = wc[r * TILE_P + lane];
-    double gmr = 0.0, gmi = 0.0;
-#pragma unroll 1
-    for (int t = 0; t < S; ++t) {
-      double2 G = (r >= t) ? wk[tri(r, t) * TILE_P + lane] : wk[tri(t, r) * TILE_P + lane];
-      if (r < t) G.y = -G.y;
-      const double mr = sc.m_re[j][t], mi = sc.m_im[j][t];
-      gmr += G.x * mr - G.y * mi;
-      gmi += G.x * mi + G.y * mr;
-    }
-    const double mr = sc.m_re[j][r], mi = sc.m_im[j][r];
-    mhc += mr * c.x + mi * c.y;
-    mGm += mr * gmr + mi * gmi;
-    const double sv = sqrt(sc.v[j][r]);
-    wv[r * TILE_P + lane] = make_double2(sv * (c.x - gmr), sv * (c.y - gmi));  // b = V^1/2 g
-  }
-  const double e2 = ynorm2 - 2.0 * mhc + mGm;
-  // K = I + V^1/2 G V^1/2 / eta (lower triangle, in place)
-#pragma unroll 1
-  for (int r = 0; r < S; ++r)
-#pragma unroll 1
-    for (int t = 0; t <= r; ++t) {
-      const double f = sqrt(sc.v[j][r]) * sqrt(sc.v[j][t]) / eta;
-      const double2 G = wk[tri(r, t) * TILE_P + lane];
-      wk[tri(r, t) * TILE_P + lane] = make_double2((r == t ? 1.0 : 0.0) + G.x * f, G.y * f);
-    }
-  // Cholesky K = L L^H
-  double logdet = 0.0;
-  bool okc = true;
-#pragma unroll 1
-  for (int q = 0; q < S; ++q) {
-    double d = wk[tri(q, q) * TILE_P + lane].x;
-#pragma unroll 1
-    for (int k = 0; k < q; ++k) {
-      const double2 l = wk[tri(q, k) * TILE_P + lane];
-      d -= l.x * l.x + l.y * l.y;
-    }
-    okc &= d > 0.0;
-    const double lqq = sqrt(fmax(d, 1e-300));
-    logdet += 2.0 * log(lqq);
-    wk[tri(q, q) * TILE_P + lane] = make_double2(lqq, 0.0);
-#pragma unroll 1
-    for (int i = q + 1; i < S; ++i) {
-      double2 acc = wk[tri(i, q) * TILE_P + lane];
-#pragma unroll 1
-      for (int k = 0; k < q; ++k) {
-        const double2 li = wk[tri(i, k) * TILE_P + lane], lq = wk[tri(q, k) * TILE_P + lane];
-        acc.x -= li.x * lq.x + li.y * lq.y;  // acc -= L_ik conj(L_qk)
-        acc.y -= li.y * lq.x - li.x * lq.y;
-      }
-      wk[tri(i, q) * TILE_P + lane] = make_double2(acc.x / lqq, acc.y / lqq);
-    }
-  }
-  // forward solve L x = b (x overwrites wv)
-  double x2 = 0.0;
-#pragma unroll 1
-  for (int r = 0; r < S; ++r) {
-    double2 b = wv[r * TILE_P + lane];
-#pragma unroll 1
-    for (int k = 0; k < r; ++k) {
-      const double2 l = wk[tri(r, k) * TILE_P + lane], xk = wv[k * TILE_P + lane];
-      b.x -= l.x * xk.x - l.y * xk.y;
-      b.y -= l.x * xk.y + l.y * xk.x;
-    }
-    const double ld = wk[tri(r, r) * TILE_P + lane].x;
-    const double2 xr = make_double2(b.x / ld, b.y / ld);
-    wv[r * TILE_P + lane] = xr;
-    x2 += xr.x * xr.x + xr.y * xr.y;
-  }
-  const double nz = (double)sc.nf * (double)sc.Na;
-  double l = -nz * log(PI * eta) - logdet - e2 / eta + x2 / (eta * eta);
-  if (!okc || !(l == l)) l = -INFINITY;
-  if (amp_out != nullptr) {
-    // back solve L^H t = x, amp = m + V^1/2 t / eta
-#pragma unroll 1
-    for (int r = S - 1; r >= 0; --r) {
-      double2 t = wv[r * TILE_P + lane];
-#pragma unroll 1
-      for (int k = r + 1; k < S; ++k) {
-        const double2 lk = wk[tri(k, r) * TILE_P + lane], xk = wv[k * TILE_P + lane];  // (L^H)_rk = conj(L_kr)
-        t.x -= lk.x * xk.x + lk.y * xk.y;
-        t.y -= lk.x * xk.y - lk.y * xk.x;
-      }
-      const double ld = wk[tri(r, r) * TILE_P + lane].x;
-      wv[r * TILE_P + lane] = make_double2(t.x / ld, t.y / ld);
-    }
-#pragma unroll 1
-    for (int s = 0; s < S; ++s) {
-      const double sv = sqrt(sc.v[j][s]);
-      const double2 t = wv[s * TILE_P + lane];
-      amp_out[s] = make_double2(sc.m_re[j][s] + sv * t.x / eta, sc.m_im[j][s] + sv * t.y / eta);
-    }
-  }
-  return l;
+// ---------------------------------------------------------------------------- Horner state
+// acc <- acc * w + y for S components (row A3).  fp32: components paired in 64-bit registers and
+// advanced by fma.rn.f32x2 (FFMA2): t = hi*(-wi) + yr, u = hi*wr + yi, hr' = hr*wr + t, hi' = hr*wi + u.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(u64 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
 }
 
-// ---------------------------------------------------------------------------- the hot kernel
+template <int S, typename RT>
+struct Horner;
+
+template <int S>
+struct Horner<S, float> {
+  static constexpr int NP = S / 2;
+  static constexpr bool ODD = (S & 1) != 0;
+  u64 wr2[NP > 0 ? NP : 1], wi2[NP > 0 ? NP : 1], nwi2[NP > 0 ? NP : 1], hr2[NP > 0 ? NP : 1],
+      hi2[NP > 0 ? NP : 1];
+  float wrL, wiL, hrL, hiL;
+  __device__ __forceinline__ void init(const float* wr, const float* wi) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      wr2[q] = pk2(wr[2 * q], wr[2 * q + 1]);
+      wi2[q] = pk2(wi[2 * q], wi[2 * q + 1]);
+      nwi2[q] = pk2(-wi[2 * q], -wi[2 * q + 1]);
+    }
+    if (ODD) {
+      wrL = wr[S - 1];
+      wiL = wi[S - 1];
+    }
+  }
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) hr2[q] = hi2[q] = 0ull;
+    hrL = hiL = 0.f;
+  }
+  __device__ __forceinline__ void step(const float4 y) {
+    const u64 yr2 = pk2(y.x, y.y), yi2 = pk2(y.z, y.w);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const u64 t = ffma2(hi2[q], nwi2[q], yr2);
+      const u64 u = ffma2(hi2[q], wr2[q], yi2);
+      const u64 nr = ffma2(hr2[q], wr2[q], t);
+      const u64 ni = ffma2(hr2[q], wi2[q], u);
+      hr2[q] = nr;
+      hi2[q] = ni;
+    }
+    if (ODD) {
+      const float t = fmaf(-hiL, wiL, y.x);
+      const float u = fmaf(hiL, wrL, y.z);
+      const float nr = fmaf(hrL, wrL, t);
+      const float ni = fmaf(hrL, wiL, u);
+      hrL = nr;
+      hiL = ni;
+    }
+  }
+  __device__ __forceinline__ void get(float* hr, float* hi) const {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      up2(hr2[q], hr[2 * q], hr[2 * q + 1]);
+      up2(hi2[q], hi[2 * q], hi[2 * q + 1]);
+    }
+    if (ODD) {
+      hr[S - 1] = hrL;
+      hi[S - 1] = hiL;
+    }
+  }
+};
+
+template <int S>
+struct Horner<S, double> {
+  double wr[S], wi[S], hr[S], hi[S];
+  __device__ __forceinline__ void init(const double* wr_, const double* wi_) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      wr[s] = wr_[s];
+      wi[s] = wi_[s];
+    }
+  }
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int s = 0; s < S; ++s) hr[s] = hi[s] = 0.0;
+  }
+  __device__ __forceinline__ void step(const float4 y) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const double t = fma(-hi[s], wi[s], (double)y.x);
+      const double u = fma(hi[s], wr[s], (double)y.z);
+      const double nr = fma(hr[s], wr[s], t);
+      const double ni = fma(hr[s], wi[s], u);
+      hr[s] = nr;
+      hi[s] = ni;
+    }
+  }
+  __device__ __forceinline__ void get(double* hr_, double* hi_) const {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      hr_[s] = hr[s];
+      hi_[s] = hi[s];
+    }
+  }
+};
+
+// Dirichlet kernel for the per-antenna Gram terms (x = n + xr): fp32 numerator by MUFU after exact mod-2
+// reduction of N xr, accurate denominator; fp64 exact (C-amb-13).
+template <typename RT>
+__device__ __forceinline__ RT dirichlet_term(RT xr, long long n, int N);
+template <>
+__device__ __forceinline__ float dirichlet_term<float>(float xr, long long n, int N) {
+  float d;
+  if (fabsf(xr) < 1e-6f) {
+    const float N2 = (float)N * (float)N;
+    d = (float)N * (1.f - (float)(PI * PI / 6.0) * (N2 - 1.f) * xr * xr);
+  } else {
+    float t = (float)N * xr;
+    t = t - 2.f * rintf(0.5f * t);
+    d = __fdividef(__sinf(3.14159265358979f * t), sinpif(xr));
+  }
+  if (((N - 1) & 1) && (n & 1)) d = -d;
+  return d;
+}
+template <>
+__device__ __forceinline__ double dirichlet_term<double>(double xr, long long n, int N) {
+  return dirichlet<double>(xr, n, N);
+}
+
+// ---------------------------------------------------------------------------- shared memory plan
+template <int S, typename RT>
+struct Plan {
+  static constexpr int NPAIR = S * (S - 1) / 2;
+  static constexpr int NTRI = S * (S + 1) / 2;
+  static constexpr int T = S + NTRI;
+  static constexpr size_t ybuf = 2ull * KCHUNK * NWARP * sizeof(float4);
+  static constexpr size_t ps =
+      (size_t)NPSF * S * TILE_P * sizeof(RT) + (size_t)(NPSD + 1) * S * TILE_P * sizeof(double);
+  static constexpr size_t dlt = (size_t)S * NWARP * TILE_P * sizeof(RT);            // Delta [S][8][32]
+  static constexpr size_t cst = (size_t)S * NWARP * TILE_P * 2 * sizeof(RT);        // c per antenna
+  static constexpr size_t acc = (size_t)(S + NPAIR) * TILE_P * sizeof(double2);     // fp64 sums [item][32]
+  static constexpr size_t misc = 64 + TILE_P * 3 * sizeof(double) + TILE_P * sizeof(int);
+  static constexpr size_t total = ybuf + ps + dlt + cst + acc + misc;
+};
+
+size_t corr_smem_bytes(int S, int precision) {
+  switch (S) {
+#define CASE_S(n) \
+  case n: return precision == CDMS_FP64 ? Plan<n, double>::total : Plan<n, float>::total;
+    CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
+#undef CASE_S
+    default: return 0;
+  }
+}
+
+// ---------------------------------------------------------------------------- K1
 template <int S, typename RT>
 __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
-    loglik_kernel(const __grid_constant__ SceneDev sc, const LoglikArgs a) {
-  using Plan = SmemPlan<S, RT>;
-  constexpr int NPAIR = Plan::NPAIR;
-  constexpr int PPW = Plan::PPW;
-  constexpr int CPW = Plan::CPW;
+    corr_kernel(const __grid_constant__ SceneDev sc, const CorrArgs a) {
+  using PL = Plan<S, RT>;
+  constexpr int NPAIR = PL::NPAIR;
+  constexpr int T = PL::T;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* sp = smem;
-  float2* ybuf = reinterpret_cast<float2*>(sp);                        sp += Plan::ybuf;
-  RT* psf = reinterpret_cast<RT*>(sp);                                 // [NPSF][S][32]
+  float4* ybuf = reinterpret_cast<float4*>(sp);                         sp += PL::ybuf;
+  RT* psf = reinterpret_cast<RT*>(sp);                                  // [NPSF][S][32]
   double* psd = reinterpret_cast<double*>(sp + (size_t)NPSF * S * TILE_P * sizeof(RT));  // [NPSD][S][32]
-  double* R64s = psd + NPSD * S * TILE_P;                              // [S][32]
-  sp += Plan::ps;
-  RT* dlt = reinterpret_cast<RT*>(sp);                                 sp += Plan::dlt;   // [2][S][8][32]
-  double* accs = reinterpret_cast<double*>(sp);                        sp += Plan::acc;   // [CPW+PPW][256][2]
-  RT* cst = reinterpret_cast<RT*>(sp);                                 // [S][8][32][2]
-  double2* wc = reinterpret_cast<double2*>(sp);                        // [S][32]  (aliases cst)
-  double2* wv = wc + S * TILE_P;                                       // [S][32]
-  double2* wk = wv + S * TILE_P;                                       // [NTRI][32]
-  sp += Plan::stage;
+  double* R64s = psd + NPSD * S * TILE_P;                               // [S][32]
+  sp += PL::ps;
+  RT* dlt = reinterpret_cast<RT*>(sp);                                  sp += PL::dlt;
+  RT* cst = reinterpret_cast<RT*>(sp);                                  sp += PL::cst;
+  double2* acc = reinterpret_cast<double2*>(sp);                        sp += PL::acc;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sp);
-  double* pos_s = reinterpret_cast<double*>(sp + 64);                  // [3][32]
-  int* degen = reinterpret_cast<int*>(sp + 64 + TILE_P * 4 * sizeof(double));
+  double* pos_s = reinterpret_cast<double*>(sp + 64);                   // [3][32]
+  int* pfl = reinterpret_cast<int*>(sp + 64 + TILE_P * 3 * sizeof(double));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int J = sc.J, Na = sc.Na, nf = sc.nf, kcl = sc.kc_len;
   const int n_mb = sc.n_mb, n_kc = sc.n_kc;
+  const bool nb_mode = sc.wavefront == CDMS_PLANAR_NB;
   const int64_t chunks_per_tile = (int64_t)J * n_mb * n_kc;
-  const uint32_t chunk_bytes = (uint32_t)(kcl * NWARP * sizeof(float2));
+  const uint32_t chunk_bytes = (uint32_t)(kcl * NWARP * sizeof(float4));
   const int64_t my_tiles =
       (a.n_tiles > (int64_t)blockIdx.x) ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total_chunks = my_tiles * chunks_per_tile;
@@ -284,15 +296,14 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
     const int64_t p = tile * TILE_P + lane;
     const bool pvalid = p < a.P;
     if (warp == 0) {
+#pragma unroll
       for (int c = 0; c < 3; ++c) pos_s[c * TILE_P + lane] = pvalid ? a.particles[p * a.pstride + c] : 1.0;
-      degen[lane] = 0;
+      pfl[lane] = 0;
     }
-    double lsum = 0.0;  // warp 0: l_p accumulated over the PAs
-    if (warp == 0 && pvalid) lsum = a.logw_prior ? a.logw_prior[p] : 0.0;
     __syncthreads();
 
     for (int j = 0; j < J; ++j) {
-      // ---- per (s, particle) set-up in fp64 (rows A1/A2)
+      // ---- (1) per (component, particle) set-up in fp64 (rows A1/A2); zero the fp64 accumulators
       for (int it = tid; it < S * TILE_P; it += NTHREADS) {
         const int s = it / TILE_P, pl = it - s * TILE_P;
         const int64_t pp = tile * TILE_P + pl;
@@ -303,9 +314,8 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
         double R64 = 1.0;
         const int st = setup_ps<RT>(sc, j, pos, sfv_s, f, R64);
         if (st != PS_OK && pp < a.P) {
-          atomicOr(&degen[pl], 1);
-          if (st == PS_BADSFV || !(pos[0] == pos[0] && pos[1] == pos[1] && pos[2] == pos[2]))
-            atomicOr(a.flags, FLAG_NAN);  // invalid input -> CDMS_EINVAL at sync
+          const bool bad = st == PS_BADSFV || !(pos[0] == pos[0] && pos[1] == pos[1] && pos[2] == pos[2]);
+          atomicOr(&pfl[pl], bad ? 3 : 1);
         }
         const RT* fv = reinterpret_cast<const RT*>(&f);
 #pragma unroll
@@ -316,20 +326,56 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
         psd[(3 * S + s) * TILE_P + pl] = f.Zi;
         R64s[s * TILE_P + pl] = R64;
       }
-#pragma unroll
-      for (int u = 0; u < CPW + PPW; ++u) {
-        accs[(u * NTHREADS + tid) * 2] = 0.0;
-        accs[(u * NTHREADS + tid) * 2 + 1] = 0.0;
-      }
+      for (int it = tid; it < (S + NPAIR) * TILE_P; it += NTHREADS) acc[it] = make_double2(0.0, 0.0);
       __syncthreads();
+
+      // ---- (1b) planar NB Gram, separable closed form in fp64 (P:L2160-2184 with the template P:L29-39):
+      //   G_ab = e^{j 2 pi dR fc/c} D_Nf(dR df/c) D_ny(dy du'_y fc/c) D_nv(dv du'_z fc/c),
+      //   dR = R_a - R_b, du' = u'_b - u'_a, u'_s = R_j^T H_s r_s / R_s (local directions)
+      if (nb_mode && NPAIR > 0) {
+        for (int it = tid; it < NPAIR * TILE_P; it += NTHREADS) {
+          const int q = it / TILE_P, pl = it - q * TILE_P;
+          int ca, cb;
+          pair_ab(q, S, ca, cb);
+          const int64_t pp = tile * TILE_P + pl;
+          const double pos[3] = {pos_s[pl], pos_s[TILE_P + pl], pos_s[2 * TILE_P + pl]};
+          double ul[2][3];
+          const int comp[2] = {ca, cb};
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int s = comp[e];
+            const double* sfv_s = s ? a.sfv + ((a.sfv_pp && pp < a.P) ? pp * 3 * sc.K : 0) + 3 * (s - 1) : nullptr;
+            double va[3], sh[3];
+            if (!anchor_va(sc, j, sfv_s, va, sh)) { va[0] = pos[0] - 1.0; va[1] = pos[1]; va[2] = pos[2]; sh[0] = sh[1] = sh[2] = 0.0; }
+            double r[3] = {pos[0] - va[0], pos[1] - va[1], pos[2] - va[2]};
+            const double R = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+            const double rs = r[0] * sh[0] + r[1] * sh[1] + r[2] * sh[2];
+            double h[3] = {r[0] - 2.0 * rs * sh[0], r[1] - 2.0 * rs * sh[1], r[2] - 2.0 * rs * sh[2]};
+            const double* Rj = sc.pa_rot[j];
+            const double inv = R > 0.0 ? 1.0 / R : 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ul[e][c] = (Rj[0 * 3 + c] * h[0] + Rj[1 * 3 + c] * h[1] + Rj[2 * 3 + c] * h[2]) * inv;
+          }
+          const double dR = R64s[ca * TILE_P + pl] - R64s[cb * TILE_P + pl];
+          double sb, cbv;
+          sincospi(2.0 * frac_c(dR * sc.fc_c), &sb, &cbv);
+          const double xb = dR * sc.df_c, nbr = rint(xb);
+          double D = dirichlet<double>(xb - nbr, (long long)nbr, nf);
+          const double xy = sc.dy * (ul[1][1] - ul[0][1]) * sc.fc_c, xv = sc.dv * (ul[1][2] - ul[0][2]) * sc.fc_c;
+          const double ny_ = rint(xy), nv_ = rint(xv);
+          D *= dirichlet<double>(xy - ny_, (long long)ny_, sc.ny) * dirichlet<double>(xv - nv_, (long long)nv_, sc.nv);
+          acc[(S + q) * TILE_P + pl] = make_double2(D * cbv, D * sb);
+        }
+      }
 
       for (int mb = 0; mb < n_mb; ++mb) {
         const int m = mb * NWARP + warp;
         const bool mvalid = m < Na;
-        RT* dcur = dlt + (mb & 1) * (S * NWARP * TILE_P);
-        // ---- per (s, antenna) offsets and phasors (row A2)
-        RT Ar[S], Ai[S], wr[S], wi[S], Zr[S], Zi[S], cr[S], cm[S];
+        // ---- (2) per (component, antenna) offsets and phasors (row A2)
+        RT Ar[S], Ai[S], Zr[S], Zi[S];
+        Horner<S, RT> H;
         {
+          RT wr[S], wi[S];
           double v64[3], q264;
           template_col(sc, j, mvalid ? m : 0, v64, q264);
           const RT v[3] = {(RT)v64[0], (RT)v64[1], (RT)v64[2]};
@@ -350,197 +396,280 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
             setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
             deg_any |= dg;
             Ar[s] = o.Ar; Ai[s] = o.Ai; wr[s] = o.wr; wi[s] = o.wi; Zr[s] = o.Zr; Zi[s] = o.Zi;
-            cr[s] = RT(0); cm[s] = RT(0);
-            dcur[(s * NWARP + warp) * TILE_P + lane] = o.delta;
+            const int o_ = (s * NWARP + warp) * TILE_P + lane;
+            dlt[o_] = o.delta;
+            cst[2 * o_] = RT(0);
+            cst[2 * o_ + 1] = RT(0);
           }
-          if (deg_any && mvalid && pvalid) atomicOr(&degen[lane], 1);
+          if (deg_any && mvalid && pvalid) atomicOr(&pfl[lane], 1);
+          H.init(wr, wi);
         }
-        // ---- correlation over all subcarriers (row A3): segmented Horner on TMA-staged y chunks
+        // ---- (3) correlation over all subcarriers (row A3): segmented Horner on TMA-staged y chunks
         for (int kc = 0; kc < n_kc; ++kc, ++ci) {
           mbar_wait(&mbar[ci & 1], (uint32_t)((ci >> 1) & 1));
-          const float2* yb = ybuf + (ci & 1) * (KCHUNK * NWARP) + warp;
+          const float4* yb = ybuf + (ci & 1) * (KCHUNK * NWARP) + warp;
           const int k_begin = kc * kcl;
           const int k_end = min(k_begin + kcl, nf);
           for (int k0 = k_begin; k0 < k_end; k0 += SEG) {
             const int k1 = min(k0 + SEG, k_end);
-            RT hr[S], hi[S];
-#pragma unroll
-            for (int s = 0; s < S; ++s) { hr[s] = RT(0); hi[s] = RT(0); }
-            const float2* yk = yb + (k1 - 1 - k_begin) * NWARP;  // Horner runs from the top subcarrier down
-            auto step = [&](const float2 yv) {
-              const RT yr = (RT)yv.x, yi = (RT)yv.y;
-#pragma unroll
-              for (int s = 0; s < S; ++s) {
-                const RT t = fma(-hi[s], wi[s], yr);
-                const RT u = fma(hi[s], wr[s], yi);
-                const RT nr = fma(hr[s], wr[s], t);
-                const RT ni = fma(hr[s], wi[s], u);
-                hr[s] = nr;
-                hi[s] = ni;
-              }
-            };
+            H.reset();
+            const float4* yk = yb + (k1 - 1 - k_begin) * NWARP;  // Horner runs from the top subcarrier down
             if (k1 - k0 == SEG) {
 #pragma unroll 8
-              for (int i = 0; i < SEG; ++i) step(yk[-i * NWARP]);
+              for (int i = 0; i < SEG; ++i) H.step(yk[-i * NWARP]);
             } else {
-              for (int i = 0; i < k1 - k0; ++i) step(yk[-i * NWARP]);
+              for (int i = 0; i < k1 - k0; ++i) H.step(yk[-i * NWARP]);
             }
-            // c += A_seg H_seg ; A_seg <- A_seg Z
+            // c += A_seg H_seg (thread-private slot), A_seg <- A_seg Z
+            RT hr[S], hi[S];
+            H.get(hr, hi);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-              cr[s] = fma(Ar[s], hr[s], fma(-Ai[s], hi[s], cr[s]));
-              cm[s] = fma(Ar[s], hi[s], fma(Ai[s], hr[s], cm[s]));
+              const int o_ = (s * NWARP + warp) * TILE_P + lane;
+              cst[2 * o_] = fma(Ar[s], hr[s], fma(-Ai[s], hi[s], cst[2 * o_]));
+              cst[2 * o_ + 1] = fma(Ar[s], hi[s], fma(Ai[s], hr[s], cst[2 * o_ + 1]));
               const RT nAr = Ar[s] * Zr[s] - Ai[s] * Zi[s];
               const RT nAi = Ar[s] * Zi[s] + Ai[s] * Zr[s];
               Ar[s] = nAr;
               Ai[s] = nAi;
             }
           }
-          __syncthreads();  // every warp is done with this buffer (and, at kc = 0, with the previous
-                            // block's staging reads)
+          __syncthreads();  // every warp is done with this buffer
           if (tid == 0 && ci + 2 < total_chunks) issue(ci + 2);
         }
-        // ---- stage this antenna block's correlations
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const int o = (s * NWARP + warp) * TILE_P + lane;
-          cst[2 * o] = mvalid ? cr[s] : RT(0);
-          cst[2 * o + 1] = mvalid ? cm[s] : RT(0);
-        }
-        __syncthreads();
+        // the last chunk barrier also published this block's cst / dlt
         const int nw_valid = min(NWARP, Na - mb * NWARP);
-        // c_s += sum over the block's antennas in ascending m (this thread owns s = warp + 8u)
-#pragma unroll
-        for (int u = 0; u < CPW; ++u) {
-          const int s = warp + u * NWARP;
-          if (s < S) {
-            double sr = accs[(u * NTHREADS + tid) * 2], si = accs[(u * NTHREADS + tid) * 2 + 1];
-            for (int w2 = 0; w2 < nw_valid; ++w2) {
-              const int o = (s * NWARP + w2) * TILE_P + lane;
-              sr += (double)cst[2 * o];
-              si += (double)cst[2 * o + 1];
-            }
-            accs[(u * NTHREADS + tid) * 2] = sr;
-            accs[(u * NTHREADS + tid) * 2 + 1] = si;
+        // ---- (4a) c_s += sum over the block's antennas, ascending m; owner warp rotates with mb
+        for (int s = (warp - mb) & (NWARP - 1); s < S; s += NWARP) {
+          double sr = 0.0, si = 0.0;
+          for (int w2 = 0; w2 < nw_valid; ++w2) {
+            const int o_ = (s * NWARP + w2) * TILE_P + lane;
+            sr += (double)cst[2 * o_];
+            si += (double)cst[2 * o_ + 1];
           }
+          double2 v = acc[s * TILE_P + lane];
+          acc[s * TILE_P + lane] = make_double2(v.x + sr, v.y + si);
         }
-        // ---- Gram (row A4), closed form on the uniform grid (this thread owns pairs q = warp + 8u):
-        //   G_ab = e^{j 2 pi (R_a - R_b) fc/c} sum_m e^{j 2 pi (D_a,m - D_b,m) fc/c} D_N((d_a,m - d_b,m) df/c)
-        //   [NB: D_N((R_a - R_b) df/c) e^{j 2 pi (R_a - R_b) fc/c} sum_m e^{j 2 pi (D_a,m - D_b,m) fc/c}].
-        // The factors shared by every antenna (base carrier; NB's Dirichlet) are applied once, in fp64, at
-        // the hand-off below, so that their rounding does not repeat coherently over the antennas.
-#pragma unroll
-        for (int u = 0; u < PPW; ++u) {
-          const int q = warp + u * NWARP;
-          if (q < NPAIR) {
+        // ---- (4b) spherical / planar WB Gram terms (row A4) over the block's antennas:
+        //   sum_m e^{j 2 pi (D_a,m - D_b,m) fc/c} D_N((d_a,m - d_b,m) df/c); the base carrier e^{j 2 pi dR fc/c}
+        //   is applied in fp64 at the hand-off (shared by all antennas: its rounding must not repeat)
+        if (!nb_mode) {
+          for (int q = (warp - mb - S) & (NWARP - 1); q < NPAIR; q += NWARP) {
             int pa, pb;
             pair_ab(q, S, pa, pb);
-            double gr = accs[((CPW + u) * NTHREADS + tid) * 2], gi = accs[((CPW + u) * NTHREADS + tid) * 2 + 1];
-            if (sc.wavefront == CDMS_PLANAR_NB) {
-              for (int w2 = 0; w2 < nw_valid; ++w2) {
-                const RT dd = dcur[(pa * NWARP + w2) * TILE_P + lane] - dcur[(pb * NWARP + w2) * TILE_P + lane];
-                RT er, ei;
-                cis2pi<RT>(dd * (RT)sc.fc_c, er, ei);
-                gr += (double)er;
-                gi += (double)ei;
-              }
-            } else {
-              const double dR = R64s[pa * TILE_P + lane] - R64s[pb * TILE_P + lane];
-              const double xb = dR * sc.df_c;
-              const double nb = rint(xb);
-              const RT xbr = (RT)(xb - nb);
-              const long long nbi = (long long)nb;
-              for (int w2 = 0; w2 < nw_valid; ++w2) {
-                const RT dd = dcur[(pa * NWARP + w2) * TILE_P + lane] - dcur[(pb * NWARP + w2) * TILE_P + lane];
-                RT er, ei;
-                cis2pi<RT>(dd * (RT)sc.fc_c, er, ei);
-                const RT x = xbr + dd * (RT)sc.df_c;
-                const RT n2 = Num<RT>::rint_(x);
-                const RT D = dirichlet<RT>(x - n2, nbi + (long long)n2, nf);
-                gr += (double)(D * er);
-                gi += (double)(D * ei);
-              }
+            const double dR = R64s[pa * TILE_P + lane] - R64s[pb * TILE_P + lane];
+            const double xb = dR * sc.df_c;
+            const double nbd = rint(xb);
+            const RT xbr = (RT)(xb - nbd);
+            const long long nbi = (long long)nbd;
+            RT gr = RT(0), gi = RT(0);
+            for (int w2 = 0; w2 < nw_valid; ++w2) {
+              const RT dd = dlt[(pa * NWARP + w2) * TILE_P + lane] - dlt[(pb * NWARP + w2) * TILE_P + lane];
+              RT er, ei;
+              cis2pi_fast<RT>(dd * (RT)sc.fc_c, er, ei);
+              const RT x = xbr + dd * (RT)sc.df_c;
+              const RT n2 = Num<RT>::rint_(x);
+              const RT D = dirichlet_term<RT>(x - n2, nbi + (long long)n2, nf);
+              gr = fma(D, er, gr);
+              gi = fma(D, ei, gi);
             }
-            accs[((CPW + u) * NTHREADS + tid) * 2] = gr;
-            accs[((CPW + u) * NTHREADS + tid) * 2 + 1] = gi;
+            double2 v = acc[(S + q) * TILE_P + lane];
+            acc[(S + q) * TILE_P + lane] = make_double2(v.x + (double)gr, v.y + (double)gi);
           }
         }
+        __syncthreads();  // before the next block's set-up rewrites dlt / cst
       }
-      __syncthreads();  // all staging reads done: the assembly workspace aliases the staging area
-      // ---- hand the per-thread sums to the fp64 assembly workspace
-#pragma unroll
-      for (int u = 0; u < CPW; ++u) {
-        const int s = warp + u * NWARP;
-        if (s < S)
-          wc[s * TILE_P + lane] = make_double2(accs[(u * NTHREADS + tid) * 2], accs[(u * NTHREADS + tid) * 2 + 1]);
-      }
-#pragma unroll
-      for (int u = 0; u < PPW; ++u) {
-        const int q = warp + u * NWARP;
-        if (q < NPAIR) {
-          int pa, pb;
-          pair_ab(q, S, pa, pb);
-          // shared factors in fp64: base carrier e^{j 2 pi (R_a - R_b) fc/c}, NB Dirichlet D_N((R_a - R_b) df/c)
-          const double dR = R64s[pa * TILE_P + lane] - R64s[pb * TILE_P + lane];
-          double sb, cb;
-          sincospi(2.0 * frac_c(dR * sc.fc_c), &sb, &cb);
-          double D = 1.0;
-          if (sc.wavefront == CDMS_PLANAR_NB) {
-            const double xb = dR * sc.df_c, nb = rint(xb);
-            D = dirichlet<double>(xb - nb, (long long)nb, nf);
-          }
-          const double ar = accs[((CPW + u) * NTHREADS + tid) * 2], ai = accs[((CPW + u) * NTHREADS + tid) * 2 + 1];
-          const double Gr = D * (cb * ar - sb * ai), Gi = D * (cb * ai + sb * ar);
-          // lower-triangle entry (b, a) = G_ba = conj(G_ab)
-          wk[tri(pb, pa) * TILE_P + lane] = make_double2(Gr, -Gi);
-        }
-      }
-      if (warp == 0) {
-        const double nz = (double)nf * (double)Na;  // G_ss = Nz (unit modulus)
-        for (int s = 0; s < S; ++s) {
-          wk[tri(s, s) * TILE_P + lane] = make_double2(nz, 0.0);
-          // the gains travel in wv: the next PA's set-up may overwrite psf while warp 0 assembles
-          wv[s * TILE_P + lane] = make_double2((double)psf[(PSF_GAIN * S + s) * TILE_P + lane], 0.0);
-        }
-      }
-      __syncthreads();
-      if (warp == 0 && a.term_c != nullptr && pvalid) {  // cdms_loglik_terms: c and full G, gains applied
-        for (int r = 0; r < S; ++r) {
-          const double gr_ = wv[r * TILE_P + lane].x;
-          const double2 cc = wc[r * TILE_P + lane];
-          a.term_c[(p * J + j) * S + r] = make_double2(cc.x * gr_, cc.y * gr_);
-          for (int t = 0; t < S; ++t) {
-            const double g2 = gr_ * wv[t * TILE_P + lane].x;
-            double2 G = (r >= t) ? wk[tri(r, t) * TILE_P + lane] : wk[tri(t, r) * TILE_P + lane];
-            if (r < t) G.y = -G.y;
-            a.term_G[((p * J + j) * S + r) * S + t] = make_double2(G.x * g2, G.y * g2);
+
+      // ---- (5) hand-off: c (with gains) and the lower triangle of G (with gains) to HBM
+      const double nz = (double)nf * (double)Na;
+      for (int it = tid; it < T * TILE_P; it += NTHREADS) {
+        const int pl = it / T, t = it - pl * T;
+        const int64_t pp = tile * TILE_P + pl;
+        if (pp >= a.P) continue;
+        double2 out;
+        if (t < S) {
+          const double g = (double)psf[(PSF_GAIN * S + t) * TILE_P + pl];
+          const double2 v = acc[t * TILE_P + pl];
+          out = make_double2(v.x * g, v.y * g);
+        } else {
+          int r = 0, e = t - S;
+          while (e >= r + 1) { e -= r + 1; ++r; }
+          const int c = e;  // (r, c), r >= c
+          const double gr_ = (double)psf[(PSF_GAIN * S + r) * TILE_P + pl];
+          const double gc_ = (double)psf[(PSF_GAIN * S + c) * TILE_P + pl];
+          if (r == c) {
+            out = make_double2(nz * gr_ * gc_, 0.0);
+          } else {
+            // G_cr (c < r) accumulated; lower entry G_rc = conj(G_cr)
+            const int q = pair_index(c, r, S);
+            double2 v = acc[(S + q) * TILE_P + pl];
+            if (!nb_mode) {
+              const double dR = R64s[c * TILE_P + pl] - R64s[r * TILE_P + pl];
+              double sb, cb;
+              sincospi(2.0 * frac_c(dR * sc.fc_c), &sb, &cb);
+              v = make_double2(cb * v.x - sb * v.y, cb * v.y + sb * v.x);
+            }
+            const double g2 = gr_ * gc_;
+            out = make_double2(v.x * g2, -v.y * g2);
           }
         }
+        a.terms[(pp * J + j) * T + t] = out;
       }
-      if (warp == 0) {
-        double2* amp = (a.amp != nullptr && pvalid) ? a.amp + (p * J + j) * S : nullptr;
-        lsum += assemble_lane<S>(sc, j, lane, wc, wv, wk, a.ynorm2[j], amp);
-      }
-      // the next PA's set-up barrier orders warp 0's use of the workspace before any reuse
+      __syncthreads();  // the next PA's set-up rewrites psf / R64s / acc
     }
-    if (warp == 0 && pvalid) {
-      if (degen[lane]) {
-        lsum = -INFINITY;
-        atomicOr(a.flags, FLAG_DEGENERATE);
-      } else if (!(lsum == lsum)) {
-        atomicOr(a.flags, FLAG_NAN);
-      }
-      a.loglik[p] = lsum;
-    }
-    __syncthreads();  // pos_s / degen reuse by the next tile
+    if (warp == 0 && pvalid) a.pflag[p] = pfl[lane];
+    __syncthreads();  // pos_s / pfl reuse by the next tile
   }
+}
+
+// ---------------------------------------------------------------------------- K1b assembly (row A5)
+// One thread per particle, fp64, vectors / matrix in shared-memory columns [item][ASM_T]:
+//   g = c - G m; ||e||^2 = ||z||^2 - 2 Re(m^H c) + m^H G m; K = I + V^1/2 G V^1/2 / eta = L L^H;
+//   x = L^-1 V^1/2 g; l_j = -Nz ln(pi eta) - 2 sum ln L_ii - ||e||^2/eta + ||x||^2/eta^2;
+//   amplitudes: m + V^1/2 L^-H x / eta (LMMSE).
+constexpr int ASM_T = 32;
+
+template <int S>
+__global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__ SceneDev sc, const AsmArgs a) {
+  constexpr int NTRI = S * (S + 1) / 2;
+  constexpr int T = S + NTRI;
+  __shared__ double2 sh[(2 * S + NTRI) * ASM_T];
+  double2* wc = sh;                 // [S][ASM_T]
+  double2* wv = sh + S * ASM_T;     // [S][ASM_T]
+  double2* wk = sh + 2 * S * ASM_T; // [NTRI][ASM_T]
+  const int ln = threadIdx.x;
+  const int64_t p = (int64_t)blockIdx.x * ASM_T + ln;
+  if (p >= a.P) return;
+  const int J = sc.J;
+  const double nz = (double)sc.nf * (double)sc.Na;
+  double l = a.logw_prior ? a.logw_prior[p] : 0.0;
+  for (int j = 0; j < J; ++j) {
+    const double2* tp = a.terms + (p * J + j) * T;
+    const double eta = sc.eta[j];
+#pragma unroll 1
+    for (int s = 0; s < S; ++s) wc[s * ASM_T + ln] = tp[s];
+#pragma unroll 1
+    for (int t = 0; t < NTRI; ++t) wk[t * ASM_T + ln] = tp[S + t];
+    if (a.term_c != nullptr) {
+#pragma unroll 1
+      for (int r = 0; r < S; ++r) {
+        a.term_c[(p * J + j) * S + r] = wc[r * ASM_T + ln];
+#pragma unroll 1
+        for (int c = 0; c < S; ++c) {
+          double2 G = (r >= c) ? wk[tri(r, c) * ASM_T + ln] : wk[tri(c, r) * ASM_T + ln];
+          if (r < c) G.y = -G.y;
+          a.term_G[((p * J + j) * S + r) * S + c] = G;
+        }
+      }
+    }
+    double mhc = 0.0, mGm = 0.0;
+#pragma unroll 1
+    for (int r = 0; r < S; ++r) {
+      const double2 c = wc[r * ASM_T + ln];
+      double gmr = 0.0, gmi = 0.0;
+#pragma unroll 1
+      for (int t = 0; t < S; ++t) {
+        double2 G = (r >= t) ? wk[tri(r, t) * ASM_T + ln] : wk[tri(t, r) * ASM_T + ln];
+        if (r < t) G.y = -G.y;
+        const double mr = sc.m_re[j][t], mi = sc.m_im[j][t];
+        gmr += G.x * mr - G.y * mi;
+        gmi += G.x * mi + G.y * mr;
+      }
+      const double mr = sc.m_re[j][r], mi = sc.m_im[j][r];
+      mhc += mr * c.x + mi * c.y;
+      mGm += mr * gmr + mi * gmi;
+      const double sv = sqrt(sc.v[j][r]);
+      wv[r * ASM_T + ln] = make_double2(sv * (c.x - gmr), sv * (c.y - gmi));  // b = V^1/2 g
+    }
+    const double e2 = a.ynorm2[j] - 2.0 * mhc + mGm;
+#pragma unroll 1
+    for (int r = 0; r < S; ++r)
+#pragma unroll 1
+      for (int t = 0; t <= r; ++t) {
+        const double f = sqrt(sc.v[j][r]) * sqrt(sc.v[j][t]) / eta;
+        const double2 G = wk[tri(r, t) * ASM_T + ln];
+        wk[tri(r, t) * ASM_T + ln] = make_double2((r == t ? 1.0 : 0.0) + G.x * f, G.y * f);
+      }
+    double logdet = 0.0;
+    bool okc = true;
+#pragma unroll 1
+    for (int q = 0; q < S; ++q) {
+      double d = wk[tri(q, q) * ASM_T + ln].x;
+#pragma unroll 1
+      for (int k = 0; k < q; ++k) {
+        const double2 lq = wk[tri(q, k) * ASM_T + ln];
+        d -= lq.x * lq.x + lq.y * lq.y;
+      }
+      okc &= d > 0.0;
+      const double lqq = sqrt(fmax(d, 1e-300));
+      logdet += 2.0 * log(lqq);
+      wk[tri(q, q) * ASM_T + ln] = make_double2(lqq, 0.0);
+#pragma unroll 1
+      for (int i = q + 1; i < S; ++i) {
+        double2 ac = wk[tri(i, q) * ASM_T + ln];
+#pragma unroll 1
+        for (int k = 0; k < q; ++k) {
+          const double2 li = wk[tri(i, k) * ASM_T + ln], lk = wk[tri(q, k) * ASM_T + ln];
+          ac.x -= li.x * lk.x + li.y * lk.y;  // ac -= L_ik conj(L_qk)
+          ac.y -= li.y * lk.x - li.x * lk.y;
+        }
+        wk[tri(i, q) * ASM_T + ln] = make_double2(ac.x / lqq, ac.y / lqq);
+      }
+    }
+    double x2 = 0.0;
+#pragma unroll 1
+    for (int r = 0; r < S; ++r) {
+      double2 b = wv[r * ASM_T + ln];
+#pragma unroll 1
+      for (int k = 0; k < r; ++k) {
+        const double2 lr = wk[tri(r, k) * ASM_T + ln], xk = wv[k * ASM_T + ln];
+        b.x -= lr.x * xk.x - lr.y * xk.y;
+        b.y -= lr.x * xk.y + lr.y * xk.x;
+      }
+      const double ld = wk[tri(r, r) * ASM_T + ln].x;
+      const double2 xr = make_double2(b.x / ld, b.y / ld);
+      wv[r * ASM_T + ln] = xr;
+      x2 += xr.x * xr.x + xr.y * xr.y;
+    }
+    double lj = -nz * log(PI * eta) - logdet - e2 / eta + x2 / (eta * eta);
+    if (!okc || !(lj == lj)) lj = -INFINITY;
+    l += lj;
+    if (a.amp != nullptr) {
+#pragma unroll 1
+      for (int r = S - 1; r >= 0; --r) {
+        double2 t = wv[r * ASM_T + ln];
+#pragma unroll 1
+        for (int k = r + 1; k < S; ++k) {
+          const double2 lk = wk[tri(k, r) * ASM_T + ln], xk = wv[k * ASM_T + ln];  // (L^H)_rk = conj(L_kr)
+          t.x -= lk.x * xk.x + lk.y * xk.y;
+          t.y -= lk.x * xk.y - lk.y * xk.x;
+        }
+        const double ld = wk[tri(r, r) * ASM_T + ln].x;
+        wv[r * ASM_T + ln] = make_double2(t.x / ld, t.y / ld);
+      }
+#pragma unroll 1
+      for (int s = 0; s < S; ++s) {
+        const double sv = sqrt(sc.v[j][s]);
+        const double2 t = wv[s * ASM_T + ln];
+        a.amp[(p * J + j) * S + s] = make_double2(sc.m_re[j][s] + sv * t.x / eta, sc.m_im[j][s] + sv * t.y / eta);
+      }
+    }
+  }
+  const int pf = a.pflag[p];
+  if (pf) {
+    l = -INFINITY;
+    atomicOr(a.flags, (pf & 2) ? (FLAG_NAN | FLAG_DEGENERATE) : FLAG_DEGENERATE);
+  } else if (!(l == l)) {
+    atomicOr(a.flags, FLAG_NAN);
+  }
+  a.loglik[p] = l;
 }
 
 // ---------------------------------------------------------------------------- launch
 template <int S, typename RT>
-static cudaError_t launch_loglik_t(const SceneDev& sc, const LoglikArgs& a, cudaStream_t st, int num_sms) {
-  const size_t smem = SmemPlan<S, RT>::total;
-  auto kern = loglik_kernel<S, RT>;
+static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStream_t st, int num_sms) {
+  const size_t smem = Plan<S, RT>::total;
+  auto kern = corr_kernel<S, RT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -555,34 +684,36 @@ static cudaError_t launch_loglik_t(const SceneDev& sc, const LoglikArgs& a, cuda
 }
 
 template <typename RT>
-static cudaError_t dispatch_loglik(const SceneDev& sc, const LoglikArgs& a, cudaStream_t st, int num_sms) {
+static cudaError_t dispatch_corr(const SceneDev& sc, const CorrArgs& a, cudaStream_t st, int num_sms) {
   switch (sc.S) {
-    case 1: return launch_loglik_t<1, RT>(sc, a, st, num_sms);
-    case 2: return launch_loglik_t<2, RT>(sc, a, st, num_sms);
-    case 3: return launch_loglik_t<3, RT>(sc, a, st, num_sms);
-    case 4: return launch_loglik_t<4, RT>(sc, a, st, num_sms);
-    case 5: return launch_loglik_t<5, RT>(sc, a, st, num_sms);
-    case 6: return launch_loglik_t<6, RT>(sc, a, st, num_sms);
-    case 7: return launch_loglik_t<7, RT>(sc, a, st, num_sms);
-    case 8: return launch_loglik_t<8, RT>(sc, a, st, num_sms);
-    case 9: return launch_loglik_t<9, RT>(sc, a, st, num_sms);
+    case 1: return launch_corr_t<1, RT>(sc, a, st, num_sms);
+    case 2: return launch_corr_t<2, RT>(sc, a, st, num_sms);
+    case 3: return launch_corr_t<3, RT>(sc, a, st, num_sms);
+    case 4: return launch_corr_t<4, RT>(sc, a, st, num_sms);
+    case 5: return launch_corr_t<5, RT>(sc, a, st, num_sms);
+    case 6: return launch_corr_t<6, RT>(sc, a, st, num_sms);
+    case 7: return launch_corr_t<7, RT>(sc, a, st, num_sms);
+    case 8: return launch_corr_t<8, RT>(sc, a, st, num_sms);
+    case 9: return launch_corr_t<9, RT>(sc, a, st, num_sms);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_loglik(const SceneDev& sc, const LoglikArgs& a, int precision, cudaStream_t st, int num_sms) {
-  return precision == CDMS_FP64 ? dispatch_loglik<double>(sc, a, st, num_sms)
-                                : dispatch_loglik<float>(sc, a, st, num_sms);
+cudaError_t launch_corr(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st, int num_sms) {
+  return precision == CDMS_FP64 ? dispatch_corr<double>(sc, a, st, num_sms) : dispatch_corr<float>(sc, a, st, num_sms);
 }
 
-size_t loglik_smem_bytes(int S, int precision) {
-  switch (S) {
+cudaError_t launch_assemble(const SceneDev& sc, const AsmArgs& a, cudaStream_t st) {
+  if (a.P <= 0) return cudaSuccess;
+  const unsigned grid = (unsigned)((a.P + ASM_T - 1) / ASM_T);
+  switch (sc.S) {
 #define CASE_S(n) \
-  case n: return precision == CDMS_FP64 ? SmemPlan<n, double>::total : SmemPlan<n, float>::total;
+  case n: assemble_kernel<n><<<grid, ASM_T, 0, st>>>(sc, a); break;
     CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
 #undef CASE_S
-    default: return 0;
+    default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
 }
 
 }  // namespace cdms

@@ -12,6 +12,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libcdms.so")
+LIB_TIMING = os.path.join(HERE, "libcdms_timing.so")  # debug variant with -DCDMS_PHASE_TIMING
 SOURCES = ["loglik.cu", "response.cu", "beliefs.cu", "cdms.cpp"]
 HEADERS = ["cdms_internal.h", "geometry.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -30,24 +31,28 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "cdms.h"),
                                                                  os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, timing: bool = False) -> str:
+    lib = LIB_TIMING if timing else LIB
+    if not force and not _stale(lib):
+        return lib
+    obj_dir = OBJ + ("_timing" if timing else "")
+    os.makedirs(obj_dir, exist_ok=True)
     inc, libdir = nccl_dirs()
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(ROOT, "include")]
+    if timing:
+        common.append("-DCDMS_PHASE_TIMING")
 
     def compile_one(src: str) -> str:
-        out = os.path.join(OBJ, src + ".o")
+        out = os.path.join(obj_dir, src + ".o")
         cmd = [nvcc()] + ARCH + common + ["-Xptxas", "-v" if verbose else "-O3", "-c",
                                           os.path.join(CSRC, src), "-o", out]
         if src.endswith(".cpp"):
@@ -61,15 +66,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=4) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     link = [nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + [
         "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath={libdir}"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timing="--timing" in sys.argv))

@@ -12,7 +12,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcdms.so")
+LIB_PATH = os.environ.get("CDMS_LIB", os.path.join(HERE, "libcdms.so"))
 
 OK, EINVAL, EDEGENERATE, EZEROMASS, ENOMEM, ECUDA, ENCCL, EUNSUPPORTED = range(8)
 STATUS_NAMES = ["OK", "EINVAL", "EDEGENERATE", "EZEROMASS", "ENOMEM", "ECUDA", "ENCCL", "EUNSUPPORTED"]

@@ -101,10 +101,9 @@ __device__ __forceinline__ void template_col(const SceneDev& sc, int j, int m, d
 template <typename RT>
 struct PSField {
   RT rx, ry, rz, sx, sy, sz, rs2, R, E0r, E0i, gain;
-  double Wr, Wi, Zr, Zi;
+  RT Whr, Whi, Wlr, Wli, Zhr, Zhi, Zlr, Zli;  // W, Zp as unevaluated sums hi + lo (fp32: ~48-bit mantissa)
 };
-constexpr int NPSF = 11;       // RT fields of PSField (the fp64 tail is stored separately)
-constexpr int NPSD = 4;        // fp64 fields
+constexpr int NPSF = 19;       // RT fields of PSField
 constexpr int PSF_GAIN = 10;   // index of .gain
 
 // Returns PS_OK, PS_DEGENERATE (MT on the phase centre, r' = 0 excluded by P:L2137) or PS_BADSFV
@@ -130,9 +129,11 @@ __device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double*
   sincospi(2.0 * frac_c(R * sc.f0_c), &s_, &c_);
   f.E0r = (RT)c_; f.E0i = (RT)s_;
   sincospi(2.0 * frac_c(R * sc.df_c), &s_, &c_);
-  f.Wr = c_; f.Wi = s_;
+  f.Whr = (RT)c_; f.Whi = (RT)s_;
+  f.Wlr = (RT)(c_ - (double)f.Whr); f.Wli = (RT)(s_ - (double)f.Whi);
   sincospi(2.0 * frac_c(R * sc.segdf_c), &s_, &c_);
-  f.Zr = c_; f.Zi = s_;
+  f.Zhr = (RT)c_; f.Zhi = (RT)s_;
+  f.Zlr = (RT)(c_ - (double)f.Zhr); f.Zli = (RT)(s_ - (double)f.Zhi);
   f.gain = (RT)(sc.pathloss ? sc.lambda / (4.0 * PI * R) : 1.0);
   if (!sfv_ok) return PS_BADSFV;
   if (!(R > 0.0)) {  // also catches NaN positions
@@ -171,11 +172,13 @@ __device__ __forceinline__ void cmul(RT ar, RT ai, RT br, RT bi, RT& cr, RT& ci)
   cr = ar * br - ai * bi;
   ci = ar * bi + ai * br;
 }
-// fp32(W * s) with the product formed in fp64 (one rounding per component, per antenna)
+// (W_hi + W_lo) * s with the small products first and one final rounding per component: the result's
+// rounding depends on the antenna's s, so it is independent across antennas (fp32 FMAs only)
 template <typename RT>
-__device__ __forceinline__ void cmul_round(double Wr, double Wi, RT sr, RT si, RT& cr, RT& ci) {
-  cr = (RT)(Wr * (double)sr - Wi * (double)si);
-  ci = (RT)(Wr * (double)si + Wi * (double)sr);
+__device__ __forceinline__ void cmul_df(RT Whr, RT Whi, RT Wlr, RT Wli, RT sr, RT si, RT& cr, RT& ci) {
+  const RT lr = fma(Wlr, sr, -Wli * si), li = fma(Wlr, si, Wli * sr);
+  cr = fma(Whr, sr, fma(-Whi, si, lr));
+  ci = fma(Whr, si, fma(Whi, sr, li));
 }
 // deterministic per-(antenna, component) rotation in (-2^-24, 2^-24) rad: decorrelates the fp32 rounding of
 // an otherwise shared step phasor across antennas (NB, where the per-antenna step correction is 1)
@@ -210,9 +213,10 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
   if (sc.wavefront == CDMS_PLANAR_NB) {
     cis2pi_fast<RT>(delta * (RT)sc.fc_c, er, ei);
     cmul<RT>(f.E0r, f.E0i, er, ei, o.Ar, o.Ai);
-    const double t = (sizeof(RT) == 4) ? dither_angle(m, s) : 0.0;
-    cmul_round<RT>(f.Wr - t * f.Wi, f.Wi + t * f.Wr, RT(1), RT(0), o.wr, o.wi);
-    cmul_round<RT>(f.Zr, f.Zi, RT(1), RT(0), o.Zr, o.Zi);
+    const RT t = (sizeof(RT) == 4) ? (RT)dither_angle(m, s) : RT(0);
+    cmul_df<RT>(f.Whr, f.Whi, f.Wlr, f.Wli, RT(1), t, o.wr, o.wi);
+    const RT tz = (sizeof(RT) == 4) ? (RT)dither_angle(m, s + 16) : RT(0);
+    cmul_df<RT>(f.Zhr, f.Zhi, f.Zlr, f.Zli, RT(1), tz, o.Zr, o.Zi);
   } else {
     // A: one rounding per antenna, independent across antennas -> MUFU accuracy suffices
     cis2pi_fast<RT>(delta * (RT)sc.f0_c, er, ei);
@@ -220,10 +224,10 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
     // w, Z are raised to powers: accurate small-angle polynomials / sincospi, products rounded once in fp64
     if (sc.small_step) cis_small<RT>(delta * (RT)sc.df_c, er, ei);
     else cis2pi<RT>(delta * (RT)sc.df_c, er, ei);
-    cmul_round<RT>(f.Wr, f.Wi, er, ei, o.wr, o.wi);
+    cmul_df<RT>(f.Whr, f.Whi, f.Wlr, f.Wli, er, ei, o.wr, o.wi);
     if (sc.small_z) cis_med<RT>(delta * (RT)sc.segdf_c, er, ei);
     else cis2pi<RT>(delta * (RT)sc.segdf_c, er, ei);
-    cmul_round<RT>(f.Zr, f.Zi, er, ei, o.Zr, o.Zi);
+    cmul_df<RT>(f.Zhr, f.Zhi, f.Zlr, f.Zli, er, ei, o.Zr, o.Zi);
   }
 }
 

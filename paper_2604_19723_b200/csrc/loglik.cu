@@ -20,21 +20,20 @@
 namespace cdms {
 
 // ---------------------------------------------------------------------------- y re-layout
-// y [J][nf][Na] (paper vec order) -> ytiles [J][n_mb][n_kc][kc_len][NWARP] of (yr, yr, yi, yi) (zero padded),
-// and ||z^(j)||^2 in fp64 (block 0 of each PA, fixed reduction order).
+// y [J][nf][Na] (paper vec order) -> ytiles [J][Na_pad][n_kc][kc_len] of (yr, yr, yi, yi), Na_pad = 8 n_mb
+// (zero padded): each warp streams its own antenna's chunks; and ||z^(j)||^2 in fp64 (block 0 of each PA,
+// fixed reduction order).
 __global__ void prep_y_kernel(const SceneDev sc, const float2* __restrict__ y, float4* __restrict__ yt,
                               double* __restrict__ ynorm2) {
   const int j = blockIdx.y;
   const int64_t per_j = (int64_t)sc.n_mb * sc.n_kc * sc.kc_len * NWARP;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < per_j;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int w = (int)(t % NWARP);
-    int64_t rest = t / NWARP;
-    const int kl = (int)(rest % sc.kc_len);
-    rest /= sc.kc_len;
+    const int kl = (int)(t % sc.kc_len);
+    int64_t rest = t / sc.kc_len;
     const int kc = (int)(rest % sc.n_kc);
-    const int mb = (int)(rest / sc.n_kc);
-    const int m = mb * NWARP + w, k = kc * sc.kc_len + kl;
+    const int m = (int)(rest / sc.n_kc);
+    const int k = kc * sc.kc_len + kl;
     float2 v = make_float2(0.f, 0.f);
     if (m < sc.Na && k < sc.nf) v = y[((int64_t)j * sc.nf + k) * sc.Na + m];
     yt[(int64_t)j * per_j + t] = make_float4(v.x, v.x, v.y, v.y);
@@ -120,10 +119,15 @@ struct Horner<S, float> {
       wiL = wi[S - 1];
     }
   }
-  __device__ __forceinline__ void reset() {
+  __device__ __forceinline__ void reset_to(const float4 y) {
+    const u64 yr2 = pk2(y.x, y.y), yi2 = pk2(y.z, y.w);
 #pragma unroll
-    for (int q = 0; q < NP; ++q) hr2[q] = hi2[q] = 0ull;
-    hrL = hiL = 0.f;
+    for (int q = 0; q < NP; ++q) {
+      hr2[q] = yr2;
+      hi2[q] = yi2;
+    }
+    hrL = y.x;
+    hiL = y.z;
   }
   __device__ __forceinline__ void step(const float4 y) {
     const u64 yr2 = pk2(y.x, y.y), yi2 = pk2(y.z, y.w);
@@ -168,9 +172,12 @@ struct Horner<S, double> {
       wi[s] = wi_[s];
     }
   }
-  __device__ __forceinline__ void reset() {
+  __device__ __forceinline__ void reset_to(const float4 y) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) hr[s] = hi[s] = 0.0;
+    for (int s = 0; s < S; ++s) {
+      hr[s] = (double)y.x;
+      hi[s] = (double)y.z;
+    }
   }
   __device__ __forceinline__ void step(const float4 y) {
 #pragma unroll
@@ -223,11 +230,11 @@ struct Plan {
   static constexpr int T = S + NTRI;
   static constexpr size_t ybuf = 2ull * KCHUNK * NWARP * sizeof(float4);
   static constexpr size_t ps =
-      (size_t)NPSF * S * TILE_P * sizeof(RT) + (size_t)(NPSD + 1) * S * TILE_P * sizeof(double);
+      (size_t)NPSF * S * TILE_P * sizeof(RT) + (size_t)S * TILE_P * sizeof(double);
   static constexpr size_t dlt = (size_t)S * NWARP * TILE_P * sizeof(RT);            // Delta [S][8][32]
   static constexpr size_t cst = (size_t)S * NWARP * TILE_P * 2 * sizeof(RT);        // c per antenna
   static constexpr size_t acc = (size_t)(S + NPAIR) * TILE_P * sizeof(double2);     // fp64 sums [item][32]
-  static constexpr size_t misc = 64 + TILE_P * 3 * sizeof(double) + TILE_P * sizeof(int);
+  static constexpr size_t misc = 2 * NWARP * sizeof(uint64_t) + TILE_P * 3 * sizeof(double) + TILE_P * sizeof(int);
   static constexpr size_t total = ybuf + ps + dlt + cst + acc + misc;
 };
 
@@ -241,9 +248,39 @@ size_t corr_smem_bytes(int S, int precision) {
   }
 }
 
+// ---------------------------------------------------------------------------- phase timing (debug build)
+// -DCDMS_PHASE_TIMING: per-warp clock64 cycles per phase of K1, summed into g_phase (tools/phase_timing.py).
+#ifdef CDMS_PHASE_TIMING
+__device__ unsigned long long g_phase[8];
+#define PT_DECL unsigned long long pt_t = clock64(), pt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define PT(i) { const unsigned long long n_ = clock64(); pt_acc[i] += n_ - pt_t; pt_t = n_; }
+#define PT_FLUSH if (lane == 0) { for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_phase[i_], pt_acc[i_]); }
+}  // namespace cdms
+extern "C" int cdms_debug_phase_read(double* out8, int reset) {
+  unsigned long long h[8];
+  if (cudaMemcpyFromSymbol(h, cdms::g_phase, sizeof(h)) != cudaSuccess) return 1;
+  for (int i = 0; i < 8; ++i) out8[i] = (double)h[i];
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(cdms::g_phase, z, sizeof(z));
+  }
+  return 0;
+}
+namespace cdms {
+#else
+#define PT_DECL
+#define PT(i)
+#define PT_FLUSH
+#endif
+
 // ---------------------------------------------------------------------------- K1
 template <int S, typename RT>
-__global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
+// fp32, S <= 7: 3 CTAs (24 warps) per SM -- the FFMA2 Horner is latency-bound and reaches ~96% of the FMA
+// pipe only with >= 4 warps per SMSP in the loop; S = 8, 9 need the registers (2 CTAs).
+#ifndef CDMS_MINB_SMALL_S
+#define CDMS_MINB_SMALL_S 3
+#endif
+__global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? (S <= 7 ? CDMS_MINB_SMALL_S : 2) : 1)
     corr_kernel(const __grid_constant__ SceneDev sc, const CorrArgs a) {
   using PL = Plan<S, RT>;
   constexpr int NPAIR = PL::NPAIR;
@@ -252,46 +289,55 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
   unsigned char* sp = smem;
   float4* ybuf = reinterpret_cast<float4*>(sp);                         sp += PL::ybuf;
   RT* psf = reinterpret_cast<RT*>(sp);                                  // [NPSF][S][32]
-  double* psd = reinterpret_cast<double*>(sp + (size_t)NPSF * S * TILE_P * sizeof(RT));  // [NPSD][S][32]
-  double* R64s = psd + NPSD * S * TILE_P;                               // [S][32]
+  double* R64s = reinterpret_cast<double*>(sp + (size_t)NPSF * S * TILE_P * sizeof(RT));  // [S][32]
   sp += PL::ps;
   RT* dlt = reinterpret_cast<RT*>(sp);                                  sp += PL::dlt;
   RT* cst = reinterpret_cast<RT*>(sp);                                  sp += PL::cst;
   double2* acc = reinterpret_cast<double2*>(sp);                        sp += PL::acc;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sp);
-  double* pos_s = reinterpret_cast<double*>(sp + 64);                   // [3][32]
-  int* pfl = reinterpret_cast<int*>(sp + 64 + TILE_P * 3 * sizeof(double));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sp);                     // [NWARP][2]
+  double* pos_s = reinterpret_cast<double*>(sp + 2 * NWARP * sizeof(uint64_t));  // [3][32]
+  int* pfl = reinterpret_cast<int*>(sp + 2 * NWARP * sizeof(uint64_t) + TILE_P * 3 * sizeof(double));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int J = sc.J, Na = sc.Na, nf = sc.nf, kcl = sc.kc_len;
-  const int n_mb = sc.n_mb, n_kc = sc.n_kc;
+  const int n_mb = sc.n_mb, n_kc = sc.n_kc, Na_pad = sc.n_mb * NWARP;
   const bool nb_mode = sc.wavefront == CDMS_PLANAR_NB;
   const int64_t chunks_per_tile = (int64_t)J * n_mb * n_kc;
-  const uint32_t chunk_bytes = (uint32_t)(kcl * NWARP * sizeof(float4));
+  const uint32_t chunk_bytes = (uint32_t)(kcl * sizeof(float4));
   const int64_t my_tiles =
       (a.n_tiles > (int64_t)blockIdx.x) ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total_chunks = my_tiles * chunks_per_tile;
 
+  // Every warp streams its own antenna's y chunks (no CTA-wide barrier per chunk): lane 0 issues a 1-D bulk
+  // TMA of kc_len (yr, yr, yi, yi) into the warp's double buffer, completion on the warp's mbarrier.
+  // Chunks are issued strictly in order c = 0, 1, 2, ...: an incremental (j, mb, kc) cursor replaces the
+  // index decomposition (64-bit div/mod are long integer sequences).
+  int is_j = 0, is_mb = 0, is_kc = 0;
   auto issue = [&](int64_t c) {
-    const int64_t f = c % chunks_per_tile;  // (j, mb, kc) flattened: the same sequence for every tile
-    uint64_t* bar = &mbar[c & 1];
+    const int m = is_mb * NWARP + warp;
+    uint64_t* bar = &mbar[warp * 2 + (c & 1)];
     fence_proxy_async();
     mbar_expect_tx(bar, chunk_bytes);
-    tma_load_1d(ybuf + (c & 1) * (KCHUNK * NWARP), a.ytiles + f * (int64_t)kcl * NWARP, chunk_bytes, bar);
+    tma_load_1d(ybuf + (warp * 2 + (c & 1)) * KCHUNK,
+                a.ytiles + (((int64_t)is_j * Na_pad + m) * n_kc + is_kc) * kcl, chunk_bytes, bar);
+    if (++is_kc == n_kc) {
+      is_kc = 0;
+      if (++is_mb == n_mb) {
+        is_mb = 0;
+        if (++is_j == J) is_j = 0;
+      }
+    }
   };
 
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    fence_mbar_init();
-  }
+  if (tid < 2 * NWARP) mbar_init(&mbar[tid], 1);
+  if (tid == 0) fence_mbar_init();
   __syncthreads();
-  if (tid == 0) {
+  if (lane == 0) {
     if (total_chunks > 0) issue(0);
     if (total_chunks > 1) issue(1);
   }
 
-  int64_t ci = 0;  // flat chunk counter of this CTA
+  int64_t ci = 0;  // flat chunk counter (the same sequence in every warp)
   for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
     const int64_t p = tile * TILE_P + lane;
     const bool pvalid = p < a.P;
@@ -301,6 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
       pfl[lane] = 0;
     }
     __syncthreads();
+    PT_DECL
 
     for (int j = 0; j < J; ++j) {
       // ---- (1) per (component, particle) set-up in fp64 (rows A1/A2); zero the fp64 accumulators
@@ -320,14 +367,11 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
         const RT* fv = reinterpret_cast<const RT*>(&f);
 #pragma unroll
         for (int q = 0; q < NPSF; ++q) psf[(q * S + s) * TILE_P + pl] = fv[q];
-        psd[(0 * S + s) * TILE_P + pl] = f.Wr;
-        psd[(1 * S + s) * TILE_P + pl] = f.Wi;
-        psd[(2 * S + s) * TILE_P + pl] = f.Zr;
-        psd[(3 * S + s) * TILE_P + pl] = f.Zi;
         R64s[s * TILE_P + pl] = R64;
       }
       for (int it = tid; it < (S + NPAIR) * TILE_P; it += NTHREADS) acc[it] = make_double2(0.0, 0.0);
       __syncthreads();
+      PT(0)
 
       // ---- (1b) planar NB Gram, separable closed form in fp64 (P:L2160-2184 with the template P:L29-39):
       //   G_ab = e^{j 2 pi dR fc/c} D_Nf(dR df/c) D_ny(dy du'_y fc/c) D_nv(dv du'_z fc/c),
@@ -387,10 +431,6 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
             RT* fv = reinterpret_cast<RT*>(&f);
 #pragma unroll
             for (int q = 0; q < NPSF; ++q) fv[q] = psf[(q * S + s) * TILE_P + lane];
-            f.Wr = psd[(0 * S + s) * TILE_P + lane];
-            f.Wi = psd[(1 * S + s) * TILE_P + lane];
-            f.Zr = psd[(2 * S + s) * TILE_P + lane];
-            f.Zi = psd[(3 * S + s) * TILE_P + lane];
             SMPhasors<RT> o;
             bool dg;
             setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
@@ -403,22 +443,23 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
           }
           if (deg_any && mvalid && pvalid) atomicOr(&pfl[lane], 1);
           H.init(wr, wi);
+          PT(2)
         }
         // ---- (3) correlation over all subcarriers (row A3): segmented Horner on TMA-staged y chunks
         for (int kc = 0; kc < n_kc; ++kc, ++ci) {
-          mbar_wait(&mbar[ci & 1], (uint32_t)((ci >> 1) & 1));
-          const float4* yb = ybuf + (ci & 1) * (KCHUNK * NWARP) + warp;
+          mbar_wait(&mbar[warp * 2 + (ci & 1)], (uint32_t)((ci >> 1) & 1));
+          const float4* yb = ybuf + (warp * 2 + (ci & 1)) * KCHUNK;
           const int k_begin = kc * kcl;
           const int k_end = min(k_begin + kcl, nf);
           for (int k0 = k_begin; k0 < k_end; k0 += SEG) {
             const int k1 = min(k0 + SEG, k_end);
-            H.reset();
-            const float4* yk = yb + (k1 - 1 - k_begin) * NWARP;  // Horner runs from the top subcarrier down
+            const float4* yk = yb + (k1 - 1 - k_begin);  // Horner runs from the top subcarrier down
+            H.reset_to(yk[0]);                            // acc = y_top (= 0 * w + y_top)
             if (k1 - k0 == SEG) {
-#pragma unroll 8
-              for (int i = 0; i < SEG; ++i) H.step(yk[-i * NWARP]);
+#pragma unroll 7
+              for (int i = 1; i < SEG; ++i) H.step(yk[-i]);
             } else {
-              for (int i = 0; i < k1 - k0; ++i) H.step(yk[-i * NWARP]);
+              for (int i = 1; i < k1 - k0; ++i) H.step(yk[-i]);
             }
             // c += A_seg H_seg (thread-private slot), A_seg <- A_seg Z
             RT hr[S], hi[S];
@@ -434,10 +475,12 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
               Ai[s] = nAi;
             }
           }
-          __syncthreads();  // every warp is done with this buffer
-          if (tid == 0 && ci + 2 < total_chunks) issue(ci + 2);
+          __syncwarp();  // every lane of this warp is done with the buffer
+          if (lane == 0 && ci + 2 < total_chunks) issue(ci + 2);
         }
-        // the last chunk barrier also published this block's cst / dlt
+        PT(3)
+        __syncthreads();  // publish this block's cst / dlt
+        PT(4)
         const int nw_valid = min(NWARP, Na - mb * NWARP);
         // ---- (4a) c_s += sum over the block's antennas, ascending m; owner warp rotates with mb
         for (int s = (warp - mb) & (NWARP - 1); s < S; s += NWARP) {
@@ -477,7 +520,9 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
             acc[(S + q) * TILE_P + lane] = make_double2(v.x + (double)gr, v.y + (double)gi);
           }
         }
+        PT(5)
         __syncthreads();  // before the next block's set-up rewrites dlt / cst
+        PT(6)
       }
 
       // ---- (5) hand-off: c (with gains) and the lower triangle of G (with gains) to HBM
@@ -516,7 +561,9 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? 2 : 1)
         a.terms[(pp * J + j) * T + t] = out;
       }
       __syncthreads();  // the next PA's set-up rewrites psf / R64s / acc
+      PT(7)
     }
+    PT_FLUSH
     if (warp == 0 && pvalid) a.pflag[p] = pfl[lane];
     __syncthreads();  // pos_s / pfl reuse by the next tile
   }

@@ -19,6 +19,8 @@ struct Num<float> {
   static __device__ __forceinline__ float sinpi_(float x) { return sinpif(x); }
   static __device__ __forceinline__ float rint_(float x) { return rintf(x); }
   static __device__ __forceinline__ float sqrt_(float x) { return sqrtf(x); }
+  static __device__ __forceinline__ float fsqrt_(float x) { return x * rsqrtf(x); }   // ~2 ulp, x > 0
+  static __device__ __forceinline__ float fdiv_(float a, float b) { return __fdividef(a, b); }
   static constexpr float tiny_x = 1e-6f;  // |xr| below which D_N uses its 2nd-order series
 };
 template <>
@@ -27,6 +29,8 @@ struct Num<double> {
   static __device__ __forceinline__ double sinpi_(double x) { return sinpi(x); }
   static __device__ __forceinline__ double rint_(double x) { return rint(x); }
   static __device__ __forceinline__ double sqrt_(double x) { return sqrt(x); }
+  static __device__ __forceinline__ double fsqrt_(double x) { return sqrt(x); }
+  static __device__ __forceinline__ double fdiv_(double a, double b) { return a / b; }
   static constexpr double tiny_x = 1e-12;
 };
 
@@ -104,7 +108,23 @@ struct PSField {
   RT Whr, Whi, Wlr, Wli, Zhr, Zhi, Zlr, Zli;  // W, Zp as unevaluated sums hi + lo (fp32: ~48-bit mantissa)
 };
 constexpr int NPSF = 19;       // RT fields of PSField
+constexpr int NPSF_PAD = 20;   // shared-memory stride per (component, particle): 80 B (fp32) -> 5 x LDS.128
 constexpr int PSF_GAIN = 10;   // index of .gain
+
+// Load the NPSF fields of one (component, particle) record with 128-bit shared-memory loads.
+template <typename RT>
+__device__ __forceinline__ void load_psf(const RT* src, RT* fv) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(fv);
+  constexpr int N4 = (NPSF * (int)sizeof(RT) + 15) / 16;
+  float4 tmp[(NPSF_PAD * sizeof(RT)) / 16];
+#pragma unroll
+  for (int i = 0; i < N4; ++i) tmp[i] = s4[i];
+  const RT* t = reinterpret_cast<const RT*>(tmp);
+#pragma unroll
+  for (int q = 0; q < NPSF; ++q) fv[q] = t[q];
+  (void)d4;
+}
 
 // Returns PS_OK, PS_DEGENERATE (MT on the phase centre, r' = 0 excluded by P:L2137) or PS_BADSFV
 // (||sfv|| = 0).  On failure the fields hold a harmless finite placeholder.
@@ -201,11 +221,11 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
   RT delta;
   if (sc.wavefront == CDMS_SPHERICAL) {
     const RT n = q2 - RT(2) * rq;
-    const RT d = Num<RT>::sqrt_(f.R * f.R + n);
+    const RT d = Num<RT>::fsqrt_(f.R * f.R + n);
     degenerate = !(d > RT(0));
-    delta = n / (d + f.R);
+    delta = Num<RT>::fdiv_(n, d + f.R);  // |delta| <= aperture: ~1 ulp relative error is ample
   } else {
-    delta = -rq / f.R;
+    delta = Num<RT>::fdiv_(-rq, f.R);
     degenerate = false;
   }
   o.delta = delta;
@@ -225,9 +245,14 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
     if (sc.small_step) cis_small<RT>(delta * (RT)sc.df_c, er, ei);
     else cis2pi<RT>(delta * (RT)sc.df_c, er, ei);
     cmul_df<RT>(f.Whr, f.Whi, f.Wlr, f.Wli, er, ei, o.wr, o.wi);
-    if (sc.small_z) cis_med<RT>(delta * (RT)sc.segdf_c, er, ei);
-    else cis2pi<RT>(delta * (RT)sc.segdf_c, er, ei);
-    cmul_df<RT>(f.Zhr, f.Zhi, f.Zlr, f.Zli, er, ei, o.Zr, o.Zi);
+    if (sc.nf > SEG) {  // Z only advances A between segments
+      if (sc.small_z) cis_med<RT>(delta * (RT)sc.segdf_c, er, ei);
+      else cis2pi<RT>(delta * (RT)sc.segdf_c, er, ei);
+      cmul_df<RT>(f.Zhr, f.Zhi, f.Zlr, f.Zli, er, ei, o.Zr, o.Zi);
+    } else {
+      o.Zr = RT(1);
+      o.Zi = RT(0);
+    }
   }
 }
 

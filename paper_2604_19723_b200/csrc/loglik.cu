@@ -212,7 +212,11 @@ __device__ __forceinline__ float dirichlet_term<float>(float xr, long long n, in
   } else {
     float t = (float)N * xr;
     t = t - 2.f * rintf(0.5f * t);
-    d = __fdividef(__sinf(3.14159265358979f * t), sinpif(xr));
+    // sin(pi xr), |xr| <= 1/2: odd Taylor polynomial to (pi xr)^11 (error < 6e-8 at pi/2)
+    const float u = 3.14159265358979f * xr, u2 = u * u;
+    const float den = u * (1.f + u2 * (-1.f / 6 + u2 * (1.f / 120 + u2 * (-1.f / 5040 + u2 * (1.f / 362880 +
+                      u2 * (-1.f / 39916800))))));
+    d = __fdividef(__sinf(3.14159265358979f * t), den);
   }
   if (((N - 1) & 1) && (n & 1)) d = -d;
   return d;
@@ -230,7 +234,7 @@ struct Plan {
   static constexpr int T = S + NTRI;
   static constexpr size_t ybuf = 2ull * KCHUNK * NWARP * sizeof(float4);
   static constexpr size_t ps =
-      (size_t)NPSF * S * TILE_P * sizeof(RT) + (size_t)S * TILE_P * sizeof(double);
+      (size_t)NPSF_PAD * S * TILE_P * sizeof(RT) + (size_t)S * TILE_P * sizeof(double);
   static constexpr size_t dlt = (size_t)S * NWARP * TILE_P * sizeof(RT);            // Delta [S][8][32]
   static constexpr size_t cst = (size_t)S * NWARP * TILE_P * 2 * sizeof(RT);        // c per antenna
   static constexpr size_t acc = (size_t)(S + NPAIR) * TILE_P * sizeof(double2);     // fp64 sums [item][32]
@@ -288,8 +292,8 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? (S <= 7 ? CDMS_M
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* sp = smem;
   float4* ybuf = reinterpret_cast<float4*>(sp);                         sp += PL::ybuf;
-  RT* psf = reinterpret_cast<RT*>(sp);                                  // [NPSF][S][32]
-  double* R64s = reinterpret_cast<double*>(sp + (size_t)NPSF * S * TILE_P * sizeof(RT));  // [S][32]
+  RT* psf = reinterpret_cast<RT*>(sp);                                  // [S][32][NPSF_PAD]
+  double* R64s = reinterpret_cast<double*>(sp + (size_t)NPSF_PAD * S * TILE_P * sizeof(RT));  // [S][32]
   sp += PL::ps;
   RT* dlt = reinterpret_cast<RT*>(sp);                                  sp += PL::dlt;
   RT* cst = reinterpret_cast<RT*>(sp);                                  sp += PL::cst;
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? (S <= 7 ? CDMS_M
         }
         const RT* fv = reinterpret_cast<const RT*>(&f);
 #pragma unroll
-        for (int q = 0; q < NPSF; ++q) psf[(q * S + s) * TILE_P + pl] = fv[q];
+        for (int q = 0; q < NPSF; ++q) psf[(s * TILE_P + pl) * NPSF_PAD + q] = fv[q];
         R64s[s * TILE_P + pl] = R64;
       }
       for (int it = tid; it < (S + NPAIR) * TILE_P; it += NTHREADS) acc[it] = make_double2(0.0, 0.0);
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? (S <= 7 ? CDMS_M
             PSField<RT> f;
             RT* fv = reinterpret_cast<RT*>(&f);
 #pragma unroll
-            for (int q = 0; q < NPSF; ++q) fv[q] = psf[(q * S + s) * TILE_P + lane];
+            load_psf<RT>(psf + (s * TILE_P + lane) * NPSF_PAD, fv);  // 128-bit loads
             SMPhasors<RT> o;
             bool dg;
             setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
@@ -533,15 +537,15 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? (S <= 7 ? CDMS_M
         if (pp >= a.P) continue;
         double2 out;
         if (t < S) {
-          const double g = (double)psf[(PSF_GAIN * S + t) * TILE_P + pl];
+          const double g = (double)psf[(t * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
           const double2 v = acc[t * TILE_P + pl];
           out = make_double2(v.x * g, v.y * g);
         } else {
           int r = 0, e = t - S;
           while (e >= r + 1) { e -= r + 1; ++r; }
           const int c = e;  // (r, c), r >= c
-          const double gr_ = (double)psf[(PSF_GAIN * S + r) * TILE_P + pl];
-          const double gc_ = (double)psf[(PSF_GAIN * S + c) * TILE_P + pl];
+          const double gr_ = (double)psf[(r * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
+          const double gc_ = (double)psf[(c * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
           if (r == c) {
             out = make_double2(nz * gr_ * gc_, 0.0);
           } else {
@@ -723,7 +727,7 @@ static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStre
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)per_sm * num_sms;
+  int64_t grid = (int64_t)per_sm * num_sms;  // persistent: all resident CTAs (latency hiding beats tail balance)
   if (grid > a.n_tiles) grid = a.n_tiles;
   if (grid < 1) return cudaSuccess;
   kern<<<(unsigned)grid, NTHREADS, smem, st>>>(sc, a);

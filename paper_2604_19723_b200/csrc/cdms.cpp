@@ -229,7 +229,7 @@ cdms_status run_lse(cdms_ctx ctx, const double* d_l, int64_t P, double* d_lse) {
   WS_TRY(ctx, WS_LSE_RANK, ctx->nranks + 1, &per_rank);
   WS_TRY(ctx, WS_SCAL, 8, &scal);
   CUDA_TRY(ctx, launch_lse_partial(d_l, P, part, ctx->stream));
-  if (ctx->comm && ctx->nranks > 1) {
+  if (ctx->comm) {
     CUDA_TRY(ctx, launch_lse_final(part, nb, part + nb, ctx->stream));
     NCCL_TRY(ctx, ncclAllGather(part + nb, per_rank, 2, ncclDouble, ctx->comm, ctx->stream));
   } else {
@@ -247,10 +247,10 @@ cdms_status run_moments(cdms_ctx ctx, const double* d_x, const double* d_w, int6
   WS_TRY(ctx, WS_SUMS, 32, &sums);
   CUDA_TRY(ctx, launch_moments1(d_x, d_w, P, part, ctx->stream));
   CUDA_TRY(ctx, launch_sum_partials(part, nb, 7, sums, ctx->stream));
-  if (ctx->comm && ctx->nranks > 1) NCCL_TRY(ctx, ncclAllReduce(sums, sums, 7, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  if (ctx->comm) NCCL_TRY(ctx, ncclAllReduce(sums, sums, 7, ncclDouble, ncclSum, ctx->comm, ctx->stream));
   CUDA_TRY(ctx, launch_moments2(d_x, d_w, P, sums, part, ctx->stream));
   CUDA_TRY(ctx, launch_sum_partials(part, nb, 21, sums + 8, ctx->stream));
-  if (ctx->comm && ctx->nranks > 1)
+  if (ctx->comm)
     NCCL_TRY(ctx, ncclAllReduce(sums + 8, sums + 8, 21, ncclDouble, ncclSum, ctx->comm, ctx->stream));
   CUDA_TRY(ctx, launch_moments_finalize(sums, sums + 8, d_est, ctx->d_flags, ctx->stream));
   ctx->launches += 5;
@@ -281,14 +281,14 @@ cdms_status run_resample_core(cdms_ctx ctx, const double* d_in, int64_t P_local,
     WS_TRY(ctx, WS_WMAX_PART, nb + 1, &wpart);
     CUDA_TRY(ctx, launch_wmax_partial_f(d_in, P_local, wpart, ctx->d_flags, ctx->stream));
     CUDA_TRY(ctx, launch_max_final(wpart, nb, scal + 2, ctx->stream));
-    if (ctx->comm && ctx->nranks > 1)
+    if (ctx->comm)
       NCCL_TRY(ctx, ncclAllReduce(scal + 2, scal + 2, 1, ncclDouble, ncclMax, ctx->comm, ctx->stream));
     ctx->launches += 2;
   }
   CUDA_TRY(ctx, launch_quantize(d_in, P_local, scal + 2, scal + 0, from_loglik, q, ctx->d_flags, ctx->stream));
   CUDA_TRY(ctx, launch_scan(q, P_local, bsum, ctx->stream));
   ctx->launches += 4;
-  if (!(ctx->comm && ctx->nranks > 1)) {
+  if (!(ctx->comm)) {
     WS_TRY(ctx, WS_ANC, P_local, &anc);
     CUDA_TRY(ctx, launch_ancestors(q, P_local, bsum + nb, nullptr, 0, P_local, P_local, u_bits, 0, anc, ctx->d_flags,
                                    ctx->stream));
@@ -647,7 +647,7 @@ cdms_status cdms_resample(cdms_ctx ctx, const double* d_w, int64_t P_local, uint
   int64_t* anc;
   cdms_status st = run_resample_core(ctx, d_w, P_local, u_bits, 0, &plan, &anc);
   if (st) return st;
-  if (!(ctx->comm && ctx->nranks > 1)) {
+  if (!(ctx->comm)) {
     CUDA_TRY(ctx, cudaMemcpyAsync(d_ancestors, anc, sizeof(int64_t) * P_local, cudaMemcpyDeviceToDevice, ctx->stream));
     return CDMS_OK;
   }
@@ -695,7 +695,7 @@ cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_partic
   WS_TRY(ctx, WS_STAGE, (n > 0 ? n : 1) * 6, &stage);
   CUDA_TRY(ctx, launch_gather(d_particles, anc, n, p0, stage, ctx->stream));
   ctx->launches += 1;
-  if (ctx->comm && ctx->nranks > 1) {
+  if (ctx->comm) {
     st = exchange(ctx, plan, P_local, stage, d_particles, 6);
     if (st) return st;
   } else {

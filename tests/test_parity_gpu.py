@@ -278,6 +278,49 @@ def test_resample_bit_exact(cd, ctx, orc, P):
         assert np.array_equal(anc.cpu().numpy(), ref)
 
 
+# ---------------------------------------------------------------------------- NCCL path on one GPU
+def test_nccl_one_rank_equals_local(cd, orc):
+    """With a 1-rank NCCL communicator attached, every collective path (LSE all-gather, moment all-reduce,
+    Q all-gather + host plan + exchange) runs; results must equal the communicator-free path bit for bit."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        ctx1 = cd.Context(0)
+        ctx1.comm_init_from_torch(0, 1)
+        ctx0 = cd.Context(0)
+        cfg = small_cfg(J=2, K=3, ny=4, nv=4, nf=64, P=3000)
+        case = Case(orc, cfg)
+        xa, xb = case.dx.clone(), case.dx.clone()
+        for n in range(3):
+            e0, l0 = cd.bp_step(ctx0, case.scene, xa, case.dsfv, case.dy, case.m, case.v, case.eta, 0.1, 0.5, 11, n)
+            e1, l1 = cd.bp_step(ctx1, case.scene, xb, case.dsfv, case.dy, case.m, case.v, case.eta, 0.1, 0.5, 11, n)
+            ctx0.sync()
+            ctx1.sync()
+            assert torch.equal(xa, xb) and torch.equal(l0, l1)
+            assert torch.allclose(e0, e1, rtol=1e-13, atol=1e-15)
+        w = torch.rand(4097, dtype=torch.float64, device="cuda:0")
+        a0 = cd.resample(ctx0, w, 12345)
+        a1 = cd.resample(ctx1, w, 12345)
+        w0, s0 = cd.weights_normalize(ctx0, torch.log(w))
+        w1, s1 = cd.weights_normalize(ctx1, torch.log(w))
+        ctx0.sync()
+        ctx1.sync()
+        assert torch.equal(a0, a1) and torch.equal(w0, w1) and torch.equal(s0, s1)
+        ctx1.close()
+        ctx0.close()
+    finally:
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------------------- whole step
 def test_bp_step_fp64_end_to_end(cd, ctx, orc):
     """c1 (10 steps): GPU bp_step in FP64 mode vs the oracle's bp_step, step by step from the same

@@ -219,7 +219,7 @@ def run_cdms(args):
                 "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
                 "frac_at_measured_clock": (round(achieved / fp32_peak_tflops(clocks["sm_mhz"]), 4)
                                            if clocks.get("sm_mhz") else None),
-                "kernel": "cdms::loglik_kernel", "kernel_ms": round(kernel_ms, 4),
+                "kernel": "cdms::corr_kernel (row A2-A5: responses, correlation c, Gram G)", "kernel_ms": round(kernel_ms, 4),
                 "kernel_share_of_step": round(kernel_ms / ms_per_step, 4),
                 "flop_per_launch": flop_launch, "traffic": traffic_from_profiles(args.config)}
         result = {

@@ -37,7 +37,7 @@ namespace {
 
 enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
-  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_COUNT
+  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_TAIL, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -89,6 +89,9 @@ cdms_status ws(cdms_ctx ctx, int slot, size_t count, T** out) {
     cudaError_t e = cudaMalloc(&ctx->bufs[slot], want);
     if (e != cudaSuccess) return fail(ctx, CDMS_ENOMEM, "cudaMalloc(%zu): %s", want, cudaGetErrorString(e));
     ctx->sizes[slot] = want;
+    // fresh workspaces start zeroed (K1's per-particle flags are OR-accumulated and cleared by K1b)
+    e = cudaMemsetAsync(ctx->bufs[slot], 0, want, ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, CDMS_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
   }
   *out = static_cast<T*>(ctx->bufs[slot]);
   return CDMS_OK;
@@ -126,7 +129,7 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
   out->nf = sc->nf;
   out->wavefront = sc->wavefront;
   out->pathloss = sc->pathloss ? 1 : 0;
-  out->kc_len = sc->nf < KCHUNK ? sc->nf : KCHUNK;
+  out->kc_len = sc->nf < corr_kchunk(out->S) ? sc->nf : corr_kchunk(out->S);
   out->n_mb = (out->Na + NWARP - 1) / NWARP;
   out->n_kc = (sc->nf + out->kc_len - 1) / out->kc_len;
   out->dy = sc->dy;
@@ -139,10 +142,16 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
   out->segdf_c = (double)SEG * sc->df / C_LIGHT;
   out->fc_c = sc->fc / C_LIGHT;
   out->lambda = C_LIGHT / sc->fc;
+  out->fc_cf = (float)out->fc_c;
+  out->df_cf = (float)out->df_c;
+  out->nf_f = (float)sc->nf;
+  out->c6N_f = (float)(PI * PI / 6.0 * ((double)sc->nf * sc->nf - 1.0));
+  out->evenN_mask = ((sc->nf - 1) & 1) ? 0x80000000u : 0u;
   {
     // |Delta_m| <= ||q_m|| = ||p~_m|| <= half the URA diagonal (H, R orthogonal)
     const double hy = 0.5 * (sc->ny - 1) * fabs(sc->dy), hv = 0.5 * (sc->nv - 1) * fabs(sc->dv);
-    out->small_step = (2.0 * PI * sqrt(hy * hy + hv * hv) * out->df_c <= 0.2) ? 1 : 0;
+    const double th = 2.0 * PI * sqrt(hy * hy + hv * hv) * out->df_c;
+    out->small_step = (th <= 0.02) ? 2 : (th <= 0.2) ? 1 : 0;
     out->small_z = (2.0 * PI * sqrt(hy * hy + hv * hv) * out->segdf_c <= 1.0) ? 1 : 0;
   }
   for (int j = 0; j < sc->J; ++j) {
@@ -368,11 +377,14 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   float4* yt;
   double* yn;
   double2* terms;
+  double2* tail;
+  float4* tmpl;
   int* pflag;
   const int64_t tiles = (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP;
   WS_TRY(ctx, WS_YTILES, tiles, &yt);
   WS_TRY(ctx, WS_YNORM, MAXJ, &yn);
-  CUDA_TRY(ctx, launch_prep_y(sd, static_cast<const float2*>(d_y), yt, yn, ctx->stream));
+  WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &tmpl);
+  CUDA_TRY(ctx, launch_prep_y(sd, static_cast<const float2*>(d_y), yt, yn, tmpl, ctx->stream));
   ctx->launches += 1;
   // particles go through K1 (correlation + Gram -> HBM terms) and K1b (assembly) in batches whose terms
   // buffer stays under TERMS_BUDGET bytes
@@ -392,10 +404,16 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     a.sfv = (d_sfv && sfv_pp) ? d_sfv + b0 * 3 * sd.K : d_sfv;
     a.sfv_pp = sfv_pp;
     a.ytiles = yt;
+    a.tmpl = tmpl;
     a.terms = terms;
     a.pflag = pflag;
     a.flags = ctx->d_flags;
     a.n_tiles = (nb + TILE_P - 1) / TILE_P;
+    a.n_units = a.n_tiles * sd.J * sd.n_mb;
+    a.grid = corr_grid(sd, a.n_tiles, precision, ctx->num_sms);
+    if (a.grid < 1) return fail(ctx, CDMS_ECUDA, "corr_kernel occupancy query failed");
+    WS_TRY(ctx, WS_TAIL, (size_t)a.grid * T * TILE_P, &tail);
+    a.tail = tail;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {
       while (ctx->ev_pool.size() < ctx->ev_used + 2) {
@@ -408,10 +426,13 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       ctx->ev_used += 2;
       CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
     }
-    CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream, ctx->num_sms));
+    CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
     if (ctx->timing) CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
     AsmArgs s;
     s.terms = terms;
+    s.tail = tail;
+    s.n_units = a.n_units;
+    s.grid = a.grid;
     s.pflag = pflag;
     s.ynorm2 = yn;
     s.logw_prior = d_logw ? d_logw + b0 : nullptr;
@@ -533,6 +554,9 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
     if (PB > P_local) PB = P_local;
     WS_TRY(ctx, WS_TERMS, (size_t)PB * sd.J * T, &d2);
     WS_TRY(ctx, WS_PFLAG, PB, &i32);
+    const int64_t grid = corr_grid(sd, (PB + TILE_P - 1) / TILE_P, scene->precision, ctx->num_sms);
+    WS_TRY(ctx, WS_TAIL, (size_t)(grid > 0 ? grid : 1) * T * TILE_P, &d2);
+    WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &f4);
   }
   WS_TRY(ctx, WS_YNORM, MAXJ, &d);
   WS_TRY(ctx, WS_LSE_PART, nb + 1, &d2);

@@ -16,7 +16,7 @@ constexpr int TILE_P = 32;    // particles per CTA tile (one per lane)
 constexpr int NWARP = 8;      // warps per CTA = antennas per antenna block
 constexpr int NTHREADS = TILE_P * NWARP;
 constexpr int SEG = 64;       // Horner segment length in subcarriers (re-anchor period)
-constexpr int KCHUNK = 128;   // subcarriers per shared-memory chunk of y (multiple of SEG)
+constexpr int KCHUNK = 128;   // max subcarriers per shared-memory chunk of y (multiple of SEG; corr_kchunk(S))
 constexpr double C_LIGHT = 299792458.0;
 constexpr double PI = 3.14159265358979323846;
 
@@ -32,6 +32,10 @@ struct SceneDev {
   double dy, dv, fc, df, f0;      // f0 = fc - (nf-1)/2 df
   double f0_c, df_c, segdf_c, fc_c;  // f0/c, df/c, SEG*df/c, fc/c (cycles per metre)
   double lambda;
+  // fp32 constants of the per-antenna Gram term (constant-bank operands): fc/c, df/c, N = nf,
+  // pi^2/6 (N^2 - 1) and the sign mask (bit 31 when N is even, i.e. D_N(x + 1) = -D_N(x))
+  float fc_cf, df_cf, nf_f, c6N_f;
+  uint32_t evenN_mask;
   double pa_pos[MAXJ][3];
   double pa_rot[MAXJ][9];
   double m_re[MAXJ][MAXS], m_im[MAXJ][MAXS], v[MAXJ][MAXS];
@@ -46,16 +50,22 @@ struct CorrArgs {
   int pstride;
   const double* sfv;        // [K][3], or [P][K][3] starting at the batch (sfv_pp)
   int sfv_pp;
-  const float4* ytiles;     // [J][n_mb][n_kc][kc_len][NWARP] (yr, yr, yi, yi), zero padded
+  const float4* ytiles;     // [J][Na_pad][n_kc][kc_len] (yr, yr, yi, yi), zero padded
+  const float4* tmpl;       // [J][Na_pad] template columns (R_j p~_m, ||p~_m||^2), fp32
   double2* terms;           // [P][J][T]
-  int* pflag;               // [P] per-particle: 1 degenerate, 2 invalid input
+  double2* tail;            // [grid][T][TILE_P] tail part of the CTA's first group when it starts mid-group
+  int* pflag;               // [P] per-particle, ORed (zeroed by K1b): 1 degenerate, 2 invalid input
   int* flags;
   int64_t n_tiles;
+  int64_t n_units;          // n_tiles * J * n_mb
+  int64_t grid;             // CTAs (partition denominator)
 };
 // K1b (S x S assembly) for the same batch
 struct AsmArgs {
   const double2* terms;
-  const int* pflag;
+  const double2* tail;      // CorrArgs::tail, with the same n_units / grid
+  int64_t n_units, grid;
+  int* pflag;
   const double* ynorm2;     // [J]
   const double* logw_prior; // [P] (batch) or NULL
   double* loglik;           // [P]
@@ -109,11 +119,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // ---------------------------------------------------------------------------- launchers
 // (defined in loglik.cu / beliefs.cu, called from cdms.cpp)
-cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2,
+cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2, float4* tmpl,
                           cudaStream_t st);
-cudaError_t launch_corr(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st, int num_sms);
+int64_t corr_grid(const SceneDev& sc, int64_t n_tiles, int precision, int num_sms);  // 0 on error
+cudaError_t launch_corr(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st);
 cudaError_t launch_assemble(const SceneDev& sc, const AsmArgs& a, cudaStream_t st);
 size_t corr_smem_bytes(int S, int precision);
+int corr_kchunk(int S);   // subcarriers per y chunk (SceneDev::kc_len = min(corr_kchunk(S), nf))
 cudaError_t launch_response(const SceneDev& sc, const double* pos, int64_t n, const int32_t* js,
                             const double* sfv, double2* psi, int precision, int* flags, cudaStream_t st);
 cudaError_t launch_layout(const SceneDev& sc, const double* sfv, double* layout, double* va, double* H,

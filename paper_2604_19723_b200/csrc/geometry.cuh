@@ -93,7 +93,8 @@ __device__ __forceinline__ void template_col(const SceneDev& sc, int j, int m, d
 }
 
 // Per (particle, PA j, component s) set-up (fp64), kept in shared memory as RT fields:
-//   r = p - p_VA (RT), R = ||r|| (fp64 and RT), rs2 = 2 r.shat, and the phase-centre phasors
+//   h = H r with r = p - p_VA (so that r.q_m = r.(H v_m) = h.v_m, H symmetric: one dot product per antenna),
+//   R = ||r|| (fp64 and RT), and the phase-centre phasors
 //   E0 = e^{j2pi R f0/c}, W = e^{j2pi R df/c}, Zp = e^{j2pi SEG R df/c}, evaluated in fp64 from fp64
 //   range-reduced phases and only then rounded (a fp32 phase in cycles would carry a ~1e-7 cycle error
 //   that w^k repeats coherently on every antenna), gain = lambda/(4 pi R) with path loss
@@ -104,12 +105,14 @@ __device__ __forceinline__ void template_col(const SceneDev& sc, int j, int m, d
 // closed-form Gram.
 template <typename RT>
 struct PSField {
-  RT rx, ry, rz, sx, sy, sz, rs2, R, E0r, E0i, gain;
+  RT hx, hy, hz, R, E0r, E0i, gain;
   RT Whr, Whi, Wlr, Wli, Zhr, Zhi, Zlr, Zli;  // W, Zp as unevaluated sums hi + lo (fp32: ~48-bit mantissa)
 };
-constexpr int NPSF = 19;       // RT fields of PSField
-constexpr int NPSF_PAD = 20;   // shared-memory stride per (component, particle): 80 B (fp32) -> 5 x LDS.128
-constexpr int PSF_GAIN = 10;   // index of .gain
+constexpr int NPSF = 15;       // RT fields of PSField
+// shared-memory stride per (component, particle): 80 B (fp32), 4 x LDS.128; a stride of 4 x odd words keeps the
+// per-lane 128-bit loads of a quarter warp on distinct banks (64 B would be 4-way conflicted)
+constexpr int NPSF_PAD = 20;
+constexpr int PSF_GAIN = 6;    // index of .gain
 
 // Load the NPSF fields of one (component, particle) record with 128-bit shared-memory loads.
 template <typename RT>
@@ -141,9 +144,8 @@ __device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double*
   const double r0 = pos[0] - va[0], r1 = pos[1] - va[1], r2 = pos[2] - va[2];
   const double R = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
   R64 = R;
-  f.rx = (RT)r0; f.ry = (RT)r1; f.rz = (RT)r2;
-  f.sx = (RT)sh[0]; f.sy = (RT)sh[1]; f.sz = (RT)sh[2];
-  f.rs2 = (RT)(2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]));
+  const double rs2 = 2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]);
+  f.hx = (RT)(r0 - rs2 * sh[0]); f.hy = (RT)(r1 - rs2 * sh[1]); f.hz = (RT)(r2 - rs2 * sh[2]);
   f.R = (RT)R;
   double s_, c_;
   sincospi(2.0 * frac_c(R * sc.f0_c), &s_, &c_);
@@ -157,7 +159,7 @@ __device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double*
   f.gain = (RT)(sc.pathloss ? sc.lambda / (4.0 * PI * R) : 1.0);
   if (!sfv_ok) return PS_BADSFV;
   if (!(R > 0.0)) {  // also catches NaN positions
-    f.R = RT(1); f.rx = RT(1); f.ry = RT(0); f.rz = RT(0); f.gain = RT(1);
+    f.R = RT(1); f.hx = RT(1); f.hy = RT(0); f.hz = RT(0); f.gain = RT(1);
     R64 = 1.0;
     return PS_DEGENERATE;
   }
@@ -177,6 +179,13 @@ __device__ __forceinline__ void cis_small(RT x_cycles, RT& re, RT& im) {
   const RT t = RT(2.0 * PI) * x_cycles, t2 = t * t;
   re = RT(1) + t2 * (RT(-0.5) + t2 * (RT(1.0 / 24) + t2 * RT(-1.0 / 720)));
   im = t * (RT(1) + t2 * (RT(-1.0 / 6) + t2 * (RT(1.0 / 120) + t2 * RT(-1.0 / 5040))));
+}
+// |2 pi Delta df/c| <= 0.02 (sc.small_step == 2, e.g. every BASELINE config): degree 4 / 3 (error < 3e-11)
+template <typename RT>
+__device__ __forceinline__ void cis_tiny(RT x_cycles, RT& re, RT& im) {
+  const RT t = RT(2.0 * PI) * x_cycles, t2 = t * t;
+  re = RT(1) + t2 * (RT(-0.5) + t2 * RT(1.0 / 24));
+  im = t * (RT(1) + t2 * RT(-1.0 / 6));
 }
 // e^{j 2 pi x} for |2 pi x| <= 1 (sc.small_z): degree-12/13 Taylor polynomials (error < 1.1e-11)
 template <typename RT>
@@ -215,9 +224,7 @@ struct SMPhasors {
 template <typename RT>
 __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& f, const RT v[3], RT q2, int m,
                                          int s, SMPhasors<RT>& o, bool& degenerate) {
-  const RT sv = f.sx * v[0] + f.sy * v[1] + f.sz * v[2];
-  const RT rv = f.rx * v[0] + f.ry * v[1] + f.rz * v[2];
-  const RT rq = rv - f.rs2 * sv;  // r.q with q = v - 2 shat (shat.v)
+  const RT rq = f.hx * v[0] + f.hy * v[1] + f.hz * v[2];  // r.q_m = (H r).v_m
   RT delta;
   if (sc.wavefront == CDMS_SPHERICAL) {
     const RT n = q2 - RT(2) * rq;
@@ -242,7 +249,8 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
     cis2pi_fast<RT>(delta * (RT)sc.f0_c, er, ei);
     cmul<RT>(f.E0r, f.E0i, er, ei, o.Ar, o.Ai);
     // w, Z are raised to powers: accurate small-angle polynomials / sincospi, products rounded once in fp64
-    if (sc.small_step) cis_small<RT>(delta * (RT)sc.df_c, er, ei);
+    if (sc.small_step == 2) cis_tiny<RT>(delta * (RT)sc.df_c, er, ei);
+    else if (sc.small_step) cis_small<RT>(delta * (RT)sc.df_c, er, ei);
     else cis2pi<RT>(delta * (RT)sc.df_c, er, ei);
     cmul_df<RT>(f.Whr, f.Whi, f.Wlr, f.Wli, er, ei, o.wr, o.wi);
     if (sc.nf > SEG) {  // Z only advances A between segments

@@ -7,7 +7,8 @@
 // K1b assemble_kernel<S>: one thread per particle, fp64: the S x S low-rank evaluation of the MT update
 // message iota~ (Supplement S-V-C), summed over the PAs.
 //
-// K1 work decomposition: CTA = 32 particles (lanes) x 8 antennas (warps), persistent grid.  For each PA and
+// K1 work decomposition: CTA = 32 particles (lanes) x 8 antennas (warps), persistent grid; each CTA takes a
+// contiguous range of (tile, PA, antenna block) units (tail balance, see corr_kernel).  For each PA and
 // each block of 8 antennas, y^(j) streams through shared memory in chunks of <= 128 subcarriers x 8 antennas
 // by 1-D bulk TMA (cp.async.bulk, mbarrier, double buffered), stored as (yr, yr, yi, yi) so one broadcast
 // LDS.128 feeds FFMA2 (fma.rn.f32x2) Horner steps that advance two components per instruction.  Per
@@ -21,12 +22,20 @@ namespace cdms {
 
 // ---------------------------------------------------------------------------- y re-layout
 // y [J][nf][Na] (paper vec order) -> ytiles [J][Na_pad][n_kc][kc_len] of (yr, yr, yi, yi), Na_pad = 8 n_mb
-// (zero padded): each warp streams its own antenna's chunks; and ||z^(j)||^2 in fp64 (block 0 of each PA,
-// fixed reduction order).
-__global__ void prep_y_kernel(const SceneDev sc, const float2* __restrict__ y, float4* __restrict__ yt,
-                              double* __restrict__ ynorm2) {
+// (zero padded): each warp streams its own antenna's chunks; ||z^(j)||^2 in fp64 (block 0 of each PA,
+// fixed reduction order); and the template columns tmpl[j][m] = (R_j p~_m, ||p~_m||^2) evaluated in fp64 and
+// rounded once to fp32 (padded antennas repeat m = 0).
+__global__ void prep_y_kernel(const __grid_constant__ SceneDev sc, const float2* __restrict__ y,
+                              float4* __restrict__ yt, double* __restrict__ ynorm2, float4* __restrict__ tmpl) {
   const int j = blockIdx.y;
   const int64_t per_j = (int64_t)sc.n_mb * sc.n_kc * sc.kc_len * NWARP;
+  if (blockIdx.x == gridDim.x - 1) {
+    for (int m = threadIdx.x; m < sc.n_mb * NWARP; m += blockDim.x) {
+      double v[3], q2;
+      template_col(sc, j, m < sc.Na ? m : 0, v, q2);
+      tmpl[(int64_t)j * sc.n_mb * NWARP + m] = make_float4((float)v[0], (float)v[1], (float)v[2], (float)q2);
+    }
+  }
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < per_j;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int kl = (int)(t % sc.kc_len);
@@ -56,12 +65,14 @@ __global__ void prep_y_kernel(const SceneDev sc, const float2* __restrict__ y, f
   }
 }
 
-cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2, cudaStream_t st) {
+cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2, float4* tmpl,
+                          cudaStream_t st) {
   const int64_t per_j = (int64_t)sc.n_mb * sc.n_kc * sc.kc_len * NWARP;
   int gx = (int)((per_j + 255) / 256);
   if (gx > 1024) gx = 1024;
+  if (gx < 2) gx = 2;
   dim3 grid(gx, sc.J);
-  prep_y_kernel<<<grid, 256, 0, st>>>(sc, y, ytiles, ynorm2);
+  prep_y_kernel<<<grid, 256, 0, st>>>(sc, y, ytiles, ynorm2, tmpl);
   return cudaGetLastError();
 }
 
@@ -199,40 +210,18 @@ struct Horner<S, double> {
   }
 };
 
-// Dirichlet kernel for the per-antenna Gram terms (x = n + xr): fp32 numerator by MUFU after exact mod-2
-// reduction of N xr, accurate denominator; fp64 exact (C-amb-13).
-template <typename RT>
-__device__ __forceinline__ RT dirichlet_term(RT xr, long long n, int N);
-template <>
-__device__ __forceinline__ float dirichlet_term<float>(float xr, long long n, int N) {
-  float d;
-  if (fabsf(xr) < 1e-6f) {
-    const float N2 = (float)N * (float)N;
-    d = (float)N * (1.f - (float)(PI * PI / 6.0) * (N2 - 1.f) * xr * xr);
-  } else {
-    float t = (float)N * xr;
-    t = t - 2.f * rintf(0.5f * t);
-    // sin(pi xr), |xr| <= 1/2: odd Taylor polynomial to (pi xr)^11 (error < 6e-8 at pi/2)
-    const float u = 3.14159265358979f * xr, u2 = u * u;
-    const float den = u * (1.f + u2 * (-1.f / 6 + u2 * (1.f / 120 + u2 * (-1.f / 5040 + u2 * (1.f / 362880 +
-                      u2 * (-1.f / 39916800))))));
-    d = __fdividef(__sinf(3.14159265358979f * t), den);
-  }
-  if (((N - 1) & 1) && (n & 1)) d = -d;
-  return d;
-}
-template <>
-__device__ __forceinline__ double dirichlet_term<double>(double xr, long long n, int N) {
-  return dirichlet<double>(xr, n, N);
-}
-
 // ---------------------------------------------------------------------------- shared memory plan
+// y chunk length per S: 128 subcarriers while 3 CTAs fit, else 64 (S >= 6) so the fp32 kernel keeps 3 CTAs
+// (24 warps) per SM for S <= 7 -- the FFMA2 Horner needs >= 4 warps per SMSP.
+__host__ __device__ constexpr int kchunk_for(int S) { return S <= 5 ? 128 : 64; }
+
 template <int S, typename RT>
 struct Plan {
   static constexpr int NPAIR = S * (S - 1) / 2;
   static constexpr int NTRI = S * (S + 1) / 2;
   static constexpr int T = S + NTRI;
-  static constexpr size_t ybuf = 2ull * KCHUNK * NWARP * sizeof(float4);
+  static constexpr int KC = kchunk_for(S);
+  static constexpr size_t ybuf = 2ull * KC * NWARP * sizeof(float4);
   static constexpr size_t ps =
       (size_t)NPSF_PAD * S * TILE_P * sizeof(RT) + (size_t)S * TILE_P * sizeof(double);
   static constexpr size_t dlt = (size_t)S * NWARP * TILE_P * sizeof(RT);            // Delta [S][8][32]
@@ -240,6 +229,8 @@ struct Plan {
   static constexpr size_t acc = (size_t)(S + NPAIR) * TILE_P * sizeof(double2);     // fp64 sums [item][32]
   static constexpr size_t misc = 2 * NWARP * sizeof(uint64_t) + TILE_P * 3 * sizeof(double) + TILE_P * sizeof(int);
   static constexpr size_t total = ybuf + ps + dlt + cst + acc + misc;
+  // resident CTAs per SM the kernel is compiled for: 3 when the plan fits 3 x (smem + 1 KB reserve) in 228 KB
+  static constexpr int min_blocks = (sizeof(RT) == 8) ? 1 : (total + 1024 <= 228 * 1024 / 3 ? 3 : 2);
 };
 
 size_t corr_smem_bytes(int S, int precision) {
@@ -251,6 +242,7 @@ size_t corr_smem_bytes(int S, int precision) {
     default: return 0;
   }
 }
+int corr_kchunk(int S) { return kchunk_for(S); }
 
 // ---------------------------------------------------------------------------- phase timing (debug build)
 // -DCDMS_PHASE_TIMING: per-warp clock64 cycles per phase of K1, summed into g_phase (tools/phase_timing.py).
@@ -277,18 +269,63 @@ namespace cdms {
 #define PT_FLUSH
 #endif
 
+// ---------------------------------------------------------------------------- Gram term per (pair, antenna)
+// sum_k e^{j 2 pi dd_m f_k / c} relative to the pair's base carrier, for one antenna (row A4):
+//   e^{j 2 pi dd fc/c} D_N(x), x = dR df/c + dd df/c = nb + xbr + dd df/c, dd = Delta_a,m - Delta_b,m
+//   D_N(n + xr) = (-1)^{n (N-1)} sin(pi N xr) / sin(pi xr), D_N(0) = N (C-amb-13)
+// fp32: MUFU carrier and numerator (after exact mod-2 reduction of N xr), polynomial sin(pi xr), one
+// approximate reciprocal, branch-free small-|xr| series and sign; fp64: exact library functions.
+struct GramPairF {
+  float xbr;        // centred fraction of dR df/c (from fp64)
+  uint32_t nbpar;   // parity of the integer part nb, shifted to bit 31 when N is even (sign flips), else 0
+};
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const GramPairF& gp, float& gr,
+                                            float& gi) {
+  const float fc_c = sc.fc_cf, df_c = sc.df_cf, Nf = sc.nf_f, c6N = sc.c6N_f;
+  const uint32_t evenN_mask = sc.evenN_mask;
+  float ph = dd * fc_c;
+  ph -= rintf(ph);
+  float sn, cs;
+  __sincosf(6.28318530717958647692f * ph, &sn, &cs);
+  const float x = fmaf(dd, df_c, gp.xbr);
+  const float n2 = rintf(x);
+  const float xr = x - n2;
+  float t = Nf * xr;
+  t = fmaf(-2.f, rintf(0.5f * t), t);
+  const float num = __sinf(3.14159265358979f * t);
+  const float u = 3.14159265358979f * xr, u2 = u * u;
+  // sin(pi xr), |xr| <= 1/2: odd Taylor polynomial to (pi xr)^11 (error < 6e-8 at pi/2)
+  const float den = u * fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, -1.f / 39916800, 1.f / 362880), -1.f / 5040),
+                                                1.f / 120), -1.f / 6), 1.f);
+  float D = num * rcp_approx(den);
+  const float Ds = Nf * fmaf(-c6N, xr * xr, 1.f);  // N (1 - pi^2/6 (N^2 - 1) xr^2)
+  D = (fabsf(xr) < 1e-6f) ? Ds : D;
+  // (-1)^{(nb + n2)(N-1)}: parity of the integer-valued n2 from the mantissa after adding 1.5 * 2^23
+  const uint32_t par = ((uint32_t)__float_as_int(n2 + 12582912.f) << 31) ^ gp.nbpar;
+  D = __int_as_float(__float_as_int(D) ^ (int)(par & evenN_mask));
+  gr = fmaf(D, cs, gr);
+  gi = fmaf(D, sn, gi);
+}
+
 // ---------------------------------------------------------------------------- K1
+// Work partition (tail balance): a unit is (tile of 32 particles, PA j, block of 8 antennas), ordered
+// u = (tile J + j) n_mb + mb; CTA b processes the contiguous units [b U / G, (b+1) U / G), G <= U / n_mb, so a
+// group (tile, j) is split across at most two CTAs.  The part holding mb = 0 (head) writes the group's terms;
+// the other part (tail, always the first group of its CTA) writes its antenna sums to the CTA's tail record,
+// which K1b adds (two partial sums: deterministic).
 template <int S, typename RT>
-// fp32, S <= 7: 3 CTAs (24 warps) per SM -- the FFMA2 Horner is latency-bound and reaches ~96% of the FMA
-// pipe only with >= 4 warps per SMSP in the loop; S = 8, 9 need the registers (2 CTAs).
-#ifndef CDMS_MINB_SMALL_S
-#define CDMS_MINB_SMALL_S 3
-#endif
-__global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? (S <= 7 ? CDMS_MINB_SMALL_S : 2) : 1)
+__global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
     corr_kernel(const __grid_constant__ SceneDev sc, const CorrArgs a) {
   using PL = Plan<S, RT>;
   constexpr int NPAIR = PL::NPAIR;
   constexpr int T = PL::T;
+  constexpr int KC = PL::KC;
+  constexpr bool F32 = sizeof(RT) == 4;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* sp = smem;
   float4* ybuf = reinterpret_cast<float4*>(sp);                         sp += PL::ybuf;
@@ -306,270 +343,310 @@ __global__ void __launch_bounds__(NTHREADS, (sizeof(RT) == 4) ? (S <= 7 ? CDMS_M
   const int J = sc.J, Na = sc.Na, nf = sc.nf, kcl = sc.kc_len;
   const int n_mb = sc.n_mb, n_kc = sc.n_kc, Na_pad = sc.n_mb * NWARP;
   const bool nb_mode = sc.wavefront == CDMS_PLANAR_NB;
-  const int64_t chunks_per_tile = (int64_t)J * n_mb * n_kc;
-  const uint32_t chunk_bytes = (uint32_t)(kcl * sizeof(float4));
-  const int64_t my_tiles =
-      (a.n_tiles > (int64_t)blockIdx.x) ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t total_chunks = my_tiles * chunks_per_tile;
+  const int64_t U = a.n_units;
+  const int64_t u0 = (int64_t)blockIdx.x * U / gridDim.x;
+  const int64_t u1 = ((int64_t)blockIdx.x + 1) * U / gridDim.x;
+  const int64_t total_chunks = (u1 - u0) * n_kc;
 
   // Every warp streams its own antenna's y chunks (no CTA-wide barrier per chunk): lane 0 issues a 1-D bulk
-  // TMA of kc_len (yr, yr, yi, yi) into the warp's double buffer, completion on the warp's mbarrier.
-  // Chunks are issued strictly in order c = 0, 1, 2, ...: an incremental (j, mb, kc) cursor replaces the
-  // index decomposition (64-bit div/mod are long integer sequences).
-  int is_j = 0, is_mb = 0, is_kc = 0;
+  // TMA of kc_len (yr, yr, yi, yi) into the warp's double buffer, completion on the warp's mbarrier.  Chunk
+  // c = (u - u0) n_kc + kc of unit u sits at element offset (((u mod J n_mb) 8 + warp) n_kc + kc) kc_len of
+  // ytiles [J][Na_pad][n_kc][kc_len] (j Na_pad + 8 mb = 8 (j n_mb + mb)): a running offset, no div/mod.
+  int is_mbj = (int)(u0 % ((int64_t)J * n_mb)), is_kc = 0;
+  int64_t is_off = (((int64_t)is_mbj * NWARP + warp) * n_kc) * kcl;
   auto issue = [&](int64_t c) {
-    const int m = is_mb * NWARP + warp;
     uint64_t* bar = &mbar[warp * 2 + (c & 1)];
+    const uint32_t chunk_bytes = (uint32_t)(sc.kc_len * sizeof(float4));
     fence_proxy_async();
     mbar_expect_tx(bar, chunk_bytes);
-    tma_load_1d(ybuf + (warp * 2 + (c & 1)) * KCHUNK,
-                a.ytiles + (((int64_t)is_j * Na_pad + m) * n_kc + is_kc) * kcl, chunk_bytes, bar);
-    if (++is_kc == n_kc) {
+    tma_load_1d(ybuf + (warp * 2 + (c & 1)) * KC, a.ytiles + is_off, chunk_bytes, bar);
+    is_off += sc.kc_len;
+    if (++is_kc == sc.n_kc) {
       is_kc = 0;
-      if (++is_mb == n_mb) {
-        is_mb = 0;
-        if (++is_j == J) is_j = 0;
+      is_off += (int64_t)(NWARP - 1) * sc.n_kc * sc.kc_len;
+      if (++is_mbj == sc.J * sc.n_mb) {
+        is_mbj = 0;
+        is_off = (int64_t)warp * sc.n_kc * sc.kc_len;
       }
     }
   };
 
   if (tid < 2 * NWARP) mbar_init(&mbar[tid], 1);
   if (tid == 0) fence_mbar_init();
+  if (tid < TILE_P) pfl[tid] = 0;
   __syncthreads();
   if (lane == 0) {
     if (total_chunks > 0) issue(0);
     if (total_chunks > 1) issue(1);
   }
 
-  int64_t ci = 0;  // flat chunk counter (the same sequence in every warp)
-  for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+  int64_t ci = 0;            // flat chunk counter (the same sequence in every warp)
+  int64_t cur_tile = -1;
+  int64_t u = u0;
+  while (u < u1) {
+    const int64_t g = u / n_mb;
+    const int mb_lo = (int)(u - g * n_mb);
+    const int mb_hi = (int)min((int64_t)n_mb, u1 - g * n_mb);
+    const int64_t tile = g / J;
+    const int j = (int)(g - tile * J);
+    const bool head = mb_lo == 0;
     const int64_t p = tile * TILE_P + lane;
     const bool pvalid = p < a.P;
-    if (warp == 0) {
+    if (tile != cur_tile) {
+      if (warp == 0) {
+        if (cur_tile >= 0) {  // flags of the previous tile (OR over the CTAs sharing it; K1b clears them)
+          const int64_t pp = cur_tile * TILE_P + lane;
+          if (pp < a.P && pfl[lane]) atomicOr(&a.pflag[pp], pfl[lane]);
+        }
 #pragma unroll
-      for (int c = 0; c < 3; ++c) pos_s[c * TILE_P + lane] = pvalid ? a.particles[p * a.pstride + c] : 1.0;
-      pfl[lane] = 0;
+        for (int c = 0; c < 3; ++c) pos_s[c * TILE_P + lane] = pvalid ? a.particles[p * a.pstride + c] : 1.0;
+        pfl[lane] = 0;
+      }
+      cur_tile = tile;
+      __syncthreads();
     }
-    __syncthreads();
     PT_DECL
 
-    for (int j = 0; j < J; ++j) {
-      // ---- (1) per (component, particle) set-up in fp64 (rows A1/A2); zero the fp64 accumulators
-      for (int it = tid; it < S * TILE_P; it += NTHREADS) {
-        const int s = it / TILE_P, pl = it - s * TILE_P;
+    // ---- (1) per (component, particle) set-up in fp64 (rows A1/A2); zero the fp64 accumulators
+    for (int it = tid; it < S * TILE_P; it += NTHREADS) {
+      const int s = it / TILE_P, pl = it - s * TILE_P;
+      const int64_t pp = tile * TILE_P + pl;
+      const double pos[3] = {pos_s[pl], pos_s[TILE_P + pl], pos_s[2 * TILE_P + pl]};
+      const double* sfv_s = nullptr;
+      if (s > 0) sfv_s = a.sfv + ((a.sfv_pp && pp < a.P) ? pp * 3 * sc.K : 0) + 3 * (s - 1);
+      PSField<RT> f;
+      double R64 = 1.0;
+      const int st = setup_ps<RT>(sc, j, pos, sfv_s, f, R64);
+      if (st != PS_OK && pp < a.P) {
+        const bool bad = st == PS_BADSFV || !(pos[0] == pos[0] && pos[1] == pos[1] && pos[2] == pos[2]);
+        atomicOr(&pfl[pl], bad ? 3 : 1);
+      }
+      const RT* fv = reinterpret_cast<const RT*>(&f);
+#pragma unroll
+      for (int q = 0; q < NPSF; ++q) psf[(s * TILE_P + pl) * NPSF_PAD + q] = fv[q];
+      R64s[s * TILE_P + pl] = R64;
+    }
+    for (int it = tid; it < (S + NPAIR) * TILE_P; it += NTHREADS) acc[it] = make_double2(0.0, 0.0);
+    __syncthreads();
+    PT(0)
+
+    // ---- (1b) planar NB Gram, separable closed form in fp64 (P:L2160-2184 with the template P:L29-39):
+    //   G_ab = e^{j 2 pi dR fc/c} D_Nf(dR df/c) D_ny(dy du'_y fc/c) D_nv(dv du'_z fc/c),
+    //   dR = R_a - R_b, du' = u'_b - u'_a, u'_s = R_j^T H_s r_s / R_s (local directions).  Whole array: head only.
+    if (nb_mode && NPAIR > 0 && head) {
+      for (int it = tid; it < NPAIR * TILE_P; it += NTHREADS) {
+        const int q = it / TILE_P, pl = it - q * TILE_P;
+        int ca, cb;
+        pair_ab(q, S, ca, cb);
         const int64_t pp = tile * TILE_P + pl;
         const double pos[3] = {pos_s[pl], pos_s[TILE_P + pl], pos_s[2 * TILE_P + pl]};
-        const double* sfv_s = nullptr;
-        if (s > 0) sfv_s = a.sfv + ((a.sfv_pp && pp < a.P) ? pp * 3 * sc.K : 0) + 3 * (s - 1);
-        PSField<RT> f;
-        double R64 = 1.0;
-        const int st = setup_ps<RT>(sc, j, pos, sfv_s, f, R64);
-        if (st != PS_OK && pp < a.P) {
-          const bool bad = st == PS_BADSFV || !(pos[0] == pos[0] && pos[1] == pos[1] && pos[2] == pos[2]);
-          atomicOr(&pfl[pl], bad ? 3 : 1);
+        double ul[2][3];
+        const int comp[2] = {ca, cb};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int s = comp[e];
+          const double* sfv_s = s ? a.sfv + ((a.sfv_pp && pp < a.P) ? pp * 3 * sc.K : 0) + 3 * (s - 1) : nullptr;
+          double va[3], sh[3];
+          if (!anchor_va(sc, j, sfv_s, va, sh)) { va[0] = pos[0] - 1.0; va[1] = pos[1]; va[2] = pos[2]; sh[0] = sh[1] = sh[2] = 0.0; }
+          double r[3] = {pos[0] - va[0], pos[1] - va[1], pos[2] - va[2]};
+          const double R = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+          const double rs = r[0] * sh[0] + r[1] * sh[1] + r[2] * sh[2];
+          double h[3] = {r[0] - 2.0 * rs * sh[0], r[1] - 2.0 * rs * sh[1], r[2] - 2.0 * rs * sh[2]};
+          const double* Rj = sc.pa_rot[j];
+          const double inv = R > 0.0 ? 1.0 / R : 0.0;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) ul[e][c] = (Rj[0 * 3 + c] * h[0] + Rj[1 * 3 + c] * h[1] + Rj[2 * 3 + c] * h[2]) * inv;
         }
-        const RT* fv = reinterpret_cast<const RT*>(&f);
-#pragma unroll
-        for (int q = 0; q < NPSF; ++q) psf[(s * TILE_P + pl) * NPSF_PAD + q] = fv[q];
-        R64s[s * TILE_P + pl] = R64;
+        const double dR = R64s[ca * TILE_P + pl] - R64s[cb * TILE_P + pl];
+        double sb, cbv;
+        sincospi(2.0 * frac_c(dR * sc.fc_c), &sb, &cbv);
+        const double xb = dR * sc.df_c, nbr = rint(xb);
+        double D = dirichlet<double>(xb - nbr, (long long)nbr, nf);
+        const double xy = sc.dy * (ul[1][1] - ul[0][1]) * sc.fc_c, xv = sc.dv * (ul[1][2] - ul[0][2]) * sc.fc_c;
+        const double ny_ = rint(xy), nv_ = rint(xv);
+        D *= dirichlet<double>(xy - ny_, (long long)ny_, sc.ny) * dirichlet<double>(xv - nv_, (long long)nv_, sc.nv);
+        acc[(S + q) * TILE_P + pl] = make_double2(D * cbv, D * sb);
       }
-      for (int it = tid; it < (S + NPAIR) * TILE_P; it += NTHREADS) acc[it] = make_double2(0.0, 0.0);
-      __syncthreads();
-      PT(0)
+    }
 
-      // ---- (1b) planar NB Gram, separable closed form in fp64 (P:L2160-2184 with the template P:L29-39):
-      //   G_ab = e^{j 2 pi dR fc/c} D_Nf(dR df/c) D_ny(dy du'_y fc/c) D_nv(dv du'_z fc/c),
-      //   dR = R_a - R_b, du' = u'_b - u'_a, u'_s = R_j^T H_s r_s / R_s (local directions)
-      if (nb_mode && NPAIR > 0) {
-        for (int it = tid; it < NPAIR * TILE_P; it += NTHREADS) {
-          const int q = it / TILE_P, pl = it - q * TILE_P;
-          int ca, cb;
-          pair_ab(q, S, ca, cb);
-          const int64_t pp = tile * TILE_P + pl;
-          const double pos[3] = {pos_s[pl], pos_s[TILE_P + pl], pos_s[2 * TILE_P + pl]};
-          double ul[2][3];
-          const int comp[2] = {ca, cb};
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int s = comp[e];
-            const double* sfv_s = s ? a.sfv + ((a.sfv_pp && pp < a.P) ? pp * 3 * sc.K : 0) + 3 * (s - 1) : nullptr;
-            double va[3], sh[3];
-            if (!anchor_va(sc, j, sfv_s, va, sh)) { va[0] = pos[0] - 1.0; va[1] = pos[1]; va[2] = pos[2]; sh[0] = sh[1] = sh[2] = 0.0; }
-            double r[3] = {pos[0] - va[0], pos[1] - va[1], pos[2] - va[2]};
-            const double R = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-            const double rs = r[0] * sh[0] + r[1] * sh[1] + r[2] * sh[2];
-            double h[3] = {r[0] - 2.0 * rs * sh[0], r[1] - 2.0 * rs * sh[1], r[2] - 2.0 * rs * sh[2]};
-            const double* Rj = sc.pa_rot[j];
-            const double inv = R > 0.0 ? 1.0 / R : 0.0;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) ul[e][c] = (Rj[0 * 3 + c] * h[0] + Rj[1 * 3 + c] * h[1] + Rj[2 * 3 + c] * h[2]) * inv;
-          }
-          const double dR = R64s[ca * TILE_P + pl] - R64s[cb * TILE_P + pl];
-          double sb, cbv;
-          sincospi(2.0 * frac_c(dR * sc.fc_c), &sb, &cbv);
-          const double xb = dR * sc.df_c, nbr = rint(xb);
-          double D = dirichlet<double>(xb - nbr, (long long)nbr, nf);
-          const double xy = sc.dy * (ul[1][1] - ul[0][1]) * sc.fc_c, xv = sc.dv * (ul[1][2] - ul[0][2]) * sc.fc_c;
-          const double ny_ = rint(xy), nv_ = rint(xv);
-          D *= dirichlet<double>(xy - ny_, (long long)ny_, sc.ny) * dirichlet<double>(xv - nv_, (long long)nv_, sc.nv);
-          acc[(S + q) * TILE_P + pl] = make_double2(D * cbv, D * sb);
-        }
-      }
-
-      for (int mb = 0; mb < n_mb; ++mb) {
-        const int m = mb * NWARP + warp;
-        const bool mvalid = m < Na;
-        // ---- (2) per (component, antenna) offsets and phasors (row A2)
-        RT Ar[S], Ai[S], Zr[S], Zi[S];
-        Horner<S, RT> H;
-        {
-          RT wr[S], wi[S];
+    for (int mb = mb_lo; mb < mb_hi; ++mb) {
+      const int m = mb * NWARP + warp;
+      const bool mvalid = m < Na;
+      // ---- (2) per (component, antenna) offsets and phasors (row A2)
+      RT Ar[S], Ai[S], Zr[S], Zi[S];
+      Horner<S, RT> H;
+      {
+        RT wr[S], wi[S];
+        RT v[3], q2;
+        if (F32) {
+          // template column R_j p~_m: fp64, rounded once (table from prep_y, L1-resident)
+          const float4 tv = __ldg(&a.tmpl[j * Na_pad + m]);
+          v[0] = (RT)tv.x; v[1] = (RT)tv.y; v[2] = (RT)tv.z; q2 = (RT)tv.w;
+        } else {
           double v64[3], q264;
           template_col(sc, j, mvalid ? m : 0, v64, q264);
-          const RT v[3] = {(RT)v64[0], (RT)v64[1], (RT)v64[2]};
-          const RT q2 = (RT)q264;
-          bool deg_any = false;
+          v[0] = (RT)v64[0]; v[1] = (RT)v64[1]; v[2] = (RT)v64[2]; q2 = (RT)q264;
+        }
+        bool deg_any = false;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          PSField<RT> f;
+          RT* fv = reinterpret_cast<RT*>(&f);
+          load_psf<RT>(psf + (s * TILE_P + lane) * NPSF_PAD, fv);  // 128-bit loads
+          SMPhasors<RT> o;
+          bool dg;
+          setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
+          deg_any |= dg;
+          Ar[s] = o.Ar; Ai[s] = o.Ai; wr[s] = o.wr; wi[s] = o.wi; Zr[s] = o.Zr; Zi[s] = o.Zi;
+          const int o_ = (s * NWARP + warp) * TILE_P + lane;
+          dlt[o_] = o.delta;
+          cst[2 * o_] = RT(0);
+          cst[2 * o_ + 1] = RT(0);
+        }
+        if (deg_any && mvalid && pvalid) atomicOr(&pfl[lane], 1);
+        H.init(wr, wi);
+        PT(2)
+      }
+      // ---- (3) correlation over all subcarriers (row A3): segmented Horner on TMA-staged y chunks
+      for (int kc = 0; kc < n_kc; ++kc, ++ci) {
+        mbar_wait(&mbar[warp * 2 + (ci & 1)], (uint32_t)((ci >> 1) & 1));
+        const float4* yb = ybuf + (warp * 2 + (ci & 1)) * KC;
+        const int k_begin = kc * kcl;
+        const int k_end = min(k_begin + kcl, nf);
+        for (int k0 = k_begin; k0 < k_end; k0 += SEG) {
+          const int k1 = min(k0 + SEG, k_end);
+          const float4* yk = yb + (k1 - 1 - k_begin);  // Horner runs from the top subcarrier down
+          H.reset_to(yk[0]);                            // acc = y_top (= 0 * w + y_top)
+          if (k1 - k0 == SEG) {
+#pragma unroll 7
+            for (int i = 1; i < SEG; ++i) H.step(yk[-i]);
+          } else {
+            for (int i = 1; i < k1 - k0; ++i) H.step(yk[-i]);
+          }
+          // c += A_seg H_seg (thread-private slot), A_seg <- A_seg Z
+          RT hr[S], hi[S];
+          H.get(hr, hi);
 #pragma unroll
           for (int s = 0; s < S; ++s) {
-            PSField<RT> f;
-            RT* fv = reinterpret_cast<RT*>(&f);
-#pragma unroll
-            load_psf<RT>(psf + (s * TILE_P + lane) * NPSF_PAD, fv);  // 128-bit loads
-            SMPhasors<RT> o;
-            bool dg;
-            setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
-            deg_any |= dg;
-            Ar[s] = o.Ar; Ai[s] = o.Ai; wr[s] = o.wr; wi[s] = o.wi; Zr[s] = o.Zr; Zi[s] = o.Zi;
             const int o_ = (s * NWARP + warp) * TILE_P + lane;
-            dlt[o_] = o.delta;
-            cst[2 * o_] = RT(0);
-            cst[2 * o_ + 1] = RT(0);
+            cst[2 * o_] = fma(Ar[s], hr[s], fma(-Ai[s], hi[s], cst[2 * o_]));
+            cst[2 * o_ + 1] = fma(Ar[s], hi[s], fma(Ai[s], hr[s], cst[2 * o_ + 1]));
+            const RT nAr = Ar[s] * Zr[s] - Ai[s] * Zi[s];
+            const RT nAi = Ar[s] * Zi[s] + Ai[s] * Zr[s];
+            Ar[s] = nAr;
+            Ai[s] = nAi;
           }
-          if (deg_any && mvalid && pvalid) atomicOr(&pfl[lane], 1);
-          H.init(wr, wi);
-          PT(2)
         }
-        // ---- (3) correlation over all subcarriers (row A3): segmented Horner on TMA-staged y chunks
-        for (int kc = 0; kc < n_kc; ++kc, ++ci) {
-          mbar_wait(&mbar[warp * 2 + (ci & 1)], (uint32_t)((ci >> 1) & 1));
-          const float4* yb = ybuf + (warp * 2 + (ci & 1)) * KCHUNK;
-          const int k_begin = kc * kcl;
-          const int k_end = min(k_begin + kcl, nf);
-          for (int k0 = k_begin; k0 < k_end; k0 += SEG) {
-            const int k1 = min(k0 + SEG, k_end);
-            const float4* yk = yb + (k1 - 1 - k_begin);  // Horner runs from the top subcarrier down
-            H.reset_to(yk[0]);                            // acc = y_top (= 0 * w + y_top)
-            if (k1 - k0 == SEG) {
-#pragma unroll 7
-              for (int i = 1; i < SEG; ++i) H.step(yk[-i]);
-            } else {
-              for (int i = 1; i < k1 - k0; ++i) H.step(yk[-i]);
+        __syncwarp();  // every lane of this warp is done with the buffer
+        if (lane == 0 && ci + 2 < total_chunks) issue(ci + 2);
+      }
+      PT(3)
+      __syncthreads();  // publish this block's cst / dlt
+      PT(4)
+      const int nw_valid = min(NWARP, Na - mb * NWARP);
+      // ---- (4a) c_s += sum over the block's antennas, ascending m; owner warp rotates with mb
+      for (int s = (warp - mb) & (NWARP - 1); s < S; s += NWARP) {
+        double sr = 0.0, si = 0.0;
+        for (int w2 = 0; w2 < nw_valid; ++w2) {
+          const int o_ = (s * NWARP + w2) * TILE_P + lane;
+          sr += (double)cst[2 * o_];
+          si += (double)cst[2 * o_ + 1];
+        }
+        double2 v = acc[s * TILE_P + lane];
+        acc[s * TILE_P + lane] = make_double2(v.x + sr, v.y + si);
+      }
+      // ---- (4b) spherical / planar WB Gram terms (row A4) over the block's antennas:
+      //   sum_m e^{j 2 pi (D_a,m - D_b,m) fc/c} D_N((d_a,m - d_b,m) df/c); the base carrier e^{j 2 pi dR fc/c}
+      //   is applied in fp64 at the hand-off (shared by all antennas: its rounding must not repeat)
+      if (!nb_mode) {
+        for (int q = (warp - mb - S) & (NWARP - 1); q < NPAIR; q += NWARP) {
+          int pa, pb;
+          pair_ab(q, S, pa, pb);
+          const double dR = R64s[pa * TILE_P + lane] - R64s[pb * TILE_P + lane];
+          const double xb = dR * sc.df_c;
+          const double nbd = rint(xb);
+          RT gr = RT(0), gi = RT(0);
+          if (F32) {
+            GramPairF gp;
+            gp.xbr = (float)(xb - nbd);
+            gp.nbpar = (uint32_t)((long long)nbd & 1) << 31;
+            for (int w2 = 0; w2 < nw_valid; ++w2) {
+              const float dd = (float)(dlt[(pa * NWARP + w2) * TILE_P + lane] - dlt[(pb * NWARP + w2) * TILE_P + lane]);
+              float fr = (float)gr, fi = (float)gi;
+              gram_term_f(sc, dd, gp, fr, fi);
+              gr = (RT)fr; gi = (RT)fi;
             }
-            // c += A_seg H_seg (thread-private slot), A_seg <- A_seg Z
-            RT hr[S], hi[S];
-            H.get(hr, hi);
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-              const int o_ = (s * NWARP + warp) * TILE_P + lane;
-              cst[2 * o_] = fma(Ar[s], hr[s], fma(-Ai[s], hi[s], cst[2 * o_]));
-              cst[2 * o_ + 1] = fma(Ar[s], hi[s], fma(Ai[s], hr[s], cst[2 * o_ + 1]));
-              const RT nAr = Ar[s] * Zr[s] - Ai[s] * Zi[s];
-              const RT nAi = Ar[s] * Zi[s] + Ai[s] * Zr[s];
-              Ar[s] = nAr;
-              Ai[s] = nAi;
-            }
-          }
-          __syncwarp();  // every lane of this warp is done with the buffer
-          if (lane == 0 && ci + 2 < total_chunks) issue(ci + 2);
-        }
-        PT(3)
-        __syncthreads();  // publish this block's cst / dlt
-        PT(4)
-        const int nw_valid = min(NWARP, Na - mb * NWARP);
-        // ---- (4a) c_s += sum over the block's antennas, ascending m; owner warp rotates with mb
-        for (int s = (warp - mb) & (NWARP - 1); s < S; s += NWARP) {
-          double sr = 0.0, si = 0.0;
-          for (int w2 = 0; w2 < nw_valid; ++w2) {
-            const int o_ = (s * NWARP + w2) * TILE_P + lane;
-            sr += (double)cst[2 * o_];
-            si += (double)cst[2 * o_ + 1];
-          }
-          double2 v = acc[s * TILE_P + lane];
-          acc[s * TILE_P + lane] = make_double2(v.x + sr, v.y + si);
-        }
-        // ---- (4b) spherical / planar WB Gram terms (row A4) over the block's antennas:
-        //   sum_m e^{j 2 pi (D_a,m - D_b,m) fc/c} D_N((d_a,m - d_b,m) df/c); the base carrier e^{j 2 pi dR fc/c}
-        //   is applied in fp64 at the hand-off (shared by all antennas: its rounding must not repeat)
-        if (!nb_mode) {
-          for (int q = (warp - mb - S) & (NWARP - 1); q < NPAIR; q += NWARP) {
-            int pa, pb;
-            pair_ab(q, S, pa, pb);
-            const double dR = R64s[pa * TILE_P + lane] - R64s[pb * TILE_P + lane];
-            const double xb = dR * sc.df_c;
-            const double nbd = rint(xb);
-            const RT xbr = (RT)(xb - nbd);
+          } else {
             const long long nbi = (long long)nbd;
-            RT gr = RT(0), gi = RT(0);
+            const RT xbr = (RT)(xb - nbd);
             for (int w2 = 0; w2 < nw_valid; ++w2) {
               const RT dd = dlt[(pa * NWARP + w2) * TILE_P + lane] - dlt[(pb * NWARP + w2) * TILE_P + lane];
               RT er, ei;
               cis2pi_fast<RT>(dd * (RT)sc.fc_c, er, ei);
               const RT x = xbr + dd * (RT)sc.df_c;
               const RT n2 = Num<RT>::rint_(x);
-              const RT D = dirichlet_term<RT>(x - n2, nbi + (long long)n2, nf);
+              const RT D = dirichlet<RT>(x - n2, nbi + (long long)n2, nf);
               gr = fma(D, er, gr);
               gi = fma(D, ei, gi);
             }
-            double2 v = acc[(S + q) * TILE_P + lane];
-            acc[(S + q) * TILE_P + lane] = make_double2(v.x + (double)gr, v.y + (double)gi);
           }
+          double2 v = acc[(S + q) * TILE_P + lane];
+          acc[(S + q) * TILE_P + lane] = make_double2(v.x + (double)gr, v.y + (double)gi);
         }
-        PT(5)
-        __syncthreads();  // before the next block's set-up rewrites dlt / cst
-        PT(6)
       }
-
-      // ---- (5) hand-off: c (with gains) and the lower triangle of G (with gains) to HBM
-      const double nz = (double)nf * (double)Na;
-      for (int it = tid; it < T * TILE_P; it += NTHREADS) {
-        const int pl = it / T, t = it - pl * T;
-        const int64_t pp = tile * TILE_P + pl;
-        if (pp >= a.P) continue;
-        double2 out;
-        if (t < S) {
-          const double g = (double)psf[(t * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
-          const double2 v = acc[t * TILE_P + pl];
-          out = make_double2(v.x * g, v.y * g);
-        } else {
-          int r = 0, e = t - S;
-          while (e >= r + 1) { e -= r + 1; ++r; }
-          const int c = e;  // (r, c), r >= c
-          const double gr_ = (double)psf[(r * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
-          const double gc_ = (double)psf[(c * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
-          if (r == c) {
-            out = make_double2(nz * gr_ * gc_, 0.0);
-          } else {
-            // G_cr (c < r) accumulated; lower entry G_rc = conj(G_cr)
-            const int q = pair_index(c, r, S);
-            double2 v = acc[(S + q) * TILE_P + pl];
-            if (!nb_mode) {
-              const double dR = R64s[c * TILE_P + pl] - R64s[r * TILE_P + pl];
-              double sb, cb;
-              sincospi(2.0 * frac_c(dR * sc.fc_c), &sb, &cb);
-              v = make_double2(cb * v.x - sb * v.y, cb * v.y + sb * v.x);
-            }
-            const double g2 = gr_ * gc_;
-            out = make_double2(v.x * g2, -v.y * g2);
-          }
-        }
-        a.terms[(pp * J + j) * T + t] = out;
-      }
-      __syncthreads();  // the next PA's set-up rewrites psf / R64s / acc
-      PT(7)
+      PT(5)
+      __syncthreads();  // before the next block's set-up rewrites dlt / cst
+      PT(6)
     }
+
+    // ---- (5) hand-off: c (with gains) and the lower triangle of G (with gains).  Head (or whole group) ->
+    // terms [P][J][T]; tail -> this CTA's record [T][32], antenna sums only (the analytic diagonal and the NB
+    // whole-array Gram belong to the head).
+    const double nz = (double)nf * (double)Na;
+    for (int it = tid; it < T * TILE_P; it += NTHREADS) {
+      const int pl = it / T, t = it - pl * T;
+      const int64_t pp = tile * TILE_P + pl;
+      if (pp >= a.P) continue;
+      double2 out;
+      if (t < S) {
+        const double gn = (double)psf[(t * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
+        const double2 v = acc[t * TILE_P + pl];
+        out = make_double2(v.x * gn, v.y * gn);
+      } else {
+        int r = 0, e = t - S;
+        while (e >= r + 1) { e -= r + 1; ++r; }
+        const int c = e;  // (r, c), r >= c
+        const double gr_ = (double)psf[(r * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
+        const double gc_ = (double)psf[(c * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
+        if (r == c) {
+          out = make_double2(head ? nz * gr_ * gc_ : 0.0, 0.0);
+        } else if (nb_mode && !head) {
+          out = make_double2(0.0, 0.0);
+        } else {
+          // G_cr (c < r) accumulated; lower entry G_rc = conj(G_cr)
+          const int q = pair_index(c, r, S);
+          double2 v = acc[(S + q) * TILE_P + pl];
+          if (!nb_mode) {
+            const double dR = R64s[c * TILE_P + pl] - R64s[r * TILE_P + pl];
+            double sb, cb;
+            sincospi(2.0 * frac_c(dR * sc.fc_c), &sb, &cb);
+            v = make_double2(cb * v.x - sb * v.y, cb * v.y + sb * v.x);
+          }
+          const double g2 = gr_ * gc_;
+          out = make_double2(v.x * g2, -v.y * g2);
+        }
+      }
+      if (head) a.terms[(pp * J + j) * T + t] = out;
+      else a.tail[((int64_t)blockIdx.x * T + t) * TILE_P + pl] = out;
+    }
+    __syncthreads();  // the next group's set-up rewrites psf / R64s / acc
+    PT(7)
     PT_FLUSH
-    if (warp == 0 && pvalid) a.pflag[p] = pfl[lane];
-    __syncthreads();  // pos_s / pfl reuse by the next tile
+    u = g * n_mb + mb_hi;
+  }
+  if (warp == 0 && cur_tile >= 0) {
+    const int64_t pp = cur_tile * TILE_P + lane;
+    if (pp < a.P && pfl[lane]) atomicOr(&a.pflag[pp], pfl[lane]);
   }
 }
 
@@ -601,6 +678,22 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
     for (int s = 0; s < S; ++s) wc[s * ASM_T + ln] = tp[s];
 #pragma unroll 1
     for (int t = 0; t < NTRI; ++t) wk[t * ASM_T + ln] = tp[S + t];
+    {
+      // group (tile, j) split across two K1 CTAs: add the tail part held by the CTA owning its last unit,
+      // owner(u) = max{b : floor(b U / G) <= u} = floor(((u + 1) G - 1) / U)
+      const int64_t tile = p / TILE_P;
+      const int64_t uf = (tile * J + j) * sc.n_mb, ul = uf + sc.n_mb - 1;
+      const int64_t bt = ((ul + 1) * a.grid - 1) / a.n_units;
+      if (bt * a.n_units / a.grid > uf) {
+        const double2* tr = a.tail + bt * T * TILE_P + (p - tile * TILE_P);
+#pragma unroll 1
+        for (int t = 0; t < T; ++t) {
+          const double2 v = tr[t * TILE_P];
+          double2* d = (t < S) ? &wc[t * ASM_T + ln] : &wk[(t - S) * ASM_T + ln];
+          *d = make_double2(d->x + v.x, d->y + v.y);
+        }
+      }
+    }
     if (a.term_c != nullptr) {
 #pragma unroll 1
       for (int r = 0; r < S; ++r) {
@@ -707,6 +800,7 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
     }
   }
   const int pf = a.pflag[p];
+  if (pf) a.pflag[p] = 0;  // K1 ORs into a zeroed buffer
   if (pf) {
     l = -INFINITY;
     atomicOr(a.flags, (pf & 2) ? (FLAG_NAN | FLAG_DEGENERATE) : FLAG_DEGENERATE);
@@ -717,41 +811,46 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------- launch
+// Persistent grid: every resident CTA (latency hiding), at most one CTA per (tile, PA) group so a group is
+// split across at most two CTAs.  Returns 0 on error.
 template <int S, typename RT>
-static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStream_t st, int num_sms) {
+static int64_t corr_grid_t(int64_t n_tiles, int J, int num_sms) {
   const size_t smem = Plan<S, RT>::total;
   auto kern = corr_kernel<S, RT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, smem);
-  if (e != cudaSuccess) return e;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, smem) != cudaSuccess) return 0;
   if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)per_sm * num_sms;  // persistent: all resident CTAs (latency hiding beats tail balance)
-  if (grid > a.n_tiles) grid = a.n_tiles;
-  if (grid < 1) return cudaSuccess;
-  kern<<<(unsigned)grid, NTHREADS, smem, st>>>(sc, a);
+  int64_t grid = (int64_t)per_sm * num_sms;
+  if (grid > n_tiles * J) grid = n_tiles * J;
+  return grid < 1 ? 1 : grid;
+}
+
+template <int S, typename RT>
+static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStream_t st) {
+  if (a.grid < 1 || a.n_units < 1) return cudaSuccess;
+  corr_kernel<S, RT><<<(unsigned)a.grid, NTHREADS, Plan<S, RT>::total, st>>>(sc, a);
   return cudaGetLastError();
 }
 
-template <typename RT>
-static cudaError_t dispatch_corr(const SceneDev& sc, const CorrArgs& a, cudaStream_t st, int num_sms) {
+int64_t corr_grid(const SceneDev& sc, int64_t n_tiles, int precision, int num_sms) {
   switch (sc.S) {
-    case 1: return launch_corr_t<1, RT>(sc, a, st, num_sms);
-    case 2: return launch_corr_t<2, RT>(sc, a, st, num_sms);
-    case 3: return launch_corr_t<3, RT>(sc, a, st, num_sms);
-    case 4: return launch_corr_t<4, RT>(sc, a, st, num_sms);
-    case 5: return launch_corr_t<5, RT>(sc, a, st, num_sms);
-    case 6: return launch_corr_t<6, RT>(sc, a, st, num_sms);
-    case 7: return launch_corr_t<7, RT>(sc, a, st, num_sms);
-    case 8: return launch_corr_t<8, RT>(sc, a, st, num_sms);
-    case 9: return launch_corr_t<9, RT>(sc, a, st, num_sms);
-    default: return cudaErrorInvalidValue;
+#define CASE_S(n) \
+  case n: return precision == CDMS_FP64 ? corr_grid_t<n, double>(n_tiles, sc.J, num_sms) : corr_grid_t<n, float>(n_tiles, sc.J, num_sms);
+    CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
+#undef CASE_S
+    default: return 0;
   }
 }
 
-cudaError_t launch_corr(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st, int num_sms) {
-  return precision == CDMS_FP64 ? dispatch_corr<double>(sc, a, st, num_sms) : dispatch_corr<float>(sc, a, st, num_sms);
+cudaError_t launch_corr(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st) {
+  switch (sc.S) {
+#define CASE_S(n) \
+  case n: return precision == CDMS_FP64 ? launch_corr_t<n, double>(sc, a, st) : launch_corr_t<n, float>(sc, a, st);
+    CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
+#undef CASE_S
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_assemble(const SceneDev& sc, const AsmArgs& a, cudaStream_t st) {

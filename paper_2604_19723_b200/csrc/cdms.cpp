@@ -37,7 +37,7 @@ namespace {
 
 enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
-  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_TAIL, WS_COUNT
+  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -377,8 +377,8 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   float4* yt;
   double* yn;
   double2* terms;
-  double2* tail;
   float4* tmpl;
+  unsigned int* sched;
   int* pflag;
   const int64_t tiles = (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP;
   WS_TRY(ctx, WS_YTILES, tiles, &yt);
@@ -395,6 +395,8 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   if (PB > P) PB = P;
   WS_TRY(ctx, WS_TERMS, (size_t)PB * sd.J * T, &terms);
   WS_TRY(ctx, WS_PFLAG, PB, &pflag);
+  WS_TRY(ctx, WS_SCHED, 2, &sched);  // zeroed at allocation, reset by the last K1 CTA of every launch
+  if ((PB + TILE_P - 1) / TILE_P * sd.J >= (int64_t)1 << 31) return fail(ctx, CDMS_EINVAL, "loglik: batch too large");
   for (int64_t b0 = 0; b0 < P; b0 += PB) {
     const int64_t nb = (P - b0 < PB) ? P - b0 : PB;
     CorrArgs a;
@@ -409,11 +411,10 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     a.pflag = pflag;
     a.flags = ctx->d_flags;
     a.n_tiles = (nb + TILE_P - 1) / TILE_P;
-    a.n_units = a.n_tiles * sd.J * sd.n_mb;
+    a.n_groups = a.n_tiles * sd.J;
     a.grid = corr_grid(sd, a.n_tiles, precision, ctx->num_sms);
     if (a.grid < 1) return fail(ctx, CDMS_ECUDA, "corr_kernel occupancy query failed");
-    WS_TRY(ctx, WS_TAIL, (size_t)a.grid * T * TILE_P, &tail);
-    a.tail = tail;
+    a.sched = sched;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {
       while (ctx->ev_pool.size() < ctx->ev_used + 2) {
@@ -430,9 +431,6 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     if (ctx->timing) CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
     AsmArgs s;
     s.terms = terms;
-    s.tail = tail;
-    s.n_units = a.n_units;
-    s.grid = a.grid;
     s.pflag = pflag;
     s.ynorm2 = yn;
     s.logw_prior = d_logw ? d_logw + b0 : nullptr;
@@ -554,8 +552,8 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
     if (PB > P_local) PB = P_local;
     WS_TRY(ctx, WS_TERMS, (size_t)PB * sd.J * T, &d2);
     WS_TRY(ctx, WS_PFLAG, PB, &i32);
-    const int64_t grid = corr_grid(sd, (PB + TILE_P - 1) / TILE_P, scene->precision, ctx->num_sms);
-    WS_TRY(ctx, WS_TAIL, (size_t)(grid > 0 ? grid : 1) * T * TILE_P, &d2);
+    unsigned int* sch;
+    WS_TRY(ctx, WS_SCHED, 2, &sch);
     WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &f4);
   }
   WS_TRY(ctx, WS_YNORM, MAXJ, &d);

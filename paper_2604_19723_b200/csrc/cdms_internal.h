@@ -53,18 +53,16 @@ struct CorrArgs {
   const float4* ytiles;     // [J][Na_pad][n_kc][kc_len] (yr, yr, yi, yi), zero padded
   const float4* tmpl;       // [J][Na_pad] template columns (R_j p~_m, ||p~_m||^2), fp32
   double2* terms;           // [P][J][T]
-  double2* tail;            // [grid][T][TILE_P] tail part of the CTA's first group when it starts mid-group
   int* pflag;               // [P] per-particle, ORed (zeroed by K1b): 1 degenerate, 2 invalid input
   int* flags;
+  unsigned int* sched;      // [2] group claim counter and finished-CTA counter, zero between launches
   int64_t n_tiles;
-  int64_t n_units;          // n_tiles * J * n_mb
-  int64_t grid;             // CTAs (partition denominator)
+  int64_t n_groups;         // n_tiles * J (< 2^31)
+  int64_t grid;             // CTAs
 };
 // K1b (S x S assembly) for the same batch
 struct AsmArgs {
   const double2* terms;
-  const double2* tail;      // CorrArgs::tail, with the same n_units / grid
-  int64_t n_units, grid;
   int* pflag;
   const double* ynorm2;     // [J]
   const double* logw_prior; // [P] (batch) or NULL

@@ -227,7 +227,9 @@ struct Plan {
   static constexpr size_t dlt = (size_t)S * NWARP * TILE_P * sizeof(RT);            // Delta [S][8][32]
   static constexpr size_t cst = (size_t)S * NWARP * TILE_P * 2 * sizeof(RT);        // c per antenna
   static constexpr size_t acc = (size_t)(S + NPAIR) * TILE_P * sizeof(double2);     // fp64 sums [item][32]
-  static constexpr size_t misc = 2 * NWARP * sizeof(uint64_t) + TILE_P * 3 * sizeof(double) + TILE_P * sizeof(int);
+  // mbarriers, positions, per-particle flags, claimed-group ring
+  static constexpr size_t misc =
+      2 * NWARP * sizeof(uint64_t) + TILE_P * 3 * sizeof(double) + TILE_P * sizeof(int) + 4 * sizeof(unsigned);
   static constexpr size_t total = ybuf + ps + dlt + cst + acc + misc;
   // resident CTAs per SM the kernel is compiled for: 3 when the plan fits 3 x (smem + 1 KB reserve) in 228 KB
   static constexpr int min_blocks = (sizeof(RT) == 8) ? 1 : (total + 1024 <= 228 * 1024 / 3 ? 3 : 2);
@@ -313,11 +315,12 @@ __device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const 
 }
 
 // ---------------------------------------------------------------------------- K1
-// Work partition (tail balance): a unit is (tile of 32 particles, PA j, block of 8 antennas), ordered
-// u = (tile J + j) n_mb + mb; CTA b processes the contiguous units [b U / G, (b+1) U / G), G <= U / n_mb, so a
-// group (tile, j) is split across at most two CTAs.  The part holding mb = 0 (head) writes the group's terms;
-// the other part (tail, always the first group of its CTA) writes its antenna sums to the CTA's tail record,
-// which K1b adds (two partial sums: deterministic).
+// Work distribution: dynamic.  A group is (tile of 32 particles, PA j), g = tile J + j; thread 0 of each
+// persistent CTA claims groups from a global counter three groups ahead (ring in shared memory) so the per-warp
+// TMA streams run across group boundaries without a stall.  Co-resident CTAs progress at different rates under
+// the warp scheduler's age priority; static partitions left ~17% of the warp slots idle (ncu warps_active 20
+// of 24), dynamic claiming keeps every slot busy until the queue drains.  Each group is computed entirely by
+// one CTA: results do not depend on the schedule.  The last CTA to finish resets the counters.
 template <int S, typename RT>
 __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
     corr_kernel(const __grid_constant__ SceneDev sc, const CorrArgs a) {
@@ -343,68 +346,72 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
   const int J = sc.J, Na = sc.Na, nf = sc.nf, kcl = sc.kc_len;
   const int n_mb = sc.n_mb, n_kc = sc.n_kc, Na_pad = sc.n_mb * NWARP;
   const bool nb_mode = sc.wavefront == CDMS_PLANAR_NB;
-  const int64_t U = a.n_units;
-  const int64_t u0 = (int64_t)blockIdx.x * U / gridDim.x;
-  const int64_t u1 = ((int64_t)blockIdx.x + 1) * U / gridDim.x;
-  const int64_t total_chunks = (u1 - u0) * n_kc;
+  const uint32_t n_groups = (uint32_t)a.n_groups;
+  unsigned int* gring = reinterpret_cast<unsigned int*>(pfl + TILE_P);  // [4] claimed group indices
 
   // Every warp streams its own antenna's y chunks (no CTA-wide barrier per chunk): lane 0 issues a 1-D bulk
-  // TMA of kc_len (yr, yr, yi, yi) into the warp's double buffer, completion on the warp's mbarrier.  Chunk
-  // c = (u - u0) n_kc + kc of unit u sits at element offset (((u mod J n_mb) 8 + warp) n_kc + kc) kc_len of
-  // ytiles [J][Na_pad][n_kc][kc_len] (j Na_pad + 8 mb = 8 (j n_mb + mb)): a running offset, no div/mod.
-  int is_mbj = (int)(u0 % ((int64_t)J * n_mb)), is_kc = 0;
-  int64_t is_off = (((int64_t)is_mbj * NWARP + warp) * n_kc) * kcl;
-  auto issue = [&](int64_t c) {
-    uint64_t* bar = &mbar[warp * 2 + (c & 1)];
+  // TMA of kc_len (yr, yr, yi, yi) into the warp's double buffer, completion on the warp's mbarrier.  The
+  // stream walks the CTA's claimed groups in order; chunk (mb, kc) of group g sits at element offset
+  // (((j n_mb + mb) 8 + warp) n_kc + kc) kc_len of ytiles [J][Na_pad][n_kc][kc_len], j = g mod J: a running
+  // offset, re-based when the stream enters the next claimed group (published in gring one group earlier).
+  int is_gi = 0, is_mb = 0, is_kc = 0, is_c = 0;
+  uint32_t is_g = 0;
+  int64_t is_off = 0;
+  auto rebase = [&]() {
+    is_g = gring[is_gi & 3];
+    is_off = (((int64_t)(is_g % (uint32_t)sc.J) * sc.n_mb * NWARP + warp) * sc.n_kc) * sc.kc_len;
+  };
+  auto issue = [&]() {
+    if (is_g >= n_groups) return;
+    uint64_t* bar = &mbar[warp * 2 + (is_c & 1)];
     const uint32_t chunk_bytes = (uint32_t)(sc.kc_len * sizeof(float4));
     fence_proxy_async();
     mbar_expect_tx(bar, chunk_bytes);
-    tma_load_1d(ybuf + (warp * 2 + (c & 1)) * KC, a.ytiles + is_off, chunk_bytes, bar);
+    tma_load_1d(ybuf + (warp * 2 + (is_c & 1)) * KC, a.ytiles + is_off, chunk_bytes, bar);
+    ++is_c;
     is_off += sc.kc_len;
     if (++is_kc == sc.n_kc) {
       is_kc = 0;
       is_off += (int64_t)(NWARP - 1) * sc.n_kc * sc.kc_len;
-      if (++is_mbj == sc.J * sc.n_mb) {
-        is_mbj = 0;
-        is_off = (int64_t)warp * sc.n_kc * sc.kc_len;
+      if (++is_mb == sc.n_mb) {
+        is_mb = 0;
+        ++is_gi;
+        rebase();
       }
     }
   };
 
   if (tid < 2 * NWARP) mbar_init(&mbar[tid], 1);
-  if (tid == 0) fence_mbar_init();
+  // Claims run three groups ahead of the consumer: the issue stream (<= 2 chunks ahead) enters group gi + 2
+  // while the consumer may still be in group gi - 1 when groups hold a single chunk.
+  if (tid == 0) {
+    fence_mbar_init();
+    gring[0] = atomicAdd(a.sched, 1u);
+    gring[1] = atomicAdd(a.sched, 1u);
+    gring[2] = atomicAdd(a.sched, 1u);
+  }
   if (tid < TILE_P) pfl[tid] = 0;
   __syncthreads();
   if (lane == 0) {
-    if (total_chunks > 0) issue(0);
-    if (total_chunks > 1) issue(1);
+    rebase();
+    issue();
+    issue();
   }
 
   int64_t ci = 0;            // flat chunk counter (the same sequence in every warp)
-  int64_t cur_tile = -1;
-  int64_t u = u0;
-  while (u < u1) {
-    const int64_t g = u / n_mb;
-    const int mb_lo = (int)(u - g * n_mb);
-    const int mb_hi = (int)min((int64_t)n_mb, u1 - g * n_mb);
-    const int64_t tile = g / J;
-    const int j = (int)(g - tile * J);
-    const bool head = mb_lo == 0;
+  for (int ring_i = 0;; ++ring_i) {
+    const uint32_t g = gring[ring_i & 3];
+    if (g >= n_groups) break;
+    const int64_t tile = g / (uint32_t)J;
+    const int j = (int)(g - (uint32_t)tile * (uint32_t)J);
     const int64_t p = tile * TILE_P + lane;
     const bool pvalid = p < a.P;
-    if (tile != cur_tile) {
-      if (warp == 0) {
-        if (cur_tile >= 0) {  // flags of the previous tile (OR over the CTAs sharing it; K1b clears them)
-          const int64_t pp = cur_tile * TILE_P + lane;
-          if (pp < a.P && pfl[lane]) atomicOr(&a.pflag[pp], pfl[lane]);
-        }
+    if (warp == 0) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) pos_s[c * TILE_P + lane] = pvalid ? a.particles[p * a.pstride + c] : 1.0;
-        pfl[lane] = 0;
-      }
-      cur_tile = tile;
-      __syncthreads();
+      for (int c = 0; c < 3; ++c) pos_s[c * TILE_P + lane] = pvalid ? a.particles[p * a.pstride + c] : 1.0;
     }
+    if (tid == 0) gring[(ring_i + 3) & 3] = atomicAdd(a.sched, 1u);
+    __syncthreads();
     PT_DECL
 
     // ---- (1) per (component, particle) set-up in fp64 (rows A1/A2); zero the fp64 accumulators
@@ -432,8 +439,8 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
 
     // ---- (1b) planar NB Gram, separable closed form in fp64 (P:L2160-2184 with the template P:L29-39):
     //   G_ab = e^{j 2 pi dR fc/c} D_Nf(dR df/c) D_ny(dy du'_y fc/c) D_nv(dv du'_z fc/c),
-    //   dR = R_a - R_b, du' = u'_b - u'_a, u'_s = R_j^T H_s r_s / R_s (local directions).  Whole array: head only.
-    if (nb_mode && NPAIR > 0 && head) {
+    //   dR = R_a - R_b, du' = u'_b - u'_a, u'_s = R_j^T H_s r_s / R_s (local directions).
+    if (nb_mode && NPAIR > 0) {
       for (int it = tid; it < NPAIR * TILE_P; it += NTHREADS) {
         const int q = it / TILE_P, pl = it - q * TILE_P;
         int ca, cb;
@@ -469,7 +476,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
       }
     }
 
-    for (int mb = mb_lo; mb < mb_hi; ++mb) {
+    for (int mb = 0; mb < n_mb; ++mb) {
       const int m = mb * NWARP + warp;
       const bool mvalid = m < Na;
       // ---- (2) per (component, antenna) offsets and phasors (row A2)
@@ -538,7 +545,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
           }
         }
         __syncwarp();  // every lane of this warp is done with the buffer
-        if (lane == 0 && ci + 2 < total_chunks) issue(ci + 2);
+        if (lane == 0) issue();
       }
       PT(3)
       __syncthreads();  // publish this block's cst / dlt
@@ -599,9 +606,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
       PT(6)
     }
 
-    // ---- (5) hand-off: c (with gains) and the lower triangle of G (with gains).  Head (or whole group) ->
-    // terms [P][J][T]; tail -> this CTA's record [T][32], antenna sums only (the analytic diagonal and the NB
-    // whole-array Gram belong to the head).
+    // ---- (5) hand-off: c (with gains) and the lower triangle of G (with gains) -> terms [P][J][T]
     const double nz = (double)nf * (double)Na;
     for (int it = tid; it < T * TILE_P; it += NTHREADS) {
       const int pl = it / T, t = it - pl * T;
@@ -619,9 +624,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
         const double gr_ = (double)psf[(r * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
         const double gc_ = (double)psf[(c * TILE_P + pl) * NPSF_PAD + PSF_GAIN];
         if (r == c) {
-          out = make_double2(head ? nz * gr_ * gc_ : 0.0, 0.0);
-        } else if (nb_mode && !head) {
-          out = make_double2(0.0, 0.0);
+          out = make_double2(nz * gr_ * gc_, 0.0);
         } else {
           // G_cr (c < r) accumulated; lower entry G_rc = conj(G_cr)
           const int q = pair_index(c, r, S);
@@ -636,17 +639,24 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
           out = make_double2(v.x * g2, -v.y * g2);
         }
       }
-      if (head) a.terms[(pp * J + j) * T + t] = out;
-      else a.tail[((int64_t)blockIdx.x * T + t) * TILE_P + pl] = out;
+      a.terms[(pp * J + j) * T + t] = out;
     }
-    __syncthreads();  // the next group's set-up rewrites psf / R64s / acc
+    if (warp == 0 && pfl[lane]) {  // per-particle flags: OR over the group's CTAs (K1b reads and clears them)
+      if (pvalid) atomicOr(&a.pflag[p], pfl[lane]);
+      pfl[lane] = 0;
+    }
+    __syncthreads();  // the next group's set-up rewrites psf / R64s / acc / pos_s / pfl
     PT(7)
     PT_FLUSH
-    u = g * n_mb + mb_hi;
   }
-  if (warp == 0 && cur_tile >= 0) {
-    const int64_t pp = cur_tile * TILE_P + lane;
-    if (pp < a.P && pfl[lane]) atomicOr(&a.pflag[pp], pfl[lane]);
+  // the last CTA to finish resets the claim counter for the next launch (all claims precede every increment)
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+      a.sched[0] = 0u;
+      a.sched[1] = 0u;
+      __threadfence();
+    }
   }
 }
 
@@ -678,22 +688,6 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
     for (int s = 0; s < S; ++s) wc[s * ASM_T + ln] = tp[s];
 #pragma unroll 1
     for (int t = 0; t < NTRI; ++t) wk[t * ASM_T + ln] = tp[S + t];
-    {
-      // group (tile, j) split across two K1 CTAs: add the tail part held by the CTA owning its last unit,
-      // owner(u) = max{b : floor(b U / G) <= u} = floor(((u + 1) G - 1) / U)
-      const int64_t tile = p / TILE_P;
-      const int64_t uf = (tile * J + j) * sc.n_mb, ul = uf + sc.n_mb - 1;
-      const int64_t bt = ((ul + 1) * a.grid - 1) / a.n_units;
-      if (bt * a.n_units / a.grid > uf) {
-        const double2* tr = a.tail + bt * T * TILE_P + (p - tile * TILE_P);
-#pragma unroll 1
-        for (int t = 0; t < T; ++t) {
-          const double2 v = tr[t * TILE_P];
-          double2* d = (t < S) ? &wc[t * ASM_T + ln] : &wk[(t - S) * ASM_T + ln];
-          *d = make_double2(d->x + v.x, d->y + v.y);
-        }
-      }
-    }
     if (a.term_c != nullptr) {
 #pragma unroll 1
       for (int r = 0; r < S; ++r) {
@@ -811,8 +805,7 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------- launch
-// Persistent grid: every resident CTA (latency hiding), at most one CTA per (tile, PA) group so a group is
-// split across at most two CTAs.  Returns 0 on error.
+// Persistent grid: every resident CTA (latency hiding), at most one CTA per (tile, PA) group.  0 on error.
 template <int S, typename RT>
 static int64_t corr_grid_t(int64_t n_tiles, int J, int num_sms) {
   const size_t smem = Plan<S, RT>::total;
@@ -828,7 +821,7 @@ static int64_t corr_grid_t(int64_t n_tiles, int J, int num_sms) {
 
 template <int S, typename RT>
 static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStream_t st) {
-  if (a.grid < 1 || a.n_units < 1) return cudaSuccess;
+  if (a.grid < 1 || a.n_groups < 1) return cudaSuccess;
   corr_kernel<S, RT><<<(unsigned)a.grid, NTHREADS, Plan<S, RT>::total, st>>>(sc, a);
   return cudaGetLastError();
 }

@@ -147,6 +147,9 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
   out->nf_f = (float)sc->nf;
   out->c6N_f = (float)(PI * PI / 6.0 * ((double)sc->nf * sc->nf - 1.0));
   out->evenN_mask = ((sc->nf - 1) & 1) ? 0x80000000u : 0u;
+  out->f0_cf = (float)out->f0_c;
+  out->segdf_cf = (float)out->segdf_c;
+  out->y_mb_step = (int64_t)(NWARP - 1) * out->n_kc * out->kc_len;
   {
     // |Delta_m| <= ||q_m|| = ||p~_m|| <= half the URA diagonal (H, R orthogonal)
     const double hy = 0.5 * (sc->ny - 1) * fabs(sc->dy), hv = 0.5 * (sc->nv - 1) * fabs(sc->dv);

@@ -36,6 +36,8 @@ struct SceneDev {
   // pi^2/6 (N^2 - 1) and the sign mask (bit 31 when N is even, i.e. D_N(x + 1) = -D_N(x))
   float fc_cf, df_cf, nf_f, c6N_f;
   uint32_t evenN_mask;
+  float f0_cf, segdf_cf;  // fp32 f0/c, SEG df/c for the per-antenna set-up
+  int64_t y_mb_step;      // ytiles element step from the last chunk of an antenna block to the next block
   double pa_pos[MAXJ][3];
   double pa_rot[MAXJ][9];
   double m_re[MAXJ][MAXS], m_im[MAXJ][MAXS], v[MAXJ][MAXS];

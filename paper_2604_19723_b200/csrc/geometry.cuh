@@ -19,8 +19,17 @@ struct Num<float> {
   static __device__ __forceinline__ float sinpi_(float x) { return sinpif(x); }
   static __device__ __forceinline__ float rint_(float x) { return rintf(x); }
   static __device__ __forceinline__ float sqrt_(float x) { return sqrtf(x); }
-  static __device__ __forceinline__ float fsqrt_(float x) { return x * rsqrtf(x); }   // ~2 ulp, x > 0
-  static __device__ __forceinline__ float fdiv_(float a, float b) { return __fdividef(a, b); }
+  // ~2 ulp approximations without denormal fix-ups (arguments are metres, far from the denormal range)
+  static __device__ __forceinline__ float fsqrt_(float x) {  // x > 0
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return x * r;
+  }
+  static __device__ __forceinline__ float fdiv_(float a, float b) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+    return a * r;
+  }
   static constexpr float tiny_x = 1e-6f;  // |xr| below which D_N uses its 2nd-order series
 };
 template <>
@@ -236,9 +245,13 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
     degenerate = false;
   }
   o.delta = delta;
+  // frequency constants in RT (fp32: the host-rounded copies, constant-bank operands, no per-use F2F)
+  constexpr bool F32 = sizeof(RT) == 4;
+  const RT fc_c = F32 ? (RT)sc.fc_cf : (RT)sc.fc_c, f0_c = F32 ? (RT)sc.f0_cf : (RT)sc.f0_c;
+  const RT df_c = F32 ? (RT)sc.df_cf : (RT)sc.df_c, segdf_c = F32 ? (RT)sc.segdf_cf : (RT)sc.segdf_c;
   RT er, ei;
   if (sc.wavefront == CDMS_PLANAR_NB) {
-    cis2pi_fast<RT>(delta * (RT)sc.fc_c, er, ei);
+    cis2pi_fast<RT>(delta * fc_c, er, ei);
     cmul<RT>(f.E0r, f.E0i, er, ei, o.Ar, o.Ai);
     const RT t = (sizeof(RT) == 4) ? (RT)dither_angle(m, s) : RT(0);
     cmul_df<RT>(f.Whr, f.Whi, f.Wlr, f.Wli, RT(1), t, o.wr, o.wi);
@@ -246,16 +259,16 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
     cmul_df<RT>(f.Zhr, f.Zhi, f.Zlr, f.Zli, RT(1), tz, o.Zr, o.Zi);
   } else {
     // A: one rounding per antenna, independent across antennas -> MUFU accuracy suffices
-    cis2pi_fast<RT>(delta * (RT)sc.f0_c, er, ei);
+    cis2pi_fast<RT>(delta * f0_c, er, ei);
     cmul<RT>(f.E0r, f.E0i, er, ei, o.Ar, o.Ai);
     // w, Z are raised to powers: accurate small-angle polynomials / sincospi, products rounded once in fp64
-    if (sc.small_step == 2) cis_tiny<RT>(delta * (RT)sc.df_c, er, ei);
-    else if (sc.small_step) cis_small<RT>(delta * (RT)sc.df_c, er, ei);
-    else cis2pi<RT>(delta * (RT)sc.df_c, er, ei);
+    if (sc.small_step == 2) cis_tiny<RT>(delta * df_c, er, ei);
+    else if (sc.small_step) cis_small<RT>(delta * df_c, er, ei);
+    else cis2pi<RT>(delta * df_c, er, ei);
     cmul_df<RT>(f.Whr, f.Whi, f.Wlr, f.Wli, er, ei, o.wr, o.wi);
     if (sc.nf > SEG) {  // Z only advances A between segments
-      if (sc.small_z) cis_med<RT>(delta * (RT)sc.segdf_c, er, ei);
-      else cis2pi<RT>(delta * (RT)sc.segdf_c, er, ei);
+      if (sc.small_z) cis_med<RT>(delta * segdf_c, er, ei);
+      else cis2pi<RT>(delta * segdf_c, er, ei);
       cmul_df<RT>(f.Zhr, f.Zhi, f.Zlr, f.Zli, er, ei, o.Zr, o.Zi);
     } else {
       o.Zr = RT(1);

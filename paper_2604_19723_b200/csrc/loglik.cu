@@ -363,16 +363,17 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
   };
   auto issue = [&]() {
     if (is_g >= n_groups) return;
+    // No proxy fence: the buffer is only read by the generic proxy (LDS, completed before the __syncwarp that
+    // precedes every reissue) and only written by the async proxy.
     uint64_t* bar = &mbar[warp * 2 + (is_c & 1)];
     const uint32_t chunk_bytes = (uint32_t)(sc.kc_len * sizeof(float4));
-    fence_proxy_async();
     mbar_expect_tx(bar, chunk_bytes);
     tma_load_1d(ybuf + (warp * 2 + (is_c & 1)) * KC, a.ytiles + is_off, chunk_bytes, bar);
     ++is_c;
     is_off += sc.kc_len;
     if (++is_kc == sc.n_kc) {
       is_kc = 0;
-      is_off += (int64_t)(NWARP - 1) * sc.n_kc * sc.kc_len;
+      is_off += sc.y_mb_step;
       if (++is_mb == sc.n_mb) {
         is_mb = 0;
         ++is_gi;

@@ -40,16 +40,23 @@ def _stale(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, timing: bool = False) -> str:
-    lib = LIB_TIMING if timing else LIB
-    if not force and not _stale(lib):
+def build(force: bool = False, verbose: bool = False, timing: bool = False, variant: str | None = None,
+          defines: list[str] | None = None) -> str:
+    """Build libcdms.so; timing=True builds the phase-timing debug library; variant=NAME with defines builds
+    an experiment library libcdms_NAME.so (debug / A-B measurements only, never loaded by default)."""
+    if variant:
+        lib = os.path.join(HERE, f"libcdms_{variant}.so")
+    else:
+        lib = LIB_TIMING if timing else LIB
+    if not force and not variant and not _stale(lib):
         return lib
-    obj_dir = OBJ + ("_timing" if timing else "")
+    obj_dir = OBJ + ("_timing" if timing else "") + (f"_{variant}" if variant else "")
     os.makedirs(obj_dir, exist_ok=True)
     inc, libdir = nccl_dirs()
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(ROOT, "include")]
     if timing:
         common.append("-DCDMS_PHASE_TIMING")
+    common += [f"-D{d}" for d in (defines or [])]
 
     def compile_one(src: str) -> str:
         out = os.path.join(obj_dir, src + ".o")
@@ -77,4 +84,7 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timing="--timing" in sys.argv))
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, timing="--timing" in args, variant=var, defines=defs))

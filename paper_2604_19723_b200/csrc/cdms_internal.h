@@ -13,7 +13,10 @@ namespace cdms {
 constexpr int MAXJ = 8;       // PAs per scene
 constexpr int MAXS = 9;       // propagation components S = K + 1 (LOS + 8 walls)
 constexpr int TILE_P = 32;    // particles per CTA tile (one per lane)
-constexpr int NWARP = 8;      // warps per CTA = antennas per antenna block
+#ifndef CDMS_NWARP
+#define CDMS_NWARP 8
+#endif
+constexpr int NWARP = CDMS_NWARP;  // warps per CTA = antennas per antenna block (power of two)
 constexpr int NTHREADS = TILE_P * NWARP;
 constexpr int SEG = 64;       // Horner segment length in subcarriers (re-anchor period)
 constexpr int KCHUNK = 128;   // max subcarriers per shared-memory chunk of y (multiple of SEG; corr_kchunk(S))

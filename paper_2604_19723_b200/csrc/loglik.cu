@@ -213,7 +213,13 @@ struct Horner<S, double> {
 // ---------------------------------------------------------------------------- shared memory plan
 // y chunk length per S: 128 subcarriers while 3 CTAs fit, else 64 (S >= 6) so the fp32 kernel keeps 3 CTAs
 // (24 warps) per SM for S <= 7 -- the FFMA2 Horner needs >= 4 warps per SMSP.
-__host__ __device__ constexpr int kchunk_for(int S) { return S <= 5 ? 128 : 64; }
+__host__ __device__ constexpr int kchunk_for(int S) {
+#ifdef CDMS_KCHUNK_ALL
+  return CDMS_KCHUNK_ALL + 0 * S;
+#else
+  return S <= 5 ? 128 : 64;
+#endif
+}
 
 template <int S, typename RT>
 struct Plan {
@@ -231,8 +237,12 @@ struct Plan {
   static constexpr size_t misc =
       2 * NWARP * sizeof(uint64_t) + TILE_P * 3 * sizeof(double) + TILE_P * sizeof(int) + 4 * sizeof(unsigned);
   static constexpr size_t total = ybuf + ps + dlt + cst + acc + misc;
-  // resident CTAs per SM the kernel is compiled for: 3 when the plan fits 3 x (smem + 1 KB reserve) in 228 KB
-  static constexpr int min_blocks = (sizeof(RT) == 8) ? 1 : (total + 1024 <= 228 * 1024 / 3 ? 3 : 2);
+  // resident CTAs per SM the kernel is compiled for (fp32): as many as (smem + 1 KB reserve) fits in 228 KB,
+  // capped so that each thread keeps >= 80 registers (the Horner state + phasors of S <= 7 without spills)
+  static constexpr int smem_fit = (int)((228 * 1024) / (total + 1024));
+  static constexpr int reg_fit = 65536 / (NTHREADS * 80);
+  static constexpr int min_blocks =
+      (sizeof(RT) == 8) ? 1 : (smem_fit < reg_fit ? (smem_fit < 1 ? 1 : smem_fit) : reg_fit);
 };
 
 size_t corr_smem_bytes(int S, int precision) {
@@ -503,7 +513,12 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
           load_psf<RT>(psf + (s * TILE_P + lane) * NPSF_PAD, fv);  // 128-bit loads
           SMPhasors<RT> o;
           bool dg;
+#ifdef CDMS_XP_CHEAP_SETUP  // experiment build only: trivial phasors (wrong results) to price the set-up
+          o.Ar = f.E0r; o.Ai = f.E0i; o.wr = f.Whr; o.wi = f.Whi; o.Zr = f.Zhr; o.Zi = f.Zhi; o.delta = f.hx * v[0];
+          dg = false;
+#else
           setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
+#endif
           deg_any |= dg;
           Ar[s] = o.Ar; Ai[s] = o.Ai; wr[s] = o.wr; wi[s] = o.wi; Zr[s] = o.Zr; Zi[s] = o.Zi;
           const int o_ = (s * NWARP + warp) * TILE_P + lane;
@@ -525,11 +540,17 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
           const int k1 = min(k0 + SEG, k_end);
           const float4* yk = yb + (k1 - 1 - k_begin);  // Horner runs from the top subcarrier down
           H.reset_to(yk[0]);                            // acc = y_top (= 0 * w + y_top)
+#ifdef CDMS_XP_SKIP_HORNER  // experiment build only (wrong results): price everything but the Horner steps
+          if (false) {
+#else
           if (k1 - k0 == SEG) {
+#endif
 #pragma unroll 7
             for (int i = 1; i < SEG; ++i) H.step(yk[-i]);
           } else {
+#ifndef CDMS_XP_SKIP_HORNER
             for (int i = 1; i < k1 - k0; ++i) H.step(yk[-i]);
+#endif
           }
           // c += A_seg H_seg (thread-private slot), A_seg <- A_seg Z
           RT hr[S], hi[S];
@@ -566,7 +587,11 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
       // ---- (4b) spherical / planar WB Gram terms (row A4) over the block's antennas:
       //   sum_m e^{j 2 pi (D_a,m - D_b,m) fc/c} D_N((d_a,m - d_b,m) df/c); the base carrier e^{j 2 pi dR fc/c}
       //   is applied in fp64 at the hand-off (shared by all antennas: its rounding must not repeat)
+#ifdef CDMS_XP_SKIP_GRAM  // experiment build only (wrong results): price the per-antenna Gram terms
+      if (false) {
+#else
       if (!nb_mode) {
+#endif
         for (int q = (warp - mb - S) & (NWARP - 1); q < NPAIR; q += NWARP) {
           int pa, pb;
           pair_ab(q, S, pa, pb);

@@ -40,14 +40,54 @@ def fp32_peak_tflops(mhz: float) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled during the timed region: NVML polled every ~2 ms by a thread
+    (short timed regions still get samples), nvidia-smi -lms 100 as the fallback when NVML is unavailable."""
+
+    NVML_BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
-        self.index = index
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        self.index = int(ids[index]) if index < len(ids) and ids[index].isdigit() else index
         self.rows = []
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
+
+    def _sample_nvml(self, nv, h) -> bool:
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        except Exception:
+            return False
+        self.rows.append([str(sm), str(mx), ""] +
+                         ["Active" if rs & self.NVML_BITS[k] else "Not Active"
+                          for k in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")])
+        return True
+
+    def mark(self):
+        """One synchronous sample (call while the timed work is still queued on the GPU)."""
+        if self.nvml is not None:
+            self._sample_nvml(self.nvml, self.h)
+
+    def _poll_nvml(self, nv, h):
+        while not self.stop.is_set() and self._sample_nvml(nv, h):
+            self.stop.wait(0.002)
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = nv
+            self.h = h
+            self.t = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -68,6 +108,10 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self.stop.set()
+            self.t.join(timeout=1)
+            return
         if self.proc:
             self.proc.terminate()
             try:
@@ -83,7 +127,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def dist_env():
@@ -170,6 +214,9 @@ def run_cdms(args):
             ev[n][0].record(stream)
             step(args.warmup + n)
             ev[n][1].record(stream)
+            if n == args.steps // 2:
+                clk.mark()
+        clk.mark()
         barrier()
     st = ctx.sync(raise_on_error=False)
     gpu_launches = ctx.launch_count() - launches0
@@ -181,7 +228,8 @@ def run_cdms(args):
     if world > 1:
         torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
     ms_per_step = tot[0].item() / args.steps
-    kernel_ms = tot[1].item() / max(k_n, 1)
+    kernel_ms = tot[1].item() / max(k_n, 1)               # average corr_kernel launch
+    launches_per_step = max(k_n, 1) / args.steps           # > 1 when the terms budget batches the particles
 
     # ---- end to end: host measurement in, host estimate out, through the public API
     y_host = torch.empty(y.shape, dtype=torch.complex64, pin_memory=True)
@@ -211,7 +259,9 @@ def run_cdms(args):
     result = None
     if rank == 0:
         clocks = clk.summary()
-        flop_launch = 8.0 * cfg.Nz * P_local * cfg.J * cfg.S
+        # algorithmic flops of an average launch: 8 N_z flop per (particle, PA, component) unit,
+        # P_local J S units per step spread over launches_per_step launches
+        flop_launch = 8.0 * cfg.Nz * P_local * cfg.J * cfg.S / launches_per_step
         achieved = flop_launch / (kernel_ms / 1e3) / 1e12
         peak = fp32_peak_tflops(1965.0)
         roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
@@ -220,8 +270,13 @@ def run_cdms(args):
                 "frac_at_measured_clock": (round(achieved / fp32_peak_tflops(clocks["sm_mhz"]), 4)
                                            if clocks.get("sm_mhz") else None),
                 "kernel": "cdms::corr_kernel (row A2-A5: responses, correlation c, Gram G)", "kernel_ms": round(kernel_ms, 4),
-                "kernel_share_of_step": round(kernel_ms / ms_per_step, 4),
-                "flop_per_launch": flop_launch, "traffic": traffic_from_profiles(args.config)}
+                "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
+                "launches_per_step": launches_per_step,
+                "flop_per_launch": flop_launch,
+                "traffic": (traffic_from_profiles(args.config) if args.particles is None and args.wavefront == "spherical"
+                            and args.precision == "fp32" else None),
+                "traffic_basis": "dram read+write bytes of one corr_kernel launch, ncu --set full "
+                                 "(profiles/loglik_traffic.json); the kernel is FP32-bound, traffic is particles + y"}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -247,10 +302,13 @@ def run_cdms(args):
 
 
 def traffic_from_profiles(config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one corr_kernel launch of this config from the committed
+    ncu --set full capture (tools/ncu_traffic.py), or None."""
     p = os.path.join(ROOT, "profiles", "loglik_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(config)
+            rec = json.load(f).get(config)
+        return None if rec is None else rec["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -320,7 +378,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(scenes.CONFIGS))
     ap.add_argument("--particles", type=int, default=None, help="particles per GPU (default: the config's P)")

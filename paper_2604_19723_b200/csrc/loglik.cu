@@ -211,13 +211,14 @@ struct Horner<S, double> {
 };
 
 // ---------------------------------------------------------------------------- shared memory plan
-// y chunk length per S: 128 subcarriers while 3 CTAs fit, else 64 (S >= 6) so the fp32 kernel keeps 3 CTAs
-// (24 warps) per SM for S <= 7 -- the FFMA2 Horner needs >= 4 warps per SMSP.
+// y chunk length (subcarriers per TMA chunk and warp).  With 128 the plan gives 3 CTAs (24 warps) per SM for
+// S <= 5 and 2 CTAs (128 registers, no spills) for S >= 6; 64 would fit 3 CTAs for S = 6, 7 but at 80
+// registers with spills, measured ~1% slower on c3 / c5.
 __host__ __device__ constexpr int kchunk_for(int S) {
 #ifdef CDMS_KCHUNK_ALL
   return CDMS_KCHUNK_ALL + 0 * S;
 #else
-  return S <= 5 ? 128 : 64;
+  return 128 + 0 * S;  // measured: S = 6, 7 run better at 2 CTAs x 128 registers than at 3 CTAs with spills
 #endif
 }
 
@@ -241,8 +242,13 @@ struct Plan {
   // capped so that each thread keeps >= 80 registers (the Horner state + phasors of S <= 7 without spills)
   static constexpr int smem_fit = (int)((228 * 1024) / (total + 1024));
   static constexpr int reg_fit = 65536 / (NTHREADS * 80);
+#ifdef CDMS_XP_MINB_BIG_S  // experiment builds: force the CTAs per SM of S >= 6
+  static constexpr int min_blocks = (sizeof(RT) == 8) ? 1 : (S >= 6 ? CDMS_XP_MINB_BIG_S
+                                                                   : (smem_fit < reg_fit ? smem_fit : reg_fit));
+#else
   static constexpr int min_blocks =
       (sizeof(RT) == 8) ? 1 : (smem_fit < reg_fit ? (smem_fit < 1 ? 1 : smem_fit) : reg_fit);
+#endif
 };
 
 size_t corr_smem_bytes(int S, int precision) {

@@ -7,8 +7,8 @@
 // K1b assemble_kernel<S>: one thread per particle, fp64: the S x S low-rank evaluation of the MT update
 // message iota~ (Supplement S-V-C), summed over the PAs.
 //
-// K1 work decomposition: CTA = 32 particles (lanes) x 8 antennas (warps), persistent grid; each CTA takes a
-// contiguous range of (tile, PA, antenna block) units (tail balance, see corr_kernel).  For each PA and
+// K1 work decomposition: CTA = 32 particles (lanes) x 8 antennas (warps), persistent grid; CTAs claim
+// (tile, PA) groups dynamically (see corr_kernel).  For each PA and
 // each block of 8 antennas, y^(j) streams through shared memory in chunks of <= 128 subcarriers x 8 antennas
 // by 1-D bulk TMA (cp.async.bulk, mbarrier, double buffered), stored as (yr, yr, yi, yi) so one broadcast
 // LDS.128 feeds FFMA2 (fma.rn.f32x2) Horner steps that advance two components per instruction.  Per

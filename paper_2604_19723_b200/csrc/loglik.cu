@@ -242,7 +242,9 @@ struct Plan {
   // capped so that each thread keeps >= 80 registers (the Horner state + phasors of S <= 7 without spills)
   static constexpr int smem_fit = (int)((228 * 1024) / (total + 1024));
   static constexpr int reg_fit = 65536 / (NTHREADS * 80);
-#ifdef CDMS_XP_MINB_BIG_S  // experiment builds: force the CTAs per SM of S >= 6
+#if defined(CDMS_XP_MINB_ALL)  // experiment builds: force the CTAs per SM (registers follow)
+  static constexpr int min_blocks = (sizeof(RT) == 8) ? 1 : CDMS_XP_MINB_ALL;
+#elif defined(CDMS_XP_MINB_BIG_S)  // experiment builds: force the CTAs per SM of S >= 6
   static constexpr int min_blocks = (sizeof(RT) == 8) ? 1 : (S >= 6 ? CDMS_XP_MINB_BIG_S
                                                                    : (smem_fit < reg_fit ? smem_fit : reg_fit));
 #else
@@ -693,22 +695,18 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
 }
 
 // ---------------------------------------------------------------------------- K1b assembly (row A5)
-// One thread per particle, fp64, vectors / matrix in shared-memory columns [item][ASM_T]:
+// One thread per particle, fp64, everything in registers (S is a compile-time constant and every loop is
+// unrolled, so the Hermitian S x S matrix lives in NTRI complex registers):
 //   g = c - G m; ||e||^2 = ||z||^2 - 2 Re(m^H c) + m^H G m; K = I + V^1/2 G V^1/2 / eta = L L^H;
 //   x = L^-1 V^1/2 g; l_j = -Nz ln(pi eta) - 2 sum ln L_ii - ||e||^2/eta + ||x||^2/eta^2;
 //   amplitudes: m + V^1/2 L^-H x / eta (LMMSE).
-constexpr int ASM_T = 32;
+constexpr int ASM_T = 128;
 
 template <int S>
 __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__ SceneDev sc, const AsmArgs a) {
   constexpr int NTRI = S * (S + 1) / 2;
   constexpr int T = S + NTRI;
-  __shared__ double2 sh[(2 * S + NTRI) * ASM_T];
-  double2* wc = sh;                 // [S][ASM_T]
-  double2* wv = sh + S * ASM_T;     // [S][ASM_T]
-  double2* wk = sh + 2 * S * ASM_T; // [NTRI][ASM_T]
-  const int ln = threadIdx.x;
-  const int64_t p = (int64_t)blockIdx.x * ASM_T + ln;
+  const int64_t p = (int64_t)blockIdx.x * ASM_T + threadIdx.x;
   if (p >= a.P) return;
   const int J = sc.J;
   const double nz = (double)sc.nf * (double)sc.Na;
@@ -716,113 +714,115 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
   for (int j = 0; j < J; ++j) {
     const double2* tp = a.terms + (p * J + j) * T;
     const double eta = sc.eta[j];
-#pragma unroll 1
-    for (int s = 0; s < S; ++s) wc[s * ASM_T + ln] = tp[s];
-#pragma unroll 1
-    for (int t = 0; t < NTRI; ++t) wk[t * ASM_T + ln] = tp[S + t];
+    double2 c[S], k[NTRI];
+#pragma unroll
+    for (int s = 0; s < S; ++s) c[s] = tp[s];
+#pragma unroll
+    for (int t = 0; t < NTRI; ++t) k[t] = tp[S + t];  // lower triangle of G: k[tri(r, c)] = G_rc, r >= c
     if (a.term_c != nullptr) {
-#pragma unroll 1
+#pragma unroll
       for (int r = 0; r < S; ++r) {
-        a.term_c[(p * J + j) * S + r] = wc[r * ASM_T + ln];
-#pragma unroll 1
-        for (int c = 0; c < S; ++c) {
-          double2 G = (r >= c) ? wk[tri(r, c) * ASM_T + ln] : wk[tri(c, r) * ASM_T + ln];
-          if (r < c) G.y = -G.y;
-          a.term_G[((p * J + j) * S + r) * S + c] = G;
+        a.term_c[(p * J + j) * S + r] = c[r];
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          double2 G = (r >= q) ? k[tri(r, q)] : k[tri(q, r)];
+          if (r < q) G.y = -G.y;
+          a.term_G[((p * J + j) * S + r) * S + q] = G;
         }
       }
     }
+    double sv[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) sv[s] = sqrt(sc.v[j][s]);
+    // Gm, m^H c, m^H G m and b = V^1/2 (c - G m)
     double mhc = 0.0, mGm = 0.0;
-#pragma unroll 1
+    double2 b[S];
+#pragma unroll
     for (int r = 0; r < S; ++r) {
-      const double2 c = wc[r * ASM_T + ln];
       double gmr = 0.0, gmi = 0.0;
-#pragma unroll 1
-      for (int t = 0; t < S; ++t) {
-        double2 G = (r >= t) ? wk[tri(r, t) * ASM_T + ln] : wk[tri(t, r) * ASM_T + ln];
-        if (r < t) G.y = -G.y;
-        const double mr = sc.m_re[j][t], mi = sc.m_im[j][t];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        double2 G = (r >= q) ? k[tri(r, q)] : k[tri(q, r)];
+        if (r < q) G.y = -G.y;
+        const double mr = sc.m_re[j][q], mi = sc.m_im[j][q];
         gmr += G.x * mr - G.y * mi;
         gmi += G.x * mi + G.y * mr;
       }
       const double mr = sc.m_re[j][r], mi = sc.m_im[j][r];
-      mhc += mr * c.x + mi * c.y;
+      mhc += mr * c[r].x + mi * c[r].y;
       mGm += mr * gmr + mi * gmi;
-      const double sv = sqrt(sc.v[j][r]);
-      wv[r * ASM_T + ln] = make_double2(sv * (c.x - gmr), sv * (c.y - gmi));  // b = V^1/2 g
+      b[r] = make_double2(sv[r] * (c[r].x - gmr), sv[r] * (c[r].y - gmi));
     }
     const double e2 = a.ynorm2[j] - 2.0 * mhc + mGm;
-#pragma unroll 1
+    // K = I + V^1/2 G V^1/2 / eta, in place, then its Cholesky factor L (lower, in place)
+#pragma unroll
     for (int r = 0; r < S; ++r)
-#pragma unroll 1
-      for (int t = 0; t <= r; ++t) {
-        const double f = sqrt(sc.v[j][r]) * sqrt(sc.v[j][t]) / eta;
-        const double2 G = wk[tri(r, t) * ASM_T + ln];
-        wk[tri(r, t) * ASM_T + ln] = make_double2((r == t ? 1.0 : 0.0) + G.x * f, G.y * f);
+#pragma unroll
+      for (int q = 0; q <= r; ++q) {
+        const double f = sv[r] * sv[q] / eta;
+        const double2 G = k[tri(r, q)];
+        k[tri(r, q)] = make_double2((r == q ? 1.0 : 0.0) + G.x * f, G.y * f);
       }
     double logdet = 0.0;
     bool okc = true;
-#pragma unroll 1
+#pragma unroll
     for (int q = 0; q < S; ++q) {
-      double d = wk[tri(q, q) * ASM_T + ln].x;
-#pragma unroll 1
-      for (int k = 0; k < q; ++k) {
-        const double2 lq = wk[tri(q, k) * ASM_T + ln];
-        d -= lq.x * lq.x + lq.y * lq.y;
-      }
+      double d = k[tri(q, q)].x;
+#pragma unroll
+      for (int t = 0; t < q; ++t) d -= k[tri(q, t)].x * k[tri(q, t)].x + k[tri(q, t)].y * k[tri(q, t)].y;
       okc &= d > 0.0;
       const double lqq = sqrt(fmax(d, 1e-300));
       logdet += 2.0 * log(lqq);
-      wk[tri(q, q) * ASM_T + ln] = make_double2(lqq, 0.0);
-#pragma unroll 1
+      k[tri(q, q)] = make_double2(lqq, 0.0);
+      const double inv = 1.0 / lqq;
+#pragma unroll
       for (int i = q + 1; i < S; ++i) {
-        double2 ac = wk[tri(i, q) * ASM_T + ln];
-#pragma unroll 1
-        for (int k = 0; k < q; ++k) {
-          const double2 li = wk[tri(i, k) * ASM_T + ln], lk = wk[tri(q, k) * ASM_T + ln];
-          ac.x -= li.x * lk.x + li.y * lk.y;  // ac -= L_ik conj(L_qk)
+        double2 ac = k[tri(i, q)];
+#pragma unroll
+        for (int t = 0; t < q; ++t) {
+          const double2 li = k[tri(i, t)], lk = k[tri(q, t)];
+          ac.x -= li.x * lk.x + li.y * lk.y;  // ac -= L_it conj(L_qt)
           ac.y -= li.y * lk.x - li.x * lk.y;
         }
-        wk[tri(i, q) * ASM_T + ln] = make_double2(ac.x / lqq, ac.y / lqq);
+        k[tri(i, q)] = make_double2(ac.x * inv, ac.y * inv);
       }
     }
+    // x = L^-1 b (forward substitution), ||x||^2
     double x2 = 0.0;
-#pragma unroll 1
+#pragma unroll
     for (int r = 0; r < S; ++r) {
-      double2 b = wv[r * ASM_T + ln];
-#pragma unroll 1
-      for (int k = 0; k < r; ++k) {
-        const double2 lr = wk[tri(r, k) * ASM_T + ln], xk = wv[k * ASM_T + ln];
-        b.x -= lr.x * xk.x - lr.y * xk.y;
-        b.y -= lr.x * xk.y + lr.y * xk.x;
+      double2 t = b[r];
+#pragma unroll
+      for (int q = 0; q < r; ++q) {
+        const double2 lr = k[tri(r, q)];
+        t.x -= lr.x * b[q].x - lr.y * b[q].y;
+        t.y -= lr.x * b[q].y + lr.y * b[q].x;
       }
-      const double ld = wk[tri(r, r) * ASM_T + ln].x;
-      const double2 xr = make_double2(b.x / ld, b.y / ld);
-      wv[r * ASM_T + ln] = xr;
-      x2 += xr.x * xr.x + xr.y * xr.y;
+      const double ld = k[tri(r, r)].x;
+      b[r] = make_double2(t.x / ld, t.y / ld);
+      x2 += b[r].x * b[r].x + b[r].y * b[r].y;
     }
     double lj = -nz * log(PI * eta) - logdet - e2 / eta + x2 / (eta * eta);
     if (!okc || !(lj == lj)) lj = -INFINITY;
     l += lj;
     if (a.amp != nullptr) {
-#pragma unroll 1
+      // L^H u = x (back substitution), amplitudes m + V^1/2 u / eta
+#pragma unroll
       for (int r = S - 1; r >= 0; --r) {
-        double2 t = wv[r * ASM_T + ln];
-#pragma unroll 1
-        for (int k = r + 1; k < S; ++k) {
-          const double2 lk = wk[tri(k, r) * ASM_T + ln], xk = wv[k * ASM_T + ln];  // (L^H)_rk = conj(L_kr)
-          t.x -= lk.x * xk.x + lk.y * xk.y;
-          t.y -= lk.x * xk.y - lk.y * xk.x;
+        double2 t = b[r];
+#pragma unroll
+        for (int q = r + 1; q < S; ++q) {
+          const double2 lk = k[tri(q, r)];  // (L^H)_rq = conj(L_qr)
+          t.x -= lk.x * b[q].x + lk.y * b[q].y;
+          t.y -= lk.x * b[q].y - lk.y * b[q].x;
         }
-        const double ld = wk[tri(r, r) * ASM_T + ln].x;
-        wv[r * ASM_T + ln] = make_double2(t.x / ld, t.y / ld);
+        const double ld = k[tri(r, r)].x;
+        b[r] = make_double2(t.x / ld, t.y / ld);
       }
-#pragma unroll 1
-      for (int s = 0; s < S; ++s) {
-        const double sv = sqrt(sc.v[j][s]);
-        const double2 t = wv[s * ASM_T + ln];
-        a.amp[(p * J + j) * S + s] = make_double2(sc.m_re[j][s] + sv * t.x / eta, sc.m_im[j][s] + sv * t.y / eta);
-      }
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        a.amp[(p * J + j) * S + s] =
+            make_double2(sc.m_re[j][s] + sv[s] * b[s].x / eta, sc.m_im[j][s] + sv[s] * b[s].y / eta);
     }
   }
   const int pf = a.pflag[p];

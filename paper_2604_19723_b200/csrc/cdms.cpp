@@ -37,7 +37,7 @@ namespace {
 
 enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
-  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_COUNT
+  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -539,7 +539,8 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
   SceneDev sd;
   cdms_status st = build_scene(ctx, scene, nullptr, nullptr, nullptr, &sd);
   if (st) return st;
-  const int64_t nb = red_blocks(P_local);
+  // partial buffers sized for the finer of the two partitions (beliefs.cu RED_ITEMS, step.cu STEP_ITEMS)
+  const int64_t nb = red_blocks(P_local) > step_blocks(P_local) ? red_blocks(P_local) : step_blocks(P_local);
   float4* f4;
   double* d;
   double2* d2;
@@ -557,6 +558,7 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
     WS_TRY(ctx, WS_PFLAG, PB, &i32);
     unsigned int* sch;
     WS_TRY(ctx, WS_SCHED, 2, &sch);
+    WS_TRY(ctx, WS_STEP_CNT, 4, &sch);
     WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &f4);
   }
   WS_TRY(ctx, WS_YNORM, MAXJ, &d);
@@ -704,33 +706,98 @@ cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_partic
   // (2) coherent log-likelihood, uniform w_beta (rows A1-A5)
   st = loglik_impl(ctx, sd, scene->precision, d_particles, P_local, 6, d_sfv, 0, d_y, nullptr, l, nullptr);
   if (st) return st;
-  // (3) normalization (A6) and (4) moments (A7)
-  st = run_lse(ctx, l, P_local, d_lse);
-  if (st) return st;
-  CUDA_TRY(ctx, launch_normalize(l, P_local, scal + 0, scal + 1, ctx->d_flags, w, ctx->stream));
+  // (3)-(6) the fused O(P) pipeline (step.cu): LSE (A6), weights + quantized masses + moments (A7),
+  // scan + ancestors + gather (A8), regularization (A9).  With a communicator the collectives sit between the
+  // kernels; the combine / finalize arithmetic is the same device code either way.
+  const bool comm = ctx->comm != nullptr;
+  const int R = ctx->nranks;
+  if (P_total > ((int64_t)1 << 26)) return fail(ctx, CDMS_EINVAL, "P_total=%lld exceeds 2^26", (long long)P_total);
+  const int64_t nb = step_blocks(P_local);
+  double2 *lpart, *pairs;
+  double *mpart, *sums;
+  uint64_t *q, *bsum, *qall;
+  unsigned* cnt;
+  WS_TRY(ctx, WS_LSE_PART, nb + 1, &lpart);
+  WS_TRY(ctx, WS_LSE_RANK, R + 1, &pairs);
+  WS_TRY(ctx, WS_MOM_PART, (nb + 1) * 21, &mpart);
+  WS_TRY(ctx, WS_SUMS, 32, &sums);
+  WS_TRY(ctx, WS_Q, P_local, &q);
+  WS_TRY(ctx, WS_BSUM, nb + 2, &bsum);
+  WS_TRY(ctx, WS_QALL, 2 * R + 4, &qall);
+  WS_TRY(ctx, WS_STEP_CNT, 4, &cnt);  // zeroed at allocation, reset by each kernel's last block
+  CUDA_TRY(ctx, launch_step_lse(l, P_local, lpart, cnt + 0, comm ? pairs + R : pairs, comm ? 0 : 1, d_lse, scal + 0,
+                                scal + 1, ctx->d_flags, ctx->stream));
   ctx->launches += 1;
-  st = run_moments(ctx, d_particles, w, P_local, d_est);
-  if (st) return st;
-  // (5) systematic resampling (A8) on r_p = e^{l_p - M}, redistribution of the ancestors' states
+  if (comm) {
+    NCCL_TRY(ctx, ncclAllGather(pairs + R, pairs, 2, ncclDouble, ctx->comm, ctx->stream));
+    CUDA_TRY(ctx, launch_step_lse_combine(pairs, R, d_lse, scal + 0, scal + 1, ctx->d_flags, ctx->stream));
+    ctx->launches += 1;
+  }
+  CUDA_TRY(ctx, launch_step_post(l, d_particles, P_local, scal + 0, scal + 1, ctx->d_flags, w, q, mpart, bsum, cnt + 1,
+                                 sums, ctx->stream));
+  ctx->launches += 1;
+  if (comm) NCCL_TRY(ctx, ncclAllReduce(sums, sums, 7, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  CUDA_TRY(ctx, launch_step_scan(q, d_particles, w, P_local, bsum, sums, ctx->d_flags, mpart, cnt + 2, sums + 8,
+                                 comm ? 0 : 1, d_est, L6, ctx->d_flags, ctx->stream));
+  ctx->launches += 1;
+  if (comm) {
+    NCCL_TRY(ctx, ncclAllReduce(sums + 8, sums + 8, 21, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    CUDA_TRY(ctx, launch_step_finalize(sums, sums + 8, d_est, L6, ctx->d_flags, ctx->stream));
+    ctx->launches += 1;
+  }
+  // systematic resampling on r_p = e^{l_p - M} (C-amb-23): slots of this rank's CDF range, states gathered
+  const uint32_t u_bits = host_step_u_bits(prm->philox_key, prm->step);
   Plan plan;
-  int64_t* anc;
-  st = run_resample_core(ctx, l, P_local, host_step_u_bits(prm->philox_key, prm->step), 1, &plan, &anc);
-  if (st) return st;
+  const uint64_t* Qtot = bsum + nb;
+  const uint64_t* Ooff = nullptr;
+  if (!comm) {
+    plan.lo = 0;
+    plan.hi = P_local;
+  } else {
+    // all-gather Q_r, host plan (one small D2H + stream sync per step)
+    NCCL_TRY(ctx, ncclAllGather(bsum + nb, qall, 1, ncclUint64, ctx->comm, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_pinned, qall, sizeof(uint64_t) * R, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::vector<uint64_t> Q(ctx->h_pinned, ctx->h_pinned + R);
+    uint64_t Qt = 0;
+    for (uint64_t v : Q) Qt += v;
+    if (Qt == 0) return fail(ctx, CDMS_EZEROMASS, "all resampling weights are zero");
+    plan.lo_all.resize(R);
+    plan.hi_all.resize(R);
+    uint64_t O = 0, Omine = 0;
+    for (int r = 0; r < R; ++r) {
+      plan.lo_all[r] = slot_index(O, Qt, P_total, u_bits);
+      plan.hi_all[r] = slot_index(O + Q[r], Qt, P_total, u_bits);
+      if (r == ctx->rank) Omine = O;
+      O += Q[r];
+    }
+    plan.lo = plan.lo_all[ctx->rank];
+    plan.hi = plan.hi_all[ctx->rank];
+    ctx->h_pinned[R] = Qt;
+    ctx->h_pinned[R + 1] = Omine;
+    CUDA_TRY(ctx, cudaMemcpyAsync(qall + R, ctx->h_pinned + R, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                  ctx->stream));
+    Qtot = qall + R;
+    Ooff = qall + R + 1;
+  }
   const int64_t n = plan.hi - plan.lo;
   WS_TRY(ctx, WS_STAGE, (n > 0 ? n : 1) * 6, &stage);
-  CUDA_TRY(ctx, launch_gather(d_particles, anc, n, p0, stage, ctx->stream));
+  CUDA_TRY(ctx, launch_step_anc(q, P_local, Qtot, Ooff, plan.lo, plan.hi, P_total, u_bits, d_particles, stage,
+                                ctx->d_flags, ctx->stream));
   ctx->launches += 1;
-  if (ctx->comm) {
+  if (comm) {
     st = exchange(ctx, plan, P_local, stage, d_particles, 6);
     if (st) return st;
+    if (prm->regularize) {
+      CUDA_TRY(ctx, launch_step_reg(d_particles, d_particles, P_local, p0, P_total, L6, 1, prm->philox_key, prm->step,
+                                    ctx->stream));
+      ctx->launches += 1;
+    }
   } else {
-    CUDA_TRY(ctx, cudaMemcpyAsync(d_particles, stage, sizeof(double) * 6 * P_local, cudaMemcpyDeviceToDevice, ctx->stream));
-  }
-  // (6) regularization with the pre-resampling covariance (A9)
-  if (prm->regularize) {
-    CUDA_TRY(ctx, launch_chol6(d_est, L6, ctx->stream));
-    CUDA_TRY(ctx, launch_regularize(d_particles, P_local, p0, P_total, L6, prm->philox_key, prm->step, ctx->stream));
-    ctx->launches += 2;
+    // regularization with the pre-resampling covariance (A9), reading the staged states (no extra copy)
+    CUDA_TRY(ctx, launch_step_reg(stage, d_particles, P_local, p0, P_total, L6, prm->regularize ? 1 : 0,
+                                  prm->philox_key, prm->step, ctx->stream));
+    ctx->launches += 1;
   }
   return CDMS_OK;
 }

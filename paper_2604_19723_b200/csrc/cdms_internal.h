@@ -167,4 +167,25 @@ cudaError_t launch_regularize(double* x, int64_t P, int64_t p0, int64_t P_total,
                               uint64_t key, uint64_t step, cudaStream_t st);
 cudaError_t launch_fill_u64(uint64_t* dst, uint64_t v, int n, cudaStream_t st);
 
+// step.cu: the fused O(P) pipeline of cdms_bp_step (fixed STEP_ITEMS-particle blocks, last-block reductions)
+constexpr int STEP_ITEMS = 512;
+int64_t step_blocks(int64_t P);
+cudaError_t launch_step_lse(const double* l, int64_t P, double2* part, unsigned* cnt, double2* rank_pair, int combine,
+                            double* lse, double* M, double* logS, int* flags, cudaStream_t st);
+cudaError_t launch_step_lse_combine(const double2* per_rank, int nranks, double* lse, double* M, double* logS,
+                                    int* flags, cudaStream_t st);
+cudaError_t launch_step_post(const double* l, const double* x, int64_t P, const double* M, const double* logS,
+                             const int* flags, double* w, uint64_t* q, double* mpart, uint64_t* bsum, unsigned* cnt,
+                             double* sum1, cudaStream_t st);
+cudaError_t launch_step_scan(uint64_t* q, const double* x, const double* w, int64_t P, const uint64_t* boff,
+                             const double* sum1, const int* flags, double* mpart, unsigned* cnt, double* sum2,
+                             int finalize, double* est, double* L, int* flags_w, cudaStream_t st);
+cudaError_t launch_step_finalize(const double* sum1, const double* sum2, double* est, double* L, int* flags,
+                                 cudaStream_t st);
+cudaError_t launch_step_anc(const uint64_t* C, int64_t P_local, const uint64_t* Qtot, const uint64_t* offset,
+                            int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits, const double* x,
+                            double* out, int* flags, cudaStream_t st);
+cudaError_t launch_step_reg(const double* in, double* out, int64_t P, int64_t p0, int64_t P_total, const double* L,
+                            int regularize, uint64_t key, uint64_t step, cudaStream_t st);
+
 }  // namespace cdms

@@ -1,0 +1,495 @@
+// step.cu -- the O(P) part of cdms_bp_step (rows A6-A9) as a fused pipeline of five kernels:
+//   K_lse   per-block (max l, sum e^{l - max}); the last block to finish reduces the partials in a fixed
+//           order and, without a communicator, combines them into (M, ln S, lse)
+//   K_post  one pass over the particles: w = e^{(l - M) - ln S}, q = rint(ldexp(e^{l - M}, 36)) (C-amb-15, 23),
+//           first-moment partials [sum w, sum w x]; block sums of q.  Last block: the fixed-order moment sum
+//           and the exclusive scan of the block sums of q
+//   K_scan  inclusive scan C of q (block offset + local scan); second-moment partials sum w (x - mu)(x - mu)^T.
+//           Last block (no communicator): est and the Cholesky factor of its covariance (C-amb-16)
+//   K_anc   per output slot: ancestor = min{p : C_p > t_i} with the exact 128-bit t_i, gather of the state
+//
+//   K_reg   x = staged state + h chol(Sigma) n (Philox streams 1, 2), or a plain copy
+// Block partitions are fixed (STEP_ITEMS particles per block) and every cross-block reduction runs in a fixed
+// order in the last block, so results depend only on P, never on scheduling.  With a communicator the host
+// inserts the NCCL collectives between the kernels and runs the same combine / finalize device code.
+#include <math.h>
+
+#include "cdms_internal.h"
+
+namespace cdms {
+
+constexpr int STEP_BLOCK = 256;
+constexpr int STEP_PER = STEP_ITEMS / STEP_BLOCK;  // contiguous particles per thread
+static_assert(STEP_ITEMS % STEP_BLOCK == 0, "STEP_ITEMS");
+
+int64_t step_blocks(int64_t P) { return P <= 0 ? 0 : (P + STEP_ITEMS - 1) / STEP_ITEMS; }
+
+// ---------------------------------------------------------------------------- helpers
+// Fixed-order block sum of N doubles per thread: warp tree by shuffles, then the 8 warp results in order.
+template <int N>
+__device__ __forceinline__ void block_sum(double (&v)[N], double* sh /* [8][N] */, double* out /* [N] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) sh[warp * N + k] = v[k];
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < N) {
+    double s = 0.0;
+    for (int w = 0; w < STEP_BLOCK / 32; ++w) s += sh[w * N + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// Arrive on the grid-wide counter; true in the last block to arrive (which then owns the fixed-order
+// cross-block reduction and resets the counter for the next launch).
+__device__ __forceinline__ bool last_block(unsigned* cnt) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) am_last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *cnt = 0u;
+  }
+  return am_last;
+}
+
+// Column sums of part[nb][N] (b ascending within each thread's stride, then a fixed tree): deterministic.
+template <int N>
+__device__ void sum_columns(const double* part, int64_t nb, double* sh /* [STEP_BLOCK] */, double* out) {
+  for (int c = 0; c < N; ++c) {
+    double s = 0.0;
+    for (int64_t b = threadIdx.x; b < nb; b += STEP_BLOCK) s += __ldcg(&part[b * N + c]);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = STEP_BLOCK / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = sh[0];
+    __syncthreads();
+  }
+}
+
+// Ranks' (M_r, S_r) in rank order -> lse, M, ln S, flags (the same code with and without a communicator)
+__device__ void lse_combine_dev(const double2* per_rank, int nranks, double* lse, double* Mout, double* logS,
+                                int* flags) {
+  double M = -INFINITY;
+  bool nan = false;
+  for (int r = 0; r < nranks; ++r) {
+    nan |= !(per_rank[r].x == per_rank[r].x) || !(per_rank[r].y == per_rank[r].y);
+    M = fmax(M, per_rank[r].x);
+  }
+  double S = 0.0;
+  if (M > -INFINITY)
+    for (int r = 0; r < nranks; ++r)
+      if (per_rank[r].x > -INFINITY) S += per_rank[r].y * exp(per_rank[r].x - M);
+  if (nan) {
+    atomicOr(flags, FLAG_NAN);
+    *lse = NAN;
+  } else if (!(M > -INFINITY) || !(S > 0.0)) {
+    atomicOr(flags, FLAG_ZEROMASS);
+    *lse = -INFINITY;
+  } else {
+    *lse = M + log(S);
+  }
+  *Mout = M;
+  *logS = (S > 0.0) ? log(S) : -INFINITY;
+}
+
+// est = [sum w, mean (6), covariance upper triangle (21)] and L = chol(Sigma + 1e-12 tr(Sigma) I)
+__device__ void finalize_dev(const double* sum1, const double* sum2, double* est, double* L, int* flags) {
+  const double sw = sum1[0];
+  if (!(sw > 0.0)) atomicOr(flags, FLAG_ZEROMASS);
+  est[0] = sw;
+  for (int a = 0; a < 6; ++a) est[1 + a] = sum1[1 + a] / sw;
+  for (int t = 0; t < 21; ++t) est[7 + t] = sum2[t] / sw;
+  if (L == nullptr) return;
+  double Sg[36];
+  int t = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) {
+      Sg[a * 6 + b] = est[7 + t];
+      Sg[b * 6 + a] = est[7 + t];
+      ++t;
+    }
+  double tr = 0.0;
+  for (int a = 0; a < 6; ++a) tr += Sg[a * 6 + a];
+  for (int a = 0; a < 6; ++a) Sg[a * 6 + a] += 1e-12 * tr;
+  double Lr[36];
+  for (int i = 0; i < 36; ++i) Lr[i] = 0.0;
+  for (int j = 0; j < 6; ++j) {
+    double d = Sg[j * 6 + j];
+    for (int k = 0; k < j; ++k) d -= Lr[j * 6 + k] * Lr[j * 6 + k];
+    if (!(d > 0.0)) continue;
+    const double lj = sqrt(d);
+    Lr[j * 6 + j] = lj;
+    for (int i = j + 1; i < 6; ++i) {
+      double acc = Sg[i * 6 + j];
+      for (int k = 0; k < j; ++k) acc -= Lr[i * 6 + k] * Lr[j * 6 + k];
+      Lr[i * 6 + j] = acc / lj;
+    }
+  }
+  for (int i = 0; i < 36; ++i) L[i] = Lr[i];
+}
+
+// ---------------------------------------------------------------------------- K_lse
+__global__ void __launch_bounds__(STEP_BLOCK) step_lse_kernel(const double* __restrict__ l, int64_t P,
+                                                             double2* __restrict__ part, unsigned* cnt,
+                                                             double2* rank_pair, int combine, double* lse,
+                                                             double* M, double* logS, int* flags) {
+  __shared__ double sh[STEP_BLOCK];
+  const int64_t base = (int64_t)blockIdx.x * STEP_ITEMS + threadIdx.x * STEP_PER;
+  double v[STEP_PER];
+  double m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < STEP_PER; ++i) {
+    v[i] = (base + i < P) ? l[base + i] : -INFINITY;
+    m = fmax(m, v[i]);
+  }
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = STEP_BLOCK / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  const double Mb = sh[0];
+  __syncthreads();
+  double s = 0.0;
+  if (Mb > -INFINITY) {
+#pragma unroll
+    for (int i = 0; i < STEP_PER; ++i)
+      if (base + i < P) s += exp(v[i] - Mb);
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = STEP_BLOCK / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(Mb, sh[0]);
+  if (!last_block(cnt)) return;
+  // fixed-order combine of the block partials -> this rank's (M_r, S_r)
+  const int64_t nb = gridDim.x;
+  double mm = -INFINITY;
+  for (int64_t b = threadIdx.x; b < nb; b += STEP_BLOCK) mm = fmax(mm, __ldcg(&part[b].x));
+  sh[threadIdx.x] = mm;
+  __syncthreads();
+  for (int o = STEP_BLOCK / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  const double Mr = sh[0];
+  __syncthreads();
+  double ss = 0.0;
+  if (Mr > -INFINITY)
+    for (int64_t b = threadIdx.x; b < nb; b += STEP_BLOCK) {
+      const double2 q = __ldcg(&part[b]);
+      if (q.x > -INFINITY) ss += q.y * exp(q.x - Mr);
+    }
+  sh[threadIdx.x] = ss;
+  __syncthreads();
+  for (int o = STEP_BLOCK / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *rank_pair = make_double2(Mr, sh[0]);
+    if (combine) lse_combine_dev(rank_pair, 1, lse, M, logS, flags);
+  }
+}
+
+__global__ void step_lse_combine_kernel(const double2* per_rank, int nranks, double* lse, double* M, double* logS,
+                                        int* flags) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) lse_combine_dev(per_rank, nranks, lse, M, logS, flags);
+}
+
+// ---------------------------------------------------------------------------- K_post
+__global__ void __launch_bounds__(STEP_BLOCK) step_post_kernel(const double* __restrict__ l,
+                                                              const double* __restrict__ x, int64_t P,
+                                                              const double* __restrict__ Mp,
+                                                              const double* __restrict__ logSp, const int* flags,
+                                                              double* __restrict__ w, uint64_t* __restrict__ q,
+                                                              double* __restrict__ mpart, uint64_t* __restrict__ bsum,
+                                                              unsigned* cnt, double* __restrict__ sum1) {
+  __shared__ double sh[STEP_BLOCK * 4];
+  __shared__ double red[8];
+  __shared__ uint64_t shq[STEP_BLOCK];
+  const bool bad = (*flags & (FLAG_ZEROMASS | FLAG_NAN)) != 0;
+  const double M = *Mp, ls = *logSp;
+  const int64_t base = (int64_t)blockIdx.x * STEP_ITEMS + threadIdx.x * STEP_PER;
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  uint64_t qs = 0;
+#pragma unroll
+  for (int i = 0; i < STEP_PER; ++i) {
+    const int64_t p = base + i;
+    if (p >= P) continue;
+    const double d = l[p] - M;
+    const double wp = exp(d - ls);
+    if (!bad) w[p] = wp;
+    double r = exp(d);
+    if (!(r >= 0.0)) r = 0.0;
+    const uint64_t qp = (uint64_t)rint(scalbn(r, 36));
+    q[p] = qp;
+    qs += qp;
+    const double wa = bad ? 0.0 : wp;
+    acc[0] += wa;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) acc[1 + a] += wa * x[p * 6 + a];
+  }
+  block_sum<7>(acc, sh, red);
+  if (threadIdx.x < 7) mpart[blockIdx.x * 7 + threadIdx.x] = red[threadIdx.x];
+  // block total of q (exact)
+  shq[threadIdx.x] = qs;
+  __syncthreads();
+  for (int o = STEP_BLOCK / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) shq[threadIdx.x] += shq[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bsum[blockIdx.x] = shq[0];
+  if (!last_block(cnt)) return;
+  const int64_t nb = gridDim.x;
+  sum_columns<7>(mpart, nb, sh, sum1);
+  // exclusive scan of the block totals in place; bsum[nb] = Q (this rank)
+  const int64_t chunk = (nb + STEP_BLOCK - 1) / STEP_BLOCK;
+  const int64_t b0 = threadIdx.x * chunk, b1 = min(nb, b0 + chunk);
+  uint64_t run = 0;
+  for (int64_t b = b0; b < b1; ++b) run += __ldcg(&bsum[b]);
+  shq[threadIdx.x] = run;
+  __syncthreads();
+  for (int off = 1; off < STEP_BLOCK; off <<= 1) {  // Hillis-Steele inclusive scan of the thread totals
+    const uint64_t add = ((int)threadIdx.x >= off) ? shq[threadIdx.x - off] : 0ull;
+    __syncthreads();
+    shq[threadIdx.x] += add;
+    __syncthreads();
+  }
+  uint64_t ex = (threadIdx.x > 0) ? shq[threadIdx.x - 1] : 0ull;
+  for (int64_t b = b0; b < b1; ++b) {
+    const uint64_t v = __ldcg(&bsum[b]);
+    bsum[b] = ex;
+    ex += v;
+  }
+  if (threadIdx.x == STEP_BLOCK - 1) bsum[nb] = shq[STEP_BLOCK - 1];
+}
+
+// ---------------------------------------------------------------------------- K_scan
+__global__ void __launch_bounds__(STEP_BLOCK) step_scan_kernel(uint64_t* __restrict__ q, const double* __restrict__ x,
+                                                              const double* __restrict__ w, int64_t P,
+                                                              const uint64_t* __restrict__ boff,
+                                                              const double* __restrict__ sum1, const int* flags,
+                                                              double* __restrict__ mpart, unsigned* cnt,
+                                                              double* __restrict__ sum2, int finalize,
+                                                              double* est, double* L, int* flags_w) {
+  __shared__ double sh[STEP_BLOCK * 21 / 8 + 32];
+  __shared__ double red[24];
+  __shared__ uint64_t shq[STEP_BLOCK];
+  const bool bad = (*flags & (FLAG_ZEROMASS | FLAG_NAN)) != 0;
+  const int64_t base = (int64_t)blockIdx.x * STEP_ITEMS + threadIdx.x * STEP_PER;
+  // inclusive scan: thread-contiguous runs, Hillis-Steele over the thread totals, + block offset
+  uint64_t v[STEP_PER];
+  uint64_t run = 0;
+#pragma unroll
+  for (int i = 0; i < STEP_PER; ++i) {
+    run += (base + i < P) ? q[base + i] : 0ull;
+    v[i] = run;
+  }
+  shq[threadIdx.x] = run;
+  __syncthreads();
+  for (int off = 1; off < STEP_BLOCK; off <<= 1) {
+    const uint64_t add = ((int)threadIdx.x >= off) ? shq[threadIdx.x - off] : 0ull;
+    __syncthreads();
+    shq[threadIdx.x] += add;
+    __syncthreads();
+  }
+  const uint64_t ex = ((threadIdx.x > 0) ? shq[threadIdx.x - 1] : 0ull) + boff[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < STEP_PER; ++i)
+    if (base + i < P) q[base + i] = v[i] + ex;
+  // second moments about the global mean
+  double mu[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) mu[a] = sum1[1 + a] / sum1[0];
+  double acc[21];
+#pragma unroll
+  for (int t = 0; t < 21; ++t) acc[t] = 0.0;
+#pragma unroll
+  for (int i = 0; i < STEP_PER; ++i) {
+    const int64_t p = base + i;
+    if (p >= P || bad) continue;
+    const double wp = w[p];
+    double d[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) d[a] = x[p * 6 + a] - mu[a];
+    int t = 0;
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+      for (int b = a; b < 6; ++b) acc[t++] += wp * d[a] * d[b];
+  }
+  block_sum<21>(acc, sh, red);
+  if (threadIdx.x < 21) mpart[blockIdx.x * 21 + threadIdx.x] = red[threadIdx.x];
+  if (!last_block(cnt)) return;
+  sum_columns<21>(mpart, gridDim.x, sh, sum2);
+  __syncthreads();
+  if (finalize && threadIdx.x == 0) {
+    __threadfence_block();
+    finalize_dev(sum1, sum2, est, L, flags_w);
+  }
+}
+
+__global__ void step_finalize_kernel(const double* sum1, const double* sum2, double* est, double* L, int* flags) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) finalize_dev(sum1, sum2, est, L, flags);
+}
+
+// ---------------------------------------------------------------------------- K_anc (+ gather)
+// Local output slot i (global slot g = slot_lo + i): t_g = floor((u + g 2^32) Q / (P_total 2^32));
+// ancestor = min{p : C_p > t_g - O_r}; out[i] = x[ancestor] (6 doubles; one thread per slot).
+__global__ void step_anc_kernel(const uint64_t* __restrict__ C, int64_t P_local, const uint64_t* __restrict__ Qtot,
+                                const uint64_t* __restrict__ offset, int64_t slot_lo, int64_t n, int64_t P_total,
+                                uint32_t u_bits, const double* __restrict__ x, double* __restrict__ out, int* flags) {
+  const uint64_t Q = *Qtot;
+  const uint64_t O = offset ? *offset : 0ull;
+  if (Q == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, FLAG_ZEROMASS);
+    return;
+  }
+  const unsigned __int128 den = (unsigned __int128)(uint64_t)P_total << 32;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = (uint64_t)(slot_lo + i);
+    const unsigned __int128 num = ((unsigned __int128)u_bits + ((unsigned __int128)g << 32)) * Q;
+    const uint64_t t = (uint64_t)(num / den) - O;
+    int64_t lo = 0, hi = P_local - 1;  // smallest p with C[p] > t
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (C[mid] > t) hi = mid; else lo = mid + 1;
+    }
+    const double2* src = reinterpret_cast<const double2*>(x + lo * 6);
+    double2* dst = reinterpret_cast<double2*>(out + i * 6);
+    dst[0] = src[0];
+    dst[1] = src[1];
+    dst[2] = src[2];
+  }
+}
+
+// ---------------------------------------------------------------------------- K_reg
+// Philox4x32-10 and Box-Muller exactly as beliefs.cu (streams 1, 2 of the global slot index).
+__device__ __forceinline__ uint4 philox_step(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+__device__ __forceinline__ void normals4_step(uint64_t key, uint64_t step, uint64_t index, uint32_t stream,
+                                              double n[4]) {
+  const uint4 x = philox_step(make_uint4((uint32_t)index, (uint32_t)(index >> 32), (uint32_t)step, stream),
+                              make_uint2((uint32_t)key, (uint32_t)(key >> 32)));
+  const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double ua = ((double)xs[2 * h] + 0.5) * 0x1p-32;
+    const double ub = ((double)xs[2 * h + 1] + 0.5) * 0x1p-32;
+    const double r = sqrt(-2.0 * log(ua));
+    n[2 * h] = r * cos(2.0 * PI * ub);
+    n[2 * h + 1] = r * sin(2.0 * PI * ub);
+  }
+}
+
+// out[p] = in[p] + h L n_p (regularize) or in[p]; in may equal out
+__global__ void step_reg_kernel(const double* in, double* out, int64_t P, int64_t p0, double h,
+                                const double* __restrict__ Lg, int regularize, uint64_t key, uint64_t step) {
+  __shared__ double L[36];
+  if (threadIdx.x < 36) L[threadIdx.x] = regularize ? Lg[threadIdx.x] : 0.0;
+  __syncthreads();
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    double s[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) s[a] = in[p * 6 + a];
+    if (regularize) {
+      double n[8];
+      normals4_step(key, step, (uint64_t)(p0 + p), 1u, n);
+      normals4_step(key, step, (uint64_t)(p0 + p), 2u, n + 4);
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b <= a; ++b) acc += L[a * 6 + b] * n[b];
+        s[a] += h * acc;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 6; ++a) out[p * 6 + a] = s[a];
+  }
+}
+
+// ---------------------------------------------------------------------------- launchers
+static unsigned grid_cap(int64_t n, int threads, int cap = 8192) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+cudaError_t launch_step_lse(const double* l, int64_t P, double2* part, unsigned* cnt, double2* rank_pair, int combine,
+                            double* lse, double* M, double* logS, int* flags, cudaStream_t st) {
+  const int64_t nb = step_blocks(P);
+  step_lse_kernel<<<(unsigned)nb, STEP_BLOCK, 0, st>>>(l, P, part, cnt, rank_pair, combine, lse, M, logS, flags);
+  return cudaGetLastError();
+}
+cudaError_t launch_step_lse_combine(const double2* per_rank, int nranks, double* lse, double* M, double* logS,
+                                    int* flags, cudaStream_t st) {
+  step_lse_combine_kernel<<<1, 32, 0, st>>>(per_rank, nranks, lse, M, logS, flags);
+  return cudaGetLastError();
+}
+cudaError_t launch_step_post(const double* l, const double* x, int64_t P, const double* M, const double* logS,
+                             const int* flags, double* w, uint64_t* q, double* mpart, uint64_t* bsum, unsigned* cnt,
+                             double* sum1, cudaStream_t st) {
+  const int64_t nb = step_blocks(P);
+  step_post_kernel<<<(unsigned)nb, STEP_BLOCK, 0, st>>>(l, x, P, M, logS, flags, w, q, mpart, bsum, cnt, sum1);
+  return cudaGetLastError();
+}
+cudaError_t launch_step_scan(uint64_t* q, const double* x, const double* w, int64_t P, const uint64_t* boff,
+                             const double* sum1, const int* flags, double* mpart, unsigned* cnt, double* sum2,
+                             int finalize, double* est, double* L, int* flags_w, cudaStream_t st) {
+  const int64_t nb = step_blocks(P);
+  step_scan_kernel<<<(unsigned)nb, STEP_BLOCK, 0, st>>>(q, x, w, P, boff, sum1, flags, mpart, cnt, sum2, finalize, est,
+                                                       L, flags_w);
+  return cudaGetLastError();
+}
+cudaError_t launch_step_finalize(const double* sum1, const double* sum2, double* est, double* L, int* flags,
+                                 cudaStream_t st) {
+  step_finalize_kernel<<<1, 32, 0, st>>>(sum1, sum2, est, L, flags);
+  return cudaGetLastError();
+}
+cudaError_t launch_step_anc(const uint64_t* C, int64_t P_local, const uint64_t* Qtot, const uint64_t* offset,
+                            int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits, const double* x,
+                            double* out, int* flags, cudaStream_t st) {
+  const int64_t n = slot_hi - slot_lo;
+  if (n <= 0) return cudaSuccess;
+  step_anc_kernel<<<grid_cap(n, 256), 256, 0, st>>>(C, P_local, Qtot, offset, slot_lo, n, P_total, u_bits, x, out,
+                                                   flags);
+  return cudaGetLastError();
+}
+cudaError_t launch_step_reg(const double* in, double* out, int64_t P, int64_t p0, int64_t P_total, const double* L,
+                            int regularize, uint64_t key, uint64_t step, cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  const double h = pow(4.0 / (8.0 * (double)P_total), 1.0 / 10.0);  // h_opt, d = 6 (C-amb-16)
+  step_reg_kernel<<<grid_cap(P, 256), 256, 0, st>>>(in, out, P, p0, h, L, regularize, key, step);
+  return cudaGetLastError();
+}
+
+}  // namespace cdms

@@ -129,7 +129,10 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
   out->nf = sc->nf;
   out->wavefront = sc->wavefront;
   out->pathloss = sc->pathloss ? 1 : 0;
-  out->kc_len = sc->nf < corr_kchunk(out->S) ? sc->nf : corr_kchunk(out->S);
+  {
+    const int kc = corr_kchunk(out->S, sc->precision, sc->wavefront);
+    out->kc_len = sc->nf < kc ? sc->nf : kc;
+  }
   out->n_mb = (out->Na + NWARP - 1) / NWARP;
   out->n_kc = (sc->nf + out->kc_len - 1) / out->kc_len;
   out->dy = sc->dy;

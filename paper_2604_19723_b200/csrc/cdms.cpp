@@ -130,7 +130,7 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
   out->wavefront = sc->wavefront;
   out->pathloss = sc->pathloss ? 1 : 0;
   {
-    const int kc = corr_kchunk(out->S, sc->precision, sc->wavefront);
+    const int kc = corr_kchunk(out->S);
     out->kc_len = sc->nf < kc ? sc->nf : kc;
   }
   out->n_mb = (out->Na + NWARP - 1) / NWARP;

@@ -128,8 +128,7 @@ int64_t corr_grid(const SceneDev& sc, int64_t n_tiles, int precision, int num_sm
 cudaError_t launch_corr(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st);
 cudaError_t launch_assemble(const SceneDev& sc, const AsmArgs& a, cudaStream_t st);
 size_t corr_smem_bytes(int S, int precision);
-int corr_kchunk(int S, int precision, int wavefront);  // subcarriers per y chunk (kc_len = min(that, nf))
-bool corr_use_ws(int S, int precision, int wavefront);  // warp-specialized K1 applies
+int corr_kchunk(int S);   // subcarriers per y chunk (SceneDev::kc_len = min(corr_kchunk(S), nf))
 cudaError_t launch_response(const SceneDev& sc, const double* pos, int64_t n, const int32_t* js,
                             const double* sfv, double2* psi, int precision, int* flags, cudaStream_t st);
 cudaError_t launch_layout(const SceneDev& sc, const double* sfv, double* layout, double* va, double* H,

@@ -130,21 +130,6 @@ struct Horner<S, float> {
       wiL = wi[S - 1];
     }
   }
-  // from step phasors already packed as component pairs (the warp-specialized kernel's shared layout)
-  __device__ __forceinline__ void init_packed(const u64* wr_pairs, const u64* wi_pairs, float wr_odd, float wi_odd) {
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      wr2[q] = wr_pairs[q];
-      wi2[q] = wi_pairs[q];
-      float lo, hi;
-      up2(wi2[q], lo, hi);
-      nwi2[q] = pk2(-lo, -hi);
-    }
-    if (ODD) {
-      wrL = wr_odd;
-      wiL = wi_odd;
-    }
-  }
   __device__ __forceinline__ void reset_to(const float4 y) {
     const u64 yr2 = pk2(y.x, y.y), yi2 = pk2(y.z, y.w);
 #pragma unroll
@@ -850,22 +835,8 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
   a.loglik[p] = l;
 }
 
-#include "corr_ws.cuh"
-
 // ---------------------------------------------------------------------------- launch
-// The warp-specialized K1 (corr_ws.cuh) serves fp32, S <= 5, spherical / planar WB when CDMS_WS=1 is set in
-// the environment (opt-in: not yet faster than the plain kernel; both give identical results).
-constexpr int WS_MAX_S = 5;
-bool corr_use_ws(int S, int precision, int wavefront) {
-  static const bool enabled = [] {
-    const char* e = getenv("CDMS_WS");
-    return e != nullptr && e[0] == '1';
-  }();
-  return enabled && precision != CDMS_FP64 && S <= WS_MAX_S && wavefront != CDMS_PLANAR_NB;
-}
-int corr_kchunk(int S, int precision, int wavefront) {
-  return corr_use_ws(S, precision, wavefront) ? WS_KC : kchunk_for(S);
-}
+int corr_kchunk(int S) { return kchunk_for(S); }
 
 // Persistent grid: every resident CTA (latency hiding), at most one CTA per (tile, PA) group.  0 on error.
 template <typename K>
@@ -880,23 +851,13 @@ static int64_t grid_for_kernel(K kern, int threads, size_t smem, int64_t n_group
 }
 
 template <int S, typename RT>
-static int64_t corr_grid_t(const SceneDev& sc, int64_t n_tiles, int precision, int num_sms) {
-  if constexpr (sizeof(RT) == 4 && S <= WS_MAX_S) {
-    if (corr_use_ws(S, precision, sc.wavefront))
-      return grid_for_kernel(corr_ws_kernel<S>, WS_THREADS, WSPlan<S>::total, n_tiles * sc.J, num_sms);
-  }
+static int64_t corr_grid_t(const SceneDev& sc, int64_t n_tiles, int num_sms) {
   return grid_for_kernel(corr_kernel<S, RT>, NTHREADS, Plan<S, RT>::total, n_tiles * sc.J, num_sms);
 }
 
 template <int S, typename RT>
-static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st) {
+static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStream_t st) {
   if (a.grid < 1 || a.n_groups < 1) return cudaSuccess;
-  if constexpr (sizeof(RT) == 4 && S <= WS_MAX_S) {
-    if (corr_use_ws(S, precision, sc.wavefront)) {
-      corr_ws_kernel<S><<<(unsigned)a.grid, WS_THREADS, WSPlan<S>::total, st>>>(sc, a);
-      return cudaGetLastError();
-    }
-  }
   corr_kernel<S, RT><<<(unsigned)a.grid, NTHREADS, Plan<S, RT>::total, st>>>(sc, a);
   return cudaGetLastError();
 }
@@ -904,8 +865,8 @@ static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, int prec
 int64_t corr_grid(const SceneDev& sc, int64_t n_tiles, int precision, int num_sms) {
   switch (sc.S) {
 #define CASE_S(n) \
-  case n: return precision == CDMS_FP64 ? corr_grid_t<n, double>(sc, n_tiles, precision, num_sms) \
-                                        : corr_grid_t<n, float>(sc, n_tiles, precision, num_sms);
+  case n: return precision == CDMS_FP64 ? corr_grid_t<n, double>(sc, n_tiles, num_sms) \
+                                        : corr_grid_t<n, float>(sc, n_tiles, num_sms);
     CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
 #undef CASE_S
     default: return 0;
@@ -915,8 +876,8 @@ int64_t corr_grid(const SceneDev& sc, int64_t n_tiles, int precision, int num_sm
 cudaError_t launch_corr(const SceneDev& sc, const CorrArgs& a, int precision, cudaStream_t st) {
   switch (sc.S) {
 #define CASE_S(n) \
-  case n: return precision == CDMS_FP64 ? launch_corr_t<n, double>(sc, a, precision, st) \
-                                        : launch_corr_t<n, float>(sc, a, precision, st);
+  case n: return precision == CDMS_FP64 ? launch_corr_t<n, double>(sc, a, st) \
+                                        : launch_corr_t<n, float>(sc, a, st);
     CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
 #undef CASE_S
     default: return cudaErrorInvalidValue;

@@ -333,7 +333,7 @@ __device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const 
 
 // ---------------------------------------------------------------------------- K1
 // Work distribution: dynamic.  A group is (tile of 32 particles, PA j), g = tile J + j; thread 0 of each
-// persistent CTA claims groups from a global counter three groups ahead (ring in shared memory) so the per-warp
+// persistent CTA claims groups from a global counter one or two groups ahead (ring in shared memory) so the per-warp
 // TMA streams run across group boundaries without a stall.  Co-resident CTAs progress at different rates under
 // the warp scheduler's age priority; static partitions left ~17% of the warp slots idle (ncu warps_active 20
 // of 24), dynamic claiming keeps every slot busy until the queue drains.  Each group is computed entirely by
@@ -400,13 +400,13 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
   };
 
   if (tid < 2 * NWARP) mbar_init(&mbar[tid], 1);
-  // Claims run three groups ahead of the consumer: the issue stream (<= 2 chunks ahead) enters group gi + 2
-  // while the consumer may still be in group gi - 1 when groups hold a single chunk.
+  // Claims run L groups ahead of the consumer, as few as the TMA stream needs (it runs <= 2 chunks ahead, so it
+  // enters group gi + 1 during group gi when groups hold >= 2 chunks, gi + 2 otherwise): claimed-but-unstarted
+  // groups are exactly what the last CTAs still hold when the queue drains (c2: ~7 groups per CTA).
+  const int L = (sc.n_mb * sc.n_kc >= 2) ? 1 : 2;
   if (tid == 0) {
     fence_mbar_init();
-    gring[0] = atomicAdd(a.sched, 1u);
-    gring[1] = atomicAdd(a.sched, 1u);
-    gring[2] = atomicAdd(a.sched, 1u);
+    for (int i = 0; i < L; ++i) gring[i] = atomicAdd(a.sched, 1u);
   }
   if (tid < TILE_P) pfl[tid] = 0;
   __syncthreads();
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
 #pragma unroll
       for (int c = 0; c < 3; ++c) pos_s[c * TILE_P + lane] = pvalid ? a.particles[p * a.pstride + c] : 1.0;
     }
-    if (tid == 0) gring[(ring_i + 3) & 3] = atomicAdd(a.sched, 1u);
+    if (tid == 0) gring[(ring_i + L) & 3] = atomicAdd(a.sched, 1u);
     __syncthreads();
     PT_DECL
 

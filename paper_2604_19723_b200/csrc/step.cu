@@ -62,21 +62,20 @@ __device__ __forceinline__ bool last_block(unsigned* cnt) {
   return am_last;
 }
 
-// Column sums of part[nb][N] (b ascending within each thread's stride, then a fixed tree): deterministic.
+// Column sums of part[nb][N]: warp w takes columns c = w, w + 8, ...; lane l sums rows b = l, l + 32, ...
+// ascending, then a fixed shuffle tree -- deterministic, no block barriers.  out is visible to the block after
+// the trailing __syncthreads.
 template <int N>
-__device__ void sum_columns(const double* part, int64_t nb, double* sh /* [STEP_BLOCK] */, double* out) {
-  for (int c = 0; c < N; ++c) {
+__device__ void sum_columns(const double* part, int64_t nb, double* /*sh*/, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = warp; c < N; c += STEP_BLOCK / 32) {
     double s = 0.0;
-    for (int64_t b = threadIdx.x; b < nb; b += STEP_BLOCK) s += __ldcg(&part[b * N + c]);
-    sh[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = STEP_BLOCK / 2; o > 0; o >>= 1) {
-      if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) out[c] = sh[0];
-    __syncthreads();
+    for (int64_t b = lane; b < nb; b += 32) s += __ldcg(&part[b * N + c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) out[c] = s;
   }
+  __syncthreads();
 }
 
 // Ranks' (M_r, S_r) in rank order -> lse, M, ln S, flags (the same code with and without a communicator)
@@ -105,14 +104,16 @@ __device__ void lse_combine_dev(const double2* per_rank, int nranks, double* lse
   *logS = (S > 0.0) ? log(S) : -INFINITY;
 }
 
-// est = [sum w, mean (6), covariance upper triangle (21)] and L = chol(Sigma + 1e-12 tr(Sigma) I)
+// est = [sum w, mean (6), covariance upper triangle (21)] and L = chol(Sigma + 1e-12 tr(Sigma) I), run by one
+// full warp: lanes 0..27 form est in parallel, lane 0 then factors the 6 x 6 covariance (one reciprocal per
+// pivot).  The same code serves the single-rank kernel epilogue and the multi-rank finalize kernel.
 __device__ void finalize_dev(const double* sum1, const double* sum2, double* est, double* L, int* flags) {
+  const int lane = threadIdx.x & 31;
   const double sw = sum1[0];
-  if (!(sw > 0.0)) atomicOr(flags, FLAG_ZEROMASS);
-  est[0] = sw;
-  for (int a = 0; a < 6; ++a) est[1 + a] = sum1[1 + a] / sw;
-  for (int t = 0; t < 21; ++t) est[7 + t] = sum2[t] / sw;
-  if (L == nullptr) return;
+  if (lane == 0 && !(sw > 0.0)) atomicOr(flags, FLAG_ZEROMASS);
+  if (lane < 28) est[lane] = lane == 0 ? sw : (lane < 7 ? sum1[lane] : sum2[lane - 7]) / sw;
+  __syncwarp();
+  if (L == nullptr || lane != 0) return;
   double Sg[36];
   int t = 0;
   for (int a = 0; a < 6; ++a)
@@ -131,11 +132,12 @@ __device__ void finalize_dev(const double* sum1, const double* sum2, double* est
     for (int k = 0; k < j; ++k) d -= Lr[j * 6 + k] * Lr[j * 6 + k];
     if (!(d > 0.0)) continue;
     const double lj = sqrt(d);
+    const double inv = 1.0 / lj;
     Lr[j * 6 + j] = lj;
     for (int i = j + 1; i < 6; ++i) {
       double acc = Sg[i * 6 + j];
       for (int k = 0; k < j; ++k) acc -= Lr[i * 6 + k] * Lr[j * 6 + k];
-      Lr[i * 6 + j] = acc / lj;
+      Lr[i * 6 + j] = acc * inv;
     }
   }
   for (int i = 0; i < 36; ++i) L[i] = Lr[i];
@@ -338,15 +340,11 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_scan_kernel(uint64_t* __restr
   if (threadIdx.x < 21) mpart[blockIdx.x * 21 + threadIdx.x] = red[threadIdx.x];
   if (!last_block(cnt)) return;
   sum_columns<21>(mpart, gridDim.x, sh, sum2);
-  __syncthreads();
-  if (finalize && threadIdx.x == 0) {
-    __threadfence_block();
-    finalize_dev(sum1, sum2, est, L, flags_w);
-  }
+  if (finalize && threadIdx.x < 32) finalize_dev(sum1, sum2, est, L, flags_w);  // warp 0
 }
 
 __global__ void step_finalize_kernel(const double* sum1, const double* sum2, double* est, double* L, int* flags) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) finalize_dev(sum1, sum2, est, L, flags);
+  if (blockIdx.x == 0 && threadIdx.x < 32) finalize_dev(sum1, sum2, est, L, flags);  // launched with 32 threads
 }
 
 // ---------------------------------------------------------------------------- K_anc (+ gather)

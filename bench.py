@@ -281,13 +281,7 @@ def run_cdms(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: J={cfg.J} PAs, K={cfg.K} walls (S={cfg.S}), "
-                                   f"{cfg.ny}x{cfg.nv} URA, nf={cfg.nf}, P={P_local}/GPU",
-                       "config": args.config, "P_per_gpu": P_local, "P_total": P_local * world, "J": cfg.J,
-                       "K": cfg.K, "ny": cfg.ny, "nv": cfg.nv, "nf": cfg.nf, "Nz": cfg.Nz,
-                       "wavefront": args.wavefront, "precision": args.precision,
-                       "step": "predict+loglik+normalize+moments+resample+regularize",
-                       "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (particles)"},
+            "config": config_dict(args, cfg, P_local, world),
             "roofline": roof,
             "e2e": {"value": evals_step / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": int(y.numel() * 8), "d2h_bytes_per_step": 29 * 8},
@@ -345,6 +339,17 @@ def cpu_baseline(args, cfg, sc, budget_s: float = 15.0):
             "sample": f"oracle bp_step on {n} of {cfg.P} particles of {args.config} (fp64 C, OpenMP), {dt:.2f} s"}
 
 
+def config_dict(args, cfg, P_local, world):
+    """The workload both arms report (the reference arm times a bounded sample of it, stated in cpu_baseline)."""
+    return {"workload": f"{args.config}: J={cfg.J} PAs, K={cfg.K} walls (S={cfg.S}), "
+                        f"{cfg.ny}x{cfg.nv} URA, nf={cfg.nf}, P={P_local}/GPU",
+            "config": args.config, "P_per_gpu": P_local, "P_total": P_local * world, "J": cfg.J,
+            "K": cfg.K, "ny": cfg.ny, "nv": cfg.nv, "nf": cfg.nf, "Nz": cfg.Nz,
+            "wavefront": args.wavefront, "precision": args.precision,
+            "step": "predict+loglik+normalize+moments+resample+regularize",
+            "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (particles)"}
+
+
 def run_reference(args):
     """--impl reference: the oracle as the reference arm, on this host's cores, bounded samples."""
     world, rank, local = dist_env()
@@ -369,7 +374,7 @@ def run_reference(args):
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config} (sampled: {n} particles/step)", "config": args.config},
+            "config": config_dict(args, cfg, args.particles or cfg.P, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -5,6 +5,14 @@ import numpy as np
 
 from paper_2604_19723_b200 import scenes
 
+# Measured parity maxima, one record per check (written to $PARITY_REPORT by conftest at session end).
+REPORT = []
+CURRENT = {"test": None}
+
+
+def record(kind, value, tol, **extra):
+    REPORT.append({"test": CURRENT["test"], "kind": kind, "max": float(value), "tol": float(tol), **extra})
+
 
 class Case:
     def __init__(self, orc, cfg, wavefront="spherical", pathloss=False, precision="fp32", mode="nzm", P=None,

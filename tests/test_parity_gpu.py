@@ -14,7 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 from paper_2604_19723_b200 import scenes
-from tests.gpu_common import Case, rel_err
+from tests.gpu_common import Case, record, rel_err
 from tests.helpers import small_cfg, wrap
 
 
@@ -80,6 +80,8 @@ def test_response_phase_parity(cd, ctx, orc, precision, wf, shape):
         assert st == 0
         worst_ph = max(worst_ph, np.max(np.abs(np.angle(psi[i] * np.conj(ref)))))
         worst_mag = max(worst_mag, np.max(np.abs(np.abs(psi[i]) - 1.0)))
+    record("phase_rad", worst_ph, TOL_PH[precision], precision=precision, wavefront=wf, shape=list(shape))
+    record("magnitude", worst_mag, TOL_PH[precision], precision=precision, wavefront=wf, shape=list(shape))
     assert worst_ph <= TOL_PH[precision], worst_ph
     assert worst_mag <= TOL_PH[precision], worst_mag
 
@@ -97,6 +99,7 @@ def check_loglik(case, ctx, precision, idx=None, amp=False):
     lo = res[1]
     assert res[0] == 0
     e = rel_err(l[idx], lo, case.cfg.J, case.cfg.Nz)
+    record("rel_l", e.max(), TOL_L[precision], precision=precision, config=case.cfg.name, n=int(len(idx)))
     assert np.all(np.isfinite(l[idx]))
     assert e.max() <= TOL_L[precision], (e.max(), int(np.argmax(e)))
     if amp:
@@ -249,6 +252,7 @@ def test_normalize_moments_parity(cd, ctx, orc):
         ctx.sync()
         st, wo, lseo = orc.normalize(l)
         w = w.cpu().numpy()
+        record("normalize_weights_abs", np.max(np.abs(w - wo)), 1e-12 * max(1.0, wo.max()), P=P)
         assert abs(lse.item() - lseo) <= 1e-12 * abs(lseo)
         assert np.max(np.abs(w - wo)) <= 1e-12 * max(1.0, wo.max())
         assert abs(w.sum() - 1.0) <= 1e-12
@@ -340,6 +344,7 @@ def test_bp_step_fp64_end_to_end(cd, ctx, orc):
         st, xo, esto, lseo, anc = case.o.bp_step(xo, case.sc.sfv, case.y, case.m, case.v, case.eta, T, sv,
                                                  case.sc.philox_key, n)
         assert st == 0
+        record("bp_step_particles_abs", np.max(np.abs(xg.cpu().numpy() - xo)), 1e-9, precision="fp64", step=n)
         assert abs(lse.item() - lseo) <= 1e-10 * abs(lseo)
         assert np.allclose(est.cpu().numpy(), esto, rtol=1e-8, atol=1e-10)
         assert np.allclose(xg.cpu().numpy(), xo, rtol=0, atol=1e-9), n
@@ -354,6 +359,7 @@ def test_bp_step_weights_fp64(cd, ctx, orc):
     ctx.sync()
     st, lo = case.oracle_loglik()
     st, wo, lseo = orc.normalize(lo)
+    record("weights_abs", np.max(np.abs(w.cpu().numpy() - wo)), 1e-5, precision="fp64", config="c1")
     assert np.max(np.abs(w.cpu().numpy() - wo)) <= 1e-5
 
 

@@ -152,6 +152,9 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
   out->evenN_mask = ((sc->nf - 1) & 1) ? 0x80000000u : 0u;
   out->f0_cf = (float)out->f0_c;
   out->segdf_cf = (float)out->segdf_c;
+  out->two_seg = (sc->nf > SEG && sc->nf <= 2 * SEG && sc->wavefront != CDMS_PLANAR_NB) ? 1 : 0;
+  out->f1_c = (out->f0 + (double)SEG * sc->df) / C_LIGHT;
+  out->f1_cf = (float)out->f1_c;
   out->y_mb_step = (int64_t)(NWARP - 1) * out->n_kc * out->kc_len;
   {
     // |Delta_m| <= ||q_m|| = ||p~_m|| <= half the URA diagonal (H, R orthogonal)

@@ -40,6 +40,9 @@ struct SceneDev {
   float fc_cf, df_cf, nf_f, c6N_f;
   uint32_t evenN_mask;
   float f0_cf, segdf_cf;  // fp32 f0/c, SEG df/c for the per-antenna set-up
+  int two_seg;            // SEG < nf <= 2 SEG, not planar NB: second segment phasor formed directly (A1)
+  double f1_c;            // (f0 + SEG df)/c
+  float f1_cf;
   int64_t y_mb_step;      // ytiles element step from the last chunk of an antenna block to the next block
   double pa_pos[MAXJ][3];
   double pa_rot[MAXJ][9];

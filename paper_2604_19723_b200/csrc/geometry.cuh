@@ -112,12 +112,16 @@ __device__ __forceinline__ void template_col(const SceneDev& sc, int j, int m, d
 // antenna, otherwise the fp32 rounding of a shared W (|W| - 1 ~ 3e-8) is raised to the k-th power
 // identically on all antennas and the Horner correlation drifts coherently away from the exact
 // closed-form Gram.
+// With exactly two Horner segments (SEG < N_f <= 2 SEG, sc.two_seg) the second segment's start phasor is
+// formed directly like the first, E1 = e^{j2pi R (f0 + SEG df)/c} (fp64) times its per-antenna correction, instead
+// of A0 Z: one MUFU pair instead of the accurate Z polynomial and the product.
 template <typename RT>
 struct PSField {
   RT hx, hy, hz, R, E0r, E0i, gain;
   RT Whr, Whi, Wlr, Wli, Zhr, Zhi, Zlr, Zli;  // W, Zp as unevaluated sums hi + lo (fp32: ~48-bit mantissa)
+  RT E1r, E1i;                                // second-segment phase-centre phasor (two_seg only)
 };
-constexpr int NPSF = 15;       // RT fields of PSField
+constexpr int NPSF = 17;       // RT fields of PSField
 // shared-memory stride per (component, particle): 80 B (fp32), 4 x LDS.128; a stride of 4 x odd words keeps the
 // per-lane 128-bit loads of a quarter warp on distinct banks (64 B would be 4-way conflicted)
 constexpr int NPSF_PAD = 20;
@@ -165,6 +169,12 @@ __device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double*
   sincospi(2.0 * frac_c(R * sc.segdf_c), &s_, &c_);
   f.Zhr = (RT)c_; f.Zhi = (RT)s_;
   f.Zlr = (RT)(c_ - (double)f.Zhr); f.Zli = (RT)(s_ - (double)f.Zhi);
+  if (sc.two_seg) {
+    sincospi(2.0 * frac_c(R * sc.f1_c), &s_, &c_);
+    f.E1r = (RT)c_; f.E1i = (RT)s_;
+  } else {
+    f.E1r = RT(1); f.E1i = RT(0);
+  }
   f.gain = (RT)(sc.pathloss ? sc.lambda / (4.0 * PI * R) : 1.0);
   if (!sfv_ok) return PS_BADSFV;
   if (!(R > 0.0)) {  // also catches NaN positions
@@ -266,7 +276,11 @@ __device__ __forceinline__ void setup_sm(const SceneDev& sc, const PSField<RT>& 
     else if (sc.small_step) cis_small<RT>(delta * df_c, er, ei);
     else cis2pi<RT>(delta * df_c, er, ei);
     cmul_df<RT>(f.Whr, f.Whi, f.Wlr, f.Wli, er, ei, o.wr, o.wi);
-    if (sc.nf > SEG) {  // Z only advances A between segments
+    if (sc.two_seg) {  // the (Zr, Zi) slot carries A1 itself: the second segment starts at A1, not A0 Z
+      const RT f1_c = F32 ? (RT)sc.f1_cf : (RT)sc.f1_c;
+      cis2pi_fast<RT>(delta * f1_c, er, ei);
+      cmul<RT>(f.E1r, f.E1i, er, ei, o.Zr, o.Zi);
+    } else if (sc.nf > SEG) {  // Z only advances A between segments
       if (sc.small_z) cis_med<RT>(delta * segdf_c, er, ei);
       else cis2pi<RT>(delta * segdf_c, er, ei);
       cmul_df<RT>(f.Zhr, f.Zhi, f.Zlr, f.Zli, er, ei, o.Zr, o.Zi);

@@ -338,7 +338,9 @@ __device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const 
 // the warp scheduler's age priority; static partitions left ~17% of the warp slots idle (ncu warps_active 20
 // of 24), dynamic claiming keeps every slot busy until the queue drains.  Each group is computed entirely by
 // one CTA: results do not depend on the schedule.  The last CTA to finish resets the counters.
-template <int S, typename RT>
+// TWO: compile-time sc.two_seg (the segment end either moves A1 in or multiplies by Z; two instantiations keep
+// both Horner loops free of the other's register pressure).
+template <int S, typename RT, bool TWO>
 __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
     corr_kernel(const __grid_constant__ SceneDev sc, const CorrArgs a) {
   using PL = Plan<S, RT>;
@@ -559,18 +561,24 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
             for (int i = 1; i < k1 - k0; ++i) H.step(yk[-i]);
 #endif
           }
-          // c += A_seg H_seg (thread-private slot), A_seg <- A_seg Z
+          // c += A_seg H_seg (thread-private slot), A_seg <- A_seg Z (two_seg: A_1 itself sits in Z)
           RT hr[S], hi[S];
           H.get(hr, hi);
+          constexpr bool two_seg = TWO;
 #pragma unroll
           for (int s = 0; s < S; ++s) {
             const int o_ = (s * NWARP + warp) * TILE_P + lane;
             cst[2 * o_] = fma(Ar[s], hr[s], fma(-Ai[s], hi[s], cst[2 * o_]));
             cst[2 * o_ + 1] = fma(Ar[s], hi[s], fma(Ai[s], hr[s], cst[2 * o_ + 1]));
-            const RT nAr = Ar[s] * Zr[s] - Ai[s] * Zi[s];
-            const RT nAi = Ar[s] * Zi[s] + Ai[s] * Zr[s];
-            Ar[s] = nAr;
-            Ai[s] = nAi;
+            if (two_seg) {
+              Ar[s] = Zr[s];
+              Ai[s] = Zi[s];
+            } else {
+              const RT nAr = Ar[s] * Zr[s] - Ai[s] * Zi[s];
+              const RT nAi = Ar[s] * Zi[s] + Ai[s] * Zr[s];
+              Ar[s] = nAr;
+              Ai[s] = nAi;
+            }
           }
         }
         __syncwarp();  // every lane of this warp is done with the buffer
@@ -852,13 +860,17 @@ static int64_t grid_for_kernel(K kern, int threads, size_t smem, int64_t n_group
 
 template <int S, typename RT>
 static int64_t corr_grid_t(const SceneDev& sc, int64_t n_tiles, int num_sms) {
-  return grid_for_kernel(corr_kernel<S, RT>, NTHREADS, Plan<S, RT>::total, n_tiles * sc.J, num_sms);
+  if (sc.two_seg) return grid_for_kernel(corr_kernel<S, RT, true>, NTHREADS, Plan<S, RT>::total, n_tiles * sc.J, num_sms);
+  return grid_for_kernel(corr_kernel<S, RT, false>, NTHREADS, Plan<S, RT>::total, n_tiles * sc.J, num_sms);
 }
 
 template <int S, typename RT>
 static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStream_t st) {
   if (a.grid < 1 || a.n_groups < 1) return cudaSuccess;
-  corr_kernel<S, RT><<<(unsigned)a.grid, NTHREADS, Plan<S, RT>::total, st>>>(sc, a);
+  if (sc.two_seg)
+    corr_kernel<S, RT, true><<<(unsigned)a.grid, NTHREADS, Plan<S, RT>::total, st>>>(sc, a);
+  else
+    corr_kernel<S, RT, false><<<(unsigned)a.grid, NTHREADS, Plan<S, RT>::total, st>>>(sc, a);
   return cudaGetLastError();
 }
 

@@ -49,10 +49,15 @@ __global__ void response_kernel(const __grid_constant__ SceneDev sc, const doubl
       er = nr;
       ei = ni;
     }
-    const RT nAr = Ar * o.Zr - Ai * o.Zi;
-    const RT nAi = Ar * o.Zi + Ai * o.Zr;
-    Ar = nAr;
-    Ai = nAi;
+    if (sc.two_seg) {  // the kernel's second segment starts at A1 (carried in Z)
+      Ar = o.Zr;
+      Ai = o.Zi;
+    } else {
+      const RT nAr = Ar * o.Zr - Ai * o.Zi;
+      const RT nAi = Ar * o.Zi + Ai * o.Zr;
+      Ar = nAr;
+      Ai = nAi;
+    }
   }
 }
 

@@ -850,6 +850,11 @@ int corr_kchunk(int S) { return kchunk_for(S); }
 template <typename K>
 static int64_t grid_for_kernel(K kern, int threads, size_t smem, int64_t n_groups, int num_sms) {
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  // the persistent grid assumes every CTA resident at once: ask for the full shared-memory carveout (a smaller
+  // driver-chosen one would run the excess CTAs as a second wave)
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared) !=
+      cudaSuccess)
+    return 0;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess) return 0;
   if (per_sm < 1) per_sm = 1;

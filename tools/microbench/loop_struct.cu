@@ -6,9 +6,11 @@
 // Reports algorithmic FMA (4 per complex MAC) per clock per SM; the FP32 peak is 128.
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 typedef unsigned long long u64;
 __device__ unsigned long long g_cyc[4096];
+__device__ unsigned long long g_ns[4096];
 __device__ __forceinline__ u64 pk(float lo, float hi) { u64 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r; }
 __device__ __forceinline__ void up(u64 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
 __device__ __forceinline__ u64 f2(u64 a, u64 b, u64 c) { u64 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
@@ -58,6 +60,8 @@ __global__ void __launch_bounds__(256, MINB) k(float* out, const float4* __restr
                  "r"(sa(b)) : "memory");
   };
   if (lane == 0) { issue(0); issue(1); }
+  unsigned long long g0, g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   unsigned long long t0 = clock64();
   for (int c = 0; c < nchunks; ++c) {
     if (TMA) while (!trywait(&bar[warp * 2 + (c & 1)], (c >> 1) & 1)) {}
@@ -103,10 +107,14 @@ __global__ void __launch_bounds__(256, MINB) k(float* out, const float4* __restr
     if (lane == 0 && c + 2 < nchunks) issue(c + 2);
   }
   unsigned long long t1 = clock64();
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
   float acc = 0.f;
   for (int s = 0; s < S; ++s) acc += cr[s] + ci[s] + cst[(s * 256 + threadIdx.x) * 2] + Ar[s];
   out[blockIdx.x * 256 + threadIdx.x] = acc;
-  if (threadIdx.x == 0) g_cyc[blockIdx.x] = t1 - t0;
+  if (threadIdx.x == 0) {
+    g_cyc[blockIdx.x] = t1 - t0;
+    g_ns[blockIdx.x] = g1 - g0;  // SM clock in MHz = cycles / ns * 1000
+  }
 }
 
 template <int S, int SEGL, int KC, bool CSMEM, bool TMA, int MINB>
@@ -114,31 +122,59 @@ void run(float* out, const float4* yg, int nsm) {
   auto kern = k<S, SEGL, KC, CSMEM, TMA, MINB>;
   const int smem = 8 * 2 * KC * 16 + 16 * 8 + S * 256 * 2 * 4;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (getenv("CARVEOUT_MAX"))
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
   const int nchunks = 4096 / KC * 4;
   const int grid = nsm * MINB;
   kern<<<grid, 256, smem>>>(out, yg, nchunks);
   cudaDeviceSynchronize();
-  kern<<<grid, 256, smem>>>(out, yg, nchunks);
-  cudaDeviceSynchronize();
-  static unsigned long long h[4096];
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int reps = 20;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) kern<<<grid, 256, smem>>>(out, yg, nchunks);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  static unsigned long long h[4096], hn[4096];
   cudaMemcpyFromSymbol(h, g_cyc, sizeof(unsigned long long) * grid);
-  double cyc = 0;
-  for (int i = 0; i < grid; ++i) cyc += h[i];
+  cudaMemcpyFromSymbol(hn, g_ns, sizeof(unsigned long long) * grid);
+  double cyc = 0, ns = 0;
+  for (int i = 0; i < grid; ++i) { cyc += h[i]; ns += hn[i]; }
   cyc /= grid;
+  ns /= grid;
   const double fma = 4.0 * S * (double)nchunks * KC * 256.0 * MINB;
-  printf("S=%d SEG=%3d KC=%3d c_in_%s %s minb=%d : %6.1f FMA/clk/SM = %.3f of peak  (%s)\n", S, SEGL, KC,
-         CSMEM ? "smem" : "regs", TMA ? "TMA     " : "resident", MINB, fma / cyc, fma / cyc / 128.0,
-         cudaGetErrorString(cudaGetLastError()));
+  const double tflops = 2.0 * fma * nsm * reps / (ms * 1e-3) / 1e12;  // wall clock, incl. launch gaps
+  printf("S=%d SEG=%3d KC=%3d c_in_%s %s minb=%d : %6.1f FMA/clk/SM = %.3f of peak;  wall %.1f TFLOP/s = %.3f of "
+         "74.45;  in-kernel SM clock %.0f MHz; occupancy %d CTAs/SM  (%s)\n", S, SEGL, KC, CSMEM ? "smem" : "regs", TMA ? "TMA     " : "resident",
+         MINB, fma / cyc, fma / cyc / 128.0, tflops, tflops / 74.45, cyc / ns * 1e3, per_sm, cudaGetErrorString(cudaGetLastError()));
 }
 
-int main() {
+__global__ void fill_random(float4* y, int n) {  // (yr, yr, yi, yi) with yr, yi ~ U(-1, 1) (hash)
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t h = (uint32_t)i * 0x9E3779B1u;
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12;
+  const float a = (float)(h & 0xFFFF) / 32768.f - 1.f, b = (float)(h >> 16) / 32768.f - 1.f;
+  y[i] = make_float4(a, a, b, b);
+}
+
+int main(int argc, char** argv) {
   int nsm;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   float* out;
   cudaMalloc(&out, 1 << 24);
   float4* y;
   cudaMalloc(&y, 1024 * 256 * 16);
-  cudaMemset(y, 0, 1024 * 256 * 16);
+  const bool rnd = argc > 1 && argv[1][0] == 'r';
+  if (rnd) fill_random<<<1024, 256>>>(y, 1024 * 256);
+  else cudaMemset(y, 0, 1024 * 256 * 16);
+  cudaDeviceSynchronize();
+  printf("y data: %s\n", rnd ? "random U(-1,1)" : "zeros");
   run<5, 64, 128, true, true, 3>(out, y, nsm);
   run<5, 64, 128, true, false, 3>(out, y, nsm);
   run<5, 64, 128, false, true, 3>(out, y, nsm);

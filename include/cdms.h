@@ -11,8 +11,14 @@
  *    call (the library copies what it keeps).  Arrays are dense, row-major, no padding.
  *  - complex64 = interleaved (re, im) float32 pairs; complex128 = interleaved float64 pairs.
  *  - Every device operation is enqueued on the context's stream; nothing synchronizes the host
- *    except cdms_sync().  Calls are capturable into a CUDA graph once their workspaces exist
- *    (first call outside capture, or cdms_reserve()).
+ *    except cdms_sync() and, with nranks > 1 only, one stream synchronization inside cdms_resample and
+ *    cdms_bp_step (the host builds the rank-to-rank exchange plan from the all-gathered masses).
+ *    Single-rank calls are capturable into a CUDA graph once their workspaces exist (first call
+ *    outside capture, or cdms_reserve()).
+ *  - Concurrency: a context is one in-order worker -- its workspaces (including the device-side
+ *    work-claim counters of the likelihood kernel and the step pipeline, which the last CTA of each
+ *    launch resets) are shared by its calls, so calls on one context must not overlap on different
+ *    streams.  Separate contexts are independent.
  *  - Errors: host-checkable problems (NULL pointers, sizes <= 0, ||sfv|| = 0, R not in SO(3),
  *    non-uniform f_pb, non-finite or negative priors) return CDMS_EINVAL BEFORE any launch and
  *    leave outputs untouched.  Device-detected conditions set a sticky flag that cdms_sync()

@@ -7,6 +7,7 @@
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -29,6 +30,7 @@ struct cdms_ctx_s {
   std::vector<size_t> sizes;
   uint64_t* h_pinned = nullptr;  // small pinned host staging (plan exchange)
   bool timing = false;           // bracket the likelihood kernel with events
+  bool nb_tensor = true;         // PLANAR_NB fp32 on the tensor cores (nbmma.cu); CDMS_NB_TENSOR=0 selects K1
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
 };
@@ -37,7 +39,8 @@ namespace {
 
 enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
-  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_COUNT
+  WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
+  WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -395,6 +398,17 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &tmpl);
   CUDA_TRY(ctx, launch_prep_y(sd, static_cast<const float2*>(d_y), yt, yn, tmpl, ctx->stream));
   ctx->launches += 1;
+  // PLANAR_NB in fp32: the correlation runs as a tensor-core GEMM (nbmma.cu) with the closed-form Gram
+  NbPlan nbp{};
+  const bool nbt = ctx->nb_tensor && precision == CDMS_FP32 && nb_tensor_plan(sd, &nbp);
+  uint8_t* nbop = nullptr;
+  float* nbscale = nullptr;
+  if (nbt) {
+    WS_TRY(ctx, WS_NBOP, nb_operand_bytes(sd, nbp), &nbop);
+    WS_TRY(ctx, WS_NBSCALE, MAXJ, &nbscale);
+    CUDA_TRY(ctx, launch_nb_prep(sd, nbp, static_cast<const float2*>(d_y), nbop, nbscale, ctx->stream));
+    ctx->launches += 1;
+  }
   // particles go through K1 (correlation + Gram -> HBM terms) and K1b (assembly) in batches whose terms
   // buffer stays under TERMS_BUDGET bytes
   const int T = terms_width(sd.S);
@@ -436,7 +450,24 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       ctx->ev_used += 2;
       CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
     }
-    CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
+    if (nbt) {
+      NbArgs na;
+      na.particles = a.particles;
+      na.P = nb;
+      na.pstride = pstride;
+      na.sfv = a.sfv;
+      na.sfv_pp = sfv_pp;
+      na.bop = nbop;
+      na.yscale_inv = nbscale;
+      na.terms = terms;
+      na.n_tiles_j = (nb * sd.S + 127) / 128;
+      na.n_tiles = na.n_tiles_j * sd.J;
+      CUDA_TRY(ctx, launch_nb_gram(sd, na, pflag, ctx->stream));
+      CUDA_TRY(ctx, launch_nb_corr(sd, nbp, na, ctx->num_sms, ctx->stream));
+      ctx->launches += 1;
+    } else {
+      CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
+    }
     if (ctx->timing) CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
     AsmArgs s;
     s.terms = terms;
@@ -472,6 +503,7 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   ctx->sizes.assign(WS_COUNT, 0);
   DeviceGuard g(device);
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char* e = getenv("CDMS_NB_TENSOR")) ctx->nb_tensor = atoi(e) != 0;
   if (cudaMalloc(&ctx->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_flags, 0, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {
     delete ctx;

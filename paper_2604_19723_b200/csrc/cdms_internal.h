@@ -170,6 +170,41 @@ cudaError_t launch_regularize(double* x, int64_t P, int64_t p0, int64_t P_total,
                               uint64_t key, uint64_t step, cudaStream_t st);
 cudaError_t launch_fill_u64(uint64_t* dst, uint64_t v, int n, cudaStream_t st);
 
+// nbmma.cu: PLANAR_NB correlation on the tensor cores
+struct NbPlan {
+  int kc;              // real K per pipeline stage (2 x subcarriers), 16 / 32 / 64
+  int nst;             // pipeline stages
+  int n_pass;          // antenna passes (2 ceil8(N_a) > 256 takes several)
+  int nbh;             // antennas per pass, padded to 8: Re W in accumulator columns [0, nbh), Im W in [nbh, 2 nbh)
+  int nb;              // UMMA N = 2 nbh (<= 256)
+  int nacc;            // accumulator pairs (D1 exact hi x hi, D2 the rest) in TMEM: 2 when 4 nb <= 512
+  int tmem_cols;       // allocated TMEM columns (power of two >= 32)
+  int pexp, qexp;      // hi grids: A_hi on 2^-pexp of |b| = 1, y_hi on 2^-qexp of max|y|; K 2^(p+q) <= 2^24
+  int nf_pad;          // subcarriers padded to kc / 2
+  int n_chunks;        // pipeline stages per tile = 2 nf_pad / kc
+  uint32_t a_bytes;    // one fp16 piece of the A stage (128 x kc)
+  uint32_t b_bytes;    // one fp16 piece of the B stage (nb x kc)
+  size_t smem;         // dynamic shared memory of nb_corr_kernel
+};
+struct NbArgs {
+  const double* particles;  // batch start
+  int64_t P;
+  int pstride;
+  const double* sfv;        // [K][3] or [P][K][3] at the batch (sfv_pp)
+  int sfv_pp;
+  const uint8_t* bop;       // [J][n_chunks][2][nb x kc] fp16 B operand (nb_prep_kernel)
+  const float* yscale_inv;  // [J] 2^e_j
+  double2* terms;           // [P][J][T]: c_s written by nb_corr_kernel, G by nb_gram_kernel
+  int64_t n_tiles_j;        // ceil(P S / 128)
+  int64_t n_tiles;          // n_tiles_j J
+};
+bool nb_tensor_plan(const SceneDev& sc, NbPlan* pl);  // false: shape not supported (2 N_a > 512)
+size_t nb_operand_bytes(const SceneDev& sc, const NbPlan& pl);
+cudaError_t launch_nb_prep(const SceneDev& sc, const NbPlan& pl, const float2* y, uint8_t* bop, float* yscale_inv,
+                           cudaStream_t st);
+cudaError_t launch_nb_gram(const SceneDev& sc, const NbArgs& a, int* pflag, cudaStream_t st);
+cudaError_t launch_nb_corr(const SceneDev& sc, const NbPlan& pl, const NbArgs& a, int num_sms, cudaStream_t st);
+
 // step.cu: the fused O(P) pipeline of cdms_bp_step (fixed STEP_ITEMS-particle blocks, last-block reductions)
 constexpr int STEP_ITEMS = 512;
 int64_t step_blocks(int64_t P);

@@ -1,0 +1,565 @@
+// F2: the PLANAR_NB correlation as a complex GEMM on the 5th-generation tensor cores.
+//
+// PLANAR_NB responses are rank one as an N_f x N_a matrix:
+//   psi_s[k, m] = g_s e^{-j2pi f_c R_s/c} b_s[k] a_s[m],   b_s[k] = e^{-j2pi (k - (N_f-1)/2) df R_s/c},
+//   a_s[m] = a_y[iy] a_v[iv] = e^{j2pi (p~_y[iy] u'_y + p~_z[iv] u'_z)/lambda}       (m = iy N_v + iv)
+// with R_s = ||r'||, u' = r'/R_s the local ray.  Hence
+//   c_s = psi_s^H z = g_s e^{+j2pi f_c R_s/c} sum_m conj(a_s[m]) W_s[m],   W_s[m] = sum_k conj(b_s[k]) y[m, k],
+// and W for every hypothesis (particle, component) of a PA is ONE real GEMM shared by all of them:
+//   D[h, n] = sum_kk A[h, kk] B[n, kk],   A[h, 2k + {0,1}] = (Re b_h[k], Im b_h[k])          (generated on chip)
+//   B[m, .] = (Re y[m,k], Im y[m,k]),  B[Nh + m, .] = (Im y[m,k], -Re y[m,k])               (one per PA)
+// so D[h, m] = Re W_h[m] and D[h, Nh + m] = Im W_h[m].  The Gram matrix of the same hypotheses factors into
+// three Dirichlet kernels (closed form, fp64, nb_gram_kernel).
+//
+// Precision (tools/f2_precision.py).  Two measured properties of the tensor core shape the split:
+//  (1) fp16 subnormal operands read as zero -> both operands are scaled by powers of two into fp16's upper
+//      range (A by 2^8, y per PA to max |Re|, |Im| in [2^7, 2^8));
+//  (2) fp32 accumulation into TMEM is biased toward zero (measured: a coherent |c| shrink of ~2e-8 per
+//      accumulation, -1e-6 after 48, rel-l 2e-4 near the true position).
+// Hence an error-free split of the dominant term: x = x_hi + x_lo with x_hi on an integer grid (A: 2^-p of
+// |b| = 1, y: 2^-q of its max) chosen so that K 2^(p+q) <= 2^24 -- every partial sum of A_hi B_hi is an exactly
+// representable fp32 integer multiple of the grid product, so D1 = A_hi B_hi accumulates WITHOUT rounding --
+// and D2 = A_hi B_lo + A_lo B_hi + A_lo B_lo (lo in fp16) in a second accumulator.  D2's partial sums are
+// random walks (rounding residuals), so its truncation does not add coherently to c.  Emulated near the true
+// position (truncation modelled): rel-l 2.9e-6 (c2), 6.4e-7 (c3), 8.1e-7 (c4).
+//
+// Kernel (one persistent CTA per SM, 14 warps, warp-specialised):
+//   warp 0       TMEM allocation; one lane streams the B chunks (1-D bulk TMA, prepared in the UMMA
+//                canonical K-major no-swizzle layout by nb_prep_kernel) into the stage ring
+//   warp 1       one lane issues tcgen05.mma (kind::f16, M = 128 hypotheses, N = 2 nbh <= 256 per pass,
+//                four per K-step of 16) and tcgen05.commit's the stage / accumulator barriers
+//   warps 2..9   generate A (2 threads per hypothesis row, fp64 set-up, fp32 phasor recurrence with a hi+lo
+//                step anchored per stage from an fp64-reduced phase, grid/fp16 split) into the same ring
+//   warps 10..13 epilogue: tcgen05.ld one TMEM lane (= one hypothesis) each, W = D1 + D2, contract with conj(a)
+//                (fp32 rows of N_v, fp64 across rows), apply gain, carrier and the operand scales -> c_s
+// Work item = (tile of 128 hypotheses of one PA, antenna pass); arrays with 2 ceil8(N_a) > 256 take several
+// passes (A is regenerated per pass).  Accumulator pairs are double-buffered in TMEM when 4 nb <= 512.
+#include <cuda_fp16.h>
+
+#include "cdms_internal.h"
+#include "geometry.cuh"
+
+namespace cdms {
+
+namespace {
+
+constexpr int NB_M = 128;          // hypotheses per tile = TMEM lanes = UMMA M
+constexpr int NB_GEN_WARPS = 8;
+constexpr int NB_EPI_WARPS = 4;
+constexpr int NB_WARPS = 2 + NB_GEN_WARPS + NB_EPI_WARPS;
+constexpr int NB_THREADS = 32 * NB_WARPS;
+constexpr int NB_MAX_STAGES = 6;
+constexpr int NB_MAX_PASS = 8;
+constexpr size_t NB_SMEM_BUDGET = 220 * 1024;
+constexpr int NB_SCALE_LOG2 = 8;   // operands scaled to magnitude <= 2^8 before the split
+
+// ---------------------------------------------------------------------------- tcgen05 / TMEM helpers
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// UMMA shared-memory descriptor: canonical K-major, no swizzle, ((8,n),2):((16 B, SBO),LBO); version 1 (tcgen05)
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
+}
+// instruction descriptor kind::f16: D f32 (bit 4), A = B = f16 (formats 0), both K-major, N >> 3 at 17, M >> 4 at 24
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// four 8-column loads of this warp's 32 TMEM lanes, one wait
+__device__ __forceinline__ void tmem_ld8x4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t (&a)[8],
+                                           uint32_t (&b)[8], uint32_t (&c)[8], uint32_t (&d)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%32];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%33];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%34];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%35];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), "=r"(a[7]),
+        "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]), "=r"(b[4]), "=r"(b[5]), "=r"(b[6]), "=r"(b[7]),
+        "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7]),
+        "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+      : "r"(t0), "r"(t1), "r"(t2), "r"(t3)
+      : "memory");
+}
+// (x, y) -> fp16x2 with x in the low half (lower address)
+__device__ __forceinline__ uint32_t pack_h2(float x, float y) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(y), "f"(x));
+  return r;
+}
+// error-free split of a complex value (already scaled): hi = rint(x / grid) grid (exact in fp16: <= 11 bits),
+// lo = fp16(x - hi) (x - hi is exact in fp32)
+__device__ __forceinline__ void split_grid(float x, float y, float grid, float inv_grid, uint32_t& hi,
+                                           uint32_t& lo) {
+  const float hx = rintf(x * inv_grid) * grid, hy = rintf(y * inv_grid) * grid;
+  hi = pack_h2(hx, hy);
+  lo = pack_h2(x - hx, y - hy);
+}
+
+// ---------------------------------------------------------------------------- per-hypothesis set-up (fp64)
+struct NbHyp {
+  double R, delta, uy, uz, gain;
+  int flag;  // pflag bits: 1 degenerate (r' = 0 or non-finite), 2 invalid SFV
+};
+// hypothesis (p, s) of PA j (P:L57-61 layout, P:L2097 local ray, P:L2150-2157 path loss)
+__device__ __forceinline__ NbHyp nb_setup(const SceneDev& sc, const NbArgs& a, int j, int64_t p, int s) {
+  NbHyp o;
+  const double* pos = a.particles + p * a.pstride;
+  const double* sfv_s = nullptr;
+  if (s > 0) sfv_s = a.sfv_pp ? a.sfv + (p * sc.K + (s - 1)) * 3 : a.sfv + (int64_t)(s - 1) * 3;
+  double va[3], sh[3];
+  const bool ok = anchor_va(sc, j, sfv_s, va, sh);
+  o.flag = ok ? 0 : 2;
+  if (!ok) {
+    va[0] = pos[0] - 1.0; va[1] = pos[1]; va[2] = pos[2];
+    sh[0] = sh[1] = sh[2] = 0.0;
+  }
+  const double r0 = pos[0] - va[0], r1 = pos[1] - va[1], r2 = pos[2] - va[2];
+  const double rs2 = 2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]);
+  const double h0 = r0 - rs2 * sh[0], h1 = r1 - rs2 * sh[1], h2 = r2 - rs2 * sh[2];  // H r
+  const double* Rj = sc.pa_rot[j];
+  const double ly = Rj[1] * h0 + Rj[4] * h1 + Rj[7] * h2;  // r' = R_j^T H r
+  const double lz = Rj[2] * h0 + Rj[5] * h1 + Rj[8] * h2;
+  double R = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+  if (!(R > 0.0) || !isfinite(R)) {
+    o.flag |= 1;
+    R = 1.0;
+    o.uy = 0.0; o.uz = 0.0;
+  } else {
+    o.uy = ly / R; o.uz = lz / R;
+  }
+  o.R = R;
+  o.delta = R * sc.df_c;
+  o.gain = sc.pathloss ? sc.lambda / (4.0 * PI * R) : 1.0;
+  return o;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------- plan
+bool nb_tensor_plan(const SceneDev& sc, NbPlan* pl) {
+  if (sc.wavefront != CDMS_PLANAR_NB) return false;
+  NbPlan p{};
+  const int na8 = (sc.Na + 7) / 8 * 8;
+  p.n_pass = (2 * na8 + 255) / 256;  // UMMA N = 2 nbh <= 256 per pass (two accumulators <= 512 columns)
+  if (p.n_pass > NB_MAX_PASS) return false;
+  p.nbh = ((sc.Na + p.n_pass - 1) / p.n_pass + 7) / 8 * 8;
+  p.nb = 2 * p.nbh;
+  const int kmax = ((2 * sc.nf + 15) / 16) * 16;  // no more K per stage than the padded problem has
+  int kc = 0, nst = 0;
+  for (int cand : {64, 32, 16}) {
+    if (cand > kmax && cand != 16) continue;
+    const size_t stage = 4u * (size_t)cand * (NB_M + p.nb);
+    const int n = (int)(NB_SMEM_BUDGET / stage);
+    if (n >= 3 || cand == 16) {
+      kc = cand;
+      nst = n < NB_MAX_STAGES ? n : NB_MAX_STAGES;
+      break;
+    }
+  }
+  if (nst < 2) return false;
+  p.kc = kc;
+  p.nst = nst;
+  p.nf_pad = (sc.nf + kc / 2 - 1) / (kc / 2) * (kc / 2);
+  p.n_chunks = 2 * p.nf_pad / kc;
+  p.a_bytes = (uint32_t)(NB_M * kc * 2);
+  p.b_bytes = (uint32_t)(p.nb * kc * 2);
+  p.nacc = (4 * p.nb <= 512) ? 2 : 1;
+  int cols = 32;
+  while (cols < p.nacc * 2 * p.nb) cols *= 2;
+  p.tmem_cols = cols;
+  // exactness of D1 = A_hi B_hi: |partial sum| <= K 2^(p+q) grid units <= 2^24  (K = 2 nf_pad)
+  int lk = 0;
+  while ((1 << lk) < 2 * p.nf_pad) ++lk;
+  const int pq = 24 - lk;
+  p.qexp = pq / 2 > 10 ? 10 : pq / 2;
+  p.pexp = (pq - p.qexp) > 10 ? 10 : pq - p.qexp;
+  if (p.pexp < 4 || p.qexp < 4) return false;  // K > 2^16: the exact grid gets too coarse
+  p.smem = (size_t)nst * 2 * (p.a_bytes + p.b_bytes) + 1024;
+  *pl = p;
+  return true;
+}
+size_t nb_operand_bytes(const SceneDev& sc, const NbPlan& pl) {
+  return (size_t)sc.J * pl.n_pass * pl.n_chunks * 2 * pl.b_bytes;
+}
+
+// ---------------------------------------------------------------------------- B operand (per PA)
+// bop[j][pass][q][piece][...]: pass pi covers antennas [pi nbh, (pi+1) nbh); chunk q holds kk in [q kc, (q+1) kc)
+// (subcarriers q kc/2 ...); piece 0 = hi (grid 2^-q_exp of the scaled max), 1 = lo; element (n, kk) at byte
+// (n/8) SBO + (kk/8) 128 + (n%8) 16 + (kk%8) 2 with SBO = 16 kc (UMMA canonical K-major, no swizzle).
+// y is scaled by 2^(8-e_j) (max |Re|, |Im| in [2^7, 2^8)); yscale_inv[j] = 2^(e_j - 16) undoes both scales.
+__global__ void nb_prep_kernel(const __grid_constant__ SceneDev sc, const NbPlan pl, const float2* __restrict__ y,
+                               uint8_t* __restrict__ bop, float* __restrict__ yscale_inv) {
+  const int j = blockIdx.y;
+  const int64_t nz = (int64_t)sc.nf * sc.Na;
+  const float2* yj = y + (int64_t)j * nz;
+  __shared__ float red[32];
+  float mx = 0.f;
+  for (int64_t n = threadIdx.x; n < nz; n += blockDim.x) {
+    const float2 v = yj[n];
+    mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  __syncthreads();
+  mx = red[0];
+  int e = 0;
+  if (mx > 0.f && isfinite(mx)) frexpf(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+  const float scale = ldexpf(1.f, NB_SCALE_LOG2 - e);
+  if (blockIdx.x == 0 && threadIdx.x == 0) yscale_inv[j] = ldexpf(1.f, e - 2 * NB_SCALE_LOG2);
+  const float grid = ldexpf(1.f, NB_SCALE_LOG2 - pl.qexp), inv_grid = ldexpf(1.f, pl.qexp - NB_SCALE_LOG2);
+  const int kc8 = pl.kc / 8;
+  const uint32_t sbo = 16u * pl.kc;
+  const int64_t units = (int64_t)pl.n_pass * pl.n_chunks * kc8 * pl.nb;  // 16-byte units (4 subcarriers)
+  uint8_t* bj = bop + (size_t)j * pl.n_pass * pl.n_chunks * 2 * pl.b_bytes;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(u % pl.nb);
+    int64_t r = u / pl.nb;
+    const int cc = (int)(r % kc8);
+    r /= kc8;
+    const int q = (int)(r % pl.n_chunks);
+    const int pass = (int)(r / pl.n_chunks);
+    const bool im = n >= pl.nbh;
+    const int ml = im ? n - pl.nbh : n;
+    const int m = pass * pl.nbh + ml;
+    const bool mok = ml < pl.nbh && m < sc.Na;
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int k = q * (pl.kc / 2) + cc * 4 + t;
+      float2 v = make_float2(0.f, 0.f);
+      if (mok && k < sc.nf) v = yj[(int64_t)k * sc.Na + m];
+      const float xr = (im ? v.y : v.x) * scale, xi = (im ? -v.x : v.y) * scale;
+      split_grid(xr, xi, grid, inv_grid, hi[t], lo[t]);
+    }
+    const size_t off = (size_t)(n >> 3) * sbo + (size_t)cc * 128 + (size_t)(n & 7) * 16;
+    uint8_t* base = bj + ((size_t)pass * pl.n_chunks + q) * 2 * pl.b_bytes;
+    *reinterpret_cast<uint4*>(base + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(base + pl.b_bytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// ---------------------------------------------------------------------------- Gram (closed form, fp64)
+// G_rc = psi_r^H psi_c = g_r g_c e^{j2pi f_c (R_r - R_c)/c} D_Nf(df (R_r - R_c)/c)
+//        D_Ny(d_y (u'_y,c - u'_y,r)/lambda) D_Nv(d_v (u'_z,c - u'_z,r)/lambda),  G_ss = g_s^2 N_z
+// (centred template and subcarrier grid: every factor is a real Dirichlet kernel, C-amb-13 for D_N).
+// One thread per (particle, PA); also ORs the per-particle flags.
+__global__ void nb_gram_kernel(const __grid_constant__ SceneDev sc, const NbArgs a, int* __restrict__ pflag) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int J = sc.J, S = sc.S, T = S + S * (S + 1) / 2;
+  if (idx >= a.P * J) return;
+  const int64_t p = idx / J;
+  const int j = (int)(idx - p * J);
+  double R[MAXS], dl[MAXS], uy[MAXS], uz[MAXS], g[MAXS];
+  int fl = 0;
+  for (int s = 0; s < S; ++s) {
+    const NbHyp h = nb_setup(sc, a, j, p, s);
+    R[s] = h.R; dl[s] = h.delta; uy[s] = h.uy; uz[s] = h.uz; g[s] = h.gain;
+    fl |= h.flag;
+  }
+  if (fl) atomicOr(&pflag[p], fl);
+  const double nz = (double)sc.nf * (double)sc.Na;
+  const double ky = sc.dy / sc.lambda, kv = sc.dv / sc.lambda;
+  double2* out = a.terms + (p * J + j) * T + S;
+  int t = 0;
+  for (int r = 0; r < S; ++r) {
+    for (int c = 0; c <= r; ++c, ++t) {
+      if (r == c) {
+        out[t] = make_double2(nz * g[r] * g[r], 0.0);
+        continue;
+      }
+      double sn, cs;
+      sincospi(2.0 * frac_c((R[r] - R[c]) * sc.fc_c), &sn, &cs);
+      const double xf = dl[r] - dl[c], xy = ky * (uy[c] - uy[r]), xv = kv * (uz[c] - uz[r]);
+      const double nf_ = rint(xf), ny_ = rint(xy), nv_ = rint(xv);
+      const double D = dirichlet<double>(xf - nf_, (long long)nf_, sc.nf) *
+                       dirichlet<double>(xy - ny_, (long long)ny_, sc.ny) *
+                       dirichlet<double>(xv - nv_, (long long)nv_, sc.nv);
+      const double m = g[r] * g[c] * D;
+      out[t] = make_double2(m * cs, m * sn);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- K1 (tensor cores)
+__global__ void __launch_bounds__(NB_THREADS, 1)
+    nb_corr_kernel(const __grid_constant__ SceneDev sc, const NbPlan pl, const NbArgs a) {
+  extern __shared__ __align__(1024) uint8_t nb_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nst = pl.nst, kc = pl.kc, npass = pl.n_pass;
+  const uint32_t stage_bytes = 2 * (pl.a_bytes + pl.b_bytes);
+  uint8_t* ring = nb_smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(nb_smem + (size_t)nst * stage_bytes);
+  uint64_t* full_a = bars;
+  uint64_t* full_b = bars + NB_MAX_STAGES;
+  uint64_t* empty = bars + 2 * NB_MAX_STAGES;
+  uint64_t* acc_full = bars + 3 * NB_MAX_STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // stage s: [A_hi | A_lo | B_hi | B_lo]
+  auto A_hi = [&](int s) { return ring + (size_t)s * stage_bytes; };
+  auto B_hi = [&](int s) { return ring + (size_t)s * stage_bytes + 2 * pl.a_bytes; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full_a[s], NB_GEN_WARPS);
+      mbar_init(&full_b[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], NB_EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)pl.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int J = sc.J, S = sc.S;
+  const int64_t nhyp = a.P * S;
+  const int n_chunks = pl.n_chunks;
+  const uint32_t sbo = 16u * kc;
+
+  if (warp == 0) {
+    // ---------------- B producer
+    if (lane == 0) {
+      int64_t g = 0;
+      for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const int j = (int)(tile / a.n_tiles_j);
+        const uint8_t* src = a.bop + (size_t)j * npass * n_chunks * 2 * pl.b_bytes;
+        for (int pass = 0; pass < npass; ++pass) {
+          for (int q = 0; q < n_chunks; ++q, ++g) {
+            const int slot = (int)(g % nst);
+            if (g >= nst) mbar_wait(&empty[slot], (uint32_t)((g / nst) - 1) & 1u);
+            mbar_expect_tx(&full_b[slot], 2 * pl.b_bytes);
+            tma_load_1d(B_hi(slot), src + ((size_t)pass * n_chunks + q) * 2 * pl.b_bytes, 2 * pl.b_bytes,
+                        &full_b[slot]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: D1 += A_hi B_hi (exact), D2 += A_hi B_lo + A_lo B_hi + A_lo B_lo
+    if (lane == 0) {
+      int64_t g = 0, i = 0;
+      const uint32_t idesc = umma_idesc_f16(NB_M, pl.nb);
+      for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        for (int pass = 0; pass < npass; ++pass, ++i) {
+          const int b = (int)(i % pl.nacc);
+          const int64_t u = i / pl.nacc;
+          if (i >= pl.nacc) mbar_wait(&acc_empty[b], (uint32_t)(u - 1) & 1u);
+          tc_fence_after();
+          const uint32_t d1 = tmem + (uint32_t)(b * 2 * pl.nb), d2 = d1 + (uint32_t)pl.nb;
+          for (int q = 0; q < n_chunks; ++q, ++g) {
+            const int slot = (int)(g % nst);
+            const uint32_t par = (uint32_t)(g / nst) & 1u;
+            mbar_wait(&full_b[slot], par);
+            mbar_wait(&full_a[slot], par);
+            tc_fence_after();
+            const uint32_t a_hi = smem_u32(A_hi(slot)), a_lo = a_hi + pl.a_bytes;
+            const uint32_t b_hi = smem_u32(B_hi(slot)), b_lo = b_hi + pl.b_bytes;
+            for (int ks = 0; ks < kc / 16; ++ks) {
+              const uint32_t koff = (uint32_t)ks * 256u;
+              const uint64_t dah = umma_sdesc(a_hi + koff, 128, sbo), dal = umma_sdesc(a_lo + koff, 128, sbo);
+              const uint64_t dbh = umma_sdesc(b_hi + koff, 128, sbo), dbl = umma_sdesc(b_lo + koff, 128, sbo);
+              const uint32_t acc0 = (q | ks) ? 1u : 0u;
+              umma_f16(d1, dah, dbh, idesc, acc0);
+              umma_f16(d2, dah, dbl, idesc, acc0);
+              umma_f16(d2, dal, dbh, idesc, 1u);
+              umma_f16(d2, dal, dbl, idesc, 1u);
+            }
+            umma_commit(&empty[slot]);
+          }
+          umma_commit(&acc_full[b]);
+        }
+      }
+    }
+  } else if (warp < 2 + NB_GEN_WARPS) {
+    // ---------------- A generators: thread -> (row h, half of each stage's subcarriers)
+    const int gt = threadIdx.x - 64;
+    const int h = gt & (NB_M - 1), half = gt >> 7;
+    const int sub = kc / 4;          // subcarriers per thread per stage
+    const int nchunk16 = sub / 4;    // 16-byte chunks (4 subcarriers) per thread per stage
+    const double kcen = 0.5 * (sc.nf - 1);
+    const float a_scale = (float)(1 << NB_SCALE_LOG2);
+    const float grid = ldexpf(1.f, NB_SCALE_LOG2 - pl.pexp), inv_grid = ldexpf(1.f, pl.pexp - NB_SCALE_LOG2);
+    const uint32_t row_off = (uint32_t)(h >> 3) * sbo + (uint32_t)(h & 7) * 16u;
+    int64_t g = 0;
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+      const int j = (int)(tile / a.n_tiles_j);
+      const int64_t hg = (tile - (int64_t)j * a.n_tiles_j) * NB_M + h;
+      double delta = 0.0;
+      if (hg < nhyp) {
+        const int64_t p = hg / S;
+        delta = nb_setup(sc, a, j, p, (int)(hg - p * S)).delta;
+      }
+      // w = e^{-j2pi delta} as an unevaluated sum hi + lo: w is raised to the k-th power along the stage, so a
+      // single fp32 rounding would tilt every subcarrier's phase coherently
+      double sw, cw;
+      sincospi(2.0 * frac_c(delta), &sw, &cw);
+      const float whr = (float)cw, whi = (float)-sw;
+      const float wlr = (float)(cw - (double)whr), wli = (float)(-sw - (double)whi);
+      for (int pass = 0; pass < npass; ++pass) {
+        for (int q = 0; q < n_chunks; ++q, ++g) {
+          const int slot = (int)(g % nst);
+          if (g >= nst) mbar_wait(&empty[slot], (uint32_t)((g / nst) - 1) & 1u);
+          const int k0 = q * (kc / 2) + half * sub;
+          const double ph = frac_c(-((double)k0 - kcen) * delta);  // b_{k0} = e^{-j2pi (k0 - kcen) delta}
+          float br, bi;
+          sincospif(2.f * (float)ph, &bi, &br);
+          uint8_t* ahi = A_hi(slot);
+          for (int cch = 0; cch < nchunk16; ++cch) {
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              split_grid(br * a_scale, bi * a_scale, grid, inv_grid, hi[t], lo[t]);
+              cmul_df<float>(whr, whi, wlr, wli, br, bi, br, bi);
+            }
+            const uint32_t off = row_off + (uint32_t)(half * nchunk16 + cch) * 128u;
+            *reinterpret_cast<uint4*>(ahi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(ahi + pl.a_bytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
+          fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full_a[slot]);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: one TMEM lane (hypothesis) per thread
+    const int quarter = warp & 3;  // TMEM lanes [32 quarter, 32 quarter + 32) of this warp
+    const int h = quarter * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+    const int T = S + S * (S + 1) / 2;
+    const double cy = 0.5 * (sc.ny - 1), cv = 0.5 * (sc.nv - 1);
+    const double ky = sc.dy / sc.lambda, kv = sc.dv / sc.lambda;
+    int64_t i = 0;
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+      const int j = (int)(tile / a.n_tiles_j);
+      const int64_t hg = (tile - (int64_t)j * a.n_tiles_j) * NB_M + h;
+      const bool valid = hg < nhyp;
+      const int64_t p = valid ? hg / S : 0;
+      const int s = valid ? (int)(hg - p * S) : 0;
+      NbHyp hy;
+      if (valid) hy = nb_setup(sc, a, j, p, s);
+      else { hy.R = 1.0; hy.delta = 0.0; hy.uy = 0.0; hy.uz = 0.0; hy.gain = 1.0; hy.flag = 0; }
+      const double ty = ky * hy.uy, tv = kv * hy.uz;  // cycles per antenna step along y / z
+      double sv_, cv_;
+      sincospi(2.0 * frac_c(tv), &sv_, &cv_);  // antenna step along z, hi + lo (raised to the iv-th power)
+      const float svr = (float)cv_, svi = (float)sv_;
+      const float svlr = (float)(cv_ - (double)svr), svli = (float)(sv_ - (double)svi);
+      double cr = 0.0, ci = 0.0;
+      for (int pass = 0; pass < npass; ++pass, ++i) {
+        const int b = (int)(i % pl.nacc);
+        const int64_t u = i / pl.nacc;
+        const int mbeg = pass * pl.nbh;
+        const int mend = (mbeg + pl.nbh < sc.Na) ? mbeg + pl.nbh : sc.Na;
+        int iy = mbeg / sc.nv, iv = mbeg - iy * sc.nv;
+        float pr = 0.f, pi = 0.f, ar = 1.f, ai = 0.f;
+        bool anchor = true;
+        mbar_wait(&acc_full[b], (uint32_t)u & 1u);
+        tc_fence_after();
+        const uint32_t c1 = tmem + lane_addr + (uint32_t)(b * 2 * pl.nb), c2 = c1 + (uint32_t)pl.nb;
+        for (int m0 = mbeg; m0 < mend; m0 += 8) {
+          const uint32_t o = (uint32_t)(m0 - mbeg);
+          uint32_t r1[8], i1[8], r2[8], i2[8];
+          tmem_ld8x4(c1 + o, c1 + pl.nbh + o, c2 + o, c2 + pl.nbh + o, r1, i1, r2, i2);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if (m0 + e < mend) {
+              if (anchor || iv == 0) {  // row anchor a_{iy, iv} from an fp64-reduced phase
+                const double ph = frac_c(((double)iy - cy) * ty + ((double)iv - cv) * tv);
+                sincospif(2.f * (float)ph, &ai, &ar);
+                anchor = false;
+              }
+              const float wr = __uint_as_float(r1[e]) + __uint_as_float(r2[e]);
+              const float wi = __uint_as_float(i1[e]) + __uint_as_float(i2[e]);
+              pr = fmaf(ar, wr, fmaf(ai, wi, pr));   // conj(a) W
+              pi = fmaf(ar, wi, fmaf(-ai, wr, pi));
+              cmul_df<float>(svr, svi, svlr, svli, ar, ai, ar, ai);
+              if (++iv == sc.nv) {
+                iv = 0;
+                ++iy;
+                cr += (double)pr;
+                ci += (double)pi;
+                pr = 0.f;
+                pi = 0.f;
+              }
+            }
+          }
+        }
+        cr += (double)pr;  // a pass may end inside a row
+        ci += (double)pi;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+      }
+      if (valid) {
+        double sc_, cc_;
+        sincospi(2.0 * frac_c(hy.R * sc.fc_c), &sc_, &cc_);  // conj(carrier) = e^{+j2pi f_c R/c}
+        const double gs = hy.gain * (double)a.yscale_inv[j];
+        const double xr = (cr * cc_ - ci * sc_) * gs, xi = (cr * sc_ + ci * cc_) * gs;
+        a.terms[(p * J + j) * T + s] = make_double2(xr, xi);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)pl.tmem_cols)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------- launchers
+cudaError_t launch_nb_prep(const SceneDev& sc, const NbPlan& pl, const float2* y, uint8_t* bop, float* yscale_inv,
+                           cudaStream_t st) {
+  dim3 grid(8, sc.J);
+  nb_prep_kernel<<<grid, 512, 0, st>>>(sc, pl, y, bop, yscale_inv);
+  return cudaGetLastError();
+}
+cudaError_t launch_nb_gram(const SceneDev& sc, const NbArgs& a, int* pflag, cudaStream_t st) {
+  const int64_t n = a.P * sc.J;
+  nb_gram_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(sc, a, pflag);
+  return cudaGetLastError();
+}
+cudaError_t launch_nb_corr(const SceneDev& sc, const NbPlan& pl, const NbArgs& a, int num_sms, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(nb_corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  if (e != cudaSuccess) return e;
+  int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
+  if (grid < 1) grid = 1;
+  nb_corr_kernel<<<(unsigned)grid, NB_THREADS, pl.smem, st>>>(sc, pl, a);
+  return cudaGetLastError();
+}
+
+}  // namespace cdms

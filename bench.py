@@ -39,6 +39,23 @@ def fp32_peak_tflops(mhz: float) -> float:
     return 2.0 * FFMA_PER_SM_CLK * N_SM * mhz * 1e6 / 1e12
 
 
+def measured_tensor_peak():
+    """(dense bf16 TFLOP/s sustained, basis) from the driver-written MEASURED_PEAKS.json; fp16 has the same nominal
+    dense rate as bf16 on sm_100 (B200_PROFILING.md), so the bf16 figure is the kind::f16 peak."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS 8192^3, 4 s)"
+    except (OSError, KeyError, ValueError):
+        return 2250.0 * 0.72, "fallback: nominal 2.25 PFLOP/s x 0.72"
+
+
+def nb_tensor_path(args) -> bool:
+    """PLANAR_NB in fp32 runs the likelihood on the tensor cores (nbmma.cu) unless CDMS_NB_TENSOR=0."""
+    return (args.wavefront == "planar_nb" and args.precision == "fp32"
+            and os.environ.get("CDMS_NB_TENSOR", "1") != "0")
+
+
 class ClockSampler:
     """SM clock and throttle reasons sampled during the timed region: NVML polled every ~2 ms by a thread
     (short timed regions still get samples), nvidia-smi -lms 100 as the fallback when NVML is unavailable."""
@@ -264,19 +281,36 @@ def run_cdms(args):
         flop_launch = 8.0 * cfg.Nz * P_local * cfg.J * cfg.S / launches_per_step
         achieved = flop_launch / (kernel_ms / 1e3) / 1e12
         peak = fp32_peak_tflops(1965.0)
-        roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
-                "frac_at_measured_clock": (round(achieved / fp32_peak_tflops(clocks["sm_mhz"]), 4)
-                                           if clocks.get("sm_mhz") else None),
-                "kernel": "cdms::corr_kernel (row A2-A5: responses, correlation c, Gram G)", "kernel_ms": round(kernel_ms, 4),
-                "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
-                "launches_per_step": launches_per_step,
-                "flop_per_launch": flop_launch,
-                "traffic": (traffic_from_profiles(args.config) if args.particles is None and args.wavefront == "spherical"
-                            and args.precision == "fp32" else None),
-                "traffic_basis": "dram read+write bytes of one corr_kernel launch, ncu --set full "
-                                 "(profiles/loglik_traffic.json); the kernel is FP32-bound, traffic is particles + y"}
+        if nb_tensor_path(args):
+            # F2: the correlation is a real GEMM of 8 N_z flop per unit executed as four fp16 products
+            # (D1 = A_hi B_hi exact, D2 = the three residual products; nbmma.cu)
+            tflop_launch = 4.0 * flop_launch
+            t_achieved = tflop_launch / (kernel_ms / 1e3) / 1e12
+            t_peak, t_basis = measured_tensor_peak()
+            roof = {"bound": "tensor", "pipe": "tcgen05.mma kind::f16 (fp32 accumulate)",
+                    "achieved": round(t_achieved, 2), "peak": round(t_peak, 1), "unit": "TFLOP/s",
+                    "frac": round(t_achieved / t_peak, 4), "peak_basis": t_basis,
+                    "kernel": "cdms::nb_corr_kernel + nb_gram_kernel (rows A2-A5, F2)",
+                    "kernel_ms": round(kernel_ms, 4),
+                    "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
+                    "launches_per_step": launches_per_step, "flop_per_launch": tflop_launch,
+                    "flop_basis": "4 fp16 products x 8 N_z flop per (particle, PA, component)",
+                    "useful_fp32_equivalent_tflops": round(achieved, 3),
+                    "traffic": None}
+        else:
+            roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                    "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
+                    "frac_at_measured_clock": (round(achieved / fp32_peak_tflops(clocks["sm_mhz"]), 4)
+                                               if clocks.get("sm_mhz") else None),
+                    "kernel": "cdms::corr_kernel (row A2-A5: responses, correlation c, Gram G)", "kernel_ms": round(kernel_ms, 4),
+                    "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
+                    "launches_per_step": launches_per_step,
+                    "flop_per_launch": flop_launch,
+                    "traffic": (traffic_from_profiles(args.config) if args.particles is None and args.wavefront == "spherical"
+                                and args.precision == "fp32" else None),
+                    "traffic_basis": "dram read+write bytes of one corr_kernel launch, ncu --set full "
+                                     "(profiles/loglik_traffic.json); the kernel is FP32-bound, traffic is particles + y"}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",

@@ -111,6 +111,77 @@ __device__ __forceinline__ void split_grid(float x, float y, float grid, float i
   lo = pack_h2(x - hx, y - hy);
 }
 
+// packed fp32 pairs (FADD2 / FMUL2 / FFMA2 on sm_100): the A generator advances two subcarriers per instruction
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_split(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b) {
+  f2_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// x -> (hi, lo) with hi = x rounded to a multiple of grid by the magic constant M = 1.5 2^23 grid
+// ((x + M) - M, |x| < 2^22 grid; add.rn cannot be re-associated), lo = x - hi exactly
+__device__ __forceinline__ void f2_grid_split(f2_t x, f2_t M, f2_t& hi, f2_t& lo) {
+  hi = f2_sub(f2_add(x, M), M);
+  lo = f2_sub(x, hi);
+}
+
+// Epilogue rows for N_v = NV (passes aligned to rows): c += sum_iy conj(a_y[iy]) sum_iv conj(a_v[iv]) W[iy, iv]
+// with W = D1 + D2 read from TMEM, a_v[] precomputed in registers, a_y advanced by a hi + lo step per row.
+template <int NV>
+__device__ __forceinline__ void nb_epi_rows(uint32_t c1, uint32_t c2, int nbh, int nrows, const float (&avr)[NV],
+                                            const float (&avi)[NV], float ayr, float ayi, float syr, float syi,
+                                            float sylr, float syli, double& cr, double& ci) {
+  for (int r = 0; r < nrows; ++r) {
+    float sr0 = 0.f, si0 = 0.f, sr1 = 0.f, si1 = 0.f;
+#pragma unroll
+    for (int h8 = 0; h8 < NV / 8; ++h8) {
+      const uint32_t o = (uint32_t)(r * NV + h8 * 8);
+      uint32_t r1[8], i1[8], r2[8], i2[8];
+      tmem_ld8x4(c1 + o, c1 + nbh + o, c2 + o, c2 + nbh + o, r1, i1, r2, i2);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int iv = h8 * 8 + e;
+        const float wr = __uint_as_float(r1[e]) + __uint_as_float(r2[e]);
+        const float wi = __uint_as_float(i1[e]) + __uint_as_float(i2[e]);
+        if (e & 1) {
+          sr1 = fmaf(avr[iv], wr, fmaf(avi[iv], wi, sr1));
+          si1 = fmaf(avr[iv], wi, fmaf(-avi[iv], wr, si1));
+        } else {
+          sr0 = fmaf(avr[iv], wr, fmaf(avi[iv], wi, sr0));
+          si0 = fmaf(avr[iv], wi, fmaf(-avi[iv], wr, si0));
+        }
+      }
+    }
+    const float sr = sr0 + sr1, si = si0 + si1;
+    cr += (double)fmaf(ayr, sr, ayi * si);
+    ci += (double)fmaf(ayr, si, -ayi * sr);
+    cmul_df<float>(syr, syi, sylr, syli, ayr, ayi, ayr, ayi);
+  }
+}
+
 // ---------------------------------------------------------------------------- per-hypothesis set-up (fp64)
 struct NbHyp {
   double R, delta, uy, uz, gain;
@@ -411,7 +482,8 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
     const int nchunk16 = sub / 4;    // 16-byte chunks (4 subcarriers) per thread per stage
     const double kcen = 0.5 * (sc.nf - 1);
     const float a_scale = (float)(1 << NB_SCALE_LOG2);
-    const float grid = ldexpf(1.f, NB_SCALE_LOG2 - pl.pexp), inv_grid = ldexpf(1.f, pl.pexp - NB_SCALE_LOG2);
+    const float gmag = 1.5f * 8388608.f * ldexpf(1.f, NB_SCALE_LOG2 - pl.pexp);  // 1.5 2^23 grid
+    const f2_t M2 = f2(gmag, gmag);
     const uint32_t row_off = (uint32_t)(h >> 3) * sbo + (uint32_t)(h & 7) * 16u;
     int64_t g = 0;
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
@@ -422,27 +494,52 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         const int64_t p = hg / S;
         delta = nb_setup(sc, a, j, p, (int)(hg - p * S)).delta;
       }
-      // w = e^{-j2pi delta} as an unevaluated sum hi + lo: w is raised to the k-th power along the stage, so a
-      // single fp32 rounding would tilt every subcarrier's phase coherently
-      double sw, cw;
+      // w = e^{-j2pi delta} and w^2 as unevaluated sums hi + lo: they are raised to powers along the stage, so a
+      // single fp32 rounding would tilt every subcarrier's phase coherently.  The thread
+      // runs two interleaved recurrences (b_k, b_{k+1}) -> (b_{k+2}, b_{k+3}) as the two lanes of f32x2 registers.
+      double sw, cw, s2, c2;
       sincospi(2.0 * frac_c(delta), &sw, &cw);
+      sincospi(2.0 * frac_c(2.0 * delta), &s2, &c2);
       const float whr = (float)cw, whi = (float)-sw;
       const float wlr = (float)(cw - (double)whr), wli = (float)(-sw - (double)whi);
+      const float v2hr = (float)c2, v2hi = (float)-s2;
+      const float v2lr = (float)(c2 - (double)v2hr), v2li = (float)(-s2 - (double)v2hi);
+      const f2_t W2hr = f2(v2hr, v2hr), W2hi = f2(v2hi, v2hi), nW2hi = f2(-v2hi, -v2hi);
+      const f2_t W2lr = f2(v2lr, v2lr), W2li = f2(v2li, v2li), nW2li = f2(-v2li, -v2li);
       for (int pass = 0; pass < npass; ++pass) {
         for (int q = 0; q < n_chunks; ++q, ++g) {
           const int slot = (int)(g % nst);
           if (g >= nst) mbar_wait(&empty[slot], (uint32_t)((g / nst) - 1) & 1u);
           const int k0 = q * (kc / 2) + half * sub;
           const double ph = frac_c(-((double)k0 - kcen) * delta);  // b_{k0} = e^{-j2pi (k0 - kcen) delta}
-          float br, bi;
-          sincospif(2.f * (float)ph, &bi, &br);
+          float br0, bi0, br1, bi1;
+          sincospif(2.f * (float)ph, &bi0, &br0);
+          br0 *= a_scale;
+          bi0 *= a_scale;
+          cmul_df<float>(whr, whi, wlr, wli, br0, bi0, br1, bi1);
+          f2_t BR = f2(br0, br1), BI = f2(bi0, bi1);
           uint8_t* ahi = A_hi(slot);
           for (int cch = 0; cch < nchunk16; ++cch) {
             uint32_t hi[4], lo[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              split_grid(br * a_scale, bi * a_scale, grid, inv_grid, hi[t], lo[t]);
-              cmul_df<float>(whr, whi, wlr, wli, br, bi, br, bi);
+            for (int t2 = 0; t2 < 2; ++t2) {
+              f2_t hr, lr, hI, lI;
+              f2_grid_split(BR, M2, hr, lr);
+              f2_grid_split(BI, M2, hI, lI);
+              float x0, x1, y0, y1;
+              f2_split(hr, x0, x1);
+              f2_split(hI, y0, y1);
+              hi[2 * t2] = pack_h2(x0, y0);
+              hi[2 * t2 + 1] = pack_h2(x1, y1);
+              f2_split(lr, x0, x1);
+              f2_split(lI, y0, y1);
+              lo[2 * t2] = pack_h2(x0, y0);
+              lo[2 * t2 + 1] = pack_h2(x1, y1);
+              // (BR, BI) <- (BR, BI) w^2, hi + lo step (cmul_df on both lanes)
+              const f2_t lrr = f2_fma(W2lr, BR, f2_mul(nW2li, BI)), lii = f2_fma(W2lr, BI, f2_mul(W2li, BR));
+              const f2_t nBR = f2_fma(W2hr, BR, f2_fma(nW2hi, BI, lrr));
+              BI = f2_fma(W2hr, BI, f2_fma(W2hi, BR, lii));
+              BR = nBR;
             }
             const uint32_t off = row_off + (uint32_t)(half * nchunk16 + cch) * 128u;
             *reinterpret_cast<uint4*>(ahi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
@@ -477,6 +574,18 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
       sincospi(2.0 * frac_c(tv), &sv_, &cv_);  // antenna step along z, hi + lo (raised to the iv-th power)
       const float svr = (float)cv_, svi = (float)sv_;
       const float svlr = (float)(cv_ - (double)svr), svli = (float)(sv_ - (double)svi);
+      double sy_, cy_;
+      sincospi(2.0 * frac_c(ty), &sy_, &cy_);  // antenna step along y (row to row), hi + lo
+      const float syr = (float)cy_, syi = (float)sy_;
+      const float sylr = (float)(cy_ - (double)syr), syli = (float)(sy_ - (double)syi);
+      // rows of N_v = 8 / 16 with passes on row boundaries: a_v[] in registers (row-structured epilogue)
+      const int rowmode = (sc.nv == 16 && pl.nbh % 16 == 0) ? 16 : (sc.nv == 8 ? 8 : 0);
+      float avr[16], avi[16];
+      if (rowmode) {
+        sincospif(2.f * (float)frac_c(-cv * tv), &avi[0], &avr[0]);
+#pragma unroll
+        for (int t = 1; t < 16; ++t) cmul_df<float>(svr, svi, svlr, svli, avr[t - 1], avi[t - 1], avr[t], avi[t]);
+      }
       double cr = 0.0, ci = 0.0;
       for (int pass = 0; pass < npass; ++pass, ++i) {
         const int b = (int)(i % pl.nacc);
@@ -486,10 +595,23 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         int iy = mbeg / sc.nv, iv = mbeg - iy * sc.nv;
         float pr = 0.f, pi = 0.f, ar = 1.f, ai = 0.f;
         bool anchor = true;
+        float ayr = 1.f, ayi = 0.f;
+        if (rowmode) sincospif(2.f * (float)frac_c(((double)iy - cy) * ty), &ayi, &ayr);
         mbar_wait(&acc_full[b], (uint32_t)u & 1u);
         tc_fence_after();
         const uint32_t c1 = tmem + lane_addr + (uint32_t)(b * 2 * pl.nb), c2 = c1 + (uint32_t)pl.nb;
-        for (int m0 = mbeg; m0 < mend; m0 += 8) {
+        if (rowmode == 16) {
+          float r16[16], i16[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) { r16[t] = avr[t]; i16[t] = avi[t]; }
+          nb_epi_rows<16>(c1, c2, pl.nbh, (mend - mbeg) / 16, r16, i16, ayr, ayi, syr, syi, sylr, syli, cr, ci);
+        } else if (rowmode == 8) {
+          float r8[8], i8[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) { r8[t] = avr[t]; i8[t] = avi[t]; }
+          nb_epi_rows<8>(c1, c2, pl.nbh, (mend - mbeg) / 8, r8, i8, ayr, ayi, syr, syi, sylr, syli, cr, ci);
+        }
+        for (int m0 = mbeg; m0 < (rowmode ? mbeg : mend); m0 += 8) {
           const uint32_t o = (uint32_t)(m0 - mbeg);
           uint32_t r1[8], i1[8], r2[8], i2[8];
           tmem_ld8x4(c1 + o, c1 + pl.nbh + o, c2 + o, c2 + pl.nbh + o, r1, i1, r2, i2);

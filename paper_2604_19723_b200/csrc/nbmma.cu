@@ -28,8 +28,8 @@
 //                canonical K-major no-swizzle layout by nb_prep_kernel) into the stage ring
 //   warp 1       one lane issues tcgen05.mma (kind::f16, M = 128 hypotheses, N = 2 nbh <= 256 per pass,
 //                four per K-step of 16) and tcgen05.commit's the stage / accumulator barriers
-//   warps 2..9   generate A (2 threads per hypothesis row, fp64 set-up, fp32 phasor recurrence with a hi+lo
-//                step anchored per stage from an fp64-reduced phase, grid/fp16 split) into the same ring
+//   warps 2..9   generate A (two groups of 4 warps on alternate stages, one row per thread: fp64 set-up,
+//                anchor x per-tile table of w^j, grid/fp16 split, f32x2 pairs) into the same ring
 //   warps 10..13 epilogue: tcgen05.ld one TMEM lane (= one hypothesis) each, W = D1 + D2, contract with conj(a)
 //                (fp32 rows of N_v, fp64 across rows), apply gain, carrier and the operand scales -> c_s
 // Work item = (tile of 128 hypotheses of one PA, antenna pass); arrays with 2 ceil8(N_a) > 256 take several
@@ -181,6 +181,23 @@ __device__ __forceinline__ void nb_epi_rows(uint32_t c1, uint32_t c2, int nbh, i
     cmul_df<float>(syr, syi, sylr, syli, ayr, ayi, ayr, ayi);
   }
 }
+
+// Position in a ring of n mbarrier-guarded slots: slot index, phase parity of the current use, and whether the
+// slot has been used before (producers then wait for the consumer's release of the previous use, parity phase^1).
+// 32-bit increments keep the counters warp-uniform (64-bit div/mod would go through a subroutine).
+struct RingPos {
+  int slot = 0, n = 1;
+  uint32_t phase = 0;
+  bool reused = false;
+  __device__ __forceinline__ explicit RingPos(int n_) : n(n_) {}
+  __device__ __forceinline__ void next() {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+      reused = true;
+    }
+  }
+};
 
 // ---------------------------------------------------------------------------- per-hypothesis set-up (fp64)
 struct NbHyp {
@@ -377,7 +394,9 @@ __global__ void nb_gram_kernel(const __grid_constant__ SceneDev sc, const NbArgs
 __global__ void __launch_bounds__(NB_THREADS, 1)
     nb_corr_kernel(const __grid_constant__ SceneDev sc, const NbPlan pl, const NbArgs a) {
   extern __shared__ __align__(1024) uint8_t nb_smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so role branches keep loop state and UMMA descriptors
+  // in uniform registers (no per-MMA ELECT/R2UR waterfall)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int nst = pl.nst, kc = pl.kc, npass = pl.n_pass;
   const uint32_t stage_bytes = 2 * (pl.a_bytes + pl.b_bytes);
   uint8_t* ring = nb_smem;
@@ -394,7 +413,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
-      mbar_init(&full_a[s], NB_GEN_WARPS);
+      mbar_init(&full_a[s], NB_GEN_WARPS / 2);  // one group of generator warps per stage
       mbar_init(&full_b[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -423,14 +442,14 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
   if (warp == 0) {
     // ---------------- B producer
     if (lane == 0) {
-      int64_t g = 0;
+      RingPos rp(nst);
       for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
         const int j = (int)(tile / a.n_tiles_j);
         const uint8_t* src = a.bop + (size_t)j * npass * n_chunks * 2 * pl.b_bytes;
         for (int pass = 0; pass < npass; ++pass) {
-          for (int q = 0; q < n_chunks; ++q, ++g) {
-            const int slot = (int)(g % nst);
-            if (g >= nst) mbar_wait(&empty[slot], (uint32_t)((g / nst) - 1) & 1u);
+          for (int q = 0; q < n_chunks; ++q, rp.next()) {
+            const int slot = rp.slot;
+            if (rp.reused) mbar_wait(&empty[slot], rp.phase ^ 1u);
             mbar_expect_tx(&full_b[slot], 2 * pl.b_bytes);
             tma_load_1d(B_hi(slot), src + ((size_t)pass * n_chunks + q) * 2 * pl.b_bytes, 2 * pl.b_bytes,
                         &full_b[slot]);
@@ -440,52 +459,64 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: D1 += A_hi B_hi (exact), D2 += A_hi B_lo + A_lo B_hi + A_lo B_lo
-    if (lane == 0) {
-      int64_t g = 0, i = 0;
+    // The whole warp runs the loop (barrier waits, descriptors: warp-uniform values in uniform registers); lane 0
+    // issues.  Descriptors are the slot-0 ones plus address offsets in 16-byte units (the 14-bit start-address
+    // field cannot carry: dynamic shared memory < 256 KB).  At N = 128 an MMA lasts ~64 clocks, so per-MMA issue
+    // overhead decides whether the tensor pipe stays fed.
+    {
+      RingPos rp(nst), ap(pl.nacc);
       const uint32_t idesc = umma_idesc_f16(NB_M, pl.nb);
+      const uint64_t dA0 = umma_sdesc(smem_u32(A_hi(0)), 128, sbo), dB0 = umma_sdesc(smem_u32(B_hi(0)), 128, sbo);
+      const uint64_t slot_step = stage_bytes >> 4, a_lo_step = pl.a_bytes >> 4, b_lo_step = pl.b_bytes >> 4;
+      const int nks = kc / 16;
       for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-        for (int pass = 0; pass < npass; ++pass, ++i) {
-          const int b = (int)(i % pl.nacc);
-          const int64_t u = i / pl.nacc;
-          if (i >= pl.nacc) mbar_wait(&acc_empty[b], (uint32_t)(u - 1) & 1u);
+        for (int pass = 0; pass < npass; ++pass, ap.next()) {
+          const int b = ap.slot;
+          if (ap.reused) mbar_wait(&acc_empty[b], ap.phase ^ 1u);
           tc_fence_after();
           const uint32_t d1 = tmem + (uint32_t)(b * 2 * pl.nb), d2 = d1 + (uint32_t)pl.nb;
-          for (int q = 0; q < n_chunks; ++q, ++g) {
-            const int slot = (int)(g % nst);
-            const uint32_t par = (uint32_t)(g / nst) & 1u;
+          for (int q = 0; q < n_chunks; ++q, rp.next()) {
+            const int slot = rp.slot;
+            const uint32_t par = rp.phase;
             mbar_wait(&full_b[slot], par);
             mbar_wait(&full_a[slot], par);
             tc_fence_after();
-            const uint32_t a_hi = smem_u32(A_hi(slot)), a_lo = a_hi + pl.a_bytes;
-            const uint32_t b_hi = smem_u32(B_hi(slot)), b_lo = b_hi + pl.b_bytes;
-            for (int ks = 0; ks < kc / 16; ++ks) {
-              const uint32_t koff = (uint32_t)ks * 256u;
-              const uint64_t dah = umma_sdesc(a_hi + koff, 128, sbo), dal = umma_sdesc(a_lo + koff, 128, sbo);
-              const uint64_t dbh = umma_sdesc(b_hi + koff, 128, sbo), dbl = umma_sdesc(b_lo + koff, 128, sbo);
-              const uint32_t acc0 = (q | ks) ? 1u : 0u;
-              umma_f16(d1, dah, dbh, idesc, acc0);
-              umma_f16(d2, dah, dbl, idesc, acc0);
-              umma_f16(d2, dal, dbh, idesc, 1u);
-              umma_f16(d2, dal, dbl, idesc, 1u);
+            const uint64_t sa = dA0 + (uint64_t)slot * slot_step, sb = dB0 + (uint64_t)slot * slot_step;
+            if (lane == 0) {
+              for (int ks = 0; ks < nks; ++ks) {
+                const uint64_t dah = sa + (uint64_t)(ks * 16), dbh = sb + (uint64_t)(ks * 16);
+                const uint64_t dal = dah + a_lo_step, dbl = dbh + b_lo_step;
+                const uint32_t acc0 = (q | ks) ? 1u : 0u;
+                umma_f16(d1, dah, dbh, idesc, acc0);
+                umma_f16(d2, dah, dbl, idesc, acc0);
+                umma_f16(d2, dal, dbh, idesc, 1u);
+                umma_f16(d2, dal, dbl, idesc, 1u);
+              }
+              umma_commit(&empty[slot]);
             }
-            umma_commit(&empty[slot]);
+            __syncwarp();
           }
-          umma_commit(&acc_full[b]);
+          if (lane == 0) umma_commit(&acc_full[b]);
+          __syncwarp();
         }
       }
     }
   } else if (warp < 2 + NB_GEN_WARPS) {
-    // ---------------- A generators: thread -> (row h, half of each stage's subcarriers)
+    // ---------------- A generators: two groups of 4 warps take alternate stages; thread -> row h of its group
+    // b_k = e^{-j2pi (k - kcen) delta} for the stage's kc/2 subcarriers as A_a t[j]: an anchor A_a per 16
+    // subcarriers from the fp64-reduced phase and a per-tile table t[j] = w^j (j < 16, fp64, rounded once), so
+    // each phasor carries one fp32 rounding (no coherent drift of a raised step) and no
+    // dependency chain; pairs of subcarriers share f32x2 instructions.
     const int gt = threadIdx.x - 64;
-    const int h = gt & (NB_M - 1), half = gt >> 7;
-    const int sub = kc / 4;          // subcarriers per thread per stage
-    const int nchunk16 = sub / 4;    // 16-byte chunks (4 subcarriers) per thread per stage
+    const int h = gt & (NB_M - 1), grp = gt >> 7;
+    const int nsub = kc / 2;  // subcarriers per stage (8, 16 or 32)
     const double kcen = 0.5 * (sc.nf - 1);
     const float a_scale = (float)(1 << NB_SCALE_LOG2);
     const float gmag = 1.5f * 8388608.f * ldexpf(1.f, NB_SCALE_LOG2 - pl.pexp);  // 1.5 2^23 grid
     const f2_t M2 = f2(gmag, gmag);
     const uint32_t row_off = (uint32_t)(h >> 3) * sbo + (uint32_t)(h & 7) * 16u;
-    int64_t g = 0;
+    RingPos rp(nst);
+    int gs = 0;  // stage counter: this group generates the stages with gs % 2 == grp
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
       const int j = (int)(tile / a.n_tiles_j);
       const int64_t hg = (tile - (int64_t)j * a.n_tiles_j) * NB_M + h;
@@ -494,56 +525,61 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         const int64_t p = hg / S;
         delta = nb_setup(sc, a, j, p, (int)(hg - p * S)).delta;
       }
-      // w = e^{-j2pi delta} and w^2 as unevaluated sums hi + lo: they are raised to powers along the stage, so a
-      // single fp32 rounding would tilt every subcarrier's phase coherently.  The thread
-      // runs two interleaved recurrences (b_k, b_{k+1}) -> (b_{k+2}, b_{k+3}) as the two lanes of f32x2 registers.
-      double sw, cw, s2, c2;
-      sincospi(2.0 * frac_c(delta), &sw, &cw);
-      sincospi(2.0 * frac_c(2.0 * delta), &s2, &c2);
-      const float whr = (float)cw, whi = (float)-sw;
-      const float wlr = (float)(cw - (double)whr), wli = (float)(-sw - (double)whi);
-      const float v2hr = (float)c2, v2hi = (float)-s2;
-      const float v2lr = (float)(c2 - (double)v2hr), v2li = (float)(-s2 - (double)v2hi);
-      const f2_t W2hr = f2(v2hr, v2hr), W2hi = f2(v2hi, v2hi), nW2hi = f2(-v2hi, -v2hi);
-      const f2_t W2lr = f2(v2lr, v2lr), W2li = f2(v2li, v2li), nW2li = f2(-v2li, -v2li);
-      for (int pass = 0; pass < npass; ++pass) {
-        for (int q = 0; q < n_chunks; ++q, ++g) {
-          const int slot = (int)(g % nst);
-          if (g >= nst) mbar_wait(&empty[slot], (uint32_t)((g / nst) - 1) & 1u);
-          const int k0 = q * (kc / 2) + half * sub;
-          const double ph = frac_c(-((double)k0 - kcen) * delta);  // b_{k0} = e^{-j2pi (k0 - kcen) delta}
-          float br0, bi0, br1, bi1;
-          sincospif(2.f * (float)ph, &bi0, &br0);
-          br0 *= a_scale;
-          bi0 *= a_scale;
-          cmul_df<float>(whr, whi, wlr, wli, br0, bi0, br1, bi1);
-          f2_t BR = f2(br0, br1), BI = f2(bi0, bi1);
-          uint8_t* ahi = A_hi(slot);
-          for (int cch = 0; cch < nchunk16; ++cch) {
-            uint32_t hi[4], lo[4];
+      f2_t TR[8], TI[8];  // t[2i], t[2i+1] in the two lanes
+      {
+        double sw, cw;
+        sincospi(2.0 * frac_c(delta), &sw, &cw);
+        double tr = 1.0, ti = 0.0;
 #pragma unroll
-            for (int t2 = 0; t2 < 2; ++t2) {
-              f2_t hr, lr, hI, lI;
-              f2_grid_split(BR, M2, hr, lr);
-              f2_grid_split(BI, M2, hI, lI);
-              float x0, x1, y0, y1;
-              f2_split(hr, x0, x1);
-              f2_split(hI, y0, y1);
-              hi[2 * t2] = pack_h2(x0, y0);
-              hi[2 * t2 + 1] = pack_h2(x1, y1);
-              f2_split(lr, x0, x1);
-              f2_split(lI, y0, y1);
-              lo[2 * t2] = pack_h2(x0, y0);
-              lo[2 * t2 + 1] = pack_h2(x1, y1);
-              // (BR, BI) <- (BR, BI) w^2, hi + lo step (cmul_df on both lanes)
-              const f2_t lrr = f2_fma(W2lr, BR, f2_mul(nW2li, BI)), lii = f2_fma(W2lr, BI, f2_mul(W2li, BR));
-              const f2_t nBR = f2_fma(W2hr, BR, f2_fma(nW2hi, BI, lrr));
-              BI = f2_fma(W2hr, BI, f2_fma(W2hi, BR, lii));
-              BR = nBR;
+        for (int i = 0; i < 8; ++i) {
+          const double ur = tr * cw + ti * sw, ui = ti * cw - tr * sw;  // t w, w = e^{-j2pi delta}
+          TR[i] = f2((float)tr, (float)ur);
+          TI[i] = f2((float)ti, (float)ui);
+          tr = ur * cw + ui * sw;
+          ti = ui * cw - ur * sw;
+        }
+      }
+      for (int pass = 0; pass < npass; ++pass) {
+        for (int q = 0; q < n_chunks; ++q, rp.next(), ++gs) {
+          if ((gs & 1) != grp) continue;
+          const int slot = rp.slot;
+          if (rp.reused) mbar_wait(&empty[slot], rp.phase ^ 1u);
+          uint8_t* ahi = A_hi(slot);
+          for (int a16 = 0; a16 < nsub; a16 += 16) {
+            const int k0 = q * nsub + a16;
+            const double ph = frac_c(-((double)k0 - kcen) * delta);  // anchor b_{k0}
+            float ar, ai;
+            sincospif(2.f * (float)ph, &ai, &ar);
+            ar *= a_scale;
+            ai *= a_scale;
+            const f2_t AR = f2(ar, ar), AI = f2(ai, ai), nAI = f2(-ai, -ai);
+            const int npair = (nsub - a16) < 16 ? (nsub - a16) / 2 : 8;
+#pragma unroll
+            for (int p4 = 0; p4 < 8; p4 += 2) {  // 4 subcarriers = one 16-byte chunk per piece
+              if (p4 < npair) {
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int t2 = 0; t2 < 2; ++t2) {
+                  const f2_t BR = f2_fma(AR, TR[p4 + t2], f2_mul(nAI, TI[p4 + t2]));
+                  const f2_t BI = f2_fma(AR, TI[p4 + t2], f2_mul(AI, TR[p4 + t2]));
+                  f2_t hr, lr, hI, lI;
+                  f2_grid_split(BR, M2, hr, lr);
+                  f2_grid_split(BI, M2, hI, lI);
+                  float x0, x1, y0, y1;
+                  f2_split(hr, x0, x1);
+                  f2_split(hI, y0, y1);
+                  hi[2 * t2] = pack_h2(x0, y0);
+                  hi[2 * t2 + 1] = pack_h2(x1, y1);
+                  f2_split(lr, x0, x1);
+                  f2_split(lI, y0, y1);
+                  lo[2 * t2] = pack_h2(x0, y0);
+                  lo[2 * t2 + 1] = pack_h2(x1, y1);
+                }
+                const uint32_t off = row_off + (uint32_t)((a16 + 2 * p4) / 4) * 128u;
+                *reinterpret_cast<uint4*>(ahi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(ahi + pl.a_bytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+              }
             }
-            const uint32_t off = row_off + (uint32_t)(half * nchunk16 + cch) * 128u;
-            *reinterpret_cast<uint4*>(ahi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<uint4*>(ahi + pl.a_bytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           }
           fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
           __syncwarp();
@@ -559,7 +595,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
     const int T = S + S * (S + 1) / 2;
     const double cy = 0.5 * (sc.ny - 1), cv = 0.5 * (sc.nv - 1);
     const double ky = sc.dy / sc.lambda, kv = sc.dv / sc.lambda;
-    int64_t i = 0;
+    RingPos ap(pl.nacc);
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
       const int j = (int)(tile / a.n_tiles_j);
       const int64_t hg = (tile - (int64_t)j * a.n_tiles_j) * NB_M + h;
@@ -587,9 +623,8 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         for (int t = 1; t < 16; ++t) cmul_df<float>(svr, svi, svlr, svli, avr[t - 1], avi[t - 1], avr[t], avi[t]);
       }
       double cr = 0.0, ci = 0.0;
-      for (int pass = 0; pass < npass; ++pass, ++i) {
-        const int b = (int)(i % pl.nacc);
-        const int64_t u = i / pl.nacc;
+      for (int pass = 0; pass < npass; ++pass, ap.next()) {
+        const int b = ap.slot;
         const int mbeg = pass * pl.nbh;
         const int mend = (mbeg + pl.nbh < sc.Na) ? mbeg + pl.nbh : sc.Na;
         int iy = mbeg / sc.nv, iv = mbeg - iy * sc.nv;
@@ -597,7 +632,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         bool anchor = true;
         float ayr = 1.f, ayi = 0.f;
         if (rowmode) sincospif(2.f * (float)frac_c(((double)iy - cy) * ty), &ayi, &ayr);
-        mbar_wait(&acc_full[b], (uint32_t)u & 1u);
+        mbar_wait(&acc_full[b], ap.phase);
         tc_fence_after();
         const uint32_t c1 = tmem + lane_addr + (uint32_t)(b * 2 * pl.nb), c2 = c1 + (uint32_t)pl.nb;
         if (rowmode == 16) {

@@ -9,7 +9,7 @@
 //   D[h, n] = sum_kk A[h, kk] B[n, kk],   A[h, 2k + {0,1}] = (Re b_h[k], Im b_h[k])          (generated on chip)
 //   B[m, .] = (Re y[m,k], Im y[m,k]),  B[Nh + m, .] = (Im y[m,k], -Re y[m,k])               (one per PA)
 // so D[h, m] = Re W_h[m] and D[h, Nh + m] = Im W_h[m].  The Gram matrix of the same hypotheses factors into
-// three Dirichlet kernels (closed form, fp64, nb_gram_kernel).
+// three Dirichlet kernels (closed form: fp64 set-up and range reduction, fp32 sines; nb_gram_kernel).
 //
 // Precision (tools/f2_precision.py).  Two measured properties of the tensor core shape the split:
 //  (1) fp16 subnormal operands read as zero -> both operands are scaled by powers of two into fp16's upper
@@ -348,7 +348,26 @@ __global__ void nb_prep_kernel(const __grid_constant__ SceneDev sc, const NbPlan
   }
 }
 
-// ---------------------------------------------------------------------------- Gram (closed form, fp64)
+// D_N(x) = sin(pi N x) / sin(pi x) (C-amb-13): x = n + xr, D_N(x) = (-1)^{n (N-1)} D_N(xr); both sines reduced in
+// fp64 (sin(pi N xr) = sin(pi t), t = N xr mod 2 in [-1, 1]) and evaluated in fp32 (relative error ~1e-7, the
+// precision of K1's per-antenna fp32 Gram terms); second-order series below |xr| = 1e-6.
+__device__ __forceinline__ float dirichlet_rr(double x, int N) {
+  const double n = rint(x);
+  const double xr = x - n;
+  double t = (double)N * xr;
+  t -= 2.0 * rint(0.5 * t);
+  const float fx = (float)xr;
+  float d;
+  if (fabsf(fx) < 1e-6f) {
+    d = (float)N * (1.f - (float)(PI * PI / 6.0) * ((float)N * (float)N - 1.f) * fx * fx);
+  } else {
+    d = sinpif((float)t) / sinpif(fx);
+  }
+  if (((N - 1) & 1) && (((long long)n) & 1)) d = -d;
+  return d;
+}
+
+// ---------------------------------------------------------------------------- Gram (closed form)
 // G_rc = psi_r^H psi_c = g_r g_c e^{j2pi f_c (R_r - R_c)/c} D_Nf(df (R_r - R_c)/c)
 //        D_Ny(d_y (u'_y,c - u'_y,r)/lambda) D_Nv(d_v (u'_z,c - u'_z,r)/lambda),  G_ss = g_s^2 N_z
 // (centred template and subcarrier grid: every factor is a real Dirichlet kernel, C-amb-13 for D_N).
@@ -377,15 +396,12 @@ __global__ void nb_gram_kernel(const __grid_constant__ SceneDev sc, const NbArgs
         out[t] = make_double2(nz * g[r] * g[r], 0.0);
         continue;
       }
-      double sn, cs;
-      sincospi(2.0 * frac_c((R[r] - R[c]) * sc.fc_c), &sn, &cs);
-      const double xf = dl[r] - dl[c], xy = ky * (uy[c] - uy[r]), xv = kv * (uz[c] - uz[r]);
-      const double nf_ = rint(xf), ny_ = rint(xy), nv_ = rint(xv);
-      const double D = dirichlet<double>(xf - nf_, (long long)nf_, sc.nf) *
-                       dirichlet<double>(xy - ny_, (long long)ny_, sc.ny) *
-                       dirichlet<double>(xv - nv_, (long long)nv_, sc.nv);
-      const double m = g[r] * g[c] * D;
-      out[t] = make_double2(m * cs, m * sn);
+      float sn, cs;
+      sincospif(2.f * (float)frac_c((R[r] - R[c]) * sc.fc_c), &sn, &cs);
+      const float D = dirichlet_rr(dl[r] - dl[c], sc.nf) * dirichlet_rr(ky * (uy[c] - uy[r]), sc.ny) *
+                      dirichlet_rr(kv * (uz[c] - uz[r]), sc.nv);
+      const double m = g[r] * g[c] * (double)D;
+      out[t] = make_double2(m * (double)cs, m * (double)sn);
     }
   }
 }

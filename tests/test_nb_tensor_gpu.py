@@ -51,11 +51,11 @@ def test_nb_terms_parity(cd, ctx, orc, shape):
     ec = np.max(np.abs(c - co) / (np.sqrt(cfg.Nz) * zn[None, :, None]))
     eG = np.max(np.abs(G - Go)) / cfg.Nz
     record("nb_c_rel", ec, 1e-6, shape=shape)
-    # G: both sides are fp64, but both evaluate carrier phases f R / c of 1e2..1e3 cycles, so each carries an
-    # absolute phase error ~ cycles * 2pi * 2^-53 ~ 1e-13..1e-12 (the oracle's direct sums as well)
-    record("nb_G_rel", eG, 1e-11, shape=shape)
+    # G: closed form with fp64 set-up and range reduction, fp32 sines (nbmma.cu dirichlet_rr) -- three factors
+    # of ~2 fp32 ulp each plus the carrier phasor, relative to the G scale N_z (K1's Gram terms are fp32 too)
+    record("nb_G_rel", eG, 2e-6, shape=shape)
     assert ec <= 1e-6, ec
-    assert eG <= 1e-11, eG
+    assert eG <= 2e-6, eG
 
 
 @pytest.mark.parametrize("shape", SHAPES)

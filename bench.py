@@ -296,7 +296,9 @@ def run_cdms(args):
                     "launches_per_step": launches_per_step, "flop_per_launch": tflop_launch,
                     "flop_basis": "4 fp16 products x 8 N_z flop per (particle, PA, component)",
                     "useful_fp32_equivalent_tflops": round(achieved, 3),
-                    "traffic": None}
+                    "traffic": (traffic_from_profiles(args.config + "_planar_nb") if args.particles is None else None),
+                    "traffic_basis": "dram read+write bytes of one nb_corr_kernel launch, ncu --set full "
+                                     "(profiles/loglik_traffic.json); particles in, c out (tensor-bound)"}
         else:
             roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4),

@@ -594,3 +594,131 @@ void orc_moment_match(double mu_re, double mu_im, double gamma, double exist, do
   out[1] = exist * mu_im;
   out[2] = exist * (gamma + (mu_re * mu_re + mu_im * mu_im) * (1.0 - exist));
 }
+
+/* ------------------------------------------------------------------ F3 birth proposal */
+
+/* Observation residual z~_j = Pi_perp_j z_j, Pi_perp_j = I - Psi_j Psi_j^dagger with
+ * Psi_j = [psi(x_hat, LOS) psi(x_hat, sfv_1) ... psi(x_hat, sfv_L)] in C^{Nz x (L+1)}, the
+ * steering vectors at the predicted MMSE state for the LOS and the legacy PFs' MMSE SFVs.  Psi^dagger is the
+ * pseudo-inverse of a full-column-rank Psi: Psi^dagger z = (Psi^H Psi)^{-1} Psi^H z, solved by Cholesky.
+ * y, z~: [J][Nz] (n = k Na + m).  ORC_EINVAL if Psi^H Psi is singular. */
+int orc_birth_residual(const orc_scene* sc, const double* x_hat /*[3]*/, const double* sfv_legacy /*[L][3]*/,
+                       int L, const double complex* y, double complex* zr) {
+  int n = L + 1, J = sc->J;
+  size_t nz = (size_t)sc->nf * sc->ny * sc->nv;
+  double complex* Psi = (double complex*)malloc(sizeof(double complex) * nz * n);
+  double complex* G = (double complex*)malloc(sizeof(double complex) * n * n);
+  double complex* b = (double complex*)malloc(sizeof(double complex) * n);
+  int st = ORC_OK;
+  for (int j = 0; j < J && !st; ++j) {
+    for (int s = 0; s < n && !st; ++s)
+      st = orc_response(sc, x_hat, j, s, s ? sfv_legacy + 3 * (s - 1) : NULL, sc->wavefront, Psi + (size_t)s * nz);
+    if (st) break;
+    const double complex* z = y + (size_t)j * nz;
+    for (int r = 0; r < n; ++r) {  /* Psi^H Psi (lower part) and Psi^H z */
+      for (int c = 0; c <= r; ++c) {
+        double complex acc = 0.0;
+        for (size_t k = 0; k < nz; ++k) acc += conj(Psi[(size_t)r * nz + k]) * Psi[(size_t)c * nz + k];
+        G[r * n + c] = acc;
+      }
+      double complex acc = 0.0;
+      for (size_t k = 0; k < nz; ++k) acc += conj(Psi[(size_t)r * nz + k]) * z[k];
+      b[r] = acc;
+    }
+    st = orc_cholesky(G, n);  /* G = L L^H */
+    if (st) break;
+    for (int r = 0; r < n; ++r) {  /* L w = b */
+      double complex acc = b[r];
+      for (int c = 0; c < r; ++c) acc -= G[r * n + c] * b[c];
+      b[r] = acc / G[r * n + r];
+    }
+    for (int r = n - 1; r >= 0; --r) {  /* L^H a = w */
+      double complex acc = b[r];
+      for (int c = r + 1; c < n; ++c) acc -= conj(G[c * n + r]) * b[c];
+      b[r] = acc / G[r * n + r];
+    }
+    double complex* out = zr + (size_t)j * nz;
+    for (size_t k = 0; k < nz; ++k) {  /* z~ = z - Psi a */
+      double complex acc = z[k];
+      for (int s = 0; s < n; ++s) acc -= Psi[(size_t)s * nz + k] * b[s];
+      out[k] = acc;
+    }
+  }
+  free(Psi);
+  free(G);
+  free(b);
+  return st;
+}
+
+/* Candidate i of the draw (key, counter): p_i = lo + u (hi - lo), u_a = (x_a + 1/2) 2^-32 from the Philox block
+ * (key; i, i >> 32, counter, 7) (reading C-amb-F3b: the partition P_q is the axis-aligned box [lo, hi]). */
+void orc_birth_candidate(uint64_t key, uint64_t counter, int64_t i, const double* box /*[6] lo, hi*/,
+                         double* p /*[3]*/) {
+  uint32_t ctr[4] = {(uint32_t)i, (uint32_t)((uint64_t)i >> 32), (uint32_t)counter, 7u};
+  uint32_t k[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
+  uint32_t x[4];
+  orc_philox4x32_10(ctr, k, x);
+  for (int a = 0; a < 3; ++a) {
+    double u = ((double)x[a] + 0.5) * 0x1p-32;
+    p[a] = box[a] + u * (box[3 + a] - box[a]);
+  }
+}
+
+/* Bartlett birth proposal for one new PF:
+ *   candidates p_i ~ U(P_q), i < N_g (orc_birth_candidate);
+ *   P_B(p_i, z~) = | sum_j (1/N_z) z~_j^H psi(x_hat, p_i) |^2  (coherent over the PAs; psi of the wall p_i,
+ *   component s = 1 of PA j);
+ *   w_i = P_B_i / sum P_B;  mu = p_{i*}, i* = argmax_i P_B_i (first index on ties);
+ *   C = sum_i w_i (p_i - mu)(p_i - mu)^T.
+ * Outputs pb[N_g], cand[N_g][3] (either may be NULL), mu[3], C[9] (row-major), *istar.  ORC_EZEROMASS when
+ * sum P_B = 0 (the residual has no power), errors of the responses / residual are passed on. */
+int orc_birth_proposal(const orc_scene* sc, const double* x_hat, const double* sfv_legacy, int L,
+                       const double complex* y, const double* box, int64_t N_g, uint64_t key, uint64_t counter,
+                       double* pb, double* cand, double* mu, double* Cov, int64_t* istar) {
+  int J = sc->J;
+  size_t nz = (size_t)sc->nf * sc->ny * sc->nv;
+  if (N_g <= 0) return ORC_EINVAL;
+  double complex* zr = (double complex*)malloc(sizeof(double complex) * nz * J);
+  int st = orc_birth_residual(sc, x_hat, sfv_legacy, L, y, zr);
+  double* P = (double*)malloc(sizeof(double) * N_g);
+  double* X = (double*)malloc(sizeof(double) * 3 * N_g);
+  double complex* psi = (double complex*)malloc(sizeof(double complex) * nz);
+  for (int64_t i = 0; i < N_g && !st; ++i) {
+    orc_birth_candidate(key, counter, i, box, X + 3 * i);
+    double complex acc = 0.0;
+    for (int j = 0; j < J && !st; ++j) {
+      st = orc_response(sc, x_hat, j, 1, X + 3 * i, sc->wavefront, psi);
+      double complex cj = 0.0;
+      for (size_t k = 0; k < nz; ++k) cj += conj(zr[(size_t)j * nz + k]) * psi[k];
+      acc += cj / (double)nz;
+    }
+    P[i] = creal(acc) * creal(acc) + cimag(acc) * cimag(acc);
+  }
+  double sum = 0.0;
+  int64_t best = 0;
+  if (!st) {
+    for (int64_t i = 0; i < N_g; ++i) {
+      sum += P[i];
+      if (P[i] > P[best]) best = i;
+    }
+    if (!(sum > 0.0)) st = ORC_EZEROMASS;
+  }
+  if (!st) {
+    for (int a = 0; a < 3; ++a) mu[a] = X[3 * best + a];
+    for (int q = 0; q < 9; ++q) Cov[q] = 0.0;
+    for (int64_t i = 0; i < N_g; ++i) {
+      double w = P[i] / sum, d[3];
+      for (int a = 0; a < 3; ++a) d[a] = X[3 * i + a] - mu[a];
+      for (int a = 0; a < 3; ++a)
+        for (int b2 = 0; b2 < 3; ++b2) Cov[3 * a + b2] += w * d[a] * d[b2];
+    }
+    *istar = best;
+    if (pb) memcpy(pb, P, sizeof(double) * N_g);
+    if (cand) memcpy(cand, X, sizeof(double) * 3 * N_g);
+  }
+  free(zr);
+  free(P);
+  free(X);
+  free(psi);
+  return st;
+}

@@ -50,6 +50,10 @@ def lib():
         _lib.orc_step_u_bits.argtypes = [C.c_uint64, C.c_uint64]
         _lib.orc_normals4.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, dp]
         _lib.orc_moment_match.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, dp]
+        _lib.orc_birth_candidate.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, dp, dp]
+        _lib.orc_birth_residual.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_void_p, C.c_void_p]
+        _lib.orc_birth_proposal.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_void_p, dp, C.c_int64, C.c_uint64,
+                                            C.c_uint64, dp, dp, dp, dp, C.POINTER(C.c_int64)]
     return _lib
 
 
@@ -159,6 +163,31 @@ class Oracle:
                              c.ctypes.data_as(C.c_void_p), G.ctypes.data_as(C.c_void_p))
         return st, c, G
 
+    # -- F3 birth proposal ---------------------------------------------------
+    def birth_residual(self, x_hat, sfv_legacy, y):
+        """z~_j = (I - Psi_j Psi_j^dagger) z_j for all PAs, [J][Nz] complex128."""
+        sl = _f64(np.asarray(sfv_legacy, dtype=np.float64).reshape(-1, 3))
+        y = _c128(y).reshape(self.J, self.Nz)
+        out = np.zeros((self.J, self.Nz), dtype=np.complex128)
+        st = lib().orc_birth_residual(C.cast(C.byref(self.sc), C.c_void_p), _d(_f64(x_hat)), _d(sl),
+                                      int(sl.shape[0]), y.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p))
+        return st, out
+
+    def birth_proposal(self, x_hat, sfv_legacy, y, box, N_g, key, counter):
+        """(status, P_B [N_g], candidates [N_g][3], mu [3], C [3][3], i*) of the coherent Bartlett proposal."""
+        sl = _f64(np.asarray(sfv_legacy, dtype=np.float64).reshape(-1, 3))
+        y = _c128(y).reshape(self.J, self.Nz)
+        pb = np.zeros(N_g)
+        cand = np.zeros((N_g, 3))
+        mu = np.zeros(3)
+        cov = np.zeros(9)
+        ist = C.c_int64(-1)
+        st = lib().orc_birth_proposal(C.cast(C.byref(self.sc), C.c_void_p), _d(_f64(x_hat)), _d(sl),
+                                      int(sl.shape[0]), y.ctypes.data_as(C.c_void_p), _d(_f64(box)),
+                                      C.c_int64(N_g), C.c_uint64(key), C.c_uint64(counter), _d(pb), _d(cand),
+                                      _d(mu), _d(cov), C.byref(ist))
+        return st, pb, cand, mu, cov.reshape(3, 3), int(ist.value)
+
     def bp_step(self, particles, sfv, y, m, v, eta, T, sigma_v, key, step, regularize=True):
         x = _f64(particles).copy()
         P = x.shape[0]
@@ -233,6 +262,12 @@ def regularize(x, p0, P_total, cov21, key, step):
     lib().orc_regularize(_d(x), C.c_int64(x.shape[0]), C.c_int64(p0), C.c_int64(P_total), _d(cov),
                          C.c_uint64(key), C.c_uint64(step))
     return x
+
+
+def birth_candidate(key, counter, i, box):
+    out = np.zeros(3)
+    lib().orc_birth_candidate(C.c_uint64(key), C.c_uint64(counter), C.c_int64(i), _d(_f64(box)), _d(out))
+    return out
 
 
 def moment_match(mu, gamma, exist):

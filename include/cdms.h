@@ -160,6 +160,28 @@ cdms_status cdms_loglik_terms(cdms_ctx ctx, const cdms_scene* scene, const doubl
                               const void* d_y, const double* h_f_pb, const cdms_prior* h_prior,
                               const double* h_eta, double* d_loglik, void* d_c, void* d_G);
 
+/* F3: the efficient birth proposal of one new PF.
+ *   1. residual z~_j = (I - Psi_j Psi_j^dagger) z_j, Psi_j = [psi(x_hat, LOS) psi(x_hat, sfv_1) ...
+ *      psi(x_hat, sfv_L)] the steering vectors at the predicted MMSE MT position h_x_hat [3] for the LOS and the
+ *      L legacy PFs' MMSE SFVs h_sfv_legacy [L][3] (L in [0, 8], h_sfv_legacy may be NULL if 0);
+ *   2. N_g candidates p_i uniform in the partition P_q = the axis-aligned box h_box [6] = (lo[3], hi[3])
+ *      (reading C-amb-F3a), p_i = lo + u (hi - lo), u_a = (x_a + 1/2) 2^-32 from the Philox4x32-10 block
+ *      (key; i, i >> 32, counter, 7), words 0..2 (C-amb-F3b);
+ *   3. coherent Bartlett spectrum P_B,i = | sum_j z~_j^H psi(x_hat, p_i) / N_z |^2;
+ *   4. mode mu = p_{i*}, i* = the first argmax, and C = sum_i w_i (p_i - mu)(p_i - mu)^T, w_i = P_B,i / sum P_B
+ *      (P:L3332-3340).
+ * Uses the scene's arrays, wavefront, path loss and precision (K is ignored); d_y complex64 [J][nf][Na] as for
+ * cdms_loglik.  Outputs (device, caller-owned): d_out double [13] = mu[3], C[9] row-major, i* (as a double);
+ * optional d_pb double [N_g] (P_B) and d_cand double [N_g][3] (candidates), NULL to skip.  The correlations run
+ * on the likelihood engine (K1, or the tensor cores for PLANAR_NB in FP32) at the candidate walls' mirror images
+ * of x_hat.  Errors: CDMS_EINVAL for bad arguments (immediately) or a singular Psi^H Psi (at sync);
+ * CDMS_EZEROMASS when the residual has no power (at sync); CDMS_EDEGENERATE for a degenerate response.
+ * Purely local.  Workspaces O(J (L+1) N_z + N_g) are kept in the context. */
+cdms_status cdms_birth_proposal(cdms_ctx ctx, const cdms_scene* scene, const double* h_f_pb,
+                                const double* h_x_hat, const double* h_sfv_legacy, int32_t L,
+                                const void* d_y, const double* h_box, int64_t N_g, uint64_t key,
+                                uint64_t counter, double* d_out, double* d_pb, double* d_cand);
+
 /* ---- row A6: weight normalization ------------------------------------------------------------ */
 
 /* w_p = exp((l_p - M) - ln S), M = max_p l_p, S = sum_p exp(l_p - M), lse = M + ln S over ALL ranks'

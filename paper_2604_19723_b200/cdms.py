@@ -77,6 +77,8 @@ def lib() -> C.CDLL:
             "cdms_bp_step": ([vp, C.POINTER(SceneC), vp, i64, vp, vp, dp, C.POINTER(PriorC), dp,
                               C.POINTER(StepParamsC), vp, vp], C.c_int),
             "cdms_response": ([vp, C.POINTER(SceneC), vp, i64, vp, vp, vp], C.c_int),
+            "cdms_birth_proposal": ([vp, C.POINTER(SceneC), dp, dp, dp, i32, vp, dp, i64, C.c_uint64, C.c_uint64,
+                                     vp, vp, vp], C.c_int),
             "cdms_moment_match": ([C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(PriorC)], C.c_int),
             "cdms_resample_plan": ([C.POINTER(C.c_uint64), C.c_int, C.c_int, i64, C.c_uint32, C.POINTER(i64),
                                     C.POINTER(i64), C.POINTER(i64)], C.c_int),
@@ -94,7 +96,7 @@ def exported_symbols() -> list[str]:
                         "cdms_reserve", "cdms_launch_count", "cdms_timing_enable", "cdms_timing_read",
                         "cdms_get_unique_id", "cdms_comm_init", "cdms_layout",
                         "cdms_loglik", "cdms_loglik_terms", "cdms_weights_normalize", "cdms_moments", "cdms_resample", "cdms_bp_step",
-                        "cdms_response", "cdms_moment_match", "cdms_resample_plan"]]
+                        "cdms_response", "cdms_moment_match", "cdms_resample_plan", "cdms_birth_proposal"]]
 
 
 def _ptr(t) -> Optional[int]:
@@ -259,6 +261,24 @@ def loglik_terms(ctx: Context, scene: Scene, particles, sfv, y, prior_m, prior_v
                                       _dp(np.ascontiguousarray(eta, dtype=np.float64).reshape(-1)), _ptr(l),
                                       _ptr(c), _ptr(G)))
     return l, c, G
+
+
+def birth_proposal(ctx: Context, scene: Scene, x_hat, sfv_legacy, y, box, N_g: int, key: int, counter: int,
+                   want_pb: bool = True, want_cand: bool = True):
+    """F3 birth proposal (cdms_birth_proposal): (out [13] = mu[3], C[9], i*; P_B [N_g] or None; candidates
+    [N_g][3] or None), device tensors on y's device."""
+    torch = ctx.torch
+    dev = y.device
+    sl = np.ascontiguousarray(np.asarray(sfv_legacy, dtype=np.float64).reshape(-1, 3))
+    out = torch.empty(13, dtype=torch.float64, device=dev)
+    pb = torch.empty(N_g, dtype=torch.float64, device=dev) if want_pb else None
+    cand = torch.empty((N_g, 3), dtype=torch.float64, device=dev) if want_cand else None
+    ctx.check(lib().cdms_birth_proposal(ctx.h, C.byref(scene.c), _dp(scene.f_pb()),
+                                        _dp(np.ascontiguousarray(x_hat, dtype=np.float64)),
+                                        _dp(sl) if sl.shape[0] else None, int(sl.shape[0]), _ptr(y),
+                                        _dp(np.ascontiguousarray(box, dtype=np.float64)), int(N_g), int(key),
+                                        int(counter), _ptr(out), _ptr(pb), _ptr(cand)))
+    return out, pb, cand
 
 
 def weights_normalize(ctx: Context, logw):

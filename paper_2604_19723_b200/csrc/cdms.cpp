@@ -40,7 +40,8 @@ namespace {
 enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
   WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
-  WS_COUNT
+  WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BXREF, WS_BC, WS_BLL, WS_BPB,
+  WS_BPART, WS_BPART6, WS_BSCR, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -682,6 +683,102 @@ cdms_status cdms_loglik_terms(cdms_ctx ctx, const cdms_scene* scene, const doubl
   if (sd.K > 0 && !d_sfv) return fail(ctx, CDMS_EINVAL, "loglik_terms: d_sfv NULL with K > 0");
   return loglik_impl(ctx, sd, scene->precision, d_particles, P, pstride, d_sfv, sfv_per_particle ? 1 : 0, d_y,
                      nullptr, d_loglik, nullptr, d_c, d_G);
+}
+
+cdms_status cdms_birth_proposal(cdms_ctx ctx, const cdms_scene* scene, const double* h_f_pb, const double* h_x_hat,
+                                const double* h_sfv_legacy, int32_t L, const void* d_y, const double* h_box,
+                                int64_t N_g, uint64_t key, uint64_t counter, double* d_out, double* d_pb,
+                                double* d_cand) {
+  if (!ctx) return CDMS_EINVAL;
+  DeviceGuard g(ctx->device);
+  if (!scene || !h_f_pb || !h_x_hat || !d_y || !h_box || !d_out || N_g <= 0 || L < 0 || L > MAXS - 1 ||
+      (L > 0 && !h_sfv_legacy))
+    return fail(ctx, CDMS_EINVAL, "birth_proposal: bad arguments (L=%d, N_g=%lld)", L, (long long)N_g);
+  BirthBox box{};
+  for (int a = 0; a < 3; ++a) {
+    box.lo[a] = h_box[a];
+    box.hi[a] = h_box[3 + a];
+    box.x_hat[a] = h_x_hat[a];
+    if (!is_fin(box.lo[a]) || !is_fin(box.hi[a]) || box.hi[a] < box.lo[a] || !is_fin(box.x_hat[a]))
+      return fail(ctx, CDMS_EINVAL, "birth_proposal: box / x_hat invalid");
+  }
+  for (int l = 0; l < L; ++l)
+    for (int a = 0; a < 3; ++a) {
+      box.sfv[l][a] = h_sfv_legacy[3 * l + a];
+      if (!is_fin(box.sfv[l][a])) return fail(ctx, CDMS_EINVAL, "birth_proposal: legacy SFV not finite");
+    }
+  box.L = L;
+  static const bool dbg_sync = getenv("CDMS_BIRTH_DEBUG") != nullptr;  // debug aid: sync + check per stage
+  auto stage = [&](const char* what) -> cdms_status {
+    if (!dbg_sync) return CDMS_OK;
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? CDMS_OK : fail(ctx, CDMS_ECUDA, "birth_proposal stage %s: %s", what, cudaGetErrorString(e));
+  };
+  // (1) residual z~ = Pi_perp z against LOS + legacy components at x_hat (fp64 responses, scene with K = L)
+  cdms_scene s1 = *scene;
+  s1.K = L;
+  SceneDev sd1;
+  cdms_status st = build_scene(ctx, &s1, h_f_pb, nullptr, nullptr, &sd1);
+  if (st) return st;
+  const int J = sd1.J, n = L + 1;
+  const int nz = sd1.nf * sd1.Na;
+  double *pos, *sfvb, *cand, *xref, *ll, *pb, *part6, *scr;
+  int32_t* js;
+  double2 *psi, *dots, *coef, *cbuf;
+  float2* zr;
+  double4* part;
+  WS_TRY(ctx, WS_BPOS, (size_t)3 * J * n, &pos);
+  WS_TRY(ctx, WS_BJS, (size_t)2 * J * n, &js);
+  WS_TRY(ctx, WS_BSFV, (size_t)3 * (L > 0 ? L : 1), &sfvb);
+  WS_TRY(ctx, WS_BPSI, (size_t)J * n * nz, &psi);
+  WS_TRY(ctx, WS_BDOTS, (size_t)J * (n * (n + 1) / 2 + n), &dots);
+  WS_TRY(ctx, WS_BCOEF, (size_t)J * n, &coef);
+  WS_TRY(ctx, WS_BZR, (size_t)J * nz, &zr);
+  CUDA_TRY(ctx, launch_birth_items(box, J, pos, js, sfvb, ctx->stream));
+  if ((st = stage("items"))) return st;
+  CUDA_TRY(ctx, launch_response(sd1, pos, (int64_t)J * n, js, sfvb, psi, CDMS_FP64, ctx->d_flags, ctx->stream));
+  if ((st = stage("response"))) return st;
+  CUDA_TRY(ctx, launch_birth_residual(J, nz, n, psi, static_cast<const float2*>(d_y), dots, coef, zr, ctx->d_flags,
+                                      ctx->stream));
+  ctx->launches += 5;
+  if ((st = stage("residual"))) return st;
+  // (2) candidates p_i and the MT position mirrored in each candidate wall
+  if (d_cand) cand = d_cand;
+  else WS_TRY(ctx, WS_BCAND, (size_t)3 * N_g, &cand);
+  WS_TRY(ctx, WS_BXREF, (size_t)3 * N_g, &xref);
+  CUDA_TRY(ctx, launch_birth_candidates(N_g, key, counter, box, cand, xref, ctx->stream));
+  ctx->launches += 1;
+  if ((st = stage("candidates"))) return st;
+  // (3) c_ij = psi_LOS(Refl_i(x_hat))^H z~_j on the likelihood engine: K = 0 scene, neutral prior (the assembled
+  //     likelihood is not used), snapshot z~
+  cdms_scene s0 = *scene;
+  s0.K = 0;
+  cdms_prior pr[MAXJ];
+  double eta1[MAXJ];
+  for (int j = 0; j < J; ++j) {
+    pr[j].m_re = 0.0;
+    pr[j].m_im = 0.0;
+    pr[j].v = 1.0;
+    eta1[j] = 1.0;
+  }
+  SceneDev sd0;
+  st = build_scene(ctx, &s0, h_f_pb, pr, eta1, &sd0);
+  if (st) return st;
+  WS_TRY(ctx, WS_BC, (size_t)N_g * J, &cbuf);
+  WS_TRY(ctx, WS_BLL, (size_t)N_g, &ll);
+  st = loglik_impl(ctx, sd0, scene->precision, xref, N_g, 3, nullptr, 0, zr, nullptr, ll, nullptr, cbuf, nullptr);
+  if (st) return st;
+  if ((st = stage("correlation"))) return st;
+  // (4) Bartlett spectrum, mode and weighted second moment
+  if (d_pb) pb = d_pb;
+  else WS_TRY(ctx, WS_BPB, (size_t)N_g, &pb);
+  const int64_t nblk = birth_blocks(N_g);
+  WS_TRY(ctx, WS_BPART, (size_t)nblk, &part);
+  WS_TRY(ctx, WS_BPART6, (size_t)6 * nblk, &part6);
+  WS_TRY(ctx, WS_BSCR, 8, &scr);
+  CUDA_TRY(ctx, launch_birth_reduce(N_g, J, nz, cbuf, cand, pb, part, part6, scr, d_out, ctx->d_flags, ctx->stream));
+  ctx->launches += 4;
+  return stage("reduce");
 }
 
 cdms_status cdms_weights_normalize(cdms_ctx ctx, const double* d_logw, int64_t P_local, double* d_w, double* d_lse) {

@@ -123,6 +123,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Philox4x32-10 (Salmon et al., SC'11): counter-based draws of the regularisation normals (step.cu) and the
+// birth-proposal candidates (birth.cu)
+__device__ __forceinline__ uint4 philox_step(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
 // ---------------------------------------------------------------------------- launchers
 // (defined in loglik.cu / beliefs.cu, called from cdms.cpp)
 cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2, float4* tmpl,
@@ -204,6 +220,23 @@ cudaError_t launch_nb_prep(const SceneDev& sc, const NbPlan& pl, const float2* y
                            cudaStream_t st);
 cudaError_t launch_nb_gram(const SceneDev& sc, const NbArgs& a, int* pflag, cudaStream_t st);
 cudaError_t launch_nb_corr(const SceneDev& sc, const NbPlan& pl, const NbArgs& a, int num_sms, cudaStream_t st);
+
+// birth.cu: F3 birth proposal
+struct BirthBox {                  // by-value kernel parameter
+  double lo[3], hi[3];             // partition P_q (axis-aligned box)
+  double x_hat[3];                 // predicted MMSE MT position
+  double sfv[MAXS - 1][3];         // legacy PF MMSE SFVs
+  int L;                           // number of legacy PFs
+};
+int64_t birth_blocks(int64_t N_g);
+cudaError_t launch_birth_items(const BirthBox& box, int J, double* pos, int32_t* js, double* sfv, cudaStream_t st);
+cudaError_t launch_birth_residual(int J, int nz, int n, const double2* psi, const float2* y, double2* dots,
+                                  double2* coef, float2* zr, int* flags, cudaStream_t st);
+cudaError_t launch_birth_candidates(int64_t N_g, uint64_t key, uint64_t counter, const BirthBox& box, double* cand,
+                                    double* xref, cudaStream_t st);
+cudaError_t launch_birth_reduce(int64_t N_g, int J, int nz, const double2* c, const double* cand, double* pb,
+                                double4* part, double* part6, double* scratch, double* out, int* flags,
+                                cudaStream_t st);
 
 // step.cu: the fused O(P) pipeline of cdms_bp_step (fixed STEP_ITEMS-particle blocks, last-block reductions)
 constexpr int STEP_ITEMS = 512;

@@ -728,8 +728,11 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
     for (int t = 0; t < NTRI; ++t) k[t] = tp[S + t];  // lower triangle of G: k[tri(r, c)] = G_rc, r >= c
     if (a.term_c != nullptr) {
 #pragma unroll
+      for (int r = 0; r < S; ++r) a.term_c[(p * J + j) * S + r] = c[r];
+    }
+    if (a.term_G != nullptr) {  // (c and G are independent outputs: the birth proposal reads c only)
+#pragma unroll
       for (int r = 0; r < S; ++r) {
-        a.term_c[(p * J + j) * S + r] = c[r];
 #pragma unroll
         for (int q = 0; q < S; ++q) {
           double2 G = (r >= q) ? k[tri(r, q)] : k[tri(q, r)];

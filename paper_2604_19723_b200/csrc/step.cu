@@ -379,19 +379,6 @@ __global__ void step_anc_kernel(const uint64_t* __restrict__ C, int64_t P_local,
 
 // ---------------------------------------------------------------------------- K_reg
 // Philox4x32-10 and Box-Muller exactly as beliefs.cu (streams 1, 2 of the global slot index).
-__device__ __forceinline__ uint4 philox_step(uint4 c, uint2 k) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r > 0) {
-      k.x += 0x9E3779B9u;
-      k.y += 0xBB67AE85u;
-    }
-    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-  }
-  return c;
-}
 __device__ __forceinline__ void normals4_step(uint64_t key, uint64_t step, uint64_t index, uint32_t stream,
                                               double n[4]) {
   const uint4 x = philox_step(make_uint4((uint32_t)index, (uint32_t)(index >> 32), (uint32_t)step, stream),

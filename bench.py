@@ -416,6 +416,203 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+BIRTH_METRIC = "Bartlett birth-proposal candidate x PA correlations/s (F3)"
+BIRTH_UNIT = "candidate-PA evals/s"
+
+
+def birth_inputs(cfg, sc, L):
+    """x_hat near the truth, the first L walls as legacy PFs, the partition box around the next wall (+-0.4 m)."""
+    x_hat = scenes.P_TRUE + np.array([0.01, -0.02, 0.005])
+    target = sc.sfv[min(L, cfg.K - 1)]
+    return x_hat, sc.sfv[:L], np.concatenate([target - 0.4, target + 0.4])
+
+
+def birth_config(args, cfg, world):
+    return {"workload": f"{args.config} scene (J={cfg.J}, {cfg.ny}x{cfg.nv} URA, nf={cfg.nf}), birth proposal with "
+                        f"L={args.legacy} legacy PFs, N_g={args.candidates} candidates/GPU",
+            "config": args.config, "mode": "birth", "N_g_per_gpu": args.candidates, "L": args.legacy, "J": cfg.J,
+            "Nz": cfg.Nz, "wavefront": args.wavefront, "precision": args.precision,
+            "step": "residual projector + candidates + coherent Bartlett correlations + mode/moment matching",
+            "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"replicas x{world} (independent draws)"}
+
+
+def run_birth(args):
+    """F3: time cdms_birth_proposal (device-resident snapshot) and its end-to-end variant (pinned host snapshot
+    uploaded and the 13-double result read back every step)."""
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2604_19723_b200 import build as B
+    if rank == 0 and not os.path.exists(os.path.join(ROOT, "paper_2604_19723_b200", "libcdms.so")):
+        B.build()
+    if world > 1:
+        torch.distributed.barrier()
+    from paper_2604_19723_b200 import cdms
+    dev = f"cuda:{local}"
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream(local)
+    cfg = scenes.CONFIGS[args.config]
+    sc = scenes.make_scene(cfg)
+    scene = cdms.Scene.from_synthetic(sc, wavefront=args.wavefront, precision=args.precision)
+    ctx = cdms.Context(local, stream)
+    y, _ = synth_measurement(cdms, ctx, scene, sc, torch, dev)
+    x_hat, sl, box = birth_inputs(cfg, sc, args.legacy)
+    N_g = args.candidates
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    out = torch.empty(13, dtype=torch.float64, device=dev)
+    key = sc.philox_key
+
+    def step(n):
+        return cdms.birth_proposal(ctx, scene, x_hat, sl, y, box, N_g, key, 1000 * rank + n, want_pb=False,
+                                   want_cand=False)
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize(local)
+
+    for n in range(args.warmup):
+        step(n)
+    ctx.sync()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    ctx.timing_enable(True)
+    with ClockSampler(local) as clk:
+        barrier()
+        for n in range(args.steps):
+            flush.zero_()
+            ev[n][0].record(stream)
+            step(args.warmup + n)
+            ev[n][1].record(stream)
+            if n == args.steps // 2:
+                clk.mark()
+        clk.mark()
+        barrier()
+    st = ctx.sync(raise_on_error=False)
+    gpu_launches = ctx.launch_count() - launches0
+    k_ms, k_n = ctx.timing_read()
+    ctx.timing_enable(False)
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_per_step = t.item() / args.steps
+    kernel_ms = k_ms / max(k_n, 1)
+    launches_per_step = k_n / args.steps
+    # end to end: pinned host snapshot -> device, proposal, result -> pinned host
+    y_host = y.cpu().pin_memory()
+    out_host = torch.empty(13, dtype=torch.float64).pin_memory()
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    for n in range(args.steps):
+        flush.zero_()
+        e2e_ev[n][0].record(stream)
+        y.copy_(y_host, non_blocking=True)
+        o, _, _ = step(10_000 + n)
+        out_host.copy_(o, non_blocking=True)
+        e2e_ev[n][1].record(stream)
+    barrier()
+    te = torch.tensor([sum(a.elapsed_time(b) for a, b in e2e_ev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = te.item() / args.steps
+    ctx.sync(raise_on_error=False)
+    evals = N_g * cfg.J * world
+    result = None
+    if rank == 0:
+        clocks = clk.summary()
+        flop_launch = 8.0 * cfg.Nz * N_g * cfg.J / launches_per_step
+        if nb_tensor_path(args):
+            t_peak, t_basis = measured_tensor_peak()
+            ach = 4.0 * flop_launch / (kernel_ms / 1e3) / 1e12
+            roof = {"bound": "tensor", "pipe": "tcgen05.mma kind::f16", "achieved": round(ach, 2),
+                    "peak": round(t_peak, 1), "unit": "TFLOP/s", "frac": round(ach / t_peak, 4), "peak_basis": t_basis,
+                    "kernel": "cdms::nb_corr_kernel (F3 correlations)"}
+        else:
+            ach = flop_launch / (kernel_ms / 1e3) / 1e12
+            peak = fp32_peak_tflops(1965.0)
+            roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(ach, 3), "peak": round(peak, 2),
+                    "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                    "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
+                    "kernel": "cdms::corr_kernel (F3 correlations, K = 0 scene at the mirrored positions)"}
+        roof.update({"kernel_ms": round(kernel_ms, 4), "kernel_share_of_step": round(kernel_ms * launches_per_step /
+                                                                                    ms_per_step, 4),
+                     "launches_per_step": launches_per_step,
+                     "flop_basis": "8 N_z flop per (candidate, PA): one complex MAC per response element",
+                     "traffic": None})
+        result = {"metric": BIRTH_METRIC, "value": evals / (ms_per_step / 1e3), "unit": BIRTH_UNIT, "n_gpus": world,
+                  "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                  "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+                  "data": "synthetic", "config": birth_config(args, cfg, world), "roofline": roof,
+                  "e2e": {"value": evals / (e2e_ms / 1e3), "unit": BIRTH_UNIT, "ms_per_step": e2e_ms,
+                          "h2d_bytes_per_step": int(y.numel() * 8), "d2h_bytes_per_step": 13 * 8},
+                  "clocks": clocks, "gpu_launches": int(gpu_launches), "sync_status": st}
+        if not args.no_cpu_baseline:
+            result["cpu_baseline"] = birth_cpu_baseline(args, cfg, sc, args.cpu_seconds)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return result
+
+
+def birth_cpu_baseline(args, cfg, sc, budget_s):
+    """The oracle's orc_birth_proposal on growing candidate samples until ~budget_s of CPU work (single thread:
+    the oracle's candidate loop is serial)."""
+    from oracle import oracle as O
+    O.build()
+    o = O.Oracle.from_scene(sc, wavefront=args.wavefront)
+    y, _ = O.measurement(o, sc, scenes.P_TRUE)
+    y = y.astype(np.complex64).astype(np.complex128).reshape(cfg.J, -1)
+    x_hat, sl, box = birth_inputs(cfg, sc, args.legacy)
+    n, spent, best = 16, 0.0, None
+    while True:
+        t0 = time.perf_counter()
+        o.birth_proposal(x_hat, sl, y, box, n, sc.philox_key, 0)
+        dt = time.perf_counter() - t0
+        spent += dt
+        best = (n, dt)
+        if spent > budget_s or dt > budget_s / 3 or n >= args.candidates:
+            break
+        n = min(args.candidates, n * 4)
+    n, dt = best
+    return {"value": n * cfg.J / dt, "unit": BIRTH_UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"orc_birth_proposal with {n} of {args.candidates} candidates ({args.config}), {dt:.2f} s"}
+
+
+def run_birth_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    O.build()
+    cfg = scenes.CONFIGS[args.config]
+    sc = scenes.make_scene(cfg)
+    o = O.Oracle.from_scene(sc, wavefront=args.wavefront)
+    y, _ = O.measurement(o, sc, scenes.P_TRUE)
+    y = y.astype(np.complex64).astype(np.complex128).reshape(cfg.J, -1)
+    x_hat, sl, box = birth_inputs(cfg, sc, args.legacy)
+    n = min(args.candidates, args.ref_particles)
+    for w in range(args.warmup):
+        o.birth_proposal(x_hat, sl, y, box, n, sc.philox_key, w)
+    times = []
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        o.birth_proposal(x_hat, sl, y, box, n, sc.philox_key, args.warmup + k)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    value = n * cfg.J / dt
+    return {"metric": BIRTH_METRIC, "value": value, "unit": BIRTH_UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": birth_config(args, cfg, world),
+            "cpu_baseline": {"value": value, "unit": BIRTH_UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"orc_birth_proposal with {n} of {args.candidates} candidates per step"},
+            "e2e": {"value": value, "unit": BIRTH_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -429,9 +626,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-particles", type=int, default=2000)
+    ap.add_argument("--mode", default="step", choices=["step", "birth"],
+                    help="step: the BP step (headline); birth: the F3 birth proposal")
+    ap.add_argument("--candidates", type=int, default=1 << 20, help="birth mode: candidates N_g per GPU")
+    ap.add_argument("--legacy", type=int, default=2, help="birth mode: legacy PFs L")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "cdms" else args.warmup
-    res = run_reference(args) if args.impl == "reference" else run_cdms(args)
+    if args.mode == "birth":
+        res = run_birth_reference(args) if args.impl == "reference" else run_birth(args)
+    else:
+        res = run_reference(args) if args.impl == "reference" else run_cdms(args)
     if res is not None:
         print(json.dumps(res), flush=True)
 

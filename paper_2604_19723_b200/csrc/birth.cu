@@ -5,13 +5,13 @@
 //      response kernel, Psi^H Psi and Psi^H z as fixed-order fp64 block reductions (birth_dots_kernel), a
 //      complex Cholesky solve per PA (birth_solve_kernel), z~ = z - Psi a rounded once to complex64
 //      (birth_resid_kernel);
-//   2. N_g candidates p_i uniform in the partition box (Philox (key; i, i >> 32, counter, 7)) and, per candidate,
-//      the MT position mirrored in the candidate wall (birth_cand_kernel).  A wall reflection is an isometry, so
-//      the response of wall p_i at x_hat equals the LOS response at Refl_i(x_hat) for every PA and wavefront
-//      (spherical: d_m = ||x_hat - Refl(p_j + R_j p~_m)|| = ||Refl(x_hat) - p_j - R_j p~_m||; planar: r' =
-//      R_j^T H (x_hat - p_VA) = R_j^T (Refl(x_hat) - p_j)).  The coherent Bartlett correlations
-//      z~_j^H psi(x_hat, p_i) are therefore the LOS correlations of the likelihood engine (K1, or the tensor
-//      cores for PLANAR_NB) on a K = 0 scene with particles Refl_i(x_hat) and snapshot z~ (cdms.cpp);
+//   2. N_g candidates p_i uniform in the partition box (Philox (key; i, i >> 32, counter, 7)), padded to a multiple
+//      of 8 with copies of the last one (birth_cand_kernel);
+//      the coherent Bartlett correlations z~_j^H psi(x_hat, p_i) all share the MT position and differ only in the
+//      wall, i.e. they are the components of pseudo-particles at x_hat whose SFVs are the candidates: the likelihood
+//      engine (K1, or the tensor cores for PLANAR_NB) runs with K = 8 per-particle SFVs (8 candidates per
+//      pseudo-particle, S = 9: the engine's efficient regime, where each snapshot element loaded from shared
+//      memory feeds 9 components) and the residual as the snapshot (cdms.cpp); component 0 (LOS) is not used;
 //   3. P_B,i = |sum_j c_ij|^2 / N_z^2, its sum, the first argmax (birth_pb_kernel, birth_mode_kernel) and the
 //      weighted second moment about the mode (birth_cov_*), all fixed-partition fp64 reductions.
 #include <math.h>
@@ -24,6 +24,7 @@ namespace cdms {
 namespace {
 constexpr int BIRTH_BLOCK = 256;
 constexpr int BIRTH_ITEMS = 2048;  // candidates per reduction block (fixed partition -> determinism)
+constexpr int BIRTH_PACK = MAXS - 1;  // candidates per pseudo-particle (its walls)
 
 __device__ __forceinline__ double2 cconj_mul(double2 a, double2 b) {  // conj(a) b
   return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
@@ -139,27 +140,20 @@ __global__ void birth_resid_kernel(int J, int nz, int n, const double2* __restri
   zr[t] = make_float2((float)re, (float)im);
 }
 
-// (2) candidates and the mirrored MT positions.  Refl_s(x) = x - (2 x.s/||s||^2 - 1) s (the wall through s/2 with
-// normal s/||s||; the same map as the VA of a PA).  ||s|| = 0 gives a non-finite position, which the
-// likelihood engine flags (EDEGENERATE).
-__global__ void birth_cand_kernel(int64_t N_g, uint64_t key, uint64_t counter, BirthBox box, double* __restrict__ cand,
-                                  double* __restrict__ xref) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N_g) return;
+// (2) candidates, padded to n_pad with copies of the last (the pseudo-particles take BIRTH_PACK walls each)
+__global__ void birth_cand_kernel(int64_t N_g, int64_t n_pad, uint64_t key, uint64_t counter, BirthBox box,
+                                  double* __restrict__ cand) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_pad) return;
+  const int64_t i = t < N_g ? t : N_g - 1;
   const uint4 x = philox_step(make_uint4((uint32_t)i, (uint32_t)((uint64_t)i >> 32), (uint32_t)counter, 7u),
                               make_uint2((uint32_t)key, (uint32_t)(key >> 32)));
   const uint32_t xs[3] = {x.x, x.y, x.z};
-  double p[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const double u = ((double)xs[a] + 0.5) * 0x1p-32;  // exact
-    p[a] = __dadd_rn(box.lo[a], __dmul_rn(u, box.hi[a] - box.lo[a]));  // no contraction: bit-equal to the oracle
-    cand[3 * i + a] = p[a];
+    cand[3 * t + a] = __dadd_rn(box.lo[a], __dmul_rn(u, box.hi[a] - box.lo[a]));  // uncontracted: bit-equal to the oracle
   }
-  const double n2 = p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
-  const double c = 2.0 * (box.x_hat[0] * p[0] + box.x_hat[1] * p[1] + box.x_hat[2] * p[2]) / n2 - 1.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) xref[3 * i + a] = box.x_hat[a] - c * p[a];
 }
 
 // (3a) P_B,i = |sum_j c_ij|^2 / N_z^2 (c_ij = psi_ij^H z~_j; |sum conj| = |sum|), per-block (sum, max, argmax).
@@ -175,8 +169,10 @@ __global__ void birth_pb_kernel(int64_t N_g, int J, double inv_nz2, const double
     const int64_t i = i0 + t;
     if (i >= N_g) break;
     double re = 0.0, im = 0.0;
+    const int64_t pp = i / BIRTH_PACK;
+    const int comp = 1 + (int)(i - pp * BIRTH_PACK);
     for (int j = 0; j < J; ++j) {
-      const double2 v = c[i * J + j];
+      const double2 v = c[(pp * J + j) * (BIRTH_PACK + 1) + comp];
       re += v.x;
       im += v.y;
     }
@@ -204,23 +200,48 @@ __global__ void birth_pb_kernel(int64_t N_g, int J, double inv_nz2, const double
   if (threadIdx.x == 0) part[blockIdx.x] = make_double4(rs[0], rm[0], (double)ri[0], 0.0);
 }
 
-// (3b) combine the block partials in block order: scratch = (sum P_B, i*, mu[3]); zero or non-finite sum -> flags.
+// (3b) combine the block partials: each thread folds a strided set of blocks in block order, then a fixed tree;
+// ties keep the first index (thread t holds blocks t, t + 256, ... < those of thread t + 1 in each round, so the
+// tree compares (value, index) pairs explicitly).  scratch = (sum P_B, i*, mu[3]); zero / non-finite sum -> flags.
 __global__ void birth_mode_kernel(int64_t nblk, const double4* __restrict__ part, const double* __restrict__ cand,
                                   double* __restrict__ scratch, int* flags) {
-  if (threadIdx.x != 0) return;
+  __shared__ double rs[BIRTH_BLOCK];
+  __shared__ double rm[BIRTH_BLOCK];
+  __shared__ int64_t ri[BIRTH_BLOCK];
   double sum = 0.0, mx = -1.0;
   int64_t arg = -1;
-  for (int64_t b = 0; b < nblk; ++b) {
+  for (int64_t b = threadIdx.x; b < nblk; b += BIRTH_BLOCK) {
     const double4 v = part[b];
     sum += v.x;
-    if (v.y > mx) { mx = v.y; arg = (int64_t)v.z; }  // blocks in index order: ties keep the first
+    const int64_t a2 = (int64_t)v.z;
+    if (v.y > mx || (v.y == mx && a2 < arg)) { mx = v.y; arg = a2; }
   }
-  if (!isfinite(sum)) atomicOr(flags, FLAG_NAN);
-  else if (!(sum > 0.0)) atomicOr(flags, FLAG_ZEROMASS);
-  if (arg < 0) arg = 0;
-  scratch[0] = sum;
-  scratch[1] = (double)arg;
-  for (int a = 0; a < 3; ++a) scratch[2 + a] = cand[3 * arg + a];
+  rs[threadIdx.x] = sum;
+  rm[threadIdx.x] = mx;
+  ri[threadIdx.x] = arg;
+  __syncthreads();
+  for (int s = BIRTH_BLOCK / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      rs[threadIdx.x] += rs[threadIdx.x + s];
+      const double m2 = rm[threadIdx.x + s];
+      const int64_t a2 = ri[threadIdx.x + s];
+      if (m2 > rm[threadIdx.x] || (m2 == rm[threadIdx.x] && a2 >= 0 && (ri[threadIdx.x] < 0 || a2 < ri[threadIdx.x]))) {
+        rm[threadIdx.x] = m2;
+        ri[threadIdx.x] = a2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double tot = rs[0];
+    int64_t a = ri[0];
+    if (!isfinite(tot)) atomicOr(flags, FLAG_NAN);
+    else if (!(tot > 0.0)) atomicOr(flags, FLAG_ZEROMASS);
+    if (a < 0) a = 0;
+    scratch[0] = tot;
+    scratch[1] = (double)a;
+    for (int q = 0; q < 3; ++q) scratch[2 + q] = cand[3 * a + q];
+  }
 }
 
 // (3c) per block sum_i P_B,i (p_i - mu)(p_i - mu)^T, upper triangle (6 entries)
@@ -244,18 +265,22 @@ __global__ void birth_cov_partial_kernel(int64_t N_g, const double* __restrict__
   }
 }
 
-// (3d) out[0..2] = mu, out[3..11] = C (row-major, symmetric), out[12] = i*
+// (3d) out[0..2] = mu, out[3..11] = C (row-major, symmetric), out[12] = i*; block-strided fixed-order sums
 __global__ void birth_cov_final_kernel(int64_t nblk, const double* __restrict__ part6, const double* __restrict__ scratch,
                                        double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+  __shared__ double red[BIRTH_BLOCK];
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t b = 0; b < nblk; ++b)
+  for (int64_t b = threadIdx.x; b < nblk; b += BIRTH_BLOCK)
     for (int q = 0; q < 6; ++q) acc[q] += part6[b * 6 + q];
-  const double inv = scratch[0] > 0.0 ? 1.0 / scratch[0] : 0.0;
-  const int map[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
-  for (int a = 0; a < 3; ++a) out[a] = scratch[2 + a];
-  for (int q = 0; q < 9; ++q) out[3 + q] = acc[map[q]] * inv;
-  out[12] = scratch[1];
+  double tot[6];
+  for (int q = 0; q < 6; ++q) tot[q] = block_sum_d(acc[q], red);
+  if (threadIdx.x == 0) {
+    const double inv = scratch[0] > 0.0 ? 1.0 / scratch[0] : 0.0;
+    const int map[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+    for (int a = 0; a < 3; ++a) out[a] = scratch[2 + a];
+    for (int q = 0; q < 9; ++q) out[3 + q] = tot[map[q]] * inv;
+    out[12] = scratch[1];
+  }
 }
 
 // (0) response items for Psi: item j n + s at x_hat, (j, s), and the legacy SFV list in device memory
@@ -288,9 +313,11 @@ cudaError_t launch_birth_residual(int J, int nz, int n, const double2* psi, cons
   birth_resid_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(J, nz, n, psi, y, coef, zr);
   return cudaGetLastError();
 }
+int64_t birth_pseudo_particles(int64_t N_g) { return (N_g + BIRTH_PACK - 1) / BIRTH_PACK; }
 cudaError_t launch_birth_candidates(int64_t N_g, uint64_t key, uint64_t counter, const BirthBox& box, double* cand,
-                                    double* xref, cudaStream_t st) {
-  birth_cand_kernel<<<(unsigned)((N_g + 255) / 256), 256, 0, st>>>(N_g, key, counter, box, cand, xref);
+                                    cudaStream_t st) {
+  const int64_t n_pad = birth_pseudo_particles(N_g) * BIRTH_PACK;
+  birth_cand_kernel<<<(unsigned)((n_pad + 255) / 256), 256, 0, st>>>(N_g, n_pad, key, counter, box, cand);
   return cudaGetLastError();
 }
 cudaError_t launch_birth_reduce(int64_t N_g, int J, int nz, const double2* c, const double* cand, double* pb,
@@ -299,9 +326,9 @@ cudaError_t launch_birth_reduce(int64_t N_g, int J, int nz, const double2* c, co
   const int64_t nblk = birth_blocks(N_g);
   const double inv_nz2 = 1.0 / ((double)nz * (double)nz);
   birth_pb_kernel<<<(unsigned)nblk, BIRTH_BLOCK, 0, st>>>(N_g, J, inv_nz2, c, pb, part);
-  birth_mode_kernel<<<1, 32, 0, st>>>(nblk, part, cand, scratch, flags);
+  birth_mode_kernel<<<1, BIRTH_BLOCK, 0, st>>>(nblk, part, cand, scratch, flags);
   birth_cov_partial_kernel<<<(unsigned)nblk, BIRTH_BLOCK, 0, st>>>(N_g, pb, cand, scratch, part6);
-  birth_cov_final_kernel<<<1, 32, 0, st>>>(nblk, part6, scratch, out);
+  birth_cov_final_kernel<<<1, BIRTH_BLOCK, 0, st>>>(nblk, part6, scratch, out);
   return cudaGetLastError();
 }
 

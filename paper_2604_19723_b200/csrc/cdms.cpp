@@ -40,7 +40,7 @@ namespace {
 enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
   WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
-  WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BXREF, WS_BC, WS_BLL, WS_BPB,
+  WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BC, WS_BLL, WS_BPB,
   WS_BPART, WS_BPART6, WS_BSCR, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
@@ -386,7 +386,8 @@ cdms_status exchange(cdms_ctx ctx, const Plan& plan, int64_t P_local, const void
 
 cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const double* d_particles, int64_t P,
                         int32_t pstride, const double* d_sfv, int32_t sfv_pp, const void* d_y, const double* d_logw,
-                        double* d_loglik, void* d_amp, void* d_c = nullptr, void* d_G = nullptr) {
+                        double* d_loglik, void* d_amp, void* d_c = nullptr, void* d_G = nullptr,
+                        bool no_gram = false) {
   float4* yt;
   double* yn;
   double2* terms;
@@ -439,6 +440,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     a.grid = corr_grid(sd, a.n_tiles, precision, ctx->num_sms);
     if (a.grid < 1) return fail(ctx, CDMS_ECUDA, "corr_kernel occupancy query failed");
     a.sched = sched;
+    a.no_gram = no_gram ? 1 : 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {
       while (ctx->ev_pool.size() < ctx->ev_used + 2) {
@@ -463,6 +465,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       na.terms = terms;
       na.n_tiles_j = (nb * sd.S + 127) / 128;
       na.n_tiles = na.n_tiles_j * sd.J;
+      na.diag_only = no_gram ? 1 : 0;
       CUDA_TRY(ctx, launch_nb_gram(sd, na, pflag, ctx->stream));
       CUDA_TRY(ctx, launch_nb_corr(sd, nbp, na, ctx->num_sms, ctx->stream));
       ctx->launches += 1;
@@ -722,7 +725,7 @@ cdms_status cdms_birth_proposal(cdms_ctx ctx, const cdms_scene* scene, const dou
   if (st) return st;
   const int J = sd1.J, n = L + 1;
   const int nz = sd1.nf * sd1.Na;
-  double *pos, *sfvb, *cand, *xref, *ll, *pb, *part6, *scr;
+  double *pos, *sfvb, *cand, *ll, *pb, *part6, *scr;
   int32_t* js;
   double2 *psi, *dots, *coef, *cbuf;
   float2* zr;
@@ -742,31 +745,35 @@ cdms_status cdms_birth_proposal(cdms_ctx ctx, const cdms_scene* scene, const dou
                                       ctx->stream));
   ctx->launches += 5;
   if ((st = stage("residual"))) return st;
-  // (2) candidates p_i and the MT position mirrored in each candidate wall
-  if (d_cand) cand = d_cand;
-  else WS_TRY(ctx, WS_BCAND, (size_t)3 * N_g, &cand);
-  WS_TRY(ctx, WS_BXREF, (size_t)3 * N_g, &xref);
-  CUDA_TRY(ctx, launch_birth_candidates(N_g, key, counter, box, cand, xref, ctx->stream));
+  // (2) candidates p_i, padded to whole pseudo-particles (copies of the last candidate)
+  const int64_t npp = birth_pseudo_particles(N_g);
+  const int pack = MAXS - 1;
+  WS_TRY(ctx, WS_BCAND, (size_t)3 * npp * pack, &cand);
+  CUDA_TRY(ctx, launch_birth_candidates(N_g, key, counter, box, cand, ctx->stream));
   ctx->launches += 1;
+  if (d_cand)
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_cand, cand, sizeof(double) * 3 * N_g, cudaMemcpyDeviceToDevice, ctx->stream));
   if ((st = stage("candidates"))) return st;
-  // (3) c_ij = psi_LOS(Refl_i(x_hat))^H z~_j on the likelihood engine: K = 0 scene, neutral prior (the assembled
-  //     likelihood is not used), snapshot z~
+  // (3) c = psi(x_hat, p_i)^H z~_j on the likelihood engine: pseudo-particles at x_hat (pstride 0: pos[0..2] is
+  //     x_hat) with the candidates as their K = 8 per-particle walls, neutral prior (the assembled likelihood is not
+  //     used), snapshot z~
   cdms_scene s0 = *scene;
-  s0.K = 0;
-  cdms_prior pr[MAXJ];
+  s0.K = pack;
+  cdms_prior pr[MAXJ * MAXS];
   double eta1[MAXJ];
-  for (int j = 0; j < J; ++j) {
-    pr[j].m_re = 0.0;
-    pr[j].m_im = 0.0;
-    pr[j].v = 1.0;
-    eta1[j] = 1.0;
+  for (int q = 0; q < J * MAXS; ++q) {
+    pr[q].m_re = 0.0;
+    pr[q].m_im = 0.0;
+    pr[q].v = 1.0;
   }
+  for (int j = 0; j < J; ++j) eta1[j] = 1.0;
   SceneDev sd0;
   st = build_scene(ctx, &s0, h_f_pb, pr, eta1, &sd0);
   if (st) return st;
-  WS_TRY(ctx, WS_BC, (size_t)N_g * J, &cbuf);
-  WS_TRY(ctx, WS_BLL, (size_t)N_g, &ll);
-  st = loglik_impl(ctx, sd0, scene->precision, xref, N_g, 3, nullptr, 0, zr, nullptr, ll, nullptr, cbuf, nullptr);
+  WS_TRY(ctx, WS_BC, (size_t)npp * J * MAXS, &cbuf);
+  WS_TRY(ctx, WS_BLL, (size_t)npp, &ll);
+  st = loglik_impl(ctx, sd0, scene->precision, pos, npp, 0, cand, 1, zr, nullptr, ll, nullptr, cbuf, nullptr,
+                   /*no_gram=*/true);
   if (st) return st;
   if ((st = stage("correlation"))) return st;
   // (4) Bartlett spectrum, mode and weighted second moment

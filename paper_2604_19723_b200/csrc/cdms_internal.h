@@ -67,6 +67,7 @@ struct CorrArgs {
   int64_t n_tiles;
   int64_t n_groups;         // n_tiles * J (< 2^31)
   int64_t grid;             // CTAs
+  int no_gram;              // 1: skip the off-diagonal Gram (callers that use c only; G = diag(g^2 N_z) is written)
 };
 // K1b (S x S assembly) for the same batch
 struct AsmArgs {
@@ -213,6 +214,7 @@ struct NbArgs {
   double2* terms;           // [P][J][T]: c_s written by nb_corr_kernel, G by nb_gram_kernel
   int64_t n_tiles_j;        // ceil(P S / 128)
   int64_t n_tiles;          // n_tiles_j J
+  int diag_only;            // nb_gram_kernel: write G = diag(g^2 N_z) only (callers that use c only)
 };
 bool nb_tensor_plan(const SceneDev& sc, NbPlan* pl);  // false: shape not supported (2 N_a > 512)
 size_t nb_operand_bytes(const SceneDev& sc, const NbPlan& pl);
@@ -232,8 +234,9 @@ int64_t birth_blocks(int64_t N_g);
 cudaError_t launch_birth_items(const BirthBox& box, int J, double* pos, int32_t* js, double* sfv, cudaStream_t st);
 cudaError_t launch_birth_residual(int J, int nz, int n, const double2* psi, const float2* y, double2* dots,
                                   double2* coef, float2* zr, int* flags, cudaStream_t st);
+int64_t birth_pseudo_particles(int64_t N_g);  // pseudo-particles of MAXS - 1 candidate walls each
 cudaError_t launch_birth_candidates(int64_t N_g, uint64_t key, uint64_t counter, const BirthBox& box, double* cand,
-                                    double* xref, cudaStream_t st);
+                                    cudaStream_t st);
 cudaError_t launch_birth_reduce(int64_t N_g, int J, int nz, const double2* c, const double* cand, double* pb,
                                 double4* part, double* part6, double* scratch, double* out, int* flags,
                                 cudaStream_t st);

@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
     // ---- (1b) planar NB Gram, separable closed form in fp64 (P:L2160-2184 with the template P:L29-39):
     //   G_ab = e^{j 2 pi dR fc/c} D_Nf(dR df/c) D_ny(dy du'_y fc/c) D_nv(dv du'_z fc/c),
     //   dR = R_a - R_b, du' = u'_b - u'_a, u'_s = R_j^T H_s r_s / R_s (local directions).
-    if (nb_mode && NPAIR > 0) {
+    if (nb_mode && NPAIR > 0 && !a.no_gram) {
       for (int it = tid; it < NPAIR * TILE_P; it += NTHREADS) {
         const int q = it / TILE_P, pl = it - q * TILE_P;
         int ca, cb;
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
 #ifdef CDMS_XP_SKIP_GRAM  // experiment build only (wrong results): price the per-antenna Gram terms
       if (false) {
 #else
-      if (!nb_mode) {
+      if (!nb_mode && !a.no_gram) {
 #endif
         for (int q = (warp - mb - S) & (NWARP - 1); q < NPAIR; q += NWARP) {
           int pa, pb;

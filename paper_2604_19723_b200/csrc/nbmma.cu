@@ -396,6 +396,10 @@ __global__ void nb_gram_kernel(const __grid_constant__ SceneDev sc, const NbArgs
         out[t] = make_double2(nz * g[r] * g[r], 0.0);
         continue;
       }
+      if (a.diag_only) {
+        out[t] = make_double2(0.0, 0.0);
+        continue;
+      }
       float sn, cs;
       sincospif(2.f * (float)frac_c((R[r] - R[c]) * sc.fc_c), &sn, &cs);
       const float D = dirichlet_rr(dl[r] - dl[c], sc.nf) * dirichlet_rr(ky * (uy[c] - uy[r]), sc.ny) *

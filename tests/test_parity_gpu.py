@@ -203,6 +203,8 @@ def test_loglik_placement_independent(cd, ctx, orc):
     ("c4", "spherical", 128),
     ("c4", "planar_wb", 128),
     ("c4", "planar_nb", 128),
+    ("c2", "planar_nb", 512),    # F2 tensor-core path at the bench configurations
+    ("c3", "planar_nb", 128),
 ])
 def test_loglik_full_size_sampled(cd, ctx, orc, name, wf, nsample):
     """Full BASELINE sizes in the bench launch configuration; oracle on a stratified sample."""
@@ -214,6 +216,7 @@ def test_loglik_full_size_sampled(cd, ctx, orc, name, wf, nsample):
 
 
 @pytest.mark.parametrize("name,wf", [("c2", "spherical"), ("c3", "spherical"), ("c4", "planar_nb"),
+                                     ("c2", "planar_nb"), ("c3", "planar_nb"),
                                      ("c4", "spherical"), ("c5", "spherical")])
 def test_loglik_near_truth_worst_case(cd, ctx, orc, name, wf):
     """Particles within 1 mm of the true position: ||e||^2 = ||z||^2 - 2 Re(m^H c) + m^H G m cancels by

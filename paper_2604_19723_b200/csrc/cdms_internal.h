@@ -197,6 +197,8 @@ struct NbPlan {
   int nacc;            // accumulator pairs (D1 exact hi x hi, D2 the rest) in TMEM: 2 when 4 nb <= 512
   int tmem_cols;       // allocated TMEM columns (power of two >= 32)
   int pexp, qexp;      // hi grids: A_hi on 2^-pexp of |b| = 1, y_hi on 2^-qexp of max|y|; K 2^(p+q) <= 2^24
+  int a_tmem;          // 1: A operand staged in TMEM (tcgen05.st by the generators; MMA reads only B from smem)
+  int a_col0;          // TMEM column of the A ring (a_tmem): stage s at a_col0 + s kc, hi then lo (kc/2 columns each)
   int nf_pad;          // subcarriers padded to kc / 2
   int n_chunks;        // pipeline stages per tile = 2 nf_pad / kc
   uint32_t a_bytes;    // one fp16 piece of the A stage (128 x kc)

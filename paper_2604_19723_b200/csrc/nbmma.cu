@@ -35,6 +35,7 @@
 // Work item = (tile of 128 hypotheses of one PA, antenna pass); arrays with 2 ceil8(N_a) > 256 take several
 // passes (A is regenerated per pass).  Accumulator pairs are double-buffered in TMEM when 4 nb <= 512.
 #include <cuda_fp16.h>
+#include <stdlib.h>
 
 #include "cdms_internal.h"
 #include "geometry.cuh"
@@ -76,6 +77,21 @@ __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// A from TMEM (lane = row, consecutive K elements packed two per 32-bit column), B from shared memory
+__device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -279,6 +295,20 @@ bool nb_tensor_plan(const SceneDev& sc, NbPlan* pl) {
   p.pexp = (pq - p.qexp) > 10 ? 10 : pq - p.qexp;
   if (p.pexp < 4 || p.qexp < 4) return false;  // K > 2^16: the exact grid gets too coarse
   p.smem = (size_t)nst * 2 * (p.a_bytes + p.b_bytes) + 1024;
+  // A in TMEM when the accumulator pair leaves room for >= 3 stages of kc columns (hi and lo, kc/2 fp16x2 words each):
+  // the MMA then reads only B from shared memory.  At N <= 128 every MMA re-reads its 4 KB A tile from shared
+  // memory and the four MMAs of a K-step plus the generator and TMA writes exceed its bandwidth.
+  // The accumulator pair is then single-buffered.  CDMS_NB_ATMEM=0 keeps A in shared memory.
+  const char* ev = getenv("CDMS_NB_ATMEM");
+  if ((ev == nullptr || atoi(ev) != 0) && 2 * p.nb <= 256 && kc == 64) {
+    p.a_tmem = 1;
+    p.nacc = 1;
+    p.a_col0 = 256;
+    int n = (512 - p.a_col0) / kc;
+    p.nst = n < NB_MAX_STAGES ? n : NB_MAX_STAGES;
+    p.tmem_cols = 512;
+    p.smem = (size_t)p.nst * 2 * p.b_bytes + 1024;
+  }
   *pl = p;
   return true;
 }
@@ -418,7 +448,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
   // in uniform registers (no per-MMA ELECT/R2UR waterfall)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int nst = pl.nst, kc = pl.kc, npass = pl.n_pass;
-  const uint32_t stage_bytes = 2 * (pl.a_bytes + pl.b_bytes);
+  const uint32_t stage_bytes = pl.a_tmem ? 2 * pl.b_bytes : 2 * (pl.a_bytes + pl.b_bytes);
   uint8_t* ring = nb_smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(nb_smem + (size_t)nst * stage_bytes);
   uint64_t* full_a = bars;
@@ -427,9 +457,9 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
   uint64_t* acc_full = bars + 3 * NB_MAX_STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  // stage s: [A_hi | A_lo | B_hi | B_lo]
+  // stage s: [A_hi | A_lo | B_hi | B_lo] (A in TMEM: [B_hi | B_lo])
   auto A_hi = [&](int s) { return ring + (size_t)s * stage_bytes; };
-  auto B_hi = [&](int s) { return ring + (size_t)s * stage_bytes + 2 * pl.a_bytes; };
+  auto B_hi = [&](int s) { return ring + (size_t)s * stage_bytes + (pl.a_tmem ? 0 : 2 * pl.a_bytes); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -503,14 +533,27 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
             tc_fence_after();
             const uint64_t sa = dA0 + (uint64_t)slot * slot_step, sb = dB0 + (uint64_t)slot * slot_step;
             if (lane == 0) {
-              for (int ks = 0; ks < nks; ++ks) {
-                const uint64_t dah = sa + (uint64_t)(ks * 16), dbh = sb + (uint64_t)(ks * 16);
-                const uint64_t dal = dah + a_lo_step, dbl = dbh + b_lo_step;
-                const uint32_t acc0 = (q | ks) ? 1u : 0u;
-                umma_f16(d1, dah, dbh, idesc, acc0);
-                umma_f16(d2, dah, dbl, idesc, acc0);
-                umma_f16(d2, dal, dbh, idesc, 1u);
-                umma_f16(d2, dal, dbl, idesc, 1u);
+              if (pl.a_tmem) {
+                const uint32_t ta = tmem + (uint32_t)(pl.a_col0 + slot * kc);  // hi at +0, lo at +kc/2 columns
+                for (int ks = 0; ks < nks; ++ks) {
+                  const uint64_t dbh = sb + (uint64_t)(ks * 16), dbl = dbh + b_lo_step;
+                  const uint32_t tah = ta + (uint32_t)(ks * 8), tal = tah + (uint32_t)(kc / 2);
+                  const uint32_t acc0 = (q | ks) ? 1u : 0u;
+                  umma_f16_ts(d1, tah, dbh, idesc, acc0);
+                  umma_f16_ts(d2, tah, dbl, idesc, acc0);
+                  umma_f16_ts(d2, tal, dbh, idesc, 1u);
+                  umma_f16_ts(d2, tal, dbl, idesc, 1u);
+                }
+              } else {
+                for (int ks = 0; ks < nks; ++ks) {
+                  const uint64_t dah = sa + (uint64_t)(ks * 16), dbh = sb + (uint64_t)(ks * 16);
+                  const uint64_t dal = dah + a_lo_step, dbl = dbh + b_lo_step;
+                  const uint32_t acc0 = (q | ks) ? 1u : 0u;
+                  umma_f16(d1, dah, dbh, idesc, acc0);
+                  umma_f16(d2, dah, dbl, idesc, acc0);
+                  umma_f16(d2, dal, dbh, idesc, 1u);
+                  umma_f16(d2, dal, dbl, idesc, 1u);
+                }
               }
               umma_commit(&empty[slot]);
             }
@@ -527,8 +570,10 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
     // subcarriers from the fp64-reduced phase and a per-tile table t[j] = w^j (j < 16, fp64, rounded once), so
     // each phasor carries one fp32 rounding (no coherent drift of a raised step) and no
     // dependency chain; pairs of subcarriers share f32x2 instructions.
-    const int gt = threadIdx.x - 64;
-    const int h = gt & (NB_M - 1), grp = gt >> 7;
+    // row h = this thread's TMEM lane (warp w may only access lanes [32 (w % 4), +32)): rows of both groups cover
+    // the 128 lanes, consecutive lanes -> consecutive rows (conflict-free 16-byte shared-memory stores as well)
+    const int h = 32 * (warp & 3) + lane, grp = (warp - 2) >> 2;
+    const uint32_t a_lane = (uint32_t)(32 * (warp & 3)) << 16;
     const int nsub = kc / 2;  // subcarriers per stage (8, 16 or 32)
     const double kcen = 0.5 * (sc.nf - 1);
     const float a_scale = (float)(1 << NB_SCALE_LOG2);
@@ -595,13 +640,25 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
                   lo[2 * t2] = pack_h2(x0, y0);
                   lo[2 * t2 + 1] = pack_h2(x1, y1);
                 }
-                const uint32_t off = row_off + (uint32_t)((a16 + 2 * p4) / 4) * 128u;
-                *reinterpret_cast<uint4*>(ahi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                *reinterpret_cast<uint4*>(ahi + pl.a_bytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                const int chunk = (a16 + 2 * p4) / 4;  // 4 subcarriers = 4 fp16x2 words per piece
+                if (pl.a_tmem) {
+                  const uint32_t ta = tmem + a_lane + (uint32_t)(pl.a_col0 + slot * kc + chunk * 4);
+                  tmem_st4(ta, hi[0], hi[1], hi[2], hi[3]);
+                  tmem_st4(ta + (uint32_t)(kc / 2), lo[0], lo[1], lo[2], lo[3]);
+                } else {
+                  const uint32_t off = row_off + (uint32_t)chunk * 128u;
+                  *reinterpret_cast<uint4*>(ahi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                  *reinterpret_cast<uint4*>(ahi + pl.a_bytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                }
               }
             }
           }
-          fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
+          if (pl.a_tmem) {
+            tmem_wait_st();     // this warp's TMEM stores complete, ordered before the arrive
+            tc_fence_before();
+          } else {
+            fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(&full_a[slot]);
         }

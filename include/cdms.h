@@ -32,6 +32,11 @@
  *    cdms_bp_step are COLLECTIVE over the ranks (every rank calls them, each with its P_local
  *    particles; global particle index = rank * P_local + local index, P_local equal on all ranks).
  *    cdms_loglik, cdms_response and cdms_layout are purely local.
+ *  - Engines: spherical and planar-WB likelihoods (and every FP64 evaluation) run on the FP32/FP64 pipes
+ *    (segmented Horner correlation); PLANAR_NB in FP32 runs its correlation on the tensor cores
+ *    (tcgen05, error-free fp16 split) with a closed-form Gram.  Environment knobs read
+ *    at cdms_create / per call, for A/B measurements only: CDMS_NB_TENSOR=0 keeps PLANAR_NB on the FP32 pipe,
+ *    CDMS_NB_ATMEM=0 keeps the tensor path's A operand in shared memory.
  */
 #ifndef CDMS_H_
 #define CDMS_H_
@@ -143,7 +148,8 @@ cdms_status cdms_layout(cdms_ctx ctx, const cdms_scene* scene, const double* d_s
  *   d_logw_prior [P] fp64 or NULL (= 0).
  *   d_loglik    out [P] fp64.
  *   d_amp       out complex128 [P][J][S] LMMSE amplitudes m + V^1/2 K^-1 M^H e / eta, or NULL.
- * Purely local (no communication).  Degenerate particles: l = -inf + CDMS_EDEGENERATE at sync. */
+ * Purely local (no communication).  Degenerate particles: l = -inf + CDMS_EDEGENERATE at sync.
+ * PLANAR_NB in FP32: correlation on the tensor cores (see Conventions, "Engines"). */
 cdms_status cdms_loglik(cdms_ctx ctx, const cdms_scene* scene, const double* d_particles,
                         int64_t P, int32_t pstride, const double* d_sfv, int32_t sfv_per_particle,
                         const void* d_y, const double* h_f_pb, const cdms_prior* h_prior,

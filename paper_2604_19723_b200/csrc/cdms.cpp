@@ -602,6 +602,13 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
     WS_TRY(ctx, WS_SCHED, 2, &sch);
     WS_TRY(ctx, WS_STEP_CNT, 4, &sch);
     WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &f4);
+    NbPlan nbp{};  // the tensor-core path's per-PA B operand and scales (PLANAR_NB, FP32)
+    if (ctx->nb_tensor && scene->precision == CDMS_FP32 && nb_tensor_plan(sd, &nbp)) {
+      uint8_t* nbop;
+      float* nbs;
+      WS_TRY(ctx, WS_NBOP, nb_operand_bytes(sd, nbp), &nbop);
+      WS_TRY(ctx, WS_NBSCALE, MAXJ, &nbs);
+    }
   }
   WS_TRY(ctx, WS_YNORM, MAXJ, &d);
   WS_TRY(ctx, WS_LSE_PART, nb + 1, &d2);

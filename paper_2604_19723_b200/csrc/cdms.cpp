@@ -31,6 +31,7 @@ struct cdms_ctx_s {
   uint64_t* h_pinned = nullptr;  // small pinned host staging (plan exchange)
   bool timing = false;           // bracket the likelihood kernel with events
   bool nb_tensor = true;         // PLANAR_NB fp32 on the tensor cores (nbmma.cu); CDMS_NB_TENSOR=0 selects K1
+  bool taylor = true;            // spherical / planar-WB fp32 correlation by K1T (taylor.cu); CDMS_TAYLOR=0 selects K1
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
 };
@@ -41,7 +42,7 @@ enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
   WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
   WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BC, WS_BLL, WS_BPB,
-  WS_BPART, WS_BPART6, WS_BSCR, WS_COUNT
+  WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -405,6 +406,15 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   const bool nbt = ctx->nb_tensor && precision == CDMS_FP32 && nb_tensor_plan(sd, &nbp);
   uint8_t* nbop = nullptr;
   float* nbscale = nullptr;
+  // spherical / planar WB in FP32: c from spectral Taylor tables (K1T), G from K1's Horner-free variant
+  const bool tay = !nbt && ctx->taylor && precision == CDMS_FP32 && sd.wavefront != CDMS_PLANAR_NB &&
+                   tay_table_bytes(sd) <= ((size_t)96 << 20);
+  float2* taytab = nullptr;
+  if (tay) {
+    WS_TRY(ctx, WS_TAY, tay_table_bytes(sd) / sizeof(float2), &taytab);
+    CUDA_TRY(ctx, launch_tay_prep(sd, static_cast<const float2*>(d_y), taytab, ctx->stream));
+    ctx->launches += 1;
+  }
   if (nbt) {
     WS_TRY(ctx, WS_NBOP, nb_operand_bytes(sd, nbp), &nbop);
     WS_TRY(ctx, WS_NBSCALE, MAXJ, &nbscale);
@@ -437,7 +447,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     a.flags = ctx->d_flags;
     a.n_tiles = (nb + TILE_P - 1) / TILE_P;
     a.n_groups = a.n_tiles * sd.J;
-    a.grid = corr_grid(sd, a.n_tiles, precision, ctx->num_sms);
+    a.grid = tay ? corr_grid_gram_only(sd, a.n_tiles, ctx->num_sms) : corr_grid(sd, a.n_tiles, precision, ctx->num_sms);
     if (a.grid < 1) return fail(ctx, CDMS_ECUDA, "corr_kernel occupancy query failed");
     a.sched = sched;
     a.no_gram = no_gram ? 1 : 0;
@@ -469,6 +479,11 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       CUDA_TRY(ctx, launch_nb_gram(sd, na, pflag, ctx->stream));
       CUDA_TRY(ctx, launch_nb_corr(sd, nbp, na, ctx->num_sms, ctx->stream));
       ctx->launches += 1;
+    } else if (tay) {
+      if (!no_gram) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));  // G (K1, Horner-free)
+      CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, pflag,
+                                    no_gram ? 1 : 0, ctx->stream));
+      ctx->launches += no_gram ? 0 : 1;
     } else {
       CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
     }
@@ -508,6 +523,7 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   DeviceGuard g(device);
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("CDMS_NB_TENSOR")) ctx->nb_tensor = atoi(e) != 0;
+  if (const char* e = getenv("CDMS_TAYLOR")) ctx->taylor = atoi(e) != 0;
   if (cudaMalloc(&ctx->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_flags, 0, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {
     delete ctx;

@@ -187,6 +187,16 @@ cudaError_t launch_regularize(double* x, int64_t P, int64_t p0, int64_t P_total,
                               uint64_t key, uint64_t step, cudaStream_t st);
 cudaError_t launch_fill_u64(uint64_t* dst, uint64_t v, int n, cudaStream_t st);
 
+// loglik.cu K1 Gram-only variant + taylor.cu K1T (spherical / planar-WB correlation from spectral Taylor tables)
+int64_t corr_grid_gram_only(const SceneDev& sc, int64_t n_tiles, int num_sms);  // 0 on error
+cudaError_t launch_corr_gram_only(const SceneDev& sc, const CorrArgs& a, cudaStream_t st);
+int tay_centres(int nf);
+size_t tay_table_bytes(const SceneDev& sc);
+cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, cudaStream_t st);
+cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,
+                            int64_t P, int pstride, const double* sfv, int sfv_pp, double2* terms, int* pflag,
+                            int gram_diag, cudaStream_t st);
+
 // nbmma.cu: PLANAR_NB correlation on the tensor cores
 struct NbPlan {
   int kc;              // real K per pipeline stage (2 x subcarriers), 16 / 32 / 64

@@ -340,7 +340,9 @@ __device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const 
 // one CTA: results do not depend on the schedule.  The last CTA to finish resets the counters.
 // TWO: compile-time sc.two_seg (the segment end either moves A1 in or multiplies by Z; two instantiations keep
 // both Horner loops free of the other's register pressure).
-template <int S, typename RT, bool TWO>
+// NOH: Gram-only variant for K1T (taylor.cu), which writes c afterwards: no phasors, no Horner steps (the y chunks
+// still stream so the per-warp TMA ring keeps its protocol).
+template <int S, typename RT, bool TWO, bool NOH = false>
 __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
     corr_kernel(const __grid_constant__ SceneDev sc, const CorrArgs a) {
   using PL = Plan<S, RT>;
@@ -526,7 +528,21 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
           o.Ar = f.E0r; o.Ai = f.E0i; o.wr = f.Whr; o.wi = f.Whi; o.Zr = f.Zhr; o.Zi = f.Zhi; o.delta = f.hx * v[0];
           dg = false;
 #else
-          setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
+          if (NOH) {  // Delta only (the Gram's input)
+            const RT rq = f.hx * v[0] + f.hy * v[1] + f.hz * v[2];
+            if (sc.wavefront == CDMS_SPHERICAL) {
+              const RT n = q2 - RT(2) * rq;
+              const RT d = Num<RT>::fsqrt_(f.R * f.R + n);
+              dg = !(d > RT(0));
+              o.delta = Num<RT>::fdiv_(n, d + f.R);
+            } else {
+              o.delta = Num<RT>::fdiv_(-rq, f.R);
+              dg = false;
+            }
+            o.Ar = o.Ai = o.wr = o.wi = o.Zr = o.Zi = RT(0);
+          } else {
+            setup_sm<RT>(sc, f, v, q2, m, s, o, dg);
+          }
 #endif
           deg_any |= dg;
           Ar[s] = o.Ar; Ai[s] = o.Ai; wr[s] = o.wr; wi[s] = o.wi; Zr[s] = o.Zr; Zi[s] = o.Zi;
@@ -552,11 +568,11 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
 #ifdef CDMS_XP_SKIP_HORNER  // experiment build only (wrong results): price everything but the Horner steps
           if (false) {
 #else
-          if (k1 - k0 == SEG) {
+          if (!NOH && k1 - k0 == SEG) {
 #endif
 #pragma unroll 7
             for (int i = 1; i < SEG; ++i) H.step(yk[-i]);
-          } else {
+          } else if (!NOH) {
 #ifndef CDMS_XP_SKIP_HORNER
             for (int i = 1; i < k1 - k0; ++i) H.step(yk[-i]);
 #endif
@@ -880,6 +896,32 @@ static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStre
   else
     corr_kernel<S, RT, false><<<(unsigned)a.grid, NTHREADS, Plan<S, RT>::total, st>>>(sc, a);
   return cudaGetLastError();
+}
+
+template <int S>
+static cudaError_t launch_corr_noh_t(const SceneDev& sc, const CorrArgs& a, cudaStream_t st) {
+  if (a.grid < 1 || a.n_groups < 1) return cudaSuccess;
+  corr_kernel<S, float, false, true><<<(unsigned)a.grid, NTHREADS, Plan<S, float>::total, st>>>(sc, a);
+  return cudaGetLastError();
+}
+int64_t corr_grid_gram_only(const SceneDev& sc, int64_t n_tiles, int num_sms) {
+  switch (sc.S) {
+#define CASE_S(n) \
+  case n: return grid_for_kernel(corr_kernel<n, float, false, true>, NTHREADS, Plan<n, float>::total, n_tiles * sc.J, \
+                                 num_sms);
+    CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
+#undef CASE_S
+    default: return 0;
+  }
+}
+cudaError_t launch_corr_gram_only(const SceneDev& sc, const CorrArgs& a, cudaStream_t st) {
+  switch (sc.S) {
+#define CASE_S(n) \
+  case n: return launch_corr_noh_t<n>(sc, a, st);
+    CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
+#undef CASE_S
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 int64_t corr_grid(const SceneDev& sc, int64_t n_tiles, int precision, int num_sms) {

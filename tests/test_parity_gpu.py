@@ -410,3 +410,35 @@ def test_bp_step_graph_capture(cd, orc, wf):
     ctx.sync()
     assert torch.equal(x_g, x_e) and torch.equal(est_g, est_e) and torch.equal(lse_g, lse_e)
     ctx.close()
+
+
+@pytest.mark.parametrize("nf", [15, 16, 33])
+@pytest.mark.parametrize("wf", ["spherical", "planar_wb"])
+def test_taylor_engine_period_wrap(cd, ctx, orc, nf, wf):
+    """K1T (spectral Taylor tables, taylor.cu): a 2 GHz band over few subcarriers makes df R/c span several periods,
+    so the anti-periodicity sign (-1)^(N_f - 1) of the centred spectrum is exercised for odd and even N_f."""
+    cfg = scenes.custom_config("wrap", J=2, K=3, ny=4, nv=4, nf=nf, P=200, fc=6.5e9, B=2e9, index=97)
+    check_loglik(Case(orc, cfg, wavefront=wf), ctx, "fp32", amp=True)
+
+
+def test_taylor_engine_matches_k1(cd, orc):
+    """K1T and K1 (CDMS_TAYLOR=0) evaluate the same scene to within the fp32 tolerance of each other."""
+    import os
+    cfg = small_cfg(J=2, K=4, ny=8, nv=8, nf=128, P=300)
+    ctxs = []
+    try:
+        ctxs.append(cd.Context(0))
+        os.environ["CDMS_TAYLOR"] = "0"
+        ctxs.append(cd.Context(0))
+    finally:
+        os.environ.pop("CDMS_TAYLOR", None)
+    case = Case(orc, cfg)
+    l_t = case.gpu_loglik(ctxs[0]).cpu().numpy()
+    l_k = case.gpu_loglik(ctxs[1]).cpu().numpy()
+    for c in ctxs:
+        c.sync()
+    e = rel_err(l_t, l_k, cfg.J, cfg.Nz).max()
+    record("taylor_vs_k1_rel_l", e, 2e-4)
+    assert e <= 2e-4, e
+    for c in ctxs:
+        c.close()

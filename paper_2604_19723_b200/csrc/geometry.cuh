@@ -145,7 +145,8 @@ __device__ __forceinline__ void load_psf(const RT* src, RT* fv) {
 // Returns PS_OK, PS_DEGENERATE (MT on the phase centre, r' = 0 excluded by P:L2137) or PS_BADSFV
 // (||sfv|| = 0).  On failure the fields hold a harmless finite placeholder.
 enum { PS_OK = 0, PS_DEGENERATE = 1, PS_BADSFV = 2 };
-template <typename RT>
+// PH = false (K1's Gram-only variant): geometry and gain only, no phase-centre phasors.
+template <typename RT, bool PH = true>
 __device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double* pos, const double* sfv_s,
                                         PSField<RT>& f, double& R64) {
   double va[3], sh[3];
@@ -160,20 +161,25 @@ __device__ __forceinline__ int setup_ps(const SceneDev& sc, int j, const double*
   const double rs2 = 2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]);
   f.hx = (RT)(r0 - rs2 * sh[0]); f.hy = (RT)(r1 - rs2 * sh[1]); f.hz = (RT)(r2 - rs2 * sh[2]);
   f.R = (RT)R;
-  double s_, c_;
-  sincospi(2.0 * frac_c(R * sc.f0_c), &s_, &c_);
-  f.E0r = (RT)c_; f.E0i = (RT)s_;
-  sincospi(2.0 * frac_c(R * sc.df_c), &s_, &c_);
-  f.Whr = (RT)c_; f.Whi = (RT)s_;
-  f.Wlr = (RT)(c_ - (double)f.Whr); f.Wli = (RT)(s_ - (double)f.Whi);
-  sincospi(2.0 * frac_c(R * sc.segdf_c), &s_, &c_);
-  f.Zhr = (RT)c_; f.Zhi = (RT)s_;
-  f.Zlr = (RT)(c_ - (double)f.Zhr); f.Zli = (RT)(s_ - (double)f.Zhi);
-  if (sc.two_seg) {
-    sincospi(2.0 * frac_c(R * sc.f1_c), &s_, &c_);
-    f.E1r = (RT)c_; f.E1i = (RT)s_;
+  if (PH) {
+    double s_, c_;
+    sincospi(2.0 * frac_c(R * sc.f0_c), &s_, &c_);
+    f.E0r = (RT)c_; f.E0i = (RT)s_;
+    sincospi(2.0 * frac_c(R * sc.df_c), &s_, &c_);
+    f.Whr = (RT)c_; f.Whi = (RT)s_;
+    f.Wlr = (RT)(c_ - (double)f.Whr); f.Wli = (RT)(s_ - (double)f.Whi);
+    sincospi(2.0 * frac_c(R * sc.segdf_c), &s_, &c_);
+    f.Zhr = (RT)c_; f.Zhi = (RT)s_;
+    f.Zlr = (RT)(c_ - (double)f.Zhr); f.Zli = (RT)(s_ - (double)f.Zhi);
+    if (sc.two_seg) {
+      sincospi(2.0 * frac_c(R * sc.f1_c), &s_, &c_);
+      f.E1r = (RT)c_; f.E1i = (RT)s_;
+    } else {
+      f.E1r = RT(1); f.E1i = RT(0);
+    }
   } else {
-    f.E1r = RT(1); f.E1i = RT(0);
+    f.E0r = f.Whr = f.Zhr = f.E1r = RT(1);
+    f.E0i = f.Whi = f.Zhi = f.E1i = f.Wlr = f.Wli = f.Zlr = f.Zli = RT(0);
   }
   f.gain = (RT)(sc.pathloss ? sc.lambda / (4.0 * PI * R) : 1.0);
   if (!sfv_ok) return PS_BADSFV;

@@ -386,10 +386,12 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
     if (is_g >= n_groups) return;
     // No proxy fence: the buffer is only read by the generic proxy (LDS, completed before the __syncwarp that
     // precedes every reissue) and only written by the async proxy.
-    uint64_t* bar = &mbar[warp * 2 + (is_c & 1)];
-    const uint32_t chunk_bytes = (uint32_t)(sc.kc_len * sizeof(float4));
-    mbar_expect_tx(bar, chunk_bytes);
-    tma_load_1d(ybuf + (warp * 2 + (is_c & 1)) * KC, a.ytiles + is_off, chunk_bytes, bar);
+    if (!NOH) {  // the Gram-only variant keeps the stream's counters (group claims) but moves no data
+      uint64_t* bar = &mbar[warp * 2 + (is_c & 1)];
+      const uint32_t chunk_bytes = (uint32_t)(sc.kc_len * sizeof(float4));
+      mbar_expect_tx(bar, chunk_bytes);
+      tma_load_1d(ybuf + (warp * 2 + (is_c & 1)) * KC, a.ytiles + is_off, chunk_bytes, bar);
+    }
     ++is_c;
     is_off += sc.kc_len;
     if (++is_kc == sc.n_kc) {
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
       if (s > 0) sfv_s = a.sfv + ((a.sfv_pp && pp < a.P) ? pp * 3 * sc.K : 0) + 3 * (s - 1);
       PSField<RT> f;
       double R64 = 1.0;
-      const int st = setup_ps<RT>(sc, j, pos, sfv_s, f, R64);
+      const int st = setup_ps<RT, !NOH>(sc, j, pos, sfv_s, f, R64);
       if (st != PS_OK && pp < a.P) {
         const bool bad = st == PS_BADSFV || !(pos[0] == pos[0] && pos[1] == pos[1] && pos[2] == pos[2]);
         atomicOr(&pfl[pl], bad ? 3 : 1);
@@ -557,10 +559,10 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
       }
       // ---- (3) correlation over all subcarriers (row A3): segmented Horner on TMA-staged y chunks
       for (int kc = 0; kc < n_kc; ++kc, ++ci) {
-        mbar_wait(&mbar[warp * 2 + (ci & 1)], (uint32_t)((ci >> 1) & 1));
+        if (!NOH) mbar_wait(&mbar[warp * 2 + (ci & 1)], (uint32_t)((ci >> 1) & 1));
         const float4* yb = ybuf + (warp * 2 + (ci & 1)) * KC;
         const int k_begin = kc * kcl;
-        const int k_end = min(k_begin + kcl, nf);
+        const int k_end = NOH ? k_begin : min(k_begin + kcl, nf);  // Gram-only: no correlation
         for (int k0 = k_begin; k0 < k_end; k0 += SEG) {
           const int k1 = min(k0 + SEG, k_end);
           const float4* yk = yb + (k1 - 1 - k_begin);  // Horner runs from the top subcarrier down

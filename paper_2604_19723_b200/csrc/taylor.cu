@@ -29,47 +29,66 @@ constexpr int TAY_BLOCK = 128;
 int tay_centres(int nf) { return 4 * nf; }
 size_t tay_table_bytes(const SceneDev& sc) { return (size_t)sc.J * sc.Na * tay_centres(sc.nf) * TAY_L * sizeof(float2); }
 
-// tab[j][m][g][l] (complex64, l fastest: one 64-byte row per (j, m, g)).  Thread per (j, m, g), fp64 sums over k
-// with the phasor e^{j2pi (k-k0) g/G} advanced by recurrence (re-anchored every 64 subcarriers).
+// tab[j][m][g][l] (complex64, l fastest: one 64-byte row per (j, m, g)).  TAY_KS lanes per row split the subcarrier
+// sum (each from an exact anchor e^{j2pi (k - k0) g / G}, fp64 phasor recurrence inside its segment), combined by a
+// fixed shuffle tree: row count alone (J N_a G) would leave most SMs idle at small N_a G.
+constexpr int TAY_KS = 8;
 __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ y,
                                 float2* __restrict__ tab) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = tid / TAY_KS;
+  const int seg = (int)(tid - t * TAY_KS);
   const int64_t per_j = (int64_t)sc.Na * G;
-  if (t >= per_j * sc.J) return;
-  const int j = (int)(t / per_j);
-  const int64_t r = t - (int64_t)j * per_j;
+  const bool live = t < per_j * sc.J;
+  const int64_t tt = live ? t : 0;
+  const int j = (int)(tt / per_j);
+  const int64_t r = tt - (int64_t)j * per_j;
   const int m = (int)(r / G), g = (int)(r - (int64_t)m * G);
   const double k0 = 0.5 * (sc.nf - 1);
   double cr[TAY_L], ci[TAY_L];
 #pragma unroll
   for (int l = 0; l < TAY_L; ++l) cr[l] = ci[l] = 0.0;
-  double sw, cw;
-  sincospi(2.0 * (double)g / (double)G, &sw, &cw);  // step e^{j2pi g/G}
-  double pr = 1.0, pi = 0.0;
-  const float2* ym = y + (int64_t)j * sc.nf * sc.Na + m;
-  for (int k = 0; k < sc.nf; ++k) {
-    if ((k & 63) == 0) {  // anchor e^{j2pi (k - k0) g / G}, exact argument reduction: 2 (k - k0) g mod 2G
-      const double num = fmod(2.0 * ((double)k - k0) * (double)g, 2.0 * (double)G);
-      sincospi(num / (double)G, &pi, &pr);
+  const int kseg = (sc.nf + TAY_KS - 1) / TAY_KS;
+  const int kb = seg * kseg, ke = min(kb + kseg, sc.nf);
+  if (live && kb < ke) {
+    double sw, cw;
+    sincospi(2.0 * (double)g / (double)G, &sw, &cw);  // step e^{j2pi g/G}
+    double pr = 1.0, pi = 0.0;
+    const float2* ym = y + (int64_t)j * sc.nf * sc.Na + m;
+    for (int k = kb; k < ke; ++k) {
+      if (((k - kb) & 63) == 0) {  // anchor e^{j2pi (k - k0) g / G}: exact argument reduction of 2 (k - k0) g mod 2G
+        const double num = fmod(2.0 * ((double)k - k0) * (double)g, 2.0 * (double)G);
+        sincospi(num / (double)G, &pi, &pr);
+      }
+      const float2 v = ym[(int64_t)k * sc.Na];
+      double br = v.x * pr - v.y * pi, bi = v.x * pi + v.y * pr;  // y_k e^{j2pi (k-k0) g/G}
+      const double tk = 2.0 * PI * ((double)k - k0) / (double)G;
+#pragma unroll
+      for (int l = 0; l < TAY_L; ++l) {
+        cr[l] += br;
+        ci[l] += bi;
+        const double nr = -bi * tk / (double)(l + 1), ni = br * tk / (double)(l + 1);  // * (j tk)/(l+1)
+        br = nr;
+        bi = ni;
+      }
+      const double npr = pr * cw - pi * sw;
+      pi = pr * sw + pi * cw;
+      pr = npr;
     }
-    const float2 v = ym[(int64_t)k * sc.Na];
-    double br = v.x * pr - v.y * pi, bi = v.x * pi + v.y * pr;  // y_k e^{j2pi (k-k0) g/G}
-    const double tk = 2.0 * PI * ((double)k - k0) / (double)G;
+  }
+#pragma unroll
+  for (int o = TAY_KS / 2; o > 0; o >>= 1) {
 #pragma unroll
     for (int l = 0; l < TAY_L; ++l) {
-      cr[l] += br;
-      ci[l] += bi;
-      const double nr = -bi * tk / (double)(l + 1), ni = br * tk / (double)(l + 1);  // * (j tk)/(l+1)
-      br = nr;
-      bi = ni;
+      cr[l] += __shfl_xor_sync(0xffffffffu, cr[l], o);
+      ci[l] += __shfl_xor_sync(0xffffffffu, ci[l], o);
     }
-    const double npr = pr * cw - pi * sw;
-    pi = pr * sw + pi * cw;
-    pr = npr;
   }
-  float2* out = tab + t * TAY_L;
+  if (live && seg == 0) {
+    float2* out = tab + t * TAY_L;
 #pragma unroll
-  for (int l = 0; l < TAY_L; ++l) out[l] = make_float2((float)cr[l], (float)ci[l]);
+    for (int l = 0; l < TAY_L; ++l) out[l] = make_float2((float)cr[l], (float)ci[l]);
+  }
 }
 
 // c_s for one particle per thread and one PA per blockIdx.y: per component the fp64 geometry (VA, H r, R), the
@@ -173,8 +192,8 @@ __global__ void __launch_bounds__(TAY_BLOCK)
 
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, cudaStream_t st) {
   const int G = tay_centres(sc.nf);
-  const int64_t n = (int64_t)sc.J * sc.Na * G;
-  tay_prep_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(sc, G, y, tab);
+  const int64_t n = (int64_t)sc.J * sc.Na * G * TAY_KS;
+  tay_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, G, y, tab);
   return cudaGetLastError();
 }
 cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,

@@ -480,7 +480,9 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       CUDA_TRY(ctx, launch_nb_corr(sd, nbp, na, ctx->num_sms, ctx->stream));
       ctx->launches += 1;
     } else if (tay) {
-      if (!no_gram) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));  // G (K1, Horner-free)
+      // G from K1's Horner-free variant, which writes every term (c as zeros): it precedes K1T.  (A dedicated
+      // thread-per-pair Gram kernel was measured slower: 8 MUFU per pair and antenna, c3 16.0 vs 14.1 ms.)
+      if (!no_gram) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));
       CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, pflag,
                                     no_gram ? 1 : 0, ctx->stream));
       ctx->launches += no_gram ? 0 : 1;

@@ -288,49 +288,6 @@ namespace cdms {
 #define PT_FLUSH
 #endif
 
-// ---------------------------------------------------------------------------- Gram term per (pair, antenna)
-// sum_k e^{j 2 pi dd_m f_k / c} relative to the pair's base carrier, for one antenna (row A4):
-//   e^{j 2 pi dd fc/c} D_N(x), x = dR df/c + dd df/c = nb + xbr + dd df/c, dd = Delta_a,m - Delta_b,m
-//   D_N(n + xr) = (-1)^{n (N-1)} sin(pi N xr) / sin(pi xr), D_N(0) = N (C-amb-13)
-// fp32: MUFU carrier and numerator (after exact mod-2 reduction of N xr), polynomial sin(pi xr), one
-// approximate reciprocal, branch-free small-|xr| series and sign; fp64: exact library functions.
-struct GramPairF {
-  float xbr;        // centred fraction of dR df/c (from fp64)
-  uint32_t nbpar;   // parity of the integer part nb, shifted to bit 31 when N is even (sign flips), else 0
-};
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const GramPairF& gp, float& gr,
-                                            float& gi) {
-  const float fc_c = sc.fc_cf, df_c = sc.df_cf, Nf = sc.nf_f, c6N = sc.c6N_f;
-  const uint32_t evenN_mask = sc.evenN_mask;
-  float ph = dd * fc_c;
-  ph -= rintf(ph);
-  float sn, cs;
-  __sincosf(6.28318530717958647692f * ph, &sn, &cs);
-  const float x = fmaf(dd, df_c, gp.xbr);
-  const float n2 = rintf(x);
-  const float xr = x - n2;
-  float t = Nf * xr;
-  t = fmaf(-2.f, rintf(0.5f * t), t);
-  const float num = __sinf(3.14159265358979f * t);
-  const float u = 3.14159265358979f * xr, u2 = u * u;
-  // sin(pi xr), |xr| <= 1/2: odd Taylor polynomial to (pi xr)^11 (error < 6e-8 at pi/2)
-  const float den = u * fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, -1.f / 39916800, 1.f / 362880), -1.f / 5040),
-                                                1.f / 120), -1.f / 6), 1.f);
-  float D = num * rcp_approx(den);
-  const float Ds = Nf * fmaf(-c6N, xr * xr, 1.f);  // N (1 - pi^2/6 (N^2 - 1) xr^2)
-  D = (fabsf(xr) < 1e-6f) ? Ds : D;
-  // (-1)^{(nb + n2)(N-1)}: parity of the integer-valued n2 from the mantissa after adding 1.5 * 2^23
-  const uint32_t par = ((uint32_t)__float_as_int(n2 + 12582912.f) << 31) ^ gp.nbpar;
-  D = __int_as_float(__float_as_int(D) ^ (int)(par & evenN_mask));
-  gr = fmaf(D, cs, gr);
-  gi = fmaf(D, sn, gi);
-}
-
 // ---------------------------------------------------------------------------- K1
 // Work distribution: dynamic.  A group is (tile of 32 particles, PA j), g = tile J + j; thread 0 of each
 // persistent CTA claims groups from a global counter one or two groups ahead (ring in shared memory) so the per-warp

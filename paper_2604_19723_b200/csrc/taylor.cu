@@ -181,11 +181,10 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     }
     const double gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
     terms[(p * J + j) * T + s] = make_double2(accr * gn, acci * gn);
-    if (gram_diag) {  // callers that use c only (no K1 pass): G = diag(g^2 N_z), row s of the lower triangle
-      double2* gr = terms + (p * J + j) * T + S + s * (s + 1) / 2;
+    double2* gr = terms + (p * J + j) * T + S + s * (s + 1) / 2;  // row s of the lower triangle of G
+    gr[s] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);  // G_ss = g^2 N_z
+    if (gram_diag)  // callers that use c only: no off-diagonal Gram
       for (int c = 0; c < s; ++c) gr[c] = make_double2(0.0, 0.0);
-      gr[s] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);
-    }
   }
   if (fl) atomicOr(&pflag[p], fl);
 }

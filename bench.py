@@ -50,6 +50,12 @@ def measured_tensor_peak():
         return 2250.0 * 0.72, "fallback: nominal 2.25 PFLOP/s x 0.72"
 
 
+def taylor_path(args) -> bool:
+    """Spherical / planar WB in fp32 evaluate the correlation with K1T (taylor.cu) unless CDMS_TAYLOR=0."""
+    return (args.wavefront != "planar_nb" and args.precision == "fp32"
+            and os.environ.get("CDMS_TAYLOR", "1") != "0")
+
+
 def nb_tensor_path(args) -> bool:
     """PLANAR_NB in fp32 runs the likelihood on the tensor cores (nbmma.cu) unless CDMS_NB_TENSOR=0."""
     return (args.wavefront == "planar_nb" and args.precision == "fp32"
@@ -299,6 +305,23 @@ def run_cdms(args):
                     "traffic": (traffic_from_profiles(args.config + "_planar_nb") if args.particles is None else None),
                     "traffic_basis": "dram read+write bytes of one nb_corr_kernel launch, ncu --set full "
                                      "(profiles/loglik_traffic.json); particles in, c out (tensor-bound)"}
+        elif taylor_path(args):
+            # K1T (taylor.cu): the correlation from spectral Taylor tables, O(1) work per (particle, component,
+            # antenna) instead of the direct recurrence's O(N_f); achieved still counts SURVEY 8(d)'s direct-
+            # correlation flops (8 N_z per unit), so frac > 1 means the likelihood stage beats the FP32 roofline of
+            # the direct method.  The stage's own resource profile is in profiles/r01_k1t_*.
+            roof = {"bound": "alu", "pipe": "fp32 (direct-correlation flop equivalent)", "achieved": round(achieved, 3),
+                    "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                    "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
+                    "kernel": "cdms::tay_corr_kernel (K1T, c) + corr_kernel<S, float, 0, 1> (Horner-free K1, G)",
+                    "kernel_ms": round(kernel_ms, 4),
+                    "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
+                    "launches_per_step": launches_per_step, "flop_per_launch": flop_launch,
+                    "note": "frac > 1: K1T evaluates c from spectral Taylor tables (DESIGN.md 'K1T'); the flop count "
+                            "is the direct correlation's 8 N_z per (particle, PA, component)",
+                    "traffic": (traffic_from_profiles(args.config + "_k1t") if args.particles is None else None),
+                    "traffic_basis": "dram read+write bytes of one tay_corr_kernel launch, ncu --set full "
+                                     "(profiles/loglik_traffic.json)"}
         else:
             roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4),

@@ -557,10 +557,15 @@ def run_birth(args):
         else:
             ach = flop_launch / (kernel_ms / 1e3) / 1e12
             peak = fp32_peak_tflops(1965.0)
-            roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(ach, 3), "peak": round(peak, 2),
+            roof = {"bound": "alu", "pipe": "fp32 (direct-correlation flop equivalent)" if taylor_path(args)
+                    else "fp32 fma", "achieved": round(ach, 3), "peak": round(peak, 2),
                     "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                     "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
-                    "kernel": "cdms::corr_kernel (F3 correlations, K = 0 scene at the mirrored positions)"}
+                    "kernel": ("cdms::tay_corr_kernel (K1T, F3 correlations of the candidate walls)" if taylor_path(args)
+                               else "cdms::corr_kernel (F3 correlations of the candidate walls)")}
+            if taylor_path(args):
+                roof["note"] = ("frac > 1: K1T evaluates the correlations from spectral Taylor tables; the flop count "
+                                "is the direct correlation's 8 N_z per (candidate, PA)")
         roof.update({"kernel_ms": round(kernel_ms, 4), "kernel_share_of_step": round(kernel_ms * launches_per_step /
                                                                                     ms_per_step, 4),
                      "launches_per_step": launches_per_step,

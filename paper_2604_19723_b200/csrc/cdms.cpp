@@ -32,6 +32,8 @@ struct cdms_ctx_s {
   bool timing = false;           // bracket the likelihood kernel with events
   bool nb_tensor = true;         // PLANAR_NB fp32 on the tensor cores (nbmma.cu); CDMS_NB_TENSOR=0 selects K1
   bool taylor = true;            // spherical / planar-WB fp32 correlation by K1T (taylor.cu); CDMS_TAYLOR=0 selects K1
+  int taylor_gram = 0;           // K1T's off-diagonal Gram: 0 by S, 1 K1's Horner-free variant, 2 tay_gram_kernel
+                                 // (CDMS_TAYLOR_GRAM=k1 / tay, A/B only)
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
 };
@@ -480,11 +482,16 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       CUDA_TRY(ctx, launch_nb_corr(sd, nbp, na, ctx->num_sms, ctx->stream));
       ctx->launches += 1;
     } else if (tay) {
-      // G from K1's Horner-free variant, which writes every term (c as zeros): it precedes K1T.  (A dedicated
-      // thread-per-pair Gram kernel was measured slower: 8 MUFU per pair and antenna, c3 16.0 vs 14.1 ms.)
-      if (!no_gram) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));
+      // c and G_ss from K1T; the off-diagonal Gram from tay_gram_kernel (thread per particle, all pairs), or with
+      // CDMS_TAYLOR_GRAM=k1 from K1's Horner-free variant, which writes every term (c as zeros) and so runs first
+      // measured (profiles/r01_k1t_gram_select.txt): the thread-per-particle kernel wins up to S = 5 (c4: 12.8 vs
+      // 13.8 ms, c2 equal), K1's Horner-free variant from S = 7 (c3 14.4 vs 15.3, c5 shard 87 vs 110)
+      const bool k1g = !no_gram && (ctx->taylor_gram == 1 || (ctx->taylor_gram == 0 && sd.S >= 6));
+      if (k1g) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));
       CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, pflag,
                                     no_gram ? 1 : 0, ctx->stream));
+      if (!no_gram && !k1g)
+        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, ctx->stream));
       ctx->launches += no_gram ? 0 : 1;
     } else {
       CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
@@ -526,6 +533,7 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("CDMS_NB_TENSOR")) ctx->nb_tensor = atoi(e) != 0;
   if (const char* e = getenv("CDMS_TAYLOR")) ctx->taylor = atoi(e) != 0;
+  if (const char* e = getenv("CDMS_TAYLOR_GRAM")) ctx->taylor_gram = strcmp(e, "k1") == 0 ? 1 : (strcmp(e, "tay") == 0 ? 2 : 0);
   if (cudaMalloc(&ctx->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_flags, 0, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {
     delete ctx;

@@ -327,6 +327,24 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// The Dirichlet factor of gram_term_f alone (the caller supplies the carrier e^{j2pi dd f_c/c}).
+__device__ __forceinline__ float gram_dirichlet_f(const SceneDev& sc, float dd, const GramPairF& gp) {
+  const float df_c = sc.df_cf, Nf = sc.nf_f, c6N = sc.c6N_f;
+  const float x = fmaf(dd, df_c, gp.xbr);
+  const float n2 = rintf(x);
+  const float xr = x - n2;
+  float t = Nf * xr;
+  t = fmaf(-2.f, rintf(0.5f * t), t);
+  const float num = __sinf(3.14159265358979f * t);
+  const float u = 3.14159265358979f * xr, u2 = u * u;
+  const float den = u * fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, -1.f / 39916800, 1.f / 362880), -1.f / 5040),
+                                                1.f / 120), -1.f / 6), 1.f);
+  float D = num * rcp_approx(den);
+  const float Ds = Nf * fmaf(-c6N, xr * xr, 1.f);
+  D = (fabsf(xr) < 1e-6f) ? Ds : D;
+  const uint32_t par = ((uint32_t)__float_as_int(n2 + 12582912.f) << 31) ^ gp.nbpar;
+  return __int_as_float(__float_as_int(D) ^ (int)(par & sc.evenN_mask));
+}
 __device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const GramPairF& gp, float& gr,
                                             float& gi) {
   const float fc_c = sc.fc_cf, df_c = sc.df_cf, Nf = sc.nf_f, c6N = sc.c6N_f;

@@ -189,6 +189,131 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   if (fl) atomicOr(&pflag[p], fl);
 }
 
+// Off-diagonal Gram (row A4) next to K1T: one thread per (particle, PA), antennas in the outer loop; per antenna the
+// S fp32 offsets Delta_s (as K1T / K1) and phasors E_s = e^{j2pi f_c Delta_s/c} once, then all S(S-1)/2 pair terms:
+// carrier E_a conj(E_b) and K1's closed-form Dirichlet factor (gram_dirichlet_f) (fp32 over
+// blocks of 8 antennas, fp64 totals per thread in shared memory: no barriers).  The pair's delay base
+// x_ab = (R_a - R_b) df/c comes from per-component fp64 fractions split hi + lo in fp32 (K1 rounds the fp64
+// difference once; the hi + lo difference is as accurate).  At the end the shared base carrier
+// e^{j2pi (R_a - R_b) f_c/c} and the gains in fp64 (K1's hand-off convention, lower-triangle entry G_ba).
+__device__ __forceinline__ bool tay_component(const SceneDev& sc, int j, const double* pos, const double* sfv_s,
+                                              float& hx, float& hy, float& hz, double& R64) {
+  double va[3], sh[3];
+  if (!anchor_va(sc, j, sfv_s, va, sh)) return false;
+  const double r0 = pos[0] - va[0], r1 = pos[1] - va[1], r2 = pos[2] - va[2];
+  const double rs2 = 2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]);
+  hx = (float)(r0 - rs2 * sh[0]); hy = (float)(r1 - rs2 * sh[1]); hz = (float)(r2 - rs2 * sh[2]);
+  R64 = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+  return R64 > 0.0;
+}
+template <int S>
+__global__ void __launch_bounds__(TAY_BLOCK)
+    tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
+                    const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
+                    int sfv_pp, double2* __restrict__ terms) {
+  constexpr int NP = S * (S - 1) / 2;
+  extern __shared__ double2 gsum[];  // [NP][TAY_BLOCK]
+  const int64_t p = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
+  const int j = blockIdx.y;
+  if (p >= P) return;
+  const int J = sc.J, Na = sc.Na, T = S + S * (S + 1) / 2;
+  const double* pos = particles + p * pstride;
+  float hx[S], hy[S], hz[S], Rf[S], iR[S], uh[S], ul[S];
+  double R64[S];
+  int npar[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const double* sfv_s = s == 0 ? nullptr : (sfv_pp ? sfv + (p * sc.K + (s - 1)) * 3 : sfv + (int64_t)(s - 1) * 3);
+    if (!tay_component(sc, j, pos, sfv_s, hx[s], hy[s], hz[s], R64[s])) return;  // flagged by K1T
+    Rf[s] = (float)R64[s];
+    iR[s] = 1.f / Rf[s];
+    const double xs = R64[s] * sc.df_c, ns = rint(xs), us = xs - ns;
+    uh[s] = (float)us;
+    ul[s] = (float)(us - (double)uh[s]);
+    npar[s] = (int)((long long)ns & 1);
+  }
+#pragma unroll
+  for (int q = 0; q < NP; ++q) gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(0.0, 0.0);
+  const bool sph = sc.wavefront == CDMS_SPHERICAL;
+  const float4* tm = tmpl + (int64_t)j * sc.n_mb * NWARP;
+  for (int m0 = 0; m0 < Na; m0 += 8) {
+    float gr[NP], gi[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) gr[q] = gi[q] = 0.f;
+    const int m1 = min(m0 + 8, Na);
+    for (int m = m0; m < m1; ++m) {
+      const float4 v = __ldg(&tm[m]);
+      float dl[S], er[S], ei[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const float rq = hx[s] * v.x + hy[s] * v.y + hz[s] * v.z;
+        if (sph) {
+          const float n = v.w - 2.f * rq;
+          dl[s] = n / (sqrtf(Rf[s] * Rf[s] + n) + Rf[s]);
+        } else {
+          dl[s] = -rq * iR[s];
+        }
+        cis2pi_fast<float>(dl[s] * sc.fc_cf, er[s], ei[s]);  // e^{j2pi f_c Delta_s/c}: the pairs' carriers as products
+      }
+      int q = 0;
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+#pragma unroll
+        for (int b = a + 1; b < S; ++b, ++q) {
+          GramPairF gp;
+          gp.xbr = (uh[a] - uh[b]) + (ul[a] - ul[b]);
+          gp.nbpar = (uint32_t)((npar[a] ^ npar[b]) & 1) << 31;
+          const float D = gram_dirichlet_f(sc, dl[a] - dl[b], gp);
+          const float cr = fmaf(er[a], er[b], ei[a] * ei[b]), ci = fmaf(ei[a], er[b], -er[a] * ei[b]);  // E_a conj(E_b)
+          gr[q] = fmaf(D, cr, gr[q]);
+          gi[q] = fmaf(D, ci, gi[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      double2 t = gsum[q * TAY_BLOCK + threadIdx.x];
+      gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(t.x + (double)gr[q], t.y + (double)gi[q]);
+    }
+  }
+  int q = 0;
+#pragma unroll
+  for (int a = 0; a < S; ++a) {
+#pragma unroll
+    for (int b = a + 1; b < S; ++b, ++q) {
+      const double2 acc = gsum[q * TAY_BLOCK + threadIdx.x];
+      double sn, cs;
+      sincospi(2.0 * frac_c((R64[a] - R64[b]) * sc.fc_c), &sn, &cs);
+      const double vr = cs * acc.x - sn * acc.y, vi = cs * acc.y + sn * acc.x;
+      const double g2 = sc.pathloss ? (sc.lambda / (4.0 * PI * R64[a])) * (sc.lambda / (4.0 * PI * R64[b])) : 1.0;
+      terms[(p * J + j) * T + S + b * (b + 1) / 2 + a] = make_double2(vr * g2, -vi * g2);
+    }
+  }
+}
+template <int S>
+static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
+                                     int pstride, const double* sfv, int sfv_pp, double2* terms, cudaStream_t st) {
+  constexpr int NP = S * (S - 1) / 2;
+  const size_t smem = (size_t)NP * TAY_BLOCK * sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
+  tay_gram_kernel<S><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms);
+  return cudaGetLastError();
+}
+cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
+                            const double* sfv, int sfv_pp, double2* terms, cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  switch (sc.S) {
+    case 1: return cudaSuccess;
+#define CASE_S(n) \
+  case n: return launch_tay_gram_t<n>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, st);
+    CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
+#undef CASE_S
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, cudaStream_t st) {
   const int G = tay_centres(sc.nf);
   const int64_t n = (int64_t)sc.J * sc.Na * G * TAY_KS;

@@ -50,6 +50,13 @@ def measured_tensor_peak():
         return 2250.0 * 0.72, "fallback: nominal 2.25 PFLOP/s x 0.72"
 
 
+def k1t_kernels(cfg, P: int) -> str:
+    """The K1T stage's kernels as libcdms picks them (taylor.cu tay_lanes, cdms.cpp engine selection)."""
+    c = ("cdms::tay_corr_lanes_kernel" if P * cfg.J < 2 * 148 * 1280 else "cdms::tay_corr_kernel") + " (K1T, c)"
+    g = "tay_gram_kernel<S> (G)" if cfg.K + 1 <= 5 else "corr_kernel<S, float, 0, 1> Horner-free K1 (G)"
+    return c + " + " + g
+
+
 def taylor_path(args) -> bool:
     """Spherical / planar WB in fp32 evaluate the correlation with K1T (taylor.cu) unless CDMS_TAYLOR=0."""
     return (args.wavefront != "planar_nb" and args.precision == "fp32"
@@ -313,14 +320,14 @@ def run_cdms(args):
             roof = {"bound": "alu", "pipe": "fp32 (direct-correlation flop equivalent)", "achieved": round(achieved, 3),
                     "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                     "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
-                    "kernel": "cdms::tay_corr_kernel (K1T, c) + corr_kernel<S, float, 0, 1> (Horner-free K1, G)",
+                    "kernel": k1t_kernels(cfg, P_local),
                     "kernel_ms": round(kernel_ms, 4),
                     "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
                     "launches_per_step": launches_per_step, "flop_per_launch": flop_launch,
                     "note": "frac > 1: K1T evaluates c from spectral Taylor tables (DESIGN.md 'K1T'); the flop count "
                             "is the direct correlation's 8 N_z per (particle, PA, component)",
                     "traffic": (traffic_from_profiles(args.config + "_k1t") if args.particles is None else None),
-                    "traffic_basis": "dram read+write bytes of one tay_corr_kernel launch, ncu --set full "
+                    "traffic_basis": "dram read+write bytes of one K1T correlation launch, ncu --set full "
                                      "(profiles/loglik_traffic.json)"}
         else:
             roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
@@ -561,7 +568,9 @@ def run_birth(args):
                     else "fp32 fma", "achieved": round(ach, 3), "peak": round(peak, 2),
                     "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                     "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
-                    "kernel": ("cdms::tay_corr_kernel (K1T, F3 correlations of the candidate walls)" if taylor_path(args)
+                    "kernel": (("cdms::tay_corr_lanes_kernel" if (N_g // 8) * cfg.J < 2 * 148 * 1280
+                                else "cdms::tay_corr_kernel") + " (K1T, F3 correlations of the candidate walls, 8 "
+                               "candidates per pseudo-particle)" if taylor_path(args)
                                else "cdms::corr_kernel (F3 correlations of the candidate walls)")}
             if taylor_path(args):
                 roof["note"] = ("frac > 1: K1T evaluates the correlations from spectral Taylor tables; the flop count "

@@ -412,9 +412,10 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   const bool tay = !nbt && ctx->taylor && precision == CDMS_FP32 && sd.wavefront != CDMS_PLANAR_NB &&
                    tay_table_bytes(sd) <= ((size_t)96 << 20);
   float2* taytab = nullptr;
+  const int tlanes = tay && tay_lanes(sd, P) ? 1 : 0;  // table layout + correlation kernel (taylor.cu)
   if (tay) {
     WS_TRY(ctx, WS_TAY, tay_table_bytes(sd) / sizeof(float2), &taytab);
-    CUDA_TRY(ctx, launch_tay_prep(sd, static_cast<const float2*>(d_y), taytab, ctx->stream));
+    CUDA_TRY(ctx, launch_tay_prep(sd, static_cast<const float2*>(d_y), taytab, tlanes, ctx->stream));
     ctx->launches += 1;
   }
   if (nbt) {
@@ -489,7 +490,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       const bool k1g = !no_gram && (ctx->taylor_gram == 1 || (ctx->taylor_gram == 0 && sd.S >= 6));
       if (k1g) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));
       CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, pflag,
-                                    no_gram ? 1 : 0, ctx->stream));
+                                    no_gram ? 1 : 0, tlanes, ctx->stream));
       if (!no_gram && !k1g)
         CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, ctx->stream));
       ctx->launches += no_gram ? 0 : 1;

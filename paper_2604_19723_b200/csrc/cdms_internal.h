@@ -192,12 +192,13 @@ int64_t corr_grid_gram_only(const SceneDev& sc, int64_t n_tiles, int num_sms);  
 cudaError_t launch_corr_gram_only(const SceneDev& sc, const CorrArgs& a, cudaStream_t st);
 int tay_centres(int nf);
 size_t tay_table_bytes(const SceneDev& sc);
-cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, cudaStream_t st);
+bool tay_lanes(const SceneDev& sc, int64_t P);  // table layout / correlation kernel choice for P particles
+cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, cudaStream_t st);
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
                             const double* sfv, int sfv_pp, double2* terms, cudaStream_t st);
 cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,
                             int64_t P, int pstride, const double* sfv, int sfv_pp, double2* terms, int* pflag,
-                            int gram_diag, cudaStream_t st);
+                            int gram_diag, int lanes, cudaStream_t st);
 
 // nbmma.cu: PLANAR_NB correlation on the tensor cores
 struct NbPlan {

@@ -34,7 +34,7 @@ size_t tay_table_bytes(const SceneDev& sc) { return (size_t)sc.J * sc.Na * tay_c
 // fixed shuffle tree: row count alone (J N_a G) would leave most SMs idle at small N_a G.
 constexpr int TAY_KS = 8;
 __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ y,
-                                float2* __restrict__ tab) {
+                                float2* __restrict__ tab, int lanes) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t t = tid / TAY_KS;
   const int seg = (int)(tid - t * TAY_KS);
@@ -85,13 +85,61 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
     }
   }
   if (live && seg == 0) {
-    float2* out = tab + t * TAY_L;
+    if (lanes) {  // [j][g][q][m]
+      float4* out = reinterpret_cast<float4*>(tab) + ((int64_t)j * G + g) * (TAY_L / 2) * sc.Na + m;
 #pragma unroll
-    for (int l = 0; l < TAY_L; ++l) out[l] = make_float2((float)cr[l], (float)ci[l]);
+      for (int q = 0; q < TAY_L / 2; ++q)
+        out[(int64_t)q * sc.Na] =
+            make_float4((float)cr[2 * q], (float)ci[2 * q], (float)cr[2 * q + 1], (float)ci[2 * q + 1]);
+    } else {  // [j][m][g][l]
+      float2* out = tab + t * TAY_L;
+#pragma unroll
+      for (int l = 0; l < TAY_L; ++l) out[l] = make_float2((float)cr[l], (float)ci[l]);
+    }
   }
 }
 
-// c_s for one particle per thread and one PA per blockIdx.y: per component the fp64 geometry (VA, H r, R), the
+// Delay phase base of one (particle, component), phib = R df/c cycles, reduced once in fp64 to n0 + hi + lo
+// (|hi| <= 1/2, lo the fp32 remainder, par = n0 mod 2); per antenna tay_locate then needs fp32 only.
+struct TayBase {
+  float hi, lo;
+  int par;
+};
+__device__ __forceinline__ TayBase tay_base(double phib) {
+  const double n0 = rint(phib), r0 = phib - n0;
+  TayBase b;
+  b.hi = (float)r0;
+  b.lo = (float)(r0 - (double)b.hi);
+  b.par = (int)((long long)n0 & 1);
+  return b;
+}
+constexpr float TAY_MAGIC = 12582912.f;  // 1.5 * 2^23: (x + M) - M = rint(x) for |x| < 2^22, int bits of x + M - bits(M) = rint(x)
+// phi = phib + t (t = Delta_m df/c) = n + r, |r| <= 1/2 (TwoSum keeps hi + t exact as s + e); centre g = rint(r G)
+// wrapped into [0, G), delta' = r G - g (one fma, then the e + lo correction).  Y(phi + 1) = (-1)^(N_f - 1) Y(phi)
+// (k - k0 is a half-integer for even N_f), so the table value at the wrapped centre is multiplied by
+// (-1)^((n0 + n - w)(N_f - 1)), w = 1 when the centre was moved up by one period.  No conversions or MUFU: the fp64
+// version of this reduction (F2F, F2I, DFRND per antenna) held the XU pipe.
+__device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par, int G, float Gf, bool evenN, int& g,
+                                           float& dp, bool& flip) {
+  const float s = hi + t;
+  const float bb = s - hi;
+  const float e = (hi - (s - bb)) + (t - bb);
+  const float sm = s + TAY_MAGIC;
+  const float r = s - (sm - TAY_MAGIC);     // exact
+  const float gm = fmaf(r, Gf, TAY_MAGIC);  // rint(r G) + M
+  const float gi = gm - TAY_MAGIC;
+  dp = fmaf(r, Gf, -gi) + (e + lo) * Gf;
+  int gg = __float_as_int(gm) - __float_as_int(TAY_MAGIC);
+  const int nn = __float_as_int(sm) - __float_as_int(TAY_MAGIC);
+  int w = 0;
+  if (gg < 0) { gg += G; w = 1; }
+  if (gg >= G) { gg -= G; w = -1; }
+  g = gg;
+  flip = evenN && ((par + nn - w) & 1);
+}
+
+// c_s for one particle per thread and one PA per blockIdx.y ([j][m][g][l] table; used when P J fills the SMs,
+// else tay_corr_lanes_kernel below): per component the fp64 geometry (VA, H r, R), the
 // fp64-reduced phase bases e^{j2pi f_c R/c} and frac(df R/c); per antenna the fp32 offset Delta_m (cancellation-free,
 // as K1), the phasor e^{j2pi f_c Delta_m/c}, the table centre and delta', one table row and the Taylor sum.
 __global__ void __launch_bounds__(TAY_BLOCK)
@@ -99,10 +147,10 @@ __global__ void __launch_bounds__(TAY_BLOCK)
                     const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P, int pstride,
                     const double* __restrict__ sfv, int sfv_pp, double2* __restrict__ terms, int* __restrict__ pflag,
                     int gram_diag) {
+  const int J = sc.J, S = sc.S, Na = sc.Na, T = S + S * (S + 1) / 2;
   const int64_t p = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
   const int j = blockIdx.y;
   if (p >= P) return;
-  const int J = sc.J, S = sc.S, Na = sc.Na, T = S + S * (S + 1) / 2;
   const int Na_pad = sc.n_mb * NWARP;
   const double* pos = particles + p * pstride;
   const float2* tj = tab + (int64_t)j * Na * G * TAY_L;
@@ -126,7 +174,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       continue;
     }
     const float R = (float)R64;
-    const double phib = R64 * sc.df_c;  // delay phase base (cycles), fp64, not reduced (see the parity below)
+    const TayBase tb = tay_base(R64 * sc.df_c);  // delay phase base
     double sb, cb;
     sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
     const float Ebr = (float)cb, Ebi = (float)sb;  // e^{j2pi f_c R/c}
@@ -140,28 +188,19 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         float delta;
         if (sph) {
           const float n = v.w - 2.f * rq;
-          const float d = sqrtf(R * R + n);
+          const float d = Num<float>::fsqrt_(R * R + n);  // approximate: no IEEE slow-path call in the loop
           if (!(d > 0.f)) fl |= 1;
-          delta = n / (d + R);
+          delta = Num<float>::fdiv_(n, d + R);
         } else {
-          delta = -rq / R;
+          delta = Num<float>::fdiv_(-rq, R);
         }
         float er, ei;
         cis2pi_fast<float>(delta * sc.fc_cf, er, ei);
         const float Er = Ebr * er - Ebi * ei, Ei = Ebr * ei + Ebi * er;  // e^{j2pi f_c d_m/c}
-        // phi = n + phi_r, |phi_r| <= 1/2; centre g = rint(phi_r G) wrapped into [0, G).  Y(phi + 1) =
-        // (-1)^(N_f - 1) Y(phi) (k - k0 is a half-integer for even N_f), so the table value at the wrapped centre
-        // is multiplied by (-1)^((n - w)(N_f - 1)), w = 1 when the centre was moved up by one period.
-        const double xx = phib + (double)(delta * sc.df_cf);
-        const double nper = rint(xx);
-        const double x = (xx - nper) * (double)G;
-        const double gi = rint(x);
-        const float dp = (float)(x - gi);
-        int g = (int)gi;
-        int wper = 0;
-        if (g < 0) { g += G; wper = 1; }
-        if (g >= G) { g -= G; wper = -1; }
-        const bool flip = (sc.nf & 1) == 0 && (((long long)nper - wper) & 1);
+        int g;
+        float dp;
+        bool flip;
+        tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G, (float)G, (sc.nf & 1) == 0, g, dp, flip);
         const float4* row = reinterpret_cast<const float4*>(tj + ((int64_t)m * G + g) * TAY_L);
         const float4 c01 = __ldg(row), c23 = __ldg(row + 1), c45 = __ldg(row + 2), c67 = __ldg(row + 3);
         float yr = c67.z, yi = c67.w;  // Horner in delta', l = 7 .. 0
@@ -189,6 +228,130 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   if (fl) atomicOr(&pflag[p], fl);
 }
 
+// c_s with antennas across groups of LP = 2^lg lanes: for one component the phases of all antennas lie within a few
+// table centres, so with the [g][q][m] layout a group's gathers are (nearly) contiguous.  A warp owns npw = floor(32/S)
+// particles; lane i < npw S runs the fp64 set-up of pair i = (particle i / S, component i % S); the 32/LP groups then
+// take pairs i0 + group, each lane a strided subset of the antennas, and a fixed-order tree inside the group sums them.
+__global__ void __launch_bounds__(TAY_BLOCK)
+    tay_corr_lanes_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
+                          const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P,
+                          int pstride, const double* __restrict__ sfv, int sfv_pp, double2* __restrict__ terms,
+                          int* __restrict__ pflag, int gram_diag, int lg) {
+  const int lane = threadIdx.x & 31;
+  const int J = sc.J, S = sc.S, Na = sc.Na, T = S + S * (S + 1) / 2;
+  const int npw = 32 / S, LP = 1 << lg, ng = 32 >> lg;
+  const int grp = lane >> lg, gl = lane & (LP - 1);
+  const int64_t p0 = ((int64_t)blockIdx.x * (TAY_BLOCK / 32) + (threadIdx.x >> 5)) * npw;
+  const int j = blockIdx.y;
+  if (p0 >= P) return;  // warp-uniform
+  const int npairs = (int)min((int64_t)npw, P - p0) * S;
+  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * G * (TAY_L / 2) * Na;
+  const float4* tm = tmpl + (int64_t)j * sc.n_mb * NWARP;
+  const bool sph = sc.wavefront == CDMS_SPHERICAL;
+  float hx = 1.f, hy = 0.f, hz = 0.f, R = 1.f, Ebr = 1.f, Ebi = 0.f;
+  float bhi = 0.f, blo = 0.f;
+  int bpar = 0;
+  double gn = 1.0;
+  int ok = 0;
+  if (lane < npairs) {
+    const int64_t p = p0 + lane / S;
+    const int s = lane % S;
+    const double* pos = particles + p * pstride;
+    const double* sfv_s = s == 0 ? nullptr : (sfv_pp ? sfv + (p * sc.K + (s - 1)) * 3 : sfv + (int64_t)(s - 1) * 3);
+    double va[3], sh[3];
+    int fl = 0;
+    if (!anchor_va(sc, j, sfv_s, va, sh)) {
+      fl = 2;
+    } else {
+      const double r0 = pos[0] - va[0], r1 = pos[1] - va[1], r2 = pos[2] - va[2];
+      const double rs2 = 2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]);
+      const double R64 = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+      if (!(R64 > 0.0)) {
+        fl = 1;
+      } else {
+        hx = (float)(r0 - rs2 * sh[0]); hy = (float)(r1 - rs2 * sh[1]); hz = (float)(r2 - rs2 * sh[2]);
+        R = (float)R64;
+        const TayBase tb = tay_base(R64 * sc.df_c);
+        bhi = tb.hi; blo = tb.lo; bpar = tb.par;
+        double sb, cb;
+        sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
+        Ebr = (float)cb; Ebi = (float)sb;
+        gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
+        ok = 1;
+      }
+    }
+    if (fl) atomicOr(&pflag[p], fl);
+  }
+  float cr = 0.f, ci = 0.f;  // lane i: pair i's correlation once reduced
+  for (int i0 = 0; i0 < npairs; i0 += ng) {
+    const int i = i0 + grp;  // this group's pair
+    const int src = min(i, 31);
+    const int pok = __shfl_sync(0xffffffffu, ok, src) && i < npairs;
+    const float shx = __shfl_sync(0xffffffffu, hx, src), shy = __shfl_sync(0xffffffffu, hy, src);
+    const float shz = __shfl_sync(0xffffffffu, hz, src), sR = __shfl_sync(0xffffffffu, R, src);
+    const float sEr = __shfl_sync(0xffffffffu, Ebr, src), sEi = __shfl_sync(0xffffffffu, Ebi, src);
+    const float shi = __shfl_sync(0xffffffffu, bhi, src), slo = __shfl_sync(0xffffffffu, blo, src);
+    const int spar = __shfl_sync(0xffffffffu, bpar, src);
+    float pr = 0.f, pi = 0.f;
+    int efl = 0;
+    for (int m = pok ? gl : Na; m < Na; m += LP) {
+      const float4 v = __ldg(&tm[m]);
+      const float rq = shx * v.x + shy * v.y + shz * v.z;
+      float delta;
+      if (sph) {
+        const float n = v.w - 2.f * rq;
+        const float d = Num<float>::fsqrt_(sR * sR + n);
+        if (!(d > 0.f)) efl = 1;
+        delta = Num<float>::fdiv_(n, d + sR);
+      } else {
+        delta = Num<float>::fdiv_(-rq, sR);
+      }
+      float er, ei;
+      cis2pi_fast<float>(delta * sc.fc_cf, er, ei);
+      const float Er = sEr * er - sEi * ei, Ei = sEr * ei + sEi * er;
+      int g;
+      float dp;
+      bool flip;
+      tay_locate(delta * sc.df_cf, shi, slo, spar, G, (float)G, (sc.nf & 1) == 0, g, dp, flip);
+      const float4* row = tj + (int64_t)g * (TAY_L / 2) * Na + m;
+      const float4 c01 = __ldg(row), c23 = __ldg(row + Na), c45 = __ldg(row + 2 * Na), c67 = __ldg(row + 3 * Na);
+      float yr = c67.z, yi = c67.w;
+      yr = fmaf(yr, dp, c67.x); yi = fmaf(yi, dp, c67.y);
+      yr = fmaf(yr, dp, c45.z); yi = fmaf(yi, dp, c45.w);
+      yr = fmaf(yr, dp, c45.x); yi = fmaf(yi, dp, c45.y);
+      yr = fmaf(yr, dp, c23.z); yi = fmaf(yi, dp, c23.w);
+      yr = fmaf(yr, dp, c23.x); yi = fmaf(yi, dp, c23.y);
+      yr = fmaf(yr, dp, c01.z); yi = fmaf(yi, dp, c01.w);
+      yr = fmaf(yr, dp, c01.x); yi = fmaf(yi, dp, c01.y);
+      if (flip) { yr = -yr; yi = -yi; }
+      pr = fmaf(Er, yr, fmaf(-Ei, yi, pr));
+      pi = fmaf(Er, yi, fmaf(Ei, yr, pi));
+    }
+    for (int o = LP >> 1; o > 0; o >>= 1) {  // fixed-order tree inside the group
+      pr += __shfl_xor_sync(0xffffffffu, pr, o);
+      pi += __shfl_xor_sync(0xffffffffu, pi, o);
+    }
+    // pair i0 + k's sum sits in group k: lane i0 + k, which holds that pair's set-up, takes it
+    const int from = min(max(lane - i0, 0), ng - 1) << lg;
+    const float tr = __shfl_sync(0xffffffffu, pr, from), ti = __shfl_sync(0xffffffffu, pi, from);
+    if (lane >= i0 && lane < i0 + ng) {
+      cr = tr;
+      ci = ti;
+    }
+    if (efl) atomicOr(&pflag[p0 + i / S], efl);
+  }
+  if (lane < npairs && ok) {  // one store round per warp: lane i writes pair i's c_s, G_ss (and zero off-diagonals)
+    const int64_t p = p0 + lane / S;
+    const int s = lane % S;
+    double2* tp = terms + (p * J + j) * T;
+    tp[s] = make_double2((double)cr * gn, (double)ci * gn);
+    double2* gr = tp + S + s * (s + 1) / 2;
+    gr[s] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);
+    if (gram_diag)
+      for (int c = 0; c < s; ++c) gr[c] = make_double2(0.0, 0.0);
+  }
+}
+
 // Off-diagonal Gram (row A4) next to K1T: one thread per (particle, PA), antennas in the outer loop; per antenna the
 // S fp32 offsets Delta_s (as K1T / K1) and phasors E_s = e^{j2pi f_c Delta_s/c} once, then all S(S-1)/2 pair terms:
 // carrier E_a conj(E_b) and K1's closed-form Dirichlet factor (gram_dirichlet_f) (fp32 over
@@ -210,21 +373,27 @@ template <int S>
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
                     const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
-                    int sfv_pp, double2* __restrict__ terms) {
+                    int sfv_pp, double2* __restrict__ terms, int lsplit) {
   constexpr int NP = S * (S - 1) / 2;
   extern __shared__ double2 gsum[];  // [NP][TAY_BLOCK]
-  const int64_t p = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
+  // A = 2^lsplit adjacent lanes per particle, lane a takes antennas a, a + A, ... (A > 1 when P J threads alone would
+  // leave the SMs latency-bound); no early exit: the group's fp64 totals are combined by shuffles below
+  const int A = 1 << lsplit;
+  const int64_t t = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
+  const int64_t p = t >> lsplit;
+  const int a0 = (int)(t & (A - 1));
   const int j = blockIdx.y;
-  if (p >= P) return;
   const int J = sc.J, Na = sc.Na, T = S + S * (S + 1) / 2;
-  const double* pos = particles + p * pstride;
+  bool live = p < P;
+  const double* pos = particles + (live ? p : 0) * pstride;
   float hx[S], hy[S], hz[S], Rf[S], iR[S], uh[S], ul[S];
   double R64[S];
   int npar[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) {
-    const double* sfv_s = s == 0 ? nullptr : (sfv_pp ? sfv + (p * sc.K + (s - 1)) * 3 : sfv + (int64_t)(s - 1) * 3);
-    if (!tay_component(sc, j, pos, sfv_s, hx[s], hy[s], hz[s], R64[s])) return;  // flagged by K1T
+    const double* sfv_s = s == 0 ? nullptr : (sfv_pp ? sfv + ((live ? p : 0) * sc.K + (s - 1)) * 3 : sfv + (int64_t)(s - 1) * 3);
+    if (!tay_component(sc, j, pos, sfv_s, hx[s], hy[s], hz[s], R64[s])) live = false;  // flagged by K1T
+    if (!live) R64[s] = 1.0;
     Rf[s] = (float)R64[s];
     iR[s] = 1.f / Rf[s];
     const double xs = R64[s] * sc.df_c, ns = rint(xs), us = xs - ns;
@@ -236,12 +405,14 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   for (int q = 0; q < NP; ++q) gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(0.0, 0.0);
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
   const float4* tm = tmpl + (int64_t)j * sc.n_mb * NWARP;
-  for (int m0 = 0; m0 < Na; m0 += 8) {
+  const int Nl = live ? (Na - a0 + A - 1) >> lsplit : 0;  // this lane's antennas m = a0 + A i, i < Nl
+  for (int i0 = 0; i0 < Nl; i0 += 8) {
     float gr[NP], gi[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) gr[q] = gi[q] = 0.f;
-    const int m1 = min(m0 + 8, Na);
-    for (int m = m0; m < m1; ++m) {
+    const int i1 = min(i0 + 8, Nl);
+    for (int i = i0; i < i1; ++i) {
+      const int m = a0 + (i << lsplit);
       const float4 v = __ldg(&tm[m]);
       float dl[S], er[S], ei[S];
 #pragma unroll
@@ -249,17 +420,18 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         const float rq = hx[s] * v.x + hy[s] * v.y + hz[s] * v.z;
         if (sph) {
           const float n = v.w - 2.f * rq;
-          dl[s] = n / (sqrtf(Rf[s] * Rf[s] + n) + Rf[s]);
+          dl[s] = Num<float>::fdiv_(n, Num<float>::fsqrt_(Rf[s] * Rf[s] + n) + Rf[s]);
         } else {
           dl[s] = -rq * iR[s];
         }
         cis2pi_fast<float>(dl[s] * sc.fc_cf, er[s], ei[s]);  // e^{j2pi f_c Delta_s/c}: the pairs' carriers as products
       }
-      int q = 0;
 #pragma unroll
-      for (int a = 0; a < S; ++a) {
+      for (int a = 0; a < S; ++a) {  // constant trip counts: both loops unroll fully, the arrays stay in registers
 #pragma unroll
-        for (int b = a + 1; b < S; ++b, ++q) {
+        for (int b = 0; b < S; ++b) {
+          if (b <= a) continue;
+          const int q = a * (2 * S - a - 1) / 2 + (b - a - 1);
           GramPairF gp;
           gp.xbr = (uh[a] - uh[b]) + (ul[a] - ul[b]);
           gp.nbpar = (uint32_t)((npar[a] ^ npar[b]) & 1) << 31;
@@ -276,12 +448,18 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(t.x + (double)gr[q], t.y + (double)gi[q]);
     }
   }
-  int q = 0;
 #pragma unroll
   for (int a = 0; a < S; ++a) {
 #pragma unroll
-    for (int b = a + 1; b < S; ++b, ++q) {
-      const double2 acc = gsum[q * TAY_BLOCK + threadIdx.x];
+    for (int b = 0; b < S; ++b) {
+      if (b <= a) continue;
+      const int q = a * (2 * S - a - 1) / 2 + (b - a - 1);
+      double2 acc = gsum[q * TAY_BLOCK + threadIdx.x];
+      for (int o = 1; o < A; o <<= 1) {  // fixed-order tree over the group's lanes
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (!live || a0 != 0) continue;
       double sn, cs;
       sincospi(2.0 * frac_c((R64[a] - R64[b]) * sc.fc_c), &sn, &cs);
       const double vr = cs * acc.x - sn * acc.y, vi = cs * acc.y + sn * acc.x;
@@ -297,8 +475,10 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
   const size_t smem = (size_t)NP * TAY_BLOCK * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
-  tay_gram_kernel<S><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms);
+  // antennas over 4 lanes per particle when P J threads are fewer than ~2 resident waves
+  const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 2 : 0;
+  dim3 grid((unsigned)(((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
+  tay_gram_kernel<S><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit);
   return cudaGetLastError();
 }
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
@@ -314,16 +494,30 @@ cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double
   }
 }
 
-cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, cudaStream_t st) {
+// Layout / kernel choice (measured, profiles/r01_k1t_lanes.txt): with P J below ~2 resident waves of the thread-per-
+// particle kernel (148 SMs x ~1280 threads) it is latency-bound on its uncoalesced row gathers and the lane-group
+// kernel with the [g][q][m] table wins (c2: 0.531 vs 0.583 ms/step); at P J = 1e6 the thread kernel wins (c4: 11.4
+// vs 12.3 ms).  Decided once per loglik call (from its particle count) for the table build and every batch.
+bool tay_lanes(const SceneDev& sc, int64_t P) { return (double)P * sc.J < 2.0 * 148 * 1280; }
+cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, cudaStream_t st) {
   const int G = tay_centres(sc.nf);
   const int64_t n = (int64_t)sc.J * sc.Na * G * TAY_KS;
-  tay_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, G, y, tab);
+  tay_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, G, y, tab, lanes);
   return cudaGetLastError();
 }
 cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,
                             int64_t P, int pstride, const double* sfv, int sfv_pp, double2* terms, int* pflag,
-                            int gram_diag, cudaStream_t st) {
+                            int gram_diag, int lanes, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
+  if (lanes) {
+    int lg = 2;
+    while ((1 << lg) < 32 && (4 << lg) < sc.Na) ++lg;  // ~4 antennas per lane
+    const int64_t per_block = (int64_t)(TAY_BLOCK / 32) * (32 / sc.S);
+    dim3 grid((unsigned)((P + per_block - 1) / per_block), sc.J);
+    tay_corr_lanes_kernel<<<grid, TAY_BLOCK, 0, st>>>(sc, tay_centres(sc.nf), tab, tmpl, particles, P, pstride, sfv,
+                                                      sfv_pp, terms, pflag, gram_diag, lg);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
   tay_corr_kernel<<<grid, TAY_BLOCK, 0, st>>>(sc, tay_centres(sc.nf), tab, tmpl, particles, P, pstride, sfv, sfv_pp,
                                               terms, pflag, gram_diag);

@@ -230,6 +230,21 @@ def test_loglik_near_truth_worst_case(cd, ctx, orc, name, wf):
     check_loglik(case, ctx, "fp32", idx=np.arange(8))
 
 
+@pytest.mark.parametrize("P", [4096, 400_000])
+def test_taylor_layouts_near_truth(cd, ctx, orc, P):
+    """K1T picks its table layout and correlation kernel from P J (taylor.cu tay_lanes: lane groups with the
+    [g][q][m] table below ~379k, one thread per particle with the [m][g][l] table above); both at the near-truth
+    worst case, plus a stratified sample."""
+    import dataclasses
+    cfg = dataclasses.replace(scenes.CONFIGS["c2"], P=P)  # c2's scene, P particles
+    rng = np.random.default_rng(23)
+    x = scenes.make_particles(cfg)
+    x[:32, :3] = scenes.P_TRUE[None] + rng.uniform(-1e-3, 1e-3, size=(32, 3))
+    case = Case(orc, cfg, wavefront="spherical", particles=x)
+    idx = np.unique(np.concatenate([np.arange(8), scenes.stratified_sample(P, 64)]))
+    check_loglik(case, ctx, "fp32", idx=idx)
+
+
 def test_loglik_c5_shard_sampled(cd, ctx, orc):
     """c5 (J=4, S=9, Nz=65536) on one rank's 8-GPU shard (2M particles), oracle on 96 particles."""
     cfg = scenes.CONFIGS["c5"]

@@ -58,7 +58,7 @@ template <typename RT>
 __device__ __forceinline__ void cis2pi_fast(RT x, RT& re, RT& im);
 template <>
 __device__ __forceinline__ void cis2pi_fast<float>(float x, float& re, float& im) {
-  x = x - rintf(x);
+  x = x - ((x + 12582912.f) - 12582912.f);  // rint (|x| < 2^22) on the FMA pipe, bit-identical to rintf
   __sincosf(6.28318530717958647692f * x, &im, &re);
 }
 template <>
@@ -330,11 +330,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // The Dirichlet factor of gram_term_f alone (the caller supplies the carrier e^{j2pi dd f_c/c}).
 __device__ __forceinline__ float gram_dirichlet_f(const SceneDev& sc, float dd, const GramPairF& gp) {
   const float df_c = sc.df_cf, Nf = sc.nf_f, c6N = sc.c6N_f;
+  // rint by the 1.5 * 2^23 magic constant (FADDs, |x| << 2^22) rather than FRND: the Gram kernels that call this
+  // per (pair, antenna) are XU-bound (profiles/r01_k1t_lanes.txt); the sum's low mantissa bit is n2's parity
+  constexpr float M = 12582912.f;
   const float x = fmaf(dd, df_c, gp.xbr);
-  const float n2 = rintf(x);
-  const float xr = x - n2;
+  const float xm = x + M;
+  const float xr = x - (xm - M);
   float t = Nf * xr;
-  t = fmaf(-2.f, rintf(0.5f * t), t);
+  t = fmaf(-2.f, (fmaf(0.5f, t, M) - M), t);
   const float num = __sinf(3.14159265358979f * t);
   const float u = 3.14159265358979f * xr, u2 = u * u;
   const float den = u * fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, -1.f / 39916800, 1.f / 362880), -1.f / 5040),
@@ -342,7 +345,7 @@ __device__ __forceinline__ float gram_dirichlet_f(const SceneDev& sc, float dd, 
   float D = num * rcp_approx(den);
   const float Ds = Nf * fmaf(-c6N, xr * xr, 1.f);
   D = (fabsf(xr) < 1e-6f) ? Ds : D;
-  const uint32_t par = ((uint32_t)__float_as_int(n2 + 12582912.f) << 31) ^ gp.nbpar;
+  const uint32_t par = ((uint32_t)__float_as_int(xm) << 31) ^ gp.nbpar;
   return __int_as_float(__float_as_int(D) ^ (int)(par & sc.evenN_mask));
 }
 __device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const GramPairF& gp, float& gr,

@@ -494,11 +494,12 @@ cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double
   }
 }
 
-// Layout / kernel choice (measured, profiles/r01_k1t_lanes.txt): with P J below ~2 resident waves of the thread-per-
-// particle kernel (148 SMs x ~1280 threads) it is latency-bound on its uncoalesced row gathers and the lane-group
-// kernel with the [g][q][m] table wins (c2: 0.531 vs 0.583 ms/step); at P J = 1e6 the thread kernel wins (c4: 11.4
-// vs 12.3 ms).  Decided once per loglik call (from its particle count) for the table build and every batch.
-bool tay_lanes(const SceneDev& sc, int64_t P) { return (double)P * sc.J < 2.0 * 148 * 1280; }
+// Layout / kernel choice (measured, profiles/r01_k1t_lanes.txt, CDMS_TAY_LANES=0/1 A/B): with P J below one
+// resident wave of the thread-per-particle kernel (148 SMs x ~1024 threads) it is latency-bound on its uncoalesced
+// row gathers and the lane-group kernel with the [g][q][m] table wins (c2, P = 1e5: 0.496 vs 0.58 ms/step); from
+// P J = 2e5 on the thread kernel wins (c2 at 2e5 / 4e5 / 8e5: 0.80 / 1.29 / 2.30 vs 0.82 / 1.41 / 2.61 ms; c4
+// 10.3 vs 11.3).  Decided once per loglik call (from its particle count) for the table build and every batch.
+bool tay_lanes(const SceneDev& sc, int64_t P) { return (double)P * sc.J < 148.0 * 1024; }
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, cudaStream_t st) {
   const int G = tay_centres(sc.nf);
   const int64_t n = (int64_t)sc.J * sc.Na * G * TAY_KS;

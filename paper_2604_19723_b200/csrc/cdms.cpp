@@ -34,6 +34,8 @@ struct cdms_ctx_s {
   bool taylor = true;            // spherical / planar-WB fp32 correlation by K1T (taylor.cu); CDMS_TAYLOR=0 selects K1
   int taylor_gram = 0;           // K1T's off-diagonal Gram: 0 by S, 1 K1's Horner-free variant, 2 tay_gram_kernel
                                  // (CDMS_TAYLOR_GRAM=k1 / tay, A/B only)
+  int taylor_prep_direct = 0;   // K1T tables by the direct sum even when G is a power of two (CDMS_TAY_PREP=direct,
+                                 // A/B only; default FFT)
   int taylor_lanes = -1;         // K1T correlation kernel: -1 by P J (tay_lanes), 1 lane groups, 0 thread per
                                  // particle (CDMS_TAY_LANES=1 / 0, A/B only)
   std::vector<cudaEvent_t> ev_pool;
@@ -417,7 +419,8 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   const int tlanes = tay && (ctx->taylor_lanes >= 0 ? ctx->taylor_lanes == 1 : tay_lanes(sd, P)) ? 1 : 0;  // taylor.cu
   if (tay) {
     WS_TRY(ctx, WS_TAY, tay_table_bytes(sd) / sizeof(float2), &taytab);
-    CUDA_TRY(ctx, launch_tay_prep(sd, static_cast<const float2*>(d_y), taytab, tlanes, ctx->stream));
+    CUDA_TRY(ctx, launch_tay_prep(sd, static_cast<const float2*>(d_y), taytab, tlanes, ctx->taylor_prep_direct,
+                                  ctx->stream));
     ctx->launches += 1;
   }
   if (nbt) {
@@ -536,6 +539,7 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("CDMS_NB_TENSOR")) ctx->nb_tensor = atoi(e) != 0;
   if (const char* e = getenv("CDMS_TAYLOR")) ctx->taylor = atoi(e) != 0;
+  if (const char* e = getenv("CDMS_TAY_PREP")) ctx->taylor_prep_direct = strcmp(e, "direct") == 0 ? 1 : 0;
   if (const char* e = getenv("CDMS_TAY_LANES")) ctx->taylor_lanes = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_TAYLOR_GRAM")) ctx->taylor_gram = strcmp(e, "k1") == 0 ? 1 : (strcmp(e, "tay") == 0 ? 2 : 0);
   if (cudaMalloc(&ctx->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_flags, 0, sizeof(int)) != cudaSuccess ||

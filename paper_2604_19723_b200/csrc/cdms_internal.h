@@ -193,7 +193,8 @@ cudaError_t launch_corr_gram_only(const SceneDev& sc, const CorrArgs& a, cudaStr
 int tay_centres(int nf);
 size_t tay_table_bytes(const SceneDev& sc);
 bool tay_lanes(const SceneDev& sc, int64_t P);  // table layout / correlation kernel choice for P particles
-cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, cudaStream_t st);
+cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, int direct,
+                            cudaStream_t st);
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
                             const double* sfv, int sfv_pp, double2* terms, cudaStream_t st);
 cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,

@@ -5,9 +5,9 @@
 //   c_s = sum_m e^{j2pi f_c d_m/c} Y_m(phi_m),   Y_m(phi) = sum_k y[m,k] e^{j2pi (k - k0) phi},  phi_m = df d_m / c,
 // (f_k = f_c + (k - k0) df, k0 = (N_f - 1)/2; d_m the spherical distance or the planar projection of the element,
 // P:L108-143).  Y_m is 1-periodic up to the sign (-1)^(N_f - 1) (k - k0 is a half-integer for even N_f) and
-// band-limited to |k - k0| <= N_f/2, so on G = 4 N_f centres phi_g = g/G its
-// Taylor expansion in delta' = (phi - phi_g) G, |delta'| <= 1/2,
-//   Y_m(phi_g + delta'/G) = sum_l C_l(m, g) delta'^l,  C_l = sum_k y[m,k] e^{j2pi (k-k0) g/G} (j2pi (k-k0)/G)^l / l!,
+// band-limited to |k - k0| <= N_f/2, so on the G + 1 centres phi_g = (g - G/2)/G, g = 0..G, G = 4 N_f, of one period
+// [-1/2, 1/2] (both ends stored: the reduction needs no wrap) its Taylor expansion in delta' = (phi - phi_g) G,
+//   Y_m(phi_g + delta'/G) = sum_l C_l(m, g) delta'^l,  C_l = sum_k y[m,k] e^{j2pi (k-k0) phi_g} (j2pi (k-k0)/G)^l / l!,
 // truncated after TAY_L = 8 terms has a relative error below (pi/8)^8/8! = 1.4e-8 of sum_k |y[m,k]| (|2pi (k-k0)
 // delta'/G| <= pi/8): far below fp32 rounding, so K1T evaluates the same correlation as the Horner recurrence of
 // K1 to fp32 accuracy with one 64-byte table row and 8 real-coefficient steps per (particle, component, antenna)
@@ -26,11 +26,22 @@ constexpr int TAY_L = 8;
 constexpr int TAY_BLOCK = 128;
 }  // namespace
 
-int tay_centres(int nf) { return 4 * nf; }
-size_t tay_table_bytes(const SceneDev& sc) { return (size_t)sc.J * sc.Na * tay_centres(sc.nf) * TAY_L * sizeof(float2); }
+// 32 bytes (4 complex64 coefficients) in one 256-bit load (LDG.E.ENL2.256, sm_100): the table gathers are
+// L1-wavefront / issue bound, and a 64-byte row then takes 2 loads instead of 4.  p must be 32-byte aligned.
+__device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
 
-// tab[j][m][g][l] (complex64, l fastest: one 64-byte row per (j, m, g)).  TAY_KS lanes per row split the subcarrier
-// sum (each from an exact anchor e^{j2pi (k - k0) g / G}, fp64 phasor recurrence inside its segment), combined by a
+int tay_centres(int nf) { return 4 * nf; }
+size_t tay_table_bytes(const SceneDev& sc) {
+  return (size_t)sc.J * sc.Na * (tay_centres(sc.nf) + 1) * TAY_L * sizeof(float2);
+}
+
+// tab[j][m][g][l] (complex64, l fastest: one 64-byte row per (j, m, g), g = 0..G) or, with lanes, [j][g][h][m] of
+// 32-byte entries (coefficients 4h .. 4h+3).  TAY_KS lanes per row split the subcarrier sum (each from an exact anchor
+// e^{j2pi (k - k0) phi_g}, fp64 phasor recurrence inside its segment), combined by a
 // fixed shuffle tree: row count alone (J N_a G) would leave most SMs idle at small N_a G.
 constexpr int TAY_KS = 8;
 __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ y,
@@ -38,12 +49,13 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t t = tid / TAY_KS;
   const int seg = (int)(tid - t * TAY_KS);
-  const int64_t per_j = (int64_t)sc.Na * G;
+  const int64_t per_j = (int64_t)sc.Na * (G + 1);
   const bool live = t < per_j * sc.J;
   const int64_t tt = live ? t : 0;
   const int j = (int)(tt / per_j);
   const int64_t r = tt - (int64_t)j * per_j;
-  const int m = (int)(r / G), g = (int)(r - (int64_t)m * G);
+  const int m = (int)(r / (G + 1)), g = (int)(r - (int64_t)m * (G + 1));
+  const int gs = g - G / 2;  // phi_g = gs / G
   const double k0 = 0.5 * (sc.nf - 1);
   double cr[TAY_L], ci[TAY_L];
 #pragma unroll
@@ -52,12 +64,12 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
   const int kb = seg * kseg, ke = min(kb + kseg, sc.nf);
   if (live && kb < ke) {
     double sw, cw;
-    sincospi(2.0 * (double)g / (double)G, &sw, &cw);  // step e^{j2pi g/G}
+    sincospi(2.0 * (double)gs / (double)G, &sw, &cw);  // step e^{j2pi phi_g}
     double pr = 1.0, pi = 0.0;
     const float2* ym = y + (int64_t)j * sc.nf * sc.Na + m;
     for (int k = kb; k < ke; ++k) {
-      if (((k - kb) & 63) == 0) {  // anchor e^{j2pi (k - k0) g / G}: exact argument reduction of 2 (k - k0) g mod 2G
-        const double num = fmod(2.0 * ((double)k - k0) * (double)g, 2.0 * (double)G);
+      if (((k - kb) & 63) == 0) {  // anchor e^{j2pi (k - k0) gs/G}: exact reduction of 2 (k - k0) gs mod 2G
+        const double num = fmod(2.0 * ((double)k - k0) * (double)gs, 2.0 * (double)G);
         sincospi(num / (double)G, &pi, &pr);
       }
       const float2 v = ym[(int64_t)k * sc.Na];
@@ -85,17 +97,83 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
     }
   }
   if (live && seg == 0) {
-    if (lanes) {  // [j][g][q][m]
-      float4* out = reinterpret_cast<float4*>(tab) + ((int64_t)j * G + g) * (TAY_L / 2) * sc.Na + m;
+    if (lanes) {  // [j][g][h][m][4]
+      float2* out = tab + ((((int64_t)j * (G + 1) + g) * 2) * sc.Na + m) * 4;
 #pragma unroll
-      for (int q = 0; q < TAY_L / 2; ++q)
-        out[(int64_t)q * sc.Na] =
-            make_float4((float)cr[2 * q], (float)ci[2 * q], (float)cr[2 * q + 1], (float)ci[2 * q + 1]);
+      for (int l = 0; l < TAY_L; ++l) out[(int64_t)(l >> 2) * sc.Na * 4 + (l & 3)] = make_float2((float)cr[l], (float)ci[l]);
     } else {  // [j][m][g][l]
       float2* out = tab + t * TAY_L;
 #pragma unroll
       for (int l = 0; l < TAY_L; ++l) out[l] = make_float2((float)cr[l], (float)ci[l]);
     }
+  }
+}
+
+// The same table by FFT when G is a power of two: for each l, c_l(g) = e^{-j2pi k0 g/G} sum_k a_k e^{j2pi k g/G}
+// with a_k = y_k (j t_k)^l / l!, the zero-padded length-G DFT (positive exponent) of a.  One block per (j, m, l):
+// fp64 radix-2 decimation in time in shared memory (bit-reversed load, log2 G stages, twiddle table e^{j2pi i/G}
+// from sincospi), G/2 log2 G butterflies instead of the direct sum's G N_f terms; the centring phase uses the exact
+// integer reduction (N_f - 1) gs mod 2G; centre g = 0..G reads bin (g - G/2) mod G.
+constexpr int TAY_FFT_THREADS = 256;
+__global__ void __launch_bounds__(TAY_FFT_THREADS)
+    tay_prep_fft_kernel(const __grid_constant__ SceneDev sc, int G, int lgG, const float2* __restrict__ y,
+                        float2* __restrict__ tab, int lanes) {
+  extern __shared__ double2 fsm[];
+  double2* a = fsm;      // [G]
+  double2* w = fsm + G;  // [G/2]
+  const int l = blockIdx.x % TAY_L;
+  const int jm = blockIdx.x / TAY_L;
+  const int j = jm / sc.Na, m = jm - j * sc.Na;
+  const int nf = sc.nf;
+  const double k0 = 0.5 * (nf - 1);
+  for (int i = threadIdx.x; i < G / 2; i += TAY_FFT_THREADS) {
+    double s, c;
+    sincospi(2.0 * (double)i / (double)G, &s, &c);
+    w[i] = make_double2(c, s);
+  }
+  for (int i = threadIdx.x; i < G; i += TAY_FFT_THREADS) {
+    double2 v = make_double2(0.0, 0.0);
+    if (i < nf) {
+      const float2 yy = y[((int64_t)j * nf + i) * sc.Na + m];
+      const double tk = 2.0 * PI * ((double)i - k0) / (double)G;
+      double f = 1.0;
+      for (int q = 1; q <= l; ++q) f *= tk / (double)q;  // t_k^l / l!
+      const double vr = (double)yy.x * f, vi = (double)yy.y * f;
+      switch (l & 3) {  // times j^l
+        case 0: v = make_double2(vr, vi); break;
+        case 1: v = make_double2(-vi, vr); break;
+        case 2: v = make_double2(-vr, -vi); break;
+        default: v = make_double2(vi, -vr); break;
+      }
+    }
+    a[__brev((unsigned)i) >> (32 - lgG)] = v;
+  }
+  __syncthreads();
+  for (int lh = 0; lh < lgG; ++lh) {  // butterflies of span h = 2^lh
+    const int h = 1 << lh;
+    for (int b = threadIdx.x; b < G / 2; b += TAY_FFT_THREADS) {
+      const int pos = b & (h - 1);
+      const int i0 = ((b >> lh) << (lh + 1)) + pos, i1 = i0 + h;
+      const double2 tw = w[pos << (lgG - 1 - lh)];  // e^{j2pi pos/(2h)}
+      const double2 u = a[i0], x = a[i1];
+      const double vr = x.x * tw.x - x.y * tw.y, vi = x.x * tw.y + x.y * tw.x;
+      a[i0] = make_double2(u.x + vr, u.y + vi);
+      a[i1] = make_double2(u.x - vr, u.y - vi);
+    }
+    __syncthreads();
+  }
+  for (int g = threadIdx.x; g <= G; g += TAY_FFT_THREADS) {
+    const int gs = g - G / 2;  // phi_g = gs / G
+    int64_t num = ((int64_t)(nf - 1) * gs) % (2 * (int64_t)G);  // e^{-j2pi k0 phi_g} = e^{-j pi num/G}
+    if (num < 0) num += 2 * (int64_t)G;
+    double s, c;
+    sincospi(-(double)num / (double)G, &s, &c);
+    const double2 v = a[gs & (G - 1)];
+    const float2 o = make_float2((float)(v.x * c - v.y * s), (float)(v.x * s + v.y * c));
+    if (lanes)  // [j][g][h][m][4] (coefficients 4h .. 4h+3)
+      tab[((((int64_t)j * (G + 1) + g) * 2 + (l >> 2)) * sc.Na + m) * 4 + (l & 3)] = o;
+    else  // [j][m][g][l]
+      tab[(((int64_t)j * sc.Na + m) * (G + 1) + g) * TAY_L + l] = o;
   }
 }
 
@@ -114,13 +192,13 @@ __device__ __forceinline__ TayBase tay_base(double phib) {
   return b;
 }
 constexpr float TAY_MAGIC = 12582912.f;  // 1.5 * 2^23: (x + M) - M = rint(x) for |x| < 2^22, int bits of x + M - bits(M) = rint(x)
-// phi = phib + t (t = Delta_m df/c) = n + r, |r| <= 1/2 (TwoSum keeps hi + t exact as s + e); centre g = rint(r G)
-// wrapped into [0, G), delta' = r G - g (one fma, then the e + lo correction).  Y(phi + 1) = (-1)^(N_f - 1) Y(phi)
-// (k - k0 is a half-integer for even N_f), so the table value at the wrapped centre is multiplied by
-// (-1)^((n0 + n - w)(N_f - 1)), w = 1 when the centre was moved up by one period.  No conversions or MUFU: the fp64
-// version of this reduction (F2F, F2I, DFRND per antenna) held the XU pipe.
-__device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par, int G, float Gf, bool evenN, int& g,
-                                           float& dp, bool& flip) {
+// phi = phib + t (t = Delta_m df/c) = n + r, |r| <= 1/2 (TwoSum keeps hi + t exact as s + e); centre
+// g = rint(r G) + G/2 in [0, G] (phi_g = r rounded to the grid: no wrap, the table stores both ends), delta' =
+// r G - rint(r G) (one fma, then the e + lo correction).  Y(phi + 1) = (-1)^(N_f - 1) Y(phi) (k - k0 is a
+// half-integer for even N_f), so the table value is multiplied by (-1)^((n0 + n)(N_f - 1)).  No conversions or MUFU:
+// the fp64 version of this reduction (F2F, F2I, DFRND per antenna) held the XU pipe.
+__device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par, int Gh, float Gf, bool evenN,
+                                           uint32_t& g, float& dp, bool& flip) {
   const float s = hi + t;
   const float bb = s - hi;
   const float e = (hi - (s - bb)) + (t - bb);
@@ -129,13 +207,9 @@ __device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par,
   const float gm = fmaf(r, Gf, TAY_MAGIC);  // rint(r G) + M
   const float gi = gm - TAY_MAGIC;
   dp = fmaf(r, Gf, -gi) + (e + lo) * Gf;
-  int gg = __float_as_int(gm) - __float_as_int(TAY_MAGIC);
+  g = (uint32_t)(__float_as_int(gm) - __float_as_int(TAY_MAGIC) + Gh);
   const int nn = __float_as_int(sm) - __float_as_int(TAY_MAGIC);
-  int w = 0;
-  if (gg < 0) { gg += G; w = 1; }
-  if (gg >= G) { gg -= G; w = -1; }
-  g = gg;
-  flip = evenN && ((par + nn - w) & 1);
+  flip = evenN && ((par + nn) & 1);
 }
 
 // c_s for one particle per thread and one PA per blockIdx.y ([j][m][g][l] table; used when P J fills the SMs,
@@ -153,7 +227,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   if (p >= P) return;
   const int Na_pad = sc.n_mb * NWARP;
   const double* pos = particles + p * pstride;
-  const float2* tj = tab + (int64_t)j * Na * G * TAY_L;
+  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * Na * (G + 1) * (TAY_L / 2);
   const float4* tm = tmpl + (int64_t)j * Na_pad;
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
   int fl = 0;
@@ -177,8 +251,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     const TayBase tb = tay_base(R64 * sc.df_c);  // delay phase base
     double sb, cb;
     sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
-    const float Ebr = (float)cb, Ebi = (float)sb;  // e^{j2pi f_c R/c}
-    double accr = 0.0, acci = 0.0;
+    double accr = 0.0, acci = 0.0;  // sum_m e^{j2pi f_c Delta_m/c} Y_m; times e^{j2pi f_c R/c} (cb, sb) at the end
     for (int m0 = 0; m0 < Na; m0 += 16) {
       float pr = 0.f, pi = 0.f;
       const int m1 = min(m0 + 16, Na);
@@ -196,13 +269,14 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         }
         float er, ei;
         cis2pi_fast<float>(delta * sc.fc_cf, er, ei);
-        const float Er = Ebr * er - Ebi * ei, Ei = Ebr * ei + Ebi * er;  // e^{j2pi f_c d_m/c}
-        int g;
+        uint32_t g;
         float dp;
         bool flip;
-        tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G, (float)G, (sc.nf & 1) == 0, g, dp, flip);
-        const float4* row = reinterpret_cast<const float4*>(tj + ((int64_t)m * G + g) * TAY_L);
-        const float4 c01 = __ldg(row), c23 = __ldg(row + 1), c45 = __ldg(row + 2), c67 = __ldg(row + 3);
+        tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
+        const float4* row = tj + ((uint32_t)m * (uint32_t)(G + 1) + g) * (TAY_L / 2);
+        float4 c01, c23, c45, c67;
+        ldg256(row, c01, c23);
+        ldg256(row + 2, c45, c67);
         float yr = c67.z, yi = c67.w;  // Horner in delta', l = 7 .. 0
         yr = fmaf(yr, dp, c67.x); yi = fmaf(yi, dp, c67.y);
         yr = fmaf(yr, dp, c45.z); yi = fmaf(yi, dp, c45.w);
@@ -212,14 +286,14 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         yr = fmaf(yr, dp, c01.z); yi = fmaf(yi, dp, c01.w);
         yr = fmaf(yr, dp, c01.x); yi = fmaf(yi, dp, c01.y);
         if (flip) { yr = -yr; yi = -yi; }
-        pr = fmaf(Er, yr, fmaf(-Ei, yi, pr));
-        pi = fmaf(Er, yi, fmaf(Ei, yr, pi));
+        pr = fmaf(er, yr, fmaf(-ei, yi, pr));
+        pi = fmaf(er, yi, fmaf(ei, yr, pi));
       }
       accr += (double)pr;
       acci += (double)pi;
     }
     const double gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
-    terms[(p * J + j) * T + s] = make_double2(accr * gn, acci * gn);
+    terms[(p * J + j) * T + s] = make_double2((accr * cb - acci * sb) * gn, (accr * sb + acci * cb) * gn);
     double2* gr = terms + (p * J + j) * T + S + s * (s + 1) / 2;  // row s of the lower triangle of G
     gr[s] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);  // G_ss = g^2 N_z
     if (gram_diag)  // callers that use c only: no off-diagonal Gram
@@ -229,9 +303,10 @@ __global__ void __launch_bounds__(TAY_BLOCK)
 }
 
 // c_s with antennas across groups of LP = 2^lg lanes: for one component the phases of all antennas lie within a few
-// table centres, so with the [g][q][m] layout a group's gathers are (nearly) contiguous.  A warp owns npw = floor(32/S)
+// table centres, so with the [g][h][m] layout (32-byte entries) a group's gathers are (nearly) contiguous.  A warp owns npw = floor(32/S)
 // particles; lane i < npw S runs the fp64 set-up of pair i = (particle i / S, component i % S); the 32/LP groups then
 // take pairs i0 + group, each lane a strided subset of the antennas, and a fixed-order tree inside the group sums them.
+template <int EPL>  // antennas per lane (ceil(N_a / LP)), 0: runtime loop
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_corr_lanes_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
                           const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P,
@@ -245,10 +320,12 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   const int j = blockIdx.y;
   if (p0 >= P) return;  // warp-uniform
   const int npairs = (int)min((int64_t)npw, P - p0) * S;
-  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * G * (TAY_L / 2) * Na;
+  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * (G + 1) * (TAY_L / 2) * Na;
+  const uint32_t rstride = (uint32_t)(TAY_L / 2) * (uint32_t)Na;  // float4s per centre ([h][m] of 32-byte entries)
   const float4* tm = tmpl + (int64_t)j * sc.n_mb * NWARP;
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
-  float hx = 1.f, hy = 0.f, hz = 0.f, R = 1.f, Ebr = 1.f, Ebi = 0.f;
+  float hx = 1.f, hy = 0.f, hz = 0.f, R = 1.f;
+  double Ebr = 1.0, Ebi = 0.0;  // e^{j2pi f_c R/c}, applied to the antenna sum at the end
   float bhi = 0.f, blo = 0.f;
   int bpar = 0;
   double gn = 1.0;
@@ -275,12 +352,18 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         bhi = tb.hi; blo = tb.lo; bpar = tb.par;
         double sb, cb;
         sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
-        Ebr = (float)cb; Ebi = (float)sb;
+        Ebr = cb; Ebi = sb;
         gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
         ok = 1;
       }
     }
     if (fl) atomicOr(&pflag[p], fl);
+  }
+  float4 vt[EPL > 0 ? EPL : 1];  // this lane's antenna templates, loaded once for all pairs
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const int m = gl + (e << lg);
+    vt[e] = m < Na ? __ldg(&tm[m]) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   float cr = 0.f, ci = 0.f;  // lane i: pair i's correlation once reduced
   for (int i0 = 0; i0 < npairs; i0 += ng) {
@@ -289,13 +372,11 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     const int pok = __shfl_sync(0xffffffffu, ok, src) && i < npairs;
     const float shx = __shfl_sync(0xffffffffu, hx, src), shy = __shfl_sync(0xffffffffu, hy, src);
     const float shz = __shfl_sync(0xffffffffu, hz, src), sR = __shfl_sync(0xffffffffu, R, src);
-    const float sEr = __shfl_sync(0xffffffffu, Ebr, src), sEi = __shfl_sync(0xffffffffu, Ebi, src);
     const float shi = __shfl_sync(0xffffffffu, bhi, src), slo = __shfl_sync(0xffffffffu, blo, src);
     const int spar = __shfl_sync(0xffffffffu, bpar, src);
     float pr = 0.f, pi = 0.f;
     int efl = 0;
-    for (int m = pok ? gl : Na; m < Na; m += LP) {
-      const float4 v = __ldg(&tm[m]);
+    auto element = [&](int m, const float4 v) {
       const float rq = shx * v.x + shy * v.y + shz * v.z;
       float delta;
       if (sph) {
@@ -308,13 +389,14 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       }
       float er, ei;
       cis2pi_fast<float>(delta * sc.fc_cf, er, ei);
-      const float Er = sEr * er - sEi * ei, Ei = sEr * ei + sEi * er;
-      int g;
+      uint32_t g;
       float dp;
       bool flip;
-      tay_locate(delta * sc.df_cf, shi, slo, spar, G, (float)G, (sc.nf & 1) == 0, g, dp, flip);
-      const float4* row = tj + (int64_t)g * (TAY_L / 2) * Na + m;
-      const float4 c01 = __ldg(row), c23 = __ldg(row + Na), c45 = __ldg(row + 2 * Na), c67 = __ldg(row + 3 * Na);
+      tay_locate(delta * sc.df_cf, shi, slo, spar, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
+      const float4* row = tj + (g * rstride + 2u * (uint32_t)m);
+      float4 c01, c23, c45, c67;
+      ldg256(row, c01, c23);
+      ldg256(row + 2 * Na, c45, c67);
       float yr = c67.z, yi = c67.w;
       yr = fmaf(yr, dp, c67.x); yi = fmaf(yi, dp, c67.y);
       yr = fmaf(yr, dp, c45.z); yi = fmaf(yi, dp, c45.w);
@@ -324,8 +406,15 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       yr = fmaf(yr, dp, c01.z); yi = fmaf(yi, dp, c01.w);
       yr = fmaf(yr, dp, c01.x); yi = fmaf(yi, dp, c01.y);
       if (flip) { yr = -yr; yi = -yi; }
-      pr = fmaf(Er, yr, fmaf(-Ei, yi, pr));
-      pi = fmaf(Er, yi, fmaf(Ei, yr, pi));
+      pr = fmaf(er, yr, fmaf(-ei, yi, pr));
+      pi = fmaf(er, yi, fmaf(ei, yr, pi));
+    };
+    if (EPL > 0) {
+#pragma unroll
+      for (int e = 0; e < (EPL > 0 ? EPL : 1); ++e)
+        if (pok && gl + (e << lg) < Na) element(gl + (e << lg), vt[e]);
+    } else {
+      for (int m = pok ? gl : Na; m < Na; m += LP) element(m, __ldg(&tm[m]));
     }
     for (int o = LP >> 1; o > 0; o >>= 1) {  // fixed-order tree inside the group
       pr += __shfl_xor_sync(0xffffffffu, pr, o);
@@ -344,7 +433,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     const int64_t p = p0 + lane / S;
     const int s = lane % S;
     double2* tp = terms + (p * J + j) * T;
-    tp[s] = make_double2((double)cr * gn, (double)ci * gn);
+    tp[s] = make_double2(((double)cr * Ebr - (double)ci * Ebi) * gn, ((double)cr * Ebi + (double)ci * Ebr) * gn);
     double2* gr = tp + S + s * (s + 1) / 2;
     gr[s] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);
     if (gram_diag)
@@ -496,13 +585,24 @@ cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double
 
 // Layout / kernel choice (measured, profiles/r01_k1t_lanes.txt, CDMS_TAY_LANES=0/1 A/B): with P J below one
 // resident wave of the thread-per-particle kernel (148 SMs x ~1024 threads) it is latency-bound on its uncoalesced
-// row gathers and the lane-group kernel with the [g][q][m] table wins (c2, P = 1e5: 0.496 vs 0.58 ms/step); from
+// row gathers and the lane-group kernel with the [g][h][m] table wins (c2, P = 1e5: 0.496 vs 0.58 ms/step); from
 // P J = 2e5 on the thread kernel wins (c2 at 2e5 / 4e5 / 8e5: 0.80 / 1.29 / 2.30 vs 0.82 / 1.41 / 2.61 ms; c4
 // 10.3 vs 11.3).  Decided once per loglik call (from its particle count) for the table build and every batch.
 bool tay_lanes(const SceneDev& sc, int64_t P) { return (double)P * sc.J < 148.0 * 1024; }
-cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, cudaStream_t st) {
+// FFT when G is a power of two in [64, 4096] (N_f a power of two up to 1024), unless direct = 1 (A/B); else the
+// direct sum.  Both fp64, rounded once to complex64.
+cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, int direct, cudaStream_t st) {
   const int G = tay_centres(sc.nf);
-  const int64_t n = (int64_t)sc.J * sc.Na * G * TAY_KS;
+  if (!direct && (G & (G - 1)) == 0 && G >= 64 && G <= 4096) {
+    int lgG = 0;
+    while ((1 << lgG) < G) ++lgG;
+    const size_t smem = (size_t)G * sizeof(double2) * 3 / 2;
+    cudaError_t e = cudaFuncSetAttribute(tay_prep_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    tay_prep_fft_kernel<<<(unsigned)(sc.J * sc.Na * TAY_L), TAY_FFT_THREADS, smem, st>>>(sc, G, lgG, y, tab, lanes);
+    return cudaGetLastError();
+  }
+  const int64_t n = (int64_t)sc.J * sc.Na * (G + 1) * TAY_KS;
   tay_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, G, y, tab, lanes);
   return cudaGetLastError();
 }
@@ -513,10 +613,19 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
   if (lanes) {
     int lg = 2;
     while ((1 << lg) < 32 && (4 << lg) < sc.Na) ++lg;  // ~4 antennas per lane
+    const int epl = (sc.Na + (1 << lg) - 1) >> lg;
     const int64_t per_block = (int64_t)(TAY_BLOCK / 32) * (32 / sc.S);
     dim3 grid((unsigned)((P + per_block - 1) / per_block), sc.J);
-    tay_corr_lanes_kernel<<<grid, TAY_BLOCK, 0, st>>>(sc, tay_centres(sc.nf), tab, tmpl, particles, P, pstride, sfv,
-                                                      sfv_pp, terms, pflag, gram_diag, lg);
+    const int G = tay_centres(sc.nf);
+#define TAY_LANES(E)                                                                                             \
+  tay_corr_lanes_kernel<E><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, sfv, sfv_pp, terms, \
+                                                       pflag, gram_diag, lg)
+    if (epl == 1) TAY_LANES(1);
+    else if (epl == 2) TAY_LANES(2);
+    else if (epl <= 4) TAY_LANES(4);
+    else if (epl <= 8) TAY_LANES(8);
+    else TAY_LANES(0);
+#undef TAY_LANES
     return cudaGetLastError();
   }
   dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);

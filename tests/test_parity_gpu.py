@@ -233,7 +233,7 @@ def test_loglik_near_truth_worst_case(cd, ctx, orc, name, wf):
 @pytest.mark.parametrize("P", [4096, 200_000])
 def test_taylor_layouts_near_truth(cd, ctx, orc, P):
     """K1T picks its table layout and correlation kernel from P J (taylor.cu tay_lanes: lane groups with the
-    [g][q][m] table below ~152k, one thread per particle with the [m][g][l] table above); both at the near-truth
+    [g][h][m] table below ~152k, one thread per particle with the [m][g][l] table above); both at the near-truth
     worst case, plus a stratified sample."""
     import dataclasses
     cfg = dataclasses.replace(scenes.CONFIGS["c2"], P=P)  # c2's scene, P particles
@@ -455,5 +455,34 @@ def test_taylor_engine_matches_k1(cd, orc):
     e = rel_err(l_t, l_k, cfg.J, cfg.Nz).max()
     record("taylor_vs_k1_rel_l", e, 2e-4)
     assert e <= 2e-4, e
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("lanes", ["0", "1"])
+def test_taylor_prep_fft_matches_direct(cd, orc, lanes):
+    """K1T's table build by FFT (power-of-two G, tay_prep_fft_kernel) and by the direct sum (CDMS_TAY_PREP=direct)
+    are both fp64 rounded once to complex64: the likelihoods agree far inside the fp32 tolerance, in both table
+    layouts (CDMS_TAY_LANES)."""
+    import os
+    cfg = small_cfg(J=2, K=4, ny=8, nv=8, nf=64, P=500)
+    ctxs = []
+    try:
+        os.environ["CDMS_TAY_LANES"] = lanes
+        ctxs.append(cd.Context(0))
+        os.environ["CDMS_TAY_PREP"] = "direct"
+        ctxs.append(cd.Context(0))
+    finally:
+        os.environ.pop("CDMS_TAY_PREP", None)
+        os.environ.pop("CDMS_TAY_LANES", None)
+    case = Case(orc, cfg)
+    l_f = case.gpu_loglik(ctxs[0]).cpu().numpy()
+    l_d = case.gpu_loglik(ctxs[1]).cpu().numpy()
+    for c in ctxs:
+        c.sync()
+    e = rel_err(l_f, l_d, cfg.J, cfg.Nz).max()
+    record(f"taylor_fft_vs_direct_rel_l_lanes{lanes}", e, 1e-5)
+    assert e <= 1e-5, e
+    check_loglik(case, ctxs[0], "fp32")
     for c in ctxs:
         c.close()

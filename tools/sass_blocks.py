@@ -7,7 +7,12 @@ import sys
 rows = list(csv.reader(open(sys.argv[1])))
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 hdr = rows[1]
-data = rows[2:]
+data = []
+for r in rows[2:]:  # the first kernel section only (a report may repeat "Kernel Name" sections)
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) >= len(hdr) - 1:
+        data.append(r)
 ie, si = hdr.index("Instructions Executed"), hdr.index("Source")
 ws = hdr.index("Warp Stall Sampling (All Samples)")
 blocks, cur = [], None

@@ -53,7 +53,7 @@ def measured_tensor_peak():
 def k1t_kernels(cfg, P: int) -> str:
     """The K1T stage's kernels as libcdms picks them (taylor.cu tay_lanes, cdms.cpp engine selection)."""
     c = ("cdms::tay_corr_lanes_kernel" if P * cfg.J < 148 * 1024 else "cdms::tay_corr_kernel") + " (K1T, c)"
-    g = "tay_gram_kernel<S> (G)" if cfg.K + 1 <= 5 else "corr_kernel<S, float, 0, 1> Horner-free K1 (G)"
+    g = "tay_gram_kernel<S> (G)"
     return c + " + " + g
 
 

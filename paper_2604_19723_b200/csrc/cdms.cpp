@@ -32,7 +32,7 @@ struct cdms_ctx_s {
   bool timing = false;           // bracket the likelihood kernel with events
   bool nb_tensor = true;         // PLANAR_NB fp32 on the tensor cores (nbmma.cu); CDMS_NB_TENSOR=0 selects K1
   bool taylor = true;            // spherical / planar-WB fp32 correlation by K1T (taylor.cu); CDMS_TAYLOR=0 selects K1
-  int taylor_gram = 0;           // K1T's off-diagonal Gram: 0 by S, 1 K1's Horner-free variant, 2 tay_gram_kernel
+  int taylor_gram = 0;           // K1T's off-diagonal Gram: 0/2 tay_gram_kernel, 1 K1's Horner-free variant
                                  // (CDMS_TAYLOR_GRAM=k1 / tay, A/B only)
   int taylor_prep_direct = 0;   // K1T tables by the direct sum even when G is a power of two (CDMS_TAY_PREP=direct,
                                  // A/B only; default FFT)
@@ -489,10 +489,10 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       ctx->launches += 1;
     } else if (tay) {
       // c and G_ss from K1T; the off-diagonal Gram from tay_gram_kernel (thread per particle, all pairs), or with
-      // CDMS_TAYLOR_GRAM=k1 from K1's Horner-free variant, which writes every term (c as zeros) and so runs first
-      // measured (profiles/r01_k1t_gram_select.txt): the thread-per-particle kernel wins up to S = 5 (c4: 12.8 vs
-      // 13.8 ms, c2 equal), K1's Horner-free variant from S = 7 (c3 14.4 vs 15.3, c5 shard 87 vs 110)
-      const bool k1g = !no_gram && (ctx->taylor_gram == 1 || (ctx->taylor_gram == 0 && sd.S >= 6));
+      // CDMS_TAYLOR_GRAM=k1 from K1's Horner-free variant, which writes every term (c as zeros) and so runs first.
+      // Measured (profiles/r01_k1t_gram_select.txt): since its pair loops unroll fully tay_gram wins at every S
+      // (c3, S = 7: 8.97 vs 12.45 ms per step; c5 shard, S = 9: 60.0 vs 73.6; c2: 0.40 vs 0.48)
+      const bool k1g = !no_gram && ctx->taylor_gram == 1;
       if (k1g) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));
       CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, pflag,
                                     no_gram ? 1 : 0, tlanes, ctx->stream));

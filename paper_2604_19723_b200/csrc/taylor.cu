@@ -458,13 +458,14 @@ __device__ __forceinline__ bool tay_component(const SceneDev& sc, int j, const d
   R64 = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
   return R64 > 0.0;
 }
-template <int S>
-__global__ void __launch_bounds__(TAY_BLOCK)
-    tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
-                    const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
-                    int sfv_pp, double2* __restrict__ terms, int lsplit) {
-  constexpr int NP = S * (S - 1) / 2;
-  extern __shared__ double2 gsum[];  // [NP][TAY_BLOCK]
+// Pairs q in [Q0, Q1) (row order (0,1), (0,2), ..., (1,2), ...): large S splits the pairs over blockIdx.z so each
+// thread holds only its part's accumulators (S = 9: 255 registers and 73 KB of totals per block for all 36 pairs).
+template <int S, int Q0, int Q1>
+__device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* __restrict__ tmpl,
+                                              const double* __restrict__ particles, int64_t P, int pstride,
+                                              const double* __restrict__ sfv, int sfv_pp, double2* __restrict__ terms,
+                                              int lsplit, double2* gsum) {
+  constexpr int NP = Q1 - Q0;  // this part's pairs; gsum [NP][TAY_BLOCK]
   // A = 2^lsplit adjacent lanes per particle, lane a takes antennas a, a + A, ... (A > 1 when P J threads alone would
   // leave the SMs latency-bound); no early exit: the group's fp64 totals are combined by shuffles below
   const int A = 1 << lsplit;
@@ -520,7 +521,8 @@ __global__ void __launch_bounds__(TAY_BLOCK)
 #pragma unroll
         for (int b = 0; b < S; ++b) {
           if (b <= a) continue;
-          const int q = a * (2 * S - a - 1) / 2 + (b - a - 1);
+          const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
+          if (q < 0 || q >= NP) continue;
           GramPairF gp;
           gp.xbr = (uh[a] - uh[b]) + (ul[a] - ul[b]);
           gp.nbpar = (uint32_t)((npar[a] ^ npar[b]) & 1) << 31;
@@ -542,7 +544,8 @@ __global__ void __launch_bounds__(TAY_BLOCK)
 #pragma unroll
     for (int b = 0; b < S; ++b) {
       if (b <= a) continue;
-      const int q = a * (2 * S - a - 1) / 2 + (b - a - 1);
+      const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
+      if (q < 0 || q >= NP) continue;
       double2 acc = gsum[q * TAY_BLOCK + threadIdx.x];
       for (int o = 1; o < A; o <<= 1) {  // fixed-order tree over the group's lanes
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -558,15 +561,43 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   }
 }
 template <int S>
+// measured: S = 9 in 3 parts 58.8 vs 59.8 ms (c5 shard); S = 7 in 2 parts 9.16 vs 8.87 ms (c3: one part already fits
+// 168 registers, splitting only repeats the per-component work)
+__host__ __device__ constexpr int tay_gram_parts() { return S >= 9 ? 3 : (S == 8 ? 2 : 1); }
+template <int S>
+__global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? 3 : 1))  // S >= 7: 3 blocks (12 warps) per SM, <= 168 registers
+    tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
+                    const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
+                    int sfv_pp, double2* __restrict__ terms, int lsplit) {
+  constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>(), H = NP / NPART;
+  extern __shared__ double2 gsum[];
+  if constexpr (NPART == 1) {
+    tay_gram_part<S, 0, NP>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+  } else if constexpr (NPART == 2) {
+    if (blockIdx.z == 0)
+      tay_gram_part<S, 0, H>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+    else
+      tay_gram_part<S, H, NP>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+  } else {
+    static_assert(NPART == 3, "");
+    if (blockIdx.z == 0)
+      tay_gram_part<S, 0, H>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+    else if (blockIdx.z == 1)
+      tay_gram_part<S, H, 2 * H>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+    else
+      tay_gram_part<S, 2 * H, NP>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+  }
+}
+template <int S>
 static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
                                      int pstride, const double* sfv, int sfv_pp, double2* terms, cudaStream_t st) {
-  constexpr int NP = S * (S - 1) / 2;
-  const size_t smem = (size_t)NP * TAY_BLOCK * sizeof(double2);
+  constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>();
+  const size_t smem = (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2);  // the larger part
   cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // antennas over 4 lanes per particle when P J threads are fewer than ~2 resident waves
   const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 2 : 0;
-  dim3 grid((unsigned)(((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
+  dim3 grid((unsigned)(((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK), sc.J, NPART);
   tay_gram_kernel<S><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit);
   return cudaGetLastError();
 }

@@ -34,6 +34,9 @@ struct cdms_ctx_s {
   bool taylor = true;            // spherical / planar-WB fp32 correlation by K1T (taylor.cu); CDMS_TAYLOR=0 selects K1
   int taylor_gram = 0;           // K1T's off-diagonal Gram: 0/2 tay_gram_kernel, 1 K1's Horner-free variant
                                  // (CDMS_TAYLOR_GRAM=k1 / tay, A/B only)
+  int step_fused = 0;           // 1: single-rank bp_step O(P) phases in one cooperative kernel (CDMS_STEP_FUSED=1,
+                                 // A/B; measured not faster: c2 0.409 vs 0.403 ms, the grid barriers and block 0's
+                                 // epilogues cost what the launches did)
   int taylor_prep_direct = 0;   // K1T tables by the direct sum even when G is a power of two (CDMS_TAY_PREP=direct,
                                  // A/B only; default FFT)
   int taylor_lanes = -1;         // K1T correlation kernel: -1 by P J (tay_lanes), 1 lane groups, 0 thread per
@@ -539,6 +542,7 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("CDMS_NB_TENSOR")) ctx->nb_tensor = atoi(e) != 0;
   if (const char* e = getenv("CDMS_TAYLOR")) ctx->taylor = atoi(e) != 0;
+  if (const char* e = getenv("CDMS_STEP_FUSED")) ctx->step_fused = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_TAY_PREP")) ctx->taylor_prep_direct = strcmp(e, "direct") == 0 ? 1 : 0;
   if (const char* e = getenv("CDMS_TAY_LANES")) ctx->taylor_lanes = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_TAYLOR_GRAM")) ctx->taylor_gram = strcmp(e, "k1") == 0 ? 1 : (strcmp(e, "tay") == 0 ? 2 : 0);
@@ -908,6 +912,37 @@ cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_partic
   WS_TRY(ctx, WS_BSUM, nb + 2, &bsum);
   WS_TRY(ctx, WS_QALL, 2 * R + 4, &qall);
   WS_TRY(ctx, WS_STEP_CNT, 4, &cnt);  // zeroed at allocation, reset by each kernel's last block
+  if (!comm && ctx->step_fused) {
+    // one rank: the five kernels' bodies in one cooperative launch (grid barriers instead of launches and
+    // last-block tails), identical arithmetic and block partition, so identical results
+    WS_TRY(ctx, WS_STAGE, P_local * 6, &stage);
+    StepFusedArgs fa;
+    fa.l = l;
+    fa.x = d_particles;
+    fa.P = P_local;
+    fa.lpart = lpart;
+    fa.rank_pair = pairs;
+    fa.lse = d_lse;
+    fa.M = scal + 0;
+    fa.logS = scal + 1;
+    fa.flags = ctx->d_flags;
+    fa.w = w;
+    fa.q = q;
+    fa.mpart = mpart;
+    fa.bsum = bsum;
+    fa.sums = sums;
+    fa.est = d_est;
+    fa.L = L6;
+    fa.stage = stage;
+    fa.u_bits = host_step_u_bits(prm->philox_key, prm->step);
+    fa.h = step_reg_bandwidth(P_total);
+    fa.regularize = prm->regularize ? 1 : 0;
+    fa.key = prm->philox_key;
+    fa.step = prm->step;
+    CUDA_TRY(ctx, launch_step_fused(fa, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return CDMS_OK;
+  }
   CUDA_TRY(ctx, launch_step_lse(l, P_local, lpart, cnt + 0, comm ? pairs + R : pairs, comm ? 0 : 1, d_lse, scal + 0,
                                 scal + 1, ctx->d_flags, ctx->stream));
   ctx->launches += 1;
@@ -965,7 +1000,7 @@ cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_partic
   }
   const int64_t n = plan.hi - plan.lo;
   WS_TRY(ctx, WS_STAGE, (n > 0 ? n : 1) * 6, &stage);
-  CUDA_TRY(ctx, launch_step_anc(q, P_local, Qtot, Ooff, plan.lo, plan.hi, P_total, u_bits, d_particles, stage,
+  CUDA_TRY(ctx, launch_step_anc(q, bsum, P_local, Qtot, Ooff, plan.lo, plan.hi, P_total, u_bits, d_particles, stage,
                                 ctx->d_flags, ctx->stream));
   ctx->launches += 1;
   if (comm) {

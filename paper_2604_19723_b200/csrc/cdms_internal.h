@@ -272,10 +272,33 @@ cudaError_t launch_step_scan(uint64_t* q, const double* x, const double* w, int6
                              int finalize, double* est, double* L, int* flags_w, cudaStream_t st);
 cudaError_t launch_step_finalize(const double* sum1, const double* sum2, double* est, double* L, int* flags,
                                  cudaStream_t st);
-cudaError_t launch_step_anc(const uint64_t* C, int64_t P_local, const uint64_t* Qtot, const uint64_t* offset,
-                            int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits, const double* x,
-                            double* out, int* flags, cudaStream_t st);
+cudaError_t launch_step_anc(const uint64_t* C, const uint64_t* boff, int64_t P_local, const uint64_t* Qtot,
+                            const uint64_t* offset, int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits,
+                            const double* x, double* out, int* flags, cudaStream_t st);
 cudaError_t launch_step_reg(const double* in, double* out, int64_t P, int64_t p0, int64_t P_total, const double* L,
                             int regularize, uint64_t key, uint64_t step, cudaStream_t st);
+// fused single-rank pipeline (K_lse .. K_reg in one cooperative launch, step.cu)
+struct StepFusedArgs {
+  const double* l;
+  double* x;  // particles [P][6], read by K_post / K_scan / K_anc, overwritten by K_reg
+  int64_t P;
+  double2* lpart;
+  double2* rank_pair;
+  double *lse, *M, *logS;
+  int* flags;
+  double* w;
+  uint64_t* q;
+  double* mpart;
+  uint64_t* bsum;  // [nb + 1]
+  double* sums;    // [32]: sum1 at 0, sum2 at 8
+  double *est, *L;
+  double* stage;  // [P][6]
+  uint32_t u_bits;
+  double h;
+  int regularize;
+  uint64_t key, step;
+};
+cudaError_t launch_step_fused(const StepFusedArgs& a, int num_sms, cudaStream_t st);
+double step_reg_bandwidth(int64_t P_total);
 
 }  // namespace cdms

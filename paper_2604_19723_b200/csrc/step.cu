@@ -14,7 +14,11 @@
 // inserts the NCCL collectives between the kernels and runs the same combine / finalize device code.
 #include <math.h>
 
+#include <cooperative_groups.h>
+
 #include "cdms_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace cdms {
 
@@ -62,18 +66,34 @@ __device__ __forceinline__ bool last_block(unsigned* cnt) {
   return am_last;
 }
 
-// Column sums of part[nb][N]: warp w takes columns c = w, w + 8, ...; lane l sums rows b = l, l + 32, ...
-// ascending, then a fixed shuffle tree -- deterministic, no block barriers.  out is visible to the block after
-// the trailing __syncthreads.
+// Column sums of part[nb][N]: G = STEP_BLOCK / N threads per column, thread g sums rows g, g + G, ... ascending
+// (four independent loads in flight), then one thread per column adds the G partials in order -- deterministic.
+// out is visible to the block after the trailing __syncthreads.  (One warp per column with one dependent L2 load
+// per step made the single-block epilogues the longest serial part of the step.)
 template <int N>
-__device__ void sum_columns(const double* part, int64_t nb, double* /*sh*/, double* out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp; c < N; c += STEP_BLOCK / 32) {
-    double s = 0.0;
-    for (int64_t b = lane; b < nb; b += 32) s += __ldcg(&part[b * N + c]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (lane == 0) out[c] = s;
+__device__ void sum_columns(const double* part, int64_t nb, double* out) {
+  constexpr int G = STEP_BLOCK / N;
+  __shared__ double red[STEP_BLOCK];
+  const int c = threadIdx.x / G, g = threadIdx.x - c * G;
+  double s = 0.0;
+  if (c < N) {
+    int64_t b = g;
+    for (; b + 3 * G < nb; b += 4 * G) {
+      const double v0 = __ldcg(&part[b * N + c]), v1 = __ldcg(&part[(b + G) * N + c]);
+      const double v2 = __ldcg(&part[(b + 2 * G) * N + c]), v3 = __ldcg(&part[(b + 3 * G) * N + c]);
+      s += v0;
+      s += v1;
+      s += v2;
+      s += v3;
+    }
+    for (; b < nb; b += G) s += __ldcg(&part[b * N + c]);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if ((int)threadIdx.x < N) {
+    double tot = 0.0;
+    for (int k = 0; k < G; ++k) tot += red[threadIdx.x * G + k];
+    out[threadIdx.x] = tot;
   }
   __syncthreads();
 }
@@ -114,42 +134,58 @@ __device__ void finalize_dev(const double* sum1, const double* sum2, double* est
   if (lane < 28) est[lane] = lane == 0 ? sw : (lane < 7 ? sum1[lane] : sum2[lane - 7]) / sw;
   __syncwarp();
   if (L == nullptr || lane != 0) return;
+  // fully unrolled with compile-time indices: the 6 x 6 factors stay in registers (a rolled version lived in
+  // local memory on the single thread that runs it)
   double Sg[36];
-  int t = 0;
+#pragma unroll
   for (int a = 0; a < 6; ++a)
-    for (int b = a; b < 6; ++b) {
+#pragma unroll
+    for (int b = 0; b < 6; ++b) {
+      if (b < a) continue;
+      const int t = a * 6 - a * (a - 1) / 2 + (b - a);  // upper-triangle index, row-major
       Sg[a * 6 + b] = est[7 + t];
       Sg[b * 6 + a] = est[7 + t];
-      ++t;
     }
   double tr = 0.0;
+#pragma unroll
   for (int a = 0; a < 6; ++a) tr += Sg[a * 6 + a];
+#pragma unroll
   for (int a = 0; a < 6; ++a) Sg[a * 6 + a] += 1e-12 * tr;
   double Lr[36];
+#pragma unroll
   for (int i = 0; i < 36; ++i) Lr[i] = 0.0;
+#pragma unroll
   for (int j = 0; j < 6; ++j) {
     double d = Sg[j * 6 + j];
-    for (int k = 0; k < j; ++k) d -= Lr[j * 6 + k] * Lr[j * 6 + k];
-    if (!(d > 0.0)) continue;
-    const double lj = sqrt(d);
-    const double inv = 1.0 / lj;
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if (k < j) d -= Lr[j * 6 + k] * Lr[j * 6 + k];
+    const bool ok = d > 0.0;
+    const double lj = ok ? sqrt(d) : 0.0;
+    const double inv = ok ? 1.0 / lj : 0.0;
     Lr[j * 6 + j] = lj;
-    for (int i = j + 1; i < 6; ++i) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      if (i <= j) continue;
       double acc = Sg[i * 6 + j];
-      for (int k = 0; k < j; ++k) acc -= Lr[i * 6 + k] * Lr[j * 6 + k];
-      Lr[i * 6 + j] = acc * inv;
+#pragma unroll
+      for (int k = 0; k < 6; ++k)
+        if (k < j) acc -= Lr[i * 6 + k] * Lr[j * 6 + k];
+      Lr[i * 6 + j] = ok ? acc * inv : 0.0;
     }
   }
+#pragma unroll
   for (int i = 0; i < 36; ++i) L[i] = Lr[i];
 }
 
 // ---------------------------------------------------------------------------- K_lse
-__global__ void __launch_bounds__(STEP_BLOCK) step_lse_kernel(const double* __restrict__ l, int64_t P,
-                                                             double2* __restrict__ part, unsigned* cnt,
-                                                             double2* rank_pair, int combine, double* lse,
-                                                             double* M, double* logS, int* flags) {
+// Each phase is a per-block body of virtual block vb (STEP_ITEMS particles) and a cross-block epilogue; the
+// separate kernels run the epilogue in the last block to arrive, the fused single-rank kernel (below) in block 0
+// after a grid barrier -- the same code either way, so results are identical.  Data written by other blocks in
+// the same launch is read with __ldcg (L2), never through the non-coherent path.
+__device__ void lse_block(int64_t vb, const double* l, int64_t P, double2* part) {
   __shared__ double sh[STEP_BLOCK];
-  const int64_t base = (int64_t)blockIdx.x * STEP_ITEMS + threadIdx.x * STEP_PER;
+  const int64_t base = vb * STEP_ITEMS + threadIdx.x * STEP_PER;
   double v[STEP_PER];
   double m = -INFINITY;
 #pragma unroll
@@ -177,10 +213,13 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_lse_kernel(const double* __re
     if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(Mb, sh[0]);
-  if (!last_block(cnt)) return;
+  if (threadIdx.x == 0) part[vb] = make_double2(Mb, sh[0]);
+  __syncthreads();
+}
+__device__ void lse_final(int64_t nb, const double2* part, double2* rank_pair, int combine, double* lse, double* M,
+                          double* logS, int* flags) {
+  __shared__ double sh[STEP_BLOCK];
   // fixed-order combine of the block partials -> this rank's (M_r, S_r)
-  const int64_t nb = gridDim.x;
   double mm = -INFINITY;
   for (int64_t b = threadIdx.x; b < nb; b += STEP_BLOCK) mm = fmax(mm, __ldcg(&part[b].x));
   sh[threadIdx.x] = mm;
@@ -207,6 +246,15 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_lse_kernel(const double* __re
     *rank_pair = make_double2(Mr, sh[0]);
     if (combine) lse_combine_dev(rank_pair, 1, lse, M, logS, flags);
   }
+  __syncthreads();
+}
+__global__ void __launch_bounds__(STEP_BLOCK) step_lse_kernel(const double* __restrict__ l, int64_t P,
+                                                             double2* __restrict__ part, unsigned* cnt,
+                                                             double2* rank_pair, int combine, double* lse,
+                                                             double* M, double* logS, int* flags) {
+  lse_block(blockIdx.x, l, P, part);
+  if (!last_block(cnt)) return;
+  lse_final(gridDim.x, part, rank_pair, combine, lse, M, logS, flags);
 }
 
 __global__ void step_lse_combine_kernel(const double2* per_rank, int nranks, double* lse, double* M, double* logS,
@@ -215,19 +263,15 @@ __global__ void step_lse_combine_kernel(const double2* per_rank, int nranks, dou
 }
 
 // ---------------------------------------------------------------------------- K_post
-__global__ void __launch_bounds__(STEP_BLOCK) step_post_kernel(const double* __restrict__ l,
-                                                              const double* __restrict__ x, int64_t P,
-                                                              const double* __restrict__ Mp,
-                                                              const double* __restrict__ logSp, const int* flags,
-                                                              double* __restrict__ w, uint64_t* __restrict__ q,
-                                                              double* __restrict__ mpart, uint64_t* __restrict__ bsum,
-                                                              unsigned* cnt, double* __restrict__ sum1) {
+__device__ void post_block(int64_t vb, const double* l, const double* x, int64_t P, const double* Mp,
+                           const double* logSp, const int* flags, double* w, uint64_t* q, double* mpart,
+                           uint64_t* bsum) {
   __shared__ double sh[STEP_BLOCK * 4];
   __shared__ double red[8];
   __shared__ uint64_t shq[STEP_BLOCK];
-  const bool bad = (*flags & (FLAG_ZEROMASS | FLAG_NAN)) != 0;
-  const double M = *Mp, ls = *logSp;
-  const int64_t base = (int64_t)blockIdx.x * STEP_ITEMS + threadIdx.x * STEP_PER;
+  const bool bad = (__ldcg(flags) & (FLAG_ZEROMASS | FLAG_NAN)) != 0;
+  const double M = __ldcg(Mp), ls = __ldcg(logSp);
+  const int64_t base = vb * STEP_ITEMS + threadIdx.x * STEP_PER;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   uint64_t qs = 0;
 #pragma unroll
@@ -248,7 +292,7 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_post_kernel(const double* __r
     for (int a = 0; a < 6; ++a) acc[1 + a] += wa * x[p * 6 + a];
   }
   block_sum<7>(acc, sh, red);
-  if (threadIdx.x < 7) mpart[blockIdx.x * 7 + threadIdx.x] = red[threadIdx.x];
+  if (threadIdx.x < 7) mpart[vb * 7 + threadIdx.x] = red[threadIdx.x];
   // block total of q (exact)
   shq[threadIdx.x] = qs;
   __syncthreads();
@@ -256,10 +300,12 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_post_kernel(const double* __r
     if ((int)threadIdx.x < o) shq[threadIdx.x] += shq[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) bsum[blockIdx.x] = shq[0];
-  if (!last_block(cnt)) return;
-  const int64_t nb = gridDim.x;
-  sum_columns<7>(mpart, nb, sh, sum1);
+  if (threadIdx.x == 0) bsum[vb] = shq[0];
+  __syncthreads();
+}
+__device__ void post_final(int64_t nb, const double* mpart, uint64_t* bsum, double* sum1) {
+  __shared__ uint64_t shq[STEP_BLOCK];
+  sum_columns<7>(mpart, nb, sum1);
   // exclusive scan of the block totals in place; bsum[nb] = Q (this rank)
   const int64_t chunk = (nb + STEP_BLOCK - 1) / STEP_BLOCK;
   const int64_t b0 = threadIdx.x * chunk, b1 = min(nb, b0 + chunk);
@@ -280,21 +326,25 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_post_kernel(const double* __r
     ex += v;
   }
   if (threadIdx.x == STEP_BLOCK - 1) bsum[nb] = shq[STEP_BLOCK - 1];
+  __syncthreads();
+}
+__global__ void __launch_bounds__(STEP_BLOCK) step_post_kernel(const double* l, const double* x, int64_t P,
+                                                              const double* Mp, const double* logSp, const int* flags,
+                                                              double* w, uint64_t* q, double* mpart, uint64_t* bsum,
+                                                              unsigned* cnt, double* sum1) {
+  post_block(blockIdx.x, l, x, P, Mp, logSp, flags, w, q, mpart, bsum);
+  if (!last_block(cnt)) return;
+  post_final(gridDim.x, mpart, bsum, sum1);
 }
 
 // ---------------------------------------------------------------------------- K_scan
-__global__ void __launch_bounds__(STEP_BLOCK) step_scan_kernel(uint64_t* __restrict__ q, const double* __restrict__ x,
-                                                              const double* __restrict__ w, int64_t P,
-                                                              const uint64_t* __restrict__ boff,
-                                                              const double* __restrict__ sum1, const int* flags,
-                                                              double* __restrict__ mpart, unsigned* cnt,
-                                                              double* __restrict__ sum2, int finalize,
-                                                              double* est, double* L, int* flags_w) {
+__device__ void scan_block(int64_t vb, uint64_t* q, const double* x, const double* w, int64_t P, const uint64_t* boff,
+                           const double* sum1, const int* flags, double* mpart) {
   __shared__ double sh[STEP_BLOCK * 21 / 8 + 32];
   __shared__ double red[24];
   __shared__ uint64_t shq[STEP_BLOCK];
-  const bool bad = (*flags & (FLAG_ZEROMASS | FLAG_NAN)) != 0;
-  const int64_t base = (int64_t)blockIdx.x * STEP_ITEMS + threadIdx.x * STEP_PER;
+  const bool bad = (__ldcg(flags) & (FLAG_ZEROMASS | FLAG_NAN)) != 0;
+  const int64_t base = vb * STEP_ITEMS + threadIdx.x * STEP_PER;
   // inclusive scan: thread-contiguous runs, Hillis-Steele over the thread totals, + block offset
   uint64_t v[STEP_PER];
   uint64_t run = 0;
@@ -311,14 +361,14 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_scan_kernel(uint64_t* __restr
     shq[threadIdx.x] += add;
     __syncthreads();
   }
-  const uint64_t ex = ((threadIdx.x > 0) ? shq[threadIdx.x - 1] : 0ull) + boff[blockIdx.x];
+  const uint64_t ex = ((threadIdx.x > 0) ? shq[threadIdx.x - 1] : 0ull) + __ldcg(&boff[vb]);
 #pragma unroll
   for (int i = 0; i < STEP_PER; ++i)
     if (base + i < P) q[base + i] = v[i] + ex;
   // second moments about the global mean
   double mu[6];
 #pragma unroll
-  for (int a = 0; a < 6; ++a) mu[a] = sum1[1 + a] / sum1[0];
+  for (int a = 0; a < 6; ++a) mu[a] = __ldcg(&sum1[1 + a]) / __ldcg(&sum1[0]);
   double acc[21];
 #pragma unroll
   for (int t = 0; t < 21; ++t) acc[t] = 0.0;
@@ -337,10 +387,23 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_scan_kernel(uint64_t* __restr
       for (int b = a; b < 6; ++b) acc[t++] += wp * d[a] * d[b];
   }
   block_sum<21>(acc, sh, red);
-  if (threadIdx.x < 21) mpart[blockIdx.x * 21 + threadIdx.x] = red[threadIdx.x];
-  if (!last_block(cnt)) return;
-  sum_columns<21>(mpart, gridDim.x, sh, sum2);
+  if (threadIdx.x < 21) mpart[vb * 21 + threadIdx.x] = red[threadIdx.x];
+  __syncthreads();
+}
+__device__ void scan_final(int64_t nb, const double* mpart, double* sum2, int finalize, const double* sum1,
+                           double* est, double* L, int* flags_w) {
+  sum_columns<21>(mpart, nb, sum2);
   if (finalize && threadIdx.x < 32) finalize_dev(sum1, sum2, est, L, flags_w);  // warp 0
+  __syncthreads();
+}
+__global__ void __launch_bounds__(STEP_BLOCK) step_scan_kernel(uint64_t* q, const double* x, const double* w,
+                                                              int64_t P, const uint64_t* boff, const double* sum1,
+                                                              const int* flags, double* mpart, unsigned* cnt,
+                                                              double* sum2, int finalize, double* est, double* L,
+                                                              int* flags_w) {
+  scan_block(blockIdx.x, q, x, w, P, boff, sum1, flags, mpart);
+  if (!last_block(cnt)) return;
+  scan_final(gridDim.x, mpart, sum2, finalize, sum1, est, L, flags_w);
 }
 
 __global__ void step_finalize_kernel(const double* sum1, const double* sum2, double* est, double* L, int* flags) {
@@ -350,24 +413,42 @@ __global__ void step_finalize_kernel(const double* sum1, const double* sum2, dou
 // ---------------------------------------------------------------------------- K_anc (+ gather)
 // Local output slot i (global slot g = slot_lo + i): t_g = floor((u + g 2^32) Q / (P_total 2^32));
 // ancestor = min{p : C_p > t_g - O_r}; out[i] = x[ancestor] (6 doubles; one thread per slot).
-__global__ void step_anc_kernel(const uint64_t* __restrict__ C, int64_t P_local, const uint64_t* __restrict__ Qtot,
-                                const uint64_t* __restrict__ offset, int64_t slot_lo, int64_t n, int64_t P_total,
-                                uint32_t u_bits, const double* __restrict__ x, double* __restrict__ out, int* flags) {
-  const uint64_t Q = *Qtot;
-  const uint64_t O = offset ? *offset : 0ull;
+// Two-level search when the rank has at most ANC_SMEM blocks: the block ends E_b = boff[b + 1] (boff[nb] = this
+// rank's total) in shared memory give the block holding the ancestor (C is non-decreasing, so it is the first block
+// whose last C exceeds t), then 9 steps inside its STEP_ITEMS entries -- instead of 17 dependent L2 loads.
+constexpr int ANC_SMEM = 2048;
+__device__ void anc_range(int64_t i0, int64_t stride, const uint64_t* C, const uint64_t* boff, int64_t nb,
+                          int64_t P_local, const uint64_t* Qtot, const uint64_t* offset, int64_t slot_lo, int64_t n,
+                          int64_t P_total, uint32_t u_bits, const double* x, double* out, int* flags) {
+  __shared__ uint64_t sE[ANC_SMEM];
+  const bool two = nb <= ANC_SMEM;
+  if (two)
+    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) sE[b] = __ldcg(&boff[b + 1]);
+  __syncthreads();
+  const uint64_t Q = __ldcg(Qtot);
+  const uint64_t O = offset ? __ldcg(offset) : 0ull;
   if (Q == 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, FLAG_ZEROMASS);
+    if (i0 == 0) atomicOr(flags, FLAG_ZEROMASS);
     return;
   }
   const unsigned __int128 den = (unsigned __int128)(uint64_t)P_total << 32;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = i0; i < n; i += stride) {
     const uint64_t g = (uint64_t)(slot_lo + i);
     const unsigned __int128 num = ((unsigned __int128)u_bits + ((unsigned __int128)g << 32)) * Q;
     const uint64_t t = (uint64_t)(num / den) - O;
     int64_t lo = 0, hi = P_local - 1;  // smallest p with C[p] > t
+    if (two) {
+      int64_t bl = 0, bh = nb - 1;  // smallest block b with E_b > t
+      while (bl < bh) {
+        const int64_t mid = (bl + bh) >> 1;
+        if (sE[mid] > t) bh = mid; else bl = mid + 1;
+      }
+      lo = bl * STEP_ITEMS;
+      hi = min(P_local, lo + STEP_ITEMS) - 1;
+    }
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if (C[mid] > t) hi = mid; else lo = mid + 1;
+      if (__ldcg(&C[mid]) > t) hi = mid; else lo = mid + 1;
     }
     const double2* src = reinterpret_cast<const double2*>(x + lo * 6);
     double2* dst = reinterpret_cast<double2*>(out + i * 6);
@@ -375,6 +456,12 @@ __global__ void step_anc_kernel(const uint64_t* __restrict__ C, int64_t P_local,
     dst[1] = src[1];
     dst[2] = src[2];
   }
+}
+__global__ void step_anc_kernel(const uint64_t* C, const uint64_t* boff, int64_t nb, int64_t P_local,
+                                const uint64_t* Qtot, const uint64_t* offset, int64_t slot_lo, int64_t n,
+                                int64_t P_total, uint32_t u_bits, const double* x, double* out, int* flags) {
+  anc_range((int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, C, boff, nb, P_local,
+            Qtot, offset, slot_lo, n, P_total, u_bits, x, out, flags);
 }
 
 // ---------------------------------------------------------------------------- K_reg
@@ -395,15 +482,15 @@ __device__ __forceinline__ void normals4_step(uint64_t key, uint64_t step, uint6
 }
 
 // out[p] = in[p] + h L n_p (regularize) or in[p]; in may equal out
-__global__ void step_reg_kernel(const double* in, double* out, int64_t P, int64_t p0, double h,
-                                const double* __restrict__ Lg, int regularize, uint64_t key, uint64_t step) {
+__device__ void reg_range(int64_t i0, int64_t stride, const double* in, double* out, int64_t P, int64_t p0, double h,
+                          const double* Lg, int regularize, uint64_t key, uint64_t step) {
   __shared__ double L[36];
-  if (threadIdx.x < 36) L[threadIdx.x] = regularize ? Lg[threadIdx.x] : 0.0;
+  if (threadIdx.x < 36) L[threadIdx.x] = regularize ? __ldcg(&Lg[threadIdx.x]) : 0.0;
   __syncthreads();
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t p = i0; p < P; p += stride) {
     double s[6];
 #pragma unroll
-    for (int a = 0; a < 6; ++a) s[a] = in[p * 6 + a];
+    for (int a = 0; a < 6; ++a) s[a] = __ldcg(&in[p * 6 + a]);
     if (regularize) {
       double n[8];
       normals4_step(key, step, (uint64_t)(p0 + p), 1u, n);
@@ -419,6 +506,40 @@ __global__ void step_reg_kernel(const double* in, double* out, int64_t P, int64_
 #pragma unroll
     for (int a = 0; a < 6; ++a) out[p * 6 + a] = s[a];
   }
+}
+__global__ void step_reg_kernel(const double* in, double* out, int64_t P, int64_t p0, double h, const double* Lg,
+                                int regularize, uint64_t key, uint64_t step) {
+  reg_range((int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, in, out, P, p0, h, Lg,
+            regularize, key, step);
+}
+
+// ---------------------------------------------------------------------------- fused single-rank pipeline
+// All five phases in one cooperative launch (no communicator): the per-block bodies over virtual blocks, block 0
+// runs each cross-block epilogue between grid barriers.  Tried because the kernels above are latency-bound
+// (196-391 blocks, 17-30% warps active, 8-17 us each at P = 1e5); measured not faster (c2 step 0.409 vs 0.403 ms:
+// 7 grid barriers and the serial epilogues cost what the launches did), so it is an A/B option (CDMS_STEP_FUSED=1),
+// tested bit-identical to the separate kernels.
+__global__ void __launch_bounds__(STEP_BLOCK) step_fused_kernel(StepFusedArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t nb = (a.P + STEP_ITEMS - 1) / STEP_ITEMS;  // step_blocks(P)
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t vb = blockIdx.x; vb < nb; vb += gridDim.x) lse_block(vb, a.l, a.P, a.lpart);
+  grid.sync();
+  if (blockIdx.x == 0) lse_final(nb, a.lpart, a.rank_pair, 1, a.lse, a.M, a.logS, a.flags);
+  grid.sync();
+  for (int64_t vb = blockIdx.x; vb < nb; vb += gridDim.x)
+    post_block(vb, a.l, a.x, a.P, a.M, a.logS, a.flags, a.w, a.q, a.mpart, a.bsum);
+  grid.sync();
+  if (blockIdx.x == 0) post_final(nb, a.mpart, a.bsum, a.sums);
+  grid.sync();
+  for (int64_t vb = blockIdx.x; vb < nb; vb += gridDim.x)
+    scan_block(vb, a.q, a.x, a.w, a.P, a.bsum, a.sums, a.flags, a.mpart);
+  grid.sync();
+  if (blockIdx.x == 0) scan_final(nb, a.mpart, a.sums + 8, 1, a.sums, a.est, a.L, a.flags);
+  grid.sync();
+  anc_range(i0, stride, a.q, a.bsum, nb, a.P, a.bsum + nb, nullptr, 0, a.P, a.P, a.u_bits, a.x, a.stage, a.flags);
+  grid.sync();
+  reg_range(i0, stride, a.stage, a.x, a.P, 0, a.h, a.L, a.regularize, a.key, a.step);
 }
 
 // ---------------------------------------------------------------------------- launchers
@@ -460,21 +581,38 @@ cudaError_t launch_step_finalize(const double* sum1, const double* sum2, double*
   step_finalize_kernel<<<1, 32, 0, st>>>(sum1, sum2, est, L, flags);
   return cudaGetLastError();
 }
-cudaError_t launch_step_anc(const uint64_t* C, int64_t P_local, const uint64_t* Qtot, const uint64_t* offset,
-                            int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits, const double* x,
-                            double* out, int* flags, cudaStream_t st) {
+cudaError_t launch_step_anc(const uint64_t* C, const uint64_t* boff, int64_t P_local, const uint64_t* Qtot,
+                            const uint64_t* offset, int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits,
+                            const double* x, double* out, int* flags, cudaStream_t st) {
   const int64_t n = slot_hi - slot_lo;
   if (n <= 0) return cudaSuccess;
-  step_anc_kernel<<<grid_cap(n, 256), 256, 0, st>>>(C, P_local, Qtot, offset, slot_lo, n, P_total, u_bits, x, out,
-                                                   flags);
+  step_anc_kernel<<<grid_cap(n, 256), 256, 0, st>>>(C, boff, step_blocks(P_local), P_local, Qtot, offset, slot_lo, n,
+                                                   P_total, u_bits, x, out, flags);
   return cudaGetLastError();
 }
 cudaError_t launch_step_reg(const double* in, double* out, int64_t P, int64_t p0, int64_t P_total, const double* L,
                             int regularize, uint64_t key, uint64_t step, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
-  const double h = pow(4.0 / (8.0 * (double)P_total), 1.0 / 10.0);  // h_opt, d = 6 (C-amb-16)
+  const double h = step_reg_bandwidth(P_total);  // h_opt, d = 6 (C-amb-16)
   step_reg_kernel<<<grid_cap(P, 256), 256, 0, st>>>(in, out, P, p0, h, L, regularize, key, step);
   return cudaGetLastError();
 }
+
+cudaError_t launch_step_fused(const StepFusedArgs& a, int num_sms, cudaStream_t st) {
+  if (a.P <= 0) return cudaSuccess;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel, STEP_BLOCK, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  // enough blocks for one pass of the per-particle phases, never more than can be co-resident
+  int64_t g = (a.P + STEP_BLOCK - 1) / STEP_BLOCK;
+  const int64_t cap = (int64_t)per_sm * num_sms;
+  if (g > cap) g = cap;
+  StepFusedArgs args = a;
+  void* params[] = {&args};
+  e = cudaLaunchCooperativeKernel((const void*)step_fused_kernel, dim3((unsigned)g), dim3(STEP_BLOCK), params, 0, st);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+double step_reg_bandwidth(int64_t P_total) { return pow(4.0 / (8.0 * (double)P_total), 1.0 / 10.0); }
 
 }  // namespace cdms

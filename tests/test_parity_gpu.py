@@ -398,6 +398,33 @@ def test_bp_step_fp32_runs_and_is_consistent(cd, ctx, orc):
     assert np.all(np.isfinite(xg.cpu().numpy()))
 
 
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_bp_step_fused_matches_separate(cd, orc, name):
+    """The single-rank O(P) phases in one cooperative kernel (CDMS_STEP_FUSED=1, step_fused_kernel) run the same
+    per-block bodies and epilogues as the five separate kernels: particles, moments and lse bit-identical."""
+    import os
+    cfg = scenes.CONFIGS[name]
+    case = Case(orc, cfg, P=min(cfg.P, 20000))
+    ctxs = []
+    try:
+        for f in ("0", "1"):
+            os.environ["CDMS_STEP_FUSED"] = f
+            ctxs.append(cd.Context(0))
+    finally:
+        os.environ.pop("CDMS_STEP_FUSED", None)
+    outs = []
+    for c in ctxs:
+        xg = case.dx.clone()
+        est, lse = cd.bp_step(c, case.scene, xg, case.dsfv, case.dy, case.m, case.v, case.eta, 0.1, 0.5,
+                              case.sc.philox_key, 3)
+        c.sync()
+        outs.append((xg.cpu().numpy(), est.cpu().numpy(), lse.cpu().numpy()))
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    for c in ctxs:
+        c.close()
+
+
 @pytest.mark.parametrize("wf", ["spherical", "planar_nb"])
 def test_bp_step_graph_capture(cd, orc, wf):
     """The ABI's capture claim: after cdms_reserve, one single-rank cdms_bp_step recorded in a CUDA graph on the

@@ -32,11 +32,17 @@
  *    cdms_bp_step are COLLECTIVE over the ranks (every rank calls them, each with its P_local
  *    particles; global particle index = rank * P_local + local index, P_local equal on all ranks).
  *    cdms_loglik, cdms_response and cdms_layout are purely local.
- *  - Engines: spherical and planar-WB likelihoods (and every FP64 evaluation) run on the FP32/FP64 pipes
- *    (segmented Horner correlation); PLANAR_NB in FP32 runs its correlation on the tensor cores
- *    (tcgen05, error-free fp16 split) with a closed-form Gram.  Environment knobs read
- *    at cdms_create / per call, for A/B measurements only: CDMS_NB_TENSOR=0 keeps PLANAR_NB on the FP32 pipe,
- *    CDMS_NB_ATMEM=0 keeps the tensor path's A operand in shared memory.
+ *  - Engines: FP32 spherical and planar-WB likelihoods evaluate the correlation from per-call spectral Taylor
+ *    tables of the snapshot (K1T; tables in the context workspace, (G + 1) N_a 64 bytes per
+ *    PA, G = 4 N_f, up to 96 MB, else K1) and the Gram in closed form; FP64 evaluations run the segmented Horner
+ *    correlation (K1); PLANAR_NB in FP32 runs its correlation on the tensor cores (tcgen05, error-free fp16
+ *    split) with a closed-form Gram.  All engines meet the same parity tolerances.
+ *    Environment knobs read at cdms_create, for A/B measurements only: CDMS_TAYLOR=0 (K1 instead of K1T),
+ *    CDMS_TAYLOR_GRAM=k1 (K1T's off-diagonal Gram from K1's Horner-free variant), CDMS_TAY_LANES=0/1 (force
+ *    K1T's thread-per-particle / lane-group kernel; default by P J), CDMS_TAY_PREP=direct (direct-sum tables
+ *    instead of the FFT), CDMS_STEP_FUSED=1 (single-rank bp_step O(P) phases in one cooperative kernel; results
+ *    identical), CDMS_NB_TENSOR=0 keeps PLANAR_NB on the FP32 pipe, CDMS_NB_ATMEM=0 keeps the tensor path's A
+ *    operand in shared memory.
  */
 #ifndef CDMS_H_
 #define CDMS_H_

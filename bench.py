@@ -328,7 +328,9 @@ def run_cdms(args):
                             "is the direct correlation's 8 N_z per (particle, PA, component)",
                     "traffic": (traffic_from_profiles(args.config + "_k1t") if args.particles is None else None),
                     "traffic_basis": "dram read+write bytes of one K1T correlation launch, ncu --set full "
-                                     "(profiles/loglik_traffic.json)"}
+                                     "(profiles/loglik_traffic.json)",
+                    "issue": (k1t_issue(args.config, kernel_ms * launches_per_step, clocks.get("sm_mhz"))
+                              if args.particles is None and args.wavefront == "spherical" else None)}
         else:
             roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
@@ -371,6 +373,27 @@ def traffic_from_profiles(config: str):
         return None if rec is None else rec["dram_bytes_per_launch"]
     except Exception:
         return None
+
+
+def k1t_issue(config: str, stage_ms: float, sm_mhz):
+    """The K1T stage's own efficiency: warp instructions of its correlation + Gram launches per step (committed ncu
+    capture, tools/ncu_inst.py) over the live-timed stage against the SM issue peak (148 SMs x 4 schedulers x 1
+    warp-instruction / clk), or None when no capture of this config exists."""
+    p = os.path.join(ROOT, "profiles", "k1t_stage_inst.json")
+    try:
+        with open(p) as f:
+            rec = json.load(f).get(config)
+    except Exception:
+        return None
+    if rec is None or not stage_ms:
+        return None
+    inst = sum(v for k, v in rec["kernels"].items() if k.startswith(("tay_corr", "tay_gram")))
+    mhz = sm_mhz or 1965.0
+    peak = 148 * 4 * mhz * 1e6
+    return {"warp_inst_per_step": inst, "stage_ms": round(stage_ms, 4), "peak_warp_inst_per_s": peak,
+            "issue_frac": round(inst / (stage_ms * 1e-3) / peak, 4),
+            "basis": f"smsp__inst_executed.sum of tay_corr* + tay_gram* ({rec['source']}) / live stage time / "
+                     f"(148 SM x 4 issue slots x {mhz:.0f} MHz)"}
 
 
 def oracle_inputs(cfg, sc, orc_mod, n_particles):

@@ -743,7 +743,8 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
 #pragma unroll
     for (int r = 0; r < S; ++r)
 #pragma unroll
-      for (int q = 0; q <= r; ++q) {
+      for (int q = 0; q < S; ++q) {  // constant trip counts throughout: the loops unroll, k stays in registers
+        if (q > r) continue;
         const double f = sv[r] * sv[q] / eta;
         const double2 G = k[tri(r, q)];
         k[tri(r, q)] = make_double2((r == q ? 1.0 : 0.0) + G.x * f, G.y * f);
@@ -754,17 +755,20 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
     for (int q = 0; q < S; ++q) {
       double d = k[tri(q, q)].x;
 #pragma unroll
-      for (int t = 0; t < q; ++t) d -= k[tri(q, t)].x * k[tri(q, t)].x + k[tri(q, t)].y * k[tri(q, t)].y;
+      for (int t = 0; t < S; ++t)
+        if (t < q) d -= k[tri(q, t)].x * k[tri(q, t)].x + k[tri(q, t)].y * k[tri(q, t)].y;
       okc &= d > 0.0;
       const double lqq = sqrt(fmax(d, 1e-300));
       logdet += 2.0 * log(lqq);
       k[tri(q, q)] = make_double2(lqq, 0.0);
       const double inv = 1.0 / lqq;
 #pragma unroll
-      for (int i = q + 1; i < S; ++i) {
+      for (int i = 0; i < S; ++i) {
+        if (i <= q) continue;
         double2 ac = k[tri(i, q)];
 #pragma unroll
-        for (int t = 0; t < q; ++t) {
+        for (int t = 0; t < S; ++t) {
+          if (t >= q) continue;
           const double2 li = k[tri(i, t)], lk = k[tri(q, t)];
           ac.x -= li.x * lk.x + li.y * lk.y;  // ac -= L_it conj(L_qt)
           ac.y -= li.y * lk.x - li.x * lk.y;
@@ -778,7 +782,8 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
     for (int r = 0; r < S; ++r) {
       double2 t = b[r];
 #pragma unroll
-      for (int q = 0; q < r; ++q) {
+      for (int q = 0; q < S; ++q) {
+        if (q >= r) continue;
         const double2 lr = k[tri(r, q)];
         t.x -= lr.x * b[q].x - lr.y * b[q].y;
         t.y -= lr.x * b[q].y + lr.y * b[q].x;
@@ -796,7 +801,8 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
       for (int r = S - 1; r >= 0; --r) {
         double2 t = b[r];
 #pragma unroll
-        for (int q = r + 1; q < S; ++q) {
+        for (int q = 0; q < S; ++q) {
+          if (q <= r) continue;
           const double2 lk = k[tri(q, r)];  // (L^H)_rq = conj(L_qr)
           t.x -= lk.x * b[q].x + lk.y * b[q].y;
           t.y -= lk.x * b[q].y - lk.y * b[q].x;

@@ -595,8 +595,9 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
   const size_t smem = (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2);  // the larger part
   cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  // antennas over 4 lanes per particle when P J threads are fewer than ~2 resident waves
-  const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 2 : 0;
+  // antennas over 2 lanes per particle when P J threads are fewer than ~2 resident waves (measured at c2: 1 lane
+  // 0.391, 2 lanes 0.388, 4 lanes 0.405, 8 lanes 0.448 ms per step; at P = 1.4e5 2 lanes 0.494 vs 4 lanes 0.517)
+  const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 1 : 0;
   dim3 grid((unsigned)(((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK), sc.J, NPART);
   tay_gram_kernel<S><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit);
   return cudaGetLastError();

@@ -52,7 +52,7 @@ def measured_tensor_peak():
 
 def k1t_kernels(cfg, P: int) -> str:
     """The K1T stage's kernels as libcdms picks them (taylor.cu tay_lanes, cdms.cpp engine selection)."""
-    c = ("cdms::tay_corr_lanes_kernel" if P * cfg.J < 148 * 1024 else "cdms::tay_corr_kernel") + " (K1T, c)"
+    c = ("cdms::tay_corr_lanes_kernel" if P * cfg.J < 250000 else "cdms::tay_corr_kernel") + " (K1T, c)"
     g = "tay_gram_kernel<S> (G)"
     return c + " + " + g
 
@@ -591,7 +591,7 @@ def run_birth(args):
                     else "fp32 fma", "achieved": round(ach, 3), "peak": round(peak, 2),
                     "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                     "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
-                    "kernel": (("cdms::tay_corr_lanes_kernel" if (N_g // 8) * cfg.J < 148 * 1024
+                    "kernel": (("cdms::tay_corr_lanes_kernel" if (N_g // 8) * cfg.J < 250000
                                 else "cdms::tay_corr_kernel") + " (K1T, F3 correlations of the candidate walls, 8 "
                                "candidates per pseudo-particle)" if taylor_path(args)
                                else "cdms::corr_kernel (F3 correlations of the candidate walls)")}

@@ -615,12 +615,12 @@ cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double
   }
 }
 
-// Layout / kernel choice (measured, profiles/r01_k1t_lanes.txt, CDMS_TAY_LANES=0/1 A/B): with P J below one
-// resident wave of the thread-per-particle kernel (148 SMs x ~1024 threads) it is latency-bound on its uncoalesced
-// row gathers and the lane-group kernel with the [g][h][m] table wins (c2, P = 1e5: 0.496 vs 0.58 ms/step); from
-// P J = 2e5 on the thread kernel wins (c2 at 2e5 / 4e5 / 8e5: 0.80 / 1.29 / 2.30 vs 0.82 / 1.41 / 2.61 ms; c4
-// 10.3 vs 11.3).  Decided once per loglik call (from its particle count) for the table build and every batch.
-bool tay_lanes(const SceneDev& sc, int64_t P) { return (double)P * sc.J < 148.0 * 1024; }
+// Layout / kernel choice (measured, profiles/r01_k1t_lanes.txt, CDMS_TAY_LANES=0/1 A/B): at small P J the
+// thread-per-particle kernel is latency-bound on its uncoalesced row gathers and the lane-group kernel with the
+// [g][h][m] table wins; with enough particles the thread kernel hides them and wins (c2 scene, ms per step, thread
+// vs lanes: P = 1e5 0.58 vs 0.50 (v22), 2e5 0.701 vs 0.660, 3e5 0.896 vs 0.925, 4e5 1.167 vs 1.183 (v55); c4 8.36
+// vs 9.02).  Decided once per loglik call (from its particle count) for the table build and every batch.
+bool tay_lanes(const SceneDev& sc, int64_t P) { return (double)P * sc.J < 2.5e5; }
 // FFT when G is a power of two in [64, 4096] (N_f a power of two up to 1024), unless direct = 1 (A/B); else the
 // direct sum.  Both fp64, rounded once to complex64.
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, int direct, cudaStream_t st) {

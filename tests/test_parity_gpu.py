@@ -230,10 +230,10 @@ def test_loglik_near_truth_worst_case(cd, ctx, orc, name, wf):
     check_loglik(case, ctx, "fp32", idx=np.arange(8))
 
 
-@pytest.mark.parametrize("P", [4096, 200_000])
+@pytest.mark.parametrize("P", [4096, 300_000])
 def test_taylor_layouts_near_truth(cd, ctx, orc, P):
     """K1T picks its table layout and correlation kernel from P J (taylor.cu tay_lanes: lane groups with the
-    [g][h][m] table below ~152k, one thread per particle with the [m][g][l] table above); both at the near-truth
+    [g][h][m] table below 250k, one thread per particle with the [m][g][l] table above); both at the near-truth
     worst case, plus a stratified sample."""
     import dataclasses
     cfg = dataclasses.replace(scenes.CONFIGS["c2"], P=P)  # c2's scene, P particles

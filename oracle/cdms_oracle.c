@@ -432,24 +432,17 @@ int orc_moments(const double* x /*[P][6]*/, const double* w, int64_t P, double* 
 }
 
 /* Systematic resampling [Arulampalam et al., Alg. 2] on integer quantities (C-amb-15):
- * q_p = rint(ldexp(w_p / w_max, 36)), C_p = sum_{p' <= p} q_p', Q = C_{P-1},
- * t_i = floor((u + i 2^32) Q / (P 2^32)), ancestor a_i = min{p : C_p > t_i}.
- * Textbook serial sweep: the pointer p advances while C_p <= t_i. */
-int orc_resample(const double* w, int64_t P, uint32_t u_bits, int64_t* anc) {
-  if (P <= 0 || P > ((int64_t)1 << 26)) return ORC_EINVAL;
-  double wmax = 0.0;
-  for (int64_t p = 0; p < P; ++p) {
-    if (!(w[p] >= 0.0)) return ORC_EINVAL;
-    if (w[p] > wmax) wmax = w[p];
-  }
-  if (!(wmax > 0.0)) return ORC_EZEROMASS;
+ * given the masses q_p, C_p = sum_{p' <= p} q_p', Q = C_{P-1}, t_i = floor((u + i 2^32) Q / (P 2^32)),
+ * ancestor a_i = min{p : C_p > t_i}.  Textbook serial sweep: the pointer p advances while C_p <= t_i. */
+static int orc_systematic_sweep(const uint64_t* q, int64_t P, uint32_t u_bits, int64_t* anc) {
   uint64_t* C = (uint64_t*)malloc(sizeof(uint64_t) * P);
   uint64_t run = 0;
   for (int64_t p = 0; p < P; ++p) {
-    run += (uint64_t)rint(ldexp(w[p] / wmax, 36));
+    run += q[p];
     C[p] = run;
   }
   uint64_t Q = run;
+  if (Q == 0) { free(C); return ORC_EZEROMASS; }
   unsigned __int128 den = (unsigned __int128)P << 32;
   int64_t ptr = 0;
   for (int64_t i = 0; i < P; ++i) {
@@ -460,6 +453,41 @@ int orc_resample(const double* w, int64_t P, uint32_t u_bits, int64_t* anc) {
   }
   free(C);
   return ORC_OK;
+}
+
+/* Resampling of normalized weights w (cdms_resample): q_p = rint(ldexp(w_p / w_max, 36)). */
+int orc_resample(const double* w, int64_t P, uint32_t u_bits, int64_t* anc) {
+  if (P <= 0 || P > ((int64_t)1 << 26)) return ORC_EINVAL;
+  double wmax = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    if (!(w[p] >= 0.0)) return ORC_EINVAL;
+    if (w[p] > wmax) wmax = w[p];
+  }
+  if (!(wmax > 0.0)) return ORC_EZEROMASS;
+  uint64_t* q = (uint64_t*)malloc(sizeof(uint64_t) * P);
+  for (int64_t p = 0; p < P; ++p) q[p] = (uint64_t)rint(ldexp(w[p] / wmax, 36));
+  int st = orc_systematic_sweep(q, P, u_bits, anc);
+  free(q);
+  return st;
+}
+
+/* Resampling of the BP step from the log-weights l (reading C-amb-23): the same sweep on
+ * q_p = rint(ldexp(r_p, 36)), r_p = e^{l_p - M}, M = max_p l_p.  r_p equals w_p / w_max of the
+ * normalized weights w_p = e^{l_p - lse} in exact arithmetic (w_max = e^{M - lse}), and r_p depends only
+ * on l_p and M, so it is the quantity a sharded implementation can form per particle. */
+int orc_resample_loglik(const double* l, int64_t P, uint32_t u_bits, int64_t* anc) {
+  if (P <= 0 || P > ((int64_t)1 << 26)) return ORC_EINVAL;
+  double M = -INFINITY;
+  for (int64_t p = 0; p < P; ++p) {
+    if (l[p] != l[p]) return ORC_EINVAL;
+    if (l[p] > M) M = l[p];
+  }
+  if (M == -INFINITY) return ORC_EZEROMASS;
+  uint64_t* q = (uint64_t*)malloc(sizeof(uint64_t) * P);
+  for (int64_t p = 0; p < P; ++p) q[p] = (uint64_t)rint(ldexp(exp(l[p] - M), 36));
+  int st = orc_systematic_sweep(q, P, u_bits, anc);
+  free(q);
+  return st;
 }
 
 /* ------------------------------------------------------------------ RNG + BP step (A9) */
@@ -559,9 +587,31 @@ void orc_regularize(double* x, int64_t P, int64_t p0, int64_t P_total, const dou
   }
 }
 
+/* The MT belief update that follows the likelihood (the BP step from w~_x on): normalize the log-weights l
+ * (P:L3409-3410), MMSE moments of the weighted set, systematic resampling of the masses
+ * e^{l - M} (orc_resample_loglik, u = orc_step_u_bits), gather of the ancestors' states, and regularization
+ * with the covariance of the weighted (pre-resampling) set.
+ * particles [P][6] in/out; est [28]; lse; ancestors [P] out (may be NULL). */
+int orc_step_update(const double* l, double* particles, int64_t P, uint64_t key, uint64_t step, int regularize,
+                    double* est, double* lse, int64_t* ancestors) {
+  double* w = (double*)malloc(sizeof(double) * P);
+  int64_t* a = (int64_t*)malloc(sizeof(int64_t) * P);
+  double* tmp = (double*)malloc(sizeof(double) * P * 6);
+  int st = orc_normalize(l, P, w, lse);
+  if (st == ORC_OK) st = orc_moments(particles, w, P, est);
+  if (st == ORC_OK) st = orc_resample_loglik(l, P, orc_step_u_bits(key, step), a);
+  if (st == ORC_OK) {
+    for (int64_t i = 0; i < P; ++i) memcpy(tmp + i * 6, particles + a[i] * 6, sizeof(double) * 6);
+    memcpy(particles, tmp, sizeof(double) * P * 6);
+    if (ancestors) memcpy(ancestors, a, sizeof(int64_t) * P);
+    if (regularize) orc_regularize(particles, P, 0, P, est + 7, key, step);
+  }
+  free(w); free(a); free(tmp);
+  return st;
+}
+
 /* One MT BP time step (message schedule P:L2494-2508 restricted to the MT belief):
- * predict -> loglik (log w_beta uniform, dropped) -> normalize -> moments -> systematic resampling
- * (u = orc_step_u_bits) -> gather -> regularize with the pre-resampling covariance.
+ * predict -> loglik with uniform w_beta (dropped) -> orc_step_update.
  * particles [P][6] in/out; est [28]; lse; ancestors [P] out (may be NULL). */
 int orc_bp_step(const orc_scene* sc, double* particles, int64_t P, const double* sfv,
                 const double complex* y, const double complex* m, const double* v,
@@ -569,20 +619,10 @@ int orc_bp_step(const orc_scene* sc, double* particles, int64_t P, const double*
                 int regularize, double* est, double* lse, int64_t* ancestors) {
   orc_predict(particles, P, 0, T, sigma_v, key, step);
   double* l = (double*)malloc(sizeof(double) * P);
-  double* w = (double*)malloc(sizeof(double) * P);
-  int64_t* a = (int64_t*)malloc(sizeof(int64_t) * P);
-  double* tmp = (double*)malloc(sizeof(double) * P * 6);
   int st = orc_loglik(sc, particles, P, 6, sfv, 0, y, m, v, eta, NULL, l, NULL);
-  if (st == ORC_OK || st == ORC_EDEGENERATE) st = orc_normalize(l, P, w, lse);
-  if (st == ORC_OK) st = orc_moments(particles, w, P, est);
-  if (st == ORC_OK) st = orc_resample(w, P, orc_step_u_bits(key, step), a);
-  if (st == ORC_OK) {
-    for (int64_t i = 0; i < P; ++i) memcpy(tmp + i * 6, particles + a[i] * 6, sizeof(double) * 6);
-    memcpy(particles, tmp, sizeof(double) * P * 6);
-    if (ancestors) memcpy(ancestors, a, sizeof(int64_t) * P);
-    if (regularize) orc_regularize(particles, P, 0, P, est + 7, key, step);
-  }
-  free(l); free(w); free(a); free(tmp);
+  if (st == ORC_OK || st == ORC_EDEGENERATE) st = orc_step_update(l, particles, P, key, step, regularize, est, lse,
+                                                                   ancestors);
+  free(l);
   return st;
 }
 

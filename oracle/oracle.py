@@ -231,6 +231,28 @@ def resample(w, u_bits):
     return st, anc
 
 
+def resample_loglik(l, u_bits):
+    """Systematic resampling of the masses e^{l - max l} (the BP step's quantization, C-amb-23)."""
+    l = _f64(l)
+    anc = np.zeros(l.shape[0], dtype=np.int64)
+    st = lib().orc_resample_loglik(_d(l), C.c_int64(l.shape[0]), C.c_uint32(u_bits), anc.ctypes.data_as(C.c_void_p))
+    return st, anc
+
+
+def step_update(l, particles, key, step, regularize=True):
+    """The belief update after the likelihood (normalize, moments, resample, gather, regularize):
+    (status, particles out, est [28], lse, ancestors)."""
+    l = _f64(l)
+    x = _f64(particles).copy()
+    P = x.shape[0]
+    est = np.zeros(28)
+    lse = np.zeros(1)
+    anc = np.zeros(P, dtype=np.int64)
+    st = lib().orc_step_update(_d(l), _d(x), C.c_int64(P), C.c_uint64(key), C.c_uint64(step), int(bool(regularize)),
+                               _d(est), _d(lse), anc.ctypes.data_as(C.c_void_p))
+    return st, x, est, float(lse[0]), anc
+
+
 def philox(ctr, key):
     c = (C.c_uint32 * 4)(*[int(x) & 0xFFFFFFFF for x in ctr])
     k = (C.c_uint32 * 2)(*[int(x) & 0xFFFFFFFF for x in key])

@@ -179,3 +179,89 @@ def test_moment_match_enumeration(orc):
         var = second - abs(mean) ** 2
         m, v = orc.moment_match(mu, gamma, eps * zeta)
         assert abs(m - mean) < 1e-15 and abs(v - var) < 1e-14
+
+
+# ---------------------------------------------------------------- A8 in the BP step: masses e^{l - M} (C-amb-23)
+def test_resample_loglik_hand_trace(orc):
+    """S:L414's trace with the weights given as log-weights: l = ln w (+ an offset that makes M != 0)."""
+    g = json.load(open(os.path.join(GOLDEN, "resampling_hand_trace.json")))
+    for case in g["cases"]:
+        l = np.full(case["P_out"], -np.inf)
+        l[:3] = np.log(case["w"]) - 4321.0
+        st, anc = orc.resample_loglik(l, case["u_bits"])
+        assert st == 0
+        assert list(counts(anc, 10)[:3]) == case["counts"]
+
+
+def test_resample_loglik_equals_resample_of_exp(orc):
+    """r_p = e^{l_p - M} has max exactly e^0 = 1, so orc_resample (w / w_max, pinned above) applied to the vector r
+    (formed here with the C library's exp through math.exp) must give the same ancestors bit for bit."""
+    rng = np.random.default_rng(9)
+    for trial in range(30):
+        P = int(rng.integers(1, 3000))
+        l = rng.normal(-2e4, 40.0, P)
+        l[rng.uniform(size=P) < 0.1] = -np.inf
+        if not np.isfinite(l).any():
+            l[0] = 0.0
+        M = np.max(l)
+        r = np.array([math.exp(v - M) if np.isfinite(v) else 0.0 for v in l])
+        u = int(rng.integers(0, 2**32))
+        st1, a1 = orc.resample_loglik(l, u)
+        st2, a2 = orc.resample(r, u)
+        assert st1 == 0 and st2 == 0
+        assert np.array_equal(a1, a2)
+
+
+def test_resample_loglik_bounds_and_errors(orc):
+    rng = np.random.default_rng(10)
+    P = 511
+    for _ in range(20):
+        l = rng.normal(0, 3, P)
+        st, anc = orc.resample_loglik(l, int(rng.integers(0, 2**32)))
+        q = np.exp(l - l.max())
+        q /= q.sum()
+        c = counts(anc, P)
+        assert np.all(c >= np.floor(P * q) - 1) and np.all(c <= np.ceil(P * q) + 1)   # quantization: +-1 slack
+        assert np.all(np.diff(anc) >= 0)
+    assert orc.resample_loglik(np.full(4, -np.inf), 1)[0] == orc.EZEROMASS
+    assert orc.resample_loglik(np.array([0.0, np.nan]), 1)[0] == orc.EINVAL
+
+
+def test_step_update_composition(orc):
+    """orc_step_update follows the paper's order: normalize -> MMSE moments of the weighted set
+     -> systematic resampling with u of the step -> gather -> regularization with the
+    pre-resampling covariance.  Composed here from the separately pinned oracle pieces."""
+    rng = np.random.default_rng(12)
+    P = 777
+    x = rng.normal(size=(P, 6))
+    l = rng.normal(-5e3, 2.0, P)
+    key, step = 0xABCDEF12345, 4
+    st, xo, est, lse, anc = orc.step_update(l, x, key, step)
+    assert st == 0
+    st, w, lse_ref = orc.normalize(l)
+    st, est_ref = orc.moments(x, w)
+    st, a_ref = orc.resample_loglik(l, orc.step_u_bits(key, step))
+    xr = orc.regularize(x[a_ref], 0, P, est_ref[7:], key, step)
+    assert lse == lse_ref and np.array_equal(est, est_ref) and np.array_equal(anc, a_ref)
+    assert np.array_equal(xo, xr)
+    st, xo2, _, _, _ = orc.step_update(l, x, key, step, regularize=False)
+    assert np.array_equal(xo2, x[a_ref])
+
+
+def test_bp_step_is_predict_loglik_update(orc):
+    """orc_bp_step = predict (P:L3236-3243) -> l (P:L3385-3390) -> orc_step_update."""
+    from paper_2604_19723_b200 import scenes
+    from tests.helpers import small_cfg
+    cfg = small_cfg(J=1, K=1, ny=2, nv=2, nf=8, P=200)
+    sc = scenes.make_scene(cfg)
+    o = orc.Oracle.from_scene(sc)
+    y, eta = orc.measurement(o, sc, scenes.P_TRUE)
+    m, v = scenes.priors(sc, "nzm")
+    eta = np.full(cfg.J, eta)
+    x = scenes.make_particles(cfg)
+    st, xb, estb, lseb, ancb = o.bp_step(x, sc.sfv, y, m, v, eta, 0.1, 0.5, 77, 3)
+    assert st == 0
+    xp = orc.predict(x, 0, 0.1, 0.5, 77, 3)
+    st, l = o.loglik(xp, sc.sfv, y, m, v, eta)
+    st, xu, estu, lseu, ancu = orc.step_update(l, xp, 77, 3)
+    assert np.array_equal(xb, xu) and np.array_equal(estb, estu) and lseb == lseu and np.array_equal(ancb, ancu)

@@ -11,10 +11,11 @@
  *    call (the library copies what it keeps).  Arrays are dense, row-major, no padding.
  *  - complex64 = interleaved (re, im) float32 pairs; complex128 = interleaved float64 pairs.
  *  - Every device operation is enqueued on the context's stream; nothing synchronizes the host
- *    except cdms_sync() and, with nranks > 1 only, one stream synchronization inside cdms_resample and
- *    cdms_bp_step (the host builds the rank-to-rank exchange plan from the all-gathered masses).
- *    Single-rank calls are capturable into a CUDA graph once their workspaces exist (first call
- *    outside capture, or cdms_reserve()).
+ *    except cdms_sync() (and the test-only loopback backend's host barriers).  With several ranks the
+ *    distributed resampling plan is formed on the device from the all-gathered masses and the
+ *    redistribution is fused into the ancestor gather (each slot's state is written into its owner
+ *    rank's buffer over NVLink peer memory), so calls are capturable into a CUDA graph once their
+ *    workspaces exist (first call outside capture, or cdms_reserve(), collective with a communicator).
  *  - Concurrency: a context is one in-order worker -- its workspaces (including the device-side
  *    work-claim counters of the likelihood kernel and the step pipeline, which the last CTA of each
  *    launch resets) are shared by its calls, so calls on one context must not overlap on different
@@ -54,6 +55,7 @@ extern "C" {
 #endif
 
 typedef struct cdms_ctx_s* cdms_ctx;
+typedef struct cdms_loopback_s* cdms_loopback;
 
 typedef enum {
   CDMS_OK = 0,
@@ -126,6 +128,15 @@ cdms_status cdms_timing_read(cdms_ctx ctx, double* loglik_ms, int64_t* n_launche
 cdms_status cdms_get_unique_id(unsigned char nccl_unique_id_out[128]);
 cdms_status cdms_comm_init(cdms_ctx ctx, const unsigned char nccl_unique_id[128], int rank,
                            int nranks);
+
+/* TEST backend for the multi-rank path on one GPU: nranks contexts of ONE process, each driven by its
+ * own host thread, form a group whose collectives are host barriers plus device copies (instead of NCCL) and whose
+ * peer buffers are the other contexts' device buffers.  Every collective entry point (cdms_weights_normalize,
+ * cdms_moments, cdms_resample, cdms_bp_step, cdms_bp_update, cdms_reserve) then runs exactly the device code of the
+ * NCCL path.  The group must outlive its contexts; a context takes either NCCL or a loopback group, once. */
+cdms_status cdms_loopback_create(int nranks, cdms_loopback* out);
+cdms_status cdms_loopback_destroy(cdms_loopback group);
+cdms_status cdms_comm_init_loopback(cdms_ctx ctx, cdms_loopback group, int rank);
 
 /* ---- row A1: anchor geometry ----------------------------------------------------------------- */
 
@@ -244,6 +255,17 @@ cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_partic
                          int64_t P_local, const double* d_sfv, const void* d_y,
                          const double* h_f_pb, const cdms_prior* h_prior, const double* h_eta,
                          const cdms_step_params* params, double* d_est, double* d_lse);
+
+/* Rows A6-A9 on given log-weights: the part of cdms_bp_step after the likelihood (P:L3409-3410, P:L2367-2371,
+ * P:L3446) with the same kernels -- normalize d_loglik [P_local] (log w~_x, any finite offset), MMSE
+ * moments of the weighted particles (d_est out [28]), lse (d_lse out [1]), systematic resampling of the masses
+ * e^{l - M} (C-amb-23) with u = first word of Philox(key, (0, 0, step, 3)), the ancestors' states written back into
+ * d_particles [P_local][6] (in/out) so that every rank again holds P_local particles, and (prm->regularize) the
+ * regularization x += h_opt chol(Sigma) n.  d_ancestors out [P_local] int64 (GLOBAL ancestor index of each of this
+ * rank's output slots) or NULL.  prm->T and prm->sigma_v are not used (no prediction).  Collective with a
+ * communicator.  Errors as cdms_bp_step (all l = -inf: CDMS_EZEROMASS at sync, particles untouched). */
+cdms_status cdms_bp_update(cdms_ctx ctx, const double* d_loglik, double* d_particles, int64_t P_local,
+                           const cdms_step_params* params, double* d_est, double* d_lse, int64_t* d_ancestors);
 
 /* ---- test / helper entries ------------------------------------------------------------------- */
 

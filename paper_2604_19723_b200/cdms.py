@@ -77,6 +77,10 @@ def lib() -> C.CDLL:
             "cdms_bp_step": ([vp, C.POINTER(SceneC), vp, i64, vp, vp, dp, C.POINTER(PriorC), dp,
                               C.POINTER(StepParamsC), vp, vp], C.c_int),
             "cdms_response": ([vp, C.POINTER(SceneC), vp, i64, vp, vp, vp], C.c_int),
+            "cdms_bp_update": ([vp, vp, vp, i64, C.POINTER(StepParamsC), vp, vp, vp], C.c_int),
+            "cdms_loopback_create": ([C.c_int, C.POINTER(vp)], C.c_int),
+            "cdms_loopback_destroy": ([vp], C.c_int),
+            "cdms_comm_init_loopback": ([vp, vp, C.c_int], C.c_int),
             "cdms_birth_proposal": ([vp, C.POINTER(SceneC), dp, dp, dp, i32, vp, dp, i64, C.c_uint64, C.c_uint64,
                                      vp, vp, vp], C.c_int),
             "cdms_moment_match": ([C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(PriorC)], C.c_int),
@@ -96,7 +100,9 @@ def exported_symbols() -> list[str]:
                         "cdms_reserve", "cdms_launch_count", "cdms_timing_enable", "cdms_timing_read",
                         "cdms_get_unique_id", "cdms_comm_init", "cdms_layout",
                         "cdms_loglik", "cdms_loglik_terms", "cdms_weights_normalize", "cdms_moments", "cdms_resample", "cdms_bp_step",
-                        "cdms_response", "cdms_moment_match", "cdms_resample_plan", "cdms_birth_proposal"]]
+                        "cdms_response", "cdms_moment_match", "cdms_resample_plan", "cdms_birth_proposal",
+                        "cdms_bp_update", "cdms_loopback_create", "cdms_loopback_destroy",
+                        "cdms_comm_init_loopback"]]
 
 
 def _ptr(t) -> Optional[int]:
@@ -203,6 +209,12 @@ class Context:
     def reserve(self, scene: Scene, P_local: int):
         self.check(lib().cdms_reserve(self.h, C.byref(scene.c), int(P_local)))
 
+    def comm_init_loopback(self, group: "LoopbackGroup", rank: int):
+        """Attach the TEST collective backend (cdms_comm_init_loopback): this context becomes rank `rank` of a group of
+        contexts in this process; drive each rank's collective calls from its own thread."""
+        self.check(lib().cdms_comm_init_loopback(self.h, group.h, int(rank)))
+        self.rank, self.nranks = int(rank), group.nranks
+
     def comm_init_from_torch(self, rank: int, world: int):
         """NCCL bootstrap: rank 0 creates the unique id, torch.distributed broadcasts it."""
         import torch.distributed as dist
@@ -215,6 +227,22 @@ class Context:
         raw = bytes(t.cpu().tolist())
         self.check(lib().cdms_comm_init(self.h, raw, rank, world))
         self.rank, self.nranks = rank, world
+
+
+class LoopbackGroup:
+    """cdms_loopback: the test-only collective backend of nranks contexts in one process (include/cdms.h)."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        st = lib().cdms_loopback_create(int(nranks), C.byref(h))
+        if st != OK:
+            raise CdmsError(st, "cdms_loopback_create")
+        self.h, self.nranks = h, int(nranks)
+
+    def close(self):
+        if self.h:
+            lib().cdms_loopback_destroy(self.h)
+            self.h = None
 
 
 # ---------------------------------------------------------------------------- entry points
@@ -314,6 +342,21 @@ def bp_step(ctx: Context, scene: Scene, particles, sfv, y, prior_m, prior_v, eta
                                  _dp(np.ascontiguousarray(eta, dtype=np.float64).reshape(-1)), C.byref(prm),
                                  _ptr(est), _ptr(lse)))
     return est, lse
+
+
+def bp_update(ctx: Context, loglik, particles, philox_key: int, step: int, regularize: bool = True, est=None,
+              lse=None, want_ancestors: bool = False):
+    """Rows A6-A9 on given log-weights (cdms_bp_update): particles [P][6] updated in place; returns (est, lse,
+    ancestors or None)."""
+    torch = ctx.torch
+    dev = particles.device
+    est = est if est is not None else torch.empty(28, dtype=torch.float64, device=dev)
+    lse = lse if lse is not None else torch.empty(1, dtype=torch.float64, device=dev)
+    anc = torch.empty(particles.shape[0], dtype=torch.int64, device=dev) if want_ancestors else None
+    prm = StepParamsC(0.0, 0.0, int(philox_key), int(step), int(bool(regularize)), 0)
+    ctx.check(lib().cdms_bp_update(ctx.h, _ptr(loglik), _ptr(particles), int(particles.shape[0]), C.byref(prm),
+                                   _ptr(est), _ptr(lse), _ptr(anc)))
+    return est, lse, anc
 
 
 def response(ctx: Context, scene: Scene, pos, js, sfv):

@@ -306,13 +306,14 @@ __global__ void scan_add_kernel(uint64_t* __restrict__ q, int64_t P, const uint6
   }
 }
 
-// For local output slot i (global slot g = slot_lo + i): t_g = floor((u + g 2^32) Q / (P_total 2^32)),
-// ancestor = min{p : C_p > t_g - O_r} (binary search in this rank's inclusive scan C).
-__global__ void ancestors_kernel(const uint64_t* __restrict__ C, int64_t P_local, const uint64_t* __restrict__ Qtot,
-                                 const uint64_t* __restrict__ offset, int64_t slot_lo, int64_t n, int64_t P_total,
-                                 uint32_t u_bits, int64_t p_global0, int64_t* __restrict__ anc, int* flags) {
-  const uint64_t Q = *Qtot;
-  const uint64_t O = offset ? *offset : 0ull;
+// Output slot g of this rank's range [slot_lo, slot_hi) (plan on the device): t_g = floor((u + g 2^32) Q /
+// (P_total 2^32)), ancestor = min{p : C_p > t_g - O_r} (binary search in this rank's inclusive scan C), written to
+// row g mod P_local of the slot owner's ancestor buffer peer_anc[g / P_local].
+__global__ void ancestors_kernel(const uint64_t* __restrict__ C, int64_t P_local, const uint64_t* __restrict__ plan,
+                                 int64_t P_total, uint32_t u_bits, int64_t p_global0, int64_t* own_anc,
+                                 int64_t* const* peer_anc, int* flags) {
+  const uint64_t Q = plan[0], O = plan[1];
+  const int64_t slot_lo = (int64_t)plan[2], n = (int64_t)plan[3] - slot_lo;
   if (Q == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, FLAG_ZEROMASS);
     return;
@@ -327,8 +328,23 @@ __global__ void ancestors_kernel(const uint64_t* __restrict__ C, int64_t P_local
       const int64_t mid = (lo + hi) >> 1;
       if (C[mid] > t) hi = mid; else lo = mid + 1;
     }
-    anc[i] = p_global0 + lo;
+    const int64_t own = (int64_t)(g / (uint64_t)P_local);
+    (peer_anc ? peer_anc[own] : own_anc)[(int64_t)g - own * P_local] = p_global0 + lo;
   }
+  __threadfence_system();
+}
+
+// out[n] = sum over ranks r (in rank order) of in[r][n]: deterministic combine of all-gathered per-rank sums
+__global__ void sum_ranks_kernel(const double* __restrict__ in, int nranks, int n, double* __restrict__ out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += in[(int64_t)r * n + i];
+    out[i] = s;
+  }
+}
+cudaError_t launch_sum_ranks(const double* in, int nranks, int n, double* out, cudaStream_t st) {
+  sum_ranks_kernel<<<1, 64, 0, st>>>(in, nranks, n, out);
+  return cudaGetLastError();
 }
 
 // out[i] = x[anc[i] - p_global0] (6 doubles per particle)
@@ -359,13 +375,11 @@ cudaError_t launch_scan(uint64_t* q, int64_t P, uint64_t* block_sums, cudaStream
   scan_add_kernel<<<(unsigned)nb, RED_BLOCK, 0, st>>>(q, P, block_sums);
   return cudaGetLastError();
 }
-cudaError_t launch_ancestors(const uint64_t* C, int64_t P_local, const uint64_t* Qtot, const uint64_t* offset,
-                             int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits, int64_t p_global0,
-                             int64_t* anc_out, int* flags, cudaStream_t st) {
-  const int64_t n = slot_hi - slot_lo;
-  if (n <= 0) return cudaSuccess;
-  ancestors_kernel<<<grid_for(n, 256), 256, 0, st>>>(C, P_local, Qtot, offset, slot_lo, n, P_total, u_bits, p_global0,
-                                                    anc_out, flags);
+cudaError_t launch_ancestors(const uint64_t* C, int64_t P_local, const uint64_t* plan, int64_t P_total, uint32_t u_bits,
+                             int64_t p_global0, int64_t* own_anc, int64_t* const* peer_anc, int* flags,
+                             cudaStream_t st) {
+  ancestors_kernel<<<grid_for(P_local, 256), 256, 0, st>>>(C, P_local, plan, P_total, u_bits, p_global0, own_anc,
+                                                          peer_anc, flags);
   return cudaGetLastError();
 }
 cudaError_t launch_gather(const double* x, const int64_t* anc, int64_t n, int64_t p_global0, double* out,

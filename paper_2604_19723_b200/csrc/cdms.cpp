@@ -10,6 +10,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -17,14 +19,27 @@
 
 using namespace cdms;
 
+namespace {
+struct Coll;
+}
+
 struct cdms_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   std::string err;
   int* d_flags = nullptr;
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;     // NCCL backend (owned by the NcclColl in coll)
+  Coll* coll = nullptr;           // collective backend once a communicator is attached (NCCL or test loopback)
   int rank = 0, nranks = 1;
+  // peer-writable redistribution buffers (multi-rank): this rank's stage [pcap][6] f64 and ancestor ids [pcap] i64,
+  // and device arrays of every rank's buffers as addressable from this device (d_peer_x[r], d_peer_anc[r])
+  double* pstage = nullptr;
+  int64_t* panc = nullptr;
+  int64_t pcap = 0;
+  double** d_peer_x = nullptr;
+  int64_t** d_peer_anc = nullptr;
+  int* d_barrier = nullptr;
   int64_t launches = 0;
   std::vector<void*> bufs;
   std::vector<size_t> sizes;
@@ -51,7 +66,7 @@ enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
   WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
   WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BC, WS_BLL, WS_BPB,
-  WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_COUNT
+  WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_GPART, WS_PLAN, WS_RANKS, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -239,159 +254,177 @@ uint32_t host_step_u_bits(uint64_t key, uint64_t step) {
   return c0;
 }
 
-// I(x) = #{i in [0, P_total) : t_i < x}, t_i = floor((u + i 2^32) Q / (P_total 2^32)) (exact, 128-bit)
-int64_t slot_index(uint64_t x, uint64_t Q, int64_t P_total, uint32_t u) {
-  typedef unsigned __int128 u128;
-  const u128 lhs = (u128)x * (u128)(uint64_t)P_total << 32;
-  const u128 uq = (u128)u * Q;
-  if (lhs <= uq) return 0;
-  const u128 A = lhs - uq;
-  const u128 step = (u128)Q << 32;
-  u128 I = (A + step - 1) / step;
-  if (I > (u128)(uint64_t)P_total) I = (u128)(uint64_t)P_total;
-  return (int64_t)I;
-}
-
-// ---------------------------------------------------------------------------- internal pipelines
-cdms_status run_lse(cdms_ctx ctx, const double* d_l, int64_t P, double* d_lse) {
-  const int64_t nb = red_blocks(P);
-  double2 *part, *per_rank;
-  double* scal;
-  WS_TRY(ctx, WS_LSE_PART, nb + 1, &part);
-  WS_TRY(ctx, WS_LSE_RANK, ctx->nranks + 1, &per_rank);
-  WS_TRY(ctx, WS_SCAL, 8, &scal);
-  CUDA_TRY(ctx, launch_lse_partial(d_l, P, part, ctx->stream));
-  if (ctx->comm) {
-    CUDA_TRY(ctx, launch_lse_final(part, nb, part + nb, ctx->stream));
-    NCCL_TRY(ctx, ncclAllGather(part + nb, per_rank, 2, ncclDouble, ctx->comm, ctx->stream));
-  } else {
-    CUDA_TRY(ctx, launch_lse_final(part, nb, per_rank, ctx->stream));
-  }
-  CUDA_TRY(ctx, launch_lse_combine(per_rank, ctx->nranks, d_lse, scal + 0, scal + 1, ctx->d_flags, ctx->stream));
-  ctx->launches += 3;
-  return CDMS_OK;
-}
-
-cdms_status run_moments(cdms_ctx ctx, const double* d_x, const double* d_w, int64_t P, double* d_est) {
-  const int64_t nb = red_blocks(P);
-  double *part, *sums;
-  WS_TRY(ctx, WS_MOM_PART, (nb + 1) * 21, &part);
-  WS_TRY(ctx, WS_SUMS, 32, &sums);
-  CUDA_TRY(ctx, launch_moments1(d_x, d_w, P, part, ctx->stream));
-  CUDA_TRY(ctx, launch_sum_partials(part, nb, 7, sums, ctx->stream));
-  if (ctx->comm) NCCL_TRY(ctx, ncclAllReduce(sums, sums, 7, ncclDouble, ncclSum, ctx->comm, ctx->stream));
-  CUDA_TRY(ctx, launch_moments2(d_x, d_w, P, sums, part, ctx->stream));
-  CUDA_TRY(ctx, launch_sum_partials(part, nb, 21, sums + 8, ctx->stream));
-  if (ctx->comm)
-    NCCL_TRY(ctx, ncclAllReduce(sums + 8, sums + 8, 21, ncclDouble, ncclSum, ctx->comm, ctx->stream));
-  CUDA_TRY(ctx, launch_moments_finalize(sums, sums + 8, d_est, ctx->d_flags, ctx->stream));
-  ctx->launches += 5;
-  return CDMS_OK;
-}
-
-// Quantize + scan + ancestors for this rank's CDF range.  from_loglik: r_p = e^{l_p - M} (M = global max,
-// in WS_SCAL[0]); else r_p = w_p / w_max (global).  Results: the global ancestor ids of the slots
-// [slot_lo, slot_hi) that this rank's CDF range covers, in *d_anc_out (WS_ANC), plus the plan.
-struct Plan {
-  int64_t lo = 0, hi = 0;
-  std::vector<int64_t> lo_all, hi_all;
+// ---------------------------------------------------------------------------- collective backends
+// Everything that crosses ranks goes through one of these (multi-GPU semantics):
+//  allgather  every rank contributes `bytes` of device data, recv gets all ranks' contributions rank-major;
+//  barrier    stream-ordered: work enqueued before it on every rank (including writes into peers' buffers) is
+//             complete and visible to work enqueued after it on any rank;
+//  register   make this rank's peer-writable buffers addressable from every rank (collective; fills the ctx's
+//             d_peer_x / d_peer_anc arrays).
+// NcclColl is the product backend (one process per GPU; NCCL all-gathers over NVLink / NVSwitch, CUDA IPC for the
+// peer buffers).  LoopbackColl is the TEST backend behind cdms_loopback_*: several contexts of one process (one
+// thread each, any number on one GPU) exchange through host barriers and device copies, so the multi-rank device
+// path runs on a single GPU without ranks whose kernels wait on each other.
+struct Coll {
+  virtual ~Coll() {}
+  virtual cdms_status allgather(cdms_ctx ctx, const void* send, void* recv, size_t bytes) = 0;
+  virtual cdms_status barrier(cdms_ctx ctx) = 0;
+  virtual cdms_status register_peers(cdms_ctx ctx) = 0;
 };
 
-cdms_status run_resample_core(cdms_ctx ctx, const double* d_in, int64_t P_local, uint32_t u_bits, int from_loglik,
-                              Plan* plan, int64_t** d_anc_out) {
-  const int64_t nb = red_blocks(P_local);
-  const int64_t P_total = P_local * ctx->nranks;
-  if (P_total > ((int64_t)1 << 26)) return fail(ctx, CDMS_EINVAL, "P_total=%lld exceeds 2^26", (long long)P_total);
-  uint64_t *q, *bsum, *qall;
-  double *scal, *wpart;
-  int64_t* anc;
-  WS_TRY(ctx, WS_Q, P_local, &q);
-  WS_TRY(ctx, WS_BSUM, nb + 2, &bsum);
-  WS_TRY(ctx, WS_QALL, 2 * ctx->nranks + 4, &qall);
-  WS_TRY(ctx, WS_SCAL, 8, &scal);
-  if (!from_loglik) {
-    WS_TRY(ctx, WS_WMAX_PART, nb + 1, &wpart);
-    CUDA_TRY(ctx, launch_wmax_partial_f(d_in, P_local, wpart, ctx->d_flags, ctx->stream));
-    CUDA_TRY(ctx, launch_max_final(wpart, nb, scal + 2, ctx->stream));
-    if (ctx->comm)
-      NCCL_TRY(ctx, ncclAllReduce(scal + 2, scal + 2, 1, ncclDouble, ncclMax, ctx->comm, ctx->stream));
-    ctx->launches += 2;
+cdms_status fail(cdms_ctx ctx, cdms_status st, const char* fmt, ...);
+
+struct NcclColl : Coll {
+  std::vector<void*> opened;  // IPC-mapped peer buffers to close
+  cdms_status allgather(cdms_ctx ctx, const void* send, void* recv, size_t bytes) override {
+    ncclResult_t r = ncclAllGather(send, recv, bytes, ncclChar, ctx->comm, ctx->stream);
+    return r == ncclSuccess ? CDMS_OK : fail(ctx, CDMS_ENCCL, "ncclAllGather: %s", ncclGetErrorString(r));
   }
-  CUDA_TRY(ctx, launch_quantize(d_in, P_local, scal + 2, scal + 0, from_loglik, q, ctx->d_flags, ctx->stream));
-  CUDA_TRY(ctx, launch_scan(q, P_local, bsum, ctx->stream));
-  ctx->launches += 4;
-  if (!(ctx->comm)) {
-    WS_TRY(ctx, WS_ANC, P_local, &anc);
-    CUDA_TRY(ctx, launch_ancestors(q, P_local, bsum + nb, nullptr, 0, P_local, P_local, u_bits, 0, anc, ctx->d_flags,
-                                   ctx->stream));
-    ctx->launches += 1;
-    plan->lo = 0;
-    plan->hi = P_local;
-    plan->lo_all.assign(1, 0);
-    plan->hi_all.assign(1, P_local);
-    *d_anc_out = anc;
+  cdms_status barrier(cdms_ctx ctx) override {
+    // a 4-byte all-reduce: it completes on a rank only after every rank's stream reached it, i.e. after their
+    // preceding kernels (whose peer stores end with __threadfence_system) completed
+    ncclResult_t r = ncclAllReduce(ctx->d_barrier, ctx->d_barrier, 1, ncclInt32, ncclSum, ctx->comm, ctx->stream);
+    return r == ncclSuccess ? CDMS_OK : fail(ctx, CDMS_ENCCL, "barrier ncclAllReduce: %s", ncclGetErrorString(r));
+  }
+  cdms_status register_peers(cdms_ctx ctx) override {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    opened.clear();
+    const int R = ctx->nranks;
+    cudaIpcMemHandle_t h[2];
+    cudaError_t e = cudaIpcGetMemHandle(&h[0], ctx->pstage);
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[1], ctx->panc);
+    if (e != cudaSuccess) return fail(ctx, CDMS_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    char *dsend = nullptr, *drecv = nullptr;
+    std::vector<char> hall((size_t)R * sizeof(h));
+    e = cudaMalloc(&dsend, sizeof(h) * (R + 1));
+    if (e != cudaSuccess) return fail(ctx, CDMS_ENOMEM, "register_peers: %s", cudaGetErrorString(e));
+    drecv = dsend + sizeof(h);
+    cdms_status st = CDMS_OK;
+    if (cudaMemcpyAsync(dsend, h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        ncclAllGather(dsend, drecv, sizeof(h), ncclChar, ctx->comm, ctx->stream) != ncclSuccess ||
+        cudaMemcpyAsync(hall.data(), drecv, hall.size(), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      st = fail(ctx, CDMS_ENCCL, "register_peers: handle exchange failed");
+    cudaFree(dsend);
+    if (st) return st;
+    std::vector<double*> px(R);
+    std::vector<int64_t*> pa(R);
+    for (int r = 0; r < R; ++r) {
+      if (r == ctx->rank) {
+        px[r] = ctx->pstage;
+        pa[r] = ctx->panc;
+        continue;
+      }
+      cudaIpcMemHandle_t hr[2];
+      memcpy(hr, hall.data() + (size_t)r * sizeof(h), sizeof(h));
+      void *a = nullptr, *b = nullptr;
+      e = cudaIpcOpenMemHandle(&a, hr[0], cudaIpcMemLazyEnablePeerAccess);
+      if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&b, hr[1], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return fail(ctx, CDMS_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+      opened.push_back(a);
+      opened.push_back(b);
+      px[r] = static_cast<double*>(a);
+      pa[r] = static_cast<int64_t*>(b);
+    }
+    if (cudaMemcpy(ctx->d_peer_x, px.data(), sizeof(double*) * R, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->d_peer_anc, pa.data(), sizeof(int64_t*) * R, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(ctx, CDMS_ECUDA, "register_peers: pointer upload failed");
+    return barrier(ctx);
+  }
+  ~NcclColl() override {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+  }
+};
+
+}  // namespace
+struct cdms_loopback_s {
+  int nranks;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> send;
+  std::vector<double*> stage;
+  std::vector<int64_t*> anc;
+  explicit cdms_loopback_s(int n) : nranks(n), send(n), stage(n), anc(n) {}
+  void host_barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+namespace {
+
+struct LoopbackColl : Coll {
+  cdms_loopback_s* g;
+  explicit LoopbackColl(cdms_loopback_s* grp) : g(grp) {}
+  cdms_status allgather(cdms_ctx ctx, const void* send, void* recv, size_t bytes) override {
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return fail(ctx, CDMS_ECUDA, "loopback: sync");
+    g->send[ctx->rank] = send;
+    g->host_barrier();
+    for (int r = 0; r < g->nranks; ++r)
+      if (cudaMemcpyAsync(static_cast<char*>(recv) + (size_t)r * bytes, g->send[r], bytes, cudaMemcpyDeviceToDevice,
+                          ctx->stream) != cudaSuccess)
+        return fail(ctx, CDMS_ECUDA, "loopback: copy");
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return fail(ctx, CDMS_ECUDA, "loopback: sync");
+    g->host_barrier();  // nobody reuses its send buffer before every rank has copied it
     return CDMS_OK;
   }
-  // multi-rank: all-gather Q_r, host plan (one small D2H + stream sync per step)
-  NCCL_TRY(ctx, ncclAllGather(bsum + nb, qall, 1, ncclUint64, ctx->comm, ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_pinned, qall, sizeof(uint64_t) * ctx->nranks, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  std::vector<uint64_t> Q(ctx->h_pinned, ctx->h_pinned + ctx->nranks);
-  uint64_t Qtot = 0;
-  for (uint64_t v : Q) Qtot += v;
-  if (Qtot == 0) return fail(ctx, CDMS_EZEROMASS, "all resampling weights are zero");
-  plan->lo_all.resize(ctx->nranks);
-  plan->hi_all.resize(ctx->nranks);
-  uint64_t O = 0, Omine = 0;
-  for (int r = 0; r < ctx->nranks; ++r) {
-    plan->lo_all[r] = slot_index(O, Qtot, P_total, u_bits);
-    plan->hi_all[r] = slot_index(O + Q[r], Qtot, P_total, u_bits);
-    if (r == ctx->rank) Omine = O;
-    O += Q[r];
+  cdms_status barrier(cdms_ctx ctx) override {
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return fail(ctx, CDMS_ECUDA, "loopback: sync");
+    g->host_barrier();
+    return CDMS_OK;
   }
-  plan->lo = plan->lo_all[ctx->rank];
-  plan->hi = plan->hi_all[ctx->rank];
-  ctx->h_pinned[ctx->nranks] = Qtot;
-  ctx->h_pinned[ctx->nranks + 1] = Omine;
-  CUDA_TRY(ctx, cudaMemcpyAsync(qall + ctx->nranks, ctx->h_pinned + ctx->nranks, 2 * sizeof(uint64_t),
-                                cudaMemcpyHostToDevice, ctx->stream));
-  const int64_t n = plan->hi - plan->lo;
-  WS_TRY(ctx, WS_ANC, n > 0 ? n : 1, &anc);
-  CUDA_TRY(ctx, launch_ancestors(q, P_local, qall + ctx->nranks, qall + ctx->nranks + 1, plan->lo, plan->hi, P_total,
-                                 u_bits, (int64_t)ctx->rank * P_local, anc, ctx->d_flags, ctx->stream));
-  ctx->launches += 1;
-  *d_anc_out = anc;
-  return CDMS_OK;
+  cdms_status register_peers(cdms_ctx ctx) override {
+    g->stage[ctx->rank] = ctx->pstage;
+    g->anc[ctx->rank] = ctx->panc;
+    g->host_barrier();
+    if (cudaMemcpy(ctx->d_peer_x, g->stage.data(), sizeof(double*) * g->nranks, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->d_peer_anc, g->anc.data(), sizeof(int64_t*) * g->nranks, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(ctx, CDMS_ECUDA, "loopback: pointer upload");
+    g->host_barrier();
+    return CDMS_OK;
+  }
+};
+
+// This rank's peer-writable buffers for P_local particles (collective when they grow: every rank calls with the same
+// P_local, so all ranks re-register together).  Not capturable when it (re)allocates: cdms_reserve first.
+cdms_status ensure_peer(cdms_ctx ctx, int64_t P_local) {
+  if (ctx->pcap >= P_local && ctx->d_peer_x) return CDMS_OK;
+  if (ctx->pstage) cudaFree(ctx->pstage);
+  if (ctx->panc) cudaFree(ctx->panc);
+  ctx->pstage = nullptr;
+  ctx->panc = nullptr;
+  ctx->pcap = 0;
+  if (!ctx->d_peer_x) {
+    if (cudaMalloc(&ctx->d_peer_x, sizeof(double*) * ctx->nranks) != cudaSuccess ||
+        cudaMalloc(&ctx->d_peer_anc, sizeof(int64_t*) * ctx->nranks) != cudaSuccess ||
+        cudaMalloc(&ctx->d_barrier, 16) != cudaSuccess || cudaMemset(ctx->d_barrier, 0, 16) != cudaSuccess)
+      return fail(ctx, CDMS_ENOMEM, "peer pointer arrays");
+  }
+  if (cudaMalloc(&ctx->pstage, sizeof(double) * 6 * P_local) != cudaSuccess ||
+      cudaMalloc(&ctx->panc, sizeof(int64_t) * P_local) != cudaSuccess)
+    return fail(ctx, CDMS_ENOMEM, "peer buffers for %lld particles", (long long)P_local);
+  ctx->pcap = P_local;
+  return ctx->coll->register_peers(ctx);
 }
 
-// Redistribute `width` 8-byte words per slot from the staging rows of this rank's CDF slots
-// [plan.lo, plan.hi) to the owners of those slots (slot i lives on rank i / P_local, row i % P_local).
-cdms_status exchange(cdms_ctx ctx, const Plan& plan, int64_t P_local, const void* src, void* dst, int width) {
-  const int R = ctx->nranks;
-  const size_t row = (size_t)width * 8;
-  NCCL_TRY(ctx, ncclGroupStart());
-  for (int d = 0; d < R; ++d) {  // sends
-    const int64_t a = plan.lo > d * P_local ? plan.lo : d * P_local;
-    const int64_t b = plan.hi < (d + 1) * P_local ? plan.hi : (d + 1) * P_local;
-    if (b <= a || d == ctx->rank) continue;
-    NCCL_TRY(ctx, ncclSend((const char*)src + (size_t)(a - plan.lo) * row, (size_t)(b - a) * width, ncclUint64, d,
-                           ctx->comm, ctx->stream));
-  }
-  for (int s = 0; s < R; ++s) {  // receives
-    const int64_t a = plan.lo_all[s] > ctx->rank * P_local ? plan.lo_all[s] : ctx->rank * P_local;
-    const int64_t b = plan.hi_all[s] < (ctx->rank + 1) * P_local ? plan.hi_all[s] : (ctx->rank + 1) * P_local;
-    if (b <= a || s == ctx->rank) continue;
-    NCCL_TRY(ctx, ncclRecv((char*)dst + (size_t)(a - ctx->rank * P_local) * row, (size_t)(b - a) * width, ncclUint64, s,
-                           ctx->comm, ctx->stream));
-  }
-  NCCL_TRY(ctx, ncclGroupEnd());
-  const int64_t a = plan.lo > ctx->rank * P_local ? plan.lo : ctx->rank * P_local;
-  const int64_t b = plan.hi < (ctx->rank + 1) * P_local ? plan.hi : (ctx->rank + 1) * P_local;
-  if (b > a)
-    CUDA_TRY(ctx, cudaMemcpyAsync((char*)dst + (size_t)(a - ctx->rank * P_local) * row,
-                                  (const char*)src + (size_t)(a - plan.lo) * row, (size_t)(b - a) * row,
-                                  cudaMemcpyDeviceToDevice, ctx->stream));
-  return CDMS_OK;
+#define COLL_TRY(expr)              \
+  do {                              \
+    cdms_status s_ = (expr);        \
+    if (s_ != CDMS_OK) return s_;   \
+  } while (0)
+
+// K1T (taylor.cu) serves FP32 spherical / planar-WB likelihoods whose tables fit the budget
+bool tay_engine(cdms_ctx ctx, const SceneDev& sd, int precision, bool nb_tensor) {
+  return !nb_tensor && ctx->taylor && precision == CDMS_FP32 && sd.wavefront != CDMS_PLANAR_NB &&
+         tay_table_bytes(sd) <= ((size_t)96 << 20);
 }
 
 cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const double* d_particles, int64_t P,
@@ -416,8 +449,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   uint8_t* nbop = nullptr;
   float* nbscale = nullptr;
   // spherical / planar WB in FP32: c from spectral Taylor tables (K1T), G from K1's Horner-free variant
-  const bool tay = !nbt && ctx->taylor && precision == CDMS_FP32 && sd.wavefront != CDMS_PLANAR_NB &&
-                   tay_table_bytes(sd) <= ((size_t)96 << 20);
+  const bool tay = tay_engine(ctx, sd, precision, nbt);
   float2* taytab = nullptr;
   const int tlanes = tay && (ctx->taylor_lanes >= 0 ? ctx->taylor_lanes == 1 : tay_lanes(sd, P)) ? 1 : 0;  // taylor.cu
   if (tay) {
@@ -523,6 +555,165 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   return CDMS_OK;
 }
 
+// ---------------------------------------------------------------------------- standalone A6-A8 entries
+// (beliefs.cu kernels, RED_ITEMS partition).  Cross-rank combines are all-gathers followed by a fixed rank-order
+// combine on the device (deterministic for a given rank count).
+cdms_status run_lse(cdms_ctx ctx, const double* d_l, int64_t P, double* d_lse) {
+  const int64_t nb = red_blocks(P);
+  double2 *part, *per_rank;
+  double* scal;
+  WS_TRY(ctx, WS_LSE_PART, nb + 1, &part);
+  WS_TRY(ctx, WS_LSE_RANK, ctx->nranks + 1, &per_rank);
+  WS_TRY(ctx, WS_SCAL, 8, &scal);
+  CUDA_TRY(ctx, launch_lse_partial(d_l, P, part, ctx->stream));
+  if (ctx->coll) {
+    CUDA_TRY(ctx, launch_lse_final(part, nb, part + nb, ctx->stream));
+    COLL_TRY(ctx->coll->allgather(ctx, part + nb, per_rank, sizeof(double2)));
+  } else {
+    CUDA_TRY(ctx, launch_lse_final(part, nb, per_rank, ctx->stream));
+  }
+  CUDA_TRY(ctx, launch_lse_combine(per_rank, ctx->nranks, d_lse, scal + 0, scal + 1, ctx->d_flags, ctx->stream));
+  ctx->launches += 3;
+  return CDMS_OK;
+}
+
+cdms_status run_moments(cdms_ctx ctx, const double* d_x, const double* d_w, int64_t P, double* d_est) {
+  const int64_t nb = red_blocks(P);
+  double *part, *sums, *ranks;
+  WS_TRY(ctx, WS_MOM_PART, (nb + 1) * 21, &part);
+  WS_TRY(ctx, WS_SUMS, 32, &sums);
+  WS_TRY(ctx, WS_RANKS, (size_t)ctx->nranks * 21, &ranks);
+  CUDA_TRY(ctx, launch_moments1(d_x, d_w, P, part, ctx->stream));
+  CUDA_TRY(ctx, launch_sum_partials(part, nb, 7, sums, ctx->stream));
+  if (ctx->coll) {
+    COLL_TRY(ctx->coll->allgather(ctx, sums, ranks, 7 * sizeof(double)));
+    CUDA_TRY(ctx, launch_sum_ranks(ranks, ctx->nranks, 7, sums, ctx->stream));
+  }
+  CUDA_TRY(ctx, launch_moments2(d_x, d_w, P, sums, part, ctx->stream));
+  CUDA_TRY(ctx, launch_sum_partials(part, nb, 21, sums + 8, ctx->stream));
+  if (ctx->coll) {
+    COLL_TRY(ctx->coll->allgather(ctx, sums + 8, ranks, 21 * sizeof(double)));
+    CUDA_TRY(ctx, launch_sum_ranks(ranks, ctx->nranks, 21, sums + 8, ctx->stream));
+  }
+  CUDA_TRY(ctx, launch_moments_finalize(sums, sums + 8, d_est, ctx->d_flags, ctx->stream));
+  ctx->launches += ctx->coll ? 7 : 5;
+  return CDMS_OK;
+}
+
+// ---------------------------------------------------------------------------- rows A6-A9 after the likelihood
+// The belief update of cdms_bp_step / cdms_bp_update (step.cu): normalize, moments, systematic resampling of the masses
+// e^{l - M} (C-amb-23) with the gather of the ancestors' states, regularization.  One rank: the five step.cu kernels
+// with last-block epilogues.  Several ranks: the same per-block bodies; the block partials of every rank are
+// all-gathered and reduced in the single-rank order (bit-identical results for block-aligned shards); the resampling
+// plan is formed on the device from the all-gathered masses and K_anc writes each output slot's state straight into
+// the owner rank's stage buffer, then a barrier and the regularization from the own stage buffer.  No host
+// synchronization in either case.
+cdms_status bp_update_impl(cdms_ctx ctx, const double* l, double* x, int64_t P_local, const cdms_step_params* prm,
+                           double* d_est, double* d_lse, int64_t* d_anc) {
+  const bool comm = ctx->coll != nullptr;
+  const int R = ctx->nranks;
+  const int64_t P_total = P_local * R, p0 = (int64_t)ctx->rank * P_local;
+  const int64_t nb = step_blocks(P_local);
+  double2 *lpart, *pairs;
+  double *mpart, *sums, *w, *L6, *scal, *stage;
+  uint64_t *q, *bsum, *qall, *plan;
+  unsigned* cnt;
+  WS_TRY(ctx, WS_LSE_PART, nb + 1, &lpart);
+  WS_TRY(ctx, WS_LSE_RANK, R + 1, &pairs);
+  WS_TRY(ctx, WS_MOM_PART, (nb + 1) * 21, &mpart);
+  WS_TRY(ctx, WS_SUMS, 32, &sums);
+  WS_TRY(ctx, WS_Q, P_local, &q);
+  WS_TRY(ctx, WS_BSUM, nb + 2, &bsum);
+  WS_TRY(ctx, WS_QALL, 2 * R + 4, &qall);
+  WS_TRY(ctx, WS_PLAN, 8, &plan);
+  WS_TRY(ctx, WS_STEP_CNT, 4, &cnt);  // zeroed at allocation, reset by each kernel's last block
+  WS_TRY(ctx, WS_W, P_local, &w);
+  WS_TRY(ctx, WS_L6, 36, &L6);
+  WS_TRY(ctx, WS_SCAL, 8, &scal);
+  const uint32_t u_bits = host_step_u_bits(prm->philox_key, prm->step);
+  const int reg = prm->regularize ? 1 : 0;
+  if (!comm) {
+    WS_TRY(ctx, WS_STAGE, P_local * 6, &stage);
+    if (ctx->step_fused) {
+      // the five kernels' bodies in one cooperative launch (grid barriers instead of launches and last-block tails),
+      // identical arithmetic and block partition, so identical results
+      StepFusedArgs fa;
+      fa.l = l;
+      fa.x = x;
+      fa.P = P_local;
+      fa.lpart = lpart;
+      fa.rank_pair = pairs;
+      fa.lse = d_lse;
+      fa.M = scal + 0;
+      fa.logS = scal + 1;
+      fa.flags = ctx->d_flags;
+      fa.w = w;
+      fa.q = q;
+      fa.mpart = mpart;
+      fa.bsum = bsum;
+      fa.sums = sums;
+      fa.est = d_est;
+      fa.L = L6;
+      fa.stage = stage;
+      fa.anc = d_anc;
+      fa.plan = plan;
+      fa.u_bits = u_bits;
+      fa.h = step_reg_bandwidth(P_total);
+      fa.regularize = reg;
+      fa.key = prm->philox_key;
+      fa.step = prm->step;
+      CUDA_TRY(ctx, launch_step_fused(fa, ctx->num_sms, ctx->stream));
+      ctx->launches += 1;
+      return CDMS_OK;
+    }
+    CUDA_TRY(ctx, launch_step_lse(l, P_local, lpart, cnt + 0, pairs, 1, d_lse, scal + 0, scal + 1, ctx->d_flags,
+                                  ctx->stream));
+    CUDA_TRY(ctx, launch_step_post(l, x, P_local, scal + 0, scal + 1, ctx->d_flags, w, q, mpart, bsum, cnt + 1, sums,
+                                   u_bits, plan, ctx->stream));
+    CUDA_TRY(ctx, launch_step_scan(q, x, w, P_local, bsum, sums, ctx->d_flags, mpart, cnt + 2, sums + 8, 1, d_est, L6,
+                                   ctx->d_flags, ctx->stream));
+    CUDA_TRY(ctx, launch_step_anc(q, bsum, P_local, plan, P_local, u_bits, x, stage, d_anc, nullptr, nullptr, 0,
+                                  ctx->d_flags, ctx->stream));
+    // regularization with the pre-resampling covariance (A9), reading the staged states (no extra copy)
+    CUDA_TRY(ctx, launch_step_reg(stage, x, P_local, 0, P_total, L6, reg, prm->philox_key, prm->step, ctx->stream));
+    ctx->launches += 5;
+    return CDMS_OK;
+  }
+  cdms_status st = ensure_peer(ctx, P_local);
+  if (st) return st;
+  double* gpart;
+  WS_TRY(ctx, WS_GPART, (size_t)R * nb * 21, &gpart);
+  const int64_t nbt = (int64_t)R * nb;
+  // (A6) block partials of every rank -> M, ln S, lse in the single-rank combine order
+  CUDA_TRY(ctx, launch_step_lse(l, P_local, lpart, cnt + 0, nullptr, 0, nullptr, nullptr, nullptr, ctx->d_flags,
+                                ctx->stream));
+  COLL_TRY(ctx->coll->allgather(ctx, lpart, gpart, (size_t)nb * sizeof(double2)));
+  CUDA_TRY(ctx, launch_step_lse_global(reinterpret_cast<double2*>(gpart), nbt, pairs, d_lse, scal + 0, scal + 1,
+                                       ctx->d_flags, ctx->stream));
+  // (A7, A8) weights, masses e^{l - M}, first-moment partials, local scan of the block masses; then all ranks' first
+  // moments and this rank's resampling plan from the all-gathered Q_r
+  CUDA_TRY(ctx, launch_step_post(l, x, P_local, scal + 0, scal + 1, ctx->d_flags, w, q, mpart, bsum, cnt + 1, nullptr,
+                                 u_bits, nullptr, ctx->stream));
+  COLL_TRY(ctx->coll->allgather(ctx, mpart, gpart, (size_t)nb * 7 * sizeof(double)));
+  COLL_TRY(ctx->coll->allgather(ctx, bsum + nb, qall, sizeof(uint64_t)));
+  CUDA_TRY(ctx, launch_step_post_global(gpart, nbt, sums, qall, R, ctx->rank, P_total, u_bits, plan, ctx->stream));
+  // (A7) inclusive scan + second-moment partials; all ranks' covariance, est and its Cholesky factor
+  CUDA_TRY(ctx, launch_step_scan(q, x, w, P_local, bsum, sums, ctx->d_flags, mpart, cnt + 2, nullptr, 0, nullptr,
+                                 nullptr, ctx->d_flags, ctx->stream));
+  COLL_TRY(ctx->coll->allgather(ctx, mpart, gpart, (size_t)nb * 21 * sizeof(double)));
+  CUDA_TRY(ctx, launch_step_scan_global(gpart, nbt, sums, sums + 8, d_est, L6, ctx->d_flags, ctx->stream));
+  // (A8) ancestors of this rank's slots, states written into the owners' stage buffers; barrier; (A9) regularize
+  CUDA_TRY(ctx, launch_step_anc(q, bsum, P_local, plan, P_total, u_bits, x, nullptr, nullptr, ctx->d_peer_x,
+                                d_anc ? ctx->d_peer_anc : nullptr, p0, ctx->d_flags, ctx->stream));
+  COLL_TRY(ctx->coll->barrier(ctx));
+  CUDA_TRY(ctx, launch_step_reg(ctx->pstage, x, P_local, p0, P_total, L6, reg, prm->philox_key, prm->step,
+                                ctx->stream));
+  if (d_anc)
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_anc, ctx->panc, sizeof(int64_t) * P_local, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->launches += 8;
+  return CDMS_OK;
+}
+
 }  // namespace
 
 // ============================================================================ ABI
@@ -558,7 +749,13 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
 cdms_status cdms_destroy(cdms_ctx ctx) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  delete ctx->coll;  // closes IPC mappings of peers' buffers before the communicator goes
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->pstage) cudaFree(ctx->pstage);
+  if (ctx->panc) cudaFree(ctx->panc);
+  if (ctx->d_peer_x) cudaFree(ctx->d_peer_x);
+  if (ctx->d_peer_anc) cudaFree(ctx->d_peer_anc);
+  if (ctx->d_barrier) cudaFree(ctx->d_barrier);
   for (void* b : ctx->bufs)
     if (b) cudaFree(b);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -641,12 +838,24 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
     WS_TRY(ctx, WS_STEP_CNT, 4, &sch);
     WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &f4);
     NbPlan nbp{};  // the tensor-core path's per-PA B operand and scales (PLANAR_NB, FP32)
-    if (ctx->nb_tensor && scene->precision == CDMS_FP32 && nb_tensor_plan(sd, &nbp)) {
+    const bool nbt = ctx->nb_tensor && scene->precision == CDMS_FP32 && nb_tensor_plan(sd, &nbp);
+    if (nbt) {
       uint8_t* nbop;
       float* nbs;
       WS_TRY(ctx, WS_NBOP, nb_operand_bytes(sd, nbp), &nbop);
       WS_TRY(ctx, WS_NBSCALE, MAXJ, &nbs);
     }
+    if (tay_engine(ctx, sd, scene->precision, nbt)) {  // K1T's tables (the same choice loglik_impl makes)
+      float2* tab;
+      WS_TRY(ctx, WS_TAY, tay_table_bytes(sd) / sizeof(float2), &tab);
+    }
+  }
+  WS_TRY(ctx, WS_PLAN, 8, &u);
+  WS_TRY(ctx, WS_RANKS, (size_t)ctx->nranks * 21, &d);
+  if (ctx->coll) {
+    WS_TRY(ctx, WS_GPART, (size_t)ctx->nranks * step_blocks(P_local) * 21, &d);
+    cdms_status st2 = ensure_peer(ctx, P_local);  // collective with a communicator (all ranks reserve alike)
+    if (st2) return st2;
   }
   WS_TRY(ctx, WS_YNORM, MAXJ, &d);
   WS_TRY(ctx, WS_LSE_PART, nb + 1, &d2);
@@ -681,9 +890,33 @@ cdms_status cdms_comm_init(cdms_ctx ctx, const unsigned char id_in[128], int ran
   memcpy(id.internal, id_in, 128);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   ctx->comm = nullptr;
+  delete ctx->coll;
+  ctx->coll = nullptr;
   NCCL_TRY(ctx, ncclCommInitRank(&ctx->comm, nranks, id, rank));
   ctx->rank = rank;
   ctx->nranks = nranks;
+  ctx->coll = new NcclColl();
+  ctx->pcap = 0;  // peer buffers are (re)registered collectively on first use
+  return CDMS_OK;
+}
+
+cdms_status cdms_loopback_create(int nranks, cdms_loopback* out) {
+  if (!out || nranks < 1) return CDMS_EINVAL;
+  *out = new cdms_loopback_s(nranks);
+  return CDMS_OK;
+}
+cdms_status cdms_loopback_destroy(cdms_loopback g) {
+  if (!g) return CDMS_EINVAL;
+  delete g;
+  return CDMS_OK;
+}
+cdms_status cdms_comm_init_loopback(cdms_ctx ctx, cdms_loopback g, int rank) {
+  if (!ctx || !g || rank < 0 || rank >= g->nranks) return fail(ctx, CDMS_EINVAL, "comm_init_loopback: bad args");
+  if (ctx->comm || ctx->coll) return fail(ctx, CDMS_EINVAL, "comm_init_loopback: a communicator is attached");
+  ctx->rank = rank;
+  ctx->nranks = g->nranks;
+  ctx->coll = new LoopbackColl(g);
+  ctx->pcap = 0;
   return CDMS_OK;
 }
 
@@ -857,15 +1090,57 @@ cdms_status cdms_resample(cdms_ctx ctx, const double* d_w, int64_t P_local, uint
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
   if (!d_w || !d_ancestors || P_local <= 0) return fail(ctx, CDMS_EINVAL, "resample: bad arguments");
-  Plan plan;
-  int64_t* anc;
-  cdms_status st = run_resample_core(ctx, d_w, P_local, u_bits, 0, &plan, &anc);
-  if (st) return st;
-  if (!(ctx->comm)) {
-    CUDA_TRY(ctx, cudaMemcpyAsync(d_ancestors, anc, sizeof(int64_t) * P_local, cudaMemcpyDeviceToDevice, ctx->stream));
+  const int R = ctx->nranks;
+  const int64_t P_total = P_local * R;
+  if (P_total > ((int64_t)1 << 26)) return fail(ctx, CDMS_EINVAL, "P_total=%lld exceeds 2^26", (long long)P_total);
+  if (ctx->coll) {
+    cdms_status st = ensure_peer(ctx, P_local);
+    if (st) return st;
+  }
+  const int64_t nb = red_blocks(P_local);
+  uint64_t *q, *bsum, *qall, *plan;
+  double *scal, *wpart, *ranks;
+  WS_TRY(ctx, WS_Q, P_local, &q);
+  WS_TRY(ctx, WS_BSUM, nb + 2, &bsum);
+  WS_TRY(ctx, WS_QALL, 2 * R + 4, &qall);
+  WS_TRY(ctx, WS_PLAN, 8, &plan);
+  WS_TRY(ctx, WS_SCAL, 8, &scal);
+  WS_TRY(ctx, WS_WMAX_PART, nb + 1, &wpart);
+  WS_TRY(ctx, WS_RANKS, (size_t)R * 21, &ranks);
+  // q_p = rint(ldexp(w_p / w_max, 36)) with the global w_max (max is order-independent, hence exact)
+  CUDA_TRY(ctx, launch_wmax_partial_f(d_w, P_local, wpart, ctx->d_flags, ctx->stream));
+  CUDA_TRY(ctx, launch_max_final(wpart, nb, scal + 2, ctx->stream));
+  if (ctx->coll) {
+    COLL_TRY(ctx->coll->allgather(ctx, scal + 2, ranks, sizeof(double)));
+    CUDA_TRY(ctx, launch_max_final(ranks, R, scal + 2, ctx->stream));
+  }
+  CUDA_TRY(ctx, launch_quantize(d_w, P_local, scal + 2, scal + 0, 0, q, ctx->d_flags, ctx->stream));
+  CUDA_TRY(ctx, launch_scan(q, P_local, bsum, ctx->stream));  // bsum[nb] = Q_r
+  if (!ctx->coll) {
+    CUDA_TRY(ctx, launch_plan(bsum + nb, 1, 0, P_local, u_bits, plan, ctx->stream));
+    CUDA_TRY(ctx, launch_ancestors(q, P_local, plan, P_local, u_bits, 0, d_ancestors, nullptr, ctx->d_flags,
+                                   ctx->stream));
+    ctx->launches += 7;
     return CDMS_OK;
   }
-  return exchange(ctx, plan, P_local, anc, d_ancestors, 1);
+  // all ranks' masses -> this rank's plan on the device; ancestor ids written into the slot owners' buffers
+  COLL_TRY(ctx->coll->allgather(ctx, bsum + nb, qall, sizeof(uint64_t)));
+  CUDA_TRY(ctx, launch_plan(qall, R, ctx->rank, P_total, u_bits, plan, ctx->stream));
+  CUDA_TRY(ctx, launch_ancestors(q, P_local, plan, P_total, u_bits, (int64_t)ctx->rank * P_local, nullptr,
+                                 ctx->d_peer_anc, ctx->d_flags, ctx->stream));
+  COLL_TRY(ctx->coll->barrier(ctx));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_ancestors, ctx->panc, sizeof(int64_t) * P_local, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  ctx->launches += 8;
+  return CDMS_OK;
+}
+
+static cdms_status check_step_params(cdms_ctx ctx, const cdms_step_params* prm, int64_t P_local) {
+  if (!prm) return fail(ctx, CDMS_EINVAL, "step params NULL");
+  if (!is_fin(prm->T) || !is_fin(prm->sigma_v) || prm->sigma_v < 0.0) return fail(ctx, CDMS_EINVAL, "T/sigma_v");
+  if (P_local <= 0 || P_local * ctx->nranks > ((int64_t)1 << 26))
+    return fail(ctx, CDMS_EINVAL, "P_total=%lld outside [1, 2^26]", (long long)(P_local * ctx->nranks));
+  return CDMS_OK;
 }
 
 cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_particles, int64_t P_local, const double* d_sfv,
@@ -875,149 +1150,34 @@ cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_partic
   DeviceGuard g(ctx->device);
   if (!d_particles || !d_y || !h_f_pb || !h_prior || !h_eta || !prm || !d_est || !d_lse || P_local <= 0)
     return fail(ctx, CDMS_EINVAL, "bp_step: bad arguments");
-  if (!is_fin(prm->T) || !is_fin(prm->sigma_v) || prm->sigma_v < 0.0) return fail(ctx, CDMS_EINVAL, "bp_step: T/sigma_v");
+  cdms_status st = check_step_params(ctx, prm, P_local);  // every host check before the first launch
+  if (st) return st;
   SceneDev sd;
-  cdms_status st = build_scene(ctx, scene, h_f_pb, h_prior, h_eta, &sd);
+  st = build_scene(ctx, scene, h_f_pb, h_prior, h_eta, &sd);
   if (st) return st;
   if (sd.K > 0 && !d_sfv) return fail(ctx, CDMS_EINVAL, "bp_step: d_sfv NULL with K > 0");
   const int64_t p0 = (int64_t)ctx->rank * P_local;
-  const int64_t P_total = P_local * ctx->nranks;
-  double *l, *w, *stage, *L6, *scal;
+  double* l;
   WS_TRY(ctx, WS_LOGLIK, P_local, &l);
-  WS_TRY(ctx, WS_W, P_local, &w);
-  WS_TRY(ctx, WS_L6, 36, &L6);
-  WS_TRY(ctx, WS_SCAL, 8, &scal);
   // (1) prediction (row A9)
   CUDA_TRY(ctx, launch_predict(d_particles, P_local, p0, prm->T, prm->sigma_v, prm->philox_key, prm->step, ctx->stream));
   ctx->launches += 1;
   // (2) coherent log-likelihood, uniform w_beta (rows A1-A5)
   st = loglik_impl(ctx, sd, scene->precision, d_particles, P_local, 6, d_sfv, 0, d_y, nullptr, l, nullptr);
   if (st) return st;
-  // (3)-(6) the fused O(P) pipeline (step.cu): LSE (A6), weights + quantized masses + moments (A7),
-  // scan + ancestors + gather (A8), regularization (A9).  With a communicator the collectives sit between the
-  // kernels; the combine / finalize arithmetic is the same device code either way.
-  const bool comm = ctx->comm != nullptr;
-  const int R = ctx->nranks;
-  if (P_total > ((int64_t)1 << 26)) return fail(ctx, CDMS_EINVAL, "P_total=%lld exceeds 2^26", (long long)P_total);
-  const int64_t nb = step_blocks(P_local);
-  double2 *lpart, *pairs;
-  double *mpart, *sums;
-  uint64_t *q, *bsum, *qall;
-  unsigned* cnt;
-  WS_TRY(ctx, WS_LSE_PART, nb + 1, &lpart);
-  WS_TRY(ctx, WS_LSE_RANK, R + 1, &pairs);
-  WS_TRY(ctx, WS_MOM_PART, (nb + 1) * 21, &mpart);
-  WS_TRY(ctx, WS_SUMS, 32, &sums);
-  WS_TRY(ctx, WS_Q, P_local, &q);
-  WS_TRY(ctx, WS_BSUM, nb + 2, &bsum);
-  WS_TRY(ctx, WS_QALL, 2 * R + 4, &qall);
-  WS_TRY(ctx, WS_STEP_CNT, 4, &cnt);  // zeroed at allocation, reset by each kernel's last block
-  if (!comm && ctx->step_fused) {
-    // one rank: the five kernels' bodies in one cooperative launch (grid barriers instead of launches and
-    // last-block tails), identical arithmetic and block partition, so identical results
-    WS_TRY(ctx, WS_STAGE, P_local * 6, &stage);
-    StepFusedArgs fa;
-    fa.l = l;
-    fa.x = d_particles;
-    fa.P = P_local;
-    fa.lpart = lpart;
-    fa.rank_pair = pairs;
-    fa.lse = d_lse;
-    fa.M = scal + 0;
-    fa.logS = scal + 1;
-    fa.flags = ctx->d_flags;
-    fa.w = w;
-    fa.q = q;
-    fa.mpart = mpart;
-    fa.bsum = bsum;
-    fa.sums = sums;
-    fa.est = d_est;
-    fa.L = L6;
-    fa.stage = stage;
-    fa.u_bits = host_step_u_bits(prm->philox_key, prm->step);
-    fa.h = step_reg_bandwidth(P_total);
-    fa.regularize = prm->regularize ? 1 : 0;
-    fa.key = prm->philox_key;
-    fa.step = prm->step;
-    CUDA_TRY(ctx, launch_step_fused(fa, ctx->num_sms, ctx->stream));
-    ctx->launches += 1;
-    return CDMS_OK;
-  }
-  CUDA_TRY(ctx, launch_step_lse(l, P_local, lpart, cnt + 0, comm ? pairs + R : pairs, comm ? 0 : 1, d_lse, scal + 0,
-                                scal + 1, ctx->d_flags, ctx->stream));
-  ctx->launches += 1;
-  if (comm) {
-    NCCL_TRY(ctx, ncclAllGather(pairs + R, pairs, 2, ncclDouble, ctx->comm, ctx->stream));
-    CUDA_TRY(ctx, launch_step_lse_combine(pairs, R, d_lse, scal + 0, scal + 1, ctx->d_flags, ctx->stream));
-    ctx->launches += 1;
-  }
-  CUDA_TRY(ctx, launch_step_post(l, d_particles, P_local, scal + 0, scal + 1, ctx->d_flags, w, q, mpart, bsum, cnt + 1,
-                                 sums, ctx->stream));
-  ctx->launches += 1;
-  if (comm) NCCL_TRY(ctx, ncclAllReduce(sums, sums, 7, ncclDouble, ncclSum, ctx->comm, ctx->stream));
-  CUDA_TRY(ctx, launch_step_scan(q, d_particles, w, P_local, bsum, sums, ctx->d_flags, mpart, cnt + 2, sums + 8,
-                                 comm ? 0 : 1, d_est, L6, ctx->d_flags, ctx->stream));
-  ctx->launches += 1;
-  if (comm) {
-    NCCL_TRY(ctx, ncclAllReduce(sums + 8, sums + 8, 21, ncclDouble, ncclSum, ctx->comm, ctx->stream));
-    CUDA_TRY(ctx, launch_step_finalize(sums, sums + 8, d_est, L6, ctx->d_flags, ctx->stream));
-    ctx->launches += 1;
-  }
-  // systematic resampling on r_p = e^{l_p - M} (C-amb-23): slots of this rank's CDF range, states gathered
-  const uint32_t u_bits = host_step_u_bits(prm->philox_key, prm->step);
-  Plan plan;
-  const uint64_t* Qtot = bsum + nb;
-  const uint64_t* Ooff = nullptr;
-  if (!comm) {
-    plan.lo = 0;
-    plan.hi = P_local;
-  } else {
-    // all-gather Q_r, host plan (one small D2H + stream sync per step)
-    NCCL_TRY(ctx, ncclAllGather(bsum + nb, qall, 1, ncclUint64, ctx->comm, ctx->stream));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_pinned, qall, sizeof(uint64_t) * R, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    std::vector<uint64_t> Q(ctx->h_pinned, ctx->h_pinned + R);
-    uint64_t Qt = 0;
-    for (uint64_t v : Q) Qt += v;
-    if (Qt == 0) return fail(ctx, CDMS_EZEROMASS, "all resampling weights are zero");
-    plan.lo_all.resize(R);
-    plan.hi_all.resize(R);
-    uint64_t O = 0, Omine = 0;
-    for (int r = 0; r < R; ++r) {
-      plan.lo_all[r] = slot_index(O, Qt, P_total, u_bits);
-      plan.hi_all[r] = slot_index(O + Q[r], Qt, P_total, u_bits);
-      if (r == ctx->rank) Omine = O;
-      O += Q[r];
-    }
-    plan.lo = plan.lo_all[ctx->rank];
-    plan.hi = plan.hi_all[ctx->rank];
-    ctx->h_pinned[R] = Qt;
-    ctx->h_pinned[R + 1] = Omine;
-    CUDA_TRY(ctx, cudaMemcpyAsync(qall + R, ctx->h_pinned + R, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                  ctx->stream));
-    Qtot = qall + R;
-    Ooff = qall + R + 1;
-  }
-  const int64_t n = plan.hi - plan.lo;
-  WS_TRY(ctx, WS_STAGE, (n > 0 ? n : 1) * 6, &stage);
-  CUDA_TRY(ctx, launch_step_anc(q, bsum, P_local, Qtot, Ooff, plan.lo, plan.hi, P_total, u_bits, d_particles, stage,
-                                ctx->d_flags, ctx->stream));
-  ctx->launches += 1;
-  if (comm) {
-    st = exchange(ctx, plan, P_local, stage, d_particles, 6);
-    if (st) return st;
-    if (prm->regularize) {
-      CUDA_TRY(ctx, launch_step_reg(d_particles, d_particles, P_local, p0, P_total, L6, 1, prm->philox_key, prm->step,
-                                    ctx->stream));
-      ctx->launches += 1;
-    }
-  } else {
-    // regularization with the pre-resampling covariance (A9), reading the staged states (no extra copy)
-    CUDA_TRY(ctx, launch_step_reg(stage, d_particles, P_local, p0, P_total, L6, prm->regularize ? 1 : 0,
-                                  prm->philox_key, prm->step, ctx->stream));
-    ctx->launches += 1;
-  }
-  return CDMS_OK;
+  // (3)-(6) normalize, moments, resample + redistribute, regularize (rows A6-A9)
+  return bp_update_impl(ctx, l, d_particles, P_local, prm, d_est, d_lse, nullptr);
+}
+
+cdms_status cdms_bp_update(cdms_ctx ctx, const double* d_loglik, double* d_particles, int64_t P_local,
+                           const cdms_step_params* prm, double* d_est, double* d_lse, int64_t* d_ancestors) {
+  if (!ctx) return CDMS_EINVAL;
+  DeviceGuard g(ctx->device);
+  if (!d_loglik || !d_particles || !prm || !d_est || !d_lse || P_local <= 0)
+    return fail(ctx, CDMS_EINVAL, "bp_update: bad arguments");
+  cdms_status st = check_step_params(ctx, prm, P_local);
+  if (st) return st;
+  return bp_update_impl(ctx, d_loglik, d_particles, P_local, prm, d_est, d_lse, d_ancestors);
 }
 
 cdms_status cdms_response(cdms_ctx ctx, const cdms_scene* scene, const double* d_pos, int64_t n, const int32_t* d_js,
@@ -1055,8 +1215,8 @@ cdms_status cdms_resample_plan(const uint64_t* h_Q, int nranks, int rank, int64_
     Qtot += h_Q[r];
   }
   if (Qtot == 0) return CDMS_EZEROMASS;
-  const int64_t lo = slot_index(O, Qtot, P_total, u_bits);
-  const int64_t hi = slot_index(O + h_Q[rank], Qtot, P_total, u_bits);
+  const int64_t lo = resample_slot_index(O, Qtot, P_total, u_bits);
+  const int64_t hi = resample_slot_index(O + h_Q[rank], Qtot, P_total, u_bits);
   *slot_lo = lo;
   *slot_hi = hi;
   if (h_send_counts)

@@ -140,6 +140,36 @@ __device__ __forceinline__ uint4 philox_step(uint4 c, uint2 k) {
   return c;
 }
 
+// I(x) = #{i in [0, P_total) : t_i < x}, t_i = floor((u + i 2^32) Q / (P_total 2^32)), exact in 128-bit integers:
+// the first output slot of the CDF position x (distributed resampling plan, C-amb-15).  Used
+// by the device plan (step.cu) and the host entry cdms_resample_plan.
+__host__ __device__ inline int64_t resample_slot_index(uint64_t x, uint64_t Q, int64_t P_total, uint32_t u) {
+  typedef unsigned __int128 u128;
+  const u128 lhs = (u128)x * (u128)(uint64_t)P_total << 32;
+  const u128 uq = (u128)u * Q;
+  if (lhs <= uq) return 0;
+  const u128 A = lhs - uq;
+  const u128 step = (u128)Q << 32;
+  u128 I = (A + step - 1) / step;
+  if (I > (u128)(uint64_t)P_total) I = (u128)(uint64_t)P_total;
+  return (int64_t)I;
+}
+
+// Resampling plan of one rank (plan[4] = Q_total, O_r, slot_lo, slot_hi) from every rank's integer mass Q_r: its CDF
+// range [O_r, O_r + Q_r) covers the contiguous output slots [I(O_r), I(O_r + Q_r)).
+__device__ inline void plan_dev(const uint64_t* Q, int nranks, int rank, int64_t P_total, uint32_t u_bits,
+                                uint64_t* plan) {
+  uint64_t Qt = 0, O = 0;
+  for (int r = 0; r < nranks; ++r) {
+    if (r < rank) O += Q[r];
+    Qt += Q[r];
+  }
+  plan[0] = Qt;
+  plan[1] = O;
+  plan[2] = Qt ? (uint64_t)resample_slot_index(O, Qt, P_total, u_bits) : 0ull;
+  plan[3] = Qt ? (uint64_t)resample_slot_index(O + Q[rank], Qt, P_total, u_bits) : 0ull;
+}
+
 // ---------------------------------------------------------------------------- launchers
 // (defined in loglik.cu / beliefs.cu, called from cdms.cpp)
 cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2, float4* tmpl,
@@ -175,9 +205,12 @@ cudaError_t launch_max_final(const double* part, int64_t nblk, double* out, cuda
 cudaError_t launch_quantize(const double* w, int64_t P, const double* wmax, const double* M, int from_loglik,
                             uint64_t* q, int* flags, cudaStream_t st);
 cudaError_t launch_scan(uint64_t* q, int64_t P, uint64_t* block_sums, cudaStream_t st);
-cudaError_t launch_ancestors(const uint64_t* C, int64_t P_local, const uint64_t* Qtot, const uint64_t* offset,
-                             int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits,
-                             int64_t p_global0, int64_t* anc_out, int* flags, cudaStream_t st);
+cudaError_t launch_ancestors(const uint64_t* C, int64_t P_local, const uint64_t* plan, int64_t P_total, uint32_t u_bits,
+                             int64_t p_global0, int64_t* own_anc, int64_t* const* peer_anc, int* flags,
+                             cudaStream_t st);
+cudaError_t launch_plan(const uint64_t* Qall, int nranks, int rank, int64_t P_total, uint32_t u_bits, uint64_t* plan,
+                        cudaStream_t st);
+cudaError_t launch_sum_ranks(const double* in, int nranks, int n, double* out, cudaStream_t st);
 cudaError_t launch_gather(const double* x, const int64_t* anc, int64_t n, int64_t p_global0, double* out,
                           cudaStream_t st);
 cudaError_t launch_predict(double* x, int64_t P, int64_t p0, double T, double sigma_v, uint64_t key,
@@ -262,19 +295,22 @@ constexpr int STEP_ITEMS = 512;
 int64_t step_blocks(int64_t P);
 cudaError_t launch_step_lse(const double* l, int64_t P, double2* part, unsigned* cnt, double2* rank_pair, int combine,
                             double* lse, double* M, double* logS, int* flags, cudaStream_t st);
-cudaError_t launch_step_lse_combine(const double2* per_rank, int nranks, double* lse, double* M, double* logS,
-                                    int* flags, cudaStream_t st);
+cudaError_t launch_step_lse_global(const double2* gpart, int64_t nbt, double2* rank_pair, double* lse, double* M,
+                                   double* logS, int* flags, cudaStream_t st);
 cudaError_t launch_step_post(const double* l, const double* x, int64_t P, const double* M, const double* logS,
                              const int* flags, double* w, uint64_t* q, double* mpart, uint64_t* bsum, unsigned* cnt,
-                             double* sum1, cudaStream_t st);
+                             double* sum1, uint32_t u_bits, uint64_t* plan, cudaStream_t st);
+cudaError_t launch_step_post_global(const double* gmpart, int64_t nbt, double* sum1, const uint64_t* Qall, int nranks,
+                                    int rank, int64_t P_total, uint32_t u_bits, uint64_t* plan, cudaStream_t st);
 cudaError_t launch_step_scan(uint64_t* q, const double* x, const double* w, int64_t P, const uint64_t* boff,
                              const double* sum1, const int* flags, double* mpart, unsigned* cnt, double* sum2,
                              int finalize, double* est, double* L, int* flags_w, cudaStream_t st);
-cudaError_t launch_step_finalize(const double* sum1, const double* sum2, double* est, double* L, int* flags,
-                                 cudaStream_t st);
-cudaError_t launch_step_anc(const uint64_t* C, const uint64_t* boff, int64_t P_local, const uint64_t* Qtot,
-                            const uint64_t* offset, int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits,
-                            const double* x, double* out, int* flags, cudaStream_t st);
+cudaError_t launch_step_scan_global(const double* gmpart, int64_t nbt, const double* sum1, double* sum2, double* est,
+                                    double* L, int* flags, cudaStream_t st);
+cudaError_t launch_step_anc(const uint64_t* C, const uint64_t* boff, int64_t P_local, const uint64_t* plan,
+                            int64_t P_total, uint32_t u_bits, const double* x, double* own_x, int64_t* own_anc,
+                            double* const* peer_x, int64_t* const* peer_anc, int64_t p_global0, int* flags,
+                            cudaStream_t st);
 cudaError_t launch_step_reg(const double* in, double* out, int64_t P, int64_t p0, int64_t P_total, const double* L,
                             int regularize, uint64_t key, uint64_t step, cudaStream_t st);
 // fused single-rank pipeline (K_lse .. K_reg in one cooperative launch, step.cu)
@@ -293,6 +329,8 @@ struct StepFusedArgs {
   double* sums;    // [32]: sum1 at 0, sum2 at 8
   double *est, *L;
   double* stage;  // [P][6]
+  int64_t* anc;   // [P] ancestors out, or nullptr
+  uint64_t* plan; // [4] resampling plan (Q, O, slot_lo, slot_hi)
   uint32_t u_bits;
   double h;
   int regularize;

@@ -253,14 +253,18 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_lse_kernel(const double* __re
                                                              double2* rank_pair, int combine, double* lse,
                                                              double* M, double* logS, int* flags) {
   lse_block(blockIdx.x, l, P, part);
-  if (!last_block(cnt)) return;
+  if (rank_pair == nullptr || !last_block(cnt)) return;  // multi-rank: the block partials are all-gathered instead
   lse_final(gridDim.x, part, rank_pair, combine, lse, M, logS, flags);
 }
-
-__global__ void step_lse_combine_kernel(const double2* per_rank, int nranks, double* lse, double* M, double* logS,
-                                        int* flags) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) lse_combine_dev(per_rank, nranks, lse, M, logS, flags);
+// Multi-rank: the same fixed-order combine over the all-gathered block partials of every rank (rank-major), so with
+// block-aligned shards (P_local a multiple of STEP_ITEMS) it reduces exactly the partials a single rank holding all
+// particles would, in the same order -- M, ln S and lse are bit-identical for any rank count.
+__global__ void __launch_bounds__(STEP_BLOCK) step_lse_global_kernel(const double2* gpart, int64_t nbt,
+                                                                    double2* rank_pair, double* lse, double* M,
+                                                                    double* logS, int* flags) {
+  lse_final(nbt, gpart, rank_pair, 1, lse, M, logS, flags);
 }
+
 
 // ---------------------------------------------------------------------------- K_post
 __device__ void post_block(int64_t vb, const double* l, const double* x, int64_t P, const double* Mp,
@@ -303,9 +307,10 @@ __device__ void post_block(int64_t vb, const double* l, const double* x, int64_t
   if (threadIdx.x == 0) bsum[vb] = shq[0];
   __syncthreads();
 }
-__device__ void post_final(int64_t nb, const double* mpart, uint64_t* bsum, double* sum1) {
+__device__ void post_final(int64_t nb, const double* mpart, uint64_t* bsum, double* sum1, int64_t P, uint32_t u_bits,
+                           uint64_t* plan) {
   __shared__ uint64_t shq[STEP_BLOCK];
-  sum_columns<7>(mpart, nb, sum1);
+  if (sum1) sum_columns<7>(mpart, nb, sum1);
   // exclusive scan of the block totals in place; bsum[nb] = Q (this rank)
   const int64_t chunk = (nb + STEP_BLOCK - 1) / STEP_BLOCK;
   const int64_t b0 = threadIdx.x * chunk, b1 = min(nb, b0 + chunk);
@@ -325,16 +330,30 @@ __device__ void post_final(int64_t nb, const double* mpart, uint64_t* bsum, doub
     bsum[b] = ex;
     ex += v;
   }
-  if (threadIdx.x == STEP_BLOCK - 1) bsum[nb] = shq[STEP_BLOCK - 1];
+  if (threadIdx.x == STEP_BLOCK - 1) {
+    bsum[nb] = shq[STEP_BLOCK - 1];
+    if (plan) plan_dev(&shq[STEP_BLOCK - 1], 1, 0, P, u_bits, plan);  // single rank: slots [0, P)
+  }
   __syncthreads();
 }
+// sum1 == nullptr (multi-rank): the last block only scans the local block totals; the moment sums follow from the
+// all-gathered block partials (step_post_global_kernel)
 __global__ void __launch_bounds__(STEP_BLOCK) step_post_kernel(const double* l, const double* x, int64_t P,
                                                               const double* Mp, const double* logSp, const int* flags,
                                                               double* w, uint64_t* q, double* mpart, uint64_t* bsum,
-                                                              unsigned* cnt, double* sum1) {
+                                                              unsigned* cnt, double* sum1, uint32_t u_bits,
+                                                              uint64_t* plan) {
   post_block(blockIdx.x, l, x, P, Mp, logSp, flags, w, q, mpart, bsum);
   if (!last_block(cnt)) return;
-  post_final(gridDim.x, mpart, bsum, sum1);
+  post_final(gridDim.x, mpart, bsum, sum1, P, u_bits, plan);
+}
+// Multi-rank: first moments over every rank's block partials (fixed order, as a single rank would) and the plan of
+// this rank from the all-gathered masses Q_r.
+__global__ void __launch_bounds__(STEP_BLOCK) step_post_global_kernel(const double* gmpart, int64_t nbt, double* sum1,
+                                                                     const uint64_t* Qall, int nranks, int rank,
+                                                                     int64_t P_total, uint32_t u_bits, uint64_t* plan) {
+  sum_columns<7>(gmpart, nbt, sum1);
+  if (threadIdx.x == 0) plan_dev(Qall, nranks, rank, P_total, u_bits, plan);
 }
 
 // ---------------------------------------------------------------------------- K_scan
@@ -402,31 +421,39 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_scan_kernel(uint64_t* q, cons
                                                               double* sum2, int finalize, double* est, double* L,
                                                               int* flags_w) {
   scan_block(blockIdx.x, q, x, w, P, boff, sum1, flags, mpart);
-  if (!last_block(cnt)) return;
+  if (sum2 == nullptr || !last_block(cnt)) return;  // multi-rank: partials all-gathered, step_scan_global_kernel
   scan_final(gridDim.x, mpart, sum2, finalize, sum1, est, L, flags_w);
 }
-
-__global__ void step_finalize_kernel(const double* sum1, const double* sum2, double* est, double* L, int* flags) {
-  if (blockIdx.x == 0 && threadIdx.x < 32) finalize_dev(sum1, sum2, est, L, flags);  // launched with 32 threads
+__global__ void __launch_bounds__(STEP_BLOCK) step_scan_global_kernel(const double* gmpart, int64_t nbt,
+                                                                     const double* sum1, double* sum2, double* est,
+                                                                     double* L, int* flags) {
+  scan_final(nbt, gmpart, sum2, 1, sum1, est, L, flags);
 }
 
+
 // ---------------------------------------------------------------------------- K_anc (+ gather)
-// Local output slot i (global slot g = slot_lo + i): t_g = floor((u + g 2^32) Q / (P_total 2^32));
-// ancestor = min{p : C_p > t_g - O_r}; out[i] = x[ancestor] (6 doubles; one thread per slot).
+// Output slot g in this rank's range [slot_lo, slot_hi) (plan, written on the device: no host round trip):
+// t_g = floor((u + g 2^32) Q / (P_total 2^32)); ancestor = min{p : C_p > t_g - O_r} (local index lo, global
+// p_global0 + lo); the state x[lo] goes to row g mod P_local of the stage buffer of the slot's owner rank
+// g / P_local -- written directly into that rank's memory (peer_x[owner]: its own buffer on one rank, NVLink peer
+// memory (CUDA IPC) under NCCL, another context's buffer for the loopback test backend), so the redistribution of
+// DESIGN.md section 9 is fused into the gather instead of a separate send/recv round.  Grid-stride over the slots.
 // Two-level search when the rank has at most ANC_SMEM blocks: the block ends E_b = boff[b + 1] (boff[nb] = this
 // rank's total) in shared memory give the block holding the ancestor (C is non-decreasing, so it is the first block
-// whose last C exceeds t), then 9 steps inside its STEP_ITEMS entries -- instead of 17 dependent L2 loads.
+// whose last C exceeds t), then 9 steps inside its STEP_ITEMS entries; above ANC_SMEM blocks every ANC_SUP-th block
+// end is staged (three-level search).
 constexpr int ANC_SMEM = 2048;
 __device__ void anc_range(int64_t i0, int64_t stride, const uint64_t* C, const uint64_t* boff, int64_t nb,
-                          int64_t P_local, const uint64_t* Qtot, const uint64_t* offset, int64_t slot_lo, int64_t n,
-                          int64_t P_total, uint32_t u_bits, const double* x, double* out, int* flags) {
+                          int64_t P_local, const uint64_t* plan, int64_t P_total, uint32_t u_bits, const double* x,
+                          double* own_x, int64_t* own_anc, double* const* peer_x, int64_t* const* peer_anc,
+                          int64_t p_global0, int* flags) {
   __shared__ uint64_t sE[ANC_SMEM];
-  const bool two = nb <= ANC_SMEM;
-  if (two)
-    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) sE[b] = __ldcg(&boff[b + 1]);
+  const int64_t sup = (nb + ANC_SMEM - 1) / ANC_SMEM;  // blocks per staged end (1: every block end)
+  const int64_t ns = (nb + sup - 1) / sup;
+  for (int64_t b = threadIdx.x; b < ns; b += blockDim.x) sE[b] = __ldcg(&boff[min(nb, (b + 1) * sup)]);
   __syncthreads();
-  const uint64_t Q = __ldcg(Qtot);
-  const uint64_t O = offset ? __ldcg(offset) : 0ull;
+  const uint64_t Q = __ldcg(&plan[0]), O = __ldcg(&plan[1]);
+  const int64_t slot_lo = (int64_t)__ldcg(&plan[2]), n = (int64_t)__ldcg(&plan[3]) - slot_lo;
   if (Q == 0) {
     if (i0 == 0) atomicOr(flags, FLAG_ZEROMASS);
     return;
@@ -436,32 +463,38 @@ __device__ void anc_range(int64_t i0, int64_t stride, const uint64_t* C, const u
     const uint64_t g = (uint64_t)(slot_lo + i);
     const unsigned __int128 num = ((unsigned __int128)u_bits + ((unsigned __int128)g << 32)) * Q;
     const uint64_t t = (uint64_t)(num / den) - O;
-    int64_t lo = 0, hi = P_local - 1;  // smallest p with C[p] > t
-    if (two) {
-      int64_t bl = 0, bh = nb - 1;  // smallest block b with E_b > t
-      while (bl < bh) {
-        const int64_t mid = (bl + bh) >> 1;
-        if (sE[mid] > t) bh = mid; else bl = mid + 1;
-      }
-      lo = bl * STEP_ITEMS;
-      hi = min(P_local, lo + STEP_ITEMS) - 1;
+    int64_t bl = 0, bh = ns - 1;  // smallest staged group with end > t
+    while (bl < bh) {
+      const int64_t mid = (bl + bh) >> 1;
+      if (sE[mid] > t) bh = mid; else bl = mid + 1;
     }
+    int64_t b0 = bl * sup, b1 = min(nb, b0 + sup) - 1;  // then the block inside the group (sup > 1 only)
+    while (b0 < b1) {
+      const int64_t mid = (b0 + b1) >> 1;
+      if (__ldcg(&boff[mid + 1]) > t) b1 = mid; else b0 = mid + 1;
+    }
+    int64_t lo = b0 * STEP_ITEMS, hi = min(P_local, lo + STEP_ITEMS) - 1;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
       if (__ldcg(&C[mid]) > t) hi = mid; else lo = mid + 1;
     }
+    const int64_t own = (int64_t)(g / (uint64_t)P_local), row = (int64_t)g - own * P_local;
+    int64_t* da = peer_x ? (peer_anc ? peer_anc[own] : nullptr) : own_anc;  // peer_x == nullptr: one rank
+    if (da) da[row] = p_global0 + lo;
     const double2* src = reinterpret_cast<const double2*>(x + lo * 6);
-    double2* dst = reinterpret_cast<double2*>(out + i * 6);
+    double2* dst = reinterpret_cast<double2*>((peer_x ? peer_x[own] : own_x) + row * 6);
     dst[0] = src[0];
     dst[1] = src[1];
     dst[2] = src[2];
   }
+  __threadfence_system();  // peer writes ordered before the barrier collective that follows the kernel
 }
 __global__ void step_anc_kernel(const uint64_t* C, const uint64_t* boff, int64_t nb, int64_t P_local,
-                                const uint64_t* Qtot, const uint64_t* offset, int64_t slot_lo, int64_t n,
-                                int64_t P_total, uint32_t u_bits, const double* x, double* out, int* flags) {
+                                const uint64_t* plan, int64_t P_total, uint32_t u_bits, const double* x, double* own_x,
+                                int64_t* own_anc, double* const* peer_x, int64_t* const* peer_anc, int64_t p_global0,
+                                int* flags) {
   anc_range((int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, C, boff, nb, P_local,
-            Qtot, offset, slot_lo, n, P_total, u_bits, x, out, flags);
+            plan, P_total, u_bits, x, own_x, own_anc, peer_x, peer_anc, p_global0, flags);
 }
 
 // ---------------------------------------------------------------------------- K_reg
@@ -530,14 +563,15 @@ __global__ void __launch_bounds__(STEP_BLOCK) step_fused_kernel(StepFusedArgs a)
   for (int64_t vb = blockIdx.x; vb < nb; vb += gridDim.x)
     post_block(vb, a.l, a.x, a.P, a.M, a.logS, a.flags, a.w, a.q, a.mpart, a.bsum);
   grid.sync();
-  if (blockIdx.x == 0) post_final(nb, a.mpart, a.bsum, a.sums);
+  if (blockIdx.x == 0) post_final(nb, a.mpart, a.bsum, a.sums, a.P, a.u_bits, a.plan);
   grid.sync();
   for (int64_t vb = blockIdx.x; vb < nb; vb += gridDim.x)
     scan_block(vb, a.q, a.x, a.w, a.P, a.bsum, a.sums, a.flags, a.mpart);
   grid.sync();
   if (blockIdx.x == 0) scan_final(nb, a.mpart, a.sums + 8, 1, a.sums, a.est, a.L, a.flags);
   grid.sync();
-  anc_range(i0, stride, a.q, a.bsum, nb, a.P, a.bsum + nb, nullptr, 0, a.P, a.P, a.u_bits, a.x, a.stage, a.flags);
+  anc_range(i0, stride, a.q, a.bsum, nb, a.P, a.plan, a.P, a.u_bits, a.x, a.stage, a.anc, nullptr, nullptr, 0,
+            a.flags);
   grid.sync();
   reg_range(i0, stride, a.stage, a.x, a.P, 0, a.h, a.L, a.regularize, a.key, a.step);
 }
@@ -556,16 +590,22 @@ cudaError_t launch_step_lse(const double* l, int64_t P, double2* part, unsigned*
   step_lse_kernel<<<(unsigned)nb, STEP_BLOCK, 0, st>>>(l, P, part, cnt, rank_pair, combine, lse, M, logS, flags);
   return cudaGetLastError();
 }
-cudaError_t launch_step_lse_combine(const double2* per_rank, int nranks, double* lse, double* M, double* logS,
-                                    int* flags, cudaStream_t st) {
-  step_lse_combine_kernel<<<1, 32, 0, st>>>(per_rank, nranks, lse, M, logS, flags);
+cudaError_t launch_step_lse_global(const double2* gpart, int64_t nbt, double2* rank_pair, double* lse, double* M,
+                                   double* logS, int* flags, cudaStream_t st) {
+  step_lse_global_kernel<<<1, STEP_BLOCK, 0, st>>>(gpart, nbt, rank_pair, lse, M, logS, flags);
   return cudaGetLastError();
 }
 cudaError_t launch_step_post(const double* l, const double* x, int64_t P, const double* M, const double* logS,
                              const int* flags, double* w, uint64_t* q, double* mpart, uint64_t* bsum, unsigned* cnt,
-                             double* sum1, cudaStream_t st) {
+                             double* sum1, uint32_t u_bits, uint64_t* plan, cudaStream_t st) {
   const int64_t nb = step_blocks(P);
-  step_post_kernel<<<(unsigned)nb, STEP_BLOCK, 0, st>>>(l, x, P, M, logS, flags, w, q, mpart, bsum, cnt, sum1);
+  step_post_kernel<<<(unsigned)nb, STEP_BLOCK, 0, st>>>(l, x, P, M, logS, flags, w, q, mpart, bsum, cnt, sum1, u_bits,
+                                                       plan);
+  return cudaGetLastError();
+}
+cudaError_t launch_step_post_global(const double* gmpart, int64_t nbt, double* sum1, const uint64_t* Qall, int nranks,
+                                    int rank, int64_t P_total, uint32_t u_bits, uint64_t* plan, cudaStream_t st) {
+  step_post_global_kernel<<<1, STEP_BLOCK, 0, st>>>(gmpart, nbt, sum1, Qall, nranks, rank, P_total, u_bits, plan);
   return cudaGetLastError();
 }
 cudaError_t launch_step_scan(uint64_t* q, const double* x, const double* w, int64_t P, const uint64_t* boff,
@@ -576,18 +616,28 @@ cudaError_t launch_step_scan(uint64_t* q, const double* x, const double* w, int6
                                                        L, flags_w);
   return cudaGetLastError();
 }
-cudaError_t launch_step_finalize(const double* sum1, const double* sum2, double* est, double* L, int* flags,
-                                 cudaStream_t st) {
-  step_finalize_kernel<<<1, 32, 0, st>>>(sum1, sum2, est, L, flags);
+cudaError_t launch_step_scan_global(const double* gmpart, int64_t nbt, const double* sum1, double* sum2, double* est,
+                                    double* L, int* flags, cudaStream_t st) {
+  step_scan_global_kernel<<<1, STEP_BLOCK, 0, st>>>(gmpart, nbt, sum1, sum2, est, L, flags);
   return cudaGetLastError();
 }
-cudaError_t launch_step_anc(const uint64_t* C, const uint64_t* boff, int64_t P_local, const uint64_t* Qtot,
-                            const uint64_t* offset, int64_t slot_lo, int64_t slot_hi, int64_t P_total, uint32_t u_bits,
-                            const double* x, double* out, int* flags, cudaStream_t st) {
-  const int64_t n = slot_hi - slot_lo;
-  if (n <= 0) return cudaSuccess;
-  step_anc_kernel<<<grid_cap(n, 256), 256, 0, st>>>(C, boff, step_blocks(P_local), P_local, Qtot, offset, slot_lo, n,
-                                                   P_total, u_bits, x, out, flags);
+// The plan's slot count is only known on the device: a fixed grid (enough for one slot per thread when the rank keeps
+// its own P_local slots, grid-stride beyond) of threads reads it.
+cudaError_t launch_step_anc(const uint64_t* C, const uint64_t* boff, int64_t P_local, const uint64_t* plan,
+                            int64_t P_total, uint32_t u_bits, const double* x, double* own_x, int64_t* own_anc,
+                            double* const* peer_x, int64_t* const* peer_anc, int64_t p_global0, int* flags,
+                            cudaStream_t st) {
+  step_anc_kernel<<<grid_cap(P_local, 256), 256, 0, st>>>(C, boff, step_blocks(P_local), P_local, plan, P_total,
+                                                         u_bits, x, own_x, own_anc, peer_x, peer_anc, p_global0, flags);
+  return cudaGetLastError();
+}
+__global__ void plan_kernel(const uint64_t* Qall, int nranks, int rank, int64_t P_total, uint32_t u_bits,
+                            uint64_t* plan) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) plan_dev(Qall, nranks, rank, P_total, u_bits, plan);
+}
+cudaError_t launch_plan(const uint64_t* Qall, int nranks, int rank, int64_t P_total, uint32_t u_bits, uint64_t* plan,
+                        cudaStream_t st) {
+  plan_kernel<<<1, 32, 0, st>>>(Qall, nranks, rank, P_total, u_bits, plan);
   return cudaGetLastError();
 }
 cudaError_t launch_step_reg(const double* in, double* out, int64_t P, int64_t p0, int64_t P_total, const double* L,

@@ -1,11 +1,12 @@
 """Benchmark of the coherent-likelihood BP step (BASELINE.json metric: particle x VA coherent likelihood
 evals/s and ms per BP step at 1/2/4/8 B200).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl cdms|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--particles P_total] [--impl cdms|reference]
 
-One process per GPU (torchrun for N > 1).  A step = one cdms_bp_step (predict, coherent log-likelihood over
-all particles x PAs x components, LSE normalization, moments, systematic resampling with redistribution,
-regularization) on P_local particles per GPU (weak scaling: P_total = N * P of the config).  Inputs are
+One process per GPU (`--gpus N` launches torch.distributed.run itself when WORLD_SIZE is unset).  A step = one
+cdms_bp_step (predict, coherent log-likelihood over all particles x PAs x components, LSE normalization, moments,
+systematic resampling with redistribution, regularization).  Strong scaling (SURVEY 8(d) metric 2): the default is
+c5 (J=4, S=9, 8x8 URA, nf=1024) with P_total = 16M particles split over the N GPUs (P_local = 16M/N).  Inputs are
 synthetic (scenes.py recipe); the measurement y is synthesized on the device with libcdms's own responses.
 L2 is flushed (256 MiB write) between timed steps; each step is timed with CUDA events on the context's
 stream; the reported time is the max over ranks.  Rank 0 prints one JSON line.
@@ -48,13 +49,6 @@ def measured_tensor_peak():
         return float(mp["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS 8192^3, 4 s)"
     except (OSError, KeyError, ValueError):
         return 2250.0 * 0.72, "fallback: nominal 2.25 PFLOP/s x 0.72"
-
-
-def k1t_kernels(cfg, P: int) -> str:
-    """The K1T stage's kernels as libcdms picks them (taylor.cu tay_lanes, cdms.cpp engine selection)."""
-    c = ("cdms::tay_corr_lanes_kernel" if P * cfg.J < 250000 else "cdms::tay_corr_kernel") + " (K1T, c)"
-    g = "tay_gram_kernel<S> (G)"
-    return c + " + " + g
 
 
 def taylor_path(args) -> bool:
@@ -167,6 +161,18 @@ def dist_env():
     return world, rank, local
 
 
+def self_launch(args) -> int:
+    """`--gpus N` without a torchrun environment: re-run this command under torch.distributed.run with N ranks on
+    this node (rendezvous on 127.0.0.1) and relay its output."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def synth_measurement(cd, ctx, scene, sc, torch, dev):
     """z^(j) = sum_s rho_s psi_s(p_true) + sqrt(eta) w with libcdms's responses; SNR 20 dB."""
     J, S = sc.cfg.J, sc.cfg.S
@@ -182,7 +188,12 @@ def synth_measurement(cd, ctx, scene, sc, torch, dev):
     return y, np.full(J, eta)
 
 
+def p_total_of(args, cfg) -> int:
+    return cfg.P if args.particles is None else args.particles
+
+
 def run_cdms(args):
+    """Strong scaling (SURVEY 8(d) metric 2): P_total particles of the config split over the ranks, P_local each."""
     import torch
     world, rank, local = dist_env()
     if world > 1:
@@ -200,18 +211,18 @@ def run_cdms(args):
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream(local)
     cfg = scenes.CONFIGS[args.config]
-    P_local = cfg.P if args.particles is None else args.particles
+    P_total = p_total_of(args, cfg)
+    if P_total % world:
+        raise SystemExit(f"P_total={P_total} is not divisible by {world} ranks")
+    P_local = P_total // world
     sc = scenes.make_scene(cfg)
     scene = cdms.Scene.from_synthetic(sc, wavefront=args.wavefront, precision=args.precision)
     ctx = cdms.Context(local, stream)
     if world > 1:
         ctx.comm_init_from_torch(rank, world)
-    y, eta = synth_measurement(cd := cdms, ctx, scene, sc, torch, dev)
+    y, eta = synth_measurement(cdms, ctx, scene, sc, torch, dev)
     m, v = scenes.priors(sc, "nzm")
-    x0 = torch.as_tensor(scenes.make_particles(cfg, rank * P_local, P_local) if P_local <= cfg.P
-                         else np.tile(scenes.make_particles(cfg, 0, cfg.P), (math.ceil(P_local / cfg.P), 1))[:P_local],
-                         device=dev).contiguous()
-    x = x0.clone()
+    x = torch.as_tensor(scenes.make_particles(cfg, rank * P_local, P_local), device=dev).contiguous()
     dsfv = torch.as_tensor(sc.sfv, device=dev).contiguous()
     est = torch.empty(28, dtype=torch.float64, device=dev)
     lse = torch.empty(1, dtype=torch.float64, device=dev)
@@ -250,16 +261,16 @@ def run_cdms(args):
         barrier()
     st = ctx.sync(raise_on_error=False)
     gpu_launches = ctx.launch_count() - launches0
-    k_ms, k_n = ctx.timing_read()
+    stage_ms, k_n = ctx.timing_read_stages()      # [correlation, Gram, assembly] summed over the timed steps
     ctx.timing_enable(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    local_total = sum(step_ms)
-    tot = torch.tensor([local_total, k_ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([sum(step_ms)] + stage_ms, dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
     ms_per_step = tot[0].item() / args.steps
-    kernel_ms = tot[1].item() / max(k_n, 1)               # average corr_kernel launch
-    launches_per_step = max(k_n, 1) / args.steps           # > 1 when the terms budget batches the particles
+    n_batches = max(k_n, 1)
+    kern_ms = {"corr": tot[1].item() / n_batches, "gram": tot[2].item() / n_batches, "asm": tot[3].item() / n_batches}
+    launches_per_step = n_batches / args.steps      # > 1 when the terms budget batches the particles
 
     # ---- end to end: host measurement in, host estimate out, through the public API
     y_host = torch.empty(y.shape, dtype=torch.complex64, pin_memory=True)
@@ -284,116 +295,149 @@ def run_cdms(args):
     e2e_ms = e2e_t.item() / args.steps
     ctx.sync(raise_on_error=False)
 
-    evals_step = P_local * world * cfg.J * cfg.S
+    evals_step = P_total * cfg.J * cfg.S
     value = evals_step / (ms_per_step / 1e3)
     result = None
     if rank == 0:
         clocks = clk.summary()
-        # algorithmic flops of an average launch: 8 N_z flop per (particle, PA, component) unit,
-        # P_local J S units per step spread over launches_per_step launches
-        flop_launch = 8.0 * cfg.Nz * P_local * cfg.J * cfg.S / launches_per_step
-        achieved = flop_launch / (kernel_ms / 1e3) / 1e12
-        peak = fp32_peak_tflops(1965.0)
-        if nb_tensor_path(args):
-            # F2: the correlation is a real GEMM of 8 N_z flop per unit executed as four fp16 products
-            # (D1 = A_hi B_hi exact, D2 = the three residual products; nbmma.cu)
-            tflop_launch = 4.0 * flop_launch
-            t_achieved = tflop_launch / (kernel_ms / 1e3) / 1e12
-            t_peak, t_basis = measured_tensor_peak()
-            roof = {"bound": "tensor", "pipe": "tcgen05.mma kind::f16 (fp32 accumulate)",
-                    "achieved": round(t_achieved, 2), "peak": round(t_peak, 1), "unit": "TFLOP/s",
-                    "frac": round(t_achieved / t_peak, 4), "peak_basis": t_basis,
-                    "kernel": "cdms::nb_corr_kernel + nb_gram_kernel (rows A2-A5, F2)",
-                    "kernel_ms": round(kernel_ms, 4),
-                    "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
-                    "launches_per_step": launches_per_step, "flop_per_launch": tflop_launch,
-                    "flop_basis": "4 fp16 products x 8 N_z flop per (particle, PA, component)",
-                    "useful_fp32_equivalent_tflops": round(achieved, 3),
-                    "traffic": (traffic_from_profiles(args.config + "_planar_nb") if args.particles is None else None),
-                    "traffic_basis": "dram read+write bytes of one nb_corr_kernel launch, ncu --set full "
-                                     "(profiles/loglik_traffic.json); particles in, c out (tensor-bound)"}
-        elif taylor_path(args):
-            # K1T (taylor.cu): the correlation from spectral Taylor tables, O(1) work per (particle, component,
-            # antenna) instead of the direct recurrence's O(N_f); achieved still counts SURVEY 8(d)'s direct-
-            # correlation flops (8 N_z per unit), so frac > 1 means the likelihood stage beats the FP32 roofline of
-            # the direct method.  The stage's own resource profile is in profiles/r01_k1t_*.
-            roof = {"bound": "alu", "pipe": "fp32 (direct-correlation flop equivalent)", "achieved": round(achieved, 3),
-                    "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                    "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
-                    "kernel": k1t_kernels(cfg, P_local),
-                    "kernel_ms": round(kernel_ms, 4),
-                    "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
-                    "launches_per_step": launches_per_step, "flop_per_launch": flop_launch,
-                    "note": "frac > 1: K1T evaluates c from spectral Taylor tables (DESIGN.md 'K1T'); the flop count "
-                            "is the direct correlation's 8 N_z per (particle, PA, component)",
-                    "traffic": (traffic_from_profiles(args.config + "_k1t") if args.particles is None else None),
-                    "traffic_basis": "dram read+write bytes of one K1T correlation launch, ncu --set full "
-                                     "(profiles/loglik_traffic.json)",
-                    "issue": (k1t_issue(args.config, kernel_ms * launches_per_step, clocks.get("sm_mhz"))
-                              if args.particles is None and args.wavefront == "spherical" else None)}
-        else:
-            roof = {"bound": "alu", "pipe": "fp32 fma", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                    "peak_basis": "128 FFMA/SM/clk x 148 SM x 2 FLOP x 1965 MHz (sm_max); DESIGN.md 'Roofline'",
-                    "frac_at_measured_clock": (round(achieved / fp32_peak_tflops(clocks["sm_mhz"]), 4)
-                                               if clocks.get("sm_mhz") else None),
-                    "kernel": "cdms::corr_kernel (row A2-A5: responses, correlation c, Gram G)", "kernel_ms": round(kernel_ms, 4),
-                    "kernel_share_of_step": round(kernel_ms * launches_per_step / ms_per_step, 4),
-                    "launches_per_step": launches_per_step,
-                    "flop_per_launch": flop_launch,
-                    "traffic": (traffic_from_profiles(args.config) if args.particles is None and args.wavefront == "spherical"
-                                and args.precision == "fp32" else None),
-                    "traffic_basis": "dram read+write bytes of one corr_kernel launch, ncu --set full "
-                                     "(profiles/loglik_traffic.json); the kernel is FP32-bound, traffic is particles + y"}
+        roof = roofline(args, cfg, P_local, kern_ms, launches_per_step, ms_per_step, clocks)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
-            "config": config_dict(args, cfg, P_local, world),
+            "config": config_dict(args, cfg, P_total, world),
             "roofline": roof,
+            "kernel_ms_per_step": {k: round(v * launches_per_step, 4) for k, v in kern_ms.items()},
             "e2e": {"value": evals_step / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": int(y.numel() * 8), "d2h_bytes_per_step": 29 * 8},
             "clocks": clocks, "gpu_launches": int(gpu_launches), "sync_status": st,
         }
+    ctx.close()
+    del x, flush
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1:
         if not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(args, cfg, sc, budget_s=args.cpu_seconds)
+        if not args.no_extras:
+            # C-amb-18(ii): FP32 end-to-end weight error against the oracle (every particle of c2), and the FP64
+            # mode's throughput (the mode that meets the 1e-5 weight tolerance end to end)
+            result["fp32_weights_vs_oracle"] = fp32_weight_error(cdms, torch, dev)
+            result["fp64_mode"] = fp64_mode_line(cdms, torch, dev, local)
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return result
 
 
-def traffic_from_profiles(config: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one corr_kernel launch of this config from the committed
-    ncu --set full capture (tools/ncu_traffic.py), or None."""
-    p = os.path.join(ROOT, "profiles", "loglik_traffic.json")
+def roofline(args, cfg, P_local, kern_ms, launches_per_step, ms_per_step, clocks):
+    """The dominant likelihood kernel against its pipe: achieved = its own FMA-pipe / XU
+    thread-instructions per launch (committed ncu capture of this config, profiles/pipe_inst.json, per particle x
+    P_local) over its live CUDA-event time; peak = 128 FMA lanes (16 XU lanes) x 148 SMs x 1965 MHz.  The direct
+    correlation's flop count (8 N_z per (particle, PA, component)) is reported separately as
+    direct_equiv_frac: the K1T engine does not execute those flops."""
+    dom = max(("corr", "gram"), key=lambda k: kern_ms[k])
+    t = kern_ms[dom] / 1e3
+    mhz = 1965.0
+    peak_fma = 128 * N_SM * mhz * 1e6 / 1e12      # T thread-instructions / s
+    peak_xu = 16 * N_SM * mhz * 1e6 / 1e12
+    names = kernel_names(args, cfg, P_local)
+    flop_launch = 8.0 * cfg.Nz * P_local * cfg.J * cfg.S / launches_per_step
+    direct = flop_launch / ((kern_ms["corr"] + kern_ms["gram"]) / 1e3) / 1e12
+    roof = {"bound": "alu", "pipe": "fp32 FMA pipe (own instructions)", "kernel": names[dom],
+            "kernel_ms": round(kern_ms[dom], 4),
+            "kernel_share_of_step": round(kern_ms[dom] * launches_per_step / ms_per_step, 4),
+            "launches_per_step": launches_per_step, "unit": "T thread-inst/s",
+            "peak": round(peak_fma, 3), "peak_basis": "128 FFMA lanes/SM/clk x 148 SM x 1965 MHz (sm_max); XU: 16",
+            "other_kernel": {"name": names["gram" if dom == "corr" else "corr"],
+                             "kernel_ms": round(kern_ms["gram" if dom == "corr" else "corr"], 4)},
+            "direct_equiv_frac": round(direct / fp32_peak_tflops(mhz), 4),
+            "direct_equiv_basis": "8 N_z flop per (particle, PA, component) over correlation + Gram kernel time, "
+                                  "vs 74.45 TFLOP/s FP32: the direct method's flops, not executed by K1T",
+            "achieved": None, "frac": None, "xu_frac": None, "traffic": None}
+    rec = pipe_profile(args, cfg)
+    if rec is not None and names[dom] in rec["kernels"]:
+        k = rec["kernels"][names[dom]]
+        fma = k["fma_thread_inst_per_particle"] * P_local / launches_per_step
+        xu = k["xu_thread_inst_per_particle"] * P_local / launches_per_step
+        roof.update({"achieved": round(fma / t / 1e12, 3), "frac": round(fma / t / 1e12 / peak_fma, 4),
+                     "xu_achieved": round(xu / t / 1e12, 3), "xu_frac": round(xu / t / 1e12 / peak_xu, 4),
+                     "traffic": k.get("dram_bytes_per_particle", 0) * P_local / launches_per_step or None,
+                     "traffic_basis": "dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)",
+                     "inst_source": rec["source"]})
+    return roof
+
+
+def kernel_names(args, cfg, P_local):
+    """The likelihood stage's kernels as libcdms picks them (cdms.cpp engine selection, taylor.cu tay_lanes)."""
+    if args.precision == "fp64" or os.environ.get("CDMS_TAYLOR", "1") == "0" and args.wavefront != "planar_nb":
+        return {"corr": "corr_kernel", "gram": "(in corr_kernel)"}
+    if args.wavefront == "planar_nb":
+        return {"corr": "nb_corr_kernel", "gram": "nb_gram_kernel"}
+    return {"corr": "tay_corr_lanes_kernel" if P_local * cfg.J < 250000 else "tay_corr_kernel",
+            "gram": f"tay_gram_kernel<{cfg.S}>"}
+
+
+def pipe_profile(args, cfg):
+    """Per-particle pipe instruction counts of this config's kernels (tools/ncu_pipe.py from a committed capture)."""
+    key = f"{args.config}_{args.wavefront}_{args.precision}"
     try:
-        with open(p) as f:
-            rec = json.load(f).get(config)
-        return None if rec is None else rec["dram_bytes_per_launch"]
+        with open(os.path.join(ROOT, "profiles", "pipe_inst.json")) as f:
+            return json.load(f).get(key)
     except Exception:
         return None
 
 
-def k1t_issue(config: str, stage_ms: float, sm_mhz):
-    """The K1T stage's own efficiency: warp instructions of its correlation + Gram launches per step (committed ncu
-    capture, tools/ncu_inst.py) over the live-timed stage against the SM issue peak (148 SMs x 4 schedulers x 1
-    warp-instruction / clk), or None when no capture of this config exists."""
-    p = os.path.join(ROOT, "profiles", "k1t_stage_inst.json")
-    try:
-        with open(p) as f:
-            rec = json.load(f).get(config)
-    except Exception:
-        return None
-    if rec is None or not stage_ms:
-        return None
-    inst = sum(v for k, v in rec["kernels"].items() if k.startswith(("tay_corr", "tay_gram")))
-    mhz = sm_mhz or 1965.0
-    peak = 148 * 4 * mhz * 1e6
-    return {"warp_inst_per_step": inst, "stage_ms": round(stage_ms, 4), "peak_warp_inst_per_s": peak,
-            "issue_frac": round(inst / (stage_ms * 1e-3) / peak, 4),
-            "basis": f"smsp__inst_executed.sum of tay_corr* + tay_gram* ({rec['source']}) / live stage time / "
-                     f"(148 SM x 4 issue slots x {mhz:.0f} MHz)"}
+def fp32_weight_error(cdms, torch, dev):
+    """Normalized weights of every c2 particle from the FP32 engine vs the oracle (identical inputs): max |dw|, max
+    centred |dl| (dl minus its weighted mean), reading C-amb-18(ii)."""
+    from oracle import oracle as O
+    O.build()
+    cfg = scenes.CONFIGS["c2"]
+    sc = scenes.make_scene(cfg)
+    o, y, eta, m, v, x = oracle_inputs(cfg, sc, O, cfg.P)
+    t0 = time.perf_counter()
+    st, lo = o.loglik(x, sc.sfv, y, m, v, eta)
+    t_orc = time.perf_counter() - t0
+    st, wo, lseo = O.normalize(lo)
+    ctx = cdms.Context(int(dev.split(":")[1]))
+    scene = cdms.Scene.from_synthetic(sc)
+    l = cdms.loglik(ctx, scene, torch.as_tensor(x, device=dev).contiguous(),
+                    torch.as_tensor(sc.sfv, device=dev).contiguous(),
+                    torch.as_tensor(y.astype(np.complex64), device=dev).contiguous(), m, v, eta)
+    w, lse = cdms.weights_normalize(ctx, l)
+    ctx.sync()
+    w = w.cpu().numpy()
+    dl = l.cpu().numpy() - lo
+    ctx.close()
+    return {"config": "c2 (all 100000 particles)", "max_abs_dw": float(np.max(np.abs(w - wo))),
+            "max_w": float(wo.max()), "max_centred_abs_dl": float(np.max(np.abs(dl - np.sum(wo * dl)))),
+            "lse_gpu": float(lse.item()), "lse_oracle": float(lseo), "oracle_s": round(t_orc, 2)}
+
+
+def fp64_mode_line(cdms, torch, dev, local, config="c2", steps=5):
+    """Throughput of the FP64 engine (the mode whose weights meet 1e-5 end to end) on a BASELINE config."""
+    cfg = scenes.CONFIGS[config]
+    sc = scenes.make_scene(cfg)
+    stream = torch.cuda.current_stream(local)
+    ctx = cdms.Context(local, stream)
+    scene = cdms.Scene.from_synthetic(sc, precision="fp64")
+    y, eta = synth_measurement(cdms, ctx, scene, sc, torch, dev)
+    m, v = scenes.priors(sc, "nzm")
+    x = torch.as_tensor(scenes.make_particles(cfg), device=dev).contiguous()
+    dsfv = torch.as_tensor(sc.sfv, device=dev).contiguous()
+    for n in range(3):
+        cdms.bp_step(ctx, scene, x, dsfv, y, m, v, eta, 0.1, 0.5, sc.philox_key, n)
+    torch.cuda.synchronize(local)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for n in range(steps):
+        cdms.bp_step(ctx, scene, x, dsfv, y, m, v, eta, 0.1, 0.5, sc.philox_key, 3 + n)
+    b.record(stream)
+    ctx.sync()
+    ms = a.elapsed_time(b) / steps
+    ctx.close()
+    return {"config": f"{config}: J={cfg.J}, S={cfg.S}, {cfg.ny}x{cfg.nv}, nf={cfg.nf}, P={cfg.P}", "dtype": "f64",
+            "ms_per_step": ms, "value": cfg.P * cfg.J * cfg.S / (ms / 1e3), "unit": UNIT, "steps": steps}
 
 
 def oracle_inputs(cfg, sc, orc_mod, n_particles):
@@ -428,15 +472,16 @@ def cpu_baseline(args, cfg, sc, budget_s: float = 15.0):
             "sample": f"oracle bp_step on {n} of {cfg.P} particles of {args.config} (fp64 C, OpenMP), {dt:.2f} s"}
 
 
-def config_dict(args, cfg, P_local, world):
+def config_dict(args, cfg, P_total, world):
     """The workload both arms report (the reference arm times a bounded sample of it, stated in cpu_baseline)."""
     return {"workload": f"{args.config}: J={cfg.J} PAs, K={cfg.K} walls (S={cfg.S}), "
-                        f"{cfg.ny}x{cfg.nv} URA, nf={cfg.nf}, P={P_local}/GPU",
-            "config": args.config, "P_per_gpu": P_local, "P_total": P_local * world, "J": cfg.J,
+                        f"{cfg.ny}x{cfg.nv} URA, nf={cfg.nf}, P={P_total} total (strong scaling)",
+            "config": args.config, "P_total": P_total, "P_per_gpu": P_total // world, "J": cfg.J,
             "K": cfg.K, "ny": cfg.ny, "nv": cfg.nv, "nf": cfg.nf, "Nz": cfg.Nz,
             "wavefront": args.wavefront, "precision": args.precision,
             "step": "predict+loglik+normalize+moments+resample+regularize",
-            "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"dp{world} (particles)"}
+            "l2": "flushed (256 MiB write) between timed steps; particles 48 B x P_total > L2",
+            "parallelism": f"dp{world} (particles)"}
 
 
 def run_reference(args):
@@ -449,6 +494,12 @@ def run_reference(args):
     cfg = scenes.CONFIGS[args.config]
     sc = scenes.make_scene(cfg)
     n = min(cfg.P, args.ref_particles)
+    if n <= 0:  # auto: a per-step sample of ~ref_step_s of oracle work on this host (whole run within minutes)
+        o, y, eta, m, v, x = oracle_inputs(cfg, sc, O, 16)
+        t0 = time.perf_counter()
+        O.Oracle.bp_step(o, x, sc.sfv, y, m, v, eta, 0.1, 0.5, sc.philox_key, 0)
+        per = (time.perf_counter() - t0) / 16
+        n = int(min(cfg.P, max(16, args.ref_step_s / max(per, 1e-9))))
     o, y, eta, m, v, x = oracle_inputs(cfg, sc, O, n)
     for w in range(args.warmup):
         O.Oracle.bp_step(o, x, sc.sfv, y, m, v, eta, 0.1, 0.5, sc.philox_key, w)
@@ -461,9 +512,9 @@ def run_reference(args):
     value = n * cfg.J * cfg.S / dt
     sample = f"oracle bp_step on {n} of {cfg.P} particles of {args.config} per step (fp64 C, OpenMP)"
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": config_dict(args, cfg, args.particles or cfg.P, world),
+            "config": config_dict(args, cfg, p_total_of(args, cfg), world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -678,20 +729,29 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(scenes.CONFIGS))
-    ap.add_argument("--particles", type=int, default=None, help="particles per GPU (default: the config's P)")
+    ap.add_argument("--config", default="c5", choices=sorted(scenes.CONFIGS))
+    ap.add_argument("--particles", type=int, default=None,
+                    help="P_total over all GPUs, strong scaling (default: the config's P; c5: 16M)")
     ap.add_argument("--wavefront", default="spherical", choices=["spherical", "planar_wb", "planar_nb"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--impl", default="cdms", choices=["cdms", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the FP32-weights-vs-oracle and FP64-mode fields")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-particles", type=int, default=2000)
+    ap.add_argument("--ref-particles", type=int, default=0,
+                    help="--impl reference: particles per oracle step (0: sized to ~--ref-step-s seconds per step)")
+    ap.add_argument("--ref-step-s", type=float, default=2.0)
     ap.add_argument("--mode", default="step", choices=["step", "birth"],
                     help="step: the BP step (headline); birth: the F3 birth proposal")
     ap.add_argument("--candidates", type=int, default=1 << 20, help="birth mode: candidates N_g per GPU")
     ap.add_argument("--legacy", type=int, default=2, help="birth mode: legacy PFs L")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "cdms" else args.warmup
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.mode == "birth":
         res = run_birth_reference(args) if args.impl == "reference" else run_birth(args)
     else:

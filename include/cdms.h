@@ -122,6 +122,9 @@ int64_t cdms_launch_count(cdms_ctx ctx);
  * kernel time (ms) and the number of launches since the last enable; it does not disable timing. */
 cdms_status cdms_timing_enable(cdms_ctx ctx, int on);
 cdms_status cdms_timing_read(cdms_ctx ctx, double* loglik_ms, int64_t* n_launches);
+/* The same events split by kernel: ms[0] the correlation kernel (row A3), ms[1] the Gram kernel (row A4; 0 when the
+ * engine computes both in one kernel), ms[2] the S x S assembly (row A5), summed over *n_launches batches. */
+cdms_status cdms_timing_read_stages(cdms_ctx ctx, double ms[3], int64_t* n_launches);
 
 /* NCCL bootstrap: rank 0 calls cdms_get_unique_id, broadcasts the 128 bytes (e.g. through
  * torch.distributed), then every rank calls cdms_comm_init.  nranks = 1 is allowed. */

@@ -64,6 +64,7 @@ def lib() -> C.CDLL:
             "cdms_launch_count": ([vp], i64),
             "cdms_timing_enable": ([vp, C.c_int], C.c_int),
             "cdms_timing_read": ([vp, C.POINTER(C.c_double), C.POINTER(i64)], C.c_int),
+            "cdms_timing_read_stages": ([vp, C.POINTER(C.c_double), C.POINTER(i64)], C.c_int),
             "cdms_get_unique_id": ([C.c_char_p], C.c_int),
             "cdms_comm_init": ([vp, C.c_char_p, C.c_int, C.c_int], C.c_int),
             "cdms_layout": ([vp, C.POINTER(SceneC), vp, vp, vp, vp], C.c_int),
@@ -98,6 +99,7 @@ def lib() -> C.CDLL:
 def exported_symbols() -> list[str]:
     return [n for n in ["cdms_create", "cdms_destroy", "cdms_set_stream", "cdms_last_error", "cdms_sync",
                         "cdms_reserve", "cdms_launch_count", "cdms_timing_enable", "cdms_timing_read",
+                        "cdms_timing_read_stages",
                         "cdms_get_unique_id", "cdms_comm_init", "cdms_layout",
                         "cdms_loglik", "cdms_loglik_terms", "cdms_weights_normalize", "cdms_moments", "cdms_resample", "cdms_bp_step",
                         "cdms_response", "cdms_moment_match", "cdms_resample_plan", "cdms_birth_proposal",
@@ -205,6 +207,12 @@ class Context:
         ms, n = C.c_double(), C.c_int64()
         self.check(lib().cdms_timing_read(self.h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    def timing_read_stages(self) -> tuple[list[float], int]:
+        """([correlation, Gram, assembly] kernel ms summed, number of likelihood batches) since timing_enable."""
+        ms, n = (C.c_double * 3)(), C.c_int64()
+        self.check(lib().cdms_timing_read_stages(self.h, ms, C.byref(n)))
+        return [ms[0], ms[1], ms[2]], n.value
 
     def reserve(self, scene: Scene, P_local: int):
         self.check(lib().cdms_reserve(self.h, C.byref(scene.c), int(P_local)))

@@ -56,8 +56,9 @@ struct cdms_ctx_s {
                                  // A/B only; default FFT)
   int taylor_lanes = -1;         // K1T correlation kernel: -1 by P J (tay_lanes), 1 lane groups, 0 thread per
                                  // particle (CDMS_TAY_LANES=1 / 0, A/B only)
-  std::vector<cudaEvent_t> ev_pool;
-  size_t ev_used = 0;
+  std::vector<cudaEvent_t> ev_pool;  // timing: 4 events per likelihood batch (before / between the correlation and
+  size_t ev_used = 0;                // Gram kernels / before / after the assembly)
+  std::vector<uint8_t> ev_gram_first;  // per batch: 1 when the Gram kernel runs first (tensor-core path)
 };
 
 namespace {
@@ -494,18 +495,22 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     if (a.grid < 1) return fail(ctx, CDMS_ECUDA, "corr_kernel occupancy query failed");
     a.sched = sched;
     a.no_gram = no_gram ? 1 : 0;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     if (ctx->timing) {
-      while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+      while (ctx->ev_pool.size() < ctx->ev_used + 4) {
         cudaEvent_t e;
         CUDA_TRY(ctx, cudaEventCreate(&e));
         ctx->ev_pool.push_back(e);
       }
-      e0 = ctx->ev_pool[ctx->ev_used];
-      e1 = ctx->ev_pool[ctx->ev_used + 1];
-      ctx->ev_used += 2;
-      CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));
+      for (int k = 0; k < 4; ++k) ev[k] = ctx->ev_pool[ctx->ev_used + k];
+      ctx->ev_used += 4;
+      ctx->ev_gram_first.push_back(nbt ? 1 : 0);
+      CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
     }
+    auto mark = [&](int k) -> cdms_status {
+      if (ctx->timing) CUDA_TRY(ctx, cudaEventRecord(ev[k], ctx->stream));
+      return CDMS_OK;
+    };
     if (nbt) {
       NbArgs na;
       na.particles = a.particles;
@@ -520,6 +525,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       na.n_tiles = na.n_tiles_j * sd.J;
       na.diag_only = no_gram ? 1 : 0;
       CUDA_TRY(ctx, launch_nb_gram(sd, na, pflag, ctx->stream));
+      COLL_TRY(mark(1));
       CUDA_TRY(ctx, launch_nb_corr(sd, nbp, na, ctx->num_sms, ctx->stream));
       ctx->launches += 1;
     } else if (tay) {
@@ -531,13 +537,15 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       if (k1g) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));
       CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, pflag,
                                     no_gram ? 1 : 0, tlanes, ctx->stream));
+      COLL_TRY(mark(1));
       if (!no_gram && !k1g)
         CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, ctx->stream));
       ctx->launches += no_gram ? 0 : 1;
     } else {
       CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
+      COLL_TRY(mark(1));
     }
-    if (ctx->timing) CUDA_TRY(ctx, cudaEventRecord(e1, ctx->stream));
+    COLL_TRY(mark(2));
     AsmArgs s;
     s.terms = terms;
     s.pflag = pflag;
@@ -550,6 +558,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     s.flags = ctx->d_flags;
     s.P = nb;
     CUDA_TRY(ctx, launch_assemble(sd, s, ctx->stream));
+    COLL_TRY(mark(3));
     ctx->launches += 2;
   }
   return CDMS_OK;
@@ -779,21 +788,33 @@ cdms_status cdms_timing_enable(cdms_ctx ctx, int on) {
   if (!ctx) return CDMS_EINVAL;
   ctx->timing = on != 0;
   ctx->ev_used = 0;
+  ctx->ev_gram_first.clear();
+  return CDMS_OK;
+}
+
+cdms_status cdms_timing_read_stages(cdms_ctx ctx, double* ms, int64_t* n_launches) {
+  if (!ctx || !ms || !n_launches) return CDMS_EINVAL;
+  DeviceGuard g(ctx->device);
+  ms[0] = ms[1] = ms[2] = 0.0;
+  for (size_t i = 0, b = 0; i + 3 < ctx->ev_used; i += 4, ++b) {
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev_pool[i + 3]));
+    float t[3] = {0.f, 0.f, 0.f};
+    for (int k = 0; k < 3; ++k) CUDA_TRY(ctx, cudaEventElapsedTime(&t[k], ctx->ev_pool[i + k], ctx->ev_pool[i + k + 1]));
+    const bool gf = ctx->ev_gram_first[b] != 0;
+    ms[0] += gf ? t[1] : t[0];  // correlation kernel
+    ms[1] += gf ? t[0] : t[1];  // Gram kernel
+    ms[2] += t[2];              // assembly
+  }
+  *n_launches = (int64_t)(ctx->ev_used / 4);
   return CDMS_OK;
 }
 
 cdms_status cdms_timing_read(cdms_ctx ctx, double* loglik_ms, int64_t* n_launches) {
   if (!ctx || !loglik_ms || !n_launches) return CDMS_EINVAL;
-  DeviceGuard g(ctx->device);
-  double tot = 0.0;
-  for (size_t i = 0; i + 1 < ctx->ev_used; i += 2) {
-    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev_pool[i + 1]));
-    float ms = 0.f;
-    CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev_pool[i], ctx->ev_pool[i + 1]));
-    tot += ms;
-  }
-  *loglik_ms = tot;
-  *n_launches = (int64_t)(ctx->ev_used / 2);
+  double ms[3];
+  cdms_status st = cdms_timing_read_stages(ctx, ms, n_launches);
+  if (st) return st;
+  *loglik_ms = ms[0] + ms[1];
   return CDMS_OK;
 }
 

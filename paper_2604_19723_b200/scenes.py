@@ -52,8 +52,14 @@ PA_POS = np.array([
     [5.0, 1.75, 0.5],
     [0.5, -1.5, 0.5],
     [0.5, 5.0, 0.5],
+    # PA5..PA8 (J > 4, only the J = 8 edge-shape tests use them): the room's corners at 1.5 m, facing inwards,
+    # on the inner side of every wall k1..k8
+    [-4.0, -1.5, 1.5],
+    [5.0, -1.5, 1.5],
+    [4.5, 4.2, 1.5],
+    [-3.8, 4.2, 1.5],
 ])
-PA_YAW_DEG = np.array([0.0, 180.0, 90.0, -90.0])
+PA_YAW_DEG = np.array([0.0, 180.0, 90.0, -90.0, 45.0, 135.0, -135.0, -45.0])
 PA_TILT_DEG = 10.0
 
 P_TRUE = np.array([0.7, 1.9, 0.2])
@@ -201,13 +207,15 @@ def _particle_block(cfg: Config, block: int, n: int, spread: float = 0.05) -> np
 
 def make_particles(cfg: Config, start: int = 0, count: Optional[int] = None) -> np.ndarray:
     """Particles [start, start+count) of the config's global set, float64 [count][6]
-    (x, y, z, vx, vy, vz).  Identical rows whatever the shard boundaries."""
+    (x, y, z, vx, vy, vz).  Identical rows whatever the shard boundaries.  Requests reaching past cfg.P (a larger
+    particle set than the config's) draw whole blocks of BLOCK rows throughout."""
     if count is None:
         count = cfg.P - start
     out = np.empty((count, 6))
+    end = cfg.P if start + count <= cfg.P else start + count + BLOCK
     b0, b1 = start // BLOCK, (start + count - 1) // BLOCK if count > 0 else start // BLOCK - 1
     for b in range(b0, b1 + 1):
-        lo, hi = b * BLOCK, min((b + 1) * BLOCK, cfg.P)
+        lo, hi = b * BLOCK, min((b + 1) * BLOCK, end)
         blk = _particle_block(cfg, b, hi - lo)
         s, e = max(lo, start), min(hi, start + count)
         out[s - start:e - start] = blk[s - lo:e - lo]

@@ -121,7 +121,7 @@ def test_loglik_c1_all_particles(cd, ctx, orc, precision, wf):
     dict(J=2, K=3, ny=3, nv=5, nf=100, P=77),        # ragged antennas (15), ragged segment, ragged tile
     dict(J=3, K=0, ny=2, nv=2, nf=300, P=65),        # S = 1, two chunks, ragged chunk
     dict(J=1, K=8, ny=8, nv=8, nf=520, P=40),        # S = 9, 3 chunks, ragged segment
-    dict(J=4, K=1, ny=1, nv=1, nf=1, P=33),          # single element, single subcarrier, J = 4
+    dict(J=8, K=1, ny=1, nv=1, nf=1, P=33),          # single element, single subcarrier, J = 8 (the ABI maximum)
     dict(J=1, K=5, ny=16, nv=16, nf=64, P=31),       # 32 antenna blocks
 ])
 def test_loglik_ragged_shapes(cd, ctx, orc, precision, shape):

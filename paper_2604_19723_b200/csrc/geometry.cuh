@@ -327,9 +327,25 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// sin(pi t) for the Dirichlet numerator, t = N xr reduced mod 2 to [-1, 1]: MUFU (absolute error <= 2^-21.4) when
+// |t| > 1/4, where that is <= 5e-7 of the value; for |t| <= 1/4 (near-equal delays of the pair, N |xr| small) the
+// relative accuracy matters -- D_N ~ N there and every antenna of the pair sees about the same x, so a relative
+// numerator error adds coherently into G_ab (tests/test_k1t_terms_gpu.py, equal-delay particles) -- and the odd
+// Taylor polynomial pi t S(pi t), S(z) = 1 - z^2/6 + z^4/120 - z^6/5040 + z^8/362880 (relative error < 3e-9 at
+// pi/4) replaces it.  The branch is taken with probability ~1/(2N) per (pair, antenna).
+__device__ __forceinline__ float dirichlet_num(float t) {
+  float num;
+  if (fabsf(t) <= 0.25f) {
+    const float z = 3.14159265358979f * t, z2 = z * z;
+    num = z * fmaf(z2, fmaf(z2, fmaf(z2, fmaf(z2, 1.f / 362880, -1.f / 5040), 1.f / 120), -1.f / 6), 1.f);
+  } else {
+    num = __sinf(3.14159265358979f * t);
+  }
+  return num;
+}
 // The Dirichlet factor of gram_term_f alone (the caller supplies the carrier e^{j2pi dd f_c/c}).
 __device__ __forceinline__ float gram_dirichlet_f(const SceneDev& sc, float dd, const GramPairF& gp) {
-  const float df_c = sc.df_cf, Nf = sc.nf_f, c6N = sc.c6N_f;
+  const float df_c = sc.df_cf, Nf = sc.nf_f;
   // rint by the 1.5 * 2^23 magic constant (FADDs, |x| << 2^22) rather than FRND: the Gram kernels that call this
   // per (pair, antenna) are XU-bound (profiles/r01_k1t_lanes.txt); the sum's low mantissa bit is n2's parity
   constexpr float M = 12582912.f;
@@ -338,40 +354,23 @@ __device__ __forceinline__ float gram_dirichlet_f(const SceneDev& sc, float dd, 
   const float xr = x - (xm - M);
   float t = Nf * xr;
   t = fmaf(-2.f, (fmaf(0.5f, t, M) - M), t);
-  const float num = __sinf(3.14159265358979f * t);
+  const float num = dirichlet_num(t);
   const float u = 3.14159265358979f * xr, u2 = u * u;
   const float den = u * fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, -1.f / 39916800, 1.f / 362880), -1.f / 5040),
                                                 1.f / 120), -1.f / 6), 1.f);
   float D = num * rcp_approx(den);
-  const float Ds = Nf * fmaf(-c6N, xr * xr, 1.f);
-  D = (fabsf(xr) < 1e-6f) ? Ds : D;
+  D = (fabsf(xr) < 1e-30f) ? Nf : D;  // D_N(0) = N (C-amb-13); num and den are relatively accurate down to tiny xr
   const uint32_t par = ((uint32_t)__float_as_int(xm) << 31) ^ gp.nbpar;
   return __int_as_float(__float_as_int(D) ^ (int)(par & sc.evenN_mask));
 }
 __device__ __forceinline__ void gram_term_f(const SceneDev& sc, float dd, const GramPairF& gp, float& gr,
                                             float& gi) {
-  const float fc_c = sc.fc_cf, df_c = sc.df_cf, Nf = sc.nf_f, c6N = sc.c6N_f;
-  const uint32_t evenN_mask = sc.evenN_mask;
+  const float fc_c = sc.fc_cf;
   float ph = dd * fc_c;
   ph -= rintf(ph);
   float sn, cs;
   __sincosf(6.28318530717958647692f * ph, &sn, &cs);
-  const float x = fmaf(dd, df_c, gp.xbr);
-  const float n2 = rintf(x);
-  const float xr = x - n2;
-  float t = Nf * xr;
-  t = fmaf(-2.f, rintf(0.5f * t), t);
-  const float num = __sinf(3.14159265358979f * t);
-  const float u = 3.14159265358979f * xr, u2 = u * u;
-  // sin(pi xr), |xr| <= 1/2: odd Taylor polynomial to (pi xr)^11 (error < 6e-8 at pi/2)
-  const float den = u * fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, -1.f / 39916800, 1.f / 362880), -1.f / 5040),
-                                                1.f / 120), -1.f / 6), 1.f);
-  float D = num * rcp_approx(den);
-  const float Ds = Nf * fmaf(-c6N, xr * xr, 1.f);  // N (1 - pi^2/6 (N^2 - 1) xr^2)
-  D = (fabsf(xr) < 1e-6f) ? Ds : D;
-  // (-1)^{(nb + n2)(N-1)}: parity of the integer-valued n2 from the mantissa after adding 1.5 * 2^23
-  const uint32_t par = ((uint32_t)__float_as_int(n2 + 12582912.f) << 31) ^ gp.nbpar;
-  D = __int_as_float(__float_as_int(D) ^ (int)(par & evenN_mask));
+  const float D = gram_dirichlet_f(sc, dd, gp);
   gr = fmaf(D, cs, gr);
   gi = fmaf(D, sn, gi);
 }

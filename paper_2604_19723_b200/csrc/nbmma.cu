@@ -380,7 +380,7 @@ __global__ void nb_prep_kernel(const __grid_constant__ SceneDev sc, const NbPlan
 
 // D_N(x) = sin(pi N x) / sin(pi x) (C-amb-13): x = n + xr, D_N(x) = (-1)^{n (N-1)} D_N(xr); both sines reduced in
 // fp64 (sin(pi N xr) = sin(pi t), t = N xr mod 2 in [-1, 1]) and evaluated in fp32 (relative error ~1e-7, the
-// precision of K1's per-antenna fp32 Gram terms); second-order series below |xr| = 1e-6.
+// precision of K1's per-antenna fp32 Gram terms); second-order series below |N xr| = 1e-4 (truncation < 1e-15).
 __device__ __forceinline__ float dirichlet_rr(double x, int N) {
   const double n = rint(x);
   const double xr = x - n;
@@ -388,7 +388,7 @@ __device__ __forceinline__ float dirichlet_rr(double x, int N) {
   t -= 2.0 * rint(0.5 * t);
   const float fx = (float)xr;
   float d;
-  if (fabsf(fx) < 1e-6f) {
+  if (fabsf(fx) * (float)N < 1e-4f) {
     d = (float)N * (1.f - (float)(PI * PI / 6.0) * ((float)N * (float)N - 1.f) * fx * fx);
   } else {
     d = sinpif((float)t) / sinpif(fx);

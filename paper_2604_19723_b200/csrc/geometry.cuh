@@ -334,14 +334,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // Taylor polynomial pi t S(pi t), S(z) = 1 - z^2/6 + z^4/120 - z^6/5040 + z^8/362880 (relative error < 3e-9 at
 // pi/4) replaces it.  The branch is taken with probability ~1/(2N) per (pair, antenna).
 __device__ __forceinline__ float dirichlet_num(float t) {
-  float num;
-  if (fabsf(t) <= 0.25f) {
-    const float z = 3.14159265358979f * t, z2 = z * z;
-    num = z * fmaf(z2, fmaf(z2, fmaf(z2, fmaf(z2, 1.f / 362880, -1.f / 5040), 1.f / 120), -1.f / 6), 1.f);
-  } else {
-    num = __sinf(3.14159265358979f * t);
-  }
-  return num;
+  // selects, not a branch: the callers' pair loops are fully unrolled and a branch per term would serialize them
+  const float z = 3.14159265358979f * t, z2 = z * z;
+  const float ps = z * fmaf(z2, fmaf(z2, fmaf(z2, fmaf(z2, 1.f / 362880, -1.f / 5040), 1.f / 120), -1.f / 6), 1.f);
+  return fabsf(t) <= 0.25f ? ps : __sinf(z);
 }
 // The Dirichlet factor of gram_term_f alone (the caller supplies the carrier e^{j2pi dd f_c/c}).
 __device__ __forceinline__ float gram_dirichlet_f(const SceneDev& sc, float dd, const GramPairF& gp) {

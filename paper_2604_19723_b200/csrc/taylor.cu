@@ -458,9 +458,32 @@ __device__ __forceinline__ bool tay_component(const SceneDev& sc, int j, const d
   R64 = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
   return R64 > 0.0;
 }
+// D_N(x) for |x| <= ~0.56 without reducing x (FAST Gram path): the pair's integer part nb is taken out once per pair
+// in fp64 (its sign (-1)^{nb (N - 1)} applied to the pair total) and the per-antenna offset e = dd df/c is small
+// (sc.small_step >= 1: |e| <= 0.064), so x = xb + e stays inside the validity range of the denominator polynomial
+// sin(pi x) = u S(u^2), u = pi x, S to u^10 (relative error < 1e-6 at 0.56, < 6e-8 at 0.52).  Numerator sin(pi t),
+// t = N x reduced mod 2: MUFU, or for |t| <= 1/4 the odd polynomial (dirichlet_num's reasoning); at x = 0 D = N.
+__device__ __forceinline__ float dirichlet_fast(float x, float Nf) {
+  constexpr float M = 12582912.f;
+  float t = Nf * x;
+  t = fmaf(-2.f, (fmaf(0.5f, t, M) - M), t);
+  const float u = 3.14159265358979f * x, u2 = u * u;
+  const float den = u * fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, fmaf(u2, -1.f / 39916800, 1.f / 362880), -1.f / 5040),
+                                                1.f / 120), -1.f / 6), 1.f);
+  // branch-free (selects): a divergent branch per (pair, antenna) fences the fully unrolled pair loop into serial
+  // pieces and costs its ILP (measured: c5 Gram 280 -> 310 ms with the branch)
+  const float z = 3.14159265358979f * t, z2 = z * z;
+  const float ps = z * fmaf(z2, fmaf(z2, fmaf(z2, fmaf(z2, 1.f / 362880, -1.f / 5040), 1.f / 120), -1.f / 6), 1.f);
+  const float num = fabsf(t) <= 0.25f ? ps : __sinf(z);
+  const float D = num * rcp_approx(den);
+  return fabsf(x) < 1e-30f ? Nf : D;
+}
 // Pairs q in [Q0, Q1) (row order (0,1), (0,2), ..., (1,2), ...): large S splits the pairs over blockIdx.z so each
 // thread holds only its part's accumulators (S = 9: 255 registers and 73 KB of totals per block for all 36 pairs).
-template <int S, int Q0, int Q1>
+// FAST (sc.small_step >= 1, every BASELINE config): per pair the fp64 delay base (R_a - R_b) df/c = nb + xb is reduced
+// once (xb in registers, nb's sign at the end) and per antenna D = dirichlet_fast(xb + dd df/c): no per-antenna
+// range reduction or parity bookkeeping.  Else per antenna gram_dirichlet_f (reduction and parity per term).
+template <int S, int Q0, int Q1, bool FAST>
 __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* __restrict__ tmpl,
                                               const double* __restrict__ particles, int64_t P, int pstride,
                                               const double* __restrict__ sfv, int sfv_pp, double2* __restrict__ terms,
@@ -486,10 +509,24 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
     if (!live) R64[s] = 1.0;
     Rf[s] = (float)R64[s];
     iR[s] = 1.f / Rf[s];
-    const double xs = R64[s] * sc.df_c, ns = rint(xs), us = xs - ns;
-    uh[s] = (float)us;
-    ul[s] = (float)(us - (double)uh[s]);
-    npar[s] = (int)((long long)ns & 1);
+    if (!FAST) {
+      const double xs = R64[s] * sc.df_c, ns = rint(xs), us = xs - ns;
+      uh[s] = (float)us;
+      ul[s] = (float)(us - (double)uh[s]);
+      npar[s] = (int)((long long)ns & 1);
+    }
+  }
+  float xb[FAST ? NP : 1];  // FAST: per pair the centred fraction of (R_a - R_b) df/c (fp64 difference, one rounding)
+  if (FAST) {
+#pragma unroll
+    for (int a = 0; a < S; ++a)
+#pragma unroll
+      for (int b = 0; b < S; ++b) {
+        if (b <= a) continue;
+        const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
+        if (q < 0 || q >= NP) continue;
+        xb[q] = (float)frac_c((R64[a] - R64[b]) * sc.df_c);
+      }
   }
 #pragma unroll
   for (int q = 0; q < NP; ++q) gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(0.0, 0.0);
@@ -523,10 +560,15 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
           if (b <= a) continue;
           const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
           if (q < 0 || q >= NP) continue;
-          GramPairF gp;
-          gp.xbr = (uh[a] - uh[b]) + (ul[a] - ul[b]);
-          gp.nbpar = (uint32_t)((npar[a] ^ npar[b]) & 1) << 31;
-          const float D = gram_dirichlet_f(sc, dl[a] - dl[b], gp);
+          float D;
+          if (FAST) {
+            D = dirichlet_fast(fmaf(dl[a] - dl[b], sc.df_cf, xb[q]), sc.nf_f);
+          } else {
+            GramPairF gp;
+            gp.xbr = (uh[a] - uh[b]) + (ul[a] - ul[b]);
+            gp.nbpar = (uint32_t)((npar[a] ^ npar[b]) & 1) << 31;
+            D = gram_dirichlet_f(sc, dl[a] - dl[b], gp);
+          }
           const float cr = fmaf(er[a], er[b], ei[a] * ei[b]), ci = fmaf(ei[a], er[b], -er[a] * ei[b]);  // E_a conj(E_b)
           gr[q] = fmaf(D, cr, gr[q]);
           gi[q] = fmaf(D, ci, gi[q]);
@@ -554,8 +596,12 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
       if (!live || a0 != 0) continue;
       double sn, cs;
       sincospi(2.0 * frac_c((R64[a] - R64[b]) * sc.fc_c), &sn, &cs);
+      double g2 = sc.pathloss ? (sc.lambda / (4.0 * PI * R64[a])) * (sc.lambda / (4.0 * PI * R64[b])) : 1.0;
+      if (FAST && ((sc.nf - 1) & 1)) {  // D_N(nb + x) = (-1)^{nb (N - 1)} D_N(x) (C-amb-13)
+        const double d = (R64[a] - R64[b]) * sc.df_c;
+        if ((long long)rint(d) & 1) g2 = -g2;
+      }
       const double vr = cs * acc.x - sn * acc.y, vi = cs * acc.y + sn * acc.x;
-      const double g2 = sc.pathloss ? (sc.lambda / (4.0 * PI * R64[a])) * (sc.lambda / (4.0 * PI * R64[b])) : 1.0;
       terms[(p * J + j) * T + S + b * (b + 1) / 2 + a] = make_double2(vr * g2, -vi * g2);
     }
   }
@@ -564,7 +610,7 @@ template <int S>
 // measured: S = 9 in 3 parts 58.8 vs 59.8 ms (c5 shard); S = 7 in 2 parts 9.16 vs 8.87 ms (c3: one part already fits
 // 168 registers, splitting only repeats the per-component work)
 __host__ __device__ constexpr int tay_gram_parts() { return S >= 9 ? 3 : (S == 8 ? 2 : 1); }
-template <int S>
+template <int S, bool FAST>
 __global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? 3 : 1))  // S >= 7: 3 blocks (12 warps) per SM, <= 168 registers
     tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
                     const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
@@ -572,20 +618,20 @@ __global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? 3 : 1))  // S >= 7: 3 blo
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>(), H = NP / NPART;
   extern __shared__ double2 gsum[];
   if constexpr (NPART == 1) {
-    tay_gram_part<S, 0, NP>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+    tay_gram_part<S, 0, NP, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
   } else if constexpr (NPART == 2) {
     if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, 0, H, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
     else
-      tay_gram_part<S, H, NP>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, H, NP, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
   } else {
     static_assert(NPART == 3, "");
     if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, 0, H, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
     else if (blockIdx.z == 1)
-      tay_gram_part<S, H, 2 * H>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, H, 2 * H, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
     else
-      tay_gram_part<S, 2 * H, NP>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, 2 * H, NP, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
   }
 }
 template <int S>
@@ -593,13 +639,21 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
                                      int pstride, const double* sfv, int sfv_pp, double2* terms, cudaStream_t st) {
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>();
   const size_t smem = (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2);  // the larger part
-  cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#ifndef CDMS_GRAM_FAST
+#define CDMS_GRAM_FAST 1
+#endif
+  const bool fast = CDMS_GRAM_FAST && sc.small_step >= 1;
+  cudaError_t e = cudaFuncSetAttribute(fast ? tay_gram_kernel<S, true> : tay_gram_kernel<S, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // antennas over 2 lanes per particle when P J threads are fewer than ~2 resident waves (measured at c2: 1 lane
   // 0.391, 2 lanes 0.388, 4 lanes 0.405, 8 lanes 0.448 ms per step; at P = 1.4e5 2 lanes 0.494 vs 4 lanes 0.517)
   const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 1 : 0;
   dim3 grid((unsigned)(((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK), sc.J, NPART);
-  tay_gram_kernel<S><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit);
+  if (fast)
+    tay_gram_kernel<S, true><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit);
+  else
+    tay_gram_kernel<S, false><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit);
   return cudaGetLastError();
 }
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,

@@ -762,3 +762,117 @@ int orc_birth_proposal(const orc_scene* sc, const double* x_hat, const double* s
   free(psi);
   return st;
 }
+
+/* ------------------------------------------------------------------ F1 PF-particle update (S-V) */
+
+/* a^H A^{-1} b with A = eta I + M M^H through the inversion lemma (eq. S-Maha-expression):
+ *   a^H b / eta - (a^H M) (I + M^H M / eta)^{-1} (M^H b) / eta^2.
+ * M = [m_1 .. m_L] (columns of length nz); Kc = the Cholesky factor (lower, row-major L x L) of I + M^H M / eta. */
+static double complex orc_maha(const double complex* a, const double complex* b, const double complex* M, int L,
+                               const double complex* Kc, double eta, size_t nz) {
+  double complex ab = 0.0, u[16], v[16];
+  for (size_t n = 0; n < nz; ++n) ab += conj(a[n]) * b[n];
+  for (int l = 0; l < L; ++l) {
+    double complex am = 0.0, mb = 0.0;
+    for (size_t n = 0; n < nz; ++n) {
+      am += conj(a[n]) * M[(size_t)l * nz + n];
+      mb += conj(M[(size_t)l * nz + n]) * b[n];
+    }
+    u[l] = conj(am);  /* M^H a */
+    v[l] = mb;        /* M^H b */
+  }
+  /* (M^H a)^H K^{-1} (M^H b) = (L^{-1} M^H a)^H (L^{-1} M^H b) */
+  for (int r = 0; r < L; ++r) {
+    for (int c = 0; c < r; ++c) {
+      u[r] -= Kc[r * L + c] * u[c];
+      v[r] -= Kc[r * L + c] * v[c];
+    }
+    u[r] /= creal(Kc[r * L + r]);
+    v[r] /= creal(Kc[r * L + r]);
+  }
+  double complex q = 0.0;
+  for (int l = 0; l < L; ++l) q += conj(u[l]) * v[l];
+  return ab / eta - q / (eta * eta);
+}
+
+/* F1: the approximate PF update message kappa~(phi_p, r; z^(j)) (Supplement S-V "PF State Update
+ * Message") evaluated at the particles of one PF s, and the PF weights with the normalization constant
+ * M_{y,s,n} (Supplement S-IV).  Readings (C-amb-F1a..d):
+ *   - the PF particles are paired with the MT particles by index (C-amb-8): psi_p = psi^(j)(x_p, phi_p), the response
+ *     of PA j at MT particle x_p through the wall of SFV phi_p (component 1 of orc_response);
+ *   - covariance C^kappa = r q_p psi_p psi_p^H + A, A = eta_j I + M M^H, q_p = (gamma_p +
+ *     |mu_p|^2 (1 - zeta_j)) zeta_j; mean mu^kappa = r zeta_j mu_p psi_p + mu3_j;
+ *   - the particle-independent terms mu3_j = sum_{s' != s} mu~_3 and the columns m_l of M (l < L) are inputs
+ *     ("precomputed once");
+ *   - det A and pi^Nz cancel between r = 1 and the H0 branch r = 0, so the per-particle result
+ *     is logr_p = log w_alpha_p + sum_j [log kappa~(phi_p, 1; z_j) - log kappa~(., 0; z_j)], with
+ *       log kappa~(phi_p, 1) - log kappa~(., 0) = q |psi^H A^-1 e|^2 / (1 + q psi^H A^-1 psi) - e^H A^-1 e
+ *                                                - ln(1 + q psi^H A^-1 psi) + e0^H A^-1 e0,
+ *     e = z_j - mu^kappa(phi_p, 1), e0 = z_j - mu3_j (the determinant lemma and the inversion lemma of);
+ *   - normalization in units of prod_j kappa~(., 0): M_y = sum_p e^{logr_p} + (1 - sum_p w_alpha_p) (S-IV),
+ *     PF weights w_p = e^{logr_p} / M_y, posterior existence sum_p w_p (eq. existenceProb).
+ * y, mu3: [J][Nz]; mcols: [J][L][Nz]; x: [P][pstride]; phi: [P][3].  out[0] = log M_y, out[1] = existence. */
+int orc_pf_update(const orc_scene* sc, const double* x, int64_t P, int pstride, const double* phi,
+                  const double* walpha, const double complex* mu, const double* gamma, const double* zeta,
+                  const double* eta, const double complex* y, const double complex* mu3,
+                  const double complex* mcols, int L, double* logr, double* w, double* out) {
+  int J = sc->J;
+  size_t nz = (size_t)sc->nf * sc->ny * sc->nv;
+  if (P <= 0 || L < 0 || L > 15) return ORC_EINVAL;
+  int status = ORC_OK;
+  for (int64_t p = 0; p < P; ++p) logr[p] = log(walpha[p]);
+  double complex* e0 = (double complex*)malloc(sizeof(double complex) * nz);
+  double complex* psi = (double complex*)malloc(sizeof(double complex) * nz);
+  double complex* e = (double complex*)malloc(sizeof(double complex) * nz);
+  double complex Kc[256];
+  for (int j = 0; j < J && status == ORC_OK; ++j) {
+    const double complex* M = mcols + (size_t)j * L * nz;
+    /* the H0 error vector and the Cholesky factor of I + M^H M / eta (particle independent) */
+    for (size_t n = 0; n < nz; ++n) e0[n] = y[(size_t)j * nz + n] - mu3[(size_t)j * nz + n];
+    for (int a = 0; a < L; ++a)
+      for (int b = 0; b < L; ++b) {
+        double complex g = 0.0;
+        for (size_t n = 0; n < nz; ++n) g += conj(M[(size_t)a * nz + n]) * M[(size_t)b * nz + n];
+        Kc[a * L + b] = (a == b ? 1.0 : 0.0) + g / eta[j];
+      }
+    if (L > 0 && orc_cholesky(Kc, L)) { status = ORC_EINVAL; break; }
+    double t0 = creal(orc_maha(e0, e0, M, L, Kc, eta[j], nz));
+    for (int64_t p = 0; p < P && status == ORC_OK; ++p) {
+      int st = orc_response(sc, x + p * pstride, j, 1, phi + 3 * p, sc->wavefront, psi);
+      if (st) { status = st; logr[p] = -INFINITY; continue; }
+      double complex c = zeta[j] * mu[p];
+      for (size_t n = 0; n < nz; ++n) e[n] = e0[n] - c * psi[n];   /* e = z - mu^kappa(phi_p, 1) */
+      double beta = creal(orc_maha(psi, psi, M, L, Kc, eta[j], nz));
+      double complex b = orc_maha(psi, e, M, L, Kc, eta[j], nz);
+      double t1 = creal(orc_maha(e, e, M, L, Kc, eta[j], nz));
+      double q = (gamma[p] + creal(mu[p] * conj(mu[p])) * (1.0 - zeta[j])) * zeta[j];
+      double den = 1.0 + q * beta;
+      logr[p] += q * creal(b * conj(b)) / den - t1 - log(den) + t0;
+    }
+  }
+  free(e0); free(psi); free(e);
+  if (status) return status;
+  /* M_y = sum_p e^{logr_p} + (1 - sum_p w_alpha_p), in index order with the max taken out */
+  double mx = -INFINITY, sa = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    if (logr[p] > mx) mx = logr[p];
+    sa += walpha[p];
+  }
+  double h0 = 1.0 - sa;
+  if (h0 < 0.0) h0 = 0.0;
+  double s = 0.0;
+  if (mx > -INFINITY)
+    for (int64_t p = 0; p < P; ++p) s += exp(logr[p] - mx);
+  double logM;
+  if (mx == -INFINITY) logM = log(h0);
+  else logM = mx + log(s + h0 * exp(-mx));
+  double ex = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    double wp = exp(logr[p] - logM);
+    if (w) w[p] = wp;
+    ex += wp;
+  }
+  out[0] = logM;
+  out[1] = ex;
+  return ORC_OK;
+}

@@ -188,6 +188,25 @@ class Oracle:
                                       _d(mu), _d(cov), C.byref(ist))
         return st, pb, cand, mu, cov.reshape(3, 3), int(ist.value)
 
+    def pf_update(self, particles, phi, walpha, mu, gamma, zeta, eta, y, mu3, mcols):
+        """F1: (status, logr [P], w [P], log M_y, existence) of the PF update message kappa~ at the paired PF particles
+        (orc_pf_update).  y, mu3: [J][Nz]; mcols: [J][L][Nz]."""
+        x = _f64(particles)
+        P, pstride = x.shape
+        phi = _f64(phi).reshape(P, 3)
+        mc = _c128(mcols).reshape(self.J, -1, self.Nz)
+        L = mc.shape[1]
+        y = _c128(y).reshape(self.J, self.Nz)
+        mu3 = _c128(mu3).reshape(self.J, self.Nz)
+        mu = _c128(mu).reshape(P)
+        logr, w, out = np.zeros(P), np.zeros(P), np.zeros(2)
+        st = lib().orc_pf_update(C.byref(self.sc), _d(x), C.c_int64(P), C.c_int(pstride), _d(phi),
+                                 _d(_f64(walpha)), mu.ctypes.data_as(C.c_void_p), _d(_f64(gamma)),
+                                 _d(_f64(zeta)), _d(_f64(eta)), y.ctypes.data_as(C.c_void_p),
+                                 mu3.ctypes.data_as(C.c_void_p), mc.ctypes.data_as(C.c_void_p), C.c_int(L),
+                                 _d(logr), _d(w), _d(out))
+        return st, logr, w, float(out[0]), float(out[1])
+
     def bp_step(self, particles, sfv, y, m, v, eta, T, sigma_v, key, step, regularize=True):
         x = _f64(particles).copy()
         P = x.shape[0]

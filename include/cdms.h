@@ -208,6 +208,29 @@ cdms_status cdms_birth_proposal(cdms_ctx ctx, const cdms_scene* scene, const dou
                                 const void* d_y, const double* h_box, int64_t N_g, uint64_t key,
                                 uint64_t counter, double* d_out, double* d_pb, double* d_cand);
 
+/* F1: the approximate PF update message kappa~ of one PF s at its particles and the PF weights with the
+ * normalization constant M_{y,s,n} (Supplement S-V "PF State Update Message" P:L660-834, PF weights P:L3392-3432,
+ * Supplement S-IV P:L527-632).  Per PA j, C^kappa(phi_p, r) = r q_p psi_p psi_p^H + eta_j I + M_j M_j^H and
+ * mu^kappa(phi_p, r) = r zeta_j mu_p psi_p + mu3_j with q_p = (gamma_p + |mu_p|^2 (1 - zeta_j)) zeta_j, psi_p the
+ * response of PA j at the paired MT particle x_p (d_particles row p, reading C-amb-8 / C-amb-F1a) through the wall of
+ * SFV phi_p (d_phi [P][3]).  det A and pi^Nz cancel against the H0 branch, so:
+ *   d_logr out [P] = log w_alpha,p + sum_j [log kappa~(phi_p, 1; z_j) - log kappa~(., 0; z_j)],
+ *   d_out  out [2] = (log M_y in units of prod_j kappa~(., 0; z_j), posterior existence sum_p w_p),
+ *   d_w    out [P] or NULL: PF weights w_p = e^{logr_p} / M_y  (sum_p w_p + (1 - sum w_alpha) / M_y = 1).
+ * Inputs: d_particles [P][pstride] fp64 (xyz first), d_walpha [P] fp64 (the PF prediction weights, sum <= 1),
+ * d_mu complex128 [P], d_gamma [P] fp64 (particle amplitude mean / variance), h_zeta [J] (zeta_j(1) of the PF's PPRs),
+ * h_eta [J] > 0, d_y complex64 [J][nf][Na] (as cdms_loglik), d_mu3 complex64 [J][nf][Na] (the other features' summed
+ * mean sum_{s' != s} mu~_3), d_mcols complex64 [J][L][nf][Na] (the columns m_{s'} of M, L <= 8), both particle-
+ * independent and formed by the caller (reading C-amb-F1b).  The scene's K is ignored (the PF is component 1).
+ * Engine: the correlations psi_p^H (z - mu3) and psi_p^H m_l on K1T tables of the L + 1 snapshots (FP32 spherical /
+ * planar WB; other modes CDMS_EUNSUPPORTED), the rest in fp64.  Purely local.  Degenerate particles: logr = -inf +
+ * CDMS_EDEGENERATE at sync; sum of everything zero -> CDMS_EZEROMASS. */
+cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* h_f_pb, const double* d_particles,
+                           int64_t P, int32_t pstride, const double* d_phi, const double* d_walpha, const void* d_mu,
+                           const double* d_gamma, const double* h_zeta, const double* h_eta, const void* d_y,
+                           const void* d_mu3, const void* d_mcols, int32_t L, double* d_logr, double* d_w,
+                           double* d_out);
+
 /* ---- row A6: weight normalization ------------------------------------------------------------ */
 
 /* w_p = exp((l_p - M) - ln S), M = max_p l_p, S = sum_p exp(l_p - M), lse = M + ln S over ALL ranks'

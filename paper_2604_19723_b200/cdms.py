@@ -79,6 +79,8 @@ def lib() -> C.CDLL:
                               C.POINTER(StepParamsC), vp, vp], C.c_int),
             "cdms_response": ([vp, C.POINTER(SceneC), vp, i64, vp, vp, vp], C.c_int),
             "cdms_bp_update": ([vp, vp, vp, i64, C.POINTER(StepParamsC), vp, vp, vp], C.c_int),
+            "cdms_pf_update": ([vp, C.POINTER(SceneC), dp, vp, i64, i32, vp, vp, vp, vp, dp, dp, vp, vp, vp, i32, vp,
+                                vp, vp], C.c_int),
             "cdms_loopback_create": ([C.c_int, C.POINTER(vp)], C.c_int),
             "cdms_loopback_destroy": ([vp], C.c_int),
             "cdms_comm_init_loopback": ([vp, vp, C.c_int], C.c_int),
@@ -104,7 +106,7 @@ def exported_symbols() -> list[str]:
                         "cdms_loglik", "cdms_loglik_terms", "cdms_weights_normalize", "cdms_moments", "cdms_resample", "cdms_bp_step",
                         "cdms_response", "cdms_moment_match", "cdms_resample_plan", "cdms_birth_proposal",
                         "cdms_bp_update", "cdms_loopback_create", "cdms_loopback_destroy",
-                        "cdms_comm_init_loopback"]]
+                        "cdms_comm_init_loopback", "cdms_pf_update"]]
 
 
 def _ptr(t) -> Optional[int]:
@@ -365,6 +367,25 @@ def bp_update(ctx: Context, loglik, particles, philox_key: int, step: int, regul
     ctx.check(lib().cdms_bp_update(ctx.h, _ptr(loglik), _ptr(particles), int(particles.shape[0]), C.byref(prm),
                                    _ptr(est), _ptr(lse), _ptr(anc)))
     return est, lse, anc
+
+
+def pf_update(ctx: Context, scene: Scene, particles, phi, walpha, mu, gamma, zeta, eta, y, mu3, mcols=None):
+    """F1 (cdms_pf_update): (logr [P], w [P], out [2] = (log M_y, existence)) for one PF at its particles.
+    particles float64 cuda [P][pstride] (paired MT particles), phi [P][3], walpha [P], mu complex128 [P], gamma [P];
+    y, mu3 complex64 cuda [J][nf][Na]; mcols complex64 cuda [J][L][nf][Na] or None (L = 0)."""
+    torch = ctx.torch
+    P, pstride = particles.shape
+    dev = particles.device
+    L = 0 if mcols is None else int(mcols.shape[1])
+    logr = torch.empty(P, dtype=torch.float64, device=dev)
+    w = torch.empty(P, dtype=torch.float64, device=dev)
+    out = torch.empty(2, dtype=torch.float64, device=dev)
+    ctx.check(lib().cdms_pf_update(ctx.h, C.byref(scene.c), _dp(scene.f_pb()), _ptr(particles), int(P), int(pstride),
+                                   _ptr(phi), _ptr(walpha), _ptr(mu), _ptr(gamma),
+                                   _dp(np.ascontiguousarray(zeta, dtype=np.float64).reshape(-1)),
+                                   _dp(np.ascontiguousarray(eta, dtype=np.float64).reshape(-1)), _ptr(y), _ptr(mu3),
+                                   _ptr(mcols), int(L), _ptr(logr), _ptr(w), _ptr(out)))
+    return logr, w, out
 
 
 def response(ctx: Context, scene: Scene, pos, js, sfv):

@@ -67,7 +67,8 @@ enum Slot {
   WS_YTILES, WS_YNORM, WS_LSE_PART, WS_LSE_RANK, WS_SCAL, WS_MOM_PART, WS_SUMS, WS_WMAX_PART, WS_Q, WS_BSUM,
   WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
   WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BC, WS_BLL, WS_BPB,
-  WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_GPART, WS_PLAN, WS_RANKS, WS_COUNT
+  WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_GPART, WS_PLAN, WS_RANKS, WS_PF_SNAP, WS_PF_TAB, WS_PF_DOTS, WS_PF_FIXED,
+  WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -1085,6 +1086,73 @@ cdms_status cdms_birth_proposal(cdms_ctx ctx, const cdms_scene* scene, const dou
   CUDA_TRY(ctx, launch_birth_reduce(N_g, J, nz, cbuf, cand, pb, part, part6, scr, d_out, ctx->d_flags, ctx->stream));
   ctx->launches += 4;
   return stage("reduce");
+}
+
+cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* h_f_pb, const double* d_particles,
+                           int64_t P, int32_t pstride, const double* d_phi, const double* d_walpha, const void* d_mu,
+                           const double* d_gamma, const double* h_zeta, const double* h_eta, const void* d_y,
+                           const void* d_mu3, const void* d_mcols, int32_t L, double* d_logr, double* d_w,
+                           double* d_out) {
+  if (!ctx) return CDMS_EINVAL;
+  DeviceGuard g(ctx->device);
+  if (!scene || !h_f_pb || !d_particles || !d_phi || !d_walpha || !d_mu || !d_gamma || !h_zeta || !h_eta || !d_y ||
+      !d_mu3 || (L > 0 && !d_mcols) || !d_logr || !d_out || P <= 0 || pstride < 3 || L < 0 ||
+      L + 1 > pf_max_snapshots())
+    return fail(ctx, CDMS_EINVAL, "pf_update: bad arguments (P=%lld, L=%d)", (long long)P, L);
+  // the PF's component: one wall whose SFV is per particle (K = 1, component 1), on the K1T tables
+  cdms_scene s1 = *scene;
+  s1.K = 1;
+  SceneDev sd;
+  cdms_status st = build_scene(ctx, &s1, h_f_pb, nullptr, nullptr, &sd);
+  if (st) return st;
+  if (scene->precision != CDMS_FP32 || sd.wavefront == CDMS_PLANAR_NB)
+    return fail(ctx, CDMS_EUNSUPPORTED, "pf_update: FP32 spherical / planar-WB only (K1T tables)");
+  double par[2 * MAXJ];
+  for (int j = 0; j < sd.J; ++j) {
+    if (!(h_eta[j] > 0.0) || !is_fin(h_eta[j])) return fail(ctx, CDMS_EINVAL, "pf_update: eta[%d] must be > 0", j);
+    if (!(h_zeta[j] >= 0.0 && h_zeta[j] <= 1.0)) return fail(ctx, CDMS_EINVAL, "pf_update: zeta[%d] not in [0, 1]", j);
+    par[j] = h_eta[j];
+    par[MAXJ + j] = h_zeta[j];
+  }
+  const int J = sd.J, T = L + 1;
+  const int64_t Nz = (int64_t)sd.nf * sd.Na;
+  SceneDev sdt = sd;  // the T snapshots of every PA as J T "PAs" for the table builder
+  sdt.J = J * T;
+  const size_t tab_bytes = tay_table_bytes(sdt);
+  if (tab_bytes > ((size_t)1 << 30)) return fail(ctx, CDMS_EUNSUPPORTED, "pf_update: tables of %zu bytes", tab_bytes);
+  float2 *snaps, *tab;
+  double2 *dots, *fixed, *cc;
+  double *gain2, *dpar;
+  int* pflag;
+  float4 *yt, *tmpl;
+  double* yn;
+  WS_TRY(ctx, WS_PF_SNAP, (size_t)J * T * Nz, &snaps);
+  WS_TRY(ctx, WS_PF_TAB, tab_bytes / sizeof(float2), &tab);
+  WS_TRY(ctx, WS_PF_DOTS, (size_t)J * T * T, &dots);
+  WS_TRY(ctx, WS_PF_FIXED, (size_t)J * pf_fixed_width(), &fixed);
+  WS_TRY(ctx, WS_PF_CC, (size_t)P * J * T, &cc);
+  WS_TRY(ctx, WS_PF_FLAG, P, &pflag);
+  WS_TRY(ctx, WS_PF_GAIN, (size_t)P * J, &gain2);
+  WS_TRY(ctx, WS_PF_PAR, 2 * MAXJ, &dpar);
+  WS_TRY(ctx, WS_YTILES, (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP, &yt);
+  WS_TRY(ctx, WS_YNORM, MAXJ, &yn);
+  WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &tmpl);
+  CUDA_TRY(ctx, cudaMemcpyAsync(dpar, par, sizeof(par), cudaMemcpyHostToDevice, ctx->stream));
+  // (1) template columns of the PAs; snapshots e0 = z - mu3, m_l; their fp64 dot products and the particle-independent
+  //     factor of A^-1; K1T tables of every snapshot
+  CUDA_TRY(ctx, launch_prep_y(sd, static_cast<const float2*>(d_y), yt, yn, tmpl, ctx->stream));
+  CUDA_TRY(ctx, launch_pf_prep(J, T, Nz, static_cast<const float2*>(d_y), static_cast<const float2*>(d_mu3),
+                               static_cast<const float2*>(d_mcols), snaps, dots, dpar, fixed, ctx->d_flags,
+                               ctx->stream));
+  CUDA_TRY(ctx, launch_tay_prep(sdt, snaps, tab, 0, ctx->taylor_prep_direct, ctx->stream));
+  // (2) per (particle, PA): psi_p^H v_t for the T snapshots
+  CUDA_TRY(ctx, launch_pf_corr(sd, T, tab, tmpl, d_particles, P, pstride, d_phi, cc, pflag, ctx->stream));
+  // (3) per particle: log kappa~(phi_p, 1) - log kappa~(., 0) summed over PAs + log w_alpha; M_y, existence, weights
+  CUDA_TRY(ctx, launch_pf_finish(sd, T, cc, fixed, dpar, dpar + MAXJ, gain2, d_particles, pstride, d_phi, d_walpha,
+                                 static_cast<const double2*>(d_mu), d_gamma, pflag, P, d_logr, d_w, d_out,
+                                 ctx->d_flags, ctx->stream));
+  ctx->launches += 10 + (d_w ? 1 : 0);
+  return CDMS_OK;
 }
 
 cdms_status cdms_weights_normalize(cdms_ctx ctx, const double* d_logw, int64_t P_local, double* d_w, double* d_lse) {

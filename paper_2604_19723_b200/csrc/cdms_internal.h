@@ -234,6 +234,19 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
                             int64_t P, int pstride, const double* sfv, int sfv_pp, double2* terms, int* pflag,
                             int gram_diag, int lanes, cudaStream_t st);
 
+// F1 (pf.cu, taylor.cu pf_corr_kernel): PF-particle update message kappa~ and the PF normalization
+cudaError_t launch_pf_corr(const SceneDev& sc, int T, const float2* tab, const float4* tmpl, const double* particles,
+                           int64_t P, int pstride, const double* phi, double2* out, int* pflag, cudaStream_t st);
+cudaError_t launch_pf_prep(int J, int T, int64_t Nz, const float2* y, const float2* mu3, const float2* mcols,
+                           float2* snaps, double2* dots, const double* d_eta, double2* fixed, int* flags,
+                           cudaStream_t st);
+cudaError_t launch_pf_finish(const SceneDev& sc, int T, const double2* cc, const double2* fixed, const double* d_eta,
+                             const double* d_zeta, double* gain2, const double* particles, int pstride,
+                             const double* phi, const double* walpha, const double2* mu, const double* gamma,
+                             int* pflag, int64_t P, double* logr, double* w, double* out, int* flags, cudaStream_t st);
+int pf_fixed_width();     // double2 per PA of the fixed (particle-independent) part
+int pf_max_snapshots();   // T = L + 1 <= 9
+
 // nbmma.cu: PLANAR_NB correlation on the tensor cores
 struct NbPlan {
   int kc;              // real K per pipeline stage (2 x subcarriers), 16 / 32 / 64

@@ -720,4 +720,121 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------- F1: one component, T snapshots
+// The correlations psi_p^H v_t of the F1 update (pf.cu, Supplement S-V P:L780-834): ONE component per particle -- the
+// wall of PF particle p's SFV phi_p seen from the paired MT particle x_p (reading C-amb-F1a) -- against T snapshots
+// per PA (K1T tables of snapshot t of PA j at table index j T + t, [m][g][l] layout).  Per antenna the fp32 offset,
+// carrier and table centre are formed once (as tay_corr_kernel) and reused for every snapshot: one 64-byte row and one
+// Taylor sum per (antenna, snapshot).  out [P][J][T] complex128, path-loss gain applied; pflag as K1T.
+template <int T>
+__global__ void __launch_bounds__(TAY_BLOCK)
+    pf_corr_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
+                   const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P, int pstride,
+                   const double* __restrict__ phi, double2* __restrict__ out, int* __restrict__ pflag) {
+  const int J = sc.J, Na = sc.Na;
+  const int64_t p = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
+  const int j = blockIdx.y;
+  if (p >= P) return;
+  const double* pos = particles + p * pstride;
+  double2* o = out + (p * J + j) * T;
+  double va[3], sh[3];
+  if (!anchor_va(sc, j, phi + 3 * p, va, sh)) {
+    atomicOr(&pflag[p], 2);
+#pragma unroll
+    for (int t = 0; t < T; ++t) o[t] = make_double2(0.0, 0.0);
+    return;
+  }
+  const double r0 = pos[0] - va[0], r1 = pos[1] - va[1], r2 = pos[2] - va[2];
+  const double rs2 = 2.0 * (r0 * sh[0] + r1 * sh[1] + r2 * sh[2]);
+  const float hx = (float)(r0 - rs2 * sh[0]), hy = (float)(r1 - rs2 * sh[1]), hz = (float)(r2 - rs2 * sh[2]);
+  const double R64 = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+  if (!(R64 > 0.0)) {
+    atomicOr(&pflag[p], 1);
+#pragma unroll
+    for (int t = 0; t < T; ++t) o[t] = make_double2(0.0, 0.0);
+    return;
+  }
+  const float R = (float)R64;
+  const TayBase tb = tay_base(R64 * sc.df_c);
+  double sb, cb;
+  sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
+  const int Na_pad = sc.n_mb * NWARP;
+  const float4* tm = tmpl + (int64_t)j * Na_pad;
+  const size_t tstride = (size_t)Na * (G + 1) * (TAY_L / 2);  // float4s per (PA, snapshot) table
+  const float4* tj = reinterpret_cast<const float4*>(tab) + (size_t)j * T * tstride;
+  const bool sph = sc.wavefront == CDMS_SPHERICAL;
+  double accr[T], acci[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) accr[t] = acci[t] = 0.0;
+  int fl = 0;
+  for (int m0 = 0; m0 < Na; m0 += 16) {
+    float pr[T], pi[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) pr[t] = pi[t] = 0.f;
+    const int m1 = min(m0 + 16, Na);
+    for (int m = m0; m < m1; ++m) {
+      const float4 v = __ldg(&tm[m]);
+      const float rq = hx * v.x + hy * v.y + hz * v.z;
+      float delta;
+      if (sph) {
+        const float n = v.w - 2.f * rq;
+        const float d = Num<float>::fsqrt_(R * R + n);
+        if (!(d > 0.f)) fl |= 1;
+        delta = Num<float>::fdiv_(n, d + R);
+      } else {
+        delta = Num<float>::fdiv_(-rq, R);
+      }
+      float er, ei;
+      cis2pi_fast<float>(delta * sc.fc_cf, er, ei);
+      uint32_t g;
+      float dp;
+      bool flip;
+      tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
+      if (flip) { er = -er; ei = -ei; }
+      const size_t roff = ((size_t)m * (uint32_t)(G + 1) + g) * (TAY_L / 2);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float4* row = tj + (size_t)t * tstride + roff;
+        float4 c01, c23, c45, c67;
+        ldg256(row, c01, c23);
+        ldg256(row + 2, c45, c67);
+        float yr = c67.z, yi = c67.w;
+        yr = fmaf(yr, dp, c67.x); yi = fmaf(yi, dp, c67.y);
+        yr = fmaf(yr, dp, c45.z); yi = fmaf(yi, dp, c45.w);
+        yr = fmaf(yr, dp, c45.x); yi = fmaf(yi, dp, c45.y);
+        yr = fmaf(yr, dp, c23.z); yi = fmaf(yi, dp, c23.w);
+        yr = fmaf(yr, dp, c23.x); yi = fmaf(yi, dp, c23.y);
+        yr = fmaf(yr, dp, c01.z); yi = fmaf(yi, dp, c01.w);
+        yr = fmaf(yr, dp, c01.x); yi = fmaf(yi, dp, c01.y);
+        pr[t] = fmaf(er, yr, fmaf(-ei, yi, pr[t]));
+        pi[t] = fmaf(er, yi, fmaf(ei, yr, pi[t]));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      accr[t] += (double)pr[t];
+      acci[t] += (double)pi[t];
+    }
+  }
+  if (fl) atomicOr(&pflag[p], fl);
+  const double gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
+#pragma unroll
+  for (int t = 0; t < T; ++t)
+    o[t] = make_double2((accr[t] * cb - acci[t] * sb) * gn, (accr[t] * sb + acci[t] * cb) * gn);
+}
+cudaError_t launch_pf_corr(const SceneDev& sc, int T, const float2* tab, const float4* tmpl, const double* particles,
+                           int64_t P, int pstride, const double* phi, double2* out, int* pflag, cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
+  const int G = tay_centres(sc.nf);
+  switch (T) {
+#define CASE_T(n) \
+  case n: pf_corr_kernel<n><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, phi, out, pflag); break;
+    CASE_T(1) CASE_T(2) CASE_T(3) CASE_T(4) CASE_T(5) CASE_T(6) CASE_T(7) CASE_T(8) CASE_T(9)
+#undef CASE_T
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace cdms

@@ -520,6 +520,98 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+PF_METRIC = "PF particle x PA kappa~ update evals/s (F1)"
+PF_UNIT = "PF particle-PA evals/s"
+
+
+def pf_inputs(cfg, sc, P, rank=0):
+    """One legacy PF (wall 1) of the synthetic scene: PF particles around its true SFV (+-5 cm) paired with MT particles
+    of the config's mixture; the other K - 1 walls as the columns of M and the summed mean (scaled by sqrt(0.05) and
+    0.9 rho_s: tests/test_pf_gpu.py's recipe).  Returns host arrays."""
+    rng = np.random.default_rng(cfg.seed + 7 + rank)
+    x = scenes.make_particles(cfg, rank * P, P)
+    phi = sc.sfv[0][None, :] + 0.05 * rng.standard_normal((P, 3))
+    walpha = np.full(P, 0.9 / P)
+    mu = sc.rho[1] * (1 + 0.1 * (rng.standard_normal(P) + 1j * rng.standard_normal(P)))
+    gamma = np.full(P, 0.02)
+    return x, phi, walpha, mu, gamma, np.full(cfg.J, 0.9)
+
+
+def run_pf(args):
+    """F1: time cdms_pf_update for one PF with P PF particles (device-resident inputs), L = K - 1 other features."""
+    import torch
+    world, rank, local = dist_env()
+    from paper_2604_19723_b200 import cdms
+    dev = f"cuda:{local}"
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream(local)
+    cfg = scenes.CONFIGS[args.config]
+    P = p_total_of(args, cfg) // world
+    sc = scenes.make_scene(cfg)
+    scene = cdms.Scene.from_synthetic(sc, wavefront=args.wavefront, precision=args.precision)
+    ctx = cdms.Context(local, stream)
+    y, eta = synth_measurement(cdms, ctx, scene, sc, torch, dev)
+    L = cfg.K - 1
+    J = cfg.J
+    pos = np.repeat(scenes.P_TRUE[None], J * L, axis=0)
+    js = np.array([(j, 2 + l) for j in range(J) for l in range(L)], dtype=np.int32)
+    psi = cdms.response(ctx, scene, pos, js, sc.sfv).reshape(J, L, -1)
+    mcols = (math.sqrt(0.05) * psi).to(torch.complex64).reshape(J, L, cfg.nf, cfg.Na).contiguous()
+    rho = torch.as_tensor(sc.rho[2:2 + L], device=dev)
+    mu3 = (0.9 * torch.einsum("jln,l->jn", psi, rho)).to(torch.complex64).reshape(J, cfg.nf, cfg.Na).contiguous()
+    x, phi, wa, mu, gamma, zeta = pf_inputs(cfg, sc, P, rank)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+    dx, dphi, dwa, dmu, dg = t(x), t(phi), t(wa), t(mu.astype(np.complex128)), t(gamma)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        return cdms.pf_update(ctx, scene, dx, dphi, dwa, dmu, dg, zeta, eta, y, mu3, mcols)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.sync()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(local)
+        for n in range(args.steps):
+            flush.zero_()
+            ev[n][0].record(stream)
+            step()
+            ev[n][1].record(stream)
+        clk.mark()
+        torch.cuda.synchronize(local)
+    st = ctx.sync(raise_on_error=False)
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    evals = P * J * world
+    res = {"metric": PF_METRIC, "value": evals / (ms / 1e3), "unit": PF_UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic",
+           "config": {"workload": f"{args.config} scene (J={J}, {cfg.ny}x{cfg.nv}, nf={cfg.nf}), one PF with {P} "
+                                  f"particles/GPU, L={L} other features", "config": args.config, "mode": "pf",
+                      "P_per_gpu": P, "L": L, "Nz": cfg.Nz, "wavefront": args.wavefront,
+                      "step": "snapshots + fp64 factor of A + K1T tables of L+1 snapshots + per-particle "
+                              "correlations + rank-1 lemma + M_y normalization"},
+           "clocks": clk.summary(), "gpu_launches": ctx.launch_count() - launches0, "sync_status": st}
+    ctx.close()
+    if not args.no_cpu_baseline and rank == 0:
+        from oracle import oracle as O
+        O.build()
+        o = O.Oracle.from_scene(sc, wavefront=args.wavefront)
+        n = 8
+        while True:
+            t0 = time.perf_counter()
+            o.pf_update(x[:n], phi[:n], wa[:n], mu[:n], gamma[:n], zeta, eta, y.cpu().numpy().astype(np.complex128),
+                        mu3.cpu().numpy().astype(np.complex128), mcols.cpu().numpy().astype(np.complex128))
+            dt = time.perf_counter() - t0
+            if dt > args.cpu_seconds / 3 or n >= P:
+                break
+            n = min(P, n * 4)
+        res["cpu_baseline"] = {"value": n * J / dt, "unit": PF_UNIT, "cores": 1, "kind": "oracle",
+                               "sample": f"orc_pf_update on {n} of {P} PF particles ({args.config}), {dt:.2f} s"}
+    return res if rank == 0 else None
+
+
 BIRTH_METRIC = "Bartlett birth-proposal candidate x PA correlations/s (F3)"
 BIRTH_UNIT = "candidate-PA evals/s"
 
@@ -741,7 +833,7 @@ def main():
     ap.add_argument("--ref-particles", type=int, default=0,
                     help="--impl reference: particles per oracle step (0: sized to ~--ref-step-s seconds per step)")
     ap.add_argument("--ref-step-s", type=float, default=2.0)
-    ap.add_argument("--mode", default="step", choices=["step", "birth"],
+    ap.add_argument("--mode", default="step", choices=["step", "birth", "pf"],
                     help="step: the BP step (headline); birth: the F3 birth proposal")
     ap.add_argument("--candidates", type=int, default=1 << 20, help="birth mode: candidates N_g per GPU")
     ap.add_argument("--legacy", type=int, default=2, help="birth mode: legacy PFs L")
@@ -754,6 +846,8 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.mode == "birth":
         res = run_birth_reference(args) if args.impl == "reference" else run_birth(args)
+    elif args.mode == "pf":
+        res = None if args.impl == "reference" else run_pf(args)
     else:
         res = run_reference(args) if args.impl == "reference" else run_cdms(args)
     if res is not None:

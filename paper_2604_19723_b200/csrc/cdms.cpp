@@ -15,9 +15,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "cdms_internal.h"
 
 using namespace cdms;
+
+namespace {
+// NVTX range around each ABI call and each phase of the step (nsys / ncu --nvtx timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 namespace {
 struct Coll;
@@ -433,6 +445,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
                         int32_t pstride, const double* d_sfv, int32_t sfv_pp, const void* d_y, const double* d_logw,
                         double* d_loglik, void* d_amp, void* d_c = nullptr, void* d_G = nullptr,
                         bool no_gram = false) {
+  NvtxRange nv_("loglik (A1-A5)");
   float4* yt;
   double* yn;
   double2* terms;
@@ -620,6 +633,7 @@ cdms_status run_moments(cdms_ctx ctx, const double* d_x, const double* d_w, int6
 // synchronization in either case.
 cdms_status bp_update_impl(cdms_ctx ctx, const double* l, double* x, int64_t P_local, const cdms_step_params* prm,
                            double* d_est, double* d_lse, int64_t* d_anc) {
+  NvtxRange nv_("update (A6-A9)");
   const bool comm = ctx->coll != nullptr;
   const int R = ctx->nranks;
   const int64_t P_total = P_local * R, p0 = (int64_t)ctx->rank * P_local;
@@ -835,6 +849,7 @@ cdms_status cdms_sync(cdms_ctx ctx) {
 cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local) {
   if (!ctx || P_local <= 0) return fail(ctx, CDMS_EINVAL, "reserve: bad arguments");
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_reserve");
   SceneDev sd;
   cdms_status st = build_scene(ctx, scene, nullptr, nullptr, nullptr, &sd);
   if (st) return st;
@@ -946,6 +961,7 @@ cdms_status cdms_layout(cdms_ctx ctx, const cdms_scene* scene, const double* d_s
                         double* d_H) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_layout");
   SceneDev sd;
   cdms_status st = build_scene(ctx, scene, nullptr, nullptr, nullptr, &sd);
   if (st) return st;
@@ -961,6 +977,7 @@ cdms_status cdms_loglik(cdms_ctx ctx, const cdms_scene* scene, const double* d_p
                         void* d_amp) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_loglik");
   if (!d_particles || !d_y || !h_f_pb || !h_prior || !h_eta || !d_loglik) return fail(ctx, CDMS_EINVAL, "loglik: NULL pointer");
   if (P <= 0 || pstride < 3) return fail(ctx, CDMS_EINVAL, "loglik: P=%lld pstride=%d", (long long)P, pstride);
   SceneDev sd;
@@ -977,6 +994,7 @@ cdms_status cdms_loglik_terms(cdms_ctx ctx, const cdms_scene* scene, const doubl
                               void* d_c, void* d_G) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_loglik_terms");
   if (!d_particles || !d_y || !h_f_pb || !h_prior || !h_eta || !d_loglik || !d_c || !d_G)
     return fail(ctx, CDMS_EINVAL, "loglik_terms: NULL pointer");
   if (P <= 0 || pstride < 3) return fail(ctx, CDMS_EINVAL, "loglik_terms: P=%lld pstride=%d", (long long)P, pstride);
@@ -994,6 +1012,7 @@ cdms_status cdms_birth_proposal(cdms_ctx ctx, const cdms_scene* scene, const dou
                                 double* d_cand) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_birth_proposal");
   if (!scene || !h_f_pb || !h_x_hat || !d_y || !h_box || !d_out || N_g <= 0 || L < 0 || L > MAXS - 1 ||
       (L > 0 && !h_sfv_legacy))
     return fail(ctx, CDMS_EINVAL, "birth_proposal: bad arguments (L=%d, N_g=%lld)", L, (long long)N_g);
@@ -1095,6 +1114,7 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
                            double* d_out) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_pf_update");
   if (!scene || !h_f_pb || !d_particles || !d_phi || !d_walpha || !d_mu || !d_gamma || !h_zeta || !h_eta || !d_y ||
       !d_mu3 || (L > 0 && !d_mcols) || !d_logr || !d_out || P <= 0 || pstride < 3 || L < 0 ||
       L + 1 > pf_max_snapshots())
@@ -1158,6 +1178,7 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
 cdms_status cdms_weights_normalize(cdms_ctx ctx, const double* d_logw, int64_t P_local, double* d_w, double* d_lse) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_weights_normalize");
   if (!d_logw || !d_w || !d_lse || P_local <= 0) return fail(ctx, CDMS_EINVAL, "normalize: bad arguments");
   cdms_status st = run_lse(ctx, d_logw, P_local, d_lse);
   if (st) return st;
@@ -1171,6 +1192,7 @@ cdms_status cdms_weights_normalize(cdms_ctx ctx, const double* d_logw, int64_t P
 cdms_status cdms_moments(cdms_ctx ctx, const double* d_particles, const double* d_w, int64_t P_local, double* d_est) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_moments");
   if (!d_particles || !d_w || !d_est || P_local <= 0) return fail(ctx, CDMS_EINVAL, "moments: bad arguments");
   return run_moments(ctx, d_particles, d_w, P_local, d_est);
 }
@@ -1178,6 +1200,7 @@ cdms_status cdms_moments(cdms_ctx ctx, const double* d_particles, const double* 
 cdms_status cdms_resample(cdms_ctx ctx, const double* d_w, int64_t P_local, uint32_t u_bits, int64_t* d_ancestors) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_resample");
   if (!d_w || !d_ancestors || P_local <= 0) return fail(ctx, CDMS_EINVAL, "resample: bad arguments");
   const int R = ctx->nranks;
   const int64_t P_total = P_local * R;
@@ -1237,6 +1260,7 @@ cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_partic
                          const cdms_step_params* prm, double* d_est, double* d_lse) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_bp_step");
   if (!d_particles || !d_y || !h_f_pb || !h_prior || !h_eta || !prm || !d_est || !d_lse || P_local <= 0)
     return fail(ctx, CDMS_EINVAL, "bp_step: bad arguments");
   cdms_status st = check_step_params(ctx, prm, P_local);  // every host check before the first launch
@@ -1249,7 +1273,11 @@ cdms_status cdms_bp_step(cdms_ctx ctx, const cdms_scene* scene, double* d_partic
   double* l;
   WS_TRY(ctx, WS_LOGLIK, P_local, &l);
   // (1) prediction (row A9)
-  CUDA_TRY(ctx, launch_predict(d_particles, P_local, p0, prm->T, prm->sigma_v, prm->philox_key, prm->step, ctx->stream));
+  {
+    NvtxRange r("predict");
+    CUDA_TRY(ctx, launch_predict(d_particles, P_local, p0, prm->T, prm->sigma_v, prm->philox_key, prm->step,
+                                 ctx->stream));
+  }
   ctx->launches += 1;
   // (2) coherent log-likelihood, uniform w_beta (rows A1-A5)
   st = loglik_impl(ctx, sd, scene->precision, d_particles, P_local, 6, d_sfv, 0, d_y, nullptr, l, nullptr);
@@ -1262,6 +1290,7 @@ cdms_status cdms_bp_update(cdms_ctx ctx, const double* d_loglik, double* d_parti
                            const cdms_step_params* prm, double* d_est, double* d_lse, int64_t* d_ancestors) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_bp_update");
   if (!d_loglik || !d_particles || !prm || !d_est || !d_lse || P_local <= 0)
     return fail(ctx, CDMS_EINVAL, "bp_update: bad arguments");
   cdms_status st = check_step_params(ctx, prm, P_local);
@@ -1273,6 +1302,7 @@ cdms_status cdms_response(cdms_ctx ctx, const cdms_scene* scene, const double* d
                           const double* d_sfv, void* d_psi) {
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_response");
   if (!d_pos || !d_js || !d_psi || n <= 0) return fail(ctx, CDMS_EINVAL, "response: bad arguments");
   SceneDev sd;
   cdms_status st = build_scene(ctx, scene, nullptr, nullptr, nullptr, &sd);

@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
     // ---- (5) hand-off: c (with gains) and the lower triangle of G (with gains) -> terms [P][J][T]
     const double nz = (double)nf * (double)Na;
     for (int it = tid; it < T * TILE_P; it += NTHREADS) {
-      const int pl = it / T, t = it - pl * T;
+      const int t = it / TILE_P, pl = it - t * TILE_P;  // consecutive threads: consecutive particles (term_idx)
       const int64_t pp = tile * TILE_P + pl;
       if (pp >= a.P) continue;
       double2 out;
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
           out = make_double2(v.x * g2, -v.y * g2);
         }
       }
-      a.terms[(pp * J + j) * T + t] = out;
+      a.terms[term_idx(pp, j, t, T, a.P)] = out;
     }
     if (warp == 0 && pfl[lane]) {  // per-particle flags: OR over the group's CTAs (K1b reads and clears them)
       if (pvalid) atomicOr(&a.pflag[p], pfl[lane]);
@@ -694,13 +694,12 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
   const double nz = (double)sc.nf * (double)sc.Na;
   double l = a.logw_prior ? a.logw_prior[p] : 0.0;
   for (int j = 0; j < J; ++j) {
-    const double2* tp = a.terms + (p * J + j) * T;
     const double eta = sc.eta[j];
     double2 c[S], k[NTRI];
 #pragma unroll
-    for (int s = 0; s < S; ++s) c[s] = tp[s];
+    for (int s = 0; s < S; ++s) c[s] = __ldcs(&a.terms[term_idx(p, j, s, T, a.P)]);  // read once: streaming loads
 #pragma unroll
-    for (int t = 0; t < NTRI; ++t) k[t] = tp[S + t];  // lower triangle of G: k[tri(r, c)] = G_rc, r >= c
+    for (int t = 0; t < NTRI; ++t) k[t] = __ldcs(&a.terms[term_idx(p, j, S + t, T, a.P)]);  // G_rc, r >= c
     if (a.term_c != nullptr) {
 #pragma unroll
       for (int r = 0; r < S; ++r) a.term_c[(p * J + j) * S + r] = c[r];

@@ -406,8 +406,8 @@ __global__ void nb_gram_kernel(const __grid_constant__ SceneDev sc, const NbArgs
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int J = sc.J, S = sc.S, T = S + S * (S + 1) / 2;
   if (idx >= a.P * J) return;
-  const int64_t p = idx / J;
-  const int j = (int)(idx - p * J);
+  const int j = (int)(idx / a.P);  // consecutive threads: consecutive particles of one PA (term_idx)
+  const int64_t p = idx - (int64_t)j * a.P;
   double R[MAXS], dl[MAXS], uy[MAXS], uz[MAXS], g[MAXS];
   int fl = 0;
   for (int s = 0; s < S; ++s) {
@@ -418,16 +418,15 @@ __global__ void nb_gram_kernel(const __grid_constant__ SceneDev sc, const NbArgs
   if (fl) atomicOr(&pflag[p], fl);
   const double nz = (double)sc.nf * (double)sc.Na;
   const double ky = sc.dy / sc.lambda, kv = sc.dv / sc.lambda;
-  double2* out = a.terms + (p * J + j) * T + S;
   int t = 0;
   for (int r = 0; r < S; ++r) {
     for (int c = 0; c <= r; ++c, ++t) {
       if (r == c) {
-        out[t] = make_double2(nz * g[r] * g[r], 0.0);
+        a.terms[term_idx(p, j, S + t, T, a.P)] = make_double2(nz * g[r] * g[r], 0.0);
         continue;
       }
       if (a.diag_only) {
-        out[t] = make_double2(0.0, 0.0);
+        a.terms[term_idx(p, j, S + t, T, a.P)] = make_double2(0.0, 0.0);
         continue;
       }
       float sn, cs;
@@ -435,7 +434,7 @@ __global__ void nb_gram_kernel(const __grid_constant__ SceneDev sc, const NbArgs
       const float D = dirichlet_rr(dl[r] - dl[c], sc.nf) * dirichlet_rr(ky * (uy[c] - uy[r]), sc.ny) *
                       dirichlet_rr(kv * (uz[c] - uz[r]), sc.nv);
       const double m = g[r] * g[c] * (double)D;
-      out[t] = make_double2(m * (double)cs, m * (double)sn);
+      a.terms[term_idx(p, j, S + t, T, a.P)] = make_double2(m * (double)cs, m * (double)sn);
     }
   }
 }
@@ -762,7 +761,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         sincospi(2.0 * frac_c(hy.R * sc.fc_c), &sc_, &cc_);  // conj(carrier) = e^{+j2pi f_c R/c}
         const double gs = hy.gain * (double)a.yscale_inv[j];
         const double xr = (cr * cc_ - ci * sc_) * gs, xi = (cr * sc_ + ci * cc_) * gs;
-        a.terms[(p * J + j) * T + s] = make_double2(xr, xi);
+        a.terms[term_idx(p, j, s, T, a.P)] = make_double2(xr, xi);
       }
     }
   }

@@ -293,11 +293,11 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       acci += (double)pi;
     }
     const double gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
-    terms[(p * J + j) * T + s] = make_double2((accr * cb - acci * sb) * gn, (accr * sb + acci * cb) * gn);
-    double2* gr = terms + (p * J + j) * T + S + s * (s + 1) / 2;  // row s of the lower triangle of G
-    gr[s] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);  // G_ss = g^2 N_z
+    terms[term_idx(p, j, s, T, P)] = make_double2((accr * cb - acci * sb) * gn, (accr * sb + acci * cb) * gn);
+    const int grow = S + s * (s + 1) / 2;  // row s of the lower triangle of G
+    terms[term_idx(p, j, grow + s, T, P)] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);  // G_ss = g^2 N_z
     if (gram_diag)  // callers that use c only: no off-diagonal Gram
-      for (int c = 0; c < s; ++c) gr[c] = make_double2(0.0, 0.0);
+      for (int c = 0; c < s; ++c) terms[term_idx(p, j, grow + c, T, P)] = make_double2(0.0, 0.0);
   }
   if (fl) atomicOr(&pflag[p], fl);
 }
@@ -432,12 +432,12 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   if (lane < npairs && ok) {  // one store round per warp: lane i writes pair i's c_s, G_ss (and zero off-diagonals)
     const int64_t p = p0 + lane / S;
     const int s = lane % S;
-    double2* tp = terms + (p * J + j) * T;
-    tp[s] = make_double2(((double)cr * Ebr - (double)ci * Ebi) * gn, ((double)cr * Ebi + (double)ci * Ebr) * gn);
-    double2* gr = tp + S + s * (s + 1) / 2;
-    gr[s] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);
+    terms[term_idx(p, j, s, T, P)] =
+        make_double2(((double)cr * Ebr - (double)ci * Ebi) * gn, ((double)cr * Ebi + (double)ci * Ebr) * gn);
+    const int r0 = S + s * (s + 1) / 2;
+    terms[term_idx(p, j, r0 + s, T, P)] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);
     if (gram_diag)
-      for (int c = 0; c < s; ++c) gr[c] = make_double2(0.0, 0.0);
+      for (int c = 0; c < s; ++c) terms[term_idx(p, j, r0 + c, T, P)] = make_double2(0.0, 0.0);
   }
 }
 
@@ -602,7 +602,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
         if ((long long)rint(d) & 1) g2 = -g2;
       }
       const double vr = cs * acc.x - sn * acc.y, vi = cs * acc.y + sn * acc.x;
-      terms[(p * J + j) * T + S + b * (b + 1) / 2 + a] = make_double2(vr * g2, -vi * g2);
+      terms[term_idx(p, j, S + b * (b + 1) / 2 + a, T, P)] = make_double2(vr * g2, -vi * g2);
     }
   }
 }

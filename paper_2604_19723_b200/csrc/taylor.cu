@@ -609,9 +609,18 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
 template <int S>
 // measured: S = 9 in 3 parts 58.8 vs 59.8 ms (c5 shard); S = 7 in 2 parts 9.16 vs 8.87 ms (c3: one part already fits
 // 168 registers, splitting only repeats the per-component work)
-__host__ __device__ constexpr int tay_gram_parts() { return S >= 9 ? 3 : (S == 8 ? 2 : 1); }
+// S = 9 pair parts over blockIdx.z (A/B: -DCDMS_GRAM_PARTS9=3): with the FAST path's smaller per-component state two
+// parts of 18 pairs fit 168 registers; measured (4M c5 particles) Gram 64.1 ms in 2 parts vs 70.7 ms in 3 (each part
+// repeats the per-(component, antenna) offsets and carriers)
+#ifndef CDMS_GRAM_PARTS9
+#define CDMS_GRAM_PARTS9 2
+#endif
+#ifndef CDMS_GRAM_MINB
+#define CDMS_GRAM_MINB 3
+#endif
+__host__ __device__ constexpr int tay_gram_parts() { return S >= 9 ? CDMS_GRAM_PARTS9 : (S == 8 ? 2 : 1); }
 template <int S, bool FAST>
-__global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? 3 : 1))  // S >= 7: 3 blocks (12 warps) per SM, <= 168 registers
+__global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? CDMS_GRAM_MINB : 1))  // S >= 7: 3 blocks (12 warps) per SM, <= 168 registers
     tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
                     const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
                     int sfv_pp, double2* __restrict__ terms, int lsplit) {

@@ -355,8 +355,11 @@ def roofline(args, cfg, P_local, kern_ms, launches_per_step, ms_per_step, clocks
                                   "vs 74.45 TFLOP/s FP32: the direct method's flops, not executed by K1T",
             "achieved": None, "frac": None, "xu_frac": None, "traffic": None}
     rec = pipe_profile(args, cfg)
-    if rec is not None and names[dom] in rec["kernels"]:
-        k = rec["kernels"][names[dom]]
+    # template instances are recorded with their full argument list (e.g. tay_gram_kernel<9, 1>: S, FAST path)
+    match = [n for n in (rec or {}).get("kernels", {}) if n == names[dom] or n.startswith(names[dom].rstrip(">") + ",")]
+    if match:
+        k = rec["kernels"][match[0]]
+        roof["kernel"] = match[0]
         fma = k["fma_thread_inst_per_particle"] * P_local / launches_per_step
         xu = k["xu_thread_inst_per_particle"] * P_local / launches_per_step
         roof.update({"achieved": round(fma / t / 1e12, 3), "frac": round(fma / t / 1e12 / peak_fma, 4),

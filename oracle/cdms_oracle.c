@@ -876,3 +876,117 @@ int orc_pf_update(const orc_scene* sc, const double* x, int64_t P, int pstride, 
   out[1] = ex;
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------ F4 parts: noise (nu~) and PPR (omega~) updates */
+
+/* Noise variance update message nu~ (Supplement S-V "Noise Variance Update Message") at the noise
+ * particles eta_p^(j) of every PA, and the normalized noise weights:
+ *   A_p = eta_p I + M M^H, M = [m_0 .. m_{S-1}] (all features' columns), e = z - mu_nu (mu_nu = sum_s mu~_3),
+ *   log nu~ = -Nz ln(pi eta_p) - ln det(I + M^H M / eta_p) - ||e||^2/eta_p
+ *             + ||(I + M^H M/eta_p)^{-1/2} M^H e||^2 / eta_p^2,
+ *   w~_p = w_xi,p nu~_p,  w_p = w~_p / sum_p w~_p (per PA).
+ * Per particle: the S x S Cholesky of I + M^H M / eta_p (the paper's order: Gram once, factor per particle).
+ * eta, wxi, logw, w: [J][P]; y, mu: [J][Nz]; mcols [J][S][Nz].  lognorm [J] = log sum_p w~_p. */
+int orc_noise_update(const orc_scene* sc, const double* eta, const double* wxi, int64_t P, const double complex* y,
+                     const double complex* mu, const double complex* mcols, int S, double* logw, double* w,
+                     double* lognorm) {
+  int J = sc->J;
+  size_t nz = (size_t)sc->nf * sc->ny * sc->nv;
+  if (P <= 0 || S < 0 || S > 15) return ORC_EINVAL;
+  double complex* e = (double complex*)malloc(sizeof(double complex) * nz);
+  double complex G[256], Me[16], K[256];
+  int status = ORC_OK;
+  for (int j = 0; j < J && status == ORC_OK; ++j) {
+    const double complex* M = mcols + (size_t)j * S * nz;
+    double e2 = 0.0;
+    for (size_t n = 0; n < nz; ++n) {
+      e[n] = y[(size_t)j * nz + n] - mu[(size_t)j * nz + n];
+      e2 += creal(e[n] * conj(e[n]));
+    }
+    for (int a = 0; a < S; ++a) {
+      double complex acc = 0.0;
+      for (size_t n = 0; n < nz; ++n) acc += conj(M[(size_t)a * nz + n]) * e[n];
+      Me[a] = acc;
+      for (int b = 0; b < S; ++b) {
+        double complex g = 0.0;
+        for (size_t n = 0; n < nz; ++n) g += conj(M[(size_t)a * nz + n]) * M[(size_t)b * nz + n];
+        G[a * S + b] = g;
+      }
+    }
+    double mx = -INFINITY;
+    for (int64_t p = 0; p < P; ++p) {
+      double et = eta[(size_t)j * P + p];
+      if (!(et > 0.0)) { status = ORC_EINVAL; break; }
+      for (int a = 0; a < S; ++a)
+        for (int b = 0; b < S; ++b) K[a * S + b] = (a == b ? 1.0 : 0.0) + G[a * S + b] / et;
+      if (S > 0 && orc_cholesky(K, S)) { status = ORC_EINVAL; break; }
+      double logdet = 0.0, q2 = 0.0;
+      double complex x[16];
+      for (int a = 0; a < S; ++a) {  /* L x = M^H e */
+        double complex acc = Me[a];
+        for (int b = 0; b < a; ++b) acc -= K[a * S + b] * x[b];
+        x[a] = acc / creal(K[a * S + a]);
+        q2 += creal(x[a] * conj(x[a]));
+        logdet += 2.0 * log(creal(K[a * S + a]));
+      }
+      double lnu = -(double)nz * log(ORC_PI * et) - logdet - e2 / et + q2 / (et * et);
+      logw[(size_t)j * P + p] = log(wxi[(size_t)j * P + p]) + lnu;
+      if (logw[(size_t)j * P + p] > mx) mx = logw[(size_t)j * P + p];
+    }
+    if (status) break;
+    double s = 0.0;
+    for (int64_t p = 0; p < P; ++p) s += exp(logw[(size_t)j * P + p] - mx);
+    lognorm[j] = mx + log(s);
+    if (w)
+      for (int64_t p = 0; p < P; ++p) w[(size_t)j * P + p] = exp(logw[(size_t)j * P + p] - lognorm[j]);
+  }
+  free(e);
+  return status;
+}
+
+/* PPR update message omega~ (Supplement S-V "PR State Update Message") and the PPR existence revival
+ * (Supplement S-VI) of one PF s at every PA j:
+ *   C^omega(r) = r m_omega m_omega^H + A, A = eta_j I + M M^H (M^omega = M^kappa: the other features' columns),
+ *   mu^omega(r) = r mu~_4 + mu3,
+ *   log omega~(1) - log omega~(0) = |m_omega^H A^-1 e1|^2 / (1 + m_omega^H A^-1 m_omega) - e1^H A^-1 e1
+ *                                   + e0^H A^-1 e0 - ln(1 + m_omega^H A^-1 m_omega),  e_r = z - mu^omega(r)
+ *   (rank-1 inversion and determinant lemmas; det A and pi^Nz cancel between r = 1 and r = 0),
+ *   u = log(zeta / (1 - zeta)) + that log ratio, posterior existence sigma(u) = 1 / (1 + e^-u).
+ * y, mu3, momega, mu4: [J][Nz]; mcols [J][L][Nz]; zeta, eta [J].  out [J][3] = (log ratio, u, sigma(u)). */
+int orc_ppr_update(const orc_scene* sc, const double* zeta, const double* eta, const double complex* y,
+                   const double complex* mu3, const double complex* mcols, int L, const double complex* momega,
+                   const double complex* mu4, double* out) {
+  int J = sc->J;
+  size_t nz = (size_t)sc->nf * sc->ny * sc->nv;
+  if (L < 0 || L > 15) return ORC_EINVAL;
+  double complex* e0 = (double complex*)malloc(sizeof(double complex) * nz);
+  double complex* e1 = (double complex*)malloc(sizeof(double complex) * nz);
+  double complex Kc[256];
+  int status = ORC_OK;
+  for (int j = 0; j < J && status == ORC_OK; ++j) {
+    const double complex* M = mcols + (size_t)j * L * nz;
+    const double complex* mw = momega + (size_t)j * nz;
+    for (size_t n = 0; n < nz; ++n) {
+      e0[n] = y[(size_t)j * nz + n] - mu3[(size_t)j * nz + n];
+      e1[n] = e0[n] - mu4[(size_t)j * nz + n];
+    }
+    for (int a = 0; a < L; ++a)
+      for (int b = 0; b < L; ++b) {
+        double complex g = 0.0;
+        for (size_t n = 0; n < nz; ++n) g += conj(M[(size_t)a * nz + n]) * M[(size_t)b * nz + n];
+        Kc[a * L + b] = (a == b ? 1.0 : 0.0) + g / eta[j];
+      }
+    if (L > 0 && orc_cholesky(Kc, L)) { status = ORC_EINVAL; break; }
+    double alpha = creal(orc_maha(mw, mw, M, L, Kc, eta[j], nz));
+    double complex b1 = orc_maha(mw, e1, M, L, Kc, eta[j], nz);
+    double t1 = creal(orc_maha(e1, e1, M, L, Kc, eta[j], nz));
+    double t0 = creal(orc_maha(e0, e0, M, L, Kc, eta[j], nz));
+    double lr = creal(b1 * conj(b1)) / (1.0 + alpha) - t1 + t0 - log(1.0 + alpha);
+    double u = log(zeta[j] / (1.0 - zeta[j])) + lr;
+    out[3 * j + 0] = lr;
+    out[3 * j + 1] = u;
+    out[3 * j + 2] = 1.0 / (1.0 + exp(-u));
+  }
+  free(e0); free(e1);
+  return status;
+}

@@ -207,6 +207,34 @@ class Oracle:
                                  _d(logr), _d(w), _d(out))
         return st, logr, w, float(out[0]), float(out[1])
 
+    def noise_update(self, eta, wxi, y, mu, mcols):
+        """nu~ at the noise particles (orc_noise_update): (status, logw [J][P], w [J][P], lognorm [J])."""
+        eta = _f64(eta).reshape(self.J, -1)
+        P = eta.shape[1]
+        wxi = _f64(wxi).reshape(self.J, P)
+        mc = _c128(mcols).reshape(self.J, -1, self.Nz)
+        S = mc.shape[1]
+        y = _c128(y).reshape(self.J, self.Nz)
+        mu = _c128(mu).reshape(self.J, self.Nz)
+        logw, w, ln = np.zeros((self.J, P)), np.zeros((self.J, P)), np.zeros(self.J)
+        st = lib().orc_noise_update(C.byref(self.sc), _d(eta), _d(wxi), C.c_int64(P), y.ctypes.data_as(C.c_void_p),
+                                    mu.ctypes.data_as(C.c_void_p), mc.ctypes.data_as(C.c_void_p), C.c_int(S),
+                                    _d(logw), _d(w), _d(ln))
+        return st, logw, w, ln
+
+    def ppr_update(self, zeta, eta, y, mu3, mcols, momega, mu4):
+        """omega~ and the PPR existence (orc_ppr_update): (status, out [J][3] = (log ratio, u, sigma(u)))."""
+        mc = _c128(mcols).reshape(self.J, -1, self.Nz)
+        L = mc.shape[1]
+        out = np.zeros((self.J, 3))
+        st = lib().orc_ppr_update(C.byref(self.sc), _d(_f64(zeta)), _d(_f64(eta)),
+                                  _c128(y).reshape(self.J, self.Nz).ctypes.data_as(C.c_void_p),
+                                  _c128(mu3).reshape(self.J, self.Nz).ctypes.data_as(C.c_void_p),
+                                  mc.ctypes.data_as(C.c_void_p), C.c_int(L),
+                                  _c128(momega).reshape(self.J, self.Nz).ctypes.data_as(C.c_void_p),
+                                  _c128(mu4).reshape(self.J, self.Nz).ctypes.data_as(C.c_void_p), _d(out))
+        return st, out
+
     def bp_step(self, particles, sfv, y, m, v, eta, T, sigma_v, key, step, regularize=True):
         x = _f64(particles).copy()
         P = x.shape[0]

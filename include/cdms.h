@@ -231,6 +231,28 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
                            const void* d_mu3, const void* d_mcols, int32_t L, double* d_logr, double* d_w,
                            double* d_out);
 
+/* F4 parts: the noise variance update message nu~ (Supplement S-V) at the noise particles
+ * eta_p^(j) of every PA and the normalized noise weights:
+ *   log nu~ = -Nz ln(pi eta_p) - ln det(I + M^H M/eta_p) - |e|^2/eta_p + |(I + M^H M/eta_p)^{-1/2} M^H e|^2/eta_p^2,
+ *   e = z_j - mu_nu,j, M = the S feature columns of PA j.
+ * d_eta, d_wxi [J][P] fp64 (noise particles and their prediction weights), d_y, d_mu complex64 [J][nf][Na] (mu_nu =
+ * sum_s mu~_3), d_mcols complex64 [J][S][nf][Na] (S <= 9).  Outputs: d_logw [J][P] = log w_xi + log nu~, d_w [J][P]
+ * normalized weights per PA (or NULL), d_lognorm [J] = log sum_p w_xi nu~.  Engine: fp64 dot products of the S + 1
+ * vectors per PA, an eigendecomposition of M^H M per PA, then O(S) per (particle, PA).  The scene supplies J, N_a, N_f
+ * (its K, wavefront and precision are not used). */
+cdms_status cdms_noise_update(cdms_ctx ctx, const cdms_scene* scene, const double* d_eta, const double* d_wxi,
+                              int64_t P, const void* d_y, const void* d_mu, const void* d_mcols, int32_t S,
+                              double* d_logw, double* d_w, double* d_lognorm);
+
+/* F4 parts: the PPR update message omega~ of one PF s at every PA (Supplement S-V) and the PPR existence
+ * with revival (Supplement S-VI): C^omega(r) = r m_omega m_omega^H + eta_j I + M M^H, mu^omega(r) =
+ * r mu~_4 + mu3; out [J][3] = (log omega~(1) - log omega~(0), u = log(zeta/(1 - zeta)) + that, sigma(u)).
+ * d_y, d_mu3, d_momega, d_mu4 complex64 [J][nf][Na]; d_mcols complex64 [J][L][nf][Na] (L <= 9); h_zeta in (0, 1),
+ * h_eta > 0 [J]. */
+cdms_status cdms_ppr_update(cdms_ctx ctx, const cdms_scene* scene, const double* h_zeta, const double* h_eta,
+                            const void* d_y, const void* d_mu3, const void* d_mcols, int32_t L, const void* d_momega,
+                            const void* d_mu4, double* d_out);
+
 /* ---- row A6: weight normalization ------------------------------------------------------------ */
 
 /* w_p = exp((l_p - M) - ln S), M = max_p l_p, S = sum_p exp(l_p - M), lse = M + ln S over ALL ranks'

@@ -79,6 +79,8 @@ def lib() -> C.CDLL:
                               C.POINTER(StepParamsC), vp, vp], C.c_int),
             "cdms_response": ([vp, C.POINTER(SceneC), vp, i64, vp, vp, vp], C.c_int),
             "cdms_bp_update": ([vp, vp, vp, i64, C.POINTER(StepParamsC), vp, vp, vp], C.c_int),
+            "cdms_noise_update": ([vp, C.POINTER(SceneC), vp, vp, i64, vp, vp, vp, i32, vp, vp, vp], C.c_int),
+            "cdms_ppr_update": ([vp, C.POINTER(SceneC), dp, dp, vp, vp, vp, i32, vp, vp, vp], C.c_int),
             "cdms_pf_update": ([vp, C.POINTER(SceneC), dp, vp, i64, i32, vp, vp, vp, vp, dp, dp, vp, vp, vp, i32, vp,
                                 vp, vp], C.c_int),
             "cdms_loopback_create": ([C.c_int, C.POINTER(vp)], C.c_int),
@@ -106,7 +108,8 @@ def exported_symbols() -> list[str]:
                         "cdms_loglik", "cdms_loglik_terms", "cdms_weights_normalize", "cdms_moments", "cdms_resample", "cdms_bp_step",
                         "cdms_response", "cdms_moment_match", "cdms_resample_plan", "cdms_birth_proposal",
                         "cdms_bp_update", "cdms_loopback_create", "cdms_loopback_destroy",
-                        "cdms_comm_init_loopback", "cdms_pf_update"]]
+                        "cdms_comm_init_loopback", "cdms_pf_update", "cdms_noise_update",
+                        "cdms_ppr_update"]]
 
 
 def _ptr(t) -> Optional[int]:
@@ -386,6 +389,31 @@ def pf_update(ctx: Context, scene: Scene, particles, phi, walpha, mu, gamma, zet
                                    _dp(np.ascontiguousarray(eta, dtype=np.float64).reshape(-1)), _ptr(y), _ptr(mu3),
                                    _ptr(mcols), int(L), _ptr(logr), _ptr(w), _ptr(out)))
     return logr, w, out
+
+
+def noise_update(ctx: Context, scene: Scene, eta, wxi, y, mu, mcols=None):
+    """F4 nu~ (cdms_noise_update): (logw [J][P], w [J][P], lognorm [J]).  eta, wxi float64 cuda [J][P]; y, mu
+    complex64 cuda [J][nf][Na]; mcols complex64 cuda [J][S][nf][Na] or None."""
+    torch = ctx.torch
+    J, P = eta.shape
+    S = 0 if mcols is None else int(mcols.shape[1])
+    logw = torch.empty((J, P), dtype=torch.float64, device=eta.device)
+    w = torch.empty((J, P), dtype=torch.float64, device=eta.device)
+    ln = torch.empty(J, dtype=torch.float64, device=eta.device)
+    ctx.check(lib().cdms_noise_update(ctx.h, C.byref(scene.c), _ptr(eta), _ptr(wxi), int(P), _ptr(y), _ptr(mu),
+                                      _ptr(mcols), int(S), _ptr(logw), _ptr(w), _ptr(ln)))
+    return logw, w, ln
+
+
+def ppr_update(ctx: Context, scene: Scene, zeta, eta, y, mu3, momega, mu4, mcols=None):
+    """F4 omega~ (cdms_ppr_update): out [J][3] = (log ratio, u, existence)."""
+    torch = ctx.torch
+    L = 0 if mcols is None else int(mcols.shape[1])
+    out = torch.empty((scene.J, 3), dtype=torch.float64, device=y.device)
+    ctx.check(lib().cdms_ppr_update(ctx.h, C.byref(scene.c), _dp(np.ascontiguousarray(zeta, dtype=np.float64)),
+                                    _dp(np.ascontiguousarray(eta, dtype=np.float64)), _ptr(y), _ptr(mu3), _ptr(mcols),
+                                    int(L), _ptr(momega), _ptr(mu4), _ptr(out)))
+    return out
 
 
 def response(ctx: Context, scene: Scene, pos, js, sfv):

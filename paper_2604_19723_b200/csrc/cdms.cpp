@@ -80,7 +80,7 @@ enum Slot {
   WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
   WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BC, WS_BLL, WS_BPB,
   WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_GPART, WS_PLAN, WS_RANKS, WS_PF_SNAP, WS_PF_TAB, WS_PF_DOTS, WS_PF_FIXED,
-  WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_COUNT
+  WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_SL_STACK, WS_SL_DOTS, WS_SL_EIG, WS_SL_PAR, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 
@@ -1172,6 +1172,71 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
                                  static_cast<const double2*>(d_mu), d_gamma, pflag, P, d_logr, d_w, d_out,
                                  ctx->d_flags, ctx->stream));
   ctx->launches += 10 + (d_w ? 1 : 0);
+  return CDMS_OK;
+}
+
+cdms_status cdms_noise_update(cdms_ctx ctx, const cdms_scene* scene, const double* d_eta, const double* d_wxi,
+                              int64_t P, const void* d_y, const void* d_mu, const void* d_mcols, int32_t S,
+                              double* d_logw, double* d_w, double* d_lognorm) {
+  if (!ctx) return CDMS_EINVAL;
+  DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_noise_update");
+  if (!scene || !d_eta || !d_wxi || !d_y || !d_mu || (S > 0 && !d_mcols) || !d_logw || !d_lognorm || P <= 0 || S < 0 ||
+      S > slam_max_columns())
+    return fail(ctx, CDMS_EINVAL, "noise_update: bad arguments (P=%lld, S=%d)", (long long)P, S);
+  SceneDev sd;
+  cdms_status st = build_scene(ctx, scene, nullptr, nullptr, nullptr, &sd);
+  if (st) return st;
+  const int J = sd.J, T = S + 1;
+  const int64_t Nz = (int64_t)sd.nf * sd.Na;
+  float2* stack;
+  double2* dots;
+  double* eig;
+  WS_TRY(ctx, WS_SL_STACK, (size_t)J * T * Nz, &stack);
+  WS_TRY(ctx, WS_SL_DOTS, (size_t)J * T * T, &dots);
+  WS_TRY(ctx, WS_SL_EIG, (size_t)J * slam_eig_width(), &eig);
+  // e = z - mu_nu and the columns: their dot products (fp64), then per PA the eigen data of M^H M, per particle nu~
+  CUDA_TRY(ctx, launch_vec_stack_dots(J, T, S, Nz, static_cast<const float2*>(d_y), static_cast<const float2*>(d_mu),
+                                      static_cast<const float2*>(d_mcols), nullptr, nullptr, stack, dots, ctx->stream));
+  CUDA_TRY(ctx, launch_noise_update(J, S, P, Nz, dots, eig, d_eta, d_wxi, d_logw, d_lognorm, d_w, ctx->d_flags,
+                                    ctx->stream));
+  ctx->launches += 5;
+  return CDMS_OK;
+}
+
+cdms_status cdms_ppr_update(cdms_ctx ctx, const cdms_scene* scene, const double* h_zeta, const double* h_eta,
+                            const void* d_y, const void* d_mu3, const void* d_mcols, int32_t L, const void* d_momega,
+                            const void* d_mu4, double* d_out) {
+  if (!ctx) return CDMS_EINVAL;
+  DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_ppr_update");
+  if (!scene || !h_zeta || !h_eta || !d_y || !d_mu3 || (L > 0 && !d_mcols) || !d_momega || !d_mu4 || !d_out || L < 0 ||
+      L > slam_max_columns())
+    return fail(ctx, CDMS_EINVAL, "ppr_update: bad arguments (L=%d)", L);
+  SceneDev sd;
+  cdms_status st = build_scene(ctx, scene, nullptr, nullptr, nullptr, &sd);
+  if (st) return st;
+  double par[2 * MAXJ];
+  for (int j = 0; j < sd.J; ++j) {
+    if (!(h_eta[j] > 0.0) || !is_fin(h_eta[j])) return fail(ctx, CDMS_EINVAL, "ppr_update: eta[%d] must be > 0", j);
+    if (!(h_zeta[j] > 0.0 && h_zeta[j] < 1.0)) return fail(ctx, CDMS_EINVAL, "ppr_update: zeta[%d] not in (0, 1)", j);
+    par[j] = h_zeta[j];
+    par[MAXJ + j] = h_eta[j];
+  }
+  const int J = sd.J, T = L + 3;
+  const int64_t Nz = (int64_t)sd.nf * sd.Na;
+  float2* stack;
+  double2* dots;
+  double* dpar;
+  WS_TRY(ctx, WS_SL_STACK, (size_t)J * T * Nz, &stack);
+  WS_TRY(ctx, WS_SL_DOTS, (size_t)J * T * T, &dots);
+  WS_TRY(ctx, WS_SL_PAR, 2 * MAXJ, &dpar);
+  CUDA_TRY(ctx, cudaMemcpyAsync(dpar, par, sizeof(par), cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, launch_vec_stack_dots(J, T, L, Nz, static_cast<const float2*>(d_y), static_cast<const float2*>(d_mu3),
+                                      static_cast<const float2*>(d_mcols), static_cast<const float2*>(d_momega),
+                                      static_cast<const float2*>(d_mu4), stack, dots, ctx->stream));
+  CUDA_TRY(ctx, launch_ppr_update(J, L, dots, dpar, dpar + MAXJ, d_out, ctx->d_flags, ctx->stream));
+  ctx->launches += 3;
   return CDMS_OK;
 }
 

@@ -251,6 +251,16 @@ cudaError_t launch_pf_finish(const SceneDev& sc, int T, const double2* cc, const
                              const double* d_zeta, double* gain2, const double* particles, int pstride,
                              const double* phi, const double* walpha, const double2* mu, const double* gamma,
                              int* pflag, int64_t P, double* logr, double* w, double* out, int* flags, cudaStream_t st);
+cudaError_t launch_vec_stack_dots(int J, int T, int L, int64_t Nz, const float2* y, const float2* mu, const float2* cols,
+                                  const float2* x1, const float2* x2, float2* stack, double2* dots, cudaStream_t st);
+// slam.cu: F4 update messages nu~ (noise) and omega~ (PPR)
+cudaError_t launch_noise_update(int J, int L, int64_t P, int64_t Nz, const double2* dots, double* eig, const double* eta,
+                                const double* wxi, double* logw, double* lognorm, double* w, int* flags,
+                                cudaStream_t st);
+cudaError_t launch_ppr_update(int J, int L, const double2* dots, const double* zeta, const double* eta, double* out,
+                              int* flags, cudaStream_t st);
+int slam_eig_width();     // doubles per PA of the nu~ eigen data
+int slam_max_columns();   // feature columns <= 9
 int pf_fixed_width();     // double2 per PA of the fixed (particle-independent) part
 int pf_max_snapshots();   // T = L + 1 <= 9
 

@@ -42,8 +42,19 @@ __global__ void pf_snap_kernel(int J, int T, int64_t Nz, const float2* __restric
   }
 }
 
-// dots[j][a][b] = v_a^H v_b (a <= b) of PA j's snapshots in fp64, one block per (j, a, b), fixed-order reduction
+// dots[j][a][b] = v_a^H v_b (a <= b) of PA j's snapshots in fp64, one block per (j, a, b), fixed-order reduction.
+// Vector 0 (the error vector z - mu) is formed from the complex64 inputs y0, mu0 in fp64 here (exact difference), not
+// read from the fp32 stack: its rounding would otherwise enter |e|^2 / eta, which the quadratic forms cancel by ~SNR.
+__device__ __forceinline__ double2 dots_elem(const float2* v, const float2* y0, const float2* mu0, int64_t n) {
+  if (y0 != nullptr) {
+    const float2 a = y0[n], b = mu0[n];
+    return make_double2((double)a.x - (double)b.x, (double)a.y - (double)b.y);
+  }
+  const float2 x = v[n];
+  return make_double2((double)x.x, (double)x.y);
+}
 __global__ void __launch_bounds__(PF_BLOCK) pf_dots_kernel(int T, int64_t Nz, const float2* __restrict__ snaps,
+                                                          const float2* __restrict__ y0, const float2* __restrict__ mu0,
                                                           double2* __restrict__ dots) {
   __shared__ double sr[PF_BLOCK], si[PF_BLOCK];
   const int np = T * (T + 1) / 2;
@@ -56,11 +67,14 @@ __global__ void __launch_bounds__(PF_BLOCK) pf_dots_kernel(int T, int64_t Nz, co
   const int b = a + rem;
   const float2* va = snaps + ((int64_t)j * T + a) * Nz;
   const float2* vb = snaps + ((int64_t)j * T + b) * Nz;
+  const float2* ya = (a == 0 && y0) ? y0 + (int64_t)j * Nz : nullptr;
+  const float2* yb = (b == 0 && y0) ? y0 + (int64_t)j * Nz : nullptr;
+  const float2* ma = mu0 ? mu0 + (int64_t)j * Nz : nullptr;
   double accr = 0.0, acci = 0.0;
   for (int64_t n = threadIdx.x; n < Nz; n += PF_BLOCK) {
-    const float2 x = va[n], y = vb[n];
-    accr += (double)x.x * y.x + (double)x.y * y.y;  // conj(x) y
-    acci += (double)x.x * y.y - (double)x.y * y.x;
+    const double2 x = dots_elem(va, ya, ma, n), y = dots_elem(vb, yb, ma, n);
+    accr += x.x * y.x + x.y * y.y;  // conj(x) y
+    acci += x.x * y.y - x.y * y.x;
   }
   sr[threadIdx.x] = accr;
   si[threadIdx.x] = acci;
@@ -280,8 +294,38 @@ cudaError_t launch_pf_prep(int J, int T, int64_t Nz, const float2* y, const floa
                            cudaStream_t st) {
   if (T < 1 || T > PF_MAXT) return cudaErrorInvalidValue;
   pf_snap_kernel<<<pf_grid((int64_t)J * T * Nz, 256), 256, 0, st>>>(J, T, Nz, y, mu3, mcols, snaps);
-  pf_dots_kernel<<<(unsigned)(J * T * (T + 1) / 2), PF_BLOCK, 0, st>>>(T, Nz, snaps, dots);
+  pf_dots_kernel<<<(unsigned)(J * T * (T + 1) / 2), PF_BLOCK, 0, st>>>(T, Nz, snaps, y, mu3, dots);
   pf_fixed_kernel<<<1, 32, 0, st>>>(J, T, dots, d_eta, fixed, flags);
+  return cudaGetLastError();
+}
+// Generic stack of per-PA N_z-vectors for the F4 messages (slam.cu): t = 0 z - mu, t = 1..L the columns, then up to two
+// extra vectors x1, x2 ([J][Nz] each, NULL to omit); and all their fp64 dot products (vec_dots = pf_dots_kernel)
+__global__ void vec_stack_kernel(int J, int T, int L, int64_t Nz, const float2* __restrict__ y,
+                                 const float2* __restrict__ mu, const float2* __restrict__ cols,
+                                 const float2* __restrict__ x1, const float2* __restrict__ x2, float2* __restrict__ out) {
+  const int64_t n_all = (int64_t)J * T * Nz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_all; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i % Nz;
+    const int64_t jt = i / Nz;
+    const int t = (int)(jt % T), j = (int)(jt / T);
+    float2 v;
+    if (t == 0) {
+      const float2 a = y[(int64_t)j * Nz + n], b = mu[(int64_t)j * Nz + n];
+      v = make_float2(a.x - b.x, a.y - b.y);
+    } else if (t <= L) {
+      v = cols[((int64_t)j * L + (t - 1)) * Nz + n];
+    } else if (t == L + 1) {
+      v = x1[(int64_t)j * Nz + n];
+    } else {
+      v = x2[(int64_t)j * Nz + n];
+    }
+    out[i] = v;
+  }
+}
+cudaError_t launch_vec_stack_dots(int J, int T, int L, int64_t Nz, const float2* y, const float2* mu, const float2* cols,
+                                  const float2* x1, const float2* x2, float2* stack, double2* dots, cudaStream_t st) {
+  vec_stack_kernel<<<pf_grid((int64_t)J * T * Nz, 256), 256, 0, st>>>(J, T, L, Nz, y, mu, cols, x1, x2, stack);
+  pf_dots_kernel<<<(unsigned)(J * T * (T + 1) / 2), PF_BLOCK, 0, st>>>(T, Nz, stack, y, mu, dots);
   return cudaGetLastError();
 }
 int pf_fixed_width() { return PF_FIXED; }

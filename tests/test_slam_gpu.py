@@ -69,9 +69,11 @@ def test_noise_update_parity(cd, ctx, orc, name, S):
     assert st == 0
     e = np.max(np.abs(logw.cpu().numpy() - lo) / np.maximum(1.0, np.abs(lo)))
     ew = np.max(np.abs(w.cpu().numpy() - wo))
-    record("noise_logw_rel", e, 1e-11, config=name, S=S)
+    # both sides sum N_z-long fp64 dot products (relative error ~sqrt(N_z) 1e-16) into |e|^2/eta and the Woodbury term,
+    # which cancel by up to ~1e4 into log nu~: 1e-9 relative bounds that floor at N_z = 65536 (measured 2.6e-10 at c5)
+    record("noise_logw_rel", e, 1e-9, config=name, S=S)
     record("noise_w_abs", ew, 1e-8, config=name, S=S)
-    assert e <= 1e-11, e
+    assert e <= 1e-9, e
     assert ew <= 1e-8, ew
     assert np.allclose(ln.cpu().numpy(), lno, rtol=1e-12)
 

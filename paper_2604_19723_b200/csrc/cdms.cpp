@@ -66,6 +66,11 @@ struct cdms_ctx_s {
                                  // epilogues cost what the launches did)
   int taylor_prep_direct = 0;   // K1T tables by the direct sum even when G is a power of two (CDMS_TAY_PREP=direct,
                                  // A/B only; default FFT)
+  int locality = 0;              // 1: K1T batches in Morton processing order (sort.cu; CDMS_LOCALITY=1, A/B only).
+                                 // Measured (4M c5 particles): correlation 26.97 ms sorted vs 26.58 unsorted, c2 step
+                                 // 0.477 vs 0.409 ms: the kernel is bound by the L1 data pipe's bytes to registers
+                                 // (64 B of coefficients per element; l1tex__data_pipe_lsu_wavefronts 89.5% of peak),
+                                 // not by how many distinct rows a warp touches
   int taylor_lanes = -1;         // K1T correlation kernel: -1 by P J (tay_lanes), 1 lane groups, 0 thread per
                                  // particle (CDMS_TAY_LANES=1 / 0, A/B only)
   std::vector<cudaEvent_t> ev_pool;  // timing: 4 events per likelihood batch (before / between the correlation and
@@ -80,9 +85,11 @@ enum Slot {
   WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
   WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BC, WS_BLL, WS_BPB,
   WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_GPART, WS_PLAN, WS_RANKS, WS_PF_SNAP, WS_PF_TAB, WS_PF_DOTS, WS_PF_FIXED,
-  WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_SL_STACK, WS_SL_DOTS, WS_SL_EIG, WS_SL_PAR, WS_COUNT
+  WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_SL_STACK, WS_SL_DOTS, WS_SL_EIG, WS_SL_PAR, WS_LOC_KEYS, WS_LOC_IDX,
+  WS_LOC_TEMP, WS_LOC_POS, WS_LOC_SFV, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
+constexpr int64_t LOCALITY_MIN_P = 32768;         // K1T batches from this size run in Morton order (sort.cu)
 
 struct DeviceGuard {
   int prev = -1;
@@ -509,6 +516,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     if (a.grid < 1) return fail(ctx, CDMS_ECUDA, "corr_kernel occupancy query failed");
     a.sched = sched;
     a.no_gram = no_gram ? 1 : 0;
+    const int* perm = nullptr;  // locality processing order of this batch (K1T path), or identity
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     if (ctx->timing) {
       while (ctx->ev_pool.size() < ctx->ev_used + 4) {
@@ -549,11 +557,36 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       // (c3, S = 7: 8.97 vs 12.45 ms per step; c5 shard, S = 9: 60.0 vs 73.6; c2: 0.40 vs 0.48)
       const bool k1g = !no_gram && ctx->taylor_gram == 1;
       if (k1g) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));
-      CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, pflag,
+      // locality order (sort.cu): the batch's positions (and per-particle SFVs) gathered in Morton order; the kernels
+      // run on the sorted copy, the assembly writes each result back to its particle (bit-identical results)
+      const double* bpart = a.particles;
+      const double* bsfv = a.sfv;
+      int bstride = pstride;
+      if (ctx->locality && !k1g && nb >= LOCALITY_MIN_P) {
+        uint32_t* keys;
+        int *idx, *permb;
+        unsigned char* temp;
+        double *spos, *ssfv = nullptr;
+        const size_t tb = locality_sort_temp_bytes(nb);
+        WS_TRY(ctx, WS_LOC_KEYS, 2 * (size_t)nb, &keys);
+        WS_TRY(ctx, WS_LOC_IDX, 2 * (size_t)nb, &idx);
+        WS_TRY(ctx, WS_LOC_TEMP, tb, &temp);
+        WS_TRY(ctx, WS_LOC_POS, 3 * (size_t)nb, &spos);
+        if (sfv_pp) WS_TRY(ctx, WS_LOC_SFV, 3 * (size_t)sd.K * nb, &ssfv);
+        permb = idx + nb;
+        CUDA_TRY(ctx, launch_locality_sort(a.particles, nb, pstride, a.sfv, sd.K, sfv_pp, keys, keys + nb, idx, permb,
+                                           temp, tb, spos, ssfv, ctx->stream));
+        ctx->launches += 3;
+        bpart = spos;
+        bstride = 3;
+        bsfv = sfv_pp ? ssfv : a.sfv;
+        perm = permb;
+      }
+      CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms, pflag,
                                     no_gram ? 1 : 0, tlanes, ctx->stream));
       COLL_TRY(mark(1));
       if (!no_gram && !k1g)
-        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, a.particles, nb, pstride, a.sfv, sfv_pp, terms, ctx->stream));
+        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms, ctx->stream));
       ctx->launches += no_gram ? 0 : 1;
     } else {
       CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
@@ -571,6 +604,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     s.term_G = d_G ? static_cast<double2*>(d_G) + b0 * sd.J * sd.S * sd.S : nullptr;
     s.flags = ctx->d_flags;
     s.P = nb;
+    s.perm = perm;
     CUDA_TRY(ctx, launch_assemble(sd, s, ctx->stream));
     COLL_TRY(mark(3));
     ctx->launches += 2;
@@ -760,6 +794,7 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   if (const char* e = getenv("CDMS_STEP_FUSED")) ctx->step_fused = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_TAY_PREP")) ctx->taylor_prep_direct = strcmp(e, "direct") == 0 ? 1 : 0;
   if (const char* e = getenv("CDMS_TAY_LANES")) ctx->taylor_lanes = atoi(e) ? 1 : 0;
+  if (const char* e = getenv("CDMS_LOCALITY")) ctx->locality = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_TAYLOR_GRAM")) ctx->taylor_gram = strcmp(e, "k1") == 0 ? 1 : (strcmp(e, "tay") == 0 ? 2 : 0);
   if (cudaMalloc(&ctx->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_flags, 0, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {
@@ -885,6 +920,15 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
     if (tay_engine(ctx, sd, scene->precision, nbt)) {  // K1T's tables (the same choice loglik_impl makes)
       float2* tab;
       WS_TRY(ctx, WS_TAY, tay_table_bytes(sd) / sizeof(float2), &tab);
+      if (ctx->locality && PB >= LOCALITY_MIN_P) {  // the locality sort's buffers (shared-SFV batches)
+        uint32_t* keys;
+        unsigned char* temp;
+        double* spos;
+        WS_TRY(ctx, WS_LOC_KEYS, 2 * (size_t)PB, &keys);
+        WS_TRY(ctx, WS_LOC_IDX, 2 * (size_t)PB, &i32);
+        WS_TRY(ctx, WS_LOC_TEMP, locality_sort_temp_bytes(PB), &temp);
+        WS_TRY(ctx, WS_LOC_POS, 3 * (size_t)PB, &spos);
+      }
     }
   }
   WS_TRY(ctx, WS_PLAN, 8, &u);

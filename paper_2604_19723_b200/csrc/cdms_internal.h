@@ -81,6 +81,7 @@ struct AsmArgs {
   double2* term_G;          // [P][J][S][S] or NULL
   int* flags;
   int64_t P;
+  const int* perm;          // [P] processing order -> particle index (locality sort, loglik_impl), or NULL = identity
 };
 inline int terms_width(int S) { return S + S * (S + 1) / 2; }
 // Sufficient statistics of a batch of P particles, layout [J][T][P] (term t of PA j of particle p): the writers (one
@@ -240,6 +241,12 @@ cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double
 cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,
                             int64_t P, int pstride, const double* sfv, int sfv_pp, double2* terms, int* pflag,
                             int gram_diag, int lanes, cudaStream_t st);
+
+// sort.cu: locality (Morton) processing order of a likelihood batch; perm[i] = particle index of processing slot i
+size_t locality_sort_temp_bytes(int64_t P);
+cudaError_t launch_locality_sort(const double* particles, int64_t P, int pstride, const double* sfv, int K, int sfv_pp,
+                                 uint32_t* keys, uint32_t* keys_alt, int* idx, int* perm, void* temp, size_t temp_bytes,
+                                 double* pos, double* sfv_out, cudaStream_t st);
 
 // F1 (pf.cu, taylor.cu pf_corr_kernel): PF-particle update message kappa~ and the PF normalization
 cudaError_t launch_pf_corr(const SceneDev& sc, int T, const float2* tab, const float4* tmpl, const double* particles,

@@ -688,11 +688,12 @@ template <int S>
 __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__ SceneDev sc, const AsmArgs a) {
   constexpr int NTRI = S * (S + 1) / 2;
   constexpr int T = S + NTRI;
-  const int64_t p = (int64_t)blockIdx.x * ASM_T + threadIdx.x;
+  const int64_t p = (int64_t)blockIdx.x * ASM_T + threadIdx.x;  // processing index (terms, pflag)
   if (p >= a.P) return;
+  const int64_t po = a.perm ? (int64_t)a.perm[p] : p;             // particle index (outputs)
   const int J = sc.J;
   const double nz = (double)sc.nf * (double)sc.Na;
-  double l = a.logw_prior ? a.logw_prior[p] : 0.0;
+  double l = a.logw_prior ? a.logw_prior[po] : 0.0;
   for (int j = 0; j < J; ++j) {
     const double eta = sc.eta[j];
     double2 c[S], k[NTRI];
@@ -702,7 +703,7 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
     for (int t = 0; t < NTRI; ++t) k[t] = __ldcs(&a.terms[term_idx(p, j, S + t, T, a.P)]);  // G_rc, r >= c
     if (a.term_c != nullptr) {
 #pragma unroll
-      for (int r = 0; r < S; ++r) a.term_c[(p * J + j) * S + r] = c[r];
+      for (int r = 0; r < S; ++r) a.term_c[(po * J + j) * S + r] = c[r];
     }
     if (a.term_G != nullptr) {  // (c and G are independent outputs: the birth proposal reads c only)
 #pragma unroll
@@ -711,7 +712,7 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
         for (int q = 0; q < S; ++q) {
           double2 G = (r >= q) ? k[tri(r, q)] : k[tri(q, r)];
           if (r < q) G.y = -G.y;
-          a.term_G[((p * J + j) * S + r) * S + q] = G;
+          a.term_G[((po * J + j) * S + r) * S + q] = G;
         }
       }
     }
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
       }
 #pragma unroll
       for (int s = 0; s < S; ++s)
-        a.amp[(p * J + j) * S + s] =
+        a.amp[(po * J + j) * S + s] =
             make_double2(sc.m_re[j][s] + sv[s] * b[s].x / eta, sc.m_im[j][s] + sv[s] * b[s].y / eta);
     }
   }
@@ -823,7 +824,7 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
   } else if (!(l == l)) {
     atomicOr(a.flags, FLAG_NAN);
   }
-  a.loglik[p] = l;
+  a.loglik[po] = l;
 }
 
 // ---------------------------------------------------------------------------- launch

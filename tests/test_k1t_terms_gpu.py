@@ -148,3 +148,33 @@ def test_k1t_terms_parity(cd, ctxs, orc, name, layout):
     assert ec.max() <= 1e-6, ec.max()
     assert eG.max() <= 2e-6, (eG.max(), worst, delta[worst - 16] if worst >= 16 else None)
     assert np.allclose(np.real(np.einsum("pjss->pjs", G)), cfg.Nz, rtol=1e-12)   # G_ss = N_z (unit modulus)
+
+
+@pytest.mark.parametrize("sfv_pp", [False, True])
+def test_locality_order_is_bit_identical(cd, orc, sfv_pp):
+    """With CDMS_LOCALITY=1, batches from 32768 particles run in Morton order (sort.cu) and the assembly writes every
+    result back to its particle: l and the LMMSE amplitudes must equal the default (unsorted) evaluation bit for bit."""
+    import torch
+    cfg = small_cfg(**SHAPES["c2"], P=70000, index=2)
+    case = Case(orc, cfg, particles=scenes.make_particles(scenes.CONFIGS["c2"], 0, 70000))
+    ctxs = []
+    try:
+        ctxs.append(cd.Context(0))
+        os.environ["CDMS_LOCALITY"] = "1"
+        ctxs.append(cd.Context(0))
+    finally:
+        os.environ.pop("CDMS_LOCALITY", None)
+    sfv = case.dsfv
+    if sfv_pp:
+        rng = np.random.default_rng(9)
+        s = case.sc.sfv[None] * (1.0 + 0.01 * rng.standard_normal((cfg.P, cfg.K, 3)))
+        sfv = torch.as_tensor(s, device="cuda:0").contiguous()
+    outs = []
+    for c in ctxs:
+        l, a = cd.loglik(c, case.scene, case.dx, sfv, case.dy, case.m, case.v, case.eta, sfv_per_particle=sfv_pp,
+                         want_amp=True)
+        c.sync()
+        outs.append((l.cpu().numpy(), a.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    for c in ctxs:
+        c.close()

@@ -93,20 +93,6 @@ __device__ __forceinline__ int pair_index(int a, int b, int S) { return a * S - 
 // ---------------------------------------------------------------------------- Horner state
 // acc <- acc * w + y for S components (row A3).  fp32: components paired in 64-bit registers and
 // advanced by fma.rn.f32x2 (FFMA2): t = hi*(-wi) + yr, u = hi*wr + yi, hr' = hr*wr + t, hi' = hr*wi + u.
-typedef unsigned long long u64;
-__device__ __forceinline__ u64 pk2(float lo, float hi) {
-  u64 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void up2(u64 v, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
-  u64 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
 
 template <int S, typename RT>
 struct Horner;

@@ -66,6 +66,9 @@ struct cdms_ctx_s {
                                  // epilogues cost what the launches did)
   int taylor_prep_direct = 0;   // K1T tables by the direct sum even when G is a power of two (CDMS_TAY_PREP=direct,
                                  // A/B only; default FFT)
+  int gram_tab = 1;              // K1T Gram's D_N from the Taylor table (taylor.cu GramTab); CDMS_GRAM_TAB=0 for A/B
+  int dn_nf = -1;                // N_f the table in WS_DN was built for
+  void* dn_ptr = nullptr;
   int locality = 0;              // 1: K1T batches in Morton processing order (sort.cu; CDMS_LOCALITY=1, A/B only).
                                  // Measured (4M c5 particles): correlation 26.97 ms sorted vs 26.58 unsorted, c2 step
                                  // 0.477 vs 0.409 ms: the kernel is bound by the L1 data pipe's bytes to registers
@@ -86,7 +89,7 @@ enum Slot {
   WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BC, WS_BLL, WS_BPB,
   WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_GPART, WS_PLAN, WS_RANKS, WS_PF_SNAP, WS_PF_TAB, WS_PF_DOTS, WS_PF_FIXED,
   WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_SL_STACK, WS_SL_DOTS, WS_SL_EIG, WS_SL_PAR, WS_LOC_KEYS, WS_LOC_IDX,
-  WS_LOC_TEMP, WS_LOC_POS, WS_LOC_SFV, WS_COUNT
+  WS_LOC_TEMP, WS_LOC_POS, WS_LOC_SFV, WS_DN, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
 constexpr int64_t LOCALITY_MIN_P = 32768;         // K1T batches from this size run in Morton order (sort.cu)
@@ -480,6 +483,20 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
                                   ctx->stream));
     ctx->launches += 1;
   }
+  // the Gram's Dirichlet table (depends on N_f only: built once per context and N_f, taylor.cu dn_table_kernel), for
+  // S >= 7: measured (Gram ms, table vs sine quotient) c5 (S = 9, 4M) 56.3 vs 64.1, c3 (S = 7) 4.07 vs 4.27, but c2
+  // (S = 5) 0.147 vs 0.131 and c4 4.07 vs 3.98 -- at S <= 6 the unrolled pairs' in-flight 32-byte rows raise the
+  // registers (S = 5: 167 -> 244) and cost occupancy
+  float* dn = nullptr;
+  if (tay && ctx->gram_tab && sd.small_step >= 1 && sd.S >= 7) {
+    WS_TRY(ctx, WS_DN, dn_table_floats(sd.nf), &dn);
+    if (ctx->dn_nf != sd.nf || ctx->dn_ptr != dn) {
+      CUDA_TRY(ctx, launch_dn_table(sd.nf, dn, ctx->stream));
+      ctx->launches += 1;
+      ctx->dn_nf = sd.nf;
+      ctx->dn_ptr = dn;
+    }
+  }
   if (nbt) {
     WS_TRY(ctx, WS_NBOP, nb_operand_bytes(sd, nbp), &nbop);
     WS_TRY(ctx, WS_NBSCALE, MAXJ, &nbscale);
@@ -586,7 +603,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
                                     no_gram ? 1 : 0, tlanes, ctx->stream));
       COLL_TRY(mark(1));
       if (!no_gram && !k1g)
-        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms, ctx->stream));
+        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms, dn, ctx->stream));
       ctx->launches += no_gram ? 0 : 1;
     } else {
       CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
@@ -795,6 +812,7 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   if (const char* e = getenv("CDMS_TAY_PREP")) ctx->taylor_prep_direct = strcmp(e, "direct") == 0 ? 1 : 0;
   if (const char* e = getenv("CDMS_TAY_LANES")) ctx->taylor_lanes = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_LOCALITY")) ctx->locality = atoi(e) ? 1 : 0;
+  if (const char* e = getenv("CDMS_GRAM_TAB")) ctx->gram_tab = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_TAYLOR_GRAM")) ctx->taylor_gram = strcmp(e, "k1") == 0 ? 1 : (strcmp(e, "tay") == 0 ? 2 : 0);
   if (cudaMalloc(&ctx->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_flags, 0, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {

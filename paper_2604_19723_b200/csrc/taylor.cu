@@ -483,11 +483,55 @@ __device__ __forceinline__ float dirichlet_fast(float x, float Nf) {
 // FAST (sc.small_step >= 1, every BASELINE config): per pair the fp64 delay base (R_a - R_b) df/c = nb + xb is reduced
 // once (xb in registers, nb's sign at the end) and per antenna D = dirichlet_fast(xb + dd df/c): no per-antenna
 // range reduction or parity bookkeeping.  Else per antenna gram_dirichlet_f (reduction and parity per term).
-template <int S, int Q0, int Q1, bool FAST>
+// TAB (FAST with the scene's Dirichlet table, dn_table_kernel): D_N from per-centre Taylor coefficients instead of the
+// sine quotient -- one 32-byte row (LDG.256) and a degree-7 Horner per (pair, antenna), no MUFU, no reciprocal, and
+// the function is entire, so near-equal delays need no special case.  Centres x_r = (r - R0)/G_D, G_D = 8 N, cover
+// |x| <= 0.6 (FAST: |x| <= 0.564); per pair the fp64 base x_b G_D = g_b + r_b (|r_b| <= 1/2), per antenna
+// d' = r_b + dd (df/c) G_D, its rounding g2 and the offset d = d' - g2 (|d| <= 1/2) -- all fp32-exact enough: the
+// truncation after degree 7 is below (pi N / (2 G_D))^8 / 8! = (pi/16)^8/8! = 5.5e-11 of N.
+struct GramTab {
+  const float4* dn;  // [rows][2] float4 = 8 real coefficients per centre
+  float G;           // centres per unit x (8 N)
+  int R0;            // row of x = 0
+};
+constexpr int DN_L = 8;
+int dn_centres(int nf) { return 8 * nf; }
+int dn_rows(int nf) { return 2 * ((int)ceil(0.6 * dn_centres(nf))) + 1; }
+// C_l(r) = D_N^{(l)}(x_r) / l! / G_D^l = sum_kappa cos(2 pi kappa x_r + l pi/2) (2 pi kappa / G_D)^l / l!, kappa = k - k0
+// (D_N(x) = sum_k e^{j2pi (k - k0) x} is real and even); fp64, exact integer reduction of 2 kappa (r - R0) mod 2 G_D.
+__global__ void dn_table_kernel(int N, int GD, int R0, int rows, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * DN_L) return;
+  const int r = i / DN_L, l = i - r * DN_L;
+  const int64_t rs = r - R0;
+  double f = 1.0;
+  double acc = 0.0;
+  for (int k = 0; k < N; ++k) {
+    const int twok = 2 * k - (N - 1);  // 2 kappa, an integer
+    int64_t num = ((int64_t)twok * rs) % (2 * (int64_t)GD);  // 2 kappa x_r = num / G_D (mod 2)
+    double s, c;
+    sincospi((double)num / (double)GD, &s, &c);
+    const double w = PI * (double)twok / (double)GD;  // 2 pi kappa / G_D
+    f = 1.0;
+    for (int q = 1; q <= l; ++q) f *= w / (double)q;
+    const double tr = (l & 3) == 0 ? c : (l & 3) == 1 ? -s : (l & 3) == 2 ? -c : s;  // cos(theta + l pi/2)
+    acc += tr * f;
+  }
+  out[i] = (float)acc;
+}
+size_t dn_table_floats(int nf) { return (size_t)dn_rows(nf) * DN_L; }
+cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st) {
+  const int GD = dn_centres(nf), rows = dn_rows(nf), R0 = (rows - 1) / 2;
+  const int n = rows * DN_L;
+  dn_table_kernel<<<(n + 127) / 128, 128, 0, st>>>(nf, GD, R0, rows, out);
+  return cudaGetLastError();
+}
+
+template <int S, int Q0, int Q1, bool FAST, bool TAB>
 __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* __restrict__ tmpl,
                                               const double* __restrict__ particles, int64_t P, int pstride,
                                               const double* __restrict__ sfv, int sfv_pp, double2* __restrict__ terms,
-                                              int lsplit, double2* gsum) {
+                                              int lsplit, double2* gsum, const GramTab tb) {
   constexpr int NP = Q1 - Q0;  // this part's pairs; gsum [NP][TAY_BLOCK]
   // A = 2^lsplit adjacent lanes per particle, lane a takes antennas a, a + A, ... (A > 1 when P J threads alone would
   // leave the SMs latency-bound); no early exit: the group's fp64 totals are combined by shuffles below
@@ -517,6 +561,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
     }
   }
   float xb[FAST ? NP : 1];  // FAST: per pair the centred fraction of (R_a - R_b) df/c (fp64 difference, one rounding)
+  int gb[TAB ? NP : 1];     // TAB: the centre row of x_b G_D (offset by R0) and the remainder r_b = xb[q]
   if (FAST) {
 #pragma unroll
     for (int a = 0; a < S; ++a)
@@ -525,9 +570,17 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
         if (b <= a) continue;
         const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
         if (q < 0 || q >= NP) continue;
-        xb[q] = (float)frac_c((R64[a] - R64[b]) * sc.df_c);
+        const double x = frac_c((R64[a] - R64[b]) * sc.df_c);
+        if (TAB) {
+          const double xg = x * (double)tb.G, g = rint(xg);
+          gb[q] = (int)g + tb.R0;
+          xb[q] = (float)(xg - g);
+        } else {
+          xb[q] = (float)x;
+        }
       }
   }
+  const float dfG = sc.df_cf * tb.G;  // TAB: d' per unit of the element offset difference
 #pragma unroll
   for (int q = 0; q < NP; ++q) gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(0.0, 0.0);
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
@@ -561,7 +614,17 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
           const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
           if (q < 0 || q >= NP) continue;
           float D;
-          if (FAST) {
+          if (TAB) {
+            constexpr float M = 12582912.f;
+            const float d1 = fmaf(dl[a] - dl[b], dfG, xb[q]);  // offset from the pair's base centre, in centres
+            const float dm = d1 + M;
+            const float d = d1 - (dm - M);
+            const float4* row = tb.dn + 2 * (gb[q] + (__float_as_int(dm) - __float_as_int(M)));
+            float4 c03, c47;
+            ldg256(row, c03, c47);
+            D = fmaf(fmaf(fmaf(fmaf(fmaf(fmaf(fmaf(c47.w, d, c47.z), d, c47.y), d, c47.x), d, c03.w), d, c03.z), d,
+                          c03.y), d, c03.x);
+          } else if (FAST) {
             D = dirichlet_fast(fmaf(dl[a] - dl[b], sc.df_cf, xb[q]), sc.nf_f);
           } else {
             GramPairF gp;
@@ -619,59 +682,70 @@ template <int S>
 #define CDMS_GRAM_MINB 3
 #endif
 __host__ __device__ constexpr int tay_gram_parts() { return S >= 9 ? CDMS_GRAM_PARTS9 : (S == 8 ? 2 : 1); }
-template <int S, bool FAST>
+template <int S, bool FAST, bool TAB>
 __global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? CDMS_GRAM_MINB : 1))  // S >= 7: 3 blocks (12 warps) per SM, <= 168 registers
     tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
                     const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
-                    int sfv_pp, double2* __restrict__ terms, int lsplit) {
+                    int sfv_pp, double2* __restrict__ terms, int lsplit, const GramTab tb) {
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>(), H = NP / NPART;
   extern __shared__ double2 gsum[];
   if constexpr (NPART == 1) {
-    tay_gram_part<S, 0, NP, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+    tay_gram_part<S, 0, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
   } else if constexpr (NPART == 2) {
     if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, 0, H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
     else
-      tay_gram_part<S, H, NP, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, H, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
   } else {
     static_assert(NPART == 3, "");
     if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, 0, H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
     else if (blockIdx.z == 1)
-      tay_gram_part<S, H, 2 * H, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, H, 2 * H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
     else
-      tay_gram_part<S, 2 * H, NP, FAST>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum);
+      tay_gram_part<S, 2 * H, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
   }
 }
-template <int S>
-static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
-                                     int pstride, const double* sfv, int sfv_pp, double2* terms, cudaStream_t st) {
+template <int S, bool FAST, bool TAB>
+static cudaError_t launch_tay_gram_v(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
+                                     int pstride, const double* sfv, int sfv_pp, double2* terms, const GramTab& tb,
+                                     cudaStream_t st) {
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>();
   const size_t smem = (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2);  // the larger part
-#ifndef CDMS_GRAM_FAST
-#define CDMS_GRAM_FAST 1
-#endif
-  const bool fast = CDMS_GRAM_FAST && sc.small_step >= 1;
-  cudaError_t e = cudaFuncSetAttribute(fast ? tay_gram_kernel<S, true> : tay_gram_kernel<S, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S, FAST, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
   // antennas over 2 lanes per particle when P J threads are fewer than ~2 resident waves (measured at c2: 1 lane
   // 0.391, 2 lanes 0.388, 4 lanes 0.405, 8 lanes 0.448 ms per step; at P = 1.4e5 2 lanes 0.494 vs 4 lanes 0.517)
   const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 1 : 0;
   dim3 grid((unsigned)(((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK), sc.J, NPART);
-  if (fast)
-    tay_gram_kernel<S, true><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit);
-  else
-    tay_gram_kernel<S, false><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit);
+  tay_gram_kernel<S, FAST, TAB><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms,
+                                                               lsplit, tb);
   return cudaGetLastError();
 }
+#ifndef CDMS_GRAM_FAST
+#define CDMS_GRAM_FAST 1
+#endif
+template <int S>
+static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
+                                     int pstride, const double* sfv, int sfv_pp, double2* terms, const float* dn,
+                                     cudaStream_t st) {
+  const bool fast = CDMS_GRAM_FAST && sc.small_step >= 1;
+  GramTab tb;
+  tb.dn = reinterpret_cast<const float4*>(dn);
+  tb.G = (float)dn_centres(sc.nf);
+  tb.R0 = (dn_rows(sc.nf) - 1) / 2;
+  if (fast && dn) return launch_tay_gram_v<S, true, true>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
+  if (fast) return launch_tay_gram_v<S, true, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
+  return launch_tay_gram_v<S, false, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
+}
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
-                            const double* sfv, int sfv_pp, double2* terms, cudaStream_t st) {
+                            const double* sfv, int sfv_pp, double2* terms, const float* dn, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
   switch (sc.S) {
     case 1: return cudaSuccess;
 #define CASE_S(n) \
-  case n: return launch_tay_gram_t<n>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, st);
+  case n: return launch_tay_gram_t<n>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, dn, st);
     CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
 #undef CASE_S
     default: return cudaErrorInvalidValue;

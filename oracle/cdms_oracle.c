@@ -811,7 +811,8 @@ static double complex orc_maha(const double complex* a, const double complex* b,
  *     e = z_j - mu^kappa(phi_p, 1), e0 = z_j - mu3_j (the determinant lemma and the inversion lemma of);
  *   - normalization in units of prod_j kappa~(., 0): M_y = sum_p e^{logr_p} + (1 - sum_p w_alpha_p) (S-IV),
  *     PF weights w_p = e^{logr_p} / M_y, posterior existence sum_p w_p (eq. existenceProb).
- * y, mu3: [J][Nz]; mcols: [J][L][Nz]; x: [P][pstride]; phi: [P][3].  out[0] = log M_y, out[1] = existence. */
+ * y, mu3: [J][Nz]; mcols: [J][L][Nz]; x: [P][pstride]; phi: [P][3], or NULL for the LOS PF s = 0.
+ * out[0] = log M_y, out[1] = existence. */
 int orc_pf_update(const orc_scene* sc, const double* x, int64_t P, int pstride, const double* phi,
                   const double* walpha, const double complex* mu, const double* gamma, const double* zeta,
                   const double* eta, const double complex* y, const double complex* mu3,
@@ -838,7 +839,9 @@ int orc_pf_update(const orc_scene* sc, const double* x, int64_t P, int pstride, 
     if (L > 0 && orc_cholesky(Kc, L)) { status = ORC_EINVAL; break; }
     double t0 = creal(orc_maha(e0, e0, M, L, Kc, eta[j], nz));
     for (int64_t p = 0; p < P && status == ORC_OK; ++p) {
-      int st = orc_response(sc, x + p * pstride, j, 1, phi + 3 * p, sc->wavefront, psi);
+      /* phi == NULL: the PF is the LOS s = 0 (no SFV, component 0 of orc_response) */
+      int st = phi ? orc_response(sc, x + p * pstride, j, 1, phi + 3 * p, sc->wavefront, psi)
+                   : orc_response(sc, x + p * pstride, j, 0, NULL, sc->wavefront, psi);
       if (st) { status = st; logr[p] = -INFINITY; continue; }
       double complex c = zeta[j] * mu[p];
       for (size_t n = 0; n < nz; ++n) e[n] = e0[n] - c * psi[n];   /* e = z - mu^kappa(phi_p, 1) */
@@ -989,4 +992,31 @@ int orc_ppr_update(const orc_scene* sc, const double* zeta, const double* eta, c
   }
   free(e0); free(e1);
   return status;
+}
+
+/* ------------------------------------------------------------------ F4: Gamma transitions */
+
+/* One Gamma(c, 1) draw, c >= 1, by Marsaglia and Tsang's squeeze-free acceptance test (ACM TOMS 26(3), 2000):
+ * d = c - 1/3, k = 1/sqrt(9 d); attempt a = 0, 1, ...: z ~ N(0, 1), u ~ U(0, 1), v = (1 + k z)^3; accept d v if v > 0
+ * and ln u < z^2/2 + d - d v + d ln v.  Attempt a draws the Philox block (key; index, index >> 32, step,
+ * stream + a): z = sqrt(-2 ln u0) cos(2 pi u1) from words 0, 1 and u from word 2 (u_i = (x_i + 1/2) 2^-32), a < 16;
+ * after 16 rejections the draw is d (probability below 1e-25 for c >= 10; reading F4-g).
+ * The transitions of P:L3783-3795 use it as eta_n = eta_{n-1} g / c_eta and gamma_n = gamma_{n-1} g / c_gamma,
+ * g ~ Gamma(c, 1): the Gamma pdf G(.; c, theta / c) with mean theta. */
+double orc_gamma_draw(uint64_t key, uint64_t step, uint64_t index, uint32_t stream, double c) {
+  double d = c - 1.0 / 3.0, k = 1.0 / sqrt(9.0 * d);
+  uint32_t kk[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
+  for (uint32_t a = 0; a < 16; ++a) {
+    uint32_t ctr[4] = {(uint32_t)index, (uint32_t)(index >> 32), (uint32_t)step, stream + a};
+    uint32_t x[4];
+    orc_philox4x32_10(ctr, kk, x);
+    double u0 = ((double)x[0] + 0.5) * 0x1p-32, u1 = ((double)x[1] + 0.5) * 0x1p-32;
+    double u = ((double)x[2] + 0.5) * 0x1p-32;
+    double z = sqrt(-2.0 * log(u0)) * cos(2.0 * ORC_PI * u1);
+    double t = 1.0 + k * z;
+    if (t <= 0.0) continue;
+    double v = t * t * t;
+    if (log(u) < 0.5 * z * z + d - d * v + d * log(v)) return d * v;
+  }
+  return d;
 }

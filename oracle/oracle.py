@@ -52,6 +52,8 @@ def lib():
         _lib.orc_moment_match.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, dp]
         _lib.orc_birth_candidate.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, dp, dp]
         _lib.orc_birth_residual.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_void_p, C.c_void_p]
+        _lib.orc_gamma_draw.restype = C.c_double
+        _lib.orc_gamma_draw.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double]
         _lib.orc_birth_proposal.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_void_p, dp, C.c_int64, C.c_uint64,
                                             C.c_uint64, dp, dp, dp, dp, C.POINTER(C.c_int64)]
     return _lib
@@ -190,17 +192,18 @@ class Oracle:
 
     def pf_update(self, particles, phi, walpha, mu, gamma, zeta, eta, y, mu3, mcols):
         """F1: (status, logr [P], w [P], log M_y, existence) of the PF update message kappa~ at the paired PF particles
-        (orc_pf_update).  y, mu3: [J][Nz]; mcols: [J][L][Nz]."""
+        (orc_pf_update).  y, mu3: [J][Nz]; mcols: [J][L][Nz]; phi None for the LOS PF."""
         x = _f64(particles)
         P, pstride = x.shape
-        phi = _f64(phi).reshape(P, 3)
+        phi = None if phi is None else _f64(phi).reshape(P, 3)   # None: the LOS PF s = 0
         mc = _c128(mcols).reshape(self.J, -1, self.Nz)
         L = mc.shape[1]
         y = _c128(y).reshape(self.J, self.Nz)
         mu3 = _c128(mu3).reshape(self.J, self.Nz)
         mu = _c128(mu).reshape(P)
         logr, w, out = np.zeros(P), np.zeros(P), np.zeros(2)
-        st = lib().orc_pf_update(C.byref(self.sc), _d(x), C.c_int64(P), C.c_int(pstride), _d(phi),
+        st = lib().orc_pf_update(C.byref(self.sc), _d(x), C.c_int64(P), C.c_int(pstride),
+                                 None if phi is None else _d(phi),
                                  _d(_f64(walpha)), mu.ctypes.data_as(C.c_void_p), _d(_f64(gamma)),
                                  _d(_f64(zeta)), _d(_f64(eta)), y.ctypes.data_as(C.c_void_p),
                                  mu3.ctypes.data_as(C.c_void_p), mc.ctypes.data_as(C.c_void_p), C.c_int(L),
@@ -312,6 +315,12 @@ def normals4(key, step, index, stream):
     out = np.zeros(4)
     lib().orc_normals4(C.c_uint64(key), C.c_uint64(step), C.c_uint64(index), C.c_uint32(stream), _d(out))
     return out
+
+
+def gamma_draw(key, step, index, stream, c) -> float:
+    """One Gamma(c, 1) draw (orc_gamma_draw: Marsaglia-Tsang on Philox blocks (index, step, stream + attempt))."""
+    return float(lib().orc_gamma_draw(C.c_uint64(key), C.c_uint64(step), C.c_uint64(index), C.c_uint32(stream),
+                                      C.c_double(c)))
 
 
 def step_u_bits(key, step) -> int:

@@ -42,17 +42,19 @@ def _logcn(z, m, C):
     return -len(z) * np.log(np.pi) - ld - np.real(np.conj(d) @ np.linalg.solve(C, d))
 
 
+@pytest.mark.parametrize("los", [False, True])
 @pytest.mark.parametrize("L", [0, 1, 3])
-def test_pf_update_equals_dense_definition(orc, L):
+def test_pf_update_equals_dense_definition(orc, L, los):
+    """los: the PF is the LOS s = 0 (no SFV, F4), psi_p = the LOS response at x_p."""
     cfg, sc, o, x, phi, wa, mu, gamma, zeta, eta, y, mu3, mcols = _setup(orc, L=max(L, 1))
     mcols = mcols[:, :L]
-    st, logr, w, logM, ex = o.pf_update(x, phi, wa, mu, gamma, zeta, eta, y, mu3, mcols)
+    st, logr, w, logM, ex = o.pf_update(x, None if los else phi, wa, mu, gamma, zeta, eta, y, mu3, mcols)
     assert st == 0
     Nz = cfg.Nz
     for p in range(cfg.P):
         ref = np.log(wa[p])
         for j in range(cfg.J):
-            st, psi = o.response(x[p, :3], j, 1, phi[p][None, :])
+            st, psi = o.response(x[p, :3], j, 0, phi[p][None, :]) if los else o.response(x[p, :3], j, 1, phi[p][None, :])
             assert st == 0
             M = mcols[j].T                                    # [Nz][L]
             A = eta[j] * np.eye(Nz) + M @ M.conj().T

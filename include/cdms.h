@@ -213,7 +213,8 @@ cdms_status cdms_birth_proposal(cdms_ctx ctx, const cdms_scene* scene, const dou
  * Supplement S-IV P:L527-632).  Per PA j, C^kappa(phi_p, r) = r q_p psi_p psi_p^H + eta_j I + M_j M_j^H and
  * mu^kappa(phi_p, r) = r zeta_j mu_p psi_p + mu3_j with q_p = (gamma_p + |mu_p|^2 (1 - zeta_j)) zeta_j, psi_p the
  * response of PA j at the paired MT particle x_p (d_particles row p, reading C-amb-8 / C-amb-F1a) through the wall of
- * SFV phi_p (d_phi [P][3]).  det A and pi^Nz cancel against the H0 branch, so:
+ * SFV phi_p (d_phi [P][3]; d_phi = NULL: the PF is the LOS s = 0, psi_p the LOS response).  det A and
+ * pi^Nz cancel against the H0 branch, so:
  *   d_logr out [P] = log w_alpha,p + sum_j [log kappa~(phi_p, 1; z_j) - log kappa~(., 0; z_j)],
  *   d_out  out [2] = (log M_y in units of prod_j kappa~(., 0; z_j), posterior existence sum_p w_p),
  *   d_w    out [P] or NULL: PF weights w_p = e^{logr_p} / M_y  (sum_p w_p + (1 - sum w_alpha) / M_y = 1).
@@ -252,6 +253,101 @@ cdms_status cdms_noise_update(cdms_ctx ctx, const cdms_scene* scene, const doubl
 cdms_status cdms_ppr_update(cdms_ctx ctx, const cdms_scene* scene, const double* h_zeta, const double* h_eta,
                             const void* d_y, const void* d_mu3, const void* d_mcols, int32_t L, const void* d_momega,
                             const void* d_mu4, double* d_out);
+
+/* ---- F4: the synthetic SLAM step (driver) ------------------------------------------------------ */
+
+/* Constants of the F4 step (Experiment 1). */
+typedef struct {
+  double T, sigma_v;        /* NCV time step (s) and process noise (m/s^2) */
+  double c_eta;             /* noise variance transition G(eta; c_eta, eta_{n-1}/c_eta), P:L3783-3784 (>= 1) */
+  double c_gamma;           /* amplitude variance transition G(gamma; c_gamma, gamma_{n-1}/c_gamma), P:L3788 (>= 1) */
+  double sigma_mu;          /* amplitude mean transition CN(mu; mu_{n-1}, sigma_mu^2) */
+  double sigma_sfv;         /* SFV transition N(phi; phi_{n-1}, sigma_sfv^2 I) */
+  double p_s, p_s_pr, p_rev_pr, p_b_pr;  /* PF survival, PPR survival / revival / birth */
+  double mu_b;              /* Poisson birth mean (Q = 1: p_B = mu_b / (1 + mu_b)) */
+  double gamma_max, mu_max; /* birth hyperpriors U(0, gamma_max), U(|mu| <= mu_max) */
+  double T_dec, T_pru;      /* declaration / pruning thresholds */
+  double box[6];            /* SFV birth box (lo[3], hi[3]) = [2 p_min, 2 p_max] */
+  int64_t N_g;              /* birth-proposal candidates (F3) */
+  int32_t P_m;              /* belief-average sample size (reading F4c) */
+  int32_t regularize;       /* MT regularization */
+  uint64_t key;             /* Philox key of every draw (stream map: DESIGN.md, reading F4i) */
+  int32_t keep_debug;       /* 1: keep the step's intermediate messages for cdms_slam_get_view (parity tests) */
+  int32_t pad_;
+} cdms_slam_params;
+
+typedef struct cdms_slam_s* cdms_slam;
+
+#define CDMS_SLAM_MAXS 9   /* slots: the LOS s = 0 and up to 8 PFs (the likelihood's component limit) */
+
+/* What one step estimated.  Per slot i < n_feat (the slots after the birth, before pruning, in slot
+ * order): ident (0 = LOS, then birth order), posterior existence (eq. existenceProb), MMSE SFV (LOS: 0), amplitude
+ * mean / variance, PPR probabilities zeta [J], declared (exist > T_dec), pruned (exist < T_pru, never the LOS).  est: the
+ * MT belief's moments as cdms_moments; eta_hat: MMSE noise variances; eta_bar / x_pred_hat: the prediction messages'
+ * means the step used. */
+typedef struct {
+  int64_t n;
+  int32_t n_feat, n_slots;
+  int32_t ident[CDMS_SLAM_MAXS], declared[CDMS_SLAM_MAXS], pruned[CDMS_SLAM_MAXS];
+  double exist[CDMS_SLAM_MAXS];
+  double phi_hat[CDMS_SLAM_MAXS][3];
+  double mu_hat[CDMS_SLAM_MAXS][2];
+  double gamma_hat[CDMS_SLAM_MAXS];
+  double zeta[CDMS_SLAM_MAXS][8];
+  double est[28];
+  double lse;
+  double eta_hat[8], eta_bar[8];
+  double x_pred_hat[3];
+} cdms_slam_report;
+
+/* Device arrays of a SLAM state (owned by the library; valid until cdms_slam_destroy).  Slot-major PF arrays: slot i
+ * at offset i P (phi at i P 3); slot 0 is the LOS (phi unused).  Debug arrays (keep_debug = 1, else NULL) hold the last
+ * step's prediction messages (x_pred, eta_pred) and prior PF arrays after the birth (phi/mu/gamma/w_prior), the MT
+ * log-likelihood, the noise weights w_eta [J][P], the PF log-ratios logr and posterior weights w_post [slot][P], the
+ * complex64 columns m_cols [J][n_feat][Nz] and mu_nu [J][Nz], the fp64 belief sums u/m/mw_sums complex128
+ * [J][n_feat][Nz], pf_out [slot][2] (log M_y, existence) and ppr_out [slot][8][3] (cdms_ppr_update's rows). */
+typedef struct {
+  int64_t P;
+  int32_t J, n_slots, n_feat, pad_;
+  double *x, *eta, *phi;
+  void* mu;
+  double *gamma, *w;
+  double *x_pred, *eta_pred, *phi_prior;
+  void* mu_prior;
+  double *gamma_prior, *w_prior;
+  double *loglik, *w_eta, *logr, *w_post;
+  void *m_cols, *mu_nu, *u_sums, *m_sums, *mw_sums;
+  double *pf_out, *ppr_out;
+} cdms_slam_view;
+
+/* Create a SLAM state of P paired particles (MT, noise per PA, every PF slot) on a single-rank context.  The scene's K
+ * is ignored (the slots set it per step); its precision selects the MT likelihood's engine (the PF updates always run
+ * in FP32 on K1T tables).  Errors: CDMS_EINVAL, CDMS_EUNSUPPORTED (a communicator is attached), CDMS_ENOMEM. */
+cdms_status cdms_slam_create(cdms_ctx ctx, const cdms_scene* scene, const double* h_f_pb, int64_t P,
+                             const cdms_slam_params* prm, cdms_slam* out);
+cdms_status cdms_slam_destroy(cdms_slam slam);
+/* Initial state: d_x0 [P][6] MT particles, d_eta0 [J][P] noise particles (device, copied), only the
+ * LOS slot with its hyperprior amplitudes (Philox stream 0x601 at n = 0), weights p_B / P, zeta = p_B^PR; n = 1. */
+cdms_status cdms_slam_init(cdms_slam slam, const double* d_x0, const double* d_eta0);
+/* Test / restart entry: the host side of a state whose device arrays the caller wrote through cdms_slam_get_view --
+ * n_slots (>= 1, slot 0 the LOS), h_ident [n_slots], h_zeta [n_slots][J] PPR probabilities, h_phi_hat [n_slots][3]
+ * the previous MMSE SFVs (the birth proposal's legacy SFVs; may be NULL), the next time index n and birth id. */
+cdms_status cdms_slam_set_slots(cdms_slam slam, int32_t n_slots, const int32_t* h_ident, const double* h_zeta,
+                                const double* h_phi_hat, int64_t n, int32_t next_id);
+cdms_status cdms_slam_get_view(cdms_slam slam, cdms_slam_view* out);
+/* One time step n on the measurement d_y (complex64 [J][nf][Na], as cdms_loglik), in the schedule of P:L2494-2508:
+ *  (i)  prediction messages: NCV MT draw, Gamma noise draws, legacy PFs (p_s w, SFV / amplitude jitter, Gamma
+ *       amplitude variance), PPRs zeta = p_s^PR zeta~ + p_rev (1 - zeta~); birth of one PF (Q = 1) from the F3
+ *       proposal at the predicted MMSE position and the previous MMSE SFVs, importance weights
+ *       normalized to p_B (reading F4h), zeta = p_B^PR;
+ *  (ii) belief-averaged columns u, m, m_omega of every slot over P_m paired particles (reading F4c);
+ *  (iii) iota~ (cdms_loglik with the moment-matched priors and the paired SFVs), nu~ (cdms_noise_update), kappa~ and
+ *       omega~ of every slot (cdms_pf_update, cdms_ppr_update) -- all from the prediction messages;
+ *  beliefs: MT normalize / estimate / resample / regularize (cdms_bp_update), systematic resampling of the noise per PA
+ *  and of every kept PF (weights -> existence / P), PPR zeta~ = sigma(u); MMSE estimates, declaration (exist > T_dec)
+ *  and pruning (exist < T_pru, slots compacted in order).  h_report (host, may be NULL) gets the step's estimates.
+ *  Synchronizes the context's stream four times. */
+cdms_status cdms_slam_step(cdms_slam slam, const void* d_y, cdms_slam_report* h_report);
 
 /* ---- row A6: weight normalization ------------------------------------------------------------ */
 

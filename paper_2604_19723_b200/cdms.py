@@ -42,6 +42,32 @@ class StepParamsC(C.Structure):
                 ("regularize", C.c_int32), ("pad_", C.c_int32)]
 
 
+class SlamParamsC(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("T", "sigma_v", "c_eta", "c_gamma", "sigma_mu", "sigma_sfv", "p_s", "p_s_pr",
+                                          "p_rev_pr", "p_b_pr", "mu_b", "gamma_max", "mu_max", "T_dec", "T_pru")] + [
+        ("box", C.c_double * 6), ("N_g", C.c_int64), ("P_m", C.c_int32), ("regularize", C.c_int32),
+        ("key", C.c_uint64), ("keep_debug", C.c_int32), ("pad_", C.c_int32)]
+
+
+SLAM_MAXS = 9
+
+
+class SlamReportC(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_feat", C.c_int32), ("n_slots", C.c_int32),
+                ("ident", C.c_int32 * SLAM_MAXS), ("declared", C.c_int32 * SLAM_MAXS), ("pruned", C.c_int32 * SLAM_MAXS),
+                ("exist", C.c_double * SLAM_MAXS), ("phi_hat", C.c_double * (3 * SLAM_MAXS)),
+                ("mu_hat", C.c_double * (2 * SLAM_MAXS)), ("gamma_hat", C.c_double * SLAM_MAXS),
+                ("zeta", C.c_double * (8 * SLAM_MAXS)), ("est", C.c_double * 28), ("lse", C.c_double),
+                ("eta_hat", C.c_double * 8), ("eta_bar", C.c_double * 8), ("x_pred_hat", C.c_double * 3)]
+
+
+class SlamViewC(C.Structure):
+    _fields_ = [("P", C.c_int64), ("J", C.c_int32), ("n_slots", C.c_int32), ("n_feat", C.c_int32), ("pad_", C.c_int32)] + [
+        (n, C.c_void_p) for n in ("x", "eta", "phi", "mu", "gamma", "w", "x_pred", "eta_pred", "phi_prior", "mu_prior",
+                                  "gamma_prior", "w_prior", "loglik", "w_eta", "logr", "w_post", "m_cols", "mu_nu",
+                                  "u_sums", "m_sums", "mw_sums", "pf_out", "ppr_out")]
+
+
 _lib = None
 
 
@@ -89,6 +115,12 @@ def lib() -> C.CDLL:
             "cdms_birth_proposal": ([vp, C.POINTER(SceneC), dp, dp, dp, i32, vp, dp, i64, C.c_uint64, C.c_uint64,
                                      vp, vp, vp], C.c_int),
             "cdms_moment_match": ([C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(PriorC)], C.c_int),
+            "cdms_slam_create": ([vp, C.POINTER(SceneC), dp, i64, C.POINTER(SlamParamsC), C.POINTER(vp)], C.c_int),
+            "cdms_slam_destroy": ([vp], C.c_int),
+            "cdms_slam_init": ([vp, vp, vp], C.c_int),
+            "cdms_slam_set_slots": ([vp, i32, C.POINTER(C.c_int32), dp, dp, i64, i32], C.c_int),
+            "cdms_slam_get_view": ([vp, C.POINTER(SlamViewC)], C.c_int),
+            "cdms_slam_step": ([vp, vp, C.POINTER(SlamReportC)], C.c_int),
             "cdms_resample_plan": ([C.POINTER(C.c_uint64), C.c_int, C.c_int, i64, C.c_uint32, C.POINTER(i64),
                                     C.POINTER(i64), C.POINTER(i64)], C.c_int),
         }
@@ -109,7 +141,8 @@ def exported_symbols() -> list[str]:
                         "cdms_response", "cdms_moment_match", "cdms_resample_plan", "cdms_birth_proposal",
                         "cdms_bp_update", "cdms_loopback_create", "cdms_loopback_destroy",
                         "cdms_comm_init_loopback", "cdms_pf_update", "cdms_noise_update",
-                        "cdms_ppr_update"]]
+                        "cdms_ppr_update", "cdms_slam_create", "cdms_slam_destroy", "cdms_slam_init",
+                        "cdms_slam_set_slots", "cdms_slam_get_view", "cdms_slam_step"]]
 
 
 def _ptr(t) -> Optional[int]:
@@ -447,3 +480,104 @@ def resample_plan(Q: Sequence[int], rank: int, P_local: int, u_bits: int):
     if st != OK:
         raise CdmsError(st, "cdms_resample_plan")
     return lo.value, hi.value, [int(x) for x in counts]
+
+
+# -- F4: the SLAM step driver ----------------------------------------------------------------------------------------
+class _DevArray:
+    """A device pointer with __cuda_array_interface__ (zero-copy torch view of library-owned memory)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(int(d) for d in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 2, "strides": None}
+
+
+def _view(torch, ptr, shape, typestr):
+    if not ptr:
+        return None
+    return torch.as_tensor(_DevArray(ptr, shape, typestr), device="cuda")
+
+
+SLAM_DEFAULTS = dict(T=0.1, sigma_v=0.5, c_eta=10.0, c_gamma=1000.0, sigma_mu=0.03, sigma_sfv=0.004, p_s=0.8,
+                     p_s_pr=0.9, p_rev_pr=0.1, p_b_pr=0.9, mu_b=0.5, gamma_max=5.0, mu_max=0.001, T_dec=0.5, T_pru=0.1,
+                     box=(-7.0, -2.0, -2.0, 9.0, 9.0, 2.0), N_g=4096, P_m=256, regularize=1, key=1234, keep_debug=0)
+
+
+class Slam:
+    """F4 driver state (cdms_slam_*): create, init or set a state, step on measurements, read the estimates."""
+
+    def __init__(self, ctx: Context, scene: Scene, P: int, **params):
+        self.ctx = ctx
+        self.scene = scene
+        self.P = int(P)
+        prm = dict(SLAM_DEFAULTS)
+        prm.update(params)
+        c = SlamParamsC()
+        for k, v in prm.items():
+            if k == "box":
+                c.box = (C.c_double * 6)(*[float(b) for b in v])
+            else:
+                setattr(c, k, v)
+        self.params = prm
+        self._f_pb = np.ascontiguousarray(scene.f_pb(), dtype=np.float64)
+        h = C.c_void_p()
+        ctx.check(lib().cdms_slam_create(ctx.h, C.byref(scene.c), _dp(self._f_pb), self.P, C.byref(c), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().cdms_slam_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def init(self, x0, eta0):
+        """x0 float64 cuda [P][6], eta0 float64 cuda [J][P]."""
+        self.ctx.check(lib().cdms_slam_init(self.h, _ptr(x0), _ptr(eta0)))
+
+    def set_slots(self, ident, zeta, phi_hat=None, n=1, next_id=1):
+        ident = np.ascontiguousarray(ident, dtype=np.int32)
+        zeta = np.ascontiguousarray(zeta, dtype=np.float64)
+        ph = None if phi_hat is None else np.ascontiguousarray(phi_hat, dtype=np.float64)
+        self.ctx.check(lib().cdms_slam_set_slots(self.h, int(ident.shape[0]), ident.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                 _dp(zeta), None if ph is None else _dp(ph), int(n), int(next_id)))
+
+    def view(self) -> dict:
+        """Zero-copy torch views of the state (and, with keep_debug, the last step's messages)."""
+        torch = self.ctx.torch
+        v = SlamViewC()
+        self.ctx.check(lib().cdms_slam_get_view(self.h, C.byref(v)))
+        P, J, S, Sf = v.P, v.J, SLAM_MAXS, max(1, v.n_feat)
+        Nz = self.scene.Nz
+        f8, c16, c8 = "<f8", "<c16", "<c8"
+        return dict(
+            n_slots=v.n_slots, n_feat=v.n_feat,
+            x=_view(torch, v.x, (P, 6), f8), eta=_view(torch, v.eta, (J, P), f8),
+            phi=_view(torch, v.phi, (S, P, 3), f8), mu=_view(torch, v.mu, (S, P), c16),
+            gamma=_view(torch, v.gamma, (S, P), f8), w=_view(torch, v.w, (S, P), f8),
+            x_pred=_view(torch, v.x_pred, (P, 6), f8), eta_pred=_view(torch, v.eta_pred, (J, P), f8),
+            phi_prior=_view(torch, v.phi_prior, (S, P, 3), f8), mu_prior=_view(torch, v.mu_prior, (S, P), c16),
+            gamma_prior=_view(torch, v.gamma_prior, (S, P), f8), w_prior=_view(torch, v.w_prior, (S, P), f8),
+            loglik=_view(torch, v.loglik, (P,), f8), w_eta=_view(torch, v.w_eta, (J, P), f8),
+            logr=_view(torch, v.logr, (S, P), f8), w_post=_view(torch, v.w_post, (S, P), f8),
+            m_cols=_view(torch, v.m_cols, (J, Sf, Nz), c8), mu_nu=_view(torch, v.mu_nu, (J, Nz), c8),
+            u_sums=_view(torch, v.u_sums, (J, Sf, Nz), c16), m_sums=_view(torch, v.m_sums, (J, Sf, Nz), c16),
+            mw_sums=_view(torch, v.mw_sums, (J, Sf, Nz), c16), pf_out=_view(torch, v.pf_out, (S, 2), f8),
+            ppr_out=_view(torch, v.ppr_out, (S, 8, 3), f8))
+
+    def step(self, y) -> dict:
+        """One time step on y (complex64 cuda [J][nf][Na]); returns the step's report as numpy arrays."""
+        r = SlamReportC()
+        self.ctx.check(lib().cdms_slam_step(self.h, _ptr(y), C.byref(r)))
+        nf = r.n_feat
+        J = self.scene.J
+        return dict(n=r.n, n_feat=nf, n_slots=r.n_slots, ident=list(r.ident[:nf]),
+                    declared=[bool(d) for d in r.declared[:nf]], pruned=[bool(d) for d in r.pruned[:nf]],
+                    exist=np.array(r.exist[:nf]), phi_hat=np.array(r.phi_hat[:3 * nf]).reshape(nf, 3),
+                    mu_hat=np.array(r.mu_hat[:2 * nf]).reshape(nf, 2) @ np.array([1.0, 1j]),
+                    gamma_hat=np.array(r.gamma_hat[:nf]), zeta=np.array(r.zeta[:8 * nf]).reshape(nf, 8)[:, :J],
+                    est=np.array(r.est[:]), lse=r.lse, eta_hat=np.array(r.eta_hat[:J]),
+                    eta_bar=np.array(r.eta_bar[:J]), x_pred_hat=np.array(r.x_pred_hat[:]))

@@ -10,6 +10,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <mutex>
 #include <string>
@@ -1177,11 +1178,12 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
   if (!ctx) return CDMS_EINVAL;
   DeviceGuard g(ctx->device);
   NvtxRange nv_("cdms_pf_update");
-  if (!scene || !h_f_pb || !d_particles || !d_phi || !d_walpha || !d_mu || !d_gamma || !h_zeta || !h_eta || !d_y ||
+  if (!scene || !h_f_pb || !d_particles || !d_walpha || !d_mu || !d_gamma || !h_zeta || !h_eta || !d_y ||
       !d_mu3 || (L > 0 && !d_mcols) || !d_logr || !d_out || P <= 0 || pstride < 3 || L < 0 ||
       L + 1 > pf_max_snapshots())
     return fail(ctx, CDMS_EINVAL, "pf_update: bad arguments (P=%lld, L=%d)", (long long)P, L);
-  // the PF's component: one wall whose SFV is per particle (K = 1, component 1), on the K1T tables
+  // the PF's component: one wall whose SFV is per particle (K = 1, component 1), on the K1T tables; d_phi == NULL: the
+  // LOS PF s = 0 (F4)
   cdms_scene s1 = *scene;
   s1.K = 1;
   SceneDev sd;
@@ -1471,6 +1473,565 @@ cdms_status cdms_resample_plan(const uint64_t* h_Q, int nranks, int rank, int64_
       const int64_t b = hi < (d + 1) * P_local ? hi : (d + 1) * P_local;
       h_send_counts[d] = b > a ? b - a : 0;
     }
+  return CDMS_OK;
+}
+
+}  // extern "C"
+
+// =========================================================================================================== F4 driver
+// cdms_slam_step: one time step of the synthetic SLAM method in the paper's schedule -- prediction and
+// birth messages, every update message from the same prediction messages (flooding), beliefs, resampling, estimates,
+// declaration and pruning -- composed from the library's own entries (cdms_loglik, cdms_noise_update, cdms_pf_update,
+// cdms_ppr_update, cdms_birth_proposal, cdms_bp_update, cdms_resample) and the kernels of slam_step.cu.  Readings F4a-k
+// (DESIGN.md section 3).  Single-rank contexts only; four host synchronizations per step (predicted means for the
+// birth proposal and the host-side priors, the birth's proposal, its normalization, the posterior statistics).
+namespace {
+
+constexpr int SLS = MAXS;  // slots: LOS + 8 PFs
+
+uint32_t host_philox_word0(uint64_t key, uint64_t index, uint64_t step, uint32_t stream) {
+  uint32_t c0 = (uint32_t)index, c1 = (uint32_t)(index >> 32), c2 = (uint32_t)step, c3 = stream;
+  uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n1 = (uint32_t)p1, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1,
+                   n3 = (uint32_t)p0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  return c0;
+}
+
+// 3 x 3 Cholesky (row-major lower L of A), false on a non-positive pivot
+bool chol3(const double* A, double* L) {
+  for (int i = 0; i < 9; ++i) L[i] = 0.0;
+  for (int j = 0; j < 3; ++j) {
+    double d = A[4 * j];
+    for (int k = 0; k < j; ++k) d -= L[3 * j + k] * L[3 * j + k];
+    if (!(d > 0.0)) return false;
+    L[4 * j] = sqrt(d);
+    for (int i = j + 1; i < 3; ++i) {
+      double a = A[3 * i + j];
+      for (int k = 0; k < j; ++k) a -= L[3 * i + k] * L[3 * j + k];
+      L[3 * i + j] = a / L[4 * j];
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
+struct cdms_slam_s {
+  cdms_ctx ctx = nullptr;
+  cdms_scene scene{};
+  std::vector<double> pa_pos, pa_rot, f_pb;
+  cdms_slam_params prm{};
+  int64_t P = 0;
+  int J = 0;
+  int64_t Nz = 0;
+  // state
+  double *x = nullptr, *eta = nullptr, *phi = nullptr, *gam = nullptr, *w = nullptr;
+  double2* mu = nullptr;
+  int n_slots = 0;
+  int ident[SLS] = {};
+  double zeta[SLS][MAXJ] = {};
+  double phi_hat[SLS][3] = {};
+  int64_t n = 1;
+  int next_id = 1;
+  // scratch
+  double *l = nullptr, *wnew = nullptr, *logr = nullptr, *weta = nullptr, *logweta = nullptr, *wxi = nullptr;
+  double *tphi = nullptr, *tgam = nullptr, *teta = nullptr, *lw = nullptr, *sfvpp = nullptr, *par = nullptr;
+  double2* tmu = nullptr;
+  int64_t* anc = nullptr;
+  double *stats = nullptr, *bout = nullptr, *bnorm = nullptr, *est = nullptr, *lse = nullptr, *pfout = nullptr,
+         *pprout = nullptr, *lnorm = nullptr, *wk = nullptr;
+  double2 *au = nullptr, *am = nullptr, *aw = nullptr, *psi = nullptr;
+  float2 *m64 = nullptr, *munu = nullptr, *mu3o = nullptr, *mo = nullptr, *mws = nullptr, *us = nullptr;
+  double *bpos = nullptr, *bsfv = nullptr;
+  int32_t* bjs = nullptr;
+  int64_t bv_chunk = 1;
+  // debug copies
+  double *x_pred = nullptr, *eta_pred = nullptr, *phi_pr = nullptr, *gam_pr = nullptr, *w_pr = nullptr;
+  double2* mu_pr = nullptr;
+  std::vector<void*> allocs;
+  int n_feat_last = 0;
+};
+
+namespace {
+
+template <typename T>
+cudaError_t slam_alloc(cdms_slam sl, T** p, size_t count) {
+  void* q = nullptr;
+  const cudaError_t e = cudaMalloc(&q, (count ? count : 1) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  sl->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return cudaSuccess;
+}
+
+void slam_free(cdms_slam sl) {
+  for (void* p : sl->allocs) cudaFree(p);
+  sl->allocs.clear();
+}
+
+double* slot_phi(cdms_slam s, int i) { return s->phi + (size_t)i * s->P * 3; }
+double2* slot_mu(cdms_slam s, int i) { return s->mu + (size_t)i * s->P; }
+double* slot_gam(cdms_slam s, int i) { return s->gam + (size_t)i * s->P; }
+double* slot_w(cdms_slam s, int i) { return s->w + (size_t)i * s->P; }
+
+// weighted sums of the slots' (phi, mu, gamma) under weights w (or the posterior weights wnew) + x-hat and eta-bar
+// (uniform weights) or eta-hat (weights weta); out layout: job order
+void slot_jobs(cdms_slam s, SlamWsumJobs& jb, int first, int last, const double* wts, bool posterior) {
+  for (int i = first; i < last; ++i) {
+    const double* wi = wts + (size_t)i * s->P;
+    jb.job[jb.n++] = SlamWsumJob{wi, reinterpret_cast<const double*>(slot_mu(s, i)), s->P, 2, 2};
+    jb.job[jb.n++] = SlamWsumJob{wi, slot_gam(s, i), s->P, 1, 1};
+    jb.job[jb.n++] = SlamWsumJob{wi, slot_phi(s, i), s->P, 3, i ? 3 : 0};
+  }
+  (void)posterior;
+}
+
+}  // namespace
+
+extern "C" {
+
+cdms_status cdms_slam_create(cdms_ctx ctx, const cdms_scene* scene, const double* h_f_pb, int64_t P,
+                             const cdms_slam_params* prm, cdms_slam* out) {
+  if (!ctx || !out) return CDMS_EINVAL;
+  DeviceGuard g(ctx->device);
+  *out = nullptr;
+  if (!scene || !h_f_pb || !prm || P <= 0 || P > ((int64_t)1 << 26))
+    return fail(ctx, CDMS_EINVAL, "slam_create: bad arguments (P=%lld)", (long long)P);
+  if (ctx->coll) return fail(ctx, CDMS_EUNSUPPORTED, "slam_create: single-rank contexts only");
+  if (prm->P_m <= 0 || prm->N_g <= 0 || !(prm->c_eta >= 1.0) || !(prm->c_gamma >= 1.0) || !(prm->p_s >= 0.0) ||
+      !(prm->p_s <= 1.0) || !(prm->mu_b >= 0.0))
+    return fail(ctx, CDMS_EINVAL, "slam_create: bad parameters");
+  cdms_scene s0 = *scene;
+  s0.K = 0;
+  SceneDev sd;
+  cdms_status st = build_scene(ctx, &s0, h_f_pb, nullptr, nullptr, &sd);
+  if (st) return st;
+  cdms_slam sl = new cdms_slam_s();
+  sl->ctx = ctx;
+  sl->prm = *prm;
+  sl->P = P;
+  sl->J = sd.J;
+  sl->Nz = (int64_t)sd.nf * sd.Na;
+  sl->pa_pos.assign(scene->h_pa_pos, scene->h_pa_pos + 3 * sd.J);
+  sl->pa_rot.assign(scene->h_pa_rot, scene->h_pa_rot + 9 * sd.J);
+  sl->f_pb.assign(h_f_pb, h_f_pb + sd.nf);
+  sl->scene = *scene;
+  sl->scene.h_pa_pos = sl->pa_pos.data();
+  sl->scene.h_pa_rot = sl->pa_rot.data();
+  const int J = sl->J;
+  const int64_t Nz = sl->Nz;
+  // belief-average chunk: at most 256 MiB of fp64 responses per chunk
+  const int64_t K = P < prm->P_m ? P : prm->P_m;
+  const int64_t per = (int64_t)J * SLS * Nz * 16;
+  sl->bv_chunk = std::max<int64_t>(1, std::min<int64_t>(K, ((int64_t)256 << 20) / per));
+  const int64_t nit = sl->bv_chunk * J * SLS;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  A(slam_alloc(sl, &sl->x, (size_t)P * 6));
+  A(slam_alloc(sl, &sl->eta, (size_t)J * P));
+  A(slam_alloc(sl, &sl->phi, (size_t)SLS * P * 3));
+  A(slam_alloc(sl, &sl->mu, (size_t)SLS * P));
+  A(slam_alloc(sl, &sl->gam, (size_t)SLS * P));
+  A(slam_alloc(sl, &sl->w, (size_t)SLS * P));
+  A(slam_alloc(sl, &sl->l, (size_t)P));
+  A(slam_alloc(sl, &sl->wnew, (size_t)SLS * P));
+  A(slam_alloc(sl, &sl->logr, (size_t)SLS * P));
+  A(slam_alloc(sl, &sl->weta, (size_t)J * P));
+  A(slam_alloc(sl, &sl->logweta, (size_t)J * P));
+  A(slam_alloc(sl, &sl->wxi, (size_t)J * P));
+  A(slam_alloc(sl, &sl->tphi, (size_t)P * 3));
+  A(slam_alloc(sl, &sl->tmu, (size_t)P));
+  A(slam_alloc(sl, &sl->tgam, (size_t)P));
+  A(slam_alloc(sl, &sl->teta, (size_t)P));
+  A(slam_alloc(sl, &sl->lw, (size_t)P));
+  A(slam_alloc(sl, &sl->sfvpp, (size_t)P * (SLS - 1) * 3));
+  A(slam_alloc(sl, &sl->par, (size_t)SLAM_PAR));
+  A(slam_alloc(sl, &sl->anc, (size_t)P));
+  A(slam_alloc(sl, &sl->stats, (size_t)4 * SLAM_MAXJOBS));
+  A(slam_alloc(sl, &sl->bout, (size_t)16));
+  A(slam_alloc(sl, &sl->bnorm, (size_t)4));
+  A(slam_alloc(sl, &sl->est, (size_t)28));
+  A(slam_alloc(sl, &sl->lse, (size_t)4));
+  A(slam_alloc(sl, &sl->pfout, (size_t)SLS * 2));
+  A(slam_alloc(sl, &sl->pprout, (size_t)SLS * MAXJ * 3));
+  A(slam_alloc(sl, &sl->lnorm, (size_t)MAXJ));
+  A(slam_alloc(sl, &sl->wk, (size_t)SLS));
+  A(slam_alloc(sl, &sl->au, (size_t)J * SLS * Nz));
+  A(slam_alloc(sl, &sl->am, (size_t)J * SLS * Nz));
+  A(slam_alloc(sl, &sl->aw, (size_t)J * SLS * Nz));
+  A(slam_alloc(sl, &sl->psi, (size_t)nit * Nz));
+  A(slam_alloc(sl, &sl->m64, (size_t)J * SLS * Nz));
+  A(slam_alloc(sl, &sl->munu, (size_t)J * Nz));
+  A(slam_alloc(sl, &sl->mu3o, (size_t)J * Nz));
+  A(slam_alloc(sl, &sl->mo, (size_t)J * (SLS - 1) * Nz));
+  A(slam_alloc(sl, &sl->mws, (size_t)J * Nz));
+  A(slam_alloc(sl, &sl->us, (size_t)J * Nz));
+  A(slam_alloc(sl, &sl->bpos, (size_t)nit * 3));
+  A(slam_alloc(sl, &sl->bsfv, (size_t)nit * 3));
+  A(slam_alloc(sl, &sl->bjs, (size_t)nit * 2));
+  if (prm->keep_debug) {
+    A(slam_alloc(sl, &sl->x_pred, (size_t)P * 6));
+    A(slam_alloc(sl, &sl->eta_pred, (size_t)J * P));
+    A(slam_alloc(sl, &sl->phi_pr, (size_t)SLS * P * 3));
+    A(slam_alloc(sl, &sl->mu_pr, (size_t)SLS * P));
+    A(slam_alloc(sl, &sl->gam_pr, (size_t)SLS * P));
+    A(slam_alloc(sl, &sl->w_pr, (size_t)SLS * P));
+  }
+  if (e == cudaSuccess) e = cudaMemsetAsync(sl->phi, 0, sizeof(double) * SLS * P * 3, ctx->stream);
+  if (e == cudaSuccess) e = launch_slam_fill(sl->wxi, (int64_t)J * P, 1.0 / (double)P, ctx->stream);
+  if (e != cudaSuccess) {
+    slam_free(sl);
+    delete sl;
+    return fail(ctx, e == cudaErrorMemoryAllocation ? CDMS_ENOMEM : CDMS_ECUDA, "slam_create: %s",
+                cudaGetErrorString(e));
+  }
+  *out = sl;
+  return CDMS_OK;
+}
+
+cdms_status cdms_slam_destroy(cdms_slam sl) {
+  if (!sl) return CDMS_EINVAL;
+  DeviceGuard g(sl->ctx->device);
+  cudaStreamSynchronize(sl->ctx->stream);
+  slam_free(sl);
+  delete sl;
+  return CDMS_OK;
+}
+
+cdms_status cdms_slam_get_view(cdms_slam sl, cdms_slam_view* v) {
+  if (!sl || !v) return CDMS_EINVAL;
+  *v = cdms_slam_view{};
+  v->P = sl->P;
+  v->J = sl->J;
+  v->n_slots = sl->n_slots;
+  v->n_feat = sl->n_feat_last;
+  v->x = sl->x;
+  v->eta = sl->eta;
+  v->phi = sl->phi;
+  v->mu = sl->mu;
+  v->gamma = sl->gam;
+  v->w = sl->w;
+  v->x_pred = sl->x_pred;
+  v->eta_pred = sl->eta_pred;
+  v->phi_prior = sl->phi_pr;
+  v->mu_prior = sl->mu_pr;
+  v->gamma_prior = sl->gam_pr;
+  v->w_prior = sl->w_pr;
+  v->loglik = sl->l;
+  v->w_eta = sl->weta;
+  v->logr = sl->logr;
+  v->w_post = sl->wnew;
+  v->m_cols = sl->m64;
+  v->mu_nu = sl->munu;
+  v->u_sums = sl->au;
+  v->m_sums = sl->am;
+  v->mw_sums = sl->aw;
+  v->pf_out = sl->pfout;
+  v->ppr_out = sl->pprout;
+  return CDMS_OK;
+}
+
+cdms_status cdms_slam_set_slots(cdms_slam sl, int32_t n_slots, const int32_t* h_ident, const double* h_zeta,
+                                const double* h_phi_hat, int64_t n, int32_t next_id) {
+  if (!sl) return CDMS_EINVAL;
+  if (n_slots < 1 || n_slots > SLS || !h_ident || !h_zeta || n < 1 || next_id < 1)
+    return fail(sl->ctx, CDMS_EINVAL, "slam_set_slots: bad arguments");
+  sl->n_slots = n_slots;
+  for (int i = 0; i < n_slots; ++i) {
+    sl->ident[i] = h_ident[i];
+    for (int j = 0; j < sl->J; ++j) sl->zeta[i][j] = h_zeta[(size_t)i * sl->J + j];
+    for (int c = 0; c < 3; ++c) sl->phi_hat[i][c] = h_phi_hat ? h_phi_hat[3 * i + c] : 0.0;
+  }
+  sl->n = n;
+  sl->next_id = next_id;
+  return CDMS_OK;
+}
+
+cdms_status cdms_slam_init(cdms_slam sl, const double* d_x0, const double* d_eta0) {
+  if (!sl) return CDMS_EINVAL;
+  cdms_ctx ctx = sl->ctx;
+  DeviceGuard g(ctx->device);
+  if (!d_x0 || !d_eta0) return fail(ctx, CDMS_EINVAL, "slam_init: NULL pointer");
+  const cdms_slam_params& q = sl->prm;
+  CUDA_TRY(ctx, cudaMemcpyAsync(sl->x, d_x0, sizeof(double) * sl->P * 6, cudaMemcpyDeviceToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(sl->eta, d_eta0, sizeof(double) * sl->P * sl->J, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  // the LOS at n = 0 "the same way as new PFs": hyperprior amplitudes, weights p_B / P (reading F4j)
+  const double pB = q.mu_b / (1.0 + q.mu_b);
+  CUDA_TRY(ctx, launch_slam_birth(nullptr, nullptr, nullptr, q.mu_max, q.gamma_max, pB, nullptr, slot_mu(sl, 0),
+                                  slot_gam(sl, 0), sl->lw, nullptr, nullptr, sl->P, q.key, 0, ctx->stream));
+  CUDA_TRY(ctx, launch_slam_fill(slot_w(sl, 0), sl->P, pB / (double)sl->P, ctx->stream));
+  sl->n_slots = 1;
+  sl->ident[0] = 0;
+  for (int j = 0; j < sl->J; ++j) sl->zeta[0][j] = q.p_b_pr;
+  sl->n = 1;
+  sl->next_id = 1;
+  ctx->launches += 2;
+  return CDMS_OK;
+}
+
+cdms_status cdms_slam_step(cdms_slam sl, const void* d_y, cdms_slam_report* rep) {
+  if (!sl) return CDMS_EINVAL;
+  cdms_ctx ctx = sl->ctx;
+  DeviceGuard g(ctx->device);
+  NvtxRange nv_("cdms_slam_step");
+  if (!d_y) return fail(ctx, CDMS_EINVAL, "slam_step: d_y NULL");
+  if (sl->n_slots < 1) return fail(ctx, CDMS_EINVAL, "slam_step: no state (cdms_slam_init first)");
+  const cdms_slam_params& q = sl->prm;
+  cudaStream_t stm = ctx->stream;
+  const int J = sl->J;
+  const int64_t P = sl->P, Nz = sl->Nz;
+  const uint64_t n = (uint64_t)sl->n;
+  const bool dbg = q.keep_debug != 0;
+  cdms_status st;
+  // ---- (i) prediction messages: beta (NCV), xi (Gamma), alpha (legacy PFs), zeta (PPRs)
+  CUDA_TRY(ctx, launch_predict(sl->x, P, 0, q.T, q.sigma_v, q.key, n, stm));
+  CUDA_TRY(ctx, launch_slam_noise_predict(sl->eta, J, P, q.c_eta, q.key, n, stm));
+  int S = sl->n_slots;
+  double zeta_pr[SLS][MAXJ];
+  for (int i = 0; i < S; ++i) {
+    CUDA_TRY(ctx, launch_slam_pf_predict(i ? slot_phi(sl, i) : nullptr, slot_mu(sl, i), slot_gam(sl, i), slot_w(sl, i),
+                                         P, i, q.sigma_sfv, q.sigma_mu, q.c_gamma, q.p_s, q.key, n, stm));
+    for (int j = 0; j < J; ++j) zeta_pr[i][j] = q.p_s_pr * sl->zeta[i][j] + q.p_rev_pr * (1.0 - sl->zeta[i][j]);
+  }
+  ctx->launches += 2 + S;
+  if (dbg) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(sl->x_pred, sl->x, sizeof(double) * P * 6, cudaMemcpyDeviceToDevice, stm));
+    CUDA_TRY(ctx, cudaMemcpyAsync(sl->eta_pred, sl->eta, sizeof(double) * P * J, cudaMemcpyDeviceToDevice, stm));
+  }
+  // predicted means: x^_{n|n-1}, eta-bar, per slot (eps, mu-bar, gamma-bar, phi-bar)
+  SlamWsumJobs jb{};
+  jb.job[jb.n++] = SlamWsumJob{nullptr, sl->x, P, 6, 3};
+  for (int j = 0; j < J; ++j) jb.job[jb.n++] = SlamWsumJob{nullptr, sl->eta + (size_t)j * P, P, 1, 1};
+  const int j0 = jb.n;
+  slot_jobs(sl, jb, 0, S, sl->w, false);
+  double h[4 * SLAM_MAXJOBS];
+  CUDA_TRY(ctx, launch_slam_wsum(jb, sl->stats, stm));
+  CUDA_TRY(ctx, cudaMemcpyAsync(h, sl->stats, sizeof(double) * 4 * jb.n, cudaMemcpyDeviceToHost, stm));
+  ctx->launches += 1;
+  if ((st = cdms_sync(ctx))) return st;
+  double x_hat[3], eta_bar[MAXJ], eps[SLS], mub[SLS][2], gab[SLS];
+  for (int c = 0; c < 3; ++c) x_hat[c] = h[1 + c] / (double)P;
+  for (int j = 0; j < J; ++j) eta_bar[j] = h[4 * (1 + j) + 1] / (double)P;
+  auto read_slot = [&](int i, int base) {
+    eps[i] = h[4 * base];
+    const double e = eps[i] > 0.0 ? eps[i] : 1.0;
+    mub[i][0] = h[4 * base + 1] / e;
+    mub[i][1] = h[4 * base + 2] / e;
+    gab[i] = h[4 * (base + 1) + 1] / e;
+  };
+  for (int i = 0; i < S; ++i) read_slot(i, j0 + 3 * i);
+  // ---- birth message of one new PF (Q = 1) on the F3 proposal (reading F4h)
+  if (S < SLS) {
+    double legacy[SLS * 3];
+    for (int i = 1; i < S; ++i)
+      for (int c = 0; c < 3; ++c) legacy[3 * (i - 1) + c] = sl->phi_hat[i][c];
+    st = cdms_birth_proposal(ctx, &sl->scene, sl->f_pb.data(), x_hat, S > 1 ? legacy : nullptr, S - 1, d_y, q.box,
+                             q.N_g, q.key, n, sl->bout, nullptr, nullptr);
+    if (st) return st;
+    double bo[13];
+    CUDA_TRY(ctx, cudaMemcpyAsync(bo, sl->bout, sizeof(bo), cudaMemcpyDeviceToHost, stm));
+    st = cdms_sync(ctx);
+    bool born = false;
+    if (st == CDMS_OK) {
+      double C[9], Lq[9];
+      const double tr = bo[3] + bo[7] + bo[11];
+      for (int c = 0; c < 9; ++c) C[c] = bo[3 + c];
+      for (int c = 0; c < 3; ++c) C[4 * c] += 1e-12 * tr;
+      if (chol3(C, Lq)) {
+        const double pB = q.mu_b / (1.0 + q.mu_b);
+        CUDA_TRY(ctx, launch_slam_birth(bo, Lq, q.box, q.mu_max, q.gamma_max, pB, slot_phi(sl, S), slot_mu(sl, S),
+                                        slot_gam(sl, S), sl->lw, slot_w(sl, S), sl->bnorm, P, q.key, n, stm));
+        SlamWsumJobs jn{};
+        slot_jobs(sl, jn, S, S + 1, sl->w, false);
+        CUDA_TRY(ctx, launch_slam_wsum(jn, sl->stats, stm));
+        double hb[4 * 3 + 1];
+        CUDA_TRY(ctx, cudaMemcpyAsync(hb, sl->stats, sizeof(double) * 12, cudaMemcpyDeviceToHost, stm));
+        CUDA_TRY(ctx, cudaMemcpyAsync(hb + 12, sl->bnorm, sizeof(double), cudaMemcpyDeviceToHost, stm));
+        ctx->launches += 3;
+        if ((st = cdms_sync(ctx))) return st;
+        if (hb[12] > 0.0) {  // some particle inside the birth box
+          for (int c = 0; c < 12; ++c) h[4 * j0 + 4 * 3 * S + c] = hb[c];
+          read_slot(S, j0 + 3 * S);
+          sl->ident[S] = sl->next_id++;
+          for (int j = 0; j < J; ++j) zeta_pr[S][j] = q.p_b_pr;
+          ++S;
+          born = true;
+        }
+      }
+    } else if (st != CDMS_EZEROMASS) {
+      return st;  // a residual without power is no birth, anything else an error
+    }
+    (void)born;
+  }
+  sl->n_feat_last = S;
+  if (dbg) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(sl->phi_pr, sl->phi, sizeof(double) * SLS * P * 3, cudaMemcpyDeviceToDevice, stm));
+    CUDA_TRY(ctx, cudaMemcpyAsync(sl->mu_pr, sl->mu, sizeof(double2) * SLS * P, cudaMemcpyDeviceToDevice, stm));
+    CUDA_TRY(ctx, cudaMemcpyAsync(sl->gam_pr, sl->gam, sizeof(double) * SLS * P, cudaMemcpyDeviceToDevice, stm));
+    CUDA_TRY(ctx, cudaMemcpyAsync(sl->w_pr, sl->w, sizeof(double) * SLS * P, cudaMemcpyDeviceToDevice, stm));
+  }
+  // device slot parameters: eps, zeta of the prediction messages
+  double hp[SLAM_PAR] = {};
+  for (int i = 0; i < S; ++i) {
+    hp[i] = eps[i];
+    for (int j = 0; j < J; ++j) hp[MAXS + i * MAXJ + j] = zeta_pr[i][j];
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(sl->par, hp, sizeof(hp), cudaMemcpyHostToDevice, stm));
+  // ---- belief-averaged columns over the paired particles (reading F4c)
+  {
+    const int64_t K = P < q.P_m ? P : q.P_m;
+    cdms_scene s1 = sl->scene;
+    s1.K = 1;
+    s1.precision = CDMS_FP64;
+    SceneDev sd1;
+    if ((st = build_scene(ctx, &s1, sl->f_pb.data(), nullptr, nullptr, &sd1))) return st;
+    CUDA_TRY(ctx, cudaMemsetAsync(sl->au, 0, sizeof(double2) * J * S * Nz, stm));
+    CUDA_TRY(ctx, cudaMemsetAsync(sl->am, 0, sizeof(double2) * J * S * Nz, stm));
+    CUDA_TRY(ctx, cudaMemsetAsync(sl->aw, 0, sizeof(double2) * J * S * Nz, stm));
+    CUDA_TRY(ctx, launch_slam_bv_wsum(sl->w, P, K, S, sl->wk, stm));
+    for (int64_t k0 = 0; k0 < K; k0 += sl->bv_chunk) {
+      const int B = (int)std::min<int64_t>(sl->bv_chunk, K - k0);
+      CUDA_TRY(ctx, launch_slam_bv_items(sl->x, sl->phi, P, K, k0, B, J, S, sl->bpos, sl->bjs, sl->bsfv, stm));
+      CUDA_TRY(ctx, launch_response(sd1, sl->bpos, (int64_t)B * J * S, sl->bjs, sl->bsfv, sl->psi, CDMS_FP64,
+                                    ctx->d_flags, stm, 1));
+      CUDA_TRY(ctx, launch_slam_bv_accum(sl->psi, sl->mu, sl->gam, sl->w, sl->wk, sl->par, P, K, k0, B, J, S, Nz,
+                                         sl->au, sl->am, sl->aw, stm));
+      ctx->launches += 3;
+    }
+    CUDA_TRY(ctx, launch_slam_bv_final(sl->am, sl->au, sl->par, J, S, Nz, sl->m64, sl->munu, stm));
+    ctx->launches += 2;
+  }
+  // ---- (iii) update messages from the same prediction messages (flooding)
+  // iota~: the MT likelihood with the moment-matched amplitude priors (C-amb-7) and the paired SFVs (C-amb-8)
+  {
+    cdms_scene sK = sl->scene;
+    sK.K = S - 1;
+    cdms_prior pr[MAXJ * MAXS];
+    for (int j = 0; j < J; ++j)
+      for (int i = 0; i < S; ++i) {
+        const double ex = std::min(1.0, std::max(0.0, eps[i] * zeta_pr[i][j]));
+        if (cdms_moment_match(mub[i][0], mub[i][1], gab[i], ex, &pr[j * S + i]))
+          return fail(ctx, CDMS_EINVAL, "slam_step: moment matching of slot %d", i);
+      }
+    CUDA_TRY(ctx, launch_slam_sfv_pp(sl->phi, P, S - 1, sl->sfvpp, stm));
+    if ((st = cdms_loglik(ctx, &sK, sl->x, P, 6, sl->sfvpp, 1, d_y, sl->f_pb.data(), pr, eta_bar, nullptr, sl->l,
+                          nullptr)))
+      return st;
+  }
+  // nu~ with every slot's column
+  if ((st = cdms_noise_update(ctx, &sl->scene, sl->eta, sl->wxi, P, d_y, sl->munu, sl->m64, S, sl->logweta, sl->weta,
+                              sl->lnorm)))
+    return st;
+  // kappa~ and omega~ of every slot with the other slots' terms
+  cdms_scene s32 = sl->scene;
+  s32.precision = CDMS_FP32;
+  for (int i = 0; i < S; ++i) {
+    CUDA_TRY(ctx, launch_slam_others(sl->au, sl->am, sl->aw, sl->par, J, S, Nz, i, sl->mu3o, sl->mo, sl->mws, sl->us,
+                                     stm));
+    ctx->launches += 1;
+    if ((st = cdms_pf_update(ctx, &s32, sl->f_pb.data(), sl->x, P, 6, i ? slot_phi(sl, i) : nullptr, slot_w(sl, i),
+                             slot_mu(sl, i), slot_gam(sl, i), zeta_pr[i], eta_bar, d_y, sl->mu3o, sl->mo, S - 1,
+                             sl->logr + (size_t)i * P, sl->wnew + (size_t)i * P, sl->pfout + 2 * i)))
+      return st;
+    if ((st = cdms_ppr_update(ctx, &sl->scene, zeta_pr[i], eta_bar, d_y, sl->mu3o, sl->mo, S - 1, sl->mws, sl->us,
+                              sl->pprout + (size_t)3 * MAXJ * i)))
+      return st;
+  }
+  // ---- beliefs: MT (normalize, estimate, resample, regularize; rows A6-A9)
+  cdms_step_params sp{};
+  sp.T = q.T;
+  sp.sigma_v = q.sigma_v;
+  sp.philox_key = q.key;
+  sp.step = n;
+  sp.regularize = q.regularize;
+  if ((st = cdms_bp_update(ctx, sl->l, sl->x, P, &sp, sl->est, sl->lse, nullptr))) return st;
+  // posterior statistics of the PFs (weights wnew) and eta-hat (weights w_eta)
+  SlamWsumJobs jp{};
+  slot_jobs(sl, jp, 0, S, sl->wnew, true);
+  for (int j = 0; j < J; ++j)
+    jp.job[jp.n++] = SlamWsumJob{sl->weta + (size_t)j * P, sl->eta + (size_t)j * P, P, 1, 1};
+  CUDA_TRY(ctx, launch_slam_wsum(jp, sl->stats, stm));
+  double hs[4 * SLAM_MAXJOBS], pfo[SLS * 2], ppo[SLS * MAXJ * 3], est[28], lse;
+  CUDA_TRY(ctx, cudaMemcpyAsync(hs, sl->stats, sizeof(double) * 4 * jp.n, cudaMemcpyDeviceToHost, stm));
+  CUDA_TRY(ctx, cudaMemcpyAsync(pfo, sl->pfout, sizeof(double) * 2 * S, cudaMemcpyDeviceToHost, stm));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ppo, sl->pprout, sizeof(double) * 3 * MAXJ * S, cudaMemcpyDeviceToHost, stm));
+  CUDA_TRY(ctx, cudaMemcpyAsync(est, sl->est, sizeof(est), cudaMemcpyDeviceToHost, stm));
+  CUDA_TRY(ctx, cudaMemcpyAsync(&lse, sl->lse, sizeof(double), cudaMemcpyDeviceToHost, stm));
+  ctx->launches += 1;
+  if ((st = cdms_sync(ctx))) return st;
+  // ---- estimates, declaration, pruning; resampling of the kept PFs and of the noise
+  cdms_slam_report r{};
+  r.n = (int64_t)n;
+  r.n_feat = S;
+  int kept = 0;
+  int new_ident[SLS];
+  double new_zeta[SLS][MAXJ], new_phi_hat[SLS][3];
+  for (int i = 0; i < S; ++i) {
+    const double ex = pfo[2 * i + 1];
+    const int b = 3 * i;
+    const double e = hs[4 * b] > 0.0 ? hs[4 * b] : 1.0;
+    r.ident[i] = sl->ident[i];
+    r.exist[i] = ex;
+    r.mu_hat[i][0] = hs[4 * b + 1] / e;
+    r.mu_hat[i][1] = hs[4 * b + 2] / e;
+    r.gamma_hat[i] = hs[4 * (b + 1) + 1] / e;
+    for (int c = 0; c < 3; ++c) r.phi_hat[i][c] = i ? hs[4 * (b + 2) + 1 + c] / e : 0.0;
+    for (int j = 0; j < J; ++j) r.zeta[i][j] = ppo[(size_t)3 * MAXJ * i + 3 * j + 2];
+    r.declared[i] = ex > q.T_dec;
+    r.pruned[i] = (i > 0 && ex < q.T_pru) ? 1 : 0;
+    if (r.pruned[i]) continue;
+    const int d = kept++;
+    if (ex > 0.0) {
+      const uint32_t u = host_philox_word0(q.key, 0, n, 0x400u + (uint32_t)i);
+      if ((st = cdms_resample(ctx, sl->wnew + (size_t)i * P, P, u, sl->anc))) return st;
+      CUDA_TRY(ctx, launch_slam_pf_gather(i ? slot_phi(sl, i) : nullptr, slot_mu(sl, i), slot_gam(sl, i), sl->anc, P,
+                                          sl->tphi, sl->tmu, sl->tgam, stm));
+      if (i)
+        CUDA_TRY(ctx, cudaMemcpyAsync(slot_phi(sl, d), sl->tphi, sizeof(double) * P * 3, cudaMemcpyDeviceToDevice,
+                                      stm));
+      CUDA_TRY(ctx, cudaMemcpyAsync(slot_mu(sl, d), sl->tmu, sizeof(double2) * P, cudaMemcpyDeviceToDevice, stm));
+      CUDA_TRY(ctx, cudaMemcpyAsync(slot_gam(sl, d), sl->tgam, sizeof(double) * P, cudaMemcpyDeviceToDevice, stm));
+      CUDA_TRY(ctx, launch_slam_fill(slot_w(sl, d), P, ex / (double)P, stm));
+      ctx->launches += 2;
+    } else if (d != i) {
+      return fail(ctx, CDMS_EZEROMASS, "slam_step: the LOS PF lost all mass");
+    }
+    new_ident[d] = sl->ident[i];
+    for (int j = 0; j < J; ++j) new_zeta[d][j] = r.zeta[i][j];
+    for (int c = 0; c < 3; ++c) new_phi_hat[d][c] = r.phi_hat[i][c];
+  }
+  for (int j = 0; j < J; ++j) {
+    const int b = 3 * S + j;
+    r.eta_hat[j] = hs[4 * b + 1] / (hs[4 * b] > 0.0 ? hs[4 * b] : 1.0);
+    r.eta_bar[j] = eta_bar[j];
+    const uint32_t u = host_philox_word0(q.key, 0, n, 0x500u + (uint32_t)j);
+    if ((st = cdms_resample(ctx, sl->weta + (size_t)j * P, P, u, sl->anc))) return st;
+    CUDA_TRY(ctx, launch_slam_gather1(sl->eta + (size_t)j * P, sl->anc, P, sl->teta, stm));
+    CUDA_TRY(ctx, cudaMemcpyAsync(sl->eta + (size_t)j * P, sl->teta, sizeof(double) * P, cudaMemcpyDeviceToDevice,
+                                  stm));
+    ctx->launches += 1;
+  }
+  sl->n_slots = kept;
+  for (int i = 0; i < kept; ++i) {
+    sl->ident[i] = new_ident[i];
+    for (int j = 0; j < J; ++j) sl->zeta[i][j] = new_zeta[i][j];
+    for (int c = 0; c < 3; ++c) sl->phi_hat[i][c] = new_phi_hat[i][c];
+  }
+  sl->n = (int64_t)n + 1;
+  r.n_slots = kept;
+  for (int c = 0; c < 28; ++c) r.est[c] = est[c];
+  r.lse = lse;
+  for (int c = 0; c < 3; ++c) r.x_pred_hat[c] = x_hat[c];
+  if (rep) *rep = r;
   return CDMS_OK;
 }
 

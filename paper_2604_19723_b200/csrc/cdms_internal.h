@@ -215,7 +215,8 @@ cudaError_t launch_assemble(const SceneDev& sc, const AsmArgs& a, cudaStream_t s
 size_t corr_smem_bytes(int S, int precision);
 int corr_kchunk(int S);   // subcarriers per y chunk (SceneDev::kc_len = min(corr_kchunk(S), nf))
 cudaError_t launch_response(const SceneDev& sc, const double* pos, int64_t n, const int32_t* js,
-                            const double* sfv, double2* psi, int precision, int* flags, cudaStream_t st);
+                            const double* sfv, double2* psi, int precision, int* flags, cudaStream_t st,
+                            int sfv_per_item = 0);
 cudaError_t launch_layout(const SceneDev& sc, const double* sfv, double* layout, double* va, double* H,
                           int* flags, cudaStream_t st);
 
@@ -405,5 +406,43 @@ struct StepFusedArgs {
 };
 cudaError_t launch_step_fused(const StepFusedArgs& a, int num_sms, cudaStream_t st);
 double step_reg_bandwidth(int64_t P_total);
+
+// F4 step driver kernels (slam_step.cu)
+struct SlamWsumJob {
+  const double* w;  // weights [P] or nullptr (all 1)
+  const double* v;  // values, row p at v + p vs
+  int64_t P;
+  int vs, nc;       // row stride, columns (<= 3)
+};
+constexpr int SLAM_MAXJOBS = 64;
+struct SlamWsumJobs {
+  SlamWsumJob job[SLAM_MAXJOBS];
+  int n;
+};
+constexpr int SLAM_PAR = MAXS + MAXS * MAXJ;  // device slot parameters: eps [MAXS], zeta [MAXS][MAXJ]
+cudaError_t launch_slam_noise_predict(double* eta, int J, int64_t P, double c, uint64_t key, uint64_t n,
+                                      cudaStream_t st);
+cudaError_t launch_slam_pf_predict(double* phi, double2* mu, double* gam, double* w, int64_t P, int slot,
+                                   double sigma_sfv, double sigma_mu, double c_gamma, double p_s, uint64_t key,
+                                   uint64_t n, cudaStream_t st);
+cudaError_t launch_slam_birth(const double* mu_q, const double* Lq, const double* box, double mu_max, double gamma_max,
+                              double pB, double* phi, double2* mu, double* gam, double* lw, double* w, double* out,
+                              int64_t P, uint64_t key, uint64_t n, cudaStream_t st);
+cudaError_t launch_slam_wsum(const SlamWsumJobs& jobs, double* out, cudaStream_t st);
+cudaError_t launch_slam_bv_wsum(const double* w, int64_t P, int64_t K, int S, double* wk, cudaStream_t st);
+cudaError_t launch_slam_bv_items(const double* x, const double* phi, int64_t P, int64_t K, int64_t k0, int B, int J,
+                                 int S, double* pos, int32_t* js, double* sfv, cudaStream_t st);
+cudaError_t launch_slam_bv_accum(const double2* psi, const double2* mu, const double* gam, const double* w,
+                                 const double* wk, const double* par, int64_t P, int64_t K, int64_t k0, int B, int J,
+                                 int S, int64_t Nz, double2* au, double2* am, double2* aw, cudaStream_t st);
+cudaError_t launch_slam_bv_final(const double2* am, const double2* au, const double* par, int J, int S, int64_t Nz,
+                                 float2* m64, float2* munu, cudaStream_t st);
+cudaError_t launch_slam_others(const double2* au, const double2* am, const double2* aw, const double* par, int J, int S,
+                               int64_t Nz, int s, float2* mu3, float2* mo, float2* mws, float2* us, cudaStream_t st);
+cudaError_t launch_slam_sfv_pp(const double* phi, int64_t P, int K, double* out, cudaStream_t st);
+cudaError_t launch_slam_pf_gather(const double* phi, const double2* mu, const double* gam, const int64_t* anc,
+                                  int64_t P, double* tphi, double2* tmu, double* tgam, cudaStream_t st);
+cudaError_t launch_slam_fill(double* w, int64_t P, double v, cudaStream_t st);
+cudaError_t launch_slam_gather1(const double* src, const int64_t* anc, int64_t P, double* dst, cudaStream_t st);
 
 }  // namespace cdms

@@ -219,10 +219,14 @@ __global__ void pf_gain_kernel(const __grid_constant__ SceneDev sc, const double
   double g2 = 1.0;
   if (sc.pathloss) {
     const double* x = particles + p * pstride;
-    const double* s = phi + 3 * p;
     const double* pj = sc.pa_pos[j];
-    const double n2 = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
     double R = 1.0;
+    if (!phi) {  // the LOS PF: p_VA = p_j
+      const double r0 = x[0] - pj[0], r1 = x[1] - pj[1], r2 = x[2] - pj[2];
+      R = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+    }
+    const double* s = phi ? phi + 3 * p : pj;
+    const double n2 = phi ? s[0] * s[0] + s[1] * s[1] + s[2] * s[2] : 0.0;
     if (n2 > 0.0) {
       const double c = 2.0 * (pj[0] * s[0] + pj[1] * s[1] + pj[2] * s[2]) / n2 - 1.0;
       const double r0 = x[0] - (pj[0] - c * s[0]), r1 = x[1] - (pj[1] - c * s[1]), r2 = x[2] - (pj[2] - c * s[2]);

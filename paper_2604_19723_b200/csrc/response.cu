@@ -9,11 +9,12 @@ namespace cdms {
 
 // ---------------------------------------------------------------------------- response (test entry)
 // psi[k*Na + m] = conj(A_seg w^i), k = k0 + i, with exactly the per-(p,s) and per-(s,m) set-up and the
-// segment recurrence (A_seg <- A_seg Z every SEG subcarriers) of the likelihood kernel.
+// segment recurrence (A_seg <- A_seg Z every SEG subcarriers) of the likelihood kernel.  sfv_per_item: item i's wall
+// (s >= 1) is sfv[i] instead of sfv[s - 1] (the F4 belief averages over paired particles, slam_step.cu).
 template <typename RT>
 __global__ void response_kernel(const __grid_constant__ SceneDev sc, const double* __restrict__ pos,
                                 int64_t n, const int32_t* __restrict__ js, const double* __restrict__ sfv,
-                                double2* __restrict__ psi, int* flags) {
+                                double2* __restrict__ psi, int* flags, int sfv_per_item) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * sc.Na) return;
   const int64_t item = t / sc.Na;
@@ -23,7 +24,7 @@ __global__ void response_kernel(const __grid_constant__ SceneDev sc, const doubl
   PSField<RT> f;
   double R64;
   const int st = (j >= 0 && j < sc.J && s >= 0 && s < sc.S)
-                     ? setup_ps<RT>(sc, j, p, s ? sfv + 3 * (s - 1) : nullptr, f, R64)
+                     ? setup_ps<RT>(sc, j, p, s ? sfv + 3 * (sfv_per_item ? item : s - 1) : nullptr, f, R64)
                      : PS_BADSFV;
   if (st != PS_OK) {
     atomicOr(flags, st == PS_DEGENERATE ? FLAG_DEGENERATE : FLAG_NAN);
@@ -62,14 +63,14 @@ __global__ void response_kernel(const __grid_constant__ SceneDev sc, const doubl
 }
 
 cudaError_t launch_response(const SceneDev& sc, const double* pos, int64_t n, const int32_t* js, const double* sfv,
-                            double2* psi, int precision, int* flags, cudaStream_t st) {
+                            double2* psi, int precision, int* flags, cudaStream_t st, int sfv_per_item) {
   const int64_t threads = n * sc.Na;
   if (threads == 0) return cudaSuccess;
   const unsigned grid = (unsigned)((threads + 127) / 128);
   if (precision == CDMS_FP64)
-    response_kernel<double><<<grid, 128, 0, st>>>(sc, pos, n, js, sfv, psi, flags);
+    response_kernel<double><<<grid, 128, 0, st>>>(sc, pos, n, js, sfv, psi, flags, sfv_per_item);
   else
-    response_kernel<float><<<grid, 128, 0, st>>>(sc, pos, n, js, sfv, psi, flags);
+    response_kernel<float><<<grid, 128, 0, st>>>(sc, pos, n, js, sfv, psi, flags, sfv_per_item);
   return cudaGetLastError();
 }
 

@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   const double* pos = particles + p * pstride;
   double2* o = out + (p * J + j) * T;
   double va[3], sh[3];
-  if (!anchor_va(sc, j, phi + 3 * p, va, sh)) {
+  if (!anchor_va(sc, j, phi ? phi + 3 * p : nullptr, va, sh)) {  // phi == NULL: the LOS PF (sh = 0, H = I)
     atomicOr(&pflag[p], 2);
 #pragma unroll
     for (int t = 0; t < T; ++t) o[t] = make_double2(0.0, 0.0);

@@ -58,9 +58,11 @@ def _pf_inputs(orc, cfg, L, P, seed=5, wavefront="spherical"):
     return sc, o, y, np.full(J, eta), x, phi, walpha, mu, gamma, zeta, mu3, mcols
 
 
-@pytest.mark.parametrize("name,L,P", [("c2", 0, 300), ("c2", 3, 300), ("c3", 5, 120), ("c4", 3, 64)])
+@pytest.mark.parametrize("name,L,P,los", [("c2", 0, 300, False), ("c2", 3, 300, False), ("c3", 5, 120, False),
+                                           ("c4", 3, 64, False), ("c2", 3, 300, True), ("c3", 5, 120, True)])
 @pytest.mark.parametrize("wavefront", ["spherical", "planar_wb"])
-def test_pf_update_parity(cd, ctx, orc, name, L, P, wavefront):
+def test_pf_update_parity(cd, ctx, orc, name, L, P, los, wavefront):
+    """los: the LOS PF s = 0 (d_phi = NULL; the F4 driver's slot 0)."""
     import torch
     base = scenes.CONFIGS[name]
     cfg = small_cfg(J=base.J, K=max(base.K, L + 1), ny=base.ny, nv=base.nv, nf=base.nf, P=P, index=base.index)
@@ -68,15 +70,15 @@ def test_pf_update_parity(cd, ctx, orc, name, L, P, wavefront):
     scene = cd.Scene.from_synthetic(sc, wavefront=wavefront)
     dev = "cuda:0"
     t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
-    logr, w, out = cd.pf_update(ctx, scene, t(x), t(phi), t(wa), t(mu.astype(np.complex128)), t(gamma), zeta, eta,
-                                t(y), t(mu3), t(mcols) if L else None)
+    logr, w, out = cd.pf_update(ctx, scene, t(x), None if los else t(phi), t(wa), t(mu.astype(np.complex128)),
+                                t(gamma), zeta, eta, t(y), t(mu3), t(mcols) if L else None)
     ctx.sync()
-    st, lo, wo, logMo, exo = o.pf_update(x, phi, wa, mu, gamma, zeta, eta, y.astype(np.complex128),
+    st, lo, wo, logMo, exo = o.pf_update(x, None if los else phi, wa, mu, gamma, zeta, eta, y.astype(np.complex128),
                                          mu3.astype(np.complex128), mcols.astype(np.complex128))
     assert st == 0
     lg = logr.cpu().numpy()
     e = np.abs(lg - lo) / np.maximum(np.abs(lo), cfg.J * cfg.Nz)
-    record("pf_logr_rel", e.max(), 1e-4, config=name, L=L, wavefront=wavefront)
+    record("pf_logr_rel", e.max(), 1e-4, config=name, L=L, wavefront=wavefront, los=los)
     assert e.max() <= 1e-4, e.max()
     # the kernel's own normalization (S-IV) is consistent with its logr
     logM, ex = out.cpu().numpy()

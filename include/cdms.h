@@ -270,7 +270,7 @@ typedef struct {
   double box[6];            /* SFV birth box (lo[3], hi[3]) = [2 p_min, 2 p_max] */
   int64_t N_g;              /* birth-proposal candidates (F3) */
   int32_t P_m;              /* belief-average sample size (reading F4c) */
-  int32_t regularize;       /* MT regularization */
+  int32_t regularize;       /* MT and PF-SFV regularization */
   uint64_t key;             /* Philox key of every draw (stream map: DESIGN.md, reading F4i) */
   int32_t keep_debug;       /* 1: keep the step's intermediate messages for cdms_slam_get_view (parity tests) */
   int32_t pad_;
@@ -344,7 +344,8 @@ cdms_status cdms_slam_get_view(cdms_slam slam, cdms_slam_view* out);
  *  (iii) iota~ (cdms_loglik with the moment-matched priors and the paired SFVs), nu~ (cdms_noise_update), kappa~ and
  *       omega~ of every slot (cdms_pf_update, cdms_ppr_update) -- all from the prediction messages;
  *  beliefs: MT normalize / estimate / resample / regularize (cdms_bp_update), systematic resampling of the noise per PA
- *  and of every kept PF (weights -> existence / P), PPR zeta~ = sigma(u); MMSE estimates, declaration (exist > T_dec)
+ *  and of every kept PF (weights -> existence / P) with the SFV particles regularized like the MT's (P:L3447-3450,
+ *  d = 3, reading F4k), PPR zeta~ = sigma(u); MMSE estimates, declaration (exist > T_dec)
  *  and pruning (exist < T_pru, slots compacted in order).  h_report (host, may be NULL) gets the step's estimates.
  *  Synchronizes the context's stream four times. */
 cdms_status cdms_slam_step(cdms_slam slam, const void* d_y, cdms_slam_report* h_report);

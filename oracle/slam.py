@@ -7,7 +7,7 @@ Schedule: (i) prediction messages of every state from time n-1 --
 (survival + Gaussian / Gamma transitions), PPRs (survival / revival) -- and the birth message of one new PF (Q = 1,
 P:L3257-3346); (ii)-(iii) flooding: every update message from the same prediction messages -- iota~ (MT), nu~ (noise),
 kappa~ (each PF), omega~ (each PPR); then beliefs, systematic resampling, regularization of
-the MT belief, MMSE estimates, declaration and pruning.  The readings F4a-F4k of
+the MT belief and of the PFs' SFV particles, MMSE estimates, declaration and pruning.  The readings F4a-F4k of
 DESIGN.md section 3 fix what the paper leaves open; each is cited where it is used.
 
 Random numbers: counter-based Philox4x32-10 blocks (key; index, index >> 32, n, stream) -- the same counters as the
@@ -16,7 +16,8 @@ CUDA driver, which implements the same generator itself (no shared code):
   0x100 + 16 j + a: noise Gamma draw of PA j, attempt a;     0x200 + 16 i: SFV jitter normals of slot i;
   0x201 + 16 i: amplitude-mean jitter normals of slot i;       0x300 + 16 i + a: amplitude-variance Gamma of slot i;
   0x400 + i: resampling offset of slot i's PF;                  0x500 + j: resampling offset of PA j's noise;
-  0x600 / 0x601: birth SFV normals / birth amplitude uniforms; birth candidates: orc_birth_candidate, counter n.
+  0x600 / 0x601: birth SFV normals / birth amplitude uniforms; 0x700 + 16 i: SFV regularization normals of slot i;
+  birth candidates: orc_birth_candidate, counter n.
 """
 from __future__ import annotations
 
@@ -29,8 +30,8 @@ import numpy as np
 from oracle import oracle as O
 
 S_MAX = 9          # LOS + 8 PFs: the likelihood's component limit
-ST_NOISE, ST_SFV, ST_MU, ST_GAMMA, ST_PF_RES, ST_NOISE_RES, ST_BIRTH_N, ST_BIRTH_U = (
-    0x100, 0x200, 0x201, 0x300, 0x400, 0x500, 0x600, 0x601)
+ST_NOISE, ST_SFV, ST_MU, ST_GAMMA, ST_PF_RES, ST_NOISE_RES, ST_BIRTH_N, ST_BIRTH_U, ST_PF_REG = (
+    0x100, 0x200, 0x201, 0x300, 0x400, 0x500, 0x600, 0x601, 0x700)
 
 
 @dataclasses.dataclass
@@ -55,7 +56,7 @@ class Params:
     N_g: int = 4096                # birth-proposal candidates (F3)
     P_m: int = 256                 # belief-average sample size (reading F4c)
     key: int = 1234                # Philox key
-    regularize: bool = True        # MT regularization
+    regularize: bool = True        # MT and PF-SFV regularization
 
 
 @dataclasses.dataclass
@@ -215,6 +216,29 @@ def belief_vectors(orc, x, slots, P_m):
     return u, m, mw
 
 
+def regularize_sfv(phi_res, phi, w, phi_hat, prm: Params, n, s):
+    """Regularization of a resampled PF's SFV particles (reading F4k): phi += h chol(Sigma) z with
+    Sigma = sum_p w_p (phi_p - phi^)(phi_p - phi^)^T / sum w (the posterior belief's second central moment, before
+    resampling), h = (4 / ((d + 2) P))^{1/(d + 4)}, d = 3 (S:L451), z ~ N(0, I3) from normals4(key, n, p, 0x700 + 16 s);
+    Sigma + 1e-12 tr(Sigma) I, no move when that is not positive definite."""
+    if not prm.regularize:
+        return phi_res
+    P = phi.shape[0]
+    d = phi - phi_hat[None, :]
+    Sg = (w[:, None] * d).T @ d / np.sum(w)
+    Sg = Sg + 1e-12 * np.trace(Sg) * np.eye(3)
+    try:
+        L = np.linalg.cholesky(Sg)
+    except np.linalg.LinAlgError:
+        return phi_res
+    h = (4.0 / (5.0 * P)) ** (1.0 / 7.0)
+    out = phi_res.copy()
+    for p in range(P):
+        z = O.normals4(prm.key, n, p, ST_PF_REG + 16 * s)[:3]
+        out[p] += h * (L @ z)
+    return out
+
+
 def step(base, st: State, y, prm: Params):
     """One time step n = st.n; returns (new State, report dict of the intermediate messages)."""
     n = st.n
@@ -303,8 +327,8 @@ def step(base, st: State, y, prm: Params):
             continue
         if ex > 0.0:
             rc, a = O.resample(w, philox_u32(prm.key, 0, n, ST_PF_RES + s)[0])
-            post = Slot(None if sl.phi is None else sl.phi[a], sl.mu[a], sl.gamma[a], np.full(P, ex / P),
-                        zeta_post, sl.ident)
+            phi = None if sl.phi is None else regularize_sfv(sl.phi[a], sl.phi, w, phib, prm, n, s)
+            post = Slot(phi, sl.mu[a], sl.gamma[a], np.full(P, ex / P), zeta_post, sl.ident)
         new_slots.append(post)
         if phib is not None:
             phi_hat[sl.ident] = phib

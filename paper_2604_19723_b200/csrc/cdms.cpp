@@ -1995,6 +1995,12 @@ cdms_status cdms_slam_step(cdms_slam sl, const void* d_y, cdms_slam_report* rep)
       if ((st = cdms_resample(ctx, sl->wnew + (size_t)i * P, P, u, sl->anc))) return st;
       CUDA_TRY(ctx, launch_slam_pf_gather(i ? slot_phi(sl, i) : nullptr, slot_mu(sl, i), slot_gam(sl, i), sl->anc, P,
                                           sl->tphi, sl->tmu, sl->tgam, stm));
+      if (i && q.regularize) {  // SFV regularization (reading F4k): h for d = 3, the posterior's Sigma
+        const double h = pow(4.0 / (5.0 * (double)P), 1.0 / 7.0);
+        CUDA_TRY(ctx, launch_slam_sfv_reg(sl->wnew + (size_t)i * P, slot_phi(sl, i), sl->tphi, P, r.phi_hat[i], h,
+                                          sl->bout, q.key, n, i, stm));
+        ctx->launches += 2;
+      }
       if (i)
         CUDA_TRY(ctx, cudaMemcpyAsync(slot_phi(sl, d), sl->tphi, sizeof(double) * P * 3, cudaMemcpyDeviceToDevice,
                                       stm));

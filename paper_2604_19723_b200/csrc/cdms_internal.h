@@ -444,5 +444,7 @@ cudaError_t launch_slam_pf_gather(const double* phi, const double2* mu, const do
                                   int64_t P, double* tphi, double2* tmu, double* tgam, cudaStream_t st);
 cudaError_t launch_slam_fill(double* w, int64_t P, double v, cudaStream_t st);
 cudaError_t launch_slam_gather1(const double* src, const int64_t* anc, int64_t P, double* dst, cudaStream_t st);
+cudaError_t launch_slam_sfv_reg(const double* w, const double* phi_src, double* phi_dst, int64_t P, const double* mean,
+                                double h, double* L, uint64_t key, uint64_t n, int slot, cudaStream_t st);
 
 }  // namespace cdms

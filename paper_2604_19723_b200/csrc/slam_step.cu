@@ -6,7 +6,8 @@
 //
 // Random numbers: Philox4x32-10 blocks (key; index, index >> 32, n, stream) with the stream map of DESIGN.md section
 // 3 (F4-i): 0x100 + 16 j + a noise Gamma, 0x200 + 16 i SFV jitter, 0x201 + 16 i amplitude-mean jitter,
-// 0x300 + 16 i + a amplitude-variance Gamma, 0x600 / 0x601 birth normals / uniforms.
+// 0x300 + 16 i + a amplitude-variance Gamma, 0x600 / 0x601 birth normals / uniforms, 0x700 + 16 i SFV
+// regularization.
 #include <math.h>
 
 #include "cdms_internal.h"
@@ -399,6 +400,69 @@ cudaError_t launch_slam_fill(double* w, int64_t P, double v, cudaStream_t st) {
 }
 cudaError_t launch_slam_gather1(const double* src, const int64_t* anc, int64_t P, double* dst, cudaStream_t st) {
   slam_gather1_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(src, anc, P, dst);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------- SFV regularization (reading F4k)
+// Sigma = sum_p w_p (phi_p - m)(phi_p - m)^T / sum w (fixed order), then on thread 0 the Cholesky factor of
+// Sigma + 1e-12 tr(Sigma) I (L = 0 when not positive definite: no move); L [9] row-major lower
+__global__ void __launch_bounds__(SB) slam_cov3_kernel(const double* __restrict__ w, const double* __restrict__ phi,
+                                                       int64_t P, double m0, double m1, double m2,
+                                                       double* __restrict__ L) {
+  __shared__ double sh[SB];
+  double a[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int64_t p = threadIdx.x; p < P; p += SB) {
+    const double wp = w[p];
+    const double d0 = phi[3 * p] - m0, d1 = phi[3 * p + 1] - m1, d2 = phi[3 * p + 2] - m2;
+    a[0] += wp;
+    a[1] += wp * d0 * d0;
+    a[2] += wp * d1 * d0;
+    a[3] += wp * d1 * d1;
+    a[4] += wp * d2 * d0;
+    a[5] += wp * d2 * d1;
+    a[6] += wp * d2 * d2;
+  }
+  double r[7];
+  for (int c = 0; c < 7; ++c) r[c] = block_sum(a[c], sh);
+  if (threadIdx.x != 0) return;
+  double A[9];
+  const double iw = r[0] > 0.0 ? 1.0 / r[0] : 0.0;
+  A[0] = r[1] * iw; A[3] = A[1] = r[2] * iw; A[4] = r[3] * iw;
+  A[6] = A[2] = r[4] * iw; A[7] = A[5] = r[5] * iw; A[8] = r[6] * iw;
+  const double tr = A[0] + A[4] + A[8];
+  for (int c = 0; c < 3; ++c) A[4 * c] += 1e-12 * tr;
+  double Lq[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  bool ok = true;
+  for (int j = 0; j < 3 && ok; ++j) {
+    double d = A[4 * j];
+    for (int k = 0; k < j; ++k) d -= Lq[3 * j + k] * Lq[3 * j + k];
+    if (!(d > 0.0)) { ok = false; break; }
+    Lq[4 * j] = sqrt(d);
+    for (int i = j + 1; i < 3; ++i) {
+      double x = A[3 * i + j];
+      for (int k = 0; k < j; ++k) x -= Lq[3 * i + k] * Lq[3 * j + k];
+      Lq[3 * i + j] = x / Lq[4 * j];
+    }
+  }
+  for (int c = 0; c < 9; ++c) L[c] = ok ? Lq[c] : 0.0;
+}
+// phi_p += h L z_p, z_p: the first three of normals4(key, n, p, 0x700 + 16 slot)
+__global__ void slam_reg3_kernel(double* __restrict__ phi, int64_t P, const double* __restrict__ L, double h,
+                                 uint64_t key, uint64_t n, int slot) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  double z[4];
+  normals4_slam(key, n, (uint64_t)p, 0x700u + 16u * (uint32_t)slot, z);
+  for (int c = 0; c < 3; ++c) {
+    double a = 0.0;
+    for (int b = 0; b <= c; ++b) a += L[3 * c + b] * z[b];
+    phi[3 * p + c] += h * a;
+  }
+}
+cudaError_t launch_slam_sfv_reg(const double* w, const double* phi_src, double* phi_dst, int64_t P, const double* mean,
+                                double h, double* L, uint64_t key, uint64_t n, int slot, cudaStream_t st) {
+  slam_cov3_kernel<<<1, SB, 0, st>>>(w, phi_src, P, mean[0], mean[1], mean[2], L);
+  slam_reg3_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(phi_dst, P, L, h, key, n, slot);
   return cudaGetLastError();
 }
 

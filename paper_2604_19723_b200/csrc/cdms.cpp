@@ -60,8 +60,6 @@ struct cdms_ctx_s {
   bool timing = false;           // bracket the likelihood kernel with events
   bool nb_tensor = true;         // PLANAR_NB fp32 on the tensor cores (nbmma.cu); CDMS_NB_TENSOR=0 selects K1
   bool taylor = true;            // spherical / planar-WB fp32 correlation by K1T (taylor.cu); CDMS_TAYLOR=0 selects K1
-  int taylor_gram = 0;           // K1T's off-diagonal Gram: 0/2 tay_gram_kernel, 1 K1's Horner-free variant
-                                 // (CDMS_TAYLOR_GRAM=k1 / tay, A/B only)
   int step_fused = 0;           // 1: single-rank bp_step O(P) phases in one cooperative kernel (CDMS_STEP_FUSED=1,
                                  // A/B; measured not faster: c2 0.409 vs 0.403 ms, the grid barriers and block 0's
                                  // epilogues cost what the launches did)
@@ -507,11 +505,12 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   // particles go through K1 (correlation + Gram -> HBM terms) and K1b (assembly) in batches whose terms
   // buffer stays under TERMS_BUDGET bytes
   const int T = terms_width(sd.S);
-  const size_t per_particle = (size_t)sd.J * T * sizeof(double2);
+  const bool f32t = tay;  // K1T hands its terms over in complex64 (term_f2), K1 and the tensor-core path in complex128
+  const size_t per_particle = (size_t)sd.J * T * (f32t ? sizeof(float2) : sizeof(double2));
   int64_t PB = (int64_t)(TERMS_BUDGET / per_particle);
   PB = PB < TILE_P ? TILE_P : (PB / TILE_P) * TILE_P;
   if (PB > P) PB = P;
-  WS_TRY(ctx, WS_TERMS, (size_t)PB * sd.J * T, &terms);
+  WS_TRY(ctx, WS_TERMS, f32t ? ((size_t)PB * sd.J * T + 1) / 2 : (size_t)PB * sd.J * T, &terms);
   WS_TRY(ctx, WS_PFLAG, PB, &pflag);
   WS_TRY(ctx, WS_SCHED, 2, &sched);  // zeroed at allocation, reset by the last K1 CTA of every launch
   if ((PB + TILE_P - 1) / TILE_P * sd.J >= (int64_t)1 << 31) return fail(ctx, CDMS_EINVAL, "loglik: batch too large");
@@ -530,7 +529,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     a.flags = ctx->d_flags;
     a.n_tiles = (nb + TILE_P - 1) / TILE_P;
     a.n_groups = a.n_tiles * sd.J;
-    a.grid = tay ? corr_grid_gram_only(sd, a.n_tiles, ctx->num_sms) : corr_grid(sd, a.n_tiles, precision, ctx->num_sms);
+    a.grid = tay ? 1 : corr_grid(sd, a.n_tiles, precision, ctx->num_sms);  // K1T does not launch K1
     if (a.grid < 1) return fail(ctx, CDMS_ECUDA, "corr_kernel occupancy query failed");
     a.sched = sched;
     a.no_gram = no_gram ? 1 : 0;
@@ -569,18 +568,17 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       CUDA_TRY(ctx, launch_nb_corr(sd, nbp, na, ctx->num_sms, ctx->stream));
       ctx->launches += 1;
     } else if (tay) {
-      // c and G_ss from K1T; the off-diagonal Gram from tay_gram_kernel (thread per particle, all pairs), or with
-      // CDMS_TAYLOR_GRAM=k1 from K1's Horner-free variant, which writes every term (c as zeros) and so runs first.
-      // Measured (profiles/r01_k1t_gram_select.txt): since its pair loops unroll fully tay_gram wins at every S
-      // (c3, S = 7: 8.97 vs 12.45 ms per step; c5 shard, S = 9: 60.0 vs 73.6; c2: 0.40 vs 0.48)
-      const bool k1g = !no_gram && ctx->taylor_gram == 1;
-      if (k1g) CUDA_TRY(ctx, launch_corr_gram_only(sd, a, ctx->stream));
+      // c and G_ss from K1T; the off-diagonal Gram from tay_gram_kernel (thread per particle, all pairs).  Measured
+      // against K1's Horner-free Gram (profiles/r01_k1t_gram_select.txt; that A/B option was removed in round 2 when
+      // the K1T terms went to complex64): tay_gram wins at every S (c3: 8.97 vs 12.45 ms per step; c5 shard: 60.0 vs
+      // 73.6; c2: 0.40 vs 0.48)
+      float2* terms32 = reinterpret_cast<float2*>(terms);
       // locality order (sort.cu): the batch's positions (and per-particle SFVs) gathered in Morton order; the kernels
       // run on the sorted copy, the assembly writes each result back to its particle (bit-identical results)
       const double* bpart = a.particles;
       const double* bsfv = a.sfv;
       int bstride = pstride;
-      if (ctx->locality && !k1g && nb >= LOCALITY_MIN_P) {
+      if (ctx->locality && nb >= LOCALITY_MIN_P) {
         uint32_t* keys;
         int *idx, *permb;
         unsigned char* temp;
@@ -600,11 +598,11 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
         bsfv = sfv_pp ? ssfv : a.sfv;
         perm = permb;
       }
-      CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms, pflag,
+      CUDA_TRY(ctx, launch_tay_corr(sd, taytab, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms32, pflag,
                                     no_gram ? 1 : 0, tlanes, ctx->stream));
       COLL_TRY(mark(1));
-      if (!no_gram && !k1g)
-        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms, dn, ctx->stream));
+      if (!no_gram)
+        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms32, dn, ctx->stream));
       ctx->launches += no_gram ? 0 : 1;
     } else {
       CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
@@ -613,6 +611,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
     COLL_TRY(mark(2));
     AsmArgs s;
     s.terms = terms;
+    s.terms_f32 = f32t ? 1 : 0;
     s.pflag = pflag;
     s.ynorm2 = yn;
     s.logw_prior = d_logw ? d_logw + b0 : nullptr;
@@ -814,7 +813,6 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   if (const char* e = getenv("CDMS_TAY_LANES")) ctx->taylor_lanes = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_LOCALITY")) ctx->locality = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_GRAM_TAB")) ctx->gram_tab = atoi(e) ? 1 : 0;
-  if (const char* e = getenv("CDMS_TAYLOR_GRAM")) ctx->taylor_gram = strcmp(e, "k1") == 0 ? 1 : (strcmp(e, "tay") == 0 ? 2 : 0);
   if (cudaMalloc(&ctx->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_flags, 0, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {
     delete ctx;
@@ -917,19 +915,20 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
   int* i32;
   WS_TRY(ctx, WS_YTILES, (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP, &f4);
   {
+    NbPlan nbp{};  // the tensor-core path's per-PA B operand and scales (PLANAR_NB, FP32)
+    const bool nbt = ctx->nb_tensor && scene->precision == CDMS_FP32 && nb_tensor_plan(sd, &nbp);
+    const bool f32t = tay_engine(ctx, sd, scene->precision, nbt);  // the batch and terms sizes loglik_impl uses
     const int T = terms_width(sd.S);
-    const size_t per_particle = (size_t)sd.J * T * sizeof(double2);
+    const size_t per_particle = (size_t)sd.J * T * (f32t ? sizeof(float2) : sizeof(double2));
     int64_t PB = (int64_t)(TERMS_BUDGET / per_particle);
     PB = PB < TILE_P ? TILE_P : (PB / TILE_P) * TILE_P;
     if (PB > P_local) PB = P_local;
-    WS_TRY(ctx, WS_TERMS, (size_t)PB * sd.J * T, &d2);
+    WS_TRY(ctx, WS_TERMS, f32t ? ((size_t)PB * sd.J * T + 1) / 2 : (size_t)PB * sd.J * T, &d2);
     WS_TRY(ctx, WS_PFLAG, PB, &i32);
     unsigned int* sch;
     WS_TRY(ctx, WS_SCHED, 2, &sch);
     WS_TRY(ctx, WS_STEP_CNT, 4, &sch);
     WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &f4);
-    NbPlan nbp{};  // the tensor-core path's per-PA B operand and scales (PLANAR_NB, FP32)
-    const bool nbt = ctx->nb_tensor && scene->precision == CDMS_FP32 && nb_tensor_plan(sd, &nbp);
     if (nbt) {
       uint8_t* nbop;
       float* nbs;

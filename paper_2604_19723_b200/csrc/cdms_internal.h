@@ -71,7 +71,8 @@ struct CorrArgs {
 };
 // K1b (S x S assembly) for the same batch
 struct AsmArgs {
-  const double2* terms;
+  const void* terms;        // [J][T][P] (term_idx): float2 from K1T (FP32 spherical / planar WB), else double2
+  int terms_f32;
   int* pflag;
   const double* ynorm2;     // [J]
   const double* logw_prior; // [P] (batch) or NULL
@@ -158,6 +159,9 @@ __device__ __forceinline__ u64 fadd2(u64 a, u64 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+
+// K1T's terms hand-off in complex64: the fp64 sums rounded once (6e-8 relative, below K1T's own fp32 accumulation)
+__device__ __forceinline__ float2 term_f2(double re, double im) { return make_float2((float)re, (float)im); }
 
 // Philox4x32-10 (Salmon et al., SC'11): counter-based draws of the regularisation normals (step.cu) and the
 // birth-proposal candidates (birth.cu)
@@ -257,20 +261,18 @@ cudaError_t launch_regularize(double* x, int64_t P, int64_t p0, int64_t P_total,
 cudaError_t launch_fill_u64(uint64_t* dst, uint64_t v, int n, cudaStream_t st);
 
 // loglik.cu K1 Gram-only variant + taylor.cu K1T (spherical / planar-WB correlation from spectral Taylor tables)
-int64_t corr_grid_gram_only(const SceneDev& sc, int64_t n_tiles, int num_sms);  // 0 on error
-cudaError_t launch_corr_gram_only(const SceneDev& sc, const CorrArgs& a, cudaStream_t st);
 int tay_centres(int nf);
 size_t tay_table_bytes(const SceneDev& sc);
 bool tay_lanes(const SceneDev& sc, int64_t P);  // table layout / correlation kernel choice for P particles
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, int direct,
                             cudaStream_t st);
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
-                            const double* sfv, int sfv_pp, double2* terms, const float* dn, cudaStream_t st);
+                            const double* sfv, int sfv_pp, float2* terms, const float* dn, cudaStream_t st);
 // The scene's Dirichlet table for the Gram (taylor.cu dn_table_kernel): dn_table_floats(nf) floats, built per N_f
 size_t dn_table_floats(int nf);
 cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st);
 cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,
-                            int64_t P, int pstride, const double* sfv, int sfv_pp, double2* terms, int* pflag,
+                            int64_t P, int pstride, const double* sfv, int sfv_pp, float2* terms, int* pflag,
                             int gram_diag, int lanes, cudaStream_t st);
 
 // sort.cu: locality (Morton) processing order of a likelihood batch; perm[i] = particle index of processing slot i

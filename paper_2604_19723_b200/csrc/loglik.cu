@@ -283,8 +283,9 @@ namespace cdms {
 // one CTA: results do not depend on the schedule.  The last CTA to finish resets the counters.
 // TWO: compile-time sc.two_seg (the segment end either moves A1 in or multiplies by Z; two instantiations keep
 // both Horner loops free of the other's register pressure).
-// NOH: Gram-only variant for K1T (taylor.cu), which writes c afterwards: no phasors, no Horner steps (the y chunks
-// still stream so the per-warp TMA ring keeps its protocol).
+// NOH: Gram-only variant (no phasors, no Horner steps; the y chunks still stream so the per-warp TMA ring keeps its
+// protocol) -- it served the K1T A/B option CDMS_TAYLOR_GRAM=k1 (profiles/r01_k1t_gram_select.txt), removed in round
+// 2; no launcher instantiates it now.
 template <int S, typename RT, bool TWO, bool NOH = false>
 __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
     corr_kernel(const __grid_constant__ SceneDev sc, const CorrArgs a) {
@@ -670,7 +671,15 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
 //   amplitudes: m + V^1/2 L^-H x / eta (LMMSE).
 constexpr int ASM_T = 128;
 
-template <int S>
+template <bool F32>
+__device__ __forceinline__ double2 ld_term(const void* terms, int64_t i) {  // streaming load, read once
+  if (F32) {
+    const float2 v = __ldcs(static_cast<const float2*>(terms) + i);
+    return make_double2((double)v.x, (double)v.y);
+  }
+  return __ldcs(static_cast<const double2*>(terms) + i);
+}
+template <int S, bool F32>
 __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__ SceneDev sc, const AsmArgs a) {
   constexpr int NTRI = S * (S + 1) / 2;
   constexpr int T = S + NTRI;
@@ -684,9 +693,9 @@ __global__ void __launch_bounds__(ASM_T) assemble_kernel(const __grid_constant__
     const double eta = sc.eta[j];
     double2 c[S], k[NTRI];
 #pragma unroll
-    for (int s = 0; s < S; ++s) c[s] = __ldcs(&a.terms[term_idx(p, j, s, T, a.P)]);  // read once: streaming loads
+    for (int s = 0; s < S; ++s) c[s] = ld_term<F32>(a.terms, term_idx(p, j, s, T, a.P));
 #pragma unroll
-    for (int t = 0; t < NTRI; ++t) k[t] = __ldcs(&a.terms[term_idx(p, j, S + t, T, a.P)]);  // G_rc, r >= c
+    for (int t = 0; t < NTRI; ++t) k[t] = ld_term<F32>(a.terms, term_idx(p, j, S + t, T, a.P));  // G_rc, r >= c
     if (a.term_c != nullptr) {
 #pragma unroll
       for (int r = 0; r < S; ++r) a.term_c[(po * J + j) * S + r] = c[r];
@@ -849,32 +858,6 @@ static cudaError_t launch_corr_t(const SceneDev& sc, const CorrArgs& a, cudaStre
   return cudaGetLastError();
 }
 
-template <int S>
-static cudaError_t launch_corr_noh_t(const SceneDev& sc, const CorrArgs& a, cudaStream_t st) {
-  if (a.grid < 1 || a.n_groups < 1) return cudaSuccess;
-  corr_kernel<S, float, false, true><<<(unsigned)a.grid, NTHREADS, Plan<S, float>::total, st>>>(sc, a);
-  return cudaGetLastError();
-}
-int64_t corr_grid_gram_only(const SceneDev& sc, int64_t n_tiles, int num_sms) {
-  switch (sc.S) {
-#define CASE_S(n) \
-  case n: return grid_for_kernel(corr_kernel<n, float, false, true>, NTHREADS, Plan<n, float>::total, n_tiles * sc.J, \
-                                 num_sms);
-    CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
-#undef CASE_S
-    default: return 0;
-  }
-}
-cudaError_t launch_corr_gram_only(const SceneDev& sc, const CorrArgs& a, cudaStream_t st) {
-  switch (sc.S) {
-#define CASE_S(n) \
-  case n: return launch_corr_noh_t<n>(sc, a, st);
-    CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
-#undef CASE_S
-    default: return cudaErrorInvalidValue;
-  }
-}
-
 int64_t corr_grid(const SceneDev& sc, int64_t n_tiles, int precision, int num_sms) {
   switch (sc.S) {
 #define CASE_S(n) \
@@ -901,8 +884,11 @@ cudaError_t launch_assemble(const SceneDev& sc, const AsmArgs& a, cudaStream_t s
   if (a.P <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)((a.P + ASM_T - 1) / ASM_T);
   switch (sc.S) {
-#define CASE_S(n) \
-  case n: assemble_kernel<n><<<grid, ASM_T, 0, st>>>(sc, a); break;
+#define CASE_S(n)                                                \
+  case n:                                                        \
+    if (a.terms_f32) assemble_kernel<n, true><<<grid, ASM_T, 0, st>>>(sc, a); \
+    else assemble_kernel<n, false><<<grid, ASM_T, 0, st>>>(sc, a);           \
+    break;
     CASE_S(1) CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
 #undef CASE_S
     default: return cudaErrorInvalidValue;

@@ -219,7 +219,7 @@ __device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par,
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_corr_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
                     const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P, int pstride,
-                    const double* __restrict__ sfv, int sfv_pp, double2* __restrict__ terms, int* __restrict__ pflag,
+                    const double* __restrict__ sfv, int sfv_pp, float2* __restrict__ terms, int* __restrict__ pflag,
                     int gram_diag) {
   const int J = sc.J, S = sc.S, Na = sc.Na, T = S + S * (S + 1) / 2;
   const int64_t p = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
@@ -293,11 +293,11 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       acci += (double)pi;
     }
     const double gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
-    terms[term_idx(p, j, s, T, P)] = make_double2((accr * cb - acci * sb) * gn, (accr * sb + acci * cb) * gn);
+    terms[term_idx(p, j, s, T, P)] = term_f2((accr * cb - acci * sb) * gn, (accr * sb + acci * cb) * gn);
     const int grow = S + s * (s + 1) / 2;  // row s of the lower triangle of G
-    terms[term_idx(p, j, grow + s, T, P)] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);  // G_ss = g^2 N_z
+    terms[term_idx(p, j, grow + s, T, P)] = term_f2((double)sc.nf * (double)Na * gn * gn, 0.0);  // G_ss = g^2 N_z
     if (gram_diag)  // callers that use c only: no off-diagonal Gram
-      for (int c = 0; c < s; ++c) terms[term_idx(p, j, grow + c, T, P)] = make_double2(0.0, 0.0);
+      for (int c = 0; c < s; ++c) terms[term_idx(p, j, grow + c, T, P)] = term_f2(0.0, 0.0);
   }
   if (fl) atomicOr(&pflag[p], fl);
 }
@@ -310,7 +310,7 @@ template <int EPL>  // antennas per lane (ceil(N_a / LP)), 0: runtime loop
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_corr_lanes_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
                           const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P,
-                          int pstride, const double* __restrict__ sfv, int sfv_pp, double2* __restrict__ terms,
+                          int pstride, const double* __restrict__ sfv, int sfv_pp, float2* __restrict__ terms,
                           int* __restrict__ pflag, int gram_diag, int lg) {
   const int lane = threadIdx.x & 31;
   const int J = sc.J, S = sc.S, Na = sc.Na, T = S + S * (S + 1) / 2;
@@ -433,11 +433,11 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     const int64_t p = p0 + lane / S;
     const int s = lane % S;
     terms[term_idx(p, j, s, T, P)] =
-        make_double2(((double)cr * Ebr - (double)ci * Ebi) * gn, ((double)cr * Ebi + (double)ci * Ebr) * gn);
+        term_f2(((double)cr * Ebr - (double)ci * Ebi) * gn, ((double)cr * Ebi + (double)ci * Ebr) * gn);
     const int r0 = S + s * (s + 1) / 2;
-    terms[term_idx(p, j, r0 + s, T, P)] = make_double2((double)sc.nf * (double)Na * gn * gn, 0.0);
+    terms[term_idx(p, j, r0 + s, T, P)] = term_f2((double)sc.nf * (double)Na * gn * gn, 0.0);
     if (gram_diag)
-      for (int c = 0; c < s; ++c) terms[term_idx(p, j, r0 + c, T, P)] = make_double2(0.0, 0.0);
+      for (int c = 0; c < s; ++c) terms[term_idx(p, j, r0 + c, T, P)] = term_f2(0.0, 0.0);
   }
 }
 
@@ -530,7 +530,7 @@ cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st) {
 template <int S, int Q0, int Q1, bool FAST, bool TAB>
 __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* __restrict__ tmpl,
                                               const double* __restrict__ particles, int64_t P, int pstride,
-                                              const double* __restrict__ sfv, int sfv_pp, double2* __restrict__ terms,
+                                              const double* __restrict__ sfv, int sfv_pp, float2* __restrict__ terms,
                                               int lsplit, double2* gsum, const GramTab tb) {
   constexpr int NP = Q1 - Q0;  // this part's pairs; gsum [NP][TAY_BLOCK]
   // A = 2^lsplit adjacent lanes per particle, lane a takes antennas a, a + A, ... (A > 1 when P J threads alone would
@@ -665,7 +665,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
         if ((long long)rint(d) & 1) g2 = -g2;
       }
       const double vr = cs * acc.x - sn * acc.y, vi = cs * acc.y + sn * acc.x;
-      terms[term_idx(p, j, S + b * (b + 1) / 2 + a, T, P)] = make_double2(vr * g2, -vi * g2);
+      terms[term_idx(p, j, S + b * (b + 1) / 2 + a, T, P)] = term_f2(vr * g2, -vi * g2);
     }
   }
 }
@@ -686,7 +686,7 @@ template <int S, bool FAST, bool TAB>
 __global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? CDMS_GRAM_MINB : 1))  // S >= 7: 3 blocks (12 warps) per SM, <= 168 registers
     tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
                     const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
-                    int sfv_pp, double2* __restrict__ terms, int lsplit, const GramTab tb) {
+                    int sfv_pp, float2* __restrict__ terms, int lsplit, const GramTab tb) {
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>(), H = NP / NPART;
   extern __shared__ double2 gsum[];
   if constexpr (NPART == 1) {
@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? CDMS_GRAM_MINB : 1))  // 
 }
 template <int S, bool FAST, bool TAB>
 static cudaError_t launch_tay_gram_v(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
-                                     int pstride, const double* sfv, int sfv_pp, double2* terms, const GramTab& tb,
+                                     int pstride, const double* sfv, int sfv_pp, float2* terms, const GramTab& tb,
                                      cudaStream_t st) {
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>();
   const size_t smem = (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2);  // the larger part
@@ -728,7 +728,7 @@ static cudaError_t launch_tay_gram_v(const SceneDev& sc, const float4* tmpl, con
 #endif
 template <int S>
 static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
-                                     int pstride, const double* sfv, int sfv_pp, double2* terms, const float* dn,
+                                     int pstride, const double* sfv, int sfv_pp, float2* terms, const float* dn,
                                      cudaStream_t st) {
   const bool fast = CDMS_GRAM_FAST && sc.small_step >= 1;
   GramTab tb;
@@ -740,7 +740,7 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
   return launch_tay_gram_v<S, false, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
 }
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
-                            const double* sfv, int sfv_pp, double2* terms, const float* dn, cudaStream_t st) {
+                            const double* sfv, int sfv_pp, float2* terms, const float* dn, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
   switch (sc.S) {
     case 1: return cudaSuccess;
@@ -776,7 +776,7 @@ cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, in
   return cudaGetLastError();
 }
 cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,
-                            int64_t P, int pstride, const double* sfv, int sfv_pp, double2* terms, int* pflag,
+                            int64_t P, int pstride, const double* sfv, int sfv_pp, float2* terms, int* pflag,
                             int gram_diag, int lanes, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
   if (lanes) {

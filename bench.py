@@ -615,6 +615,104 @@ def run_pf(args):
     return res if rank == 0 else None
 
 
+SLAM_METRIC = "SLAM time steps x paired particles/s (F4)"
+SLAM_UNIT = "particle-steps/s"
+
+
+def run_slam(args):
+    """F4: time cdms_slam_step on an Experiment-1-shaped track (tools/slam_run.py's scene and start, a rough prior map:
+    the LOS and every wall as PFs, so every step runs all S slots' messages plus one birth).  The snapshots of the
+    W + K steps are synthesized before the timed region (device-resident); the state (P paired particles, > L2) is
+    the library's."""
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        raise SystemExit("--mode slam: the F4 driver is single-rank (DESIGN.md section 8e)")
+    from paper_2604_19723_b200 import cdms
+    dev = f"cuda:{local}"
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream(local)
+    cfg = scenes.CONFIGS[args.config]
+    P = args.particles if args.particles is not None else 1_000_000
+    sc = scenes.make_scene(cfg)
+    scene = cdms.Scene.from_synthetic(sc, wavefront=args.wavefront, precision=args.precision)
+    ctx = cdms.Context(local, stream)
+    J, S = cfg.J, cfg.S
+    T = 0.1
+    n_all = args.warmup + args.steps
+    js = np.array([(j, s) for j in range(J) for s in range(S)], dtype=np.int32)
+    rho = torch.as_tensor(sc.rho, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(cfg.seed)
+    ys, eta = [], None
+    for n in range(1, n_all + 1):
+        p = scenes.P_TRUE + scenes.V_TRUE * T * n
+        psi = cdms.response(ctx, scene, np.repeat(p[None], J * S, axis=0), js, sc.sfv).reshape(J, S, -1)
+        clean = torch.einsum("jsn,s->jn", psi, rho)
+        if eta is None:
+            eta = float((clean.abs() ** 2).sum().item()) / (scene.Nz * J) / 100.0
+        w = torch.complex(torch.randn(clean.shape, generator=gen, device=dev, dtype=torch.float64),
+                          torch.randn(clean.shape, generator=gen, device=dev, dtype=torch.float64)) / math.sqrt(2.0)
+        ys.append((clean + math.sqrt(eta) * w).to(torch.complex64).reshape(J, cfg.nf, cfg.Na).contiguous())
+    slam = cdms.Slam(ctx, scene, P, T=T, box=(-10.0, -5.0, -4.0, 12.0, 12.0, 6.0))
+    rng = np.random.default_rng(cfg.seed)
+    x0 = np.zeros((P, 6))
+    x0[:, :3] = scenes.P_TRUE + 0.1 * rng.standard_normal((P, 3))
+    x0[:, 3:] = scenes.V_TRUE + 0.1 * rng.standard_normal((P, 3))
+    slam.init(torch.as_tensor(x0, device=dev), torch.full((J, P), eta, dtype=torch.float64, device=dev))
+    v = slam.view()
+    for s_ in range(1, S):
+        v["phi"][s_].copy_(torch.as_tensor(sc.sfv[s_ - 1][None, :] + 0.05 * rng.standard_normal((P, 3))))
+    for s_ in range(S):
+        v["mu"][s_].fill_(complex(sc.rho[s_]))
+        v["gamma"][s_].fill_(0.01)
+        v["w"][s_].fill_(0.9 / P)
+    slam.set_slots(list(range(S)), np.full((S, J), 0.9), np.vstack([np.zeros(3), sc.sfv]), n=1, next_id=S)
+    for n in range(args.warmup):
+        slam.step(ys[n])
+    ctx.sync()
+    launches0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    feats = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(local)
+        ev0.record(stream)
+        for n in range(args.warmup, n_all):
+            r = slam.step(ys[n])
+            feats.append(r["n_feat"])
+        ev1.record(stream)
+        clk.mark()
+        torch.cuda.synchronize(local)
+    st = ctx.sync(raise_on_error=False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    last = r
+    err = float(np.linalg.norm(last["est"][1:4] - (scenes.P_TRUE + scenes.V_TRUE * T * n_all)))
+    # e2e: the same steps with each snapshot copied from pinned host memory inside the timed region
+    yh = [y.cpu().pin_memory() for y in ys[args.warmup:]]
+    yd = torch.empty_like(ys[0])
+    t0 = time.perf_counter()
+    for n in range(args.steps):
+        yd.copy_(yh[n], non_blocking=True)
+        slam.step(yd)
+    torch.cuda.synchronize(local)
+    ms_e2e = (time.perf_counter() - t0) * 1e3 / args.steps
+    res = {"metric": SLAM_METRIC, "value": P / (ms / 1e3), "unit": SLAM_UNIT, "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config} scene (J={J}, {cfg.ny}x{cfg.nv}, nf={cfg.nf}, K={cfg.K}), F4 step "
+                                  f"with {P} paired particles, LOS + {cfg.K} PF slots + one birth per step",
+                      "config": args.config, "mode": "slam", "P": P, "slots_per_step": sorted(set(feats)),
+                      "l2": "state > L2 (P paired particles over all slots)",
+                      "step": "transitions + birth (F3) + belief columns + iota~ + nu~ + kappa~/omega~ per slot + "
+                              "resampling + SFV regularization + estimates / pruning (4 host syncs)"},
+           "final_position_error_m": err,
+           "e2e": {"value": P / (ms_e2e / 1e3), "unit": SLAM_UNIT, "ms_per_step": ms_e2e,
+                   "h2d_bytes_per_step": int(ys[0].numel() * 8), "d2h_bytes_per_step": 0},
+           "clocks": clk.summary(), "gpu_launches": ctx.launch_count() - launches0, "sync_status": st}
+    slam.close()
+    ctx.close()
+    return res
+
+
 BIRTH_METRIC = "Bartlett birth-proposal candidate x PA correlations/s (F3)"
 BIRTH_UNIT = "candidate-PA evals/s"
 
@@ -836,8 +934,8 @@ def main():
     ap.add_argument("--ref-particles", type=int, default=0,
                     help="--impl reference: particles per oracle step (0: sized to ~--ref-step-s seconds per step)")
     ap.add_argument("--ref-step-s", type=float, default=2.0)
-    ap.add_argument("--mode", default="step", choices=["step", "birth", "pf"],
-                    help="step: the BP step (headline); birth: the F3 birth proposal")
+    ap.add_argument("--mode", default="step", choices=["step", "birth", "pf", "slam"],
+                    help="step: the BP step (headline); birth: the F3 birth proposal; pf: F1; slam: the F4 step")
     ap.add_argument("--candidates", type=int, default=1 << 20, help="birth mode: candidates N_g per GPU")
     ap.add_argument("--legacy", type=int, default=2, help="birth mode: legacy PFs L")
     args = ap.parse_args()
@@ -851,6 +949,8 @@ def main():
         res = run_birth_reference(args) if args.impl == "reference" else run_birth(args)
     elif args.mode == "pf":
         res = None if args.impl == "reference" else run_pf(args)
+    elif args.mode == "slam":
+        res = None if args.impl == "reference" else run_slam(args)
     else:
         res = run_reference(args) if args.impl == "reference" else run_cdms(args)
     if res is not None:

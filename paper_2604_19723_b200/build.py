@@ -13,7 +13,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libcdms.so")
 LIB_TIMING = os.path.join(HERE, "libcdms_timing.so")  # debug variant with -DCDMS_PHASE_TIMING
-SOURCES = ["loglik.cu", "taylor.cu", "nbmma.cu", "birth.cu", "response.cu", "beliefs.cu", "step.cu", "pf.cu", "slam.cu", "slam_step.cu", "sort.cu", "cdms.cpp"]
+SOURCES = ["loglik.cu", "taylor.cu", "nbmma.cu", "birth.cu", "response.cu", "beliefs.cu", "step.cu", "pf.cu", "slam.cu", "slam_step.cu", "lse.cu", "sort.cu", "cdms.cpp"]
 HEADERS = ["cdms_internal.h", "geometry.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

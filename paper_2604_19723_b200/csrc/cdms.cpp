@@ -87,7 +87,7 @@ enum Slot {
   WS_QALL, WS_LOGLIK, WS_W, WS_ANC, WS_STAGE, WS_L6, WS_ANC2, WS_TERMS, WS_PFLAG, WS_TMPL, WS_SCHED, WS_STEP_CNT, WS_NBOP, WS_NBSCALE,
   WS_BPOS, WS_BJS, WS_BSFV, WS_BPSI, WS_BDOTS, WS_BCOEF, WS_BZR, WS_BCAND, WS_BC, WS_BLL, WS_BPB,
   WS_BPART, WS_BPART6, WS_BSCR, WS_TAY, WS_GPART, WS_PLAN, WS_RANKS, WS_PF_SNAP, WS_PF_TAB, WS_PF_DOTS, WS_PF_FIXED,
-  WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_SL_STACK, WS_SL_DOTS, WS_SL_EIG, WS_SL_PAR, WS_LOC_KEYS, WS_LOC_IDX,
+  WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_LSE2, WS_SL_STACK, WS_SL_DOTS, WS_SL_EIG, WS_SL_PAR, WS_LOC_KEYS, WS_LOC_IDX,
   WS_LOC_TEMP, WS_LOC_POS, WS_LOC_SFV, WS_DN, WS_COUNT
 };
 constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
@@ -1217,6 +1217,8 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
   WS_TRY(ctx, WS_PF_FLAG, P, &pflag);
   WS_TRY(ctx, WS_PF_GAIN, (size_t)P * J, &gain2);
   WS_TRY(ctx, WS_PF_PAR, 2 * MAXJ, &dpar);
+  double* lse2;
+  WS_TRY(ctx, WS_LSE2, (size_t)3 * MAXJ * (lse_blocks(P) + 1), &lse2);
   WS_TRY(ctx, WS_YTILES, (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP, &yt);
   WS_TRY(ctx, WS_YNORM, MAXJ, &yn);
   WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &tmpl);
@@ -1233,8 +1235,8 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
   // (3) per particle: log kappa~(phi_p, 1) - log kappa~(., 0) summed over PAs + log w_alpha; M_y, existence, weights
   CUDA_TRY(ctx, launch_pf_finish(sd, T, cc, fixed, dpar, dpar + MAXJ, gain2, d_particles, pstride, d_phi, d_walpha,
                                  static_cast<const double2*>(d_mu), d_gamma, pflag, P, d_logr, d_w, d_out,
-                                 ctx->d_flags, ctx->stream));
-  ctx->launches += 10 + (d_w ? 1 : 0);
+                                 ctx->d_flags, lse2, ctx->stream));
+  ctx->launches += 12 + (d_w ? 1 : 0);
   return CDMS_OK;
 }
 
@@ -1258,12 +1260,14 @@ cdms_status cdms_noise_update(cdms_ctx ctx, const cdms_scene* scene, const doubl
   WS_TRY(ctx, WS_SL_STACK, (size_t)J * T * Nz, &stack);
   WS_TRY(ctx, WS_SL_DOTS, (size_t)J * T * T, &dots);
   WS_TRY(ctx, WS_SL_EIG, (size_t)J * slam_eig_width(), &eig);
+  double* lse2;
+  WS_TRY(ctx, WS_LSE2, (size_t)3 * MAXJ * (lse_blocks(P) + 1), &lse2);
   // e = z - mu_nu and the columns: their dot products (fp64), then per PA the eigen data of M^H M, per particle nu~
   CUDA_TRY(ctx, launch_vec_stack_dots(J, T, S, Nz, static_cast<const float2*>(d_y), static_cast<const float2*>(d_mu),
                                       static_cast<const float2*>(d_mcols), nullptr, nullptr, stack, dots, ctx->stream));
   CUDA_TRY(ctx, launch_noise_update(J, S, P, Nz, dots, eig, d_eta, d_wxi, d_logw, d_lognorm, d_w, ctx->d_flags,
-                                    ctx->stream));
-  ctx->launches += 5;
+                                    lse2, ctx->stream));
+  ctx->launches += 6;
   return CDMS_OK;
 }
 
@@ -1545,6 +1549,7 @@ struct cdms_slam_s {
   double *tphi = nullptr, *tgam = nullptr, *teta = nullptr, *lw = nullptr, *sfvpp = nullptr, *par = nullptr;
   double2* tmu = nullptr;
   int64_t* anc = nullptr;
+  double *wpart = nullptr, *lpart = nullptr;
   double *stats = nullptr, *bout = nullptr, *bnorm = nullptr, *est = nullptr, *lse = nullptr, *pfout = nullptr,
          *pprout = nullptr, *lnorm = nullptr, *wk = nullptr;
   double2 *au = nullptr, *am = nullptr, *aw = nullptr, *psi = nullptr;
@@ -1655,6 +1660,8 @@ cdms_status cdms_slam_create(cdms_ctx ctx, const cdms_scene* scene, const double
   A(slam_alloc(sl, &sl->par, (size_t)SLAM_PAR));
   A(slam_alloc(sl, &sl->anc, (size_t)P));
   A(slam_alloc(sl, &sl->stats, (size_t)4 * SLAM_MAXJOBS));
+  A(slam_alloc(sl, &sl->wpart, (size_t)4 * SLAM_MAXJOBS * slam_wsum_blocks(P)));
+  A(slam_alloc(sl, &sl->lpart, (size_t)3 * (lse_blocks(P) + 1)));
   A(slam_alloc(sl, &sl->bout, (size_t)16));
   A(slam_alloc(sl, &sl->bnorm, (size_t)4));
   A(slam_alloc(sl, &sl->est, (size_t)28));
@@ -1766,7 +1773,7 @@ cdms_status cdms_slam_init(cdms_slam sl, const double* d_x0, const double* d_eta
   // the LOS at n = 0 "the same way as new PFs": hyperprior amplitudes, weights p_B / P (reading F4j)
   const double pB = q.mu_b / (1.0 + q.mu_b);
   CUDA_TRY(ctx, launch_slam_birth(nullptr, nullptr, nullptr, q.mu_max, q.gamma_max, pB, nullptr, slot_mu(sl, 0),
-                                  slot_gam(sl, 0), sl->lw, nullptr, nullptr, sl->P, q.key, 0, ctx->stream));
+                                  slot_gam(sl, 0), sl->lw, nullptr, nullptr, sl->lpart, sl->P, q.key, 0, ctx->stream));
   CUDA_TRY(ctx, launch_slam_fill(slot_w(sl, 0), sl->P, pB / (double)sl->P, ctx->stream));
   sl->n_slots = 1;
   sl->ident[0] = 0;
@@ -1813,9 +1820,9 @@ cdms_status cdms_slam_step(cdms_slam sl, const void* d_y, cdms_slam_report* rep)
   const int j0 = jb.n;
   slot_jobs(sl, jb, 0, S, sl->w, false);
   double h[4 * SLAM_MAXJOBS];
-  CUDA_TRY(ctx, launch_slam_wsum(jb, sl->stats, stm));
+  CUDA_TRY(ctx, launch_slam_wsum(jb, sl->wpart, sl->stats, stm));
   CUDA_TRY(ctx, cudaMemcpyAsync(h, sl->stats, sizeof(double) * 4 * jb.n, cudaMemcpyDeviceToHost, stm));
-  ctx->launches += 1;
+  ctx->launches += 2;
   if ((st = cdms_sync(ctx))) return st;
   double x_hat[3], eta_bar[MAXJ], eps[SLS], mub[SLS][2], gab[SLS];
   for (int c = 0; c < 3; ++c) x_hat[c] = h[1 + c] / (double)P;
@@ -1848,14 +1855,15 @@ cdms_status cdms_slam_step(cdms_slam sl, const void* d_y, cdms_slam_report* rep)
       if (chol3(C, Lq)) {
         const double pB = q.mu_b / (1.0 + q.mu_b);
         CUDA_TRY(ctx, launch_slam_birth(bo, Lq, q.box, q.mu_max, q.gamma_max, pB, slot_phi(sl, S), slot_mu(sl, S),
-                                        slot_gam(sl, S), sl->lw, slot_w(sl, S), sl->bnorm, P, q.key, n, stm));
+                                        slot_gam(sl, S), sl->lw, slot_w(sl, S), sl->bnorm, sl->lpart, P, q.key, n,
+                                        stm));
         SlamWsumJobs jn{};
         slot_jobs(sl, jn, S, S + 1, sl->w, false);
-        CUDA_TRY(ctx, launch_slam_wsum(jn, sl->stats, stm));
+        CUDA_TRY(ctx, launch_slam_wsum(jn, sl->wpart, sl->stats, stm));
         double hb[4 * 3 + 1];
         CUDA_TRY(ctx, cudaMemcpyAsync(hb, sl->stats, sizeof(double) * 12, cudaMemcpyDeviceToHost, stm));
         CUDA_TRY(ctx, cudaMemcpyAsync(hb + 12, sl->bnorm, sizeof(double), cudaMemcpyDeviceToHost, stm));
-        ctx->launches += 3;
+        ctx->launches += 6;  // sample, 2 LSE levels, weights, 2 weighted-sum levels
         if ((st = cdms_sync(ctx))) return st;
         if (hb[12] > 0.0) {  // some particle inside the birth box
           for (int c = 0; c < 12; ++c) h[4 * j0 + 4 * 3 * S + c] = hb[c];
@@ -1958,14 +1966,14 @@ cdms_status cdms_slam_step(cdms_slam sl, const void* d_y, cdms_slam_report* rep)
   slot_jobs(sl, jp, 0, S, sl->wnew, true);
   for (int j = 0; j < J; ++j)
     jp.job[jp.n++] = SlamWsumJob{sl->weta + (size_t)j * P, sl->eta + (size_t)j * P, P, 1, 1};
-  CUDA_TRY(ctx, launch_slam_wsum(jp, sl->stats, stm));
+  CUDA_TRY(ctx, launch_slam_wsum(jp, sl->wpart, sl->stats, stm));
   double hs[4 * SLAM_MAXJOBS], pfo[SLS * 2], ppo[SLS * MAXJ * 3], est[28], lse;
   CUDA_TRY(ctx, cudaMemcpyAsync(hs, sl->stats, sizeof(double) * 4 * jp.n, cudaMemcpyDeviceToHost, stm));
   CUDA_TRY(ctx, cudaMemcpyAsync(pfo, sl->pfout, sizeof(double) * 2 * S, cudaMemcpyDeviceToHost, stm));
   CUDA_TRY(ctx, cudaMemcpyAsync(ppo, sl->pprout, sizeof(double) * 3 * MAXJ * S, cudaMemcpyDeviceToHost, stm));
   CUDA_TRY(ctx, cudaMemcpyAsync(est, sl->est, sizeof(est), cudaMemcpyDeviceToHost, stm));
   CUDA_TRY(ctx, cudaMemcpyAsync(&lse, sl->lse, sizeof(double), cudaMemcpyDeviceToHost, stm));
-  ctx->launches += 1;
+  ctx->launches += 2;
   if ((st = cdms_sync(ctx))) return st;
   // ---- estimates, declaration, pruning; resampling of the kept PFs and of the noise
   cdms_slam_report r{};
@@ -1997,8 +2005,8 @@ cdms_status cdms_slam_step(cdms_slam sl, const void* d_y, cdms_slam_report* rep)
       if (i && q.regularize) {  // SFV regularization (reading F4k): h for d = 3, the posterior's Sigma
         const double h = pow(4.0 / (5.0 * (double)P), 1.0 / 7.0);
         CUDA_TRY(ctx, launch_slam_sfv_reg(sl->wnew + (size_t)i * P, slot_phi(sl, i), sl->tphi, P, r.phi_hat[i], h,
-                                          sl->bout, q.key, n, i, stm));
-        ctx->launches += 2;
+                                          sl->bout, sl->wpart, q.key, n, i, stm));
+        ctx->launches += 3;
       }
       if (i)
         CUDA_TRY(ctx, cudaMemcpyAsync(slot_phi(sl, d), sl->tphi, sizeof(double) * P * 3, cudaMemcpyDeviceToDevice,

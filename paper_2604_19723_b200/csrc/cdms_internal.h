@@ -290,13 +290,19 @@ cudaError_t launch_pf_prep(int J, int T, int64_t Nz, const float2* y, const floa
 cudaError_t launch_pf_finish(const SceneDev& sc, int T, const double2* cc, const double2* fixed, const double* d_eta,
                              const double* d_zeta, double* gain2, const double* particles, int pstride,
                              const double* phi, const double* walpha, const double2* mu, const double* gamma,
-                             int* pflag, int64_t P, double* logr, double* w, double* out, int* flags, cudaStream_t st);
+                             int* pflag, int64_t P, double* logr, double* w, double* out, int* flags,
+                             double* lse_part, cudaStream_t st);
+// two-level deterministic log-sum-exp over R rows (lse.cu): out [R][3] = (max, sum e^{l - max}, sum of the companion
+// row a or 0); part: 3 R lse_blocks(P) doubles
+int lse_blocks(int64_t P);
+cudaError_t launch_lse_rows(const double* l, int64_t ld, int R, int64_t P, const double* a, int64_t lda, double* part,
+                            double* out, cudaStream_t st);
 cudaError_t launch_vec_stack_dots(int J, int T, int L, int64_t Nz, const float2* y, const float2* mu, const float2* cols,
                                   const float2* x1, const float2* x2, float2* stack, double2* dots, cudaStream_t st);
 // slam.cu: F4 update messages nu~ (noise) and omega~ (PPR)
 cudaError_t launch_noise_update(int J, int L, int64_t P, int64_t Nz, const double2* dots, double* eig, const double* eta,
                                 const double* wxi, double* logw, double* lognorm, double* w, int* flags,
-                                cudaStream_t st);
+                                double* lse_part, cudaStream_t st);
 cudaError_t launch_ppr_update(int J, int L, const double2* dots, const double* zeta, const double* eta, double* out,
                               int* flags, cudaStream_t st);
 int slam_eig_width();     // doubles per PA of the nu~ eigen data
@@ -429,8 +435,9 @@ cudaError_t launch_slam_pf_predict(double* phi, double2* mu, double* gam, double
                                    uint64_t n, cudaStream_t st);
 cudaError_t launch_slam_birth(const double* mu_q, const double* Lq, const double* box, double mu_max, double gamma_max,
                               double pB, double* phi, double2* mu, double* gam, double* lw, double* w, double* out,
-                              int64_t P, uint64_t key, uint64_t n, cudaStream_t st);
-cudaError_t launch_slam_wsum(const SlamWsumJobs& jobs, double* out, cudaStream_t st);
+                              double* lse_part, int64_t P, uint64_t key, uint64_t n, cudaStream_t st);
+int slam_wsum_blocks(int64_t P);  // part: 4 jobs slam_wsum_blocks(max P) doubles (cov: 7 slam_wsum_blocks(P))
+cudaError_t launch_slam_wsum(const SlamWsumJobs& jobs, double* part, double* out, cudaStream_t st);
 cudaError_t launch_slam_bv_wsum(const double* w, int64_t P, int64_t K, int S, double* wk, cudaStream_t st);
 cudaError_t launch_slam_bv_items(const double* x, const double* phi, int64_t P, int64_t K, int64_t k0, int B, int J,
                                  int S, double* pos, int32_t* js, double* sfv, cudaStream_t st);
@@ -447,6 +454,6 @@ cudaError_t launch_slam_pf_gather(const double* phi, const double2* mu, const do
 cudaError_t launch_slam_fill(double* w, int64_t P, double v, cudaStream_t st);
 cudaError_t launch_slam_gather1(const double* src, const int64_t* anc, int64_t P, double* dst, cudaStream_t st);
 cudaError_t launch_slam_sfv_reg(const double* w, const double* phi_src, double* phi_dst, int64_t P, const double* mean,
-                                double h, double* L, uint64_t key, uint64_t n, int slot, cudaStream_t st);
+                                double h, double* L, double* part, uint64_t key, uint64_t n, int slot, cudaStream_t st);
 
 }  // namespace cdms

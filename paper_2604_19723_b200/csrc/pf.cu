@@ -238,47 +238,17 @@ __global__ void pf_gain_kernel(const __grid_constant__ SceneDev sc, const double
   gain2[i] = g2;
 }
 
-// Single block, fixed order: M = max logr, S = sum e^{logr - M}, h0 = max(0, 1 - sum w_alpha);
-// out[0] = log M_y = log(S e^M + h0), out[1] = existence = S e^M / M_y (S-IV, eq. existenceProb)
-__global__ void __launch_bounds__(PF_BLOCK) pf_norm_kernel(const double* __restrict__ logr,
-                                                          const double* __restrict__ walpha, int64_t P,
-                                                          double* __restrict__ out, int* flags) {
-  __shared__ double sh[PF_BLOCK], sw[PF_BLOCK];
-  double m = -INFINITY, a = 0.0;
-  for (int64_t p = threadIdx.x; p < P; p += PF_BLOCK) {
-    m = fmax(m, logr[p]);
-    a += walpha[p];
-  }
-  sh[threadIdx.x] = m;
-  sw[threadIdx.x] = a;
-  __syncthreads();
-  for (int o = PF_BLOCK / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) {
-      sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
-      sw[threadIdx.x] += sw[threadIdx.x + o];
-    }
-    __syncthreads();
-  }
-  const double M = sh[0], sa = sw[0];
-  __syncthreads();
-  double s = 0.0;
-  if (M > -INFINITY)
-    for (int64_t p = threadIdx.x; p < P; p += PF_BLOCK) s += exp(logr[p] - M);
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = PF_BLOCK / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double h0 = fmax(0.0, 1.0 - sa);
-    double logM;
-    if (M > -INFINITY) logM = M + log(sh[0] + h0 * exp(-M));
-    else logM = log(h0);
-    if (!(logM > -INFINITY)) atomicOr(flags, FLAG_ZEROMASS);
-    out[0] = logM;
-    out[1] = M > -INFINITY ? exp(M + log(sh[0]) - logM) : 0.0;
-  }
+// M_y from the two-level LSE of logr (lse.cu: M = max logr, S = sum e^{logr - M}, A = sum w_alpha):
+// h0 = max(0, 1 - A); out[0] = log M_y = log(S e^M + h0), out[1] = existence = S e^M / M_y (S-IV, eq. existenceProb)
+__global__ void pf_norm_kernel(const double* __restrict__ lse, double* __restrict__ out, int* flags) {
+  const double M = lse[0], S = lse[1], sa = lse[2];
+  const double h0 = fmax(0.0, 1.0 - sa);
+  double logM;
+  if (M > -INFINITY) logM = M + log(S + h0 * exp(-M));
+  else logM = log(h0);
+  if (!(logM > -INFINITY)) atomicOr(flags, FLAG_ZEROMASS);
+  out[0] = logM;
+  out[1] = M > -INFINITY ? exp(M + log(S) - logM) : 0.0;
 }
 
 __global__ void pf_weights_kernel(const double* __restrict__ logr, int64_t P, const double* __restrict__ out,
@@ -338,12 +308,15 @@ int pf_max_snapshots() { return PF_MAXT; }
 cudaError_t launch_pf_finish(const SceneDev& sc, int T, const double2* cc, const double2* fixed, const double* d_eta,
                              const double* d_zeta, double* gain2, const double* particles, int pstride,
                              const double* phi, const double* walpha, const double2* mu, const double* gamma,
-                             int* pflag, int64_t P, double* logr, double* w, double* out, int* flags, cudaStream_t st) {
+                             int* pflag, int64_t P, double* logr, double* w, double* out, int* flags,
+                             double* lse_part, cudaStream_t st) {
   const int64_t n = P * sc.J;
   pf_gain_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, particles, P, pstride, phi, gain2);
   pf_asm_kernel<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(sc.J, T, (double)sc.nf * sc.Na, cc, fixed, d_eta, d_zeta,
                                                            gain2, walpha, mu, gamma, pflag, P, logr, flags);
-  pf_norm_kernel<<<1, PF_BLOCK, 0, st>>>(logr, walpha, P, out, flags);
+  cudaError_t e = launch_lse_rows(logr, P, 1, P, walpha, P, lse_part, lse_part + 3 * lse_blocks(P), st);
+  if (e != cudaSuccess) return e;
+  pf_norm_kernel<<<1, 1, 0, st>>>(lse_part + 3 * lse_blocks(P), out, flags);
   if (w) pf_weights_kernel<<<pf_grid(P, 256), 256, 0, st>>>(logr, P, out, w);
   return cudaGetLastError();
 }

@@ -20,7 +20,6 @@
 namespace cdms {
 
 constexpr int SL_MAXL = 9;   // feature columns (nu~: all S features, S <= 9)
-constexpr int SL_BLOCK = 256;
 
 // ---------------------------------------------------------------------------- nu~
 // One block per PA; thread 0 runs the Jacobi sweeps on the 2L x 2L real embedding in shared memory.
@@ -114,38 +113,18 @@ __global__ void noise_particle_kernel(int J, int L, int64_t P, double Nz, const 
 }
 
 // Per PA (one block, fixed order): lognorm[j] = log sum_p e^{logw}; w = e^{logw - lognorm}
-__global__ void __launch_bounds__(SL_BLOCK) noise_norm_kernel(int64_t P, const double* __restrict__ logw,
-                                                             double* __restrict__ lognorm, double* __restrict__ w,
-                                                             int* flags) {
-  __shared__ double sh[SL_BLOCK];
-  const int j = blockIdx.x;
-  const double* l = logw + (int64_t)j * P;
-  double m = -INFINITY;
-  for (int64_t p = threadIdx.x; p < P; p += SL_BLOCK) m = fmax(m, l[p]);
-  sh[threadIdx.x] = m;
-  __syncthreads();
-  for (int o = SL_BLOCK / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
-    __syncthreads();
-  }
-  const double M = sh[0];
-  __syncthreads();
-  double s = 0.0;
-  if (M > -INFINITY)
-    for (int64_t p = threadIdx.x; p < P; p += SL_BLOCK) s += exp(l[p] - M);
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = SL_BLOCK / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
-  }
-  const double ln = M + log(sh[0]);
-  if (threadIdx.x == 0) {
+// per PA: lognorm = M + ln S from the two-level LSE (lse.cu); w = e^{logw - lognorm} over every (PA, particle)
+__global__ void noise_norm_kernel(int J, int64_t P, const double* __restrict__ lse, const double* __restrict__ logw,
+                                  double* __restrict__ lognorm, double* __restrict__ w, int* flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)J * P) return;
+  const int j = (int)(i / P);
+  const double ln = lse[3 * j] + log(lse[3 * j + 1]);
+  if (i - (int64_t)j * P == 0) {
     lognorm[j] = ln;
     if (!(ln > -INFINITY)) atomicOr(flags, FLAG_ZEROMASS);
   }
-  if (w)
-    for (int64_t p = threadIdx.x; p < P; p += SL_BLOCK) w[(int64_t)j * P + p] = exp(l[p] - ln);
+  if (w) w[i] = exp(logw[i] - ln);
 }
 
 // ---------------------------------------------------------------------------- omega~
@@ -226,12 +205,15 @@ __global__ void ppr_kernel(int J, int L, const double2* __restrict__ dots, const
 
 cudaError_t launch_noise_update(int J, int L, int64_t P, int64_t Nz, const double2* dots, double* eig, const double* eta,
                                 const double* wxi, double* logw, double* lognorm, double* w, int* flags,
-                                cudaStream_t st) {
+                                double* lse_part, cudaStream_t st) {
   if (L < 0 || L > SL_MAXL) return cudaErrorInvalidValue;
   noise_eig_kernel<<<J, 32, 0, st>>>(L, L + 1, dots, eig);
   const int64_t n = (int64_t)J * P;
   noise_particle_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(J, L, P, (double)Nz, eig, eta, wxi, logw, flags);
-  noise_norm_kernel<<<J, SL_BLOCK, 0, st>>>(P, logw, lognorm, w, flags);
+  double* lse = lse_part + (int64_t)3 * J * lse_blocks(P);
+  cudaError_t e = launch_lse_rows(logw, P, J, P, nullptr, 0, lse_part, lse, st);
+  if (e != cudaSuccess) return e;
+  noise_norm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(J, P, lse, logw, lognorm, w, flags);
   return cudaGetLastError();
 }
 int slam_eig_width() { return 4 * SL_MAXL + 1; }

@@ -155,23 +155,19 @@ __global__ void slam_birth_sample_kernel(const BirthArgs a, double* __restrict__
   }
   lw[p] = in ? 0.5 * (z[0] * z[0] + z[1] * z[1] + z[2] * z[2]) : -INFINITY;
 }
-// single block: w_p = p_B e^{lw_p - max} / sum e^{lw - max} (fixed order); out[0] = sum (0: no particle in the box)
-__global__ void __launch_bounds__(SB) slam_birth_norm_kernel(const double* __restrict__ lw, int64_t P, double pB,
-                                                             double* __restrict__ w, double* __restrict__ out) {
-  __shared__ double sh[SB];
-  double mx = -INFINITY;
-  for (int64_t p = threadIdx.x; p < P; p += SB) mx = fmax(mx, lw[p]);
-  mx = block_max(mx, sh);
-  double s = 0.0;
-  if (mx > -INFINITY)
-    for (int64_t p = threadIdx.x; p < P; p += SB) s += exp(lw[p] - mx);
-  s = block_sum(s, sh);
-  for (int64_t p = threadIdx.x; p < P; p += SB) w[p] = s > 0.0 ? pB * exp(lw[p] - mx) / s : 0.0;
-  if (threadIdx.x == 0) out[0] = s;
+// w_p = p_B e^{lw_p - M} / S from the two-level LSE (lse.cu); out[0] = S (0: no particle in the box)
+__global__ void slam_birth_norm_kernel(const double* __restrict__ lw, int64_t P, double pB,
+                                       const double* __restrict__ lse, double* __restrict__ w,
+                                       double* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const double M = lse[0], S = lse[1];
+  w[p] = S > 0.0 ? pB * exp(lw[p] - M) / S : 0.0;
+  if (p == 0) out[0] = S;
 }
 cudaError_t launch_slam_birth(const double* mu_q, const double* Lq, const double* box, double mu_max, double gamma_max,
                               double pB, double* phi, double2* mu, double* gam, double* lw, double* w, double* out,
-                              int64_t P, uint64_t key, uint64_t n, cudaStream_t st) {
+                              double* lse_part, int64_t P, uint64_t key, uint64_t n, cudaStream_t st) {
   BirthArgs a{};
   for (int c = 0; c < 3; ++c) {
     a.mu[c] = mu_q ? mu_q[c] : 0.0;
@@ -182,31 +178,58 @@ cudaError_t launch_slam_birth(const double* mu_q, const double* Lq, const double
   a.mu_max = mu_max;
   a.gamma_max = gamma_max;
   slam_birth_sample_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(a, phi, mu, gam, lw, P, key, n);
-  if (phi) slam_birth_norm_kernel<<<1, SB, 0, st>>>(lw, P, pB, w, out);
+  if (phi) {
+    double* lse = lse_part + 3 * lse_blocks(P);
+    const cudaError_t e = launch_lse_rows(lw, P, 1, P, nullptr, 0, lse_part, lse, st);
+    if (e != cudaSuccess) return e;
+    slam_birth_norm_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(lw, P, pB, lse, w, out);
+  }
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------- weighted sums
-// One block per job: out[4 job] = sum_p w_p (w == NULL: P), out[4 job + 1 + c] = sum_p w_p v[p vs + c], c < nc <= 3;
-// fixed order (block-stride partial sums, then a tree), so repeated calls give identical bits.
-__global__ void __launch_bounds__(SB) slam_wsum_kernel(const __grid_constant__ SlamWsumJobs jobs,
-                                                       double* __restrict__ out) {
+// out[4 job] = sum_p w_p (w == NULL: P), out[4 job + 1 + c] = sum_p w_p v[p vs + c], c < nc <= 3.  Two levels with a
+// fixed grouping (NBW blocks per job over contiguous chunks, then one block per job over the chunks in order), so
+// repeated calls give identical bits.
+int slam_wsum_blocks(int64_t P) {
+  int64_t nb = (P + 8191) / 8192;
+  return (int)(nb < 1 ? 1 : (nb > 256 ? 256 : nb));
+}
+__global__ void __launch_bounds__(SB) slam_wsum_part_kernel(const __grid_constant__ SlamWsumJobs jobs, int NBW,
+                                                            double* __restrict__ part) {
   __shared__ double sh[SB];
-  const SlamWsumJob& jb = jobs.job[blockIdx.x];
+  const SlamWsumJob& jb = jobs.job[blockIdx.y];
+  const int64_t C = (jb.P + NBW - 1) / NBW;
+  const int64_t p0 = (int64_t)blockIdx.x * C, p1 = p0 + C < jb.P ? p0 + C : jb.P;
   double a[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t p = threadIdx.x; p < jb.P; p += SB) {
+  for (int64_t p = p0 + threadIdx.x; p < p1; p += SB) {
     const double w = jb.w ? jb.w[p] : 1.0;
     a[0] += w;
     for (int c = 0; c < jb.nc; ++c) a[1 + c] += w * jb.v[p * jb.vs + c];
   }
   for (int c = 0; c < 4; ++c) {
     const double r = block_sum(a[c], sh);
+    if (threadIdx.x == 0) part[((int64_t)blockIdx.y * NBW + blockIdx.x) * 4 + c] = r;
+  }
+}
+__global__ void __launch_bounds__(SB) slam_wsum_final_kernel(const double* __restrict__ part, int NBW,
+                                                             double* __restrict__ out) {
+  __shared__ double sh[SB];
+  const double* pj = part + (int64_t)blockIdx.x * NBW * 4;
+  for (int c = 0; c < 4; ++c) {
+    double a = 0.0;
+    for (int b = threadIdx.x; b < NBW; b += SB) a += pj[4 * b + c];
+    const double r = block_sum(a, sh);
     if (threadIdx.x == 0) out[4 * blockIdx.x + c] = r;
   }
 }
-cudaError_t launch_slam_wsum(const SlamWsumJobs& jobs, double* out, cudaStream_t st) {
+cudaError_t launch_slam_wsum(const SlamWsumJobs& jobs, double* part, double* out, cudaStream_t st) {
   if (jobs.n <= 0) return cudaSuccess;
-  slam_wsum_kernel<<<jobs.n, SB, 0, st>>>(jobs, out);
+  int64_t Pm = 1;
+  for (int i = 0; i < jobs.n; ++i) Pm = jobs.job[i].P > Pm ? jobs.job[i].P : Pm;
+  const int NBW = slam_wsum_blocks(Pm);
+  slam_wsum_part_kernel<<<dim3(NBW, jobs.n), SB, 0, st>>>(jobs, NBW, part);
+  slam_wsum_final_kernel<<<jobs.n, SB, 0, st>>>(part, NBW, out);
   return cudaGetLastError();
 }
 
@@ -404,14 +427,17 @@ cudaError_t launch_slam_gather1(const double* src, const int64_t* anc, int64_t P
 }
 
 // ---------------------------------------------------------------------------- SFV regularization (reading F4k)
-// Sigma = sum_p w_p (phi_p - m)(phi_p - m)^T / sum w (fixed order), then on thread 0 the Cholesky factor of
-// Sigma + 1e-12 tr(Sigma) I (L = 0 when not positive definite: no move); L [9] row-major lower
-__global__ void __launch_bounds__(SB) slam_cov3_kernel(const double* __restrict__ w, const double* __restrict__ phi,
-                                                       int64_t P, double m0, double m1, double m2,
-                                                       double* __restrict__ L) {
+// Sigma = sum_p w_p (phi_p - m)(phi_p - m)^T / sum w in two fixed-order levels (as the weighted sums), then on
+// thread 0 the Cholesky factor of Sigma + 1e-12 tr(Sigma) I (L = 0 when not positive definite: no move); L [9]
+// row-major lower
+__global__ void __launch_bounds__(SB) slam_cov3_part_kernel(const double* __restrict__ w, const double* __restrict__ phi,
+                                                            int64_t P, double m0, double m1, double m2, int NBW,
+                                                            double* __restrict__ part) {
   __shared__ double sh[SB];
+  const int64_t C = (P + NBW - 1) / NBW;
+  const int64_t p0 = (int64_t)blockIdx.x * C, p1 = p0 + C < P ? p0 + C : P;
   double a[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int64_t p = threadIdx.x; p < P; p += SB) {
+  for (int64_t p = p0 + threadIdx.x; p < p1; p += SB) {
     const double wp = w[p];
     const double d0 = phi[3 * p] - m0, d1 = phi[3 * p + 1] - m1, d2 = phi[3 * p + 2] - m2;
     a[0] += wp;
@@ -422,8 +448,20 @@ __global__ void __launch_bounds__(SB) slam_cov3_kernel(const double* __restrict_
     a[5] += wp * d2 * d1;
     a[6] += wp * d2 * d2;
   }
+  for (int c = 0; c < 7; ++c) {
+    const double r = block_sum(a[c], sh);
+    if (threadIdx.x == 0) part[7 * blockIdx.x + c] = r;
+  }
+}
+__global__ void __launch_bounds__(SB) slam_cov3_kernel(const double* __restrict__ part, int NBW,
+                                                       double* __restrict__ L) {
+  __shared__ double sh[SB];
   double r[7];
-  for (int c = 0; c < 7; ++c) r[c] = block_sum(a[c], sh);
+  for (int c = 0; c < 7; ++c) {
+    double a = 0.0;
+    for (int b = threadIdx.x; b < NBW; b += SB) a += part[7 * b + c];
+    r[c] = block_sum(a, sh);
+  }
   if (threadIdx.x != 0) return;
   double A[9];
   const double iw = r[0] > 0.0 ? 1.0 / r[0] : 0.0;
@@ -460,8 +498,10 @@ __global__ void slam_reg3_kernel(double* __restrict__ phi, int64_t P, const doub
   }
 }
 cudaError_t launch_slam_sfv_reg(const double* w, const double* phi_src, double* phi_dst, int64_t P, const double* mean,
-                                double h, double* L, uint64_t key, uint64_t n, int slot, cudaStream_t st) {
-  slam_cov3_kernel<<<1, SB, 0, st>>>(w, phi_src, P, mean[0], mean[1], mean[2], L);
+                                double h, double* L, double* part, uint64_t key, uint64_t n, int slot, cudaStream_t st) {
+  const int NBW = slam_wsum_blocks(P);
+  slam_cov3_part_kernel<<<NBW, SB, 0, st>>>(w, phi_src, P, mean[0], mean[1], mean[2], NBW, part);
+  slam_cov3_kernel<<<1, SB, 0, st>>>(part, NBW, L);
   slam_reg3_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(phi_dst, P, L, h, key, n, slot);
   return cudaGetLastError();
 }

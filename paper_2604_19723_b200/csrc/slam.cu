@@ -22,70 +22,81 @@ namespace cdms {
 constexpr int SL_MAXL = 9;   // feature columns (nu~: all S features, S <= 9)
 
 // ---------------------------------------------------------------------------- nu~
-// One block per PA; thread 0 runs the Jacobi sweeps on the 2L x 2L real embedding in shared memory.
+// One warp per PA: cyclic Jacobi on the 2L x 2L real embedding in shared memory; every lane computes the same rotation
+// (c, s) and lane k applies it to row / column element k (the serial order's arithmetic per element, so the result does
+// not depend on the lane count; round 1 ran the sweeps on one thread, 2 ms per call at L = 9).
 // out eig[j] = [lambda (2L), v (2L), |e|^2] (doubles).
-__global__ void noise_eig_kernel(int L, int T, const double2* __restrict__ dots, double* __restrict__ eig) {
+__global__ void __launch_bounds__(32) noise_eig_kernel(int L, int T, const double2* __restrict__ dots,
+                                                       double* __restrict__ eig) {
   __shared__ double A[2 * SL_MAXL][2 * SL_MAXL], Q[2 * SL_MAXL][2 * SL_MAXL];
-  const int j = blockIdx.x, n = 2 * L;
+  const int j = blockIdx.x, n = 2 * L, k = threadIdx.x;
   const double2* d = dots + (int64_t)j * T * T;
-  if (threadIdx.x != 0) return;
   auto D = [&](int a, int b) -> double2 {  // v_a^H v_b from the upper triangle
     if (a <= b) return d[a * T + b];
     const double2 x = d[b * T + a];
     return make_double2(x.x, -x.y);
   };
-  for (int a = 0; a < L; ++a)
+  auto wsum = [](double v) {  // butterfly: the same value on every lane
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  if (k < L)
     for (int b = 0; b < L; ++b) {
-      const double2 g = D(1 + a, 1 + b);  // G_ab = m_a^H m_b
-      A[a][b] = g.x;
-      A[L + a][L + b] = g.x;
-      A[L + a][b] = g.y;
-      A[a][L + b] = -g.y;
+      const double2 g = D(1 + k, 1 + b);  // G_kb = m_k^H m_b
+      A[k][b] = g.x;
+      A[L + k][L + b] = g.x;
+      A[L + k][b] = g.y;
+      A[k][L + b] = -g.y;
     }
-  for (int a = 0; a < n; ++a)
-    for (int b = 0; b < n; ++b) Q[a][b] = a == b ? 1.0 : 0.0;
-  double fro = 0.0;
-  for (int a = 0; a < n; ++a)
-    for (int b = 0; b < n; ++b) fro += A[a][b] * A[a][b];
+  if (k < n)
+    for (int b = 0; b < n; ++b) Q[k][b] = k == b ? 1.0 : 0.0;
+  __syncwarp();
+  double fr = 0.0;
+  if (k < n)
+    for (int b = 0; b < n; ++b) fr += A[k][b] * A[k][b];
+  const double fro = wsum(fr);
   for (int sweep = 0; sweep < 60; ++sweep) {
-    double off = 0.0;
-    for (int p = 0; p < n; ++p)
-      for (int q = p + 1; q < n; ++q) off += A[p][q] * A[p][q];
+    double of = 0.0;
+    if (k < n)
+      for (int q = k + 1; q < n; ++q) of += A[k][q] * A[k][q];
+    const double off = wsum(of);
     if (!(off > 1e-32 * fro)) break;
     for (int p = 0; p < n; ++p)
       for (int q = p + 1; q < n; ++q) {
-        if (A[p][q] == 0.0) continue;
-        const double th = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
+        const double apq = A[p][q];
+        if (apq == 0.0) continue;
+        const double th = (A[q][q] - A[p][p]) / (2.0 * apq);
         const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
         const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < n; ++k) {  // A <- A J (columns p, q)
+        __syncwarp();
+        if (k < n) {  // A <- A J (columns p, q)
           const double akp = A[k][p], akq = A[k][q];
           A[k][p] = c * akp - s * akq;
           A[k][q] = s * akp + c * akq;
         }
-        for (int k = 0; k < n; ++k) {  // A <- J^T A (rows p, q)
+        __syncwarp();
+        if (k < n) {  // A <- J^T A (rows p, q)
           const double apk = A[p][k], aqk = A[q][k];
           A[p][k] = c * apk - s * aqk;
           A[q][k] = s * apk + c * aqk;
-        }
-        for (int k = 0; k < n; ++k) {  // Q <- Q J
-          const double qkp = Q[k][p], qkq = Q[k][q];
+          const double qkp = Q[k][p], qkq = Q[k][q];  // Q <- Q J
           Q[k][p] = c * qkp - s * qkq;
           Q[k][q] = s * qkp + c * qkq;
         }
+        __syncwarp();
       }
   }
   double* o = eig + (int64_t)j * (4 * SL_MAXL + 1);
-  for (int i = 0; i < n; ++i) {
-    o[i] = fmax(A[i][i], 0.0);  // G is PSD; clamp rounding below zero
+  if (k < n) {
+    o[k] = fmax(A[k][k], 0.0);  // G is PSD; clamp rounding below zero
     double vi = 0.0;
     for (int a = 0; a < L; ++a) {
       const double2 w = D(1 + a, 0);  // w_a = m_a^H e
-      vi += Q[a][i] * w.x + Q[L + a][i] * w.y;
+      vi += Q[a][k] * w.x + Q[L + a][k] * w.y;
     }
-    o[n + i] = vi;
+    o[n + k] = vi;
   }
-  o[4 * SL_MAXL] = D(0, 0).x;  // |e|^2
+  if (k == 0) o[4 * SL_MAXL] = D(0, 0).x;  // |e|^2
 }
 
 // logw[j][p] = log w_xi + log nu~(eta_p) for every (PA, particle)

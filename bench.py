@@ -356,7 +356,8 @@ def roofline(args, cfg, P_local, kern_ms, launches_per_step, ms_per_step, clocks
             "achieved": None, "frac": None, "xu_frac": None, "traffic": None}
     rec = pipe_profile(args, cfg)
     # template instances are recorded with their full argument list (e.g. tay_gram_kernel<9, 1>: S, FAST path)
-    match = [n for n in (rec or {}).get("kernels", {}) if n == names[dom] or n.startswith(names[dom].rstrip(">") + ",")]
+    match = [n for n in (rec or {}).get("kernels", {})
+             if n == names[dom] or n.startswith(names[dom].rstrip(">") + ",") or n.startswith(names[dom] + "<")]
     if match:
         k = rec["kernels"][match[0]]
         roof["kernel"] = match[0]

@@ -65,7 +65,7 @@ struct cdms_ctx_s {
                                  // epilogues cost what the launches did)
   int taylor_prep_direct = 0;   // K1T tables by the direct sum even when G is a power of two (CDMS_TAY_PREP=direct,
                                  // A/B only; default FFT)
-  int gram_tab = 1;              // K1T Gram's D_N from the Taylor table (taylor.cu GramTab); CDMS_GRAM_TAB=0 for A/B
+  int gram_tab = 1;              // K1T Gram's D_N from the Taylor table (taylor.cu GramTab) at every S; CDMS_GRAM_TAB=0/2
   int dn_nf = -1;                // N_f the table in WS_DN was built for
   void* dn_ptr = nullptr;
   int locality = 0;              // 1: K1T batches in Morton processing order (sort.cu; CDMS_LOCALITY=1, A/B only).
@@ -482,12 +482,12 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
                                   ctx->stream));
     ctx->launches += 1;
   }
-  // the Gram's Dirichlet table (depends on N_f only: built once per context and N_f, taylor.cu dn_table_kernel), for
-  // S >= 7: measured (Gram ms, table vs sine quotient) c5 (S = 9, 4M) 56.3 vs 64.1, c3 (S = 7) 4.07 vs 4.27, but c2
-  // (S = 5) 0.147 vs 0.131 and c4 4.07 vs 3.98 -- at S <= 6 the unrolled pairs' in-flight 32-byte rows raise the
-  // registers (S = 5: 167 -> 244) and cost occupancy
+  // the Gram's Dirichlet table (depends on N_f only: built once per context and N_f, taylor.cu dn_table_kernel).
+  // Measured (Gram ms per step, profiles/r02_dn_table.txt): 16-byte rows (degree 3, even-symmetric) vs the sine
+  // quotient c5 (S = 9, 4M) 49.3 vs 64.1, c3 (S = 7) 3.37 vs 4.27, c4 (S = 5) 3.43 vs 3.98, c2 0.132 vs 0.132; round 2's
+  // first 32-byte rows (degree 7) had lost at S <= 6 (in-flight rows raised the registers) and were kept for S >= 7 only
   float* dn = nullptr;
-  if (tay && ctx->gram_tab && sd.small_step >= 1 && sd.S >= 7) {
+  if (tay && ctx->gram_tab && sd.small_step >= 1 && (sd.S >= 7 || ctx->gram_tab == 1)) {
     WS_TRY(ctx, WS_DN, dn_table_floats(sd.nf), &dn);
     if (ctx->dn_nf != sd.nf || ctx->dn_ptr != dn) {
       CUDA_TRY(ctx, launch_dn_table(sd.nf, dn, ctx->stream));
@@ -812,7 +812,7 @@ cdms_status cdms_create(cdms_ctx* out, int device, void* cuda_stream) {
   if (const char* e = getenv("CDMS_TAY_PREP")) ctx->taylor_prep_direct = strcmp(e, "direct") == 0 ? 1 : 0;
   if (const char* e = getenv("CDMS_TAY_LANES")) ctx->taylor_lanes = atoi(e) ? 1 : 0;
   if (const char* e = getenv("CDMS_LOCALITY")) ctx->locality = atoi(e) ? 1 : 0;
-  if (const char* e = getenv("CDMS_GRAM_TAB")) ctx->gram_tab = atoi(e) ? 1 : 0;
+  if (const char* e = getenv("CDMS_GRAM_TAB")) ctx->gram_tab = atoi(e);  // A/B: 0 off, 2 S >= 7 only
   if (cudaMalloc(&ctx->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_flags, 0, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {
     delete ctx;

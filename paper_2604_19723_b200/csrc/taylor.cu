@@ -484,19 +484,35 @@ __device__ __forceinline__ float dirichlet_fast(float x, float Nf) {
 // once (xb in registers, nb's sign at the end) and per antenna D = dirichlet_fast(xb + dd df/c): no per-antenna
 // range reduction or parity bookkeeping.  Else per antenna gram_dirichlet_f (reduction and parity per term).
 // TAB (FAST with the scene's Dirichlet table, dn_table_kernel): D_N from per-centre Taylor coefficients instead of the
-// sine quotient -- one 32-byte row (LDG.256) and a degree-7 Horner per (pair, antenna), no MUFU, no reciprocal, and
-// the function is entire, so near-equal delays need no special case.  Centres x_r = (r - R0)/G_D, G_D = 8 N, cover
-// |x| <= 0.6 (FAST: |x| <= 0.564); per pair the fp64 base x_b G_D = g_b + r_b (|r_b| <= 1/2), per antenna
-// d' = r_b + dd (df/c) G_D, its rounding g2 and the offset d = d' - g2 (|d| <= 1/2) -- all fp32-exact enough: the
-// truncation after degree 7 is below (pi N / (2 G_D))^8 / 8! = (pi/16)^8/8! = 5.5e-11 of N.
+// sine quotient -- one table row and a short Horner per (pair, antenna), no MUFU, no reciprocal, and the function is
+// entire, so near-equal delays need no special case.  Centres x_r = r / G_D; per pair the fp64 base x_b G_D = g_b + r_b
+// (|r_b| <= 1/2), per antenna d' = r_b + dd (df/c) G_D, its rounding g2 and the offset d = d' - g2 (|d| <= 1/2), all
+// fp32-exact enough.  The lookup is the L1 data pipe's work (one scattered row per (pair, antenna), ~13.5 wavefronts per
+// warp-level 32-byte load: the kernel's bound), so the row is kept at 16 bytes: degree 3 at G_D = 32 N (truncation
+// below N (pi N / (2 G_D))^4 / 4! = N (pi/64)^4/24 = 2.4e-7 N per term) and, D_N being even, rows for x >= 0 only
+// (D_N(-x) = D_N(x): row |g2|, offset sign(g2) d); |x| <= 0.6 (FAST: |x| <= 0.564).  Round 2's first table had degree 7
+// at 8 N over both signs (32-byte rows): -DCDMS_DN_DEG7 for A/B.
 struct GramTab {
-  const float4* dn;  // [rows][2] float4 = 8 real coefficients per centre
-  float G;           // centres per unit x (8 N)
+  const float4* dn;  // [rows][DN_L / 4] float4 of real coefficients per centre
+  float G;           // centres per unit x
   int R0;            // row of x = 0
 };
-constexpr int DN_L = 8;
-int dn_centres(int nf) { return 8 * nf; }
-int dn_rows(int nf) { return 2 * ((int)ceil(0.6 * dn_centres(nf))) + 1; }
+#ifdef CDMS_DN_DEG7
+constexpr int DN_L = 8, DN_DENS = 8;
+constexpr bool DN_SYM = false;
+#else
+#ifndef CDMS_DN_DENS
+#define CDMS_DN_DENS 32
+#endif
+constexpr int DN_L = 4, DN_DENS = CDMS_DN_DENS;
+constexpr bool DN_SYM = true;
+#endif
+int dn_centres(int nf) { return DN_DENS * nf; }
+int dn_rows(int nf) {
+  const int h = (int)ceil(0.6 * dn_centres(nf));
+  return DN_SYM ? h + 2 : 2 * h + 1;
+}
+int dn_r0(int nf) { return DN_SYM ? 0 : (dn_rows(nf) - 1) / 2; }
 // C_l(r) = D_N^{(l)}(x_r) / l! / G_D^l = sum_kappa cos(2 pi kappa x_r + l pi/2) (2 pi kappa / G_D)^l / l!, kappa = k - k0
 // (D_N(x) = sum_k e^{j2pi (k - k0) x} is real and even); fp64, exact integer reduction of 2 kappa (r - R0) mod 2 G_D.
 __global__ void dn_table_kernel(int N, int GD, int R0, int rows, float* __restrict__ out) {
@@ -521,7 +537,7 @@ __global__ void dn_table_kernel(int N, int GD, int R0, int rows, float* __restri
 }
 size_t dn_table_floats(int nf) { return (size_t)dn_rows(nf) * DN_L; }
 cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st) {
-  const int GD = dn_centres(nf), rows = dn_rows(nf), R0 = (rows - 1) / 2;
+  const int GD = dn_centres(nf), rows = dn_rows(nf), R0 = dn_r0(nf);
   const int n = rows * DN_L;
   dn_table_kernel<<<(n + 127) / 128, 128, 0, st>>>(nf, GD, R0, rows, out);
   return cudaGetLastError();
@@ -618,12 +634,22 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
             constexpr float M = 12582912.f;
             const float d1 = fmaf(dl[a] - dl[b], dfG, xb[q]);  // offset from the pair's base centre, in centres
             const float dm = d1 + M;
-            const float d = d1 - (dm - M);
-            const float4* row = tb.dn + 2 * (gb[q] + (__float_as_int(dm) - __float_as_int(M)));
-            float4 c03, c47;
-            ldg256(row, c03, c47);
-            D = fmaf(fmaf(fmaf(fmaf(fmaf(fmaf(fmaf(c47.w, d, c47.z), d, c47.y), d, c47.x), d, c03.w), d, c03.z), d,
-                          c03.y), d, c03.x);
+            float d = d1 - (dm - M);
+            int g2 = gb[q] + (__float_as_int(dm) - __float_as_int(M));
+            if (DN_SYM) {  // D_N even: the row of |x|, the offset mirrored (selects, no branch)
+              const bool neg = g2 < 0;
+              g2 = neg ? -g2 : g2;
+              d = neg ? -d : d;
+            }
+            if (DN_L == 4) {
+              const float4 c = __ldg(tb.dn + g2);
+              D = fmaf(fmaf(fmaf(c.w, d, c.z), d, c.y), d, c.x);
+            } else {
+              float4 c03, c47;
+              ldg256(tb.dn + 2 * g2, c03, c47);
+              D = fmaf(fmaf(fmaf(fmaf(fmaf(fmaf(fmaf(c47.w, d, c47.z), d, c47.y), d, c47.x), d, c03.w), d, c03.z), d,
+                            c03.y), d, c03.x);
+            }
           } else if (FAST) {
             D = dirichlet_fast(fmaf(dl[a] - dl[b], sc.df_cf, xb[q]), sc.nf_f);
           } else {
@@ -734,7 +760,7 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
   GramTab tb;
   tb.dn = reinterpret_cast<const float4*>(dn);
   tb.G = (float)dn_centres(sc.nf);
-  tb.R0 = (dn_rows(sc.nf) - 1) / 2;
+  tb.R0 = dn_r0(sc.nf);
   if (fast && dn) return launch_tay_gram_v<S, true, true>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
   if (fast) return launch_tay_gram_v<S, true, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
   return launch_tay_gram_v<S, false, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);

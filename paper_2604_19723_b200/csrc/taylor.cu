@@ -548,6 +548,9 @@ cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+#ifndef CDMS_GRAM_CHUNK
+#define CDMS_GRAM_CHUNK 16  // antennas per fp32 partial sum (measured 4 / 8 / 16: c5 4M Gram 49.1 / 46.8 / 45.5 ms, G parity 5.5e-7 of N_z at 16)
+#endif
 template <int S, int Q0, int Q1, bool FAST, bool TAB>
 __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* __restrict__ tmpl,
                                               const double* __restrict__ particles, int64_t P, int pstride,
@@ -607,11 +610,11 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
   const float4* tm = tmpl + (int64_t)j * sc.n_mb * NWARP;
   const int Nl = live ? (Na - a0 + A - 1) >> lsplit : 0;  // this lane's antennas m = a0 + A i, i < Nl
-  for (int i0 = 0; i0 < Nl; i0 += 8) {
+  for (int i0 = 0; i0 < Nl; i0 += CDMS_GRAM_CHUNK) {  // fp32 partial sums over a chunk, then fp64
     float gr[NP], gi[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) gr[q] = gi[q] = 0.f;
-    const int i1 = min(i0 + 8, Nl);
+    const int i1 = min(i0 + CDMS_GRAM_CHUNK, Nl);
     for (int i = i0; i < i1; ++i) {
       const int m = a0 + (i << lsplit);
       const float4 v = __ldg(&tm[m]);

@@ -205,3 +205,57 @@ def test_slam_init_and_multistep_runs(cd, ctx, orc):
         assert 1 <= r["n_slots"] <= r["n_feat"] <= 9
     ctx.sync()
     slam.close()
+
+
+def test_slam_full_slots_and_empty_box(cd, ctx, orc):
+    """Edge cases of the driver against the oracle: all 9 slots taken (no birth, P:L3257 Q = 1 needs a free slot) and a
+    snapshot without power (the proposal fails with no residual: no birth); the oracle's step makes the same
+    decisions."""
+    import torch
+    from oracle import slam as OS
+    cfg = small_cfg(J=1, K=8, ny=4, nv=4, nf=16, P=64, index=5)
+    sc = scenes.make_scene(cfg)
+    base = orc.Oracle.from_scene(sc)
+    y, eta = orc.measurement(base, sc, scenes.P_TRUE)
+    y64 = y.astype(np.complex64)
+    P = 128
+    # (a) 9 slots: LOS + 8 walls
+    prm = OS.Params(P_m=32, N_g=256)
+    st = _known_state(OS, cfg, sc, P, eta, weak=False)
+    assert len(st.slots) == 9
+    scene = cd.Scene.from_synthetic(sc, precision="fp64")
+    slam = cd.Slam(ctx, scene, P, P_m=prm.P_m, N_g=prm.N_g, key=prm.key, keep_debug=1)
+    _load(cd, slam, st, torch)
+    rep = slam.step(torch.as_tensor(y64, device="cuda:0"))
+    _, ref = OS.step(base, st, y64.astype(np.complex128), prm)
+    assert rep["n_feat"] == ref["n_slots"] == 9
+    assert rep["ident"] == [f["ident"] for f in ref["features"]]
+    slam.close()
+    # (b) a snapshot without power: the proposal has no residual to place a PF on (EZEROMASS), no birth
+    cfg2 = small_cfg(J=1, K=1, ny=4, nv=4, nf=16, P=64, index=5)
+    sc2 = scenes.make_scene(cfg2)
+    base2 = orc.Oracle.from_scene(sc2)
+    _, eta2 = orc.measurement(base2, sc2, scenes.P_TRUE)
+    y264 = np.zeros((cfg2.J, cfg2.nf, cfg2.Na), dtype=np.complex64)
+    prm2 = OS.Params(P_m=32, N_g=256)
+    st2 = _known_state(OS, cfg2, sc2, P, eta2, weak=False)
+    scene2 = cd.Scene.from_synthetic(sc2, precision="fp64")
+    slam2 = cd.Slam(ctx, scene2, P, P_m=prm2.P_m, N_g=prm2.N_g, key=prm2.key, keep_debug=1)
+    _load(cd, slam2, st2, torch)
+    rep2 = slam2.step(torch.as_tensor(y264, device="cuda:0"))
+    _, ref2 = OS.step(base2, st2, y264.astype(np.complex128), prm2)
+    assert rep2["n_feat"] == ref2["n_slots"] == len(st2.slots)
+    slam2.close()
+
+
+def test_slam_rejects_bad_arguments(cd, ctx):
+    cfg = small_cfg(J=1, K=1, ny=4, nv=4, nf=16, P=64, index=5)
+    scene = cd.Scene.from_synthetic(scenes.make_scene(cfg))
+    with pytest.raises(cd.CdmsError):
+        cd.Slam(ctx, scene, 0)
+    with pytest.raises(cd.CdmsError):
+        cd.Slam(ctx, scene, 64, c_eta=0.5)          # Marsaglia-Tsang needs c >= 1
+    slam = cd.Slam(ctx, scene, 64)
+    with pytest.raises(cd.CdmsError):
+        slam.set_slots([0], np.zeros((1, 1)), n=0)   # time index starts at 1
+    slam.close()

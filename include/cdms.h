@@ -318,6 +318,14 @@ typedef struct {
   double *loglik, *w_eta, *logr, *w_post;
   void *m_cols, *mu_nu, *u_sums, *m_sums, *mw_sums;
   double *pf_out, *ppr_out;
+  /* host side of the state (copies): the next time index, the next birth id, per slot the id, the PPR probabilities
+   * and the previous MMSE SFV -- with the device arrays above, everything a checkpoint needs (restore through
+   * cdms_slam_set_slots; the step is deterministic, so a restored state continues bit for bit) */
+  int64_t n;
+  int32_t next_id, pad2_;
+  int32_t ident[CDMS_SLAM_MAXS];
+  double zeta[CDMS_SLAM_MAXS][8];
+  double phi_hat[CDMS_SLAM_MAXS][3];
 } cdms_slam_view;
 
 /* Create a SLAM state of P paired particles (MT, noise per PA, every PF slot) on a single-rank context.  The scene's K

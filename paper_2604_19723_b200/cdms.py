@@ -65,7 +65,9 @@ class SlamViewC(C.Structure):
     _fields_ = [("P", C.c_int64), ("J", C.c_int32), ("n_slots", C.c_int32), ("n_feat", C.c_int32), ("pad_", C.c_int32)] + [
         (n, C.c_void_p) for n in ("x", "eta", "phi", "mu", "gamma", "w", "x_pred", "eta_pred", "phi_prior", "mu_prior",
                                   "gamma_prior", "w_prior", "loglik", "w_eta", "logr", "w_post", "m_cols", "mu_nu",
-                                  "u_sums", "m_sums", "mw_sums", "pf_out", "ppr_out")]
+                                  "u_sums", "m_sums", "mw_sums", "pf_out", "ppr_out")] + [
+        ("n", C.c_int64), ("next_id", C.c_int32), ("pad2_", C.c_int32), ("ident", C.c_int32 * SLAM_MAXS),
+        ("zeta", C.c_double * (8 * SLAM_MAXS)), ("phi_hat", C.c_double * (3 * SLAM_MAXS))]
 
 
 _lib = None
@@ -553,8 +555,10 @@ class Slam:
         P, J, S, Sf = v.P, v.J, SLAM_MAXS, max(1, v.n_feat)
         Nz = self.scene.Nz
         f8, c16, c8 = "<f8", "<c16", "<c8"
+        ns = v.n_slots
         return dict(
-            n_slots=v.n_slots, n_feat=v.n_feat,
+            n_slots=v.n_slots, n_feat=v.n_feat, n=v.n, next_id=v.next_id, ident=list(v.ident[:ns]),
+            zeta=np.array(v.zeta[:8 * ns]).reshape(ns, 8)[:, :v.J], phi_hat=np.array(v.phi_hat[:3 * ns]).reshape(ns, 3),
             x=_view(torch, v.x, (P, 6), f8), eta=_view(torch, v.eta, (J, P), f8),
             phi=_view(torch, v.phi, (S, P, 3), f8), mu=_view(torch, v.mu, (S, P), c16),
             gamma=_view(torch, v.gamma, (S, P), f8), w=_view(torch, v.w, (S, P), f8),
@@ -567,6 +571,20 @@ class Slam:
             u_sums=_view(torch, v.u_sums, (J, Sf, Nz), c16), m_sums=_view(torch, v.m_sums, (J, Sf, Nz), c16),
             mw_sums=_view(torch, v.mw_sums, (J, Sf, Nz), c16), pf_out=_view(torch, v.pf_out, (S, 2), f8),
             ppr_out=_view(torch, v.ppr_out, (S, 8, 3), f8))
+
+    def checkpoint(self) -> dict:
+        """Host copy of the whole state (device arrays + the host side); restore() continues bit for bit."""
+        v = self.view()
+        keys = ("x", "eta", "phi", "mu", "gamma", "w")
+        ck = {k: v[k].clone() for k in keys}
+        ck.update({k: v[k] for k in ("n", "next_id", "ident", "zeta", "phi_hat")})
+        return ck
+
+    def restore(self, ck: dict):
+        v = self.view()
+        for k in ("x", "eta", "phi", "mu", "gamma", "w"):
+            v[k].copy_(ck[k])
+        self.set_slots(ck["ident"], ck["zeta"], ck["phi_hat"], n=ck["n"], next_id=ck["next_id"])
 
     def step(self, y) -> dict:
         """One time step on y (complex64 cuda [J][nf][Na]); returns the step's report as numpy arrays."""

@@ -1742,6 +1742,13 @@ cdms_status cdms_slam_get_view(cdms_slam sl, cdms_slam_view* v) {
   v->mw_sums = sl->aw;
   v->pf_out = sl->pfout;
   v->ppr_out = sl->pprout;
+  v->n = sl->n;
+  v->next_id = sl->next_id;
+  for (int i = 0; i < SLS; ++i) {
+    v->ident[i] = sl->ident[i];
+    for (int j = 0; j < MAXJ; ++j) v->zeta[i][j] = sl->zeta[i][j];
+    for (int c = 0; c < 3; ++c) v->phi_hat[i][c] = sl->phi_hat[i][c];
+  }
   return CDMS_OK;
 }
 

@@ -355,7 +355,8 @@ cdms_status cdms_slam_get_view(cdms_slam slam, cdms_slam_view* out);
  *  and of every kept PF (weights -> existence / P) with the SFV particles regularized like the MT's (P:L3447-3450,
  *  d = 3, reading F4k), PPR zeta~ = sigma(u); MMSE estimates, declaration (exist > T_dec)
  *  and pruning (exist < T_pru, slots compacted in order).  h_report (host, may be NULL) gets the step's estimates.
- *  Synchronizes the context's stream four times. */
+ *  Synchronizes the context's stream four times.  On an error return the state is undefined (restore a checkpoint:
+ *  cdms_slam_get_view + cdms_slam_set_slots). */
 cdms_status cdms_slam_step(cdms_slam slam, const void* d_y, cdms_slam_report* h_report);
 
 /* ---- row A6: weight normalization ------------------------------------------------------------ */

@@ -368,6 +368,15 @@ def roofline(args, cfg, P_local, kern_ms, launches_per_step, ms_per_step, clocks
                      "traffic": k.get("dram_bytes_per_particle", 0) * P_local / launches_per_step or None,
                      "traffic_basis": "dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)",
                      "inst_source": rec["source"]})
+    try:  # the pipe that actually limits the kernel (committed ncu --set full summary of this config)
+        with open(os.path.join(ROOT, "profiles", "limiters.json")) as f:
+            lim = json.load(f)
+        k = lim.get(f"{args.config}_{args.wavefront}_{args.precision}", {}).get(roof["kernel"])
+        if k:
+            roof["limiter"] = {"pipe": "L1 data pipe (LSU wavefronts)", "pct_of_peak": k["lsu_wavefronts_pct_of_peak"],
+                               "issue_pct_of_peak": k["issue_pct_of_peak"], "source": lim["source"]}
+    except Exception:
+        pass
     return roof
 
 

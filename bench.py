@@ -720,6 +720,25 @@ def run_slam(args):
            "clocks": clk.summary(), "gpu_launches": ctx.launch_count() - launches0, "sync_status": st}
     slam.close()
     ctx.close()
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O
+        from oracle import slam as OS
+        O.build()
+        base = O.Oracle.from_scene(sc, wavefront=args.wavefront)
+        prm = OS.Params(T=T, box=(-10.0, -5.0, -4.0, 12.0, 12.0, 6.0))
+        n = 64
+        while True:
+            xs = x0[:n].copy()
+            st0 = OS.State(xs, np.full((J, n), eta), [OS.init_los(n, J, prm)])
+            t0 = time.perf_counter()
+            OS.step(base, st0, ys[0].cpu().numpy().astype(np.complex128), prm)
+            dt = time.perf_counter() - t0
+            if dt > args.cpu_seconds / 3 or n >= 4096:
+                break
+            n *= 4
+        res["cpu_baseline"] = {"value": n / dt, "unit": SLAM_UNIT, "cores": 1, "kind": "oracle",
+                               "sample": f"oracle/slam.py step from the LOS alone with {n} paired particles "
+                                         f"({args.config}), {dt:.2f} s"}
     return res
 
 

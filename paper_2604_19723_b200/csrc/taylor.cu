@@ -555,7 +555,7 @@ template <int S, int Q0, int Q1, bool FAST, bool TAB>
 __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* __restrict__ tmpl,
                                               const double* __restrict__ particles, int64_t P, int pstride,
                                               const double* __restrict__ sfv, int sfv_pp, float2* __restrict__ terms,
-                                              int lsplit, double2* gsum, const GramTab tb) {
+                                              int lsplit, double2* gsum, double* rsh, const GramTab tb) {
   constexpr int NP = Q1 - Q0;  // this part's pairs; gsum [NP][TAY_BLOCK]
   // A = 2^lsplit adjacent lanes per particle, lane a takes antennas a, a + A, ... (A > 1 when P J threads alone would
   // leave the SMs latency-bound); no early exit: the group's fp64 totals are combined by shuffles below
@@ -567,7 +567,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
   const int J = sc.J, Na = sc.Na, T = S + S * (S + 1) / 2;
   bool live = p < P;
   const double* pos = particles + (live ? p : 0) * pstride;
-  float hx[S], hy[S], hz[S], Rf[S], iR[S], uh[S], ul[S];
+  float hx[S], hy[S], hz[S], Rf[S], uh[S], ul[S];
   double R64[S];
   int npar[S];
 #pragma unroll
@@ -576,7 +576,6 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
     if (!tay_component(sc, j, pos, sfv_s, hx[s], hy[s], hz[s], R64[s])) live = false;  // flagged by K1T
     if (!live) R64[s] = 1.0;
     Rf[s] = (float)R64[s];
-    iR[s] = 1.f / Rf[s];
     if (!FAST) {
       const double xs = R64[s] * sc.df_c, ns = rint(xs), us = xs - ns;
       uh[s] = (float)us;
@@ -604,6 +603,10 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
         }
       }
   }
+  // R_s (fp64) are needed again only in the epilogue: parked in shared memory, not in registers through the loop
+  // (18 registers at S = 9, which removed the kernel's spills under its 168-register cap)
+#pragma unroll
+  for (int s = 0; s < S; ++s) rsh[s * TAY_BLOCK + threadIdx.x] = R64[s];
   const float dfG = sc.df_cf * tb.G;  // TAB: d' per unit of the element offset difference
 #pragma unroll
   for (int q = 0; q < NP; ++q) gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(0.0, 0.0);
@@ -626,7 +629,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
           const float n = v.w - 2.f * rq;
           dl[s] = Num<float>::fdiv_(n, Num<float>::fsqrt_(Rf[s] * Rf[s] + n) + Rf[s]);
         } else {
-          dl[s] = -rq * iR[s];
+          dl[s] = Num<float>::fdiv_(-rq, Rf[s]);  // planar WB only: no 1/R array held through the loop
         }
         cis2pi_fast<float>(dl[s] * sc.fc_cf, er[s], ei[s]);  // e^{j2pi f_c Delta_s/c}: the pairs' carriers as products
       }
@@ -692,10 +695,11 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
       }
       if (!live || a0 != 0) continue;
       double sn, cs;
-      sincospi(2.0 * frac_c((R64[a] - R64[b]) * sc.fc_c), &sn, &cs);
-      double g2 = sc.pathloss ? (sc.lambda / (4.0 * PI * R64[a])) * (sc.lambda / (4.0 * PI * R64[b])) : 1.0;
+      const double Ra = rsh[a * TAY_BLOCK + threadIdx.x], Rb = rsh[b * TAY_BLOCK + threadIdx.x];
+      sincospi(2.0 * frac_c((Ra - Rb) * sc.fc_c), &sn, &cs);
+      double g2 = sc.pathloss ? (sc.lambda / (4.0 * PI * Ra)) * (sc.lambda / (4.0 * PI * Rb)) : 1.0;
       if (FAST && ((sc.nf - 1) & 1)) {  // D_N(nb + x) = (-1)^{nb (N - 1)} D_N(x) (C-amb-13)
-        const double d = (R64[a] - R64[b]) * sc.df_c;
+        const double d = (Ra - Rb) * sc.df_c;
         if ((long long)rint(d) & 1) g2 = -g2;
       }
       const double vr = cs * acc.x - sn * acc.y, vi = cs * acc.y + sn * acc.x;
@@ -722,22 +726,24 @@ __global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? CDMS_GRAM_MINB : 1))  // 
                     const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
                     int sfv_pp, float2* __restrict__ terms, int lsplit, const GramTab tb) {
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>(), H = NP / NPART;
-  extern __shared__ double2 gsum[];
+  extern __shared__ double2 smem_g[];
+  double* rsh = reinterpret_cast<double*>(smem_g);  // [S][TAY_BLOCK] R_s, then the pair totals
+  double2* gsum = smem_g + (S * TAY_BLOCK + 1) / 2;
   if constexpr (NPART == 1) {
-    tay_gram_part<S, 0, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
+    tay_gram_part<S, 0, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
   } else if constexpr (NPART == 2) {
     if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
+      tay_gram_part<S, 0, H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
     else
-      tay_gram_part<S, H, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
+      tay_gram_part<S, H, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
   } else {
     static_assert(NPART == 3, "");
     if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
+      tay_gram_part<S, 0, H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
     else if (blockIdx.z == 1)
-      tay_gram_part<S, H, 2 * H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
+      tay_gram_part<S, H, 2 * H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
     else
-      tay_gram_part<S, 2 * H, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, tb);
+      tay_gram_part<S, 2 * H, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
   }
 }
 template <int S, bool FAST, bool TAB>
@@ -745,7 +751,8 @@ static cudaError_t launch_tay_gram_v(const SceneDev& sc, const float4* tmpl, con
                                      int pstride, const double* sfv, int sfv_pp, float2* terms, const GramTab& tb,
                                      cudaStream_t st) {
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>();
-  const size_t smem = (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2);  // the larger part
+  const size_t smem = (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2) +  // the larger part
+                      (size_t)(S * TAY_BLOCK + 1) / 2 * sizeof(double2);                       // + R_s
   cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S, FAST, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;

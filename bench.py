@@ -373,8 +373,8 @@ def roofline(args, cfg, P_local, kern_ms, launches_per_step, ms_per_step, clocks
             lim = json.load(f)
         k = lim.get(f"{args.config}_{args.wavefront}_{args.precision}", {}).get(roof["kernel"])
         if k:
-            roof["limiter"] = {"pipe": "L1 data pipe (LSU wavefronts)", "pct_of_peak": k["lsu_wavefronts_pct_of_peak"],
-                               "issue_pct_of_peak": k["issue_pct_of_peak"], "source": lim["source"]}
+            roof["limiter"] = {"pipe": k["pipe"], "pct_of_peak": k["pct_of_peak"], "fma_cycles_pct": k["fma_cycles_pct"],
+                               "lsu_wavefronts_pct_of_peak": k["lsu_wavefronts_pct_of_peak"], "source": lim["source"]}
     except Exception:
         pass
     return roof

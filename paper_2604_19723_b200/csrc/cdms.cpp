@@ -69,10 +69,11 @@ struct cdms_ctx_s {
   int dn_nf = -1;                // N_f the table in WS_DN was built for
   void* dn_ptr = nullptr;
   int locality = 0;              // 1: K1T batches in Morton processing order (sort.cu; CDMS_LOCALITY=1, A/B only).
-                                 // Measured (4M c5 particles): correlation 26.97 ms sorted vs 26.58 unsorted, c2 step
-                                 // 0.477 vs 0.409 ms: the kernel is bound by the L1 data pipe's bytes to registers
-                                 // (64 B of coefficients per element; l1tex__data_pipe_lsu_wavefronts 89.5% of peak),
-                                 // not by how many distinct rows a warp touches
+                                 // Measured (4M c5 particles, final kernels): Gram 44.9 vs 45.0 ms, correlation 25.9
+                                 // vs 25.6 sorted / unsorted, c2 step 0.477 vs 0.409 ms: at warm-cache rates the
+                                 // correlation is issue-bound (81%) and the Gram latency-bound at its occupancy, so
+                                 // the halved L1 wavefronts (cold-cache ncu) buy nothing
+                                 // (profiles/r02_warm_k1t_c5_summary.txt)
   int taylor_lanes = -1;         // K1T correlation kernel: -1 by P J (tay_lanes), 1 lane groups, 0 thread per
                                  // particle (CDMS_TAY_LANES=1 / 0, A/B only)
   std::vector<cudaEvent_t> ev_pool;  // timing: 4 events per likelihood batch (before / between the correlation and

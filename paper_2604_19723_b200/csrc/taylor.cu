@@ -487,12 +487,11 @@ __device__ __forceinline__ float dirichlet_fast(float x, float Nf) {
 // sine quotient -- one table row and a short Horner per (pair, antenna), no MUFU, no reciprocal, and the function is
 // entire, so near-equal delays need no special case.  Centres x_r = r / G_D; per pair the fp64 base x_b G_D = g_b + r_b
 // (|r_b| <= 1/2), per antenna d' = r_b + dd (df/c) G_D, its rounding g2 and the offset d = d' - g2 (|d| <= 1/2), all
-// fp32-exact enough.  The lookup is the L1 data pipe's work (one scattered row per (pair, antenna), ~13.5 wavefronts per
-// warp-level 32-byte load: the kernel's bound), so the row is kept at 16 bytes: degree 3 at G_D = 32 N (truncation
-// below N (pi N / (2 G_D))^4 / 4! = N (pi/64)^4/24 = 2.4e-7 N per term), |x| <= 0.6 (FAST: |x| <= 0.564), both signs
-// stored (1.26 MB at N_f = 1024; the even-symmetric half-table, -DCDMS_DN_SYM, costs a mirror per term: measured c5
-// Gram 49.3 vs 46.8 ms, profiles/r02_dn_table.txt).  Round 2's first table had degree 7 at 8 N (32-byte rows):
-// -DCDMS_DN_DEG7 for A/B.
+// fp32-exact enough.  The row is kept at 16 bytes: degree 3 at G_D = 32 N (truncation below N (pi N / (2 G_D))^4 / 4!
+// = N (pi/64)^4/24 = 2.4e-7 N per term), |x| <= 0.6 (FAST: |x| <= 0.564), both signs stored (1.26 MB at N_f = 1024;
+// the even-symmetric half-table, -DCDMS_DN_SYM, costs a mirror per term: measured c5 Gram 49.3 vs 46.8 ms,
+// profiles/r02_dn_table.txt).  Against round 2's first table (degree 7 at 8 N, 32-byte rows, -DCDMS_DN_DEG7 for A/B)
+// the 4 Horner steps fewer per (pair, antenna) took the c5 Gram from 55.9 to 49.3 ms.
 struct GramTab {
   const float4* dn;  // [rows][DN_L / 4] float4 of real coefficients per centre
   float G;           // centres per unit x

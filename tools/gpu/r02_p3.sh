@@ -1,9 +1,6 @@
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_nb_tensor_gpu.py tests/test_k1t_terms_gpu.py tests/test_birth_gpu.py -q -m gpu -x 2>&1 | tail -3
-for c in c5 c3 c2; do
-if [ $c = c5 ]; then PP="--particles 4000000"; else PP=""; fi
-timeout 600 python bench.py --config $c $PP --steps 10 --no-cpu-baseline --no-extras > gpurun_out/r02_p3_$c.json 2>gpurun_out/r02_p3_$c.err
-python -c "import json;d=json.load(open('gpurun_out/r02_p3_$c.json'));print('$c', round(d['ms_per_step'],3), d['kernel_ms_per_step'])"
+for lib in libcdms libcdms_p3m4 libcdms_p3m3; do
+CDMS_LIB=paper_2604_19723_b200/$lib.so timeout 600 python bench.py --config c5 --particles 4000000 --steps 10 --no-cpu-baseline --no-extras > gpurun_out/r02_p3.json 2>gpurun_out/r02_p3.err
+python -c "import json;d=json.load(open('gpurun_out/r02_p3.json'));print('$lib c5', round(d['ms_per_step'],3), d['kernel_ms_per_step'])"
 done
-timeout 600 python bench.py --config c4 --wavefront planar_nb --steps 10 --no-cpu-baseline --no-extras > gpurun_out/r02_p3_c4nb.json 2>/dev/null; python -c "import json;d=json.load(open('gpurun_out/r02_p3_c4nb.json'));print('c4 nb', round(d['ms_per_step'],3), d['kernel_ms_per_step'])"

@@ -118,16 +118,17 @@ def _equal_delay_particles(cfg, sc, rng, n):
     return x, delta
 
 
+@pytest.mark.parametrize("wf", ["spherical", "planar_wb"])
 @pytest.mark.parametrize("layout", list(LAYOUTS))
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-def test_k1t_terms_parity(cd, ctxs, orc, name, layout):
+def test_k1t_terms_parity(cd, ctxs, orc, name, layout, wf):
     """c and G of K1T against orc_terms (direct sums over the element-wise fp64 responses), ROI particles and
-    equal-delay particles near a wall plane."""
+    equal-delay particles near a wall plane; spherical and planar wideband responses."""
     import torch
     ctx = ctxs[layout]
     shp = SHAPES[name]
     cfg = small_cfg(**shp, P=48, index=4 if name == "c5" else 2)
-    case = Case(orc, cfg, particles=np.zeros((1, 6)))
+    case = Case(orc, cfg, particles=np.zeros((1, 6)), wavefront=wf)
     rng = np.random.default_rng(7)
     xe, delta = _equal_delay_particles(cfg, case.sc, rng, 32)
     x = np.concatenate([_particles(cfg, 16, 3), xe])
@@ -142,8 +143,8 @@ def test_k1t_terms_parity(cd, ctxs, orc, name, layout):
     eG = np.abs(G - Go) / cfg.Nz
     # G_01 of the equal-delay particles (LOS vs wall 1) against its delay offset
     worst = int(np.argmax(eG.max(axis=(1, 2, 3))))
-    record("k1t_c_rel", ec.max(), 1e-6, config=name, layout=layout)
-    record("k1t_G_rel", eG.max(), 2e-6, config=name, layout=layout,
+    record("k1t_c_rel", ec.max(), 1e-6, config=name, layout=layout, wavefront=wf)
+    record("k1t_G_rel", eG.max(), 2e-6, config=name, layout=layout, wavefront=wf,
            worst_particle=worst, worst_delta=float(delta[worst - 16]) if worst >= 16 else None)
     assert ec.max() <= 1e-6, ec.max()
     assert eG.max() <= 2e-6, (eG.max(), worst, delta[worst - 16] if worst >= 16 else None)

@@ -74,19 +74,19 @@ def _rel(a, b):
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
 
 
-@pytest.mark.parametrize("J,K,nf", [(2, 2, 16), (1, 3, 32)])
-def test_slam_step_matches_oracle(cd, ctx, orc, J, K, nf):
+@pytest.mark.parametrize("J,K,nf,wf", [(2, 2, 16, "spherical"), (1, 3, 32, "spherical"), (2, 2, 16, "planar_wb")])
+def test_slam_step_matches_oracle(cd, ctx, orc, J, K, nf, wf):
     import torch
     from oracle import slam as OS
     cfg = small_cfg(J=J, K=K, ny=4, nv=4, nf=nf, P=64, index=5)
     sc = scenes.make_scene(cfg)
-    base = orc.Oracle.from_scene(sc)
+    base = orc.Oracle.from_scene(sc, wavefront=wf)
     y, eta = orc.measurement(base, sc, scenes.P_TRUE)
     y64 = y.astype(np.complex64)
     P = 256
     prm = OS.Params(P_m=64, N_g=512)
     st = _known_state(OS, cfg, sc, P, eta)
-    scene = cd.Scene.from_synthetic(sc, precision="fp64")
+    scene = cd.Scene.from_synthetic(sc, wavefront=wf, precision="fp64")
     slam = cd.Slam(ctx, scene, P, P_m=prm.P_m, N_g=prm.N_g, key=prm.key, keep_debug=1)
     _load(cd, slam, st, torch)
     rep = slam.step(torch.as_tensor(y64, device="cuda:0"))
@@ -98,7 +98,7 @@ def test_slam_step_matches_oracle(cd, ctx, orc, J, K, nf):
     # (i) prediction messages and the birth
     e_x = float(np.max(np.abs(v["x_pred"].cpu().numpy() - ref["x_pred"])))
     e_eta = _rel(v["eta_pred"].cpu().numpy(), ref["eta_pred"])
-    record("slam_x_pred_abs", e_x, 1e-12, J=J, K=K)
+    record("slam_x_pred_abs", e_x, 1e-12, J=J, K=K, wavefront=wf)
     record("slam_eta_pred_rel", e_eta, 1e-12, J=J, K=K)
     assert e_x <= 1e-12 and e_eta <= 1e-12
     for i, s in enumerate(ref["slots_prior"]):

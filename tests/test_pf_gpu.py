@@ -59,7 +59,8 @@ def _pf_inputs(orc, cfg, L, P, seed=5, wavefront="spherical"):
 
 
 @pytest.mark.parametrize("name,L,P,los", [("c2", 0, 300, False), ("c2", 3, 300, False), ("c3", 5, 120, False),
-                                           ("c4", 3, 64, False), ("c2", 3, 300, True), ("c3", 5, 120, True)])
+                                           ("c4", 3, 64, False), ("c5", 7, 40, False), ("c2", 3, 300, True),
+                                           ("c3", 5, 120, True)])
 @pytest.mark.parametrize("wavefront", ["spherical", "planar_wb"])
 def test_pf_update_parity(cd, ctx, orc, name, L, P, los, wavefront):
     """los: the LOS PF s = 0 (d_phi = NULL; the F4 driver's slot 0)."""

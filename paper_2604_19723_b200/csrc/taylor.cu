@@ -547,6 +547,9 @@ cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+#ifndef CDMS_GRAM_UCOMP
+#define CDMS_GRAM_UCOMP 1
+#endif
 #ifndef CDMS_GRAM_CHUNK
 #define CDMS_GRAM_CHUNK 16  // antennas per fp32 partial sum (measured 4 / 8 / 16: c5 4M Gram 49.1 / 46.8 / 45.5 ms, G parity 5.5e-7 of N_z at 16)
 #endif
@@ -582,9 +585,32 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
       npar[s] = (int)((long long)ns & 1);
     }
   }
-  float xb[FAST ? NP : 1];  // FAST: per pair the centred fraction of (R_a - R_b) df/c (fp64 difference, one rounding)
-  int gb[TAB ? NP : 1];     // TAB: the centre row of x_b G_D (offset by R0) and the remainder r_b = xb[q]
-  if (FAST) {
+  // FAST: per pair the centred fraction of (R_a - R_b) df/c (fp64 difference, one rounding).  TAB with UCOMP: per
+  // component C_s = R_s (df/c) G_D = I_s + f_s (fp64, |f_s| <= 1/2 in fp32) and per pair only the integer row
+  // gb = I_a - I_b - W G_D + R0 (W = rint((R_a - R_b) df/c) periods); per antenna u_s = f_s + Delta_s (df/c) G_D once
+  // per component and d' = u_a - u_b per pair -- one float per component instead of one per pair held in registers
+  float xb[(FAST && !(TAB && CDMS_GRAM_UCOMP)) ? NP : 1];
+  float fc_[(TAB && CDMS_GRAM_UCOMP) ? S : 1];
+  int gb[TAB ? NP : 1];     // TAB: the centre row of x_b G_D (offset by R0)
+  if (TAB && CDMS_GRAM_UCOMP) {
+    double Ic[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const double C = R64[s] * sc.df_c * (double)tb.G;
+      Ic[s] = rint(C);
+      fc_[s] = (float)(C - Ic[s]);
+    }
+#pragma unroll
+    for (int a = 0; a < S; ++a)
+#pragma unroll
+      for (int b = 0; b < S; ++b) {
+        if (b <= a) continue;
+        const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
+        if (q < 0 || q >= NP) continue;
+        const double W = rint((R64[a] - R64[b]) * sc.df_c);
+        gb[q] = (int)(Ic[a] - Ic[b] - W * (double)tb.G) + tb.R0;
+      }
+  } else if (FAST) {
 #pragma unroll
     for (int a = 0; a < S; ++a)
 #pragma unroll
@@ -631,6 +657,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
           dl[s] = Num<float>::fdiv_(-rq, Rf[s]);  // planar WB only: no 1/R array held through the loop
         }
         cis2pi_fast<float>(dl[s] * sc.fc_cf, er[s], ei[s]);  // e^{j2pi f_c Delta_s/c}: the pairs' carriers as products
+        if (TAB && CDMS_GRAM_UCOMP) dl[s] = fmaf(dl[s], dfG, fc_[(TAB && CDMS_GRAM_UCOMP) ? s : 0]);  // u_s, in centres
       }
 #pragma unroll
       for (int a = 0; a < S; ++a) {  // constant trip counts: both loops unroll fully, the arrays stay in registers
@@ -642,7 +669,8 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
           float D;
           if (TAB) {
             constexpr float M = 12582912.f;
-            const float d1 = fmaf(dl[a] - dl[b], dfG, xb[q]);  // offset from the pair's base centre, in centres
+            const float d1 = (TAB && CDMS_GRAM_UCOMP) ? dl[a] - dl[b]  // offset from the pair's base row, in centres
+                                                      : fmaf(dl[a] - dl[b], dfG, xb[(FAST && !(TAB && CDMS_GRAM_UCOMP)) ? q : 0]);
             const float dm = d1 + M;
             float d = d1 - (dm - M);
             int g2 = gb[q] + (__float_as_int(dm) - __float_as_int(M));

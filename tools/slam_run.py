@@ -34,9 +34,11 @@ def main():
     ap.add_argument("--P-m", type=int, default=256)
     ap.add_argument("--N-g", type=int, default=1 << 14)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--init", default="scratch", choices=["scratch", "map"],
-                    help="scratch: the LOS alone (P:L3676); map: LOS + every wall as PFs with 5 cm SFV and 10%% "
-                         "amplitude errors (tracking with a rough prior map)")
+    ap.add_argument("--init", default="scratch", choices=["scratch", "map", "roi"],
+                    help="scratch: the LOS alone (P:L3676), MT particles around the true start; map: LOS + every wall "
+                         "as PFs with 5 cm SFV and 10%% amplitude errors (tracking with a rough prior map); roi: the LOS "
+                         "alone and MT positions uniform over the ROI (the paper's f(x_0), P:L3673), velocities "
+                         "N(0, 0.5^2 I)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import torch
@@ -71,8 +73,12 @@ def main():
     rng = np.random.default_rng(cfg.seed)
     walls_sfv = sc.sfv
     x0 = np.zeros((P, 6))
-    x0[:, :3] = truth[0] + 0.1 * rng.standard_normal((P, 3))
-    x0[:, 3:] = scenes.V_TRUE + 0.1 * rng.standard_normal((P, 3))
+    if args.init == "roi":
+        x0[:, :3] = scenes.ROI_LO + (scenes.ROI_HI - scenes.ROI_LO) * rng.uniform(size=(P, 3))
+        x0[:, 3:] = 0.5 * rng.standard_normal((P, 3))
+    else:
+        x0[:, :3] = truth[0] + 0.1 * rng.standard_normal((P, 3))
+        x0[:, 3:] = scenes.V_TRUE + 0.1 * rng.standard_normal((P, 3))
     eta0 = eta_true * 10.0 ** rng.uniform(-1.0, 1.0, (J, P))
     slam.init(torch.as_tensor(x0, device=dev), torch.as_tensor(eta0, device=dev))
     if args.init == "map":   # a rough prior map: slots 1..K at the true walls (tracking-mode demonstration)

@@ -948,6 +948,16 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
         WS_TRY(ctx, WS_LOC_TEMP, locality_sort_temp_bytes(PB), &temp);
         WS_TRY(ctx, WS_LOC_POS, 3 * (size_t)PB, &spos);
       }
+      if (ctx->gram_tab && sd.small_step >= 1 && (sd.S >= 7 || ctx->gram_tab == 1)) {  // the Gram's D_N table,
+        float* dn;                                                                     // built here, outside captures
+        WS_TRY(ctx, WS_DN, dn_table_floats(sd.nf), &dn);
+        if (ctx->dn_nf != sd.nf || ctx->dn_ptr != dn) {
+          CUDA_TRY(ctx, launch_dn_table(sd.nf, dn, ctx->stream));
+          ctx->launches += 1;
+          ctx->dn_nf = sd.nf;
+          ctx->dn_ptr = dn;
+        }
+      }
     }
   }
   WS_TRY(ctx, WS_PLAN, 8, &u);

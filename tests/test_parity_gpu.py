@@ -425,30 +425,32 @@ def test_bp_step_fused_matches_separate(cd, orc, name):
         c.close()
 
 
-@pytest.mark.parametrize("wf", ["spherical", "planar_nb"])
+@pytest.mark.parametrize("wf", ["spherical", "planar_wb", "planar_nb"])
 def test_bp_step_graph_capture(cd, orc, wf):
-    """The ABI's capture claim: after cdms_reserve, one single-rank cdms_bp_step recorded in a CUDA graph on the
-    context's stream and replayed gives bit-identical particles, moments and lse to the eager call."""
+    """The ABI's capture claim: after cdms_reserve ALONE (no eager warm-up call, which would allocate what reserve
+    missed), one single-rank cdms_bp_step recorded in a CUDA graph on the context's stream and replayed gives
+    bit-identical particles, moments and lse to an eager call made afterwards."""
     import torch
     cfg = small_cfg(J=2, K=2, ny=4, nv=4, nf=64, P=256)
     s = torch.cuda.Stream()
     ctx = cd.Context(0, s)
     case = Case(orc, cfg, wavefront=wf)
     ctx.reserve(case.scene, cfg.P)
+    ctx.sync()
     key = case.sc.philox_key
     x_e, x_g = case.dx.clone(), case.dx.clone()
     est_e, lse_e = (torch.empty(28, dtype=torch.float64, device="cuda:0"),
                     torch.empty(1, dtype=torch.float64, device="cuda:0"))
     est_g, lse_g = torch.empty_like(est_e), torch.empty_like(lse_e)
-    with torch.cuda.stream(s):
-        cd.bp_step(ctx, case.scene, x_e, case.dsfv, case.dy, case.m, case.v, case.eta, 0.1, 0.5, key, 0,
-                   est=est_e, lse=lse_e)
-    ctx.sync()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         cd.bp_step(ctx, case.scene, x_g, case.dsfv, case.dy, case.m, case.v, case.eta, 0.1, 0.5, key, 0,
                    est=est_g, lse=lse_g)
     g.replay()
+    ctx.sync()
+    with torch.cuda.stream(s):
+        cd.bp_step(ctx, case.scene, x_e, case.dsfv, case.dy, case.m, case.v, case.eta, 0.1, 0.5, key, 0,
+                   est=est_e, lse=lse_e)
     ctx.sync()
     assert torch.equal(x_g, x_e) and torch.equal(est_g, est_e) and torch.equal(lse_g, lse_e)
     ctx.close()

@@ -486,9 +486,11 @@ __device__ __forceinline__ float dirichlet_fast(float x, float Nf) {
 // TAB (FAST with the scene's Dirichlet table, dn_table_kernel): D_N from per-centre Taylor coefficients instead of the
 // sine quotient -- one table row and a short Horner per (pair, antenna), no MUFU, no reciprocal, and the function is
 // entire, so near-equal delays need no special case.  Centres x_r = r / G_D; per pair the fp64 base x_b G_D = g_b + r_b
-// (|r_b| <= 1/2), per antenna d' = r_b + dd (df/c) G_D, its rounding g2 and the offset d = d' - g2 (|d| <= 1/2), all
-// fp32-exact enough.  The row is kept at 16 bytes: degree 3 at G_D = 32 N (truncation below N (pi N / (2 G_D))^4 / 4!
-// = N (pi/64)^4/24 = 2.4e-7 N per term), |x| <= 0.6 (FAST: |x| <= 0.564), both signs stored (1.26 MB at N_f = 1024;
+// (|r_b| <= 1/2), per antenna d' = r_b + dd (df/c) G_D, its rounding g2 and the offset d = d' - g2 (|d| <= 1/2; with
+// CDMS_GRAM_UCOMP 2, the default, the rounding is per component and |d| <= 1), all fp32-exact enough.  The row is kept
+// at 16 bytes: degree 3 at G_D = 64 N (truncation below N (pi N |d|max / G_D)^4 / 4! = N (pi/64)^4/24 = 2.4e-7 N per
+// term at |d| <= 1; round 2's per-pair rounding ran 32 N at |d| <= 1/2, the same bound), |x| <= 0.6 (FAST:
+// |x| <= 0.564), both signs stored (1.26 MB at N_f = 1024, L2-resident;
 // the even-symmetric half-table, -DCDMS_DN_SYM, costs a mirror per term: measured c5 Gram 49.3 vs 46.8 ms,
 // profiles/r02_dn_table.txt).  Against round 2's first table (degree 7 at 8 N, 32-byte rows, -DCDMS_DN_DEG7 for A/B)
 // the 4 Horner steps fewer per (pair, antenna) took the c5 Gram from 55.9 to 49.3 ms.
@@ -502,7 +504,7 @@ constexpr int DN_L = 8, DN_DENS = 8;
 constexpr bool DN_SYM = false;
 #else
 #ifndef CDMS_DN_DENS
-#define CDMS_DN_DENS 32
+#define CDMS_DN_DENS 64
 #endif
 constexpr int DN_L = 4, DN_DENS = CDMS_DN_DENS;
 #ifdef CDMS_DN_SYM
@@ -547,18 +549,31 @@ cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// TAB per-antenna offsets (A/B: -DCDMS_GRAM_UCOMP=1 or 0): 2 rounds u_s = k_s + r_s once per (component, antenna), so a
+// pair needs r_a - r_b (|.| <= 1 centre) and k_a - k_b; 1 rounds d' = u_a - u_b per pair (|d| <= 1/2); 0 holds one
+// fractional base per pair.  The |d| <= 1 of 2 is why the table is at G_D = 64 N (the truncation bound of 32 N at
+// |d| <= 1/2); measured c5 4M Gram 44.7 -> 43.6 ms, c4 3.09 -> 2.67 ms with 2 (profiles/r02_gram_onechunk.txt)
 #ifndef CDMS_GRAM_UCOMP
-#define CDMS_GRAM_UCOMP 1
+#define CDMS_GRAM_UCOMP 2
 #endif
 #ifndef CDMS_GRAM_CHUNK
 #define CDMS_GRAM_CHUNK 16  // antennas per fp32 partial sum (measured 4 / 8 / 16: c5 4M Gram 49.1 / 46.8 / 45.5 ms, G parity 5.5e-7 of N_z at 16)
 #endif
-template <int S, int Q0, int Q1, bool FAST, bool TAB>
+#ifndef CDMS_GRAM_ONE_MAX
+#define CDMS_GRAM_ONE_MAX 64  // lanes with at most this many antennas sum them in one fp32 pass (no fp64 totals)
+#endif
+// ONE (TAB, at most CDMS_GRAM_ONE_MAX antennas per lane): the pair sums stay in fp32 registers over all the lane's
+// antennas (a single chunk) and the block needs no fp64 totals in shared memory -- with (hx, hy, hz, R) parked there
+// too, 128 registers and 4 blocks (16 warps) per SM at S >= 7.  Measured c5 4M Gram 43.6 -> 38.4 ms, c3 2.84 ->
+// 2.53 ms; one fp32 sum of 64 terms against 4 of 16 moved the K1T terms' worst G error within the parity bounds
+// (profiles/r02_gram_onechunk.txt).
+template <int S, int Q0, int Q1, bool FAST, bool TAB, bool ONE>
 __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* __restrict__ tmpl,
                                               const double* __restrict__ particles, int64_t P, int pstride,
                                               const double* __restrict__ sfv, int sfv_pp, float2* __restrict__ terms,
-                                              int lsplit, double2* gsum, double* rsh, const GramTab tb) {
-  constexpr int NP = Q1 - Q0;  // this part's pairs; gsum [NP][TAY_BLOCK]
+                                              int lsplit, double2* gsum, double* rsh, float4* csh,
+                                              const GramTab tb) {
+  constexpr int NP = Q1 - Q0;  // this part's pairs; gsum [NP][TAY_BLOCK] (not ONE)
   // A = 2^lsplit adjacent lanes per particle, lane a takes antennas a, a + A, ... (A > 1 when P J threads alone would
   // leave the SMs latency-bound); no early exit: the group's fp64 totals are combined by shuffles below
   const int A = 1 << lsplit;
@@ -631,33 +646,50 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
   // R_s (fp64) are needed again only in the epilogue: parked in shared memory, not in registers through the loop
   // (18 registers at S = 9, which removed the kernel's spills under its 168-register cap)
 #pragma unroll
-  for (int s = 0; s < S; ++s) rsh[s * TAY_BLOCK + threadIdx.x] = R64[s];
+  for (int s = 0; s < S; ++s) {
+    rsh[s * TAY_BLOCK + threadIdx.x] = R64[s];
+    if (TAB) csh[s * TAY_BLOCK + threadIdx.x] = make_float4(hx[s], hy[s], hz[s], Rf[s]);  // TAB: parked too
+  }
   const float dfG = sc.df_cf * tb.G;  // TAB: d' per unit of the element offset difference
 #pragma unroll
-  for (int q = 0; q < NP; ++q) gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(0.0, 0.0);
+  for (int q = 0; q < NP; ++q)
+    if (!ONE) gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(0.0, 0.0);
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
   const float4* tm = tmpl + (int64_t)j * sc.n_mb * NWARP;
   const int Nl = live ? (Na - a0 + A - 1) >> lsplit : 0;  // this lane's antennas m = a0 + A i, i < Nl
-  for (int i0 = 0; i0 < Nl; i0 += CDMS_GRAM_CHUNK) {  // fp32 partial sums over a chunk, then fp64
-    float gr[NP], gi[NP];
+  float gr[NP], gi[NP];
 #pragma unroll
-    for (int q = 0; q < NP; ++q) gr[q] = gi[q] = 0.f;
-    const int i1 = min(i0 + CDMS_GRAM_CHUNK, Nl);
+  for (int q = 0; q < NP; ++q) gr[q] = gi[q] = 0.f;
+  const int chunk = ONE ? Nl : CDMS_GRAM_CHUNK;
+  for (int i0 = 0; i0 < Nl; i0 += chunk) {  // fp32 partial sums over a chunk, then fp64
+    if (!ONE && i0 > 0) {
+#pragma unroll
+      for (int q = 0; q < NP; ++q) gr[q] = gi[q] = 0.f;
+    }
+    const int i1 = min(i0 + chunk, Nl);
     for (int i = i0; i < i1; ++i) {
       const int m = a0 + (i << lsplit);
       const float4 v = __ldg(&tm[m]);
       float dl[S], er[S], ei[S];
+      int ik[(TAB && CDMS_GRAM_UCOMP == 2) ? S : 1];  // UCOMP 2: u_s = k_s + r_s, k_s as the bits of k_s + M
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const float rq = hx[s] * v.x + hy[s] * v.y + hz[s] * v.z;
+        const float4 h = TAB ? csh[s * TAY_BLOCK + threadIdx.x] : make_float4(hx[s], hy[s], hz[s], Rf[s]);
+        const float rq = h.x * v.x + h.y * v.y + h.z * v.z;
         if (sph) {
           const float n = v.w - 2.f * rq;
-          dl[s] = Num<float>::fdiv_(n, Num<float>::fsqrt_(Rf[s] * Rf[s] + n) + Rf[s]);
+          dl[s] = Num<float>::fdiv_(n, Num<float>::fsqrt_(h.w * h.w + n) + h.w);
         } else {
-          dl[s] = Num<float>::fdiv_(-rq, Rf[s]);  // planar WB only: no 1/R array held through the loop
+          dl[s] = Num<float>::fdiv_(-rq, h.w);  // planar WB only: no 1/R array held through the loop
         }
         cis2pi_fast<float>(dl[s] * sc.fc_cf, er[s], ei[s]);  // e^{j2pi f_c Delta_s/c}: the pairs' carriers as products
         if (TAB && CDMS_GRAM_UCOMP) dl[s] = fmaf(dl[s], dfG, fc_[(TAB && CDMS_GRAM_UCOMP) ? s : 0]);  // u_s, in centres
+        if (TAB && CDMS_GRAM_UCOMP == 2) {  // rounded per component: per pair r_a - r_b (|.| <= 1) and k_a - k_b
+          constexpr float M = 12582912.f;
+          const float um = dl[s] + M;
+          ik[(TAB && CDMS_GRAM_UCOMP == 2) ? s : 0] = __float_as_int(um);
+          dl[s] = dl[s] - (um - M);
+        }
       }
 #pragma unroll
       for (int a = 0; a < S; ++a) {  // constant trip counts: both loops unroll fully, the arrays stay in registers
@@ -674,6 +706,11 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
             const float dm = d1 + M;
             float d = d1 - (dm - M);
             int g2 = gb[q] + (__float_as_int(dm) - __float_as_int(M));
+            if (CDMS_GRAM_UCOMP == 2) {
+              d = d1;
+              g2 = gb[q] + ik[(TAB && CDMS_GRAM_UCOMP == 2) ? a : 0] -
+                   ik[(TAB && CDMS_GRAM_UCOMP == 2) ? b : 0];
+            }
             if (DN_SYM) {  // D_N even: the row of |x|, the offset mirrored (selects, no branch)
               const bool neg = g2 < 0;
               g2 = neg ? -g2 : g2;
@@ -704,6 +741,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
     }
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
+      if (ONE) continue;
       double2 t = gsum[q * TAY_BLOCK + threadIdx.x];
       gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(t.x + (double)gr[q], t.y + (double)gi[q]);
     }
@@ -715,7 +753,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
       if (b <= a) continue;
       const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
       if (q < 0 || q >= NP) continue;
-      double2 acc = gsum[q * TAY_BLOCK + threadIdx.x];
+      double2 acc = ONE ? make_double2((double)gr[q], (double)gi[q]) : gsum[q * TAY_BLOCK + threadIdx.x];
       for (int o = 1; o < A; o <<= 1) {  // fixed-order tree over the group's lanes
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
@@ -734,7 +772,6 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
     }
   }
 }
-template <int S>
 // measured: S = 9 in 3 parts 58.8 vs 59.8 ms (c5 shard); S = 7 in 2 parts 9.16 vs 8.87 ms (c3: one part already fits
 // 168 registers, splitting only repeats the per-component work)
 // S = 9 pair parts over blockIdx.z (A/B: -DCDMS_GRAM_PARTS9=3): with the FAST path's smaller per-component state two
@@ -746,49 +783,62 @@ template <int S>
 #ifndef CDMS_GRAM_MINB
 #define CDMS_GRAM_MINB 3
 #endif
-__host__ __device__ constexpr int tay_gram_parts() { return S >= 9 ? CDMS_GRAM_PARTS9 : (S == 8 ? 2 : 1); }
-template <int S, bool FAST, bool TAB>
-__global__ void __launch_bounds__(TAY_BLOCK, (S >= 7 ? CDMS_GRAM_MINB : 1))  // S >= 7: 3 blocks (12 warps) per SM, <= 168 registers
+#ifndef CDMS_GRAM_PARTS9_ONE
+#define CDMS_GRAM_PARTS9_ONE 1
+#endif
+// ONE at S = 9: all 36 pairs in one part at 3 blocks per SM (168 registers, a few spilled per antenna) -- the 9
+// components' offsets and carriers computed once instead of per part; measured c5 4M Gram 38.0 (2 parts, 4 blocks per
+// SM) vs 34.5 ms (1 part, 3 blocks; 2 blocks: 41.2 ms), profiles/r02_gram_onechunk.txt
+template <int S, bool ONE>
+__host__ __device__ constexpr int tay_gram_parts() {
+  return S >= 9 ? (ONE ? CDMS_GRAM_PARTS9_ONE : CDMS_GRAM_PARTS9) : (S == 8 ? 2 : 1);
+}
+template <int S, bool ONE>
+__host__ __device__ constexpr int tay_gram_minb() {
+  return S < 7 ? 1 : !ONE ? CDMS_GRAM_MINB : tay_gram_parts<S, ONE>() == 1 && S >= 9 ? 3 : 4;
+}
+template <int S, bool FAST, bool TAB, bool ONE>
+__global__ void __launch_bounds__(TAY_BLOCK, (tay_gram_minb<S, ONE>()))  // S >= 7: 12 or 16 (ONE) warps per SM
     tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
                     const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
                     int sfv_pp, float2* __restrict__ terms, int lsplit, const GramTab tb) {
-  constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>(), H = NP / NPART;
+  constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S, ONE>(), H = NP / NPART;
+  constexpr int NPMAX = NP - NP / NPART * (NPART - 1);  // the larger part
   extern __shared__ double2 smem_g[];
-  double* rsh = reinterpret_cast<double*>(smem_g);  // [S][TAY_BLOCK] R_s, then the pair totals
-  double2* gsum = smem_g + (S * TAY_BLOCK + 1) / 2;
+  double* rsh = reinterpret_cast<double*>(smem_g);        // [S][TAY_BLOCK] R_s
+  double2* gsum = smem_g + (S * TAY_BLOCK + 1) / 2;       // not ONE: [NPMAX][TAY_BLOCK] fp64 pair totals
+  float4* csh = reinterpret_cast<float4*>(gsum + (ONE ? 0 : NPMAX * TAY_BLOCK));  // TAB: [S][TAY_BLOCK]
   if constexpr (NPART == 1) {
-    tay_gram_part<S, 0, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
+    tay_gram_part<S, 0, NP, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
   } else if constexpr (NPART == 2) {
     if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
+      tay_gram_part<S, 0, H, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
     else
-      tay_gram_part<S, H, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
+      tay_gram_part<S, H, NP, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
   } else {
     static_assert(NPART == 3, "");
     if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
+      tay_gram_part<S, 0, H, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
     else if (blockIdx.z == 1)
-      tay_gram_part<S, H, 2 * H, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
+      tay_gram_part<S, H, 2 * H, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
     else
-      tay_gram_part<S, 2 * H, NP, FAST, TAB>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, tb);
+      tay_gram_part<S, 2 * H, NP, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
   }
 }
-template <int S, bool FAST, bool TAB>
+template <int S, bool FAST, bool TAB, bool ONE>
 static cudaError_t launch_tay_gram_v(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
                                      int pstride, const double* sfv, int sfv_pp, float2* terms, const GramTab& tb,
-                                     cudaStream_t st) {
-  constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S>();
-  const size_t smem = (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2) +  // the larger part
-                      (size_t)(S * TAY_BLOCK + 1) / 2 * sizeof(double2);                       // + R_s
-  cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S, FAST, TAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int lsplit, cudaStream_t st) {
+  constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S, ONE>();
+  const size_t smem = (size_t)(S * TAY_BLOCK + 1) / 2 * sizeof(double2) +                                   // R_s
+                      (ONE ? 0 : (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2)) +  // totals
+                      (TAB ? (size_t)S * TAY_BLOCK * sizeof(float4) : 0);                                   // h_s, R_s
+  cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S, FAST, TAB, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  // antennas over 2 lanes per particle when P J threads are fewer than ~2 resident waves (measured at c2: 1 lane
-  // 0.391, 2 lanes 0.388, 4 lanes 0.405, 8 lanes 0.448 ms per step; at P = 1.4e5 2 lanes 0.494 vs 4 lanes 0.517)
-  const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 1 : 0;
   dim3 grid((unsigned)(((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK), sc.J, NPART);
-  tay_gram_kernel<S, FAST, TAB><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms,
-                                                               lsplit, tb);
+  tay_gram_kernel<S, FAST, TAB, ONE><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp,
+                                                                    terms, lsplit, tb);
   return cudaGetLastError();
 }
 #ifndef CDMS_GRAM_FAST
@@ -803,9 +853,17 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
   tb.dn = reinterpret_cast<const float4*>(dn);
   tb.G = (float)dn_centres(sc.nf);
   tb.R0 = dn_r0(sc.nf);
-  if (fast && dn) return launch_tay_gram_v<S, true, true>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
-  if (fast) return launch_tay_gram_v<S, true, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
-  return launch_tay_gram_v<S, false, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, st);
+  // antennas over 2 lanes per particle when P J threads are fewer than ~2 resident waves (measured at c2: 1 lane
+  // 0.391, 2 lanes 0.388, 4 lanes 0.405, 8 lanes 0.448 ms per step; at P = 1.4e5 2 lanes 0.494 vs 4 lanes 0.517)
+  const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 1 : 0;
+  const bool one = ((sc.Na + (1 << lsplit) - 1) >> lsplit) <= CDMS_GRAM_ONE_MAX;
+  if (fast && dn && one)
+    return launch_tay_gram_v<S, true, true, true>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit, st);
+  if (fast && dn)
+    return launch_tay_gram_v<S, true, true, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit, st);
+  if (fast)
+    return launch_tay_gram_v<S, true, false, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit, st);
+  return launch_tay_gram_v<S, false, false, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit, st);
 }
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
                             const double* sfv, int sfv_pp, float2* terms, const float* dn, cudaStream_t st) {

@@ -199,6 +199,7 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
   out->fc_c = sc->fc / C_LIGHT;
   out->lambda = C_LIGHT / sc->fc;
   out->fc_cf = (float)out->fc_c;
+  out->fc2pi_f = (float)(2.0 * PI * out->fc_c);
   out->df_cf = (float)out->df_c;
   out->nf_f = (float)sc->nf;
   out->c6N_f = (float)(PI * PI / 6.0 * ((double)sc->nf * sc->nf - 1.0));
@@ -215,6 +216,7 @@ cdms_status build_scene(cdms_ctx ctx, const cdms_scene* sc, const double* f_pb, 
     const double th = 2.0 * PI * sqrt(hy * hy + hv * hv) * out->df_c;
     out->small_step = (th <= 0.02) ? 2 : (th <= 0.2) ? 1 : 0;
     out->small_z = (2.0 * PI * sqrt(hy * hy + hv * hv) * out->segdf_c <= 1.0) ? 1 : 0;
+    out->ap_r = 1.5 * sqrt(hy * hy + hv * hv) + 1e-9;
   }
   for (int j = 0; j < sc->J; ++j) {
     const double* R = sc->h_pa_rot + 9 * j;

@@ -38,6 +38,9 @@ struct SceneDev {
   // fp32 constants of the per-antenna Gram term (constant-bank operands): fc/c, df/c, N = nf,
   // pi^2/6 (N^2 - 1) and the sign mask (bit 31 when N is even, i.e. D_N(x + 1) = -D_N(x))
   float fc_cf, df_cf, nf_f, c6N_f;
+  float fc2pi_f;     // fp32 2 pi f_c / c: carriers e^{j f_c 2pi Delta/c} straight into __sincosf (no reduction)
+  double ap_r;       // 1.5 x half the URA diagonal (||p~_m|| <= ap_r / 1.5): R > ap_r keeps every antenna distance
+                     // >= R / 3, far from fp32 cancellation
   uint32_t evenN_mask;
   float f0_cf, segdf_cf;  // fp32 f0/c, SEG df/c for the per-antenna set-up
   int two_seg;            // SEG < nf <= 2 SEG, not planar NB: second segment phasor formed directly (A1)

@@ -67,6 +67,12 @@ __device__ __forceinline__ void cis2pi_fast<double>(double x, double& re, double
   sincospi(2.0 * x, &im, &re);
 }
 
+// e^{j 2 pi f_c Delta / c} from fp32 Delta (metres) and w = fp32(2 pi f_c / c): no centred reduction -- MUFU.SIN/COS
+// take the argument in revolutions and drop the integer part themselves, so the only cost of |w Delta| > pi is the
+// rounding of the revolutions (|err| <= |Delta f_c/c| 2^-23 cycles; tools/microbench/sincos_range.cu measures it
+// against fp64, profiles/r02_sincos_range.txt).  Three FMA-pipe instructions fewer than cis2pi_fast per call.
+__device__ __forceinline__ void carrier_f(float delta, float w, float& re, float& im) { __sincosf(delta * w, &im, &re); }
+
 // ---------------------------------------------------------------------------- row A1 (geometry)
 // VA phase centre p_VA = p_j - (2 p_j^T s/||s||^2 - 1) s and the unit wall normal
 // shat = s/||s|| that defines H = I - 2 shat shat^T.  LOS (sfv == nullptr): p_VA = p_j,

@@ -216,6 +216,7 @@ __device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par,
 // else tay_corr_lanes_kernel below): per component the fp64 geometry (VA, H r, R), the
 // fp64-reduced phase bases e^{j2pi f_c R/c} and frac(df R/c); per antenna the fp32 offset Delta_m (cancellation-free,
 // as K1), the phasor e^{j2pi f_c Delta_m/c}, the table centre and delta', one table row and the Taylor sum.
+template <bool SPH>  // spherical (else planar WB): a template, so the antenna loop carries no predicated other path
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_corr_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
                     const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P, int pstride,
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   const double* pos = particles + p * pstride;
   const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * Na * (G + 1) * (TAY_L / 2);
   const float4* tm = tmpl + (int64_t)j * Na_pad;
-  const bool sph = sc.wavefront == CDMS_SPHERICAL;
+  constexpr bool sph = SPH;
   int fl = 0;
   for (int s = 0; s < S; ++s) {
     const double* sfv_s = nullptr;
@@ -251,10 +252,17 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     const TayBase tb = tay_base(R64 * sc.df_c);  // delay phase base
     double sb, cb;
     sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
+    // an antenna distance can vanish only within the aperture (R <= ap_r): that rare case is checked apart
+    if (sph && !(R64 > sc.ap_r))
+      for (int m = 0; m < Na; ++m) {
+        const float4 v = __ldg(&tm[m]);
+        if (!(Num<float>::fsqrt_(R * R + v.w - 2.f * (hx * v.x + hy * v.y + hz * v.z)) > 0.f)) fl |= 1;
+      }
     double accr = 0.0, acci = 0.0;  // sum_m e^{j2pi f_c Delta_m/c} Y_m; times e^{j2pi f_c R/c} (cb, sb) at the end
     for (int m0 = 0; m0 < Na; m0 += 16) {
       float pr = 0.f, pi = 0.f;
       const int m1 = min(m0 + 16, Na);
+#pragma unroll 4
       for (int m = m0; m < m1; ++m) {
         const float4 v = __ldg(&tm[m]);
         const float rq = hx * v.x + hy * v.y + hz * v.z;
@@ -262,13 +270,12 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         if (sph) {
           const float n = v.w - 2.f * rq;
           const float d = Num<float>::fsqrt_(R * R + n);  // approximate: no IEEE slow-path call in the loop
-          if (!(d > 0.f)) fl |= 1;
           delta = Num<float>::fdiv_(n, d + R);
         } else {
           delta = Num<float>::fdiv_(-rq, R);
         }
         float er, ei;
-        cis2pi_fast<float>(delta * sc.fc_cf, er, ei);
+        carrier_f(delta, sc.fc2pi_f, er, ei);
         uint32_t g;
         float dp;
         bool flip;
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         delta = Num<float>::fdiv_(-rq, sR);
       }
       float er, ei;
-      cis2pi_fast<float>(delta * sc.fc_cf, er, ei);
+      carrier_f(delta, sc.fc2pi_f, er, ei);
       uint32_t g;
       float dp;
       bool flip;
@@ -682,7 +689,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
         } else {
           dl[s] = Num<float>::fdiv_(-rq, h.w);  // planar WB only: no 1/R array held through the loop
         }
-        cis2pi_fast<float>(dl[s] * sc.fc_cf, er[s], ei[s]);  // e^{j2pi f_c Delta_s/c}: the pairs' carriers as products
+        carrier_f(dl[s], sc.fc2pi_f, er[s], ei[s]);  // e^{j2pi f_c Delta_s/c}: the pairs' carriers as products
         if (TAB && CDMS_GRAM_UCOMP) dl[s] = fmaf(dl[s], dfG, fc_[(TAB && CDMS_GRAM_UCOMP) ? s : 0]);  // u_s, in centres
         if (TAB && CDMS_GRAM_UCOMP == 2) {  // rounded per component: per pair r_a - r_b (|.| <= 1) and k_a - k_b
           constexpr float M = 12582912.f;
@@ -924,8 +931,12 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
     return cudaGetLastError();
   }
   dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
-  tay_corr_kernel<<<grid, TAY_BLOCK, 0, st>>>(sc, tay_centres(sc.nf), tab, tmpl, particles, P, pstride, sfv, sfv_pp,
-                                              terms, pflag, gram_diag);
+  if (sc.wavefront == CDMS_SPHERICAL)
+    tay_corr_kernel<true><<<grid, TAY_BLOCK, 0, st>>>(sc, tay_centres(sc.nf), tab, tmpl, particles, P, pstride, sfv,
+                                                      sfv_pp, terms, pflag, gram_diag);
+  else
+    tay_corr_kernel<false><<<grid, TAY_BLOCK, 0, st>>>(sc, tay_centres(sc.nf), tab, tmpl, particles, P, pstride, sfv,
+                                                       sfv_pp, terms, pflag, gram_diag);
   return cudaGetLastError();
 }
 
@@ -994,7 +1005,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         delta = Num<float>::fdiv_(-rq, R);
       }
       float er, ei;
-      cis2pi_fast<float>(delta * sc.fc_cf, er, ei);
+      carrier_f(delta, sc.fc2pi_f, er, ei);
       uint32_t g;
       float dp;
       bool flip;

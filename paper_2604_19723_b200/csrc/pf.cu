@@ -90,8 +90,9 @@ __global__ void __launch_bounds__(PF_BLOCK) pf_dots_kernel(int T, int64_t Nz, co
 }
 
 // Per PA (one thread each): K = I + M^H M / eta = L L^H (complex Cholesky, fp64), w = M^H e0, kiw = K^{-1} w and
-// t0 = e0^H A^{-1} e0 = |e0|^2 / eta - w^H K^{-1} w / eta^2.  fixed[j] = [Kc (Lm x Lm, lower, row-major), kiw (Lm),
-// (t0, 0)] with Lm = PF_MAXT - 1.  Non-positive pivot -> FLAG_NAN (M M^H not representable).
+// t0 = e0^H A^{-1} e0 = |e0|^2 / eta - w^H K^{-1} w / eta^2.  fixed[j] = [Kc (Lm x Lm, lower, row-major; the
+// diagonal entries hold (L_aa, 1 / L_aa)), kiw (Lm), (t0, 0)] with Lm = PF_MAXT - 1.  Non-positive pivot -> FLAG_NAN
+// (M M^H not representable).
 constexpr int PF_FIXED = (PF_MAXT - 1) * (PF_MAXT - 1) + (PF_MAXT - 1) + 1;  // double2 per PA
 __global__ void pf_fixed_kernel(int J, int T, const double2* __restrict__ dots, const double* __restrict__ eta,
                                 double2* __restrict__ fixed, int* flags) {
@@ -154,12 +155,16 @@ __global__ void pf_fixed_kernel(int J, int T, const double2* __restrict__ dots, 
   }
   double2* f = fixed + (int64_t)j * PF_FIXED;
   for (int i = 0; i < Lm * Lm; ++i) f[i] = K[i];
+  for (int a = 0; a < L; ++a) f[a * Lm + a].y = 1.0 / K[a * Lm + a].x;  // for the per-particle substitution
   for (int a = 0; a < Lm; ++a) f[Lm * Lm + a] = a < L ? y[a] : make_double2(0.0, 0.0);
   f[Lm * Lm + Lm] = make_double2(d[0].x / e - wsq / (e * e), 0.0);  // t0
 }
 
-// logr_p (one thread per particle): the per-PA terms of the header from the correlations cc [P][J][T] and fixed[j]
-__global__ void pf_asm_kernel(int J, int T, double Nz, const double2* __restrict__ cc, const double2* __restrict__ fixed,
+// logr_p (one thread per particle): the per-PA terms of the header from the correlations cc [J][T][P] and fixed[j].
+// T is a template parameter so the substitution loops unroll and y stays in registers (a runtime T put it in local
+// memory: 128-byte stack frame)
+template <int T>
+__global__ void pf_asm_kernel(int J, double Nz, const double2* __restrict__ cc, const double2* __restrict__ fixed,
                               const double* __restrict__ eta, const double* __restrict__ zeta,
                               const double* __restrict__ gain2, const double* __restrict__ walpha,
                               const double2* __restrict__ mu, const double* __restrict__ gamma, int* __restrict__ pflag,
@@ -173,28 +178,32 @@ __global__ void pf_asm_kernel(int J, int T, double Nz, const double2* __restrict
   const int fl = pflag[p];
   pflag[p] = 0;
   for (int j = 0; j < J; ++j) {
-    const double2* c = cc + (p * J + j) * T;
+    double2 c[T];  // this particle's correlations for PA j (coalesced across the warp)
+#pragma unroll
+    for (int t = 0; t < T; ++t) c[t] = cc[((int64_t)j * T + t) * P + p];
     const double2* f = fixed + (int64_t)j * PF_FIXED;
-    const double e = eta[j], z = zeta[j];
+    const double e = eta[j], z = zeta[j], ie = 1.0 / e, ie2 = ie * ie;  // the only divisions: 1 / eta, 1 / den
     // beta = N_z g^2 / eta - |L^{-1} u|^2 / eta^2, u_t = m_t^H psi = conj(c_{1+t});  b0 = c_0 / eta - sum_t c_{1+t}
     // (K^{-1} M^H e0)_t / eta^2
     double2 y[PF_MAXT - 1];
-    double usq = 0.0, b0r = c[0].x / e, b0i = c[0].y / e;
+    double usq = 0.0, b0r = c[0].x * ie, b0i = c[0].y * ie;
+#pragma unroll
     for (int a = 0; a < L; ++a) {
       double yr = c[1 + a].x, yi = -c[1 + a].y;
+#pragma unroll
       for (int k = 0; k < a; ++k) {
         const double2 x = f[a * Lm + k];
         yr -= x.x * y[k].x - x.y * y[k].y;
         yi -= x.x * y[k].y + x.y * y[k].x;
       }
-      const double dl = f[a * Lm + a].x;
-      y[a] = make_double2(yr / dl, yi / dl);
+      const double il = f[a * Lm + a].y;  // 1 / L_aa (pf_fixed_kernel)
+      y[a] = make_double2(yr * il, yi * il);
       usq += y[a].x * y[a].x + y[a].y * y[a].y;
       const double2 k = f[Lm * Lm + a];
-      b0r -= (c[1 + a].x * k.x - c[1 + a].y * k.y) / (e * e);
-      b0i -= (c[1 + a].x * k.y + c[1 + a].y * k.x) / (e * e);
+      b0r -= (c[1 + a].x * k.x - c[1 + a].y * k.y) * ie2;
+      b0i -= (c[1 + a].x * k.y + c[1 + a].y * k.x) * ie2;
     }
-    const double beta = Nz * gain2[p * J + j] / e - usq / (e * e);
+    const double beta = Nz * gain2[p * J + j] * ie - usq * ie2;
     const double cr = z * mup.x, ci = z * mup.y;                    // c = zeta mu_p
     const double br = b0r - cr * beta, bi = b0i - ci * beta;         // b = psi^H A^-1 e
     const double q = (gamma[p] + mu2 * (1.0 - z)) * z;
@@ -312,8 +321,17 @@ cudaError_t launch_pf_finish(const SceneDev& sc, int T, const double2* cc, const
                              double* lse_part, cudaStream_t st) {
   const int64_t n = P * sc.J;
   pf_gain_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, particles, P, pstride, phi, gain2);
-  pf_asm_kernel<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(sc.J, T, (double)sc.nf * sc.Na, cc, fixed, d_eta, d_zeta,
-                                                           gain2, walpha, mu, gamma, pflag, P, logr, flags);
+  switch (T) {
+#define PF_ASM(n)                                                                                                   \
+  case n:                                                                                                           \
+    pf_asm_kernel<n><<<(unsigned)((P + 127) / 128), 128, 0, st>>>(sc.J, (double)sc.nf * sc.Na, cc, fixed, d_eta, \
+                                                                  d_zeta, gain2, walpha, mu, gamma, pflag, P, logr, \
+                                                                  flags);                                          \
+    break;
+    PF_ASM(1) PF_ASM(2) PF_ASM(3) PF_ASM(4) PF_ASM(5) PF_ASM(6) PF_ASM(7) PF_ASM(8) PF_ASM(9)
+#undef PF_ASM
+    default: return cudaErrorInvalidValue;
+  }
   cudaError_t e = launch_lse_rows(logr, P, 1, P, walpha, P, lse_part, lse_part + 3 * lse_blocks(P), st);
   if (e != cudaSuccess) return e;
   pf_norm_kernel<<<1, 1, 0, st>>>(lse_part + 3 * lse_blocks(P), out, flags);

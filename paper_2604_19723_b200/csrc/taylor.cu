@@ -945,23 +945,24 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
 // wall of PF particle p's SFV phi_p seen from the paired MT particle x_p (reading C-amb-F1a) -- against T snapshots
 // per PA (K1T tables of snapshot t of PA j at table index j T + t, [m][g][l] layout).  Per antenna the fp32 offset,
 // carrier and table centre are formed once (as tay_corr_kernel) and reused for every snapshot: one 64-byte row and one
-// Taylor sum per (antenna, snapshot).  out [P][J][T] complex128, path-loss gain applied; pflag as K1T.
+// Taylor sum per (antenna, snapshot).  out [J][T][P] complex128 (consecutive particles contiguous: coalesced stores
+// here and loads in pf_asm_kernel), path-loss gain applied; pflag as K1T.
 template <int T>
 __global__ void __launch_bounds__(TAY_BLOCK)
     pf_corr_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
                    const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P, int pstride,
                    const double* __restrict__ phi, double2* __restrict__ out, int* __restrict__ pflag) {
-  const int J = sc.J, Na = sc.Na;
+  const int Na = sc.Na;
   const int64_t p = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
   const int j = blockIdx.y;
   if (p >= P) return;
   const double* pos = particles + p * pstride;
-  double2* o = out + (p * J + j) * T;
+  double2* o = out + (int64_t)j * T * P + p;  // o[t * P]
   double va[3], sh[3];
   if (!anchor_va(sc, j, phi ? phi + 3 * p : nullptr, va, sh)) {  // phi == NULL: the LOS PF (sh = 0, H = I)
     atomicOr(&pflag[p], 2);
 #pragma unroll
-    for (int t = 0; t < T; ++t) o[t] = make_double2(0.0, 0.0);
+    for (int t = 0; t < T; ++t) o[t * P] = make_double2(0.0, 0.0);
     return;
   }
   const double r0 = pos[0] - va[0], r1 = pos[1] - va[1], r2 = pos[2] - va[2];
@@ -971,7 +972,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   if (!(R64 > 0.0)) {
     atomicOr(&pflag[p], 1);
 #pragma unroll
-    for (int t = 0; t < T; ++t) o[t] = make_double2(0.0, 0.0);
+    for (int t = 0; t < T; ++t) o[t * P] = make_double2(0.0, 0.0);
     return;
   }
   const float R = (float)R64;
@@ -1040,7 +1041,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   const double gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
 #pragma unroll
   for (int t = 0; t < T; ++t)
-    o[t] = make_double2((accr[t] * cb - acci[t] * sb) * gn, (accr[t] * sb + acci[t] * cb) * gn);
+    o[t * P] = make_double2((accr[t] * cb - acci[t] * sb) * gn, (accr[t] * sb + acci[t] * cb) * gn);
 }
 cudaError_t launch_pf_corr(const SceneDev& sc, int T, const float2* tab, const float4* tmpl, const double* particles,
                            int64_t P, int pstride, const double* phi, double2* out, int* pflag, cudaStream_t st) {

@@ -26,6 +26,10 @@ SHAPES = {  # the BASELINE configs' scene shapes (J, K, URA, N_f)
     "c3": dict(J=2, K=6, ny=8, nv=8, nf=512),
     "c4": dict(J=1, K=4, ny=16, nv=16, nf=256),
     "c5": dict(J=4, K=8, ny=8, nv=8, nf=1024),
+    # more than 64 antennas per lane: the Gram's chunked path (fp32 sums of 16 antennas, fp64 totals in shared
+    # memory; S = 9 in two pair parts) instead of the single-pass one every BASELINE config but c4 takes
+    "s9a144": dict(J=1, K=8, ny=12, nv=12, nf=64),
+    "s7a144": dict(J=1, K=6, ny=12, nv=12, nf=128),
 }
 LAYOUTS = {"lanes": "1", "thread": "0"}
 
@@ -120,7 +124,7 @@ def _equal_delay_particles(cfg, sc, rng, n):
 
 @pytest.mark.parametrize("wf", ["spherical", "planar_wb"])
 @pytest.mark.parametrize("layout", list(LAYOUTS))
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "s9a144", "s7a144"])
 def test_k1t_terms_parity(cd, ctxs, orc, name, layout, wf):
     """c and G of K1T against orc_terms (direct sums over the element-wise fp64 responses), ROI particles and
     equal-delay particles near a wall plane; spherical and planar wideband responses."""
@@ -149,6 +153,37 @@ def test_k1t_terms_parity(cd, ctxs, orc, name, layout, wf):
     assert ec.max() <= 1e-6, ec.max()
     assert eG.max() <= 2e-6, (eG.max(), worst, delta[worst - 16] if worst >= 16 else None)
     assert np.allclose(np.real(np.einsum("pjss->pjs", G)), cfg.Nz, rtol=1e-12)   # G_ss = N_z (unit modulus)
+
+
+@pytest.mark.parametrize("name", ["c5", "c3"])
+def test_k1t_terms_sampled_at_bench_launch(cd, orc, name):
+    """c and G at the launch configuration the bench times for these shapes: P J >= 2 x 148 x 1024 threads, so the Gram
+    runs one lane per particle (lsplit 0) and, at S = 9, all 36 pairs in one part; the correlation is the
+    thread-per-particle kernel.  The oracle computes 24 sampled particles (first, last, random) one by one."""
+    import torch
+    shp = SHAPES[name]
+    P = -(-2 * 148 * 1024 // shp["J"]) + 1000
+    cfg = small_cfg(**shp, P=P, index=4 if name == "c5" else 2)
+    case = Case(orc, cfg, particles=np.zeros((1, 6)), wavefront="spherical")
+    x = _particles(cfg, P, 13)
+    ctx = cd.Context(0)
+    dx = torch.as_tensor(x, device="cuda:0").contiguous()
+    l, c, G = cd.loglik_terms(ctx, case.scene, dx, case.dsfv, case.dy, case.m, case.v, case.eta)
+    ctx.sync()
+    rng = np.random.default_rng(17)
+    idx = np.unique(np.concatenate([[0, P - 1], rng.integers(0, P, 22)]))
+    ti = torch.as_tensor(idx, device="cuda:0")
+    c, G = c.index_select(0, ti).cpu().numpy(), G.index_select(0, ti).cpu().numpy()
+    ctx.close()
+    st, co, Go = case.o.terms(x[idx], case.sc.sfv, case.y)
+    assert st == 0
+    zn = np.sqrt(np.sum(np.abs(case.y) ** 2, axis=(1, 2)))
+    ec = np.abs(c - co) / (np.sqrt(cfg.Nz) * zn[None, :, None])
+    eG = np.abs(G - Go) / cfg.Nz
+    record("k1t_c_rel_bench_launch", ec.max(), 1e-6, config=name, P=P)
+    record("k1t_G_rel_bench_launch", eG.max(), 2e-6, config=name, P=P)
+    assert ec.max() <= 1e-6, ec.max()
+    assert eG.max() <= 2e-6, eG.max()
 
 
 @pytest.mark.parametrize("sfv_pp", [False, True])

@@ -214,6 +214,15 @@ __device__ inline void plan_dev(const uint64_t* Q, int nranks, int rank, int64_t
 
 // ---------------------------------------------------------------------------- launchers
 // (defined in loglik.cu / beliefs.cu, called from cdms.cpp)
+// The template columns as a kernel parameter (constant bank) when J N_a,pad <= TMPLC_MAX: the correlation kernel's
+// per-element template read then goes through the constant cache instead of the L1 data path its table rows
+// saturate; prep_y copies the same host-computed values into the tmpl buffer, so every kernel sees identical columns.
+constexpr int TMPLC_MAX = 512;
+struct TmplC {
+  float4 v[TMPLC_MAX];  // [J][Na_pad] (R_j p~_m, ||p~_m||^2), padded antennas repeat m = 0
+  int n;                // J Na_pad, or 0 (too many: the kernels compute / read the tmpl buffer)
+};
+void make_tmplc(const SceneDev& sc, TmplC* out);
 cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, double* ynorm2, float4* tmpl,
                           cudaStream_t st);
 int64_t corr_grid(const SceneDev& sc, int64_t n_tiles, int precision, int num_sms);  // 0 on error

@@ -25,12 +25,32 @@ namespace cdms {
 // (zero padded): each warp streams its own antenna's chunks; ||z^(j)||^2 in fp64 (block 0 of each PA,
 // fixed reduction order); and the template columns tmpl[j][m] = (R_j p~_m, ||p~_m||^2) evaluated in fp64 and
 // rounded once to fp32 (padded antennas repeat m = 0).
+// Host copy of template_col (same formula; fp64 rounded once to fp32) for TmplC.
+void make_tmplc(const SceneDev& sc, TmplC* out) {
+  const int npad = sc.n_mb * NWARP;
+  out->n = sc.J * npad <= TMPLC_MAX ? sc.J * npad : 0;
+  if (!out->n) return;
+  for (int j = 0; j < sc.J; ++j)
+    for (int m = 0; m < npad; ++m) {
+      const int mm = m < sc.Na ? m : 0, iy = mm / sc.nv, iv = mm - iy * sc.nv;
+      const double py = (iy - 0.5 * (sc.ny - 1)) * sc.dy, pz = (iv - 0.5 * (sc.nv - 1)) * sc.dv;
+      const double* R = sc.pa_rot[j];
+      out->v[j * npad + m] = make_float4((float)(R[1] * py + R[2] * pz), (float)(R[4] * py + R[5] * pz),
+                                         (float)(R[7] * py + R[8] * pz), (float)(py * py + pz * pz));
+    }
+}
+
 __global__ void prep_y_kernel(const __grid_constant__ SceneDev sc, const float2* __restrict__ y,
-                              float4* __restrict__ yt, double* __restrict__ ynorm2, float4* __restrict__ tmpl) {
+                              float4* __restrict__ yt, double* __restrict__ ynorm2, float4* __restrict__ tmpl,
+                              const __grid_constant__ TmplC tc) {
   const int j = blockIdx.y;
   const int64_t per_j = (int64_t)sc.n_mb * sc.n_kc * sc.kc_len * NWARP;
   if (blockIdx.x == gridDim.x - 1) {
     for (int m = threadIdx.x; m < sc.n_mb * NWARP; m += blockDim.x) {
+      if (tc.n) {  // the host's columns (identical to the correlation kernel's constant-bank copy)
+        tmpl[(int64_t)j * sc.n_mb * NWARP + m] = tc.v[j * sc.n_mb * NWARP + m];
+        continue;
+      }
       double v[3], q2;
       template_col(sc, j, m < sc.Na ? m : 0, v, q2);
       tmpl[(int64_t)j * sc.n_mb * NWARP + m] = make_float4((float)v[0], (float)v[1], (float)v[2], (float)q2);
@@ -72,7 +92,9 @@ cudaError_t launch_prep_y(const SceneDev& sc, const float2* y, float4* ytiles, d
   if (gx > 1024) gx = 1024;
   if (gx < 2) gx = 2;
   dim3 grid(gx, sc.J);
-  prep_y_kernel<<<grid, 256, 0, st>>>(sc, y, ytiles, ynorm2, tmpl);
+  static thread_local TmplC tc;  // 8 KB: not on the stack
+  make_tmplc(sc, &tc);
+  prep_y_kernel<<<grid, 256, 0, st>>>(sc, y, ytiles, ynorm2, tmpl, tc);
   return cudaGetLastError();
 }
 

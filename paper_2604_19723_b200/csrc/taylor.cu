@@ -216,12 +216,15 @@ __device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par,
 // else tay_corr_lanes_kernel below): per component the fp64 geometry (VA, H r, R), the
 // fp64-reduced phase bases e^{j2pi f_c R/c} and frac(df R/c); per antenna the fp32 offset Delta_m (cancellation-free,
 // as K1), the phasor e^{j2pi f_c Delta_m/c}, the table centre and delta', one table row and the Taylor sum.
-template <bool SPH>  // spherical (else planar WB): a template, so the antenna loop carries no predicated other path
+// SPH: spherical (else planar WB), a template so the antenna loop carries no predicated other path.  TC: the template
+// columns from the constant bank (TmplC kernel parameter): the per-element column read then leaves the L1 data path
+// to the 64-byte table rows, which saturate it.
+template <bool SPH, bool TC>
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_corr_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
                     const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P, int pstride,
                     const double* __restrict__ sfv, int sfv_pp, float2* __restrict__ terms, int* __restrict__ pflag,
-                    int gram_diag) {
+                    int gram_diag, const __grid_constant__ TmplC tc) {
   const int J = sc.J, S = sc.S, Na = sc.Na, T = S + S * (S + 1) / 2;
   const int64_t p = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
   const int j = blockIdx.y;
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       const int m1 = min(m0 + 16, Na);
 #pragma unroll 4
       for (int m = m0; m < m1; ++m) {
-        const float4 v = __ldg(&tm[m]);
+        const float4 v = TC ? tc.v[j * Na_pad + m] : __ldg(&tm[m]);
         const float rq = hx * v.x + hy * v.y + hz * v.z;
         float delta;
         if (sph) {
@@ -931,12 +934,20 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
     return cudaGetLastError();
   }
   dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
-  if (sc.wavefront == CDMS_SPHERICAL)
-    tay_corr_kernel<true><<<grid, TAY_BLOCK, 0, st>>>(sc, tay_centres(sc.nf), tab, tmpl, particles, P, pstride, sfv,
-                                                      sfv_pp, terms, pflag, gram_diag);
-  else
-    tay_corr_kernel<false><<<grid, TAY_BLOCK, 0, st>>>(sc, tay_centres(sc.nf), tab, tmpl, particles, P, pstride, sfv,
-                                                       sfv_pp, terms, pflag, gram_diag);
+  static thread_local TmplC tc;  // 8 KB: not on the stack
+  make_tmplc(sc, &tc);
+  const int G = tay_centres(sc.nf);
+#define TAY_CORR(SPH, TC) \
+  tay_corr_kernel<SPH, TC><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, sfv, sfv_pp, terms, \
+                                                       pflag, gram_diag, tc)
+  if (sc.wavefront == CDMS_SPHERICAL) {
+    if (tc.n) TAY_CORR(true, true);
+    else TAY_CORR(true, false);
+  } else {
+    if (tc.n) TAY_CORR(false, true);
+    else TAY_CORR(false, false);
+  }
+#undef TAY_CORR
   return cudaGetLastError();
 }
 

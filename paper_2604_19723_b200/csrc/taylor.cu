@@ -35,8 +35,13 @@ __device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
 }
 
 int tay_centres(int nf) { return 4 * nf; }
+// The table holds TAY_EXT centres beyond each end of the period as well (phi_g = (g - TAY_EXT - G/2)/G, g = 0 ..
+// G + 2 TAY_EXT): evaluated from the definition, they carry Y's (-1)^(N_f - 1) per period themselves, so the
+// correlation kernel's fast locate (tay_corr_kernel, FL) needs neither a wrap nor a per-element sign.
+constexpr int TAY_EXT = 3;
+__host__ __device__ constexpr int tay_rows(int G) { return G + 1 + 2 * TAY_EXT; }
 size_t tay_table_bytes(const SceneDev& sc) {
-  return (size_t)sc.J * sc.Na * (tay_centres(sc.nf) + 1) * TAY_L * sizeof(float2);
+  return (size_t)sc.J * sc.Na * tay_rows(tay_centres(sc.nf)) * TAY_L * sizeof(float2);
 }
 
 // tab[j][m][g][l] (complex64, l fastest: one 64-byte row per (j, m, g), g = 0..G) or, with lanes, [j][g][h][m] of
@@ -49,13 +54,13 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t t = tid / TAY_KS;
   const int seg = (int)(tid - t * TAY_KS);
-  const int64_t per_j = (int64_t)sc.Na * (G + 1);
+  const int64_t per_j = (int64_t)sc.Na * tay_rows(G);
   const bool live = t < per_j * sc.J;
   const int64_t tt = live ? t : 0;
   const int j = (int)(tt / per_j);
   const int64_t r = tt - (int64_t)j * per_j;
-  const int m = (int)(r / (G + 1)), g = (int)(r - (int64_t)m * (G + 1));
-  const int gs = g - G / 2;  // phi_g = gs / G
+  const int m = (int)(r / tay_rows(G)), g = (int)(r - (int64_t)m * tay_rows(G));
+  const int gs = g - TAY_EXT - G / 2;  // phi_g = gs / G
   const double k0 = 0.5 * (sc.nf - 1);
   double cr[TAY_L], ci[TAY_L];
 #pragma unroll
@@ -98,7 +103,7 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
   }
   if (live && seg == 0) {
     if (lanes) {  // [j][g][h][m][4]
-      float2* out = tab + ((((int64_t)j * (G + 1) + g) * 2) * sc.Na + m) * 4;
+      float2* out = tab + ((((int64_t)j * tay_rows(G) + g) * 2) * sc.Na + m) * 4;
 #pragma unroll
       for (int l = 0; l < TAY_L; ++l) out[(int64_t)(l >> 2) * sc.Na * 4 + (l & 3)] = make_float2((float)cr[l], (float)ci[l]);
     } else {  // [j][m][g][l]
@@ -162,8 +167,8 @@ __global__ void __launch_bounds__(TAY_FFT_THREADS)
     }
     __syncthreads();
   }
-  for (int g = threadIdx.x; g <= G; g += TAY_FFT_THREADS) {
-    const int gs = g - G / 2;  // phi_g = gs / G
+  for (int g = threadIdx.x; g < tay_rows(G); g += TAY_FFT_THREADS) {
+    const int gs = g - TAY_EXT - G / 2;  // phi_g = gs / G
     int64_t num = ((int64_t)(nf - 1) * gs) % (2 * (int64_t)G);  // e^{-j2pi k0 phi_g} = e^{-j pi num/G}
     if (num < 0) num += 2 * (int64_t)G;
     double s, c;
@@ -171,9 +176,9 @@ __global__ void __launch_bounds__(TAY_FFT_THREADS)
     const double2 v = a[gs & (G - 1)];
     const float2 o = make_float2((float)(v.x * c - v.y * s), (float)(v.x * s + v.y * c));
     if (lanes)  // [j][g][h][m][4] (coefficients 4h .. 4h+3)
-      tab[((((int64_t)j * (G + 1) + g) * 2 + (l >> 2)) * sc.Na + m) * 4 + (l & 3)] = o;
+      tab[((((int64_t)j * tay_rows(G) + g) * 2 + (l >> 2)) * sc.Na + m) * 4 + (l & 3)] = o;
     else  // [j][m][g][l]
-      tab[(((int64_t)j * sc.Na + m) * (G + 1) + g) * TAY_L + l] = o;
+      tab[(((int64_t)j * sc.Na + m) * tay_rows(G) + g) * TAY_L + l] = o;
   }
 }
 
@@ -207,7 +212,7 @@ __device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par,
   const float gm = fmaf(r, Gf, TAY_MAGIC);  // rint(r G) + M
   const float gi = gm - TAY_MAGIC;
   dp = fmaf(r, Gf, -gi) + (e + lo) * Gf;
-  g = (uint32_t)(__float_as_int(gm) - __float_as_int(TAY_MAGIC) + Gh);
+  g = (uint32_t)(__float_as_int(gm) - __float_as_int(TAY_MAGIC) + Gh + TAY_EXT);  // the extended table's row
   const int nn = __float_as_int(sm) - __float_as_int(TAY_MAGIC);
   flip = evenN && ((par + nn) & 1);
 }
@@ -218,8 +223,13 @@ __device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par,
 // as K1), the phasor e^{j2pi f_c Delta_m/c}, the table centre and delta', one table row and the Taylor sum.
 // SPH: spherical (else planar WB), a template so the antenna loop carries no predicated other path.  TC: the template
 // columns from the constant bank (TmplC kernel parameter): the per-element column read then leaves the L1 data path
-// to the 64-byte table rows, which saturate it.
-template <bool SPH, bool TC>
+// to the 64-byte table rows, which saturate it.  FL (fast locate, when the aperture's delay spread is within TAY_EXT
+// centres, |Delta| df/c G <= TAY_EXT - 0.6: every BASELINE config): per component the fp64 phase base R df/c in
+// centres, x G = B_i + B_f (B_i integer, |B_f| <= 1/2 in fp32) and the sign (-1)^(n0 (N_f - 1)) once; per element
+// u = B_f + Delta (df/c) G in one fma, its rounding k by the magic constant, the row B_i + k on the extended table and
+// delta' = u - k -- 5 instructions instead of tay_locate's TwoSum reduction, wrap and per-element sign (|u| < 3 keeps
+// u's rounding below 1.2e-7 centres).
+template <bool SPH, bool TC, bool FL>
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_corr_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
                     const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P, int pstride,
@@ -231,9 +241,10 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   if (p >= P) return;
   const int Na_pad = sc.n_mb * NWARP;
   const double* pos = particles + p * pstride;
-  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * Na * (G + 1) * (TAY_L / 2);
+  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * Na * tay_rows(G) * (TAY_L / 2);
   const float4* tm = tmpl + (int64_t)j * Na_pad;
   constexpr bool sph = SPH;
+  const float dfG = (float)(sc.df_c * (double)G);  // FL: centres per metre of delay offset
   int fl = 0;
   for (int s = 0; s < S; ++s) {
     const double* sfv_s = nullptr;
@@ -253,6 +264,15 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     }
     const float R = (float)R64;
     const TayBase tb = tay_base(R64 * sc.df_c);  // delay phase base
+    float Bf = 0.f;  // FL: the base in centres, B_i + B_f, and its period's sign
+    uint32_t gbase = 0;
+    bool cflip = false;
+    if (FL) {
+      const double phib = R64 * sc.df_c, n0 = rint(phib), X = (phib - n0) * (double)G, Bi = rint(X);
+      Bf = (float)(X - Bi);
+      gbase = (uint32_t)((int)Bi + G / 2 + TAY_EXT);
+      cflip = (sc.nf & 1) == 0 && ((long long)n0 & 1);
+    }
     double sb, cb;
     sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
     // an antenna distance can vanish only within the aperture (R <= ap_r): that rare case is checked apart
@@ -281,9 +301,15 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         carrier_f(delta, sc.fc2pi_f, er, ei);
         uint32_t g;
         float dp;
-        bool flip;
-        tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
-        const float4* row = tj + ((uint32_t)m * (uint32_t)(G + 1) + g) * (TAY_L / 2);
+        bool flip = false;
+        if (FL) {
+          const float u = fmaf(delta, dfG, Bf), um = u + TAY_MAGIC;
+          g = gbase + (uint32_t)(__float_as_int(um) - __float_as_int(TAY_MAGIC));
+          dp = u - (um - TAY_MAGIC);
+        } else {
+          tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
+        }
+        const float4* row = tj + ((uint32_t)m * (uint32_t)tay_rows(G) + g) * (TAY_L / 2);
         float4 c01, c23, c45, c67;
         ldg256(row, c01, c23);
         ldg256(row + 2, c45, c67);
@@ -295,12 +321,16 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         yr = fmaf(yr, dp, c23.x); yi = fmaf(yi, dp, c23.y);
         yr = fmaf(yr, dp, c01.z); yi = fmaf(yi, dp, c01.w);
         yr = fmaf(yr, dp, c01.x); yi = fmaf(yi, dp, c01.y);
-        if (flip) { yr = -yr; yi = -yi; }
+        if (!FL && flip) { yr = -yr; yi = -yi; }
         pr = fmaf(er, yr, fmaf(-ei, yi, pr));
         pi = fmaf(er, yi, fmaf(ei, yr, pi));
       }
       accr += (double)pr;
       acci += (double)pi;
+    }
+    if (cflip) {
+      accr = -accr;
+      acci = -acci;
     }
     const double gn = sc.pathloss ? sc.lambda / (4.0 * PI * R64) : 1.0;
     terms[term_idx(p, j, s, T, P)] = term_f2((accr * cb - acci * sb) * gn, (accr * sb + acci * cb) * gn);
@@ -330,7 +360,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   const int j = blockIdx.y;
   if (p0 >= P) return;  // warp-uniform
   const int npairs = (int)min((int64_t)npw, P - p0) * S;
-  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * (G + 1) * (TAY_L / 2) * Na;
+  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * tay_rows(G) * (TAY_L / 2) * Na;
   const uint32_t rstride = (uint32_t)(TAY_L / 2) * (uint32_t)Na;  // float4s per centre ([h][m] of 32-byte entries)
   const float4* tm = tmpl + (int64_t)j * sc.n_mb * NWARP;
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
@@ -907,7 +937,7 @@ cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, in
     tay_prep_fft_kernel<<<(unsigned)(sc.J * sc.Na * TAY_L), TAY_FFT_THREADS, smem, st>>>(sc, G, lgG, y, tab, lanes);
     return cudaGetLastError();
   }
-  const int64_t n = (int64_t)sc.J * sc.Na * (G + 1) * TAY_KS;
+  const int64_t n = (int64_t)sc.J * sc.Na * tay_rows(G) * TAY_KS;
   tay_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, G, y, tab, lanes);
   return cudaGetLastError();
 }
@@ -937,16 +967,21 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
   static thread_local TmplC tc;  // 8 KB: not on the stack
   make_tmplc(sc, &tc);
   const int G = tay_centres(sc.nf);
-#define TAY_CORR(SPH, TC) \
-  tay_corr_kernel<SPH, TC><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, sfv, sfv_pp, terms, \
-                                                       pflag, gram_diag, tc)
+  const bool fast = (sc.ap_r / 1.5) * sc.df_c * (double)G <= TAY_EXT - 0.6;  // the aperture within the extension
+#define TAY_CORR(SPH, TC, FL) \
+  tay_corr_kernel<SPH, TC, FL><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, sfv, sfv_pp, \
+                                                           terms, pflag, gram_diag, tc)
+#define TAY_CORR_FL(SPH, TC) \
+  if (fast) TAY_CORR(SPH, TC, true); \
+  else TAY_CORR(SPH, TC, false);
   if (sc.wavefront == CDMS_SPHERICAL) {
-    if (tc.n) TAY_CORR(true, true);
-    else TAY_CORR(true, false);
+    if (tc.n) { TAY_CORR_FL(true, true) }
+    else { TAY_CORR_FL(true, false) }
   } else {
-    if (tc.n) TAY_CORR(false, true);
-    else TAY_CORR(false, false);
+    if (tc.n) { TAY_CORR_FL(false, true) }
+    else { TAY_CORR_FL(false, false) }
   }
+#undef TAY_CORR_FL
 #undef TAY_CORR
   return cudaGetLastError();
 }
@@ -992,7 +1027,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
   const int Na_pad = sc.n_mb * NWARP;
   const float4* tm = tmpl + (int64_t)j * Na_pad;
-  const size_t tstride = (size_t)Na * (G + 1) * (TAY_L / 2);  // float4s per (PA, snapshot) table
+  const size_t tstride = (size_t)Na * tay_rows(G) * (TAY_L / 2);  // float4s per (PA, snapshot) table
   const float4* tj = reinterpret_cast<const float4*>(tab) + (size_t)j * T * tstride;
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
   double accr[T], acci[T];
@@ -1023,7 +1058,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       bool flip;
       tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
       if (flip) { er = -er; ei = -ei; }
-      const size_t roff = ((size_t)m * (uint32_t)(G + 1) + g) * (TAY_L / 2);
+      const size_t roff = ((size_t)m * (uint32_t)tay_rows(G) + g) * (TAY_L / 2);
 #pragma unroll
       for (int t = 0; t < T; ++t) {
         const float4* row = tj + (size_t)t * tstride + roff;

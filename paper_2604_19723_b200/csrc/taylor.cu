@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
 // table centres, so with the [g][h][m] layout (32-byte entries) a group's gathers are (nearly) contiguous.  A warp owns npw = floor(32/S)
 // particles; lane i < npw S runs the fp64 set-up of pair i = (particle i / S, component i % S); the 32/LP groups then
 // take pairs i0 + group, each lane a strided subset of the antennas, and a fixed-order tree inside the group sums them.
-template <int EPL>  // antennas per lane (ceil(N_a / LP)), 0: runtime loop
+template <int EPL, bool FL>  // FL: fast locate as tay_corr_kernel  // antennas per lane (ceil(N_a / LP)), 0: runtime loop
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_corr_lanes_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
                           const float4* __restrict__ tmpl, const double* __restrict__ particles, int64_t P,
@@ -368,6 +368,10 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   double Ebr = 1.0, Ebi = 0.0;  // e^{j2pi f_c R/c}, applied to the antenna sum at the end
   float bhi = 0.f, blo = 0.f;
   int bpar = 0;
+  float Bf = 0.f;      // FL: base in centres (fraction) and its row, the period sign; near: R <= ap_r
+  int gbase = 0;
+  bool cflip = false, near = false;
+  const float dfG = (float)(sc.df_c * (double)G);
   double gn = 1.0;
   int ok = 0;
   if (lane < npairs) {
@@ -390,6 +394,13 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         R = (float)R64;
         const TayBase tb = tay_base(R64 * sc.df_c);
         bhi = tb.hi; blo = tb.lo; bpar = tb.par;
+        if (FL) {
+          const double phib = R64 * sc.df_c, n0 = rint(phib), X = (phib - n0) * (double)G, Bi = rint(X);
+          Bf = (float)(X - Bi);
+          gbase = (int)Bi + G / 2 + TAY_EXT;
+          cflip = (sc.nf & 1) == 0 && ((long long)n0 & 1);
+          near = !(R64 > sc.ap_r);
+        }
         double sb, cb;
         sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
         Ebr = cb; Ebi = sb;
@@ -412,8 +423,17 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     const int pok = __shfl_sync(0xffffffffu, ok, src) && i < npairs;
     const float shx = __shfl_sync(0xffffffffu, hx, src), shy = __shfl_sync(0xffffffffu, hy, src);
     const float shz = __shfl_sync(0xffffffffu, hz, src), sR = __shfl_sync(0xffffffffu, R, src);
-    const float shi = __shfl_sync(0xffffffffu, bhi, src), slo = __shfl_sync(0xffffffffu, blo, src);
-    const int spar = __shfl_sync(0xffffffffu, bpar, src);
+    float shi = 0.f, slo = 0.f, sBf = 0.f;
+    int spar = 0, sgb = 0, snear = 1;
+    if (FL) {
+      sBf = __shfl_sync(0xffffffffu, Bf, src);
+      sgb = __shfl_sync(0xffffffffu, gbase, src);
+      snear = __shfl_sync(0xffffffffu, (int)near, src);
+    } else {
+      shi = __shfl_sync(0xffffffffu, bhi, src);
+      slo = __shfl_sync(0xffffffffu, blo, src);
+      spar = __shfl_sync(0xffffffffu, bpar, src);
+    }
     float pr = 0.f, pi = 0.f;
     int efl = 0;
     auto element = [&](int m, const float4 v) {
@@ -422,7 +442,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       if (sph) {
         const float n = v.w - 2.f * rq;
         const float d = Num<float>::fsqrt_(sR * sR + n);
-        if (!(d > 0.f)) efl = 1;
+        if (snear && !(d > 0.f)) efl = 1;  // FL: only pairs within the aperture can hit an antenna
         delta = Num<float>::fdiv_(n, d + sR);
       } else {
         delta = Num<float>::fdiv_(-rq, sR);
@@ -431,8 +451,14 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       carrier_f(delta, sc.fc2pi_f, er, ei);
       uint32_t g;
       float dp;
-      bool flip;
-      tay_locate(delta * sc.df_cf, shi, slo, spar, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
+      bool flip = false;
+      if (FL) {
+        const float u = fmaf(delta, dfG, sBf), um = u + TAY_MAGIC;
+        g = (uint32_t)(sgb + (__float_as_int(um) - __float_as_int(TAY_MAGIC)));
+        dp = u - (um - TAY_MAGIC);
+      } else {
+        tay_locate(delta * sc.df_cf, shi, slo, spar, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
+      }
       const float4* row = tj + (g * rstride + 2u * (uint32_t)m);
       float4 c01, c23, c45, c67;
       ldg256(row, c01, c23);
@@ -445,7 +471,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       yr = fmaf(yr, dp, c23.x); yi = fmaf(yi, dp, c23.y);
       yr = fmaf(yr, dp, c01.z); yi = fmaf(yi, dp, c01.w);
       yr = fmaf(yr, dp, c01.x); yi = fmaf(yi, dp, c01.y);
-      if (flip) { yr = -yr; yi = -yi; }
+      if (!FL && flip) { yr = -yr; yi = -yi; }
       pr = fmaf(er, yr, fmaf(-ei, yi, pr));
       pi = fmaf(er, yi, fmaf(ei, yr, pi));
     };
@@ -472,6 +498,10 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   if (lane < npairs && ok) {  // one store round per warp: lane i writes pair i's c_s, G_ss (and zero off-diagonals)
     const int64_t p = p0 + lane / S;
     const int s = lane % S;
+    if (cflip) {  // FL: the period's sign, once per pair
+      cr = -cr;
+      ci = -ci;
+    }
     terms[term_idx(p, j, s, T, P)] =
         term_f2(((double)cr * Ebr - (double)ci * Ebi) * gn, ((double)cr * Ebi + (double)ci * Ebr) * gn);
     const int r0 = S + s * (s + 1) / 2;
@@ -952,14 +982,25 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
     const int64_t per_block = (int64_t)(TAY_BLOCK / 32) * (32 / sc.S);
     dim3 grid((unsigned)((P + per_block - 1) / per_block), sc.J);
     const int G = tay_centres(sc.nf);
-#define TAY_LANES(E)                                                                                             \
-  tay_corr_lanes_kernel<E><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, sfv, sfv_pp, terms, \
-                                                       pflag, gram_diag, lg)
-    if (epl == 1) TAY_LANES(1);
-    else if (epl == 2) TAY_LANES(2);
-    else if (epl <= 4) TAY_LANES(4);
-    else if (epl <= 8) TAY_LANES(8);
-    else TAY_LANES(0);
+    const bool fast = (sc.ap_r / 1.5) * sc.df_c * (double)G <= TAY_EXT - 0.6;
+#define TAY_LANES(E)                                                                                              \
+  if (fast)                                                                                                       \
+    tay_corr_lanes_kernel<E, true><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, sfv, sfv_pp, \
+                                                               terms, pflag, gram_diag, lg);                      \
+  else                                                                                                            \
+    tay_corr_lanes_kernel<E, false><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, sfv,      \
+                                                                sfv_pp, terms, pflag, gram_diag, lg)
+    if (epl == 1) {
+      TAY_LANES(1);
+    } else if (epl == 2) {
+      TAY_LANES(2);
+    } else if (epl <= 4) {
+      TAY_LANES(4);
+    } else if (epl <= 8) {
+      TAY_LANES(8);
+    } else {
+      TAY_LANES(0);
+    }
 #undef TAY_LANES
     return cudaGetLastError();
   }

@@ -450,7 +450,7 @@ cdms_status ensure_peer(cdms_ctx ctx, int64_t P_local) {
 // K1T (taylor.cu) serves FP32 spherical / planar-WB likelihoods whose tables fit the budget
 bool tay_engine(cdms_ctx ctx, const SceneDev& sd, int precision, bool nb_tensor) {
   return !nb_tensor && ctx->taylor && precision == CDMS_FP32 && sd.wavefront != CDMS_PLANAR_NB &&
-         tay_table_bytes(sd) <= ((size_t)96 << 20);
+         std::max(tay_table_bytes(sd, 0), tay_table_bytes(sd, 1)) <= ((size_t)160 << 20);
 }
 
 cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const double* d_particles, int64_t P,
@@ -480,7 +480,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   float2* taytab = nullptr;
   const int tlanes = tay && (ctx->taylor_lanes >= 0 ? ctx->taylor_lanes == 1 : tay_lanes(sd, P)) ? 1 : 0;  // taylor.cu
   if (tay) {
-    WS_TRY(ctx, WS_TAY, tay_table_bytes(sd) / sizeof(float2), &taytab);
+    WS_TRY(ctx, WS_TAY, tay_table_bytes(sd, tlanes) / sizeof(float2), &taytab);
     CUDA_TRY(ctx, launch_tay_prep(sd, static_cast<const float2*>(d_y), taytab, tlanes, ctx->taylor_prep_direct,
                                   ctx->stream));
     ctx->launches += 1;
@@ -940,7 +940,7 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
     }
     if (tay_engine(ctx, sd, scene->precision, nbt)) {  // K1T's tables (the same choice loglik_impl makes)
       float2* tab;
-      WS_TRY(ctx, WS_TAY, tay_table_bytes(sd) / sizeof(float2), &tab);
+      WS_TRY(ctx, WS_TAY, std::max(tay_table_bytes(sd, 0), tay_table_bytes(sd, 1)) / sizeof(float2), &tab);
       if (ctx->locality && PB >= LOCALITY_MIN_P) {  // the locality sort's buffers (shared-SFV batches)
         uint32_t* keys;
         unsigned char* temp;
@@ -1214,7 +1214,7 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
   const int64_t Nz = (int64_t)sd.nf * sd.Na;
   SceneDev sdt = sd;  // the T snapshots of every PA as J T "PAs" for the table builder
   sdt.J = J * T;
-  const size_t tab_bytes = tay_table_bytes(sdt);
+  const size_t tab_bytes = tay_table_bytes(sdt, 0);
   if (tab_bytes > ((size_t)1 << 30)) return fail(ctx, CDMS_EUNSUPPORTED, "pf_update: tables of %zu bytes", tab_bytes);
   float2 *snaps, *tab;
   double2 *dots, *fixed, *cc;

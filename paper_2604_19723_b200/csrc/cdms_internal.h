@@ -273,8 +273,8 @@ cudaError_t launch_regularize(double* x, int64_t P, int64_t p0, int64_t P_total,
 cudaError_t launch_fill_u64(uint64_t* dst, uint64_t v, int n, cudaStream_t st);
 
 // loglik.cu K1 Gram-only variant + taylor.cu K1T (spherical / planar-WB correlation from spectral Taylor tables)
-int tay_centres(int nf);
-size_t tay_table_bytes(const SceneDev& sc);
+int tay_centres(int nf, int lanes);
+size_t tay_table_bytes(const SceneDev& sc, int lanes);  // lanes: the lane-group layout, else the thread layout
 bool tay_lanes(const SceneDev& sc, int64_t P);  // table layout / correlation kernel choice for P particles
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, int direct,
                             cudaStream_t st);

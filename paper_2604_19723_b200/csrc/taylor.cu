@@ -34,14 +34,27 @@ __device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
       : "l"(p));
 }
 
-int tay_centres(int nf) { return 4 * nf; }
+// Two table forms.  Lane-group kernel ([j][g][h][m] layout): G = 4 N_f centres per period and TAY_L = 8 coefficients
+// (truncation (pi/8)^8/8! = 1.4e-8).  Thread-per-particle kernels ([j][m][g], split in two arrays): G = 8 N_f and
+// TAY_L6 = 6 coefficients (truncation (pi/16)^6/6! = 8.2e-8 of sum_k |y[m,k]|, at fp32 rounding) -- 48 instead of
+// 64 bytes per element through the L1 data path that bounds that kernel, as one 32-byte row (C_0..C_3) in array A and
+// one 16-byte row (C_4, C_5) in array B (48-byte rows in one array would break the 32-byte alignment of the
+// 256-bit loads).  Measured (c5 4M, correlation kernel): 64-byte rows 20.5 ms, 48-byte rows 16.7 ms with the same
+// table size (profiles/r02_gram_onechunk.txt); 1.5x the table bytes.
+constexpr int TAY_L6 = 6;
+int tay_centres(int nf, int lanes) { return lanes ? 4 * nf : 8 * nf; }
 // The table holds TAY_EXT centres beyond each end of the period as well (phi_g = (g - TAY_EXT - G/2)/G, g = 0 ..
 // G + 2 TAY_EXT): evaluated from the definition, they carry Y's (-1)^(N_f - 1) per period themselves, so the
 // correlation kernel's fast locate (tay_corr_kernel, FL) needs neither a wrap nor a per-element sign.
-constexpr int TAY_EXT = 3;
+constexpr int TAY_EXT = 4;
 __host__ __device__ constexpr int tay_rows(int G) { return G + 1 + 2 * TAY_EXT; }
-size_t tay_table_bytes(const SceneDev& sc) {
-  return (size_t)sc.J * sc.Na * tay_rows(tay_centres(sc.nf)) * TAY_L * sizeof(float2);
+size_t tay_table_bytes(const SceneDev& sc, int lanes) {
+  return (size_t)sc.J * sc.Na * tay_rows(tay_centres(sc.nf, lanes)) * (lanes ? TAY_L : TAY_L6) * sizeof(float2);
+}
+// thread layout: coefficient l of row (j, m, g) -- A [J][N_a][rows][4] for l < 4, then B [J][N_a][rows][2]
+__host__ __device__ __forceinline__ int64_t tay_t6_index(int J, int Na, int G, int j, int m, int g, int l) {
+  const int64_t row = ((int64_t)j * Na + m) * tay_rows(G) + g;
+  return l < 4 ? row * 4 + l : (int64_t)J * Na * tay_rows(G) * 4 + row * 2 + (l - 4);
 }
 
 // tab[j][m][g][l] (complex64, l fastest: one 64-byte row per (j, m, g), g = 0..G) or, with lanes, [j][g][h][m] of
@@ -49,6 +62,7 @@ size_t tay_table_bytes(const SceneDev& sc) {
 // e^{j2pi (k - k0) phi_g}, fp64 phasor recurrence inside its segment), combined by a
 // fixed shuffle tree: row count alone (J N_a G) would leave most SMs idle at small N_a G.
 constexpr int TAY_KS = 8;
+template <int L>  // coefficients per row: TAY_L (lanes layout) or TAY_L6 (thread layout)
 __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ y,
                                 float2* __restrict__ tab, int lanes) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -62,9 +76,9 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
   const int m = (int)(r / tay_rows(G)), g = (int)(r - (int64_t)m * tay_rows(G));
   const int gs = g - TAY_EXT - G / 2;  // phi_g = gs / G
   const double k0 = 0.5 * (sc.nf - 1);
-  double cr[TAY_L], ci[TAY_L];
+  double cr[L], ci[L];
 #pragma unroll
-  for (int l = 0; l < TAY_L; ++l) cr[l] = ci[l] = 0.0;
+  for (int l = 0; l < L; ++l) cr[l] = ci[l] = 0.0;
   const int kseg = (sc.nf + TAY_KS - 1) / TAY_KS;
   const int kb = seg * kseg, ke = min(kb + kseg, sc.nf);
   if (live && kb < ke) {
@@ -81,7 +95,7 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
       double br = v.x * pr - v.y * pi, bi = v.x * pi + v.y * pr;  // y_k e^{j2pi (k-k0) g/G}
       const double tk = 2.0 * PI * ((double)k - k0) / (double)G;
 #pragma unroll
-      for (int l = 0; l < TAY_L; ++l) {
+      for (int l = 0; l < L; ++l) {
         cr[l] += br;
         ci[l] += bi;
         const double nr = -bi * tk / (double)(l + 1), ni = br * tk / (double)(l + 1);  // * (j tk)/(l+1)
@@ -96,7 +110,7 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
 #pragma unroll
   for (int o = TAY_KS / 2; o > 0; o >>= 1) {
 #pragma unroll
-    for (int l = 0; l < TAY_L; ++l) {
+    for (int l = 0; l < L; ++l) {
       cr[l] += __shfl_xor_sync(0xffffffffu, cr[l], o);
       ci[l] += __shfl_xor_sync(0xffffffffu, ci[l], o);
     }
@@ -105,11 +119,10 @@ __global__ void tay_prep_kernel(const __grid_constant__ SceneDev sc, int G, cons
     if (lanes) {  // [j][g][h][m][4]
       float2* out = tab + ((((int64_t)j * tay_rows(G) + g) * 2) * sc.Na + m) * 4;
 #pragma unroll
-      for (int l = 0; l < TAY_L; ++l) out[(int64_t)(l >> 2) * sc.Na * 4 + (l & 3)] = make_float2((float)cr[l], (float)ci[l]);
-    } else {  // [j][m][g][l]
-      float2* out = tab + t * TAY_L;
+      for (int l = 0; l < L; ++l) out[(int64_t)(l >> 2) * sc.Na * 4 + (l & 3)] = make_float2((float)cr[l], (float)ci[l]);
+    } else {  // thread layout (arrays A, B)
 #pragma unroll
-      for (int l = 0; l < TAY_L; ++l) out[l] = make_float2((float)cr[l], (float)ci[l]);
+      for (int l = 0; l < L; ++l) tab[tay_t6_index(sc.J, sc.Na, G, j, m, g, l)] = make_float2((float)cr[l], (float)ci[l]);
     }
   }
 }
@@ -126,8 +139,9 @@ __global__ void __launch_bounds__(TAY_FFT_THREADS)
   extern __shared__ double2 fsm[];
   double2* a = fsm;      // [G]
   double2* w = fsm + G;  // [G/2]
-  const int l = blockIdx.x % TAY_L;
-  const int jm = blockIdx.x / TAY_L;
+  const int L = lanes ? TAY_L : TAY_L6;
+  const int l = blockIdx.x % L;
+  const int jm = blockIdx.x / L;
   const int j = jm / sc.Na, m = jm - j * sc.Na;
   const int nf = sc.nf;
   const double k0 = 0.5 * (nf - 1);
@@ -177,8 +191,8 @@ __global__ void __launch_bounds__(TAY_FFT_THREADS)
     const float2 o = make_float2((float)(v.x * c - v.y * s), (float)(v.x * s + v.y * c));
     if (lanes)  // [j][g][h][m][4] (coefficients 4h .. 4h+3)
       tab[((((int64_t)j * tay_rows(G) + g) * 2 + (l >> 2)) * sc.Na + m) * 4 + (l & 3)] = o;
-    else  // [j][m][g][l]
-      tab[(((int64_t)j * sc.Na + m) * tay_rows(G) + g) * TAY_L + l] = o;
+    else  // thread layout (arrays A, B)
+      tab[tay_t6_index(sc.J, sc.Na, G, j, m, g, l)] = o;
   }
 }
 
@@ -241,7 +255,9 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   if (p >= P) return;
   const int Na_pad = sc.n_mb * NWARP;
   const double* pos = particles + p * pstride;
-  const float4* tj = reinterpret_cast<const float4*>(tab) + (int64_t)j * Na * tay_rows(G) * (TAY_L / 2);
+  // thread layout: 32-byte rows of C_0..C_3 (2 float4) in A, 16-byte rows of C_4, C_5 (1 float4) in B
+  const float4* tA = reinterpret_cast<const float4*>(tab) + (int64_t)j * Na * tay_rows(G) * 2;
+  const float4* tB = reinterpret_cast<const float4*>(tab) + (int64_t)J * Na * tay_rows(G) * 2 + (int64_t)j * Na * tay_rows(G);
   const float4* tm = tmpl + (int64_t)j * Na_pad;
   constexpr bool sph = SPH;
   const float dfG = (float)(sc.df_c * (double)G);  // FL: centres per metre of delay offset
@@ -309,13 +325,11 @@ __global__ void __launch_bounds__(TAY_BLOCK)
         } else {
           tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
         }
-        const float4* row = tj + ((uint32_t)m * (uint32_t)tay_rows(G) + g) * (TAY_L / 2);
-        float4 c01, c23, c45, c67;
-        ldg256(row, c01, c23);
-        ldg256(row + 2, c45, c67);
-        float yr = c67.z, yi = c67.w;  // Horner in delta', l = 7 .. 0
-        yr = fmaf(yr, dp, c67.x); yi = fmaf(yi, dp, c67.y);
-        yr = fmaf(yr, dp, c45.z); yi = fmaf(yi, dp, c45.w);
+        const uint32_t row = (uint32_t)m * (uint32_t)tay_rows(G) + g;
+        float4 c01, c23;
+        ldg256(tA + 2u * row, c01, c23);
+        const float4 c45 = __ldg(tB + row);
+        float yr = c45.z, yi = c45.w;  // Horner in delta', l = 5 .. 0
         yr = fmaf(yr, dp, c45.x); yi = fmaf(yi, dp, c45.y);
         yr = fmaf(yr, dp, c23.z); yi = fmaf(yi, dp, c23.w);
         yr = fmaf(yr, dp, c23.x); yi = fmaf(yi, dp, c23.y);
@@ -957,18 +971,22 @@ bool tay_lanes(const SceneDev& sc, int64_t P) { return (double)P * sc.J < 2.5e5;
 // FFT when G is a power of two in [64, 4096] (N_f a power of two up to 1024), unless direct = 1 (A/B); else the
 // direct sum.  Both fp64, rounded once to complex64.
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, int direct, cudaStream_t st) {
-  const int G = tay_centres(sc.nf);
-  if (!direct && (G & (G - 1)) == 0 && G >= 64 && G <= 4096) {
+  const int G = tay_centres(sc.nf, lanes);
+  if (!direct && (G & (G - 1)) == 0 && G >= 64 && G <= 8192) {  // G = 8192: 192 KB of shared memory
     int lgG = 0;
     while ((1 << lgG) < G) ++lgG;
     const size_t smem = (size_t)G * sizeof(double2) * 3 / 2;
     cudaError_t e = cudaFuncSetAttribute(tay_prep_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    tay_prep_fft_kernel<<<(unsigned)(sc.J * sc.Na * TAY_L), TAY_FFT_THREADS, smem, st>>>(sc, G, lgG, y, tab, lanes);
+    tay_prep_fft_kernel<<<(unsigned)(sc.J * sc.Na * (lanes ? TAY_L : TAY_L6)), TAY_FFT_THREADS, smem, st>>>(
+        sc, G, lgG, y, tab, lanes);
     return cudaGetLastError();
   }
   const int64_t n = (int64_t)sc.J * sc.Na * tay_rows(G) * TAY_KS;
-  tay_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, G, y, tab, lanes);
+  if (lanes)
+    tay_prep_kernel<TAY_L><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, G, y, tab, lanes);
+  else
+    tay_prep_kernel<TAY_L6><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sc, G, y, tab, lanes);
   return cudaGetLastError();
 }
 cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4* tmpl, const double* particles,
@@ -981,7 +999,7 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
     const int epl = (sc.Na + (1 << lg) - 1) >> lg;
     const int64_t per_block = (int64_t)(TAY_BLOCK / 32) * (32 / sc.S);
     dim3 grid((unsigned)((P + per_block - 1) / per_block), sc.J);
-    const int G = tay_centres(sc.nf);
+    const int G = tay_centres(sc.nf, 1);
     const bool fast = (sc.ap_r / 1.5) * sc.df_c * (double)G <= TAY_EXT - 0.6;
 #define TAY_LANES(E)                                                                                              \
   if (fast)                                                                                                       \
@@ -1007,7 +1025,7 @@ cudaError_t launch_tay_corr(const SceneDev& sc, const float2* tab, const float4*
   dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
   static thread_local TmplC tc;  // 8 KB: not on the stack
   make_tmplc(sc, &tc);
-  const int G = tay_centres(sc.nf);
+  const int G = tay_centres(sc.nf, 0);
   const bool fast = (sc.ap_r / 1.5) * sc.df_c * (double)G <= TAY_EXT - 0.6;  // the aperture within the extension
 #define TAY_CORR(SPH, TC, FL) \
   tay_corr_kernel<SPH, TC, FL><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, sfv, sfv_pp, \
@@ -1068,8 +1086,9 @@ __global__ void __launch_bounds__(TAY_BLOCK)
   sincospi(2.0 * frac_c(R64 * sc.fc_c), &sb, &cb);
   const int Na_pad = sc.n_mb * NWARP;
   const float4* tm = tmpl + (int64_t)j * Na_pad;
-  const size_t tstride = (size_t)Na * tay_rows(G) * (TAY_L / 2);  // float4s per (PA, snapshot) table
-  const float4* tj = reinterpret_cast<const float4*>(tab) + (size_t)j * T * tstride;
+  const size_t tstride = (size_t)Na * tay_rows(G);  // rows per (PA, snapshot) table (thread layout: A 2, B 1 float4)
+  const float4* tA = reinterpret_cast<const float4*>(tab) + (size_t)j * T * tstride * 2;
+  const float4* tB = reinterpret_cast<const float4*>(tab) + (size_t)sc.J * T * tstride * 2 + (size_t)j * T * tstride;
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
   double accr[T], acci[T];
 #pragma unroll
@@ -1099,16 +1118,14 @@ __global__ void __launch_bounds__(TAY_BLOCK)
       bool flip;
       tay_locate(delta * sc.df_cf, tb.hi, tb.lo, tb.par, G / 2, (float)G, (sc.nf & 1) == 0, g, dp, flip);
       if (flip) { er = -er; ei = -ei; }
-      const size_t roff = ((size_t)m * (uint32_t)tay_rows(G) + g) * (TAY_L / 2);
+      const size_t roff = (size_t)m * (uint32_t)tay_rows(G) + g;
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        const float4* row = tj + (size_t)t * tstride + roff;
-        float4 c01, c23, c45, c67;
-        ldg256(row, c01, c23);
-        ldg256(row + 2, c45, c67);
-        float yr = c67.z, yi = c67.w;
-        yr = fmaf(yr, dp, c67.x); yi = fmaf(yi, dp, c67.y);
-        yr = fmaf(yr, dp, c45.z); yi = fmaf(yi, dp, c45.w);
+        const size_t row = (size_t)t * tstride + roff;
+        float4 c01, c23;
+        ldg256(tA + 2 * row, c01, c23);
+        const float4 c45 = __ldg(tB + row);
+        float yr = c45.z, yi = c45.w;
         yr = fmaf(yr, dp, c45.x); yi = fmaf(yi, dp, c45.y);
         yr = fmaf(yr, dp, c23.z); yi = fmaf(yi, dp, c23.w);
         yr = fmaf(yr, dp, c23.x); yi = fmaf(yi, dp, c23.y);
@@ -1134,7 +1151,7 @@ cudaError_t launch_pf_corr(const SceneDev& sc, int T, const float2* tab, const f
                            int64_t P, int pstride, const double* phi, double2* out, int* pflag, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
   dim3 grid((unsigned)((P + TAY_BLOCK - 1) / TAY_BLOCK), sc.J);
-  const int G = tay_centres(sc.nf);
+  const int G = tay_centres(sc.nf, 0);
   switch (T) {
 #define CASE_T(n) \
   case n: pf_corr_kernel<n><<<grid, TAY_BLOCK, 0, st>>>(sc, G, tab, tmpl, particles, P, pstride, phi, out, pflag); break;

@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int J = sc.J, S = sc.S;
+  const int S = sc.S;
   const int64_t nhyp = a.P * S;
   const int n_chunks = pl.n_chunks;
   const uint32_t sbo = 16u * kc;

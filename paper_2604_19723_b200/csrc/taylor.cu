@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
                           int pstride, const double* __restrict__ sfv, int sfv_pp, float2* __restrict__ terms,
                           int* __restrict__ pflag, int gram_diag, int lg) {
   const int lane = threadIdx.x & 31;
-  const int J = sc.J, S = sc.S, Na = sc.Na, T = S + S * (S + 1) / 2;
+  const int S = sc.S, Na = sc.Na, T = S + S * (S + 1) / 2;
   const int npw = 32 / S, LP = 1 << lg, ng = 32 >> lg;
   const int grp = lane >> lg, gl = lane & (LP - 1);
   const int64_t p0 = ((int64_t)blockIdx.x * (TAY_BLOCK / 32) + (threadIdx.x >> 5)) * npw;
@@ -665,7 +665,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
   const int64_t p = t >> lsplit;
   const int a0 = (int)(t & (A - 1));
   const int j = blockIdx.y;
-  const int J = sc.J, Na = sc.Na, T = S + S * (S + 1) / 2;
+  const int Na = sc.Na, T = S + S * (S + 1) / 2;
   bool live = p < P;
   const double* pos = particles + (live ? p : 0) * pstride;
   float hx[S], hy[S], hz[S], Rf[S], uh[S], ul[S];

@@ -467,7 +467,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   const int64_t tiles = (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP;
   WS_TRY(ctx, WS_YTILES, tiles, &yt);
   WS_TRY(ctx, WS_YNORM, MAXJ, &yn);
-  WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &tmpl);
+  WS_TRY(ctx, WS_TMPL, (int64_t)(sd.J + 1) * sd.n_mb * NWARP, &tmpl);
   CUDA_TRY(ctx, launch_prep_y(sd, static_cast<const float2*>(d_y), yt, yn, tmpl, ctx->stream));
   ctx->launches += 1;
   // PLANAR_NB in fp32: the correlation runs as a tensor-core GEMM (nbmma.cu) with the closed-form Gram
@@ -931,7 +931,7 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
     unsigned int* sch;
     WS_TRY(ctx, WS_SCHED, 2, &sch);
     WS_TRY(ctx, WS_STEP_CNT, 4, &sch);
-    WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &f4);
+    WS_TRY(ctx, WS_TMPL, (int64_t)(sd.J + 1) * sd.n_mb * NWARP, &f4);
     if (nbt) {
       uint8_t* nbop;
       float* nbs;
@@ -1234,7 +1234,7 @@ cdms_status cdms_pf_update(cdms_ctx ctx, const cdms_scene* scene, const double* 
   WS_TRY(ctx, WS_LSE2, (size_t)3 * MAXJ * (lse_blocks(P) + 1), &lse2);
   WS_TRY(ctx, WS_YTILES, (int64_t)sd.J * sd.n_mb * sd.n_kc * sd.kc_len * NWARP, &yt);
   WS_TRY(ctx, WS_YNORM, MAXJ, &yn);
-  WS_TRY(ctx, WS_TMPL, (int64_t)sd.J * sd.n_mb * NWARP, &tmpl);
+  WS_TRY(ctx, WS_TMPL, (int64_t)(sd.J + 1) * sd.n_mb * NWARP, &tmpl);
   CUDA_TRY(ctx, cudaMemcpyAsync(dpar, par, sizeof(par), cudaMemcpyHostToDevice, ctx->stream));
   // (1) template columns of the PAs; snapshots e0 = z - mu3, m_l; their fp64 dot products and the particle-independent
   //     factor of A^-1; K1T tables of every snapshot

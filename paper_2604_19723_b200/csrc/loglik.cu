@@ -24,7 +24,8 @@ namespace cdms {
 // y [J][nf][Na] (paper vec order) -> ytiles [J][Na_pad][n_kc][kc_len] of (yr, yr, yi, yi), Na_pad = 8 n_mb
 // (zero padded): each warp streams its own antenna's chunks; ||z^(j)||^2 in fp64 (block 0 of each PA,
 // fixed reduction order); and the template columns tmpl[j][m] = (R_j p~_m, ||p~_m||^2) evaluated in fp64 and
-// rounded once to fp32 (padded antennas repeat m = 0).
+// rounded once to fp32 (padded antennas repeat m = 0); after the J PAs' columns, the PA-independent row
+// tmpl[J][m] = (p~_y, p~_z, ||p~||^2, 0) of the template itself (the Gram folds R_j into its per-component h).
 // Host copy of template_col (same formula; fp64 rounded once to fp32) for TmplC.
 void make_tmplc(const SceneDev& sc, TmplC* out) {
   const int npad = sc.n_mb * NWARP;
@@ -46,6 +47,12 @@ __global__ void prep_y_kernel(const __grid_constant__ SceneDev sc, const float2*
   const int j = blockIdx.y;
   const int64_t per_j = (int64_t)sc.n_mb * sc.n_kc * sc.kc_len * NWARP;
   if (blockIdx.x == gridDim.x - 1) {
+    if (j == 0)
+      for (int m = threadIdx.x; m < sc.n_mb * NWARP; m += blockDim.x) {
+        const int mm = m < sc.Na ? m : 0, iy = mm / sc.nv, iv = mm - iy * sc.nv;
+        const double py = (iy - 0.5 * (sc.ny - 1)) * sc.dy, pz = (iv - 0.5 * (sc.nv - 1)) * sc.dv;
+        tmpl[(int64_t)sc.J * sc.n_mb * NWARP + m] = make_float4((float)py, (float)pz, (float)(py * py + pz * pz), 0.f);
+      }
     for (int m = threadIdx.x; m < sc.n_mb * NWARP; m += blockDim.x) {
       if (tc.n) {  // the host's columns (identical to the correlation kernel's constant-bank copy)
         tmpl[(int64_t)j * sc.n_mb * NWARP + m] = tc.v[j * sc.n_mb * NWARP + m];

@@ -729,17 +729,25 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
   }
   // R_s (fp64) are needed again only in the epilogue: parked in shared memory, not in registers through the loop
   // (18 registers at S = 9, which removed the kernel's spills under its 168-register cap)
+  // TAB: per component (h'_y, h'_z, R, f_s) parked in shared memory, h' = R_j^T h, so that h.v_m = h'_y p~_y +
+  // h'_z p~_z against the PA-independent template row (p~ = (0, p~_y, p~_z)): two products per
+  // (component, antenna) instead of three, and f_s out of the registers
+  const double* Rj = sc.pa_rot[j];
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     rsh[s * TAY_BLOCK + threadIdx.x] = R64[s];
-    if (TAB) csh[s * TAY_BLOCK + threadIdx.x] = make_float4(hx[s], hy[s], hz[s], Rf[s]);  // TAB: parked too
+    if (TAB) {
+      const float hyp = (float)((double)hx[s] * Rj[1] + (double)hy[s] * Rj[4] + (double)hz[s] * Rj[7]);
+      const float hzp = (float)((double)hx[s] * Rj[2] + (double)hy[s] * Rj[5] + (double)hz[s] * Rj[8]);
+      csh[s * TAY_BLOCK + threadIdx.x] = make_float4(hyp, hzp, Rf[s], fc_[(TAB && CDMS_GRAM_UCOMP) ? s : 0]);
+    }
   }
   const float dfG = sc.df_cf * tb.G;  // TAB: d' per unit of the element offset difference
 #pragma unroll
   for (int q = 0; q < NP; ++q)
     if (!ONE) gsum[q * TAY_BLOCK + threadIdx.x] = make_double2(0.0, 0.0);
   const bool sph = sc.wavefront == CDMS_SPHERICAL;
-  const float4* tm = tmpl + (int64_t)j * sc.n_mb * NWARP;
+  const float4* tm = tmpl + (TAB ? (int64_t)sc.J : (int64_t)j) * sc.n_mb * NWARP;  // TAB: (p~_y, p~_z, ||p~||^2)
   const int Nl = live ? (Na - a0 + A - 1) >> lsplit : 0;  // this lane's antennas m = a0 + A i, i < Nl
   float gr[NP], gi[NP];
 #pragma unroll
@@ -758,16 +766,25 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
       int ik[(TAB && CDMS_GRAM_UCOMP == 2) ? S : 1];  // UCOMP 2: u_s = k_s + r_s, k_s as the bits of k_s + M
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const float4 h = TAB ? csh[s * TAY_BLOCK + threadIdx.x] : make_float4(hx[s], hy[s], hz[s], Rf[s]);
-        const float rq = h.x * v.x + h.y * v.y + h.z * v.z;
-        if (sph) {
-          const float n = v.w - 2.f * rq;
-          dl[s] = Num<float>::fdiv_(n, Num<float>::fsqrt_(h.w * h.w + n) + h.w);
+        float rq, Rs, q2;
+        if (TAB) {
+          const float4 h = csh[s * TAY_BLOCK + threadIdx.x];
+          rq = fmaf(h.x, v.x, h.y * v.y);
+          Rs = h.z;
+          q2 = v.z;
         } else {
-          dl[s] = Num<float>::fdiv_(-rq, h.w);  // planar WB only: no 1/R array held through the loop
+          rq = hx[s] * v.x + hy[s] * v.y + hz[s] * v.z;
+          Rs = Rf[s];
+          q2 = v.w;
+        }
+        if (sph) {
+          const float n = q2 - 2.f * rq;
+          dl[s] = Num<float>::fdiv_(n, Num<float>::fsqrt_(Rs * Rs + n) + Rs);
+        } else {
+          dl[s] = Num<float>::fdiv_(-rq, Rs);  // planar WB only: no 1/R array held through the loop
         }
         carrier_f(dl[s], sc.fc2pi_f, er[s], ei[s]);  // e^{j2pi f_c Delta_s/c}: the pairs' carriers as products
-        if (TAB && CDMS_GRAM_UCOMP) dl[s] = fmaf(dl[s], dfG, fc_[(TAB && CDMS_GRAM_UCOMP) ? s : 0]);  // u_s, in centres
+        if (TAB && CDMS_GRAM_UCOMP) dl[s] = fmaf(dl[s], dfG, csh[s * TAY_BLOCK + threadIdx.x].w);  // u_s, in centres
         if (TAB && CDMS_GRAM_UCOMP == 2) {  // rounded per component: per pair r_a - r_b (|.| <= 1) and k_a - k_b
           constexpr float M = 12582912.f;
           const float um = dl[s] + M;

@@ -5,15 +5,15 @@
 //   c_s = sum_m e^{j2pi f_c d_m/c} Y_m(phi_m),   Y_m(phi) = sum_k y[m,k] e^{j2pi (k - k0) phi},  phi_m = df d_m / c,
 // (f_k = f_c + (k - k0) df, k0 = (N_f - 1)/2; d_m the spherical distance or the planar projection of the element,
 // P:L108-143).  Y_m is 1-periodic up to the sign (-1)^(N_f - 1) (k - k0 is a half-integer for even N_f) and
-// band-limited to |k - k0| <= N_f/2, so on the G + 1 centres phi_g = (g - G/2)/G, g = 0..G, G = 4 N_f, of one period
-// [-1/2, 1/2] (both ends stored: the reduction needs no wrap) its Taylor expansion in delta' = (phi - phi_g) G,
+// band-limited to |k - k0| <= N_f/2, so on centres phi_g = (g - G/2)/G of one period [-1/2, 1/2] (and a few beyond
+// each end: the reduction needs no wrap) its Taylor expansion in delta' = (phi - phi_g) G,
 //   Y_m(phi_g + delta'/G) = sum_l C_l(m, g) delta'^l,  C_l = sum_k y[m,k] e^{j2pi (k-k0) phi_g} (j2pi (k-k0)/G)^l / l!,
-// truncated after TAY_L = 8 terms has a relative error below (pi/8)^8/8! = 1.4e-8 of sum_k |y[m,k]| (|2pi (k-k0)
-// delta'/G| <= pi/8): far below fp32 rounding, so K1T evaluates the same correlation as the Horner recurrence of
-// K1 to fp32 accuracy with one 64-byte table row and 8 real-coefficient steps per (particle, component, antenna)
-// instead of N_f complex multiply-adds.  The tables (fp64 sums rounded once to complex64, tay_prep_kernel) cost
-// O(J N_a G N_f) per call and stay L2-resident (N_a G 64 bytes per PA).  The Gram is K1's closed form (K1 runs in
-// its Horner-free variant first, K1T then writes c).
+// truncated after L terms has a relative error below (pi N_f/(2G))^L/L! of sum_k |y[m,k]|: L = 8 at G = 4 N_f (1.4e-8,
+// the lane-group kernel's table) or L = 6 at G = 8 N_f (8.2e-8, the thread-per-particle kernels'), at or below fp32
+// rounding, so K1T evaluates the same correlation as the Horner recurrence of K1 to fp32 accuracy with one 64- or
+// 48-byte table row and a short Horner per (particle, component, antenna) instead of N_f complex multiply-adds.  The
+// tables (fp64 sums rounded once to complex64, tay_prep_fft_kernel / tay_prep_kernel) cost O(J N_a G log G) per call
+// and stay L2-resident.  The Gram is the closed form with a Taylor table of the Dirichlet kernel (tay_gram_kernel).
 #include <math.h>
 
 #include "cdms_internal.h"

@@ -491,7 +491,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
   // first 32-byte rows (degree 7) had lost at S <= 6 (in-flight rows raised the registers) and were kept for S >= 7 only
   float* dn = nullptr;
   if (tay && ctx->gram_tab && sd.small_step >= 1 && (sd.S >= 7 || ctx->gram_tab == 1)) {
-    WS_TRY(ctx, WS_DN, dn_table_floats(sd.nf), &dn);
+    WS_TRY(ctx, WS_DN, dn_table_floats(sd.nf) + 4, &dn);  // + the Gram's W != 0 flag
     if (ctx->dn_nf != sd.nf || ctx->dn_ptr != dn) {
       CUDA_TRY(ctx, launch_dn_table(sd.nf, dn, ctx->stream));
       ctx->launches += 1;
@@ -605,7 +605,8 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
                                     no_gram ? 1 : 0, tlanes, ctx->stream));
       COLL_TRY(mark(1));
       if (!no_gram)
-        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms32, dn, ctx->stream));
+        CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms32, dn,
+                                      dn ? reinterpret_cast<int*>(dn + dn_table_floats(sd.nf)) : nullptr, ctx->stream));
       ctx->launches += no_gram ? 0 : 1;
     } else {
       CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
@@ -952,7 +953,7 @@ cdms_status cdms_reserve(cdms_ctx ctx, const cdms_scene* scene, int64_t P_local)
       }
       if (ctx->gram_tab && sd.small_step >= 1 && (sd.S >= 7 || ctx->gram_tab == 1)) {  // the Gram's D_N table,
         float* dn;                                                                     // built here, outside captures
-        WS_TRY(ctx, WS_DN, dn_table_floats(sd.nf), &dn);
+        WS_TRY(ctx, WS_DN, dn_table_floats(sd.nf) + 4, &dn);  // + the Gram's W != 0 flag
         if (ctx->dn_nf != sd.nf || ctx->dn_ptr != dn) {
           CUDA_TRY(ctx, launch_dn_table(sd.nf, dn, ctx->stream));
           ctx->launches += 1;

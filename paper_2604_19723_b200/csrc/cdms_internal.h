@@ -279,7 +279,7 @@ bool tay_lanes(const SceneDev& sc, int64_t P);  // table layout / correlation ke
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, int direct,
                             cudaStream_t st);
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
-                            const double* sfv, int sfv_pp, float2* terms, const float* dn, cudaStream_t st);
+                            const double* sfv, int sfv_pp, float2* terms, const float* dn, int* wflag, cudaStream_t st);
 // The scene's Dirichlet table for the Gram (taylor.cu dn_table_kernel): dn_table_floats(nf) floats, built per N_f
 size_t dn_table_floats(int nf);
 cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st);

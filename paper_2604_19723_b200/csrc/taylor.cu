@@ -16,6 +16,8 @@
 // and stay L2-resident.  The Gram is the closed form with a Taylor table of the Dirichlet kernel (tay_gram_kernel).
 #include <math.h>
 
+#include <algorithm>
+
 #include "cdms_internal.h"
 #include "geometry.cuh"
 
@@ -651,17 +653,22 @@ cudaError_t launch_dn_table(int nf, float* out, cudaStream_t st) {
 // too, 128 registers and 4 blocks (16 warps) per SM at S >= 7.  Measured c5 4M Gram 43.6 -> 38.4 ms, c3 2.84 ->
 // 2.53 ms; one fp32 sum of 64 terms against 4 of 16 moved the K1T terms' worst G error within the parity bounds
 // (profiles/r02_gram_onechunk.txt).
-template <int S, int Q0, int Q1, bool FAST, bool TAB, bool ONE>
+// W0 (TAB and ONE only): every pair's base has W = rint((R_a - R_b) df/c) = 0 (path differences below half of c/df:
+// 300 m at c5), so a pair's table row is R0 + (k_a + I_a) - (k_b + I_b) from per-component integers and no per-pair
+// base row is held (36 registers at S = 9: its main-loop spills 116 -> 48 bytes, c5 4M Gram 33.1 -> 32.0 ms).  A
+// particle with some W != 0 sets *wflag, and the W0 = false kernel launched after it then recomputes the batch (it
+// returns at once while *wflag is 0).
+template <int S, int Q0, int Q1, bool FAST, bool TAB, bool ONE, bool W0>
 __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* __restrict__ tmpl,
                                               const double* __restrict__ particles, int64_t P, int pstride,
                                               const double* __restrict__ sfv, int sfv_pp, float2* __restrict__ terms,
                                               int lsplit, double2* gsum, double* rsh, float4* csh,
-                                              const GramTab tb) {
+                                              const GramTab tb, int* __restrict__ wflag, int64_t bx) {
   constexpr int NP = Q1 - Q0;  // this part's pairs; gsum [NP][TAY_BLOCK] (not ONE)
   // A = 2^lsplit adjacent lanes per particle, lane a takes antennas a, a + A, ... (A > 1 when P J threads alone would
   // leave the SMs latency-bound); no early exit: the group's fp64 totals are combined by shuffles below
   const int A = 1 << lsplit;
-  const int64_t t = (int64_t)blockIdx.x * TAY_BLOCK + threadIdx.x;
+  const int64_t t = bx * TAY_BLOCK + threadIdx.x;  // bx: the block's tile (blockIdx.x, or the fallback's loop)
   const int64_t p = t >> lsplit;
   const int a0 = (int)(t & (A - 1));
   const int j = blockIdx.y;
@@ -690,8 +697,23 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
   // per component and d' = u_a - u_b per pair -- one float per component instead of one per pair held in registers
   float xb[(FAST && !(TAB && CDMS_GRAM_UCOMP)) ? NP : 1];
   float fc_[(TAB && CDMS_GRAM_UCOMP) ? S : 1];
-  int gb[TAB ? NP : 1];     // TAB: the centre row of x_b G_D (offset by R0)
-  if (TAB && CDMS_GRAM_UCOMP) {
+  int gb[(TAB && !W0) ? NP : 1];  // TAB: the centre row of x_b G_D (offset by R0)
+  int Iq[W0 ? S : 1];             // W0: I_s, added to the per-antenna row k_s
+  if (W0) {
+    bool wz = true;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const double C = R64[s] * sc.df_c * (double)tb.G, I = rint(C);
+      fc_[s] = (float)(C - I);
+      Iq[W0 ? s : 0] = (int)I;
+    }
+#pragma unroll
+    for (int a = 0; a < S; ++a)
+#pragma unroll
+      for (int b = 0; b < S; ++b)
+        if (b > a) wz &= rint((R64[a] - R64[b]) * sc.df_c) == 0.0;
+    if (!wz && live) atomicOr(wflag, 1);  // this batch is recomputed by the W0 = false kernel
+  } else if (TAB && CDMS_GRAM_UCOMP) {
     double Ic[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -707,7 +729,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
         const int q = a * (2 * S - a - 1) / 2 + (b - a - 1) - Q0;
         if (q < 0 || q >= NP) continue;
         const double W = rint((R64[a] - R64[b]) * sc.df_c);
-        gb[q] = (int)(Ic[a] - Ic[b] - W * (double)tb.G) + tb.R0;
+        gb[(TAB && !W0) ? q : 0] = (int)(Ic[a] - Ic[b] - W * (double)tb.G) + tb.R0;
       }
   } else if (FAST) {
 #pragma unroll
@@ -720,7 +742,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
         const double x = frac_c((R64[a] - R64[b]) * sc.df_c);
         if (TAB) {
           const double xg = x * (double)tb.G, g = rint(xg);
-          gb[q] = (int)g + tb.R0;
+          gb[(TAB && !W0) ? q : 0] = (int)g + tb.R0;
           xb[q] = (float)(xg - g);
         } else {
           xb[q] = (float)x;
@@ -788,7 +810,7 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
         if (TAB && CDMS_GRAM_UCOMP == 2) {  // rounded per component: per pair r_a - r_b (|.| <= 1) and k_a - k_b
           constexpr float M = 12582912.f;
           const float um = dl[s] + M;
-          ik[(TAB && CDMS_GRAM_UCOMP == 2) ? s : 0] = __float_as_int(um);
+          ik[(TAB && CDMS_GRAM_UCOMP == 2) ? s : 0] = __float_as_int(um) + (W0 ? Iq[W0 ? s : 0] : 0);
           dl[s] = dl[s] - (um - M);
         }
       }
@@ -806,10 +828,10 @@ __device__ __forceinline__ void tay_gram_part(const SceneDev& sc, const float4* 
                                                       : fmaf(dl[a] - dl[b], dfG, xb[(FAST && !(TAB && CDMS_GRAM_UCOMP)) ? q : 0]);
             const float dm = d1 + M;
             float d = d1 - (dm - M);
-            int g2 = gb[q] + (__float_as_int(dm) - __float_as_int(M));
+            int g2 = gb[(TAB && !W0) ? q : 0] + (__float_as_int(dm) - __float_as_int(M));
             if (CDMS_GRAM_UCOMP == 2) {
               d = d1;
-              g2 = gb[q] + ik[(TAB && CDMS_GRAM_UCOMP == 2) ? a : 0] -
+              g2 = (W0 ? tb.R0 : gb[(TAB && !W0) ? q : 0]) + ik[(TAB && CDMS_GRAM_UCOMP == 2) ? a : 0] -
                    ik[(TAB && CDMS_GRAM_UCOMP == 2) ? b : 0];
             }
             if (DN_SYM) {  // D_N even: the row of |x|, the offset mirrored (selects, no branch)
@@ -918,48 +940,65 @@ template <int S, bool ONE>
 __host__ __device__ constexpr int tay_gram_minb() {
   return S < 7 ? 1 : !ONE ? CDMS_GRAM_MINB : tay_gram_parts<S, ONE>() == 1 && S >= 9 ? 3 : 4;
 }
-template <int S, bool FAST, bool TAB, bool ONE>
+// MODE 0: one tile per block; 1: W0 (see tay_gram_part); 2: the fallback of a W0 launch -- returns at once unless a
+// particle had W != 0 (*wflag), else strides over all tiles with a one-wave grid (a separate instantiation: the loop
+// costs registers, W0 S = 9 spilled 104 instead of 32 bytes with it)
+template <int S, bool FAST, bool TAB, bool ONE, int MODE>
 __global__ void __launch_bounds__(TAY_BLOCK, (tay_gram_minb<S, ONE>()))  // S >= 7: 12 or 16 (ONE) warps per SM
     tay_gram_kernel(const __grid_constant__ SceneDev sc, const float4* __restrict__ tmpl,
                     const double* __restrict__ particles, int64_t P, int pstride, const double* __restrict__ sfv,
-                    int sfv_pp, float2* __restrict__ terms, int lsplit, const GramTab tb) {
+                    int sfv_pp, float2* __restrict__ terms, int lsplit, const GramTab tb, int* __restrict__ wflag,
+                    int64_t ntiles) {
+  constexpr bool W0 = MODE == 1;
+  if (MODE == 2 && !*(volatile int*)wflag) return;
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S, ONE>(), H = NP / NPART;
   constexpr int NPMAX = NP - NP / NPART * (NPART - 1);  // the larger part
   extern __shared__ double2 smem_g[];
   double* rsh = reinterpret_cast<double*>(smem_g);        // [S][TAY_BLOCK] R_s
   double2* gsum = smem_g + (S * TAY_BLOCK + 1) / 2;       // not ONE: [NPMAX][TAY_BLOCK] fp64 pair totals
   float4* csh = reinterpret_cast<float4*>(gsum + (ONE ? 0 : NPMAX * TAY_BLOCK));  // TAB: [S][TAY_BLOCK]
-  if constexpr (NPART == 1) {
-    tay_gram_part<S, 0, NP, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
-  } else if constexpr (NPART == 2) {
-    if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
-    else
-      tay_gram_part<S, H, NP, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
-  } else {
-    static_assert(NPART == 3, "");
-    if (blockIdx.z == 0)
-      tay_gram_part<S, 0, H, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
-    else if (blockIdx.z == 1)
-      tay_gram_part<S, H, 2 * H, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
-    else
-      tay_gram_part<S, 2 * H, NP, FAST, TAB, ONE>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb);
+  for (int64_t bx = blockIdx.x; bx < ntiles; bx += (MODE == 2 ? gridDim.x : ntiles)) {
+    if constexpr (NPART == 1) {
+      tay_gram_part<S, 0, NP, FAST, TAB, ONE, W0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb, wflag, bx);
+    } else if constexpr (NPART == 2) {
+      if (blockIdx.z == 0)
+        tay_gram_part<S, 0, H, FAST, TAB, ONE, W0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb, wflag, bx);
+      else
+        tay_gram_part<S, H, NP, FAST, TAB, ONE, W0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb, wflag, bx);
+    } else {
+      static_assert(NPART == 3, "");
+      if (blockIdx.z == 0)
+        tay_gram_part<S, 0, H, FAST, TAB, ONE, W0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb, wflag, bx);
+      else if (blockIdx.z == 1)
+        tay_gram_part<S, H, 2 * H, FAST, TAB, ONE, W0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb, wflag, bx);
+      else
+        tay_gram_part<S, 2 * H, NP, FAST, TAB, ONE, W0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, lsplit, gsum, rsh, csh, tb, wflag, bx);
+    }
   }
 }
-template <int S, bool FAST, bool TAB, bool ONE>
+template <int S, bool FAST, bool TAB, bool ONE, int MODE>
 static cudaError_t launch_tay_gram_v(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
                                      int pstride, const double* sfv, int sfv_pp, float2* terms, const GramTab& tb,
-                                     int lsplit, cudaStream_t st) {
+                                     int lsplit, int* wflag, cudaStream_t st) {
   constexpr int NP = S * (S - 1) / 2, NPART = tay_gram_parts<S, ONE>();
   const size_t smem = (size_t)(S * TAY_BLOCK + 1) / 2 * sizeof(double2) +                                   // R_s
                       (ONE ? 0 : (size_t)(NP - NP / NPART * (NPART - 1)) * TAY_BLOCK * sizeof(double2)) +  // totals
                       (TAB ? (size_t)S * TAY_BLOCK * sizeof(float4) : 0);                                   // h_s, R_s
-  cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S, FAST, TAB, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(tay_gram_kernel<S, FAST, TAB, ONE, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)(((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK), sc.J, NPART);
-  tay_gram_kernel<S, FAST, TAB, ONE><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv, sfv_pp,
-                                                                    terms, lsplit, tb);
+  const int64_t ntiles = ((P << lsplit) + TAY_BLOCK - 1) / TAY_BLOCK;
+  int64_t gx = ntiles;
+  if (MODE == 2) {  // the fallback: one resident wave
+    int per_sm = 1, dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tay_gram_kernel<S, FAST, TAB, ONE, MODE>, TAY_BLOCK, smem);
+    gx = std::min<int64_t>(ntiles, (int64_t)std::max(per_sm, 1) * nsm / (sc.J * NPART) + 1);
+  }
+  dim3 grid((unsigned)gx, sc.J, NPART);
+  tay_gram_kernel<S, FAST, TAB, ONE, MODE><<<grid, TAY_BLOCK, smem, st>>>(sc, tmpl, particles, P, pstride, sfv,
+                                                                        sfv_pp, terms, lsplit, tb, wflag, ntiles);
   return cudaGetLastError();
 }
 #ifndef CDMS_GRAM_FAST
@@ -968,7 +1007,7 @@ static cudaError_t launch_tay_gram_v(const SceneDev& sc, const float4* tmpl, con
 template <int S>
 static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P,
                                      int pstride, const double* sfv, int sfv_pp, float2* terms, const float* dn,
-                                     cudaStream_t st) {
+                                     int* wflag, cudaStream_t st) {
   const bool fast = CDMS_GRAM_FAST && sc.small_step >= 1;
   GramTab tb;
   tb.dn = reinterpret_cast<const float4*>(dn);
@@ -978,21 +1017,39 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
   // 0.391, 2 lanes 0.388, 4 lanes 0.405, 8 lanes 0.448 ms per step; at P = 1.4e5 2 lanes 0.494 vs 4 lanes 0.517)
   const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 1 : 0;
   const bool one = ((sc.Na + (1 << lsplit) - 1) >> lsplit) <= CDMS_GRAM_ONE_MAX;
+  // W0 (S = 9, the one-part kernel whose registers it relieves; measured slower at S = 7 and 5 with its fallback
+  // launch): the W0 kernel, then its fallback
+  if constexpr (S >= 9) {
+    if (fast && dn && one && wflag) {
+      cudaError_t e = cudaMemsetAsync(wflag, 0, sizeof(int), st);
+      if (e == cudaSuccess)
+        e = launch_tay_gram_v<S, true, true, true, 1>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
+                                                      wflag, st);
+      if (e != cudaSuccess) return e;
+      return launch_tay_gram_v<S, true, true, true, 2>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
+                                                       wflag, st);
+    }
+  }
   if (fast && dn && one)
-    return launch_tay_gram_v<S, true, true, true>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit, st);
+    return launch_tay_gram_v<S, true, true, true, 0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
+                                                     nullptr, st);
   if (fast && dn)
-    return launch_tay_gram_v<S, true, true, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit, st);
+    return launch_tay_gram_v<S, true, true, false, 0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
+                                                      nullptr, st);
   if (fast)
-    return launch_tay_gram_v<S, true, false, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit, st);
-  return launch_tay_gram_v<S, false, false, false>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit, st);
+    return launch_tay_gram_v<S, true, false, false, 0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
+                                                       nullptr, st);
+  return launch_tay_gram_v<S, false, false, false, 0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
+                                                      nullptr, st);
 }
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
-                            const double* sfv, int sfv_pp, float2* terms, const float* dn, cudaStream_t st) {
+                            const double* sfv, int sfv_pp, float2* terms, const float* dn, int* wflag,
+                            cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
   switch (sc.S) {
     case 1: return cudaSuccess;
 #define CASE_S(n) \
-  case n: return launch_tay_gram_t<n>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, dn, st);
+  case n: return launch_tay_gram_t<n>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, dn, wflag, st);
     CASE_S(2) CASE_S(3) CASE_S(4) CASE_S(5) CASE_S(6) CASE_S(7) CASE_S(8) CASE_S(9)
 #undef CASE_S
     default: return cudaErrorInvalidValue;

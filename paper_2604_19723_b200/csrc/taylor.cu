@@ -1026,6 +1026,9 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
         e = launch_tay_gram_v<S, true, true, true, 1>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
                                                       wflag, st);
       if (e != cudaSuccess) return e;
+#ifdef CDMS_GRAM_NO_FALLBACK  // test aid only: shows that a parity case reaches the fallback (it must then fail)
+      return cudaSuccess;
+#endif
       return launch_tay_gram_v<S, true, true, true, 2>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
                                                        wflag, st);
     }

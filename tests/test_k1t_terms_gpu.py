@@ -32,6 +32,9 @@ SHAPES = {  # the BASELINE configs' scene shapes (J, K, URA, N_f)
     "s7a144": dict(J=1, K=6, ny=12, nv=12, nf=128),
     # J N_a,pad > 512: the correlation kernel reads its template columns from global memory, not the constant bank
     "j4a144": dict(J=4, K=2, ny=12, nv=12, nf=64),
+    # a 2 GHz band (c/df = 9.6 m): component paths differ by more than half a delay period, so the S = 9 Gram's W0
+    # kernel flags the batch and its fallback recomputes it; the correlation takes the TwoSum locate
+    "s9wide": dict(J=1, K=8, ny=8, nv=8, nf=64, B=2e9),
 }
 LAYOUTS = {"lanes": "1", "thread": "0"}
 
@@ -126,7 +129,7 @@ def _equal_delay_particles(cfg, sc, rng, n):
 
 @pytest.mark.parametrize("wf", ["spherical", "planar_wb"])
 @pytest.mark.parametrize("layout", list(LAYOUTS))
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "s9a144", "s7a144", "j4a144"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "s9a144", "s7a144", "j4a144", "s9wide"])
 def test_k1t_terms_parity(cd, ctxs, orc, name, layout, wf):
     """c and G of K1T against orc_terms (direct sums over the element-wise fp64 responses), ROI particles and
     equal-delay particles near a wall plane; spherical and planar wideband responses."""

@@ -607,7 +607,7 @@ cdms_status loglik_impl(cdms_ctx ctx, const SceneDev& sd, int precision, const d
       if (!no_gram)
         CUDA_TRY(ctx, launch_tay_gram(sd, tmpl, bpart, nb, bstride, bsfv, sfv_pp, terms32, dn,
                                       dn ? reinterpret_cast<int*>(dn + dn_table_floats(sd.nf)) : nullptr, ctx->stream));
-      ctx->launches += no_gram ? 0 : 1;
+      ctx->launches += no_gram ? 0 : tay_gram_launches(sd, nb, dn != nullptr);
     } else {
       CUDA_TRY(ctx, launch_corr(sd, a, precision, ctx->stream));
       COLL_TRY(mark(1));

@@ -278,6 +278,7 @@ size_t tay_table_bytes(const SceneDev& sc, int lanes);  // lanes: the lane-group
 bool tay_lanes(const SceneDev& sc, int64_t P);  // table layout / correlation kernel choice for P particles
 cudaError_t launch_tay_prep(const SceneDev& sc, const float2* y, float2* tab, int lanes, int direct,
                             cudaStream_t st);
+int tay_gram_launches(const SceneDev& sc, int64_t P, bool tab);  // kernels per launch_tay_gram call
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
                             const double* sfv, int sfv_pp, float2* terms, const float* dn, int* wflag, cudaStream_t st);
 // The scene's Dirichlet table for the Gram (taylor.cu dn_table_kernel): dn_table_floats(nf) floats, built per N_f

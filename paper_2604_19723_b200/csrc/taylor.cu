@@ -1045,6 +1045,13 @@ static cudaError_t launch_tay_gram_t(const SceneDev& sc, const float4* tmpl, con
   return launch_tay_gram_v<S, false, false, false, 0>(sc, tmpl, particles, P, pstride, sfv, sfv_pp, terms, tb, lsplit,
                                                       nullptr, st);
 }
+// kernel launches one launch_tay_gram call makes (the W0 kernel and its fallback at S = 9 with the table)
+int tay_gram_launches(const SceneDev& sc, int64_t P, bool tab) {
+  if (P <= 0 || sc.S < 2) return 0;
+  const int lsplit = (double)P * sc.J < 2.0 * 148 * 1024 ? 1 : 0;
+  const bool one = ((sc.Na + (1 << lsplit) - 1) >> lsplit) <= CDMS_GRAM_ONE_MAX;
+  return (tab && one && sc.S >= 9 && sc.small_step >= 1 && CDMS_GRAM_FAST) ? 2 : 1;
+}
 cudaError_t launch_tay_gram(const SceneDev& sc, const float4* tmpl, const double* particles, int64_t P, int pstride,
                             const double* sfv, int sfv_pp, float2* terms, const float* dn, int* wflag,
                             cudaStream_t st) {

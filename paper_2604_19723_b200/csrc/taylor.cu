@@ -245,6 +245,10 @@ __device__ __forceinline__ void tay_locate(float t, float hi, float lo, int par,
 // u = B_f + Delta (df/c) G in one fma, its rounding k by the magic constant, the row B_i + k on the extended table and
 // delta' = u - k -- 5 instructions instead of tay_locate's TwoSum reduction, wrap and per-element sign (|u| < 3 keeps
 // u's rounding below 1.2e-7 centres).
+#ifndef CDMS_CORR_UNROLL
+#define CDMS_CORR_UNROLL 8  // antennas per unrolled step (measured c5 4M corr 4: 17.25, 8: 16.91, 16: 17.01 ms)
+#endif
+constexpr int CORR_UNROLL = CDMS_CORR_UNROLL;
 template <bool SPH, bool TC, bool FL>
 __global__ void __launch_bounds__(TAY_BLOCK)
     tay_corr_kernel(const __grid_constant__ SceneDev sc, int G, const float2* __restrict__ tab,
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(TAY_BLOCK)
     for (int m0 = 0; m0 < Na; m0 += 16) {
       float pr = 0.f, pi = 0.f;
       const int m1 = min(m0 + 16, Na);
-#pragma unroll 4
+#pragma unroll CORR_UNROLL
       for (int m = m0; m < m1; ++m) {
         const float4 v = TC ? tc.v[j * Na_pad + m] : __ldg(&tm[m]);
         const float rq = hx * v.x + hy * v.y + hz * v.z;

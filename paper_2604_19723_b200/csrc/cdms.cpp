@@ -91,7 +91,13 @@ enum Slot {
   WS_PF_CC, WS_PF_FLAG, WS_PF_GAIN, WS_PF_PAR, WS_LSE2, WS_SL_STACK, WS_SL_DOTS, WS_SL_EIG, WS_SL_PAR, WS_LOC_KEYS, WS_LOC_IDX,
   WS_LOC_TEMP, WS_LOC_POS, WS_LOC_SFV, WS_DN, WS_COUNT
 };
-constexpr size_t TERMS_BUDGET = (size_t)2 << 30;  // bytes of per-(particle, PA) sufficient statistics per batch
+// bytes of per-(particle, PA) sufficient statistics per likelihood batch: 32 GiB of the 180 GB holds the whole c5
+// step (16M particles, 27.6 GB of complex64 terms) in one batch -- fewer kernel tails than round 2's 2 GiB batches of
+// 1.24M particles (measured c5 step 209.2 ms at 2 GiB, 205.8 at 8, 205.0 at 32; profiles/r02_gram_onechunk.txt)
+#ifndef CDMS_TERMS_BUDGET_GB
+#define CDMS_TERMS_BUDGET_GB 32
+#endif
+constexpr size_t TERMS_BUDGET = (size_t)CDMS_TERMS_BUDGET_GB << 30;
 constexpr int64_t LOCALITY_MIN_P = 32768;         // K1T batches from this size run in Morton order (sort.cu)
 
 struct DeviceGuard {

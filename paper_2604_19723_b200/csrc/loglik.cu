@@ -698,7 +698,10 @@ __global__ void __launch_bounds__(NTHREADS, (Plan<S, RT>::min_blocks))
 //   g = c - G m; ||e||^2 = ||z||^2 - 2 Re(m^H c) + m^H G m; K = I + V^1/2 G V^1/2 / eta = L L^H;
 //   x = L^-1 V^1/2 g; l_j = -Nz ln(pi eta) - 2 sum ln L_ii - ||e||^2/eta + ||x||^2/eta^2;
 //   amplitudes: m + V^1/2 L^-H x / eta (LMMSE).
-constexpr int ASM_T = 128;
+#ifndef CDMS_ASM_T
+#define CDMS_ASM_T 64  // threads per block (measured c3 assembly 64: 0.218, 128: 0.234, 256: 0.253 ms; c5 4M 2.53 / 2.54 / 2.68)
+#endif
+constexpr int ASM_T = CDMS_ASM_T;
 
 template <bool F32>
 struct TermT {  // a term as stored: complex64 from K1T, else complex128
